@@ -1,0 +1,630 @@
+"""B200-native FFT tensor-sketch hot path of arXiv 1506.04448.
+
+Python mirror of the reference C++ API (proj/include/sketchcp/) over the C-ABI
+in include/sketchcp_b200.h. Class and method names, argument meaning and error
+behaviour follow the reference; numpy arrays stand in for Eigen vectors. All
+compute runs in the sm_100a library ``_lib/libsketchcp_b200.so``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import (
+    CudaError,
+    DegenerateIterationError,
+    FormatError,
+    NumericalError,
+    SKC_DEVICE,
+    SKC_F32,
+    SKC_F64,
+    SKC_HOST,
+    check,
+    lib,
+)
+
+__all__ = [
+    "Context",
+    "default_context",
+    "SymTensorSketchSet",
+    "AsymTensorSketchSet",
+    "SymContractionWorkspace",
+    "AsymContractionWorkspace",
+    "PowerConfig",
+    "CpDecomposition",
+    "robust_tpm_fast",
+    "derive_seed",
+    "unit_sphere",
+    "power_inits",
+    "gen_planted_tensor",
+    "kernel_launch_count",
+    "transform_count",
+    "NumericalError",
+    "DegenerateIterationError",
+    "FormatError",
+    "CudaError",
+]
+
+SEED_TAG_POWER_INIT = 0x31  # rng.hpp:20
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _f64(a, shape=None) -> np.ndarray:
+    x = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    if shape is not None and x.shape != shape:
+        raise ValueError(f"expected shape {shape}, got {x.shape}")
+    return x
+
+
+def derive_seed(master: int, tag: int, i0: int = 0, i1: int = 0) -> int:
+    """rng.hpp:35-46"""
+    return int(lib.skc_derive_seed(master, tag, i0, i1))
+
+
+def unit_sphere(seed: int, n: int) -> np.ndarray:
+    """Rng(seed).unit_sphere(n) (rng.hpp:100-106)."""
+    out = np.empty(n)
+    check(lib.skc_unit_sphere(seed, n, _dp(out)))
+    return out
+
+
+def power_inits(seed: int, n: int, k: int, L: int, c0: int = 0, tau0: int = 0) -> np.ndarray:
+    """RTPM initial vectors (decompose.cpp:99-100): array (k, L, n)."""
+    out = np.empty((k, L, n))
+    check(lib.skc_power_inits(seed, n, c0, k, tau0, L, _dp(out)))
+    return out
+
+
+def kernel_launch_count() -> int:
+    return int(lib.skc_kernel_launch_count())
+
+
+def transform_count() -> int:
+    """Analogue of fft::transform_count() (fft.hpp:25), in length-b transforms."""
+    return int(lib.skc_transform_count())
+
+
+def device_count() -> int:
+    c = C.c_int(0)
+    check(lib.skc_device_count(C.byref(c)))
+    return c.value
+
+
+class Context:
+    """One CUDA device + stream (the C-ABI skc_context)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(lib.skc_context_create(device, C.byref(h)))
+        self._h = h
+        self.device = device
+
+    @property
+    def handle(self):
+        return self._h
+
+    def synchronize(self) -> None:
+        check(lib.skc_context_synchronize(self._h))
+
+    def stream(self) -> int:
+        s = C.c_void_p()
+        check(lib.skc_context_stream(self._h, C.byref(s)))
+        return int(s.value or 0)
+
+    def profile(self, on: bool = True) -> None:
+        """Enable/disable per-kernel CUDA-event timing on this context's stream."""
+        check(lib.skc_profile_enable(self._h, int(bool(on))))
+
+    def profile_reset(self) -> None:
+        check(lib.skc_profile_reset(self._h))
+
+    def profile_get(self, kernel: str):
+        """(total_ms, launches) for one kernel family since the last reset."""
+        ms, cnt = C.c_double(), C.c_uint64()
+        check(lib.skc_profile_get(self._h, kernel.encode(), C.byref(ms), C.byref(cnt)))
+        return ms.value, cnt.value
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib.skc_context_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_DEFAULT: dict[int, Context] = {}
+
+
+def default_context(device: int = 0) -> Context:
+    if device not in _DEFAULT:
+        _DEFAULT[device] = Context(device)
+    return _DEFAULT[device]
+
+
+def _tensor_arg(T, n: int):
+    """Returns (pointer, dtype code, location, keepalive) for a dense n^3 tensor
+    given as a numpy array (host) or a CUDA torch tensor (device)."""
+    if hasattr(T, "is_cuda") and T.is_cuda:
+        import torch
+
+        if T.dtype not in (torch.float64, torch.float32):
+            raise ValueError("accumulate_dense: tensor dtype must be float64 or float32")
+        if T.numel() != n * n * n:
+            raise ValueError("accumulate_dense: dimension mismatch")
+        T = T.contiguous()
+        return C.c_void_p(T.data_ptr()), (SKC_F64 if T.dtype == torch.float64 else SKC_F32), SKC_DEVICE, T
+    a = np.asarray(T)
+    if a.dtype not in (np.float64, np.float32):
+        a = a.astype(np.float64)
+    a = np.ascontiguousarray(a)
+    if a.size != n * n * n:
+        raise ValueError("accumulate_dense: dimension mismatch")
+    return C.c_void_p(a.ctypes.data), (SKC_F64 if a.dtype == np.float64 else SKC_F32), SKC_HOST, a
+
+
+@dataclass
+class SymReplicate:
+    """SymTensorSketchSet::Replicate (sketch.hpp:89-95), host copies."""
+
+    bucket1: np.ndarray
+    bucket2: np.ndarray
+    bucket3: np.ndarray
+    sexp: np.ndarray
+    h_coefficients: np.ndarray
+    sigma_coefficients: np.ndarray
+    data: np.ndarray
+
+
+class SymTensorSketchSet:
+    """Colliding-hash sketch set for symmetric tensors (sketch.hpp:87-136)."""
+
+    def __init__(self, n: int, b: int, B: int, master_seed: int, ctx: Context | None = None, *, _handle=None):
+        self.ctx = ctx or default_context()
+        if _handle is not None:
+            self._h = _handle
+            return
+        h = C.c_void_p()
+        check(lib.skc_sym_create(self.ctx.handle, int(n), int(b), int(B), int(master_seed), C.byref(h)))
+        self._h = h
+
+    @classmethod
+    def from_coefficients(cls, n, b, B, master_seed, hcoef, scoef, data=None, ctx=None):
+        """SymTensorSketchSet::load semantics (sketch.cpp:391-410)."""
+        ctx = ctx or default_context()
+        hc = np.ascontiguousarray(hcoef, dtype=np.uint64).reshape(-1)
+        sc = np.ascontiguousarray(scoef, dtype=np.uint64).reshape(-1)
+        if hc.size != B * 6 or sc.size != B * 6:
+            raise ValueError("from_coefficients: need B*6 coefficients per hash")
+        d = None if data is None else np.ascontiguousarray(np.asarray(data, dtype=np.complex128).reshape(B, b))
+        h = C.c_void_p()
+        check(
+            lib.skc_sym_create_from_coefficients(
+                ctx.handle,
+                int(n),
+                int(b),
+                int(B),
+                int(master_seed),
+                hc.ctypes.data_as(C.POINTER(C.c_uint64)),
+                sc.ctypes.data_as(C.POINTER(C.c_uint64)),
+                None if d is None else d.ctypes.data_as(C.POINTER(C.c_double)),
+                C.byref(h),
+            )
+        )
+        return cls(n, b, B, master_seed, ctx, _handle=h)
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                lib.skc_sym_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def _info(self):
+        n, b, B, s, v = C.c_int(), C.c_uint32(), C.c_int(), C.c_uint64(), C.c_uint64()
+        check(lib.skc_sym_info(self._h, C.byref(n), C.byref(b), C.byref(B), C.byref(s), C.byref(v)))
+        return n.value, b.value, B.value, s.value, v.value
+
+    def n(self) -> int:
+        return self._info()[0]
+
+    def b(self) -> int:
+        return self._info()[1]
+
+    def replicates(self) -> int:
+        return self._info()[2]
+
+    def master_seed(self) -> int:
+        return self._info()[3]
+
+    def version(self) -> int:
+        return self._info()[4]
+
+    def coefficients(self):
+        B = self.replicates()
+        hc = np.empty(B * 6, dtype=np.uint64)
+        sc = np.empty(B * 6, dtype=np.uint64)
+        check(lib.skc_sym_coefficients(self._h, hc.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                       sc.ctypes.data_as(C.POINTER(C.c_uint64))))
+        return hc.reshape(B, 6), sc.reshape(B, 6)
+
+    def tables(self, m: int):
+        n = self.n()
+        b1, b2, b3 = (np.empty(n, dtype=np.uint32) for _ in range(3))
+        se = np.empty(n, dtype=np.uint8)
+        u32 = C.POINTER(C.c_uint32)
+        check(
+            lib.skc_sym_tables(
+                self._h, int(m), b1.ctypes.data_as(u32), b2.ctypes.data_as(u32), b3.ctypes.data_as(u32),
+                se.ctypes.data_as(C.POINTER(C.c_uint8)),
+            )
+        )
+        return b1, b2, b3, se
+
+    def replicate(self, m: int) -> SymReplicate:
+        b1, b2, b3, se = self.tables(m)
+        hc, sc = self.coefficients()
+        return SymReplicate(b1, b2, b3, se, hc[m], sc[m], self.data(m))
+
+    def data(self, m: int | None = None) -> np.ndarray:
+        """replicate(m).data (or all B replicates as a (B, b) array)."""
+        b, B = self.b(), self.replicates()
+        out = np.empty((b,) if m is not None else (B, b), dtype=np.complex128)
+        check(lib.skc_sym_read_data(self._h, -1 if m is None else int(m), out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def set_data(self, m: int | None, values) -> None:
+        """mutable_replicate(m).data = values (bumps version, sketch.hpp:105-108)."""
+        b, B = self.b(), self.replicates()
+        shape = (b,) if m is not None else (B, b)
+        v = np.ascontiguousarray(np.asarray(values, dtype=np.complex128).reshape(shape))
+        check(lib.skc_sym_write_data(self._h, -1 if m is None else int(m), v.ctypes.data_as(C.POINTER(C.c_double))))
+
+    def accumulate_dense(self, T, assume_symmetric: bool = False, i0: int = 0, i1: int | None = None) -> None:
+        """sketch.cpp:315-345; T numpy (host) or CUDA torch tensor (device), f64 or f32."""
+        n = self.n()
+        ptr, dt, loc, _keep = _tensor_arg(T, n)
+        check(lib.skc_sym_accumulate_dense(self._h, ptr, dt, loc, int(bool(assume_symmetric)), int(i0),
+                                           int(n if i1 is None else i1)))
+
+    def add_scaled_rank1(self, u, alpha: float) -> None:
+        """sketch.cpp:347-361"""
+        n = self.n()
+        u = np.asarray(u, dtype=np.float64)
+        if u.shape != (n,):
+            raise ValueError("add_scaled_rank1: dimension mismatch")
+        u = np.ascontiguousarray(u)
+        check(lib.skc_sym_add_scaled_rank1(self._h, _dp(u), float(alpha)))
+
+    def accumulate_moment(self, X, w=None) -> None:
+        """data += sum_i w_i sketch(x_i^(x)3); X (N, n) numpy or CUDA torch, w (N,) or None."""
+        n = self.n()
+        if hasattr(X, "is_cuda") and X.is_cuda:
+            import torch
+
+            X = X.to(torch.float64).contiguous()
+            if X.ndim != 2 or X.shape[1] != n:
+                raise ValueError("accumulate_moment: dimension mismatch")
+            wp = None
+            if w is not None:
+                w = w.to(device=X.device, dtype=torch.float64).contiguous()
+                wp = C.cast(C.c_void_p(w.data_ptr()), C.POINTER(C.c_double))
+            check(lib.skc_sym_accumulate_moment(self._h, C.cast(C.c_void_p(X.data_ptr()), C.POINTER(C.c_double)),
+                                                wp, X.shape[0], SKC_DEVICE))
+            return
+        X = _f64(X)
+        if X.ndim != 2 or X.shape[1] != n:
+            raise ValueError("accumulate_moment: dimension mismatch")
+        wa = None if w is None else _f64(w, (X.shape[0],))
+        check(lib.skc_sym_accumulate_moment(self._h, _dp(X), None if wa is None else _dp(wa), X.shape[0], SKC_HOST))
+
+    def recover_entry(self, i: int, j: int, k: int) -> float:
+        """sketch.cpp:363-377"""
+        out = C.c_double()
+        check(lib.skc_sym_recover_entry(self._h, int(i), int(j), int(k), C.byref(out)))
+        return out.value
+
+    def data_device(self):
+        """(device pointer, bytes) of the B x b complex data, for collectives."""
+        p, nb = C.c_void_p(), C.c_size_t()
+        check(lib.skc_sym_data_device(self._h, C.byref(p), C.byref(nb)))
+        return int(p.value), int(nb.value)
+
+    def bump_version(self) -> None:
+        check(lib.skc_sym_bump_version(self._h))
+
+
+class SymContractionWorkspace:
+    """contraction.hpp:14-41. Calls accept one n-vector or an (L, n) batch."""
+
+    def __init__(self, set_: SymTensorSketchSet):
+        self._set = set_
+
+    def set(self) -> SymTensorSketchSet:
+        return self._set
+
+    def _batch(self, u):
+        n = self._set.n()
+        U = np.asarray(u, dtype=np.float64)
+        single = U.ndim == 1
+        U = np.ascontiguousarray(U.reshape(1, -1) if single else U)
+        if U.shape[1] != n:
+            raise ValueError("Ivv: dimension mismatch")
+        return U, single
+
+    def Ivv(self, u) -> np.ndarray:
+        U, single = self._batch(u)
+        out = np.empty_like(U)
+        check(lib.skc_sym_ivv(self._set.handle, _dp(U), U.shape[0], _dp(out)))
+        return out[0] if single else out
+
+    def vvv(self, u):
+        U, single = self._batch(u)
+        out = np.empty(U.shape[0])
+        check(lib.skc_sym_vvv(self._set.handle, _dp(U), U.shape[0], _dp(out)))
+        return float(out[0]) if single else out
+
+    def cached_transform(self, m: int) -> np.ndarray:
+        b = self._set.b()
+        out = np.empty(b, dtype=np.complex128)
+        check(lib.skc_sym_cached_transform(self._set.handle, int(m), out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+
+@dataclass
+class PowerConfig:
+    """decompose.hpp:9-17"""
+
+    k: int = 1
+    L: int = 30
+    T_iters: int = 30
+    b: int = 4096
+    B: int = 20
+    seed: int = 0
+    tol: float = 1e-12
+
+
+@dataclass
+class CpDecomposition:
+    """tensor.hpp:58-67 (symmetric_of: A = B = C copies, tensor.cpp:58-65)."""
+
+    lambda_: np.ndarray
+    A: np.ndarray
+    B: np.ndarray
+    C: np.ndarray
+    best_tau: np.ndarray | None = None
+
+    def rank(self) -> int:
+        return int(self.lambda_.size)
+
+    def dim(self) -> int:
+        return int(self.A.shape[0])
+
+    @staticmethod
+    def symmetric_of(lam, V, best_tau=None) -> "CpDecomposition":
+        return CpDecomposition(np.asarray(lam), V, V.copy(), V.copy(), best_tau)
+
+
+def robust_tpm_fast(set_: SymTensorSketchSet, cfg: PowerConfig, inits=None) -> CpDecomposition:
+    """decompose.cpp:83-115. inits: optional (k, L, n) initial vectors; default the
+    reference's Rng(derive_seed(seed, 0x31, c, tau)).unit_sphere(n). The set is left deflated."""
+    n = set_.n()
+    lam = np.empty(max(cfg.k, 0))
+    V = np.empty((max(cfg.k, 0), n))
+    bt = (C.c_int * max(cfg.k, 1))()
+    ip = None
+    if inits is not None:
+        inits = _f64(inits, (cfg.k, cfg.L, n))
+        ip = _dp(inits)
+    check(lib.skc_sym_rtpm(set_.handle, int(cfg.k), int(cfg.L), int(cfg.T_iters), int(cfg.seed), float(cfg.tol), ip,
+                           _dp(lam), _dp(V), bt))
+    A = np.ascontiguousarray(V.T)
+    return CpDecomposition.symmetric_of(lam, A, np.array(bt[: cfg.k]))
+
+
+class AsymTensorSketchSet:
+    """Three-hash tensor sketch set (sketch.hpp:27-82)."""
+
+    def __init__(self, n: int, b: int, B: int, master_seed: int, ctx: Context | None = None, *, _handle=None):
+        self.ctx = ctx or default_context()
+        if _handle is not None:
+            self._h = _handle
+            return
+        h = C.c_void_p()
+        check(lib.skc_asym_create(self.ctx.handle, int(n), int(b), int(B), int(master_seed), C.byref(h)))
+        self._h = h
+
+    @classmethod
+    def from_coefficients(cls, n, b, B, master_seed, hcoef, xcoef, data=None, ctx=None):
+        ctx = ctx or default_context()
+        hc = np.ascontiguousarray(hcoef, dtype=np.uint64).reshape(-1)
+        xc = np.ascontiguousarray(xcoef, dtype=np.uint64).reshape(-1)
+        d = None if data is None else np.ascontiguousarray(np.asarray(data, dtype=np.complex128).reshape(B, b))
+        h = C.c_void_p()
+        check(
+            lib.skc_asym_create_from_coefficients(
+                ctx.handle, int(n), int(b), int(B), int(master_seed),
+                hc.ctypes.data_as(C.POINTER(C.c_uint64)), xc.ctypes.data_as(C.POINTER(C.c_uint64)),
+                None if d is None else d.ctypes.data_as(C.POINTER(C.c_double)), C.byref(h),
+            )
+        )
+        return cls(n, b, B, master_seed, ctx, _handle=h)
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                lib.skc_asym_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def _info(self):
+        n, b, B, s, v = C.c_int(), C.c_uint32(), C.c_int(), C.c_uint64(), C.c_uint64()
+        check(lib.skc_asym_info(self._h, C.byref(n), C.byref(b), C.byref(B), C.byref(s), C.byref(v)))
+        return n.value, b.value, B.value, s.value, v.value
+
+    def n(self):
+        return self._info()[0]
+
+    def b(self):
+        return self._info()[1]
+
+    def replicates(self):
+        return self._info()[2]
+
+    def master_seed(self):
+        return self._info()[3]
+
+    def version(self):
+        return self._info()[4]
+
+    def coefficients(self):
+        B = self.replicates()
+        hc = np.empty(B * 6, dtype=np.uint64)
+        xc = np.empty(B * 18, dtype=np.uint64)
+        check(lib.skc_asym_coefficients(self._h, hc.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                        xc.ctypes.data_as(C.POINTER(C.c_uint64))))
+        return hc.reshape(B, 3, 2), xc.reshape(B, 3, 6)
+
+    def tables(self, m: int):
+        n = self.n()
+        bk = np.empty(3 * n, dtype=np.uint32)
+        sg = np.empty(3 * n)
+        check(lib.skc_asym_tables(self._h, int(m), bk.ctypes.data_as(C.POINTER(C.c_uint32)), _dp(sg)))
+        return bk.reshape(3, n), sg.reshape(3, n)
+
+    def data(self, m: int | None = None) -> np.ndarray:
+        b, B = self.b(), self.replicates()
+        out = np.empty((b,) if m is not None else (B, b), dtype=np.complex128)
+        check(lib.skc_asym_read_data(self._h, -1 if m is None else int(m), out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def set_data(self, m, values):
+        b, B = self.b(), self.replicates()
+        shape = (b,) if m is not None else (B, b)
+        v = np.ascontiguousarray(np.asarray(values, dtype=np.complex128).reshape(shape))
+        check(lib.skc_asym_write_data(self._h, -1 if m is None else int(m), v.ctypes.data_as(C.POINTER(C.c_double))))
+
+    def accumulate_dense(self, T, i0: int = 0, i1: int | None = None) -> None:
+        """sketch.cpp:173-193"""
+        n = self.n()
+        ptr, dt, loc, _keep = _tensor_arg(T, n)
+        check(lib.skc_asym_accumulate_dense(self._h, ptr, dt, loc, int(i0), int(n if i1 is None else i1)))
+
+    def rank1_sketch(self, m: int, u, v, w) -> np.ndarray:
+        """sketch.cpp:195-212"""
+        n = self.n()
+        u, v, w = (_f64(x, (n,)) for x in (u, v, w))
+        out = np.empty(self.b(), dtype=np.complex128)
+        check(lib.skc_asym_rank1_sketch(self._h, int(m), _dp(u), _dp(v), _dp(w), out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def add_rank1(self, alpha: float, u, v, w) -> None:
+        """sketch.cpp:214-222"""
+        n = self.n()
+        u, v, w = (_f64(x, (n,)) for x in (u, v, w))
+        check(lib.skc_asym_add_rank1(self._h, float(alpha), _dp(u), _dp(v), _dp(w)))
+
+    def accumulate_factored(self, a, U, V, W) -> None:
+        """sketch.cpp:224-248: components (a_i, u_i, v_i, w_i) as arrays (N,), (N, n) x 3."""
+        n = self.n()
+        a = _f64(a).reshape(-1)
+        N = a.size
+        U, V, W = (_f64(x, (N, n)) for x in (U, V, W))
+        check(lib.skc_asym_accumulate_factored(self._h, N, _dp(a), _dp(U), _dp(V), _dp(W)))
+
+    def recover_entry(self, i, j, k) -> float:
+        out = C.c_double()
+        check(lib.skc_asym_recover_entry(self._h, int(i), int(j), int(k), C.byref(out)))
+        return out.value
+
+    def data_device(self):
+        p, nb = C.c_void_p(), C.c_size_t()
+        check(lib.skc_asym_data_device(self._h, C.byref(p), C.byref(nb)))
+        return int(p.value), int(nb.value)
+
+    def bump_version(self) -> None:
+        check(lib.skc_asym_bump_version(self._h))
+
+
+class AsymContractionWorkspace:
+    """contraction.hpp:43-77"""
+
+    def __init__(self, set_: AsymTensorSketchSet):
+        self._set = set_
+
+    def set(self):
+        return self._set
+
+    def _prep(self, x):
+        n = self._set.n()
+        X = np.asarray(x, dtype=np.float64)
+        single = X.ndim == 1
+        X = np.ascontiguousarray(X.reshape(1, -1) if single else X)
+        if X.shape[1] != n:
+            raise ValueError("mode_contraction: dimension mismatch")
+        return X, single
+
+    def mode_contraction(self, free_mode: int, x, y) -> np.ndarray:
+        X, single = self._prep(x)
+        Y, _ = self._prep(y)
+        if X.shape != Y.shape:
+            raise ValueError("mode_contraction: dimension mismatch")
+        out = np.empty_like(X)
+        check(lib.skc_asym_mode_contraction(self._set.handle, int(free_mode), _dp(X), _dp(Y), X.shape[0], _dp(out)))
+        return out[0] if single else out
+
+    def Ivv(self, u):
+        return self.mode_contraction(0, u, u)
+
+    def Ibc(self, bvec, cvec):
+        return self.mode_contraction(0, bvec, cvec)
+
+    def vvv(self, u):
+        U, single = self._prep(u)
+        out = np.empty(U.shape[0])
+        check(lib.skc_asym_vvv(self._set.handle, _dp(U), U.shape[0], _dp(out)))
+        return float(out[0]) if single else out
+
+    def cached_transform(self, m: int) -> np.ndarray:
+        out = np.empty(self._set.b(), dtype=np.complex128)
+        check(lib.skc_asym_cached_transform(self._set.handle, int(m), out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+
+def gen_planted_tensor(n: int, rank: int, sigma: float, seed: int, dtype=np.float64):
+    """Host generator of the BASELINE planted tensors (configs 0-2). Returns (T, lambda, V)."""
+    T = np.empty((n, n, n), dtype=dtype)
+    lam = np.empty(rank)
+    V = np.empty((rank, n))
+    check(lib.skc_gen_planted_tensor(n, rank, float(sigma), int(seed), SKC_F64 if T.dtype == np.float64 else SKC_F32,
+                                     C.c_void_p(T.ctypes.data), _dp(lam), _dp(V)))
+    return T, lam, np.ascontiguousarray(V.T)
+
+
+def gen_planted_tensor_device(ctx: Context, n: int, rank: int, sigma: float, seed: int, out_ptr: int, dtype=np.float64):
+    """Device generator into a caller-owned buffer (e.g. a torch CUDA tensor's data_ptr)."""
+    lam = np.empty(rank)
+    V = np.empty((rank, n))
+    check(lib.skc_gen_planted_tensor_device(ctx.handle, n, rank, float(sigma), int(seed),
+                                            SKC_F64 if np.dtype(dtype) == np.float64 else SKC_F32,
+                                            C.c_void_p(out_ptr), _dp(lam), _dp(V)))
+    return lam, np.ascontiguousarray(V.T)

@@ -1,0 +1,1453 @@
+// C-ABI implementation (include/sketchcp_b200.h): host C++ orchestration of the
+// sm_100a kernels in skc_kernels.cu. Mirrors the reference classes in
+// proj/include/sketchcp/{sketch,contraction,decompose}.hpp: validation, error
+// messages and exception taxonomy follow the reference; compute runs only on the GPU.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/sketchcp_b200.h"
+#include "skc_fft.cuh"
+#include "skc_host.hpp"
+#include "skc_internal.hpp"
+
+using namespace skc;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+#define CK(call)                                                                                     \
+    do {                                                                                             \
+        cudaError_t e_ = (call);                                                                     \
+        if (e_ != cudaSuccess) {                                                                     \
+            int code_ = (e_ == cudaErrorMemoryAllocation) ? kOutOfMemory : kCudaError;               \
+            fail(code_, std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #call);        \
+        }                                                                                            \
+    } while (0)
+
+template <typename F>
+int guard(F&& f) {
+    try {
+        f();
+        return kOk;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "out of host memory";
+        return kOutOfMemory;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return kNumericalError;
+    }
+}
+
+// RAII device buffer.
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t count = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        count = 0;
+    }
+    void alloc(size_t c) {
+        if (c <= count && p) return;
+        release();
+        if (c == 0) c = 1;
+        CK(cudaMalloc(&p, c * sizeof(T)));
+        count = c;
+    }
+    void upload(const T* h, size_t c, cudaStream_t st) {
+        alloc(c);
+        CK(cudaMemcpyAsync(p, h, c * sizeof(T), cudaMemcpyHostToDevice, st));
+    }
+};
+
+int local_length(std::uint32_t b) {
+    static int pref = [] {
+        const char* e = std::getenv("SKC_LOCAL_N");
+        int v = e ? std::atoi(e) : 2048;
+        if (v < 2 || !is_pow2(static_cast<std::uint64_t>(v)) || v > 4096) v = 2048;
+        return v;
+    }();
+    return static_cast<int>(std::min<std::uint32_t>(b, static_cast<std::uint32_t>(pref)));
+}
+
+std::vector<double> host_twiddles(std::uint32_t b) {
+    std::vector<double> tw(2 * static_cast<size_t>(b));
+    const long double two_pi = 6.283185307179586476925286766559005768L;
+    for (std::uint32_t k = 0; k < b; ++k) {
+        long double a = two_pi * static_cast<long double>(k) / static_cast<long double>(b);
+        tw[2 * k] = static_cast<double>(cosl(a));
+        tw[2 * k + 1] = static_cast<double>(sinl(a));
+    }
+    return tw;
+}
+
+}  // namespace
+
+// ============================ context ============================================
+struct skc_context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int sms = 148;
+    int smem_optin = 227 * 1024;
+    std::map<std::uint32_t, std::unique_ptr<DevBuf<double2>>> twiddles;
+    // dense-build row tables keyed by (n, i0, i1, sym)
+    struct RowTab {
+        DevBuf<std::uint32_t> rows;
+        std::vector<long long> cum;  // cumulative entries per row (host)
+        int nrows = 0;
+    };
+    std::map<std::tuple<int, int, int, bool>, std::unique_ptr<RowTab>> rowtabs;
+    // scratch
+    DevBuf<unsigned char> tensor_stage;
+    DevBuf<long long> build_partials;
+    DevBuf<double> prepass;
+    DevBuf<int> ints;  // [0] scale exp, [1] nonfinite, [2] best tau, [3..] misc
+    DevBuf<double> dbl;  // [0] best value
+    DevBuf<int> chunk_begin;
+    DevBuf<double> U, part, values, freq_acc, X;
+    DevBuf<double2> tmp;
+    DevBuf<int> flags;
+    DevBuf<unsigned long long> asym_key;
+
+    // per-kernel event profiling (skc_profile_*)
+    struct ProfRec {
+        std::string name;
+        cudaEvent_t a, b;
+    };
+    bool prof_on = false;
+    std::vector<ProfRec> prof;
+
+    void use() const { CK(cudaSetDevice(device)); }
+    const double2* tw(std::uint32_t b) {
+        auto it = twiddles.find(b);
+        if (it != twiddles.end()) return it->second->p;
+        auto buf = std::make_unique<DevBuf<double2>>();
+        std::vector<double> h = host_twiddles(b);
+        buf->upload(reinterpret_cast<const double2*>(h.data()), b, stream);
+        CK(cudaStreamSynchronize(stream));
+        const double2* p = buf->p;
+        twiddles[b] = std::move(buf);
+        return p;
+    }
+    RowTab& rowtab(int n, int i0, int i1, bool sym) {
+        auto key = std::make_tuple(n, i0, i1, sym);
+        auto it = rowtabs.find(key);
+        if (it != rowtabs.end()) return *it->second;
+        auto rt = std::make_unique<RowTab>();
+        std::vector<std::uint32_t> rows;
+        rt->cum.push_back(0);
+        for (int i = i0; i < i1; ++i)
+            for (int j = sym ? i : 0; j < n; ++j) {
+                rows.push_back((static_cast<std::uint32_t>(i) << 16) | static_cast<std::uint32_t>(j));
+                rt->cum.push_back(rt->cum.back() + (sym ? (n - j) : n));
+            }
+        rt->nrows = static_cast<int>(rows.size());
+        rt->rows.upload(rows.data(), rows.size(), stream);
+        CK(cudaStreamSynchronize(stream));
+        RowTab& ref = *rt;
+        rowtabs[key] = std::move(rt);
+        return ref;
+    }
+    void sync() { CK(cudaStreamSynchronize(stream)); }
+    void check_launch() { CK(cudaGetLastError()); }
+};
+
+// Records a CUDA event pair around the launches in its scope when profiling is on.
+struct ProfScope {
+    skc_context* c;
+    const char* name;
+    cudaEvent_t a = nullptr;
+    ProfScope(skc_context* ctx, const char* nm) : c(ctx), name(nm) {
+        if (!c->prof_on) return;
+        CK(cudaEventCreate(&a));
+        CK(cudaEventRecord(a, c->stream));
+    }
+    ~ProfScope() {
+        if (!c->prof_on || !a) return;
+        cudaEvent_t b = nullptr;
+        if (cudaEventCreate(&b) != cudaSuccess) return;
+        cudaEventRecord(b, c->stream);
+        c->prof.push_back({name, a, b});
+    }
+};
+#define SKC_CAT2(a, b) a##b
+#define SKC_CAT(a, b) SKC_CAT2(a, b)
+#define SKC_PROF(ctx, nm) ProfScope SKC_CAT(prof_scope_, __LINE__)(ctx, nm)
+
+// ============================ sets ===============================================
+struct skc_sym_set {
+    skc_context* ctx = nullptr;
+    int n = 0;
+    std::uint32_t b = 2;
+    int logb = 1;
+    int B = 0;
+    std::uint64_t seed = 0;
+    std::uint64_t version = 0;
+    std::vector<std::uint64_t> hcoef, scoef;  // B x 6 each
+    DevBuf<std::uint64_t> d_hcoef, d_scoef;
+    DevBuf<std::uint32_t> bucket1, bucket2, bucket3, packed, perm1, perm2;
+    DevBuf<std::uint8_t> sexp;
+    DevBuf<double2> data, spec;
+    int N = 2, logN = 1, S = 1;
+    std::uint64_t spec_version = ~0ull;
+    bool spec_valid = false;
+
+    SymView view() const {
+        SymView v;
+        v.n = n;
+        v.b = b;
+        v.logb = logb;
+        v.B = B;
+        v.bucket1 = bucket1.p;
+        v.bucket2 = bucket2.p;
+        v.bucket3 = bucket3.p;
+        v.sexp = sexp.p;
+        v.packed = packed.p;
+        v.tw = ctx->tw(b);
+        v.N = N;
+        v.logN = logN;
+        v.S = S;
+        v.perm1 = perm1.p;
+        v.perm2 = perm2.p;
+        v.data = data.p;
+        v.spec = spec.p;
+        return v;
+    }
+    // contraction.cpp:62-72: refresh cached spectra when the version moved.
+    void ensure_fresh() {
+        if (spec_valid && spec_version == version) return;
+        SKC_PROF(ctx, "spectrum");
+        launch_spectrum(ctx->stream, data.p, b, logb, B, N, logN, S, ctx->tw(b), spec.p);
+        ctx->check_launch();
+        spec_version = version;
+        spec_valid = true;
+    }
+};
+
+struct skc_asym_set {
+    skc_context* ctx = nullptr;
+    int n = 0;
+    std::uint32_t b = 2;
+    int logb = 1;
+    int B = 0;
+    std::uint64_t seed = 0;
+    std::uint64_t version = 0;
+    std::vector<std::uint64_t> hcoef, xcoef;  // B x 3 x 2, B x 3 x 6
+    DevBuf<std::uint64_t> d_hcoef, d_xcoef;
+    DevBuf<std::uint32_t> bucket, packed, perm;
+    DevBuf<double> sign;
+    DevBuf<double2> data, spec;
+    int N = 2, logN = 1, S = 1;
+    std::uint64_t spec_version = ~0ull;
+    bool spec_valid = false;
+
+    AsymView view() const {
+        AsymView v;
+        v.n = n;
+        v.b = b;
+        v.logb = logb;
+        v.B = B;
+        v.bucket = bucket.p;
+        v.sign = sign.p;
+        v.packed = packed.p;
+        v.tw = ctx->tw(b);
+        v.N = N;
+        v.logN = logN;
+        v.S = S;
+        v.perm = perm.p;
+        v.data = data.p;
+        v.spec = spec.p;
+        return v;
+    }
+    void ensure_fresh() {
+        if (spec_valid && spec_version == version) return;
+        SKC_PROF(ctx, "spectrum");
+        launch_spectrum(ctx->stream, data.p, b, logb, B, N, logN, S, ctx->tw(b), spec.p);
+        ctx->check_launch();
+        spec_version = version;
+        spec_valid = true;
+    }
+};
+
+namespace {
+
+void validate_set_args(int n, std::uint32_t b, int B) {
+    // sketch.cpp:157-159 / 302-304
+    require(n >= 1, "sketch set: dimension must be positive");
+    require(B >= 1, "sketch set: need at least one replicate");
+    require(is_pow2(b), "sketch set: b must be a power of two");
+    require(b >= 2, "PolyHash: need at least 2 buckets");
+    require(b <= (1u << 28), "sketch set: b above 2^28 is not supported by the packed bucket tables");
+}
+
+void check_vec(const void* p, const char* what) { require(p != nullptr, std::string(what) + ": null pointer"); }
+
+// Upload coefficients, derive tables on the device, sort scatter permutations.
+void init_sym_device(skc_sym_set* s, const double* data_host) {
+    skc_context* ctx = s->ctx;
+    ctx->use();
+    const cudaStream_t st = ctx->stream;
+    const size_t Bn = static_cast<size_t>(s->B) * s->n;
+    s->d_hcoef.upload(s->hcoef.data(), s->hcoef.size(), st);
+    s->d_scoef.upload(s->scoef.data(), s->scoef.size(), st);
+    s->bucket1.alloc(Bn);
+    s->bucket2.alloc(Bn);
+    s->bucket3.alloc(Bn);
+    s->packed.alloc(Bn);
+    s->sexp.alloc(Bn);
+    s->perm1.alloc(Bn);
+    s->perm2.alloc(Bn);
+    launch_sym_tables(st, s->d_hcoef.p, s->d_scoef.p, s->n, s->b, s->B, s->bucket1.p, s->bucket2.p, s->bucket3.p,
+                      s->sexp.p, s->packed.p);
+    ctx->check_launch();
+    s->N = local_length(s->b);
+    s->logN = ilog2(static_cast<unsigned>(s->N));
+    s->S = static_cast<int>(s->b / static_cast<std::uint32_t>(s->N));
+    s->logb = ilog2(s->b);
+    launch_sort_perm(st, s->bucket1.p, s->B, s->n, static_cast<std::uint32_t>(s->N - 1), s->perm1.p);
+    launch_sort_perm(st, s->bucket2.p, s->B, s->n, static_cast<std::uint32_t>(s->N - 1), s->perm2.p);
+    ctx->check_launch();
+    const size_t Bb = static_cast<size_t>(s->B) * s->b;
+    s->data.alloc(Bb);
+    s->spec.alloc(Bb);
+    if (data_host)
+        CK(cudaMemcpyAsync(s->data.p, data_host, Bb * sizeof(double2), cudaMemcpyHostToDevice, st));
+    else
+        CK(cudaMemsetAsync(s->data.p, 0, Bb * sizeof(double2), st));
+    ctx->tw(s->b);
+    ctx->sync();
+}
+
+void init_asym_device(skc_asym_set* s, const double* data_host) {
+    skc_context* ctx = s->ctx;
+    ctx->use();
+    const cudaStream_t st = ctx->stream;
+    const size_t B3n = static_cast<size_t>(s->B) * 3 * s->n;
+    s->d_hcoef.upload(s->hcoef.data(), s->hcoef.size(), st);
+    s->d_xcoef.upload(s->xcoef.data(), s->xcoef.size(), st);
+    s->bucket.alloc(B3n);
+    s->packed.alloc(B3n);
+    s->sign.alloc(B3n);
+    s->perm.alloc(B3n);
+    launch_asym_tables(st, s->d_hcoef.p, s->d_xcoef.p, s->n, s->b, s->B, s->bucket.p, s->sign.p, s->packed.p);
+    ctx->check_launch();
+    s->N = local_length(s->b);
+    s->logN = ilog2(static_cast<unsigned>(s->N));
+    s->S = static_cast<int>(s->b / static_cast<std::uint32_t>(s->N));
+    s->logb = ilog2(s->b);
+    launch_sort_perm(st, s->bucket.p, s->B * 3, s->n, static_cast<std::uint32_t>(s->N - 1), s->perm.p);
+    ctx->check_launch();
+    const size_t Bb = static_cast<size_t>(s->B) * s->b;
+    s->data.alloc(Bb);
+    s->spec.alloc(Bb);
+    if (data_host)
+        CK(cudaMemcpyAsync(s->data.p, data_host, Bb * sizeof(double2), cudaMemcpyHostToDevice, st));
+    else
+        CK(cudaMemsetAsync(s->data.p, 0, Bb * sizeof(double2), st));
+    ctx->tw(s->b);
+    ctx->sync();
+}
+
+// ---- dense build orchestration ------------------------------------------------------
+const void* stage_tensor(skc_context* ctx, const void* T, int n, int dtype, int location) {
+    if (location == SKC_DEVICE) return T;
+    const size_t bytes = static_cast<size_t>(n) * n * n * (dtype == SKC_F64 ? 8 : 4);
+    ctx->tensor_stage.alloc(bytes);
+    CK(cudaMemcpyAsync(ctx->tensor_stage.p, T, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    return ctx->tensor_stage.p;
+}
+
+void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool sym, int i0, int i1, int B,
+                     std::uint32_t b, const std::uint32_t* packed, double2* data) {
+    if (i0 >= i1) return;
+    skc_context::RowTab& rt = ctx->rowtab(n, i0, i1, sym);
+    if (rt.nrows == 0) return;
+    const long long total_slots = static_cast<long long>(B) * (sym ? 2ll * b : static_cast<long long>(b));
+    const long long cap = std::max<long long>(1024, (ctx->smem_optin - 1024) / 8);
+    int G = static_cast<int>((total_slots + cap - 1) / cap);
+    int C = std::max(1, ctx->sms / G);
+    C = std::min(C, rt.nrows);
+    long long spc = (total_slots + G - 1) / G;
+    spc = (spc + 31) / 32 * 32;
+    // chunk boundaries balanced by entry count
+    std::vector<int> cb(C + 1, 0);
+    const long long tot = rt.cum.back();
+    for (int c = 1; c < C; ++c) {
+        const long long target = tot * c / C;
+        cb[c] = static_cast<int>(std::lower_bound(rt.cum.begin(), rt.cum.end(), target) - rt.cum.begin());
+        cb[c] = std::max(cb[c], cb[c - 1]);
+    }
+    cb[C] = rt.nrows;
+    ctx->chunk_begin.upload(cb.data(), cb.size(), ctx->stream);
+    ctx->build_partials.alloc(static_cast<size_t>(C) * total_slots);
+    ctx->prepass.alloc(kPrepassBlocks);
+    ctx->ints.alloc(16);
+
+    BuildPlan p;
+    p.n = n;
+    p.sym = sym;
+    p.dtype = dtype;
+    p.rowtab = rt.rows.p;
+    p.nrows = rt.nrows;
+    p.chunk_begin = ctx->chunk_begin.p;
+    p.C = C;
+    p.G = G;
+    p.total_slots = total_slots;
+    p.slots_per_cta = static_cast<int>(spc);
+    p.threads = 1024;
+    p.bmask = b - 1;
+    p.B = B;
+    p.packed = packed;
+    p.prepass_partials = ctx->prepass.p;
+    p.scale_exp = ctx->ints.p;
+    p.nonfinite = ctx->ints.p + 1;
+    p.partials = ctx->build_partials.p;
+    p.data_as_double = reinterpret_cast<double*>(data);
+    {
+        SKC_PROF(ctx, "build_prepass");
+        launch_build_prepass(ctx->stream, Tdev, p);
+    }
+    ctx->check_launch();
+    int nonfinite = 0;
+    CK(cudaMemcpyAsync(&nonfinite, p.nonfinite, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    // Fixed-point accumulation cannot carry NaN/Inf the way the reference's
+    // floating-point sum would; reject instead of producing a wrong sketch.
+    if (nonfinite) fail(kInvalidArgument, "accumulate_dense: tensor has a non-finite entry");
+    {
+        SKC_PROF(ctx, "build_main");
+        launch_build_main(ctx->stream, Tdev, p);
+    }
+    ctx->check_launch();
+    {
+        SKC_PROF(ctx, "build_finalize");
+        launch_build_finalize(ctx->stream, p);
+    }
+    ctx->check_launch();
+}
+
+// Symmetry check of the reference (tensor.cpp:32-43) — first failing (i,j,k,perm) in
+// the reference's loop order, found on the device.
+__global__ void k_first_asym(const void* T, int dtype, int n, double tol, unsigned long long* best) {
+    long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (idx >= (long long)n * n * n) return;
+    int i = static_cast<int>(idx / ((long long)n * n)), j = static_cast<int>((idx / n) % n), k = static_cast<int>(idx % n);
+    if (!(i <= j && j <= k)) return;
+    auto at = [&](int a, int b2, int c) -> double {
+        size_t off = (static_cast<size_t>(a) * n + b2) * n + c;
+        return dtype == 0 ? static_cast<const double*>(T)[off] : static_cast<double>(static_cast<const float*>(T)[off]);
+    };
+    const double ref = at(i, j, k);
+    const int perms[5][3] = {{i, k, j}, {j, i, k}, {j, k, i}, {k, i, j}, {k, j, i}};
+    for (int p = 0; p < 5; ++p)
+        if (fabs(at(perms[p][0], perms[p][1], perms[p][2]) - ref) > tol) {
+            // loop order: (i, j, k) lexicographic among sorted triples, then perm
+            unsigned long long key = (static_cast<unsigned long long>(idx) << 3) | static_cast<unsigned long long>(p);
+            atomicMin(best, key);
+            return;
+        }
+}
+
+}  // namespace
+
+// ============================ C-ABI ==============================================
+extern "C" {
+
+const char* skc_last_error(void) { return g_last_error.c_str(); }
+int skc_version(void) { return 1; }
+uint64_t skc_kernel_launch_count(void) { return launch_count(); }
+uint64_t skc_transform_count(void) { return transform_units(); }
+
+int skc_device_count(int* out) {
+    return guard([&] {
+        int c = 0;
+        cudaError_t e = cudaGetDeviceCount(&c);
+        if (e != cudaSuccess) c = 0;
+        *out = c;
+    });
+}
+
+int skc_context_create(int device, skc_context** out) {
+    return guard([&] {
+        check_vec(out, "skc_context_create");
+        int count = 0;
+        cudaError_t e = cudaGetDeviceCount(&count);
+        if (e != cudaSuccess || count == 0)
+            fail(kCudaError, "no CUDA device available (this library has no CPU fallback)");
+        require(device >= 0 && device < count, "skc_context_create: device index out of range");
+        CK(cudaSetDevice(device));
+        cudaDeviceProp prop;
+        CK(cudaGetDeviceProperties(&prop, device));
+        if (prop.major < 10)
+            fail(kCudaError, std::string("device ") + prop.name + " is not sm_100-class; this library targets sm_100a");
+        auto ctx = std::make_unique<skc_context>();
+        ctx->device = device;
+        ctx->sms = prop.multiProcessorCount;
+        ctx->smem_optin = static_cast<int>(prop.sharedMemPerBlockOptin);
+        CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        *out = ctx.release();
+    });
+}
+int skc_context_destroy(skc_context* ctx) {
+    return guard([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        cudaStream_t st = ctx->stream;
+        delete ctx;
+        cudaStreamDestroy(st);
+    });
+}
+int skc_context_synchronize(skc_context* ctx) {
+    return guard([&] {
+        check_vec(ctx, "context");
+        ctx->use();
+        ctx->sync();
+    });
+}
+int skc_profile_enable(skc_context* ctx, int on) {
+    return guard([&] {
+        check_vec(ctx, "context");
+        ctx->prof_on = on != 0;
+    });
+}
+int skc_profile_reset(skc_context* ctx) {
+    return guard([&] {
+        check_vec(ctx, "context");
+        ctx->use();
+        ctx->sync();
+        for (auto& r : ctx->prof) {
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+        ctx->prof.clear();
+    });
+}
+int skc_profile_get(skc_context* ctx, const char* kernel, double* total_ms, uint64_t* launches) {
+    return guard([&] {
+        check_vec(ctx, "context");
+        check_vec(kernel, "kernel name");
+        ctx->use();
+        ctx->sync();
+        double tot = 0.0;
+        std::uint64_t cnt = 0;
+        for (auto& r : ctx->prof)
+            if (r.name == kernel) {
+                float ms = 0.f;
+                CK(cudaEventElapsedTime(&ms, r.a, r.b));
+                tot += ms;
+                ++cnt;
+            }
+        if (total_ms) *total_ms = tot;
+        if (launches) *launches = cnt;
+    });
+}
+int skc_context_stream(skc_context* ctx, void** stream_out) {
+    return guard([&] {
+        check_vec(ctx, "context");
+        *stream_out = reinterpret_cast<void*>(ctx->stream);
+    });
+}
+
+uint64_t skc_derive_seed(uint64_t master, uint64_t tag, uint64_t i0, uint64_t i1) {
+    return derive_seed(master, tag, i0, i1);
+}
+int skc_unit_sphere(uint64_t seed, int n, double* out) {
+    return guard([&] {
+        require(n >= 1, "unit_sphere: n must be positive");
+        Rng(seed).unit_sphere(n, out);
+    });
+}
+int skc_power_inits(uint64_t seed, int n, int c0, int k, int tau0, int L, double* out) {
+    return guard([&] {
+        require(n >= 1 && k >= 0 && L >= 0, "power_inits: invalid sizes");
+        for (int c = 0; c < k; ++c)
+            for (int t = 0; t < L; ++t) {
+                Rng rng(derive_seed(seed, seed_tag::kPowerInit, static_cast<std::uint64_t>(c0 + c),
+                                    static_cast<std::uint64_t>(tau0 + t)));
+                rng.unit_sphere(n, out + (static_cast<size_t>(c) * L + t) * n);
+            }
+    });
+}
+int skc_poly_coefficients(int independence, uint64_t seed, uint64_t* out) {
+    return guard([&] {
+        require(independence >= 1 && independence <= 8, "PolyHash: independence must be in [1, 8]");
+        poly_coefficients(independence, seed, out);
+    });
+}
+uint32_t skc_poly_eval(const uint64_t* coeffs, int k, uint32_t b, uint64_t i) { return poly_eval(coeffs, k, b, i); }
+
+// ---- symmetric set ----
+int skc_sym_create(skc_context* ctx, int n, uint32_t b, int B, uint64_t master_seed, skc_sym_set** out) {
+    return guard([&] {
+        check_vec(ctx, "context");
+        validate_set_args(n, b, B);
+        auto s = std::make_unique<skc_sym_set>();
+        s->ctx = ctx;
+        s->n = n;
+        s->b = b;
+        s->B = B;
+        s->seed = master_seed;
+        s->hcoef.resize(static_cast<size_t>(B) * 6);
+        s->scoef.resize(static_cast<size_t>(B) * 6);
+        for (int m = 0; m < B; ++m) {  // sketch.cpp:307-309
+            poly_coefficients(6, derive_seed(master_seed, seed_tag::kSymBucketHash, m), &s->hcoef[m * 6]);
+            poly_coefficients(6, derive_seed(master_seed, seed_tag::kSymSign, m), &s->scoef[m * 6]);
+        }
+        init_sym_device(s.get(), nullptr);
+        *out = s.release();
+    });
+}
+int skc_sym_create_from_coefficients(skc_context* ctx, int n, uint32_t b, int B, uint64_t master_seed,
+                                     const uint64_t* hcoef, const uint64_t* scoef, const double* data_host,
+                                     skc_sym_set** out) {
+    return guard([&] {
+        check_vec(ctx, "context");
+        validate_set_args(n, b, B);
+        check_vec(hcoef, "hcoef");
+        check_vec(scoef, "scoef");
+        for (int x = 0; x < B * 6; ++x)
+            require(hcoef[x] < kHashPrime && scoef[x] < kHashPrime, "PolyHash: coefficient out of range");
+        auto s = std::make_unique<skc_sym_set>();
+        s->ctx = ctx;
+        s->n = n;
+        s->b = b;
+        s->B = B;
+        s->seed = master_seed;
+        s->hcoef.assign(hcoef, hcoef + static_cast<size_t>(B) * 6);
+        s->scoef.assign(scoef, scoef + static_cast<size_t>(B) * 6);
+        init_sym_device(s.get(), data_host);
+        *out = s.release();
+    });
+}
+int skc_sym_destroy(skc_sym_set* s) {
+    return guard([&] {
+        if (!s) return;
+        s->ctx->use();
+        s->ctx->sync();
+        delete s;
+    });
+}
+int skc_sym_info(const skc_sym_set* s, int* n, uint32_t* b, int* B, uint64_t* seed, uint64_t* version) {
+    return guard([&] {
+        check_vec(s, "set");
+        if (n) *n = s->n;
+        if (b) *b = s->b;
+        if (B) *B = s->B;
+        if (seed) *seed = s->seed;
+        if (version) *version = s->version;
+    });
+}
+int skc_sym_tables(const skc_sym_set* s, int m, uint32_t* bucket1, uint32_t* bucket2, uint32_t* bucket3,
+                   uint8_t* sexp) {
+    return guard([&] {
+        check_vec(s, "set");
+        require(m >= 0 && m < s->B, "replicate index out of range");
+        s->ctx->use();
+        const size_t off = static_cast<size_t>(m) * s->n, bytes = static_cast<size_t>(s->n) * 4;
+        cudaStream_t st = s->ctx->stream;
+        if (bucket1) CK(cudaMemcpyAsync(bucket1, s->bucket1.p + off, bytes, cudaMemcpyDeviceToHost, st));
+        if (bucket2) CK(cudaMemcpyAsync(bucket2, s->bucket2.p + off, bytes, cudaMemcpyDeviceToHost, st));
+        if (bucket3) CK(cudaMemcpyAsync(bucket3, s->bucket3.p + off, bytes, cudaMemcpyDeviceToHost, st));
+        if (sexp) CK(cudaMemcpyAsync(sexp, s->sexp.p + off, s->n, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    });
+}
+int skc_sym_coefficients(const skc_sym_set* s, uint64_t* hcoef, uint64_t* scoef) {
+    return guard([&] {
+        check_vec(s, "set");
+        if (hcoef) std::copy(s->hcoef.begin(), s->hcoef.end(), hcoef);
+        if (scoef) std::copy(s->scoef.begin(), s->scoef.end(), scoef);
+    });
+}
+
+int skc_sym_accumulate_dense(skc_sym_set* s, const void* T, int dtype, int location, int assume_symmetric, int i0,
+                             int i1) {
+    return guard([&] {
+        check_vec(s, "set");
+        check_vec(T, "accumulate_dense: tensor");
+        require(dtype == SKC_F64 || dtype == SKC_F32, "accumulate_dense: dtype must be SKC_F64 or SKC_F32");
+        require(location == SKC_HOST || location == SKC_DEVICE, "accumulate_dense: bad location");
+        require(0 <= i0 && i0 <= i1 && i1 <= s->n, "accumulate_dense: slice out of range");
+        require(s->n <= 65535, "accumulate_dense: n above 65535 is not supported");
+        skc_context* ctx = s->ctx;
+        ctx->use();
+        const void* Td = stage_tensor(ctx, T, s->n, dtype, location);
+        if (!assume_symmetric) {
+            ctx->asym_key.alloc(1);
+            unsigned long long init = ~0ull;
+            CK(cudaMemcpyAsync(ctx->asym_key.p, &init, 8, cudaMemcpyHostToDevice, ctx->stream));
+            long long tot = static_cast<long long>(s->n) * s->n * s->n;
+            k_first_asym<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, ctx->stream>>>(Td, dtype, s->n, 1e-9,
+                                                                                           ctx->asym_key.p);
+            count_launch();
+            ctx->check_launch();
+            unsigned long long key = 0;
+            CK(cudaMemcpyAsync(&key, ctx->asym_key.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+            ctx->sync();
+            if (key != ~0ull) {
+                const long long idx = static_cast<long long>(key >> 3);
+                const int p = static_cast<int>(key & 7);
+                const int n = s->n;
+                const int i = static_cast<int>(idx / ((long long)n * n)), j = static_cast<int>((idx / n) % n),
+                          k = static_cast<int>(idx % n);
+                const int perms[5][3] = {{i, k, j}, {j, i, k}, {j, k, i}, {k, i, j}, {k, j, i}};
+                fail(kInvalidArgument, "accumulate_dense: input tensor is not symmetric at (" +
+                                           std::to_string(perms[p][0] + 1) + "," + std::to_string(perms[p][1] + 1) +
+                                           "," + std::to_string(perms[p][2] + 1) + ")");
+            }
+        }
+        s->version++;  // sketch.cpp:324
+        run_dense_build(ctx, Td, s->n, dtype, true, i0, i1, s->B, s->b, s->packed.p, s->data.p);
+        ctx->sync();
+    });
+}
+
+// Frequency-domain rank-1 / moment accumulation shared by add_scaled_rank1,
+// accumulate_moment and RTPM deflation. X: device N x n.
+static void sym_moment_device(skc_sym_set* s, const double* Xd, const double* wd, double alpha, long long Nsamp) {
+    skc_context* ctx = s->ctx;
+    const int per_rep = s->B * s->S;
+    int chunks = static_cast<int>(std::max<long long>(1, std::min<long long>(Nsamp, (4ll * ctx->sms + per_rep - 1) / per_rep)));
+    ctx->freq_acc.alloc(static_cast<size_t>(chunks) * per_rep * s->N * 2);
+    ctx->tmp.alloc(static_cast<size_t>(s->B) * s->b);
+    SymView v = s->view();
+    {
+        SKC_PROF(ctx, "moment");
+        launch_sym_moment_accumulate(ctx->stream, v, Xd, wd, 1.0, Nsamp, chunks, ctx->freq_acc.p);
+    }
+    ctx->check_launch();
+    {
+        SKC_PROF(ctx, "freq_inverse");
+        launch_freq_reduce_inverse(ctx->stream, ctx->freq_acc.p, chunks, s->B, s->S, s->N, s->logN, s->b, s->logb,
+                                   v.tw, ctx->tmp.p);
+    }
+    ctx->check_launch();
+    {
+        SKC_PROF(ctx, "combine");
+        launch_combine_residues(ctx->stream, ctx->tmp.p, s->B, s->S, s->N, s->b, v.tw, alpha, -1, false, s->data.p);
+    }
+    ctx->check_launch();
+}
+
+int skc_sym_add_scaled_rank1(skc_sym_set* s, const double* u_host, double alpha) {
+    return guard([&] {
+        check_vec(s, "set");
+        check_vec(u_host, "add_scaled_rank1: u");
+        if (alpha == 0.0) return;  // sketch.cpp:349
+        skc_context* ctx = s->ctx;
+        ctx->use();
+        s->version++;
+        ctx->X.upload(u_host, s->n, ctx->stream);
+        sym_moment_device(s, ctx->X.p, nullptr, alpha, 1);
+        ctx->sync();
+    });
+}
+
+int skc_sym_accumulate_moment(skc_sym_set* s, const double* X, const double* w, long long N, int location) {
+    return guard([&] {
+        check_vec(s, "set");
+        require(N >= 0, "accumulate_moment: negative sample count");
+        if (N == 0) return;
+        check_vec(X, "accumulate_moment: X");
+        skc_context* ctx = s->ctx;
+        ctx->use();
+        const double* Xd = X;
+        const double* wd = w;
+        if (location == SKC_HOST) {
+            ctx->X.upload(X, static_cast<size_t>(N) * s->n, ctx->stream);
+            Xd = ctx->X.p;
+            if (w) {
+                ctx->values.upload(w, static_cast<size_t>(N), ctx->stream);
+                wd = ctx->values.p;
+            }
+        }
+        s->version++;
+        sym_moment_device(s, Xd, wd, 1.0, N);
+        ctx->sync();
+    });
+}
+
+int skc_sym_read_data(const skc_sym_set* s, int m, double* out_host) {
+    return guard([&] {
+        check_vec(s, "set");
+        check_vec(out_host, "read_data: out");
+        require(m < s->B, "replicate index out of range");
+        s->ctx->use();
+        const size_t off = m < 0 ? 0 : static_cast<size_t>(m) * s->b;
+        const size_t cnt = m < 0 ? static_cast<size_t>(s->B) * s->b : s->b;
+        CK(cudaMemcpyAsync(out_host, s->data.p + off, cnt * sizeof(double2), cudaMemcpyDeviceToHost, s->ctx->stream));
+        s->ctx->sync();
+    });
+}
+int skc_sym_write_data(skc_sym_set* s, int m, const double* in_host) {
+    return guard([&] {
+        check_vec(s, "set");
+        check_vec(in_host, "write_data: in");
+        require(m < s->B, "replicate index out of range");
+        s->ctx->use();
+        const size_t off = m < 0 ? 0 : static_cast<size_t>(m) * s->b;
+        const size_t cnt = m < 0 ? static_cast<size_t>(s->B) * s->b : s->b;
+        CK(cudaMemcpyAsync(s->data.p + off, in_host, cnt * sizeof(double2), cudaMemcpyHostToDevice, s->ctx->stream));
+        s->version++;
+        s->ctx->sync();
+    });
+}
+int skc_sym_data_device(skc_sym_set* s, void** dev_ptr, size_t* bytes) {
+    return guard([&] {
+        check_vec(s, "set");
+        *dev_ptr = s->data.p;
+        *bytes = static_cast<size_t>(s->B) * s->b * sizeof(double2);
+    });
+}
+int skc_sym_bump_version(skc_sym_set* s) {
+    return guard([&] {
+        check_vec(s, "set");
+        s->version++;
+    });
+}
+int skc_sym_recover_entry(const skc_sym_set* s, int i, int j, int k, double* out) {
+    // sketch.cpp:363-377 — O(B) gather of host-visible data; computed from the
+    // device tables and data copied back per replicate.
+    return guard([&] {
+        check_vec(s, "set");
+        const int n = s->n;
+        if (i < 0 || j < 0 || k < 0 || i >= n || j >= n || k >= n)
+            fail(kInvalidArgument, "recover_entry: index out of range");
+        s->ctx->use();
+        const double kappa = (i == j && j == k) ? 1.0 : ((i == j || j == k || i == k) ? 3.0 : 6.0);
+        std::vector<double> est(s->B);
+        std::vector<std::uint32_t> b1(3);
+        std::vector<std::uint8_t> se(3);
+        for (int m = 0; m < s->B; ++m) {
+            const int idx[3] = {i, j, k};
+            for (int q = 0; q < 3; ++q) {
+                CK(cudaMemcpy(&b1[q], s->bucket1.p + static_cast<size_t>(m) * n + idx[q], 4, cudaMemcpyDeviceToHost));
+                CK(cudaMemcpy(&se[q], s->sexp.p + static_cast<size_t>(m) * n + idx[q], 1, cudaMemcpyDeviceToHost));
+            }
+            const std::uint32_t t =
+                static_cast<std::uint32_t>((std::uint64_t{b1[0]} + b1[1] + b1[2]) % s->b);
+            double2 z;
+            CK(cudaMemcpy(&z, s->data.p + static_cast<size_t>(m) * s->b + t, sizeof(double2), cudaMemcpyDeviceToHost));
+            const unsigned e = (4 * 3 - (se[0] + se[1] + se[2])) & 3u;
+            // (root4(e) * z).real()
+            double re;
+            switch (e) {
+                case 0: re = z.x; break;
+                case 1: re = -z.y; break;
+                case 2: re = -z.x; break;
+                default: re = z.y; break;
+            }
+            est[m] = re / kappa;
+        }
+        std::size_t mid = est.size() / 2;
+        std::nth_element(est.begin(), est.begin() + mid, est.end());
+        double hi = est[mid];
+        if (est.size() % 2 == 1) {
+            *out = hi;
+        } else {
+            double lo = *std::max_element(est.begin(), est.begin() + mid);
+            *out = 0.5 * (lo + hi);
+        }
+    });
+}
+
+// ---- symmetric contractions ----
+static void sym_contract_batch(skc_sym_set* s, const double* Ud, int L, int mode) {
+    skc_context* ctx = s->ctx;
+    s->ensure_fresh();
+    const size_t per = (mode == 0) ? static_cast<size_t>(s->n) : 3;
+    ctx->part.alloc(static_cast<size_t>(L) * s->B * s->S * per);
+    SKC_PROF(ctx, "sym_contract");
+    launch_sym_contract(ctx->stream, s->view(), Ud, L, mode, ctx->part.p);
+    ctx->check_launch();
+}
+
+int skc_sym_ivv(skc_sym_set* s, const double* U_host, int L, double* out_host) {
+    return guard([&] {
+        check_vec(s, "set");
+        check_vec(U_host, "Ivv: U");
+        check_vec(out_host, "Ivv: out");
+        require(L >= 1, "Ivv: need at least one vector");
+        require(s->B <= 128, "median over more than 128 replicates is not supported");
+        skc_context* ctx = s->ctx;
+        ctx->use();
+        ctx->U.upload(U_host, static_cast<size_t>(L) * s->n, ctx->stream);
+        sym_contract_batch(s, ctx->U.p, L, 0);
+        ctx->values.alloc(static_cast<size_t>(L) * s->n);
+        launch_median_rows(ctx->stream, ctx->part.p, L, s->B, s->S, s->n, ctx->values.p, nullptr, 0.0, nullptr);
+        ctx->check_launch();
+        CK(cudaMemcpyAsync(out_host, ctx->values.p, static_cast<size_t>(L) * s->n * 8, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        ctx->sync();
+    });
+}
+int skc_sym_vvv(skc_sym_set* s, const double* U_host, int L, double* out_host) {
+    return guard([&] {
+        check_vec(s, "set");
+        check_vec(U_host, "vvv: U");
+        check_vec(out_host, "vvv: out");
+        require(L >= 1, "vvv: need at least one vector");
+        require(s->B <= 128, "median over more than 128 replicates is not supported");
+        skc_context* ctx = s->ctx;
+        ctx->use();
+        ctx->U.upload(U_host, static_cast<size_t>(L) * s->n, ctx->stream);
+        sym_contract_batch(s, ctx->U.p, L, 1);
+        ctx->values.alloc(static_cast<size_t>(L));
+        launch_sym_vvv_finish(ctx->stream, ctx->part.p, L, s->B, s->S, s->b, ctx->values.p);
+        ctx->check_launch();
+        CK(cudaMemcpyAsync(out_host, ctx->values.p, static_cast<size_t>(L) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->sync();
+    });
+}
+
+// natural-order spectrum of replicate m from the residue/bit-reversed layout
+static void spectrum_to_host(skc_context* ctx, const double2* spec, int m, std::uint32_t b, int N, int logN, int S,
+                             double* out) {
+    std::vector<double2> loc(b);
+    CK(cudaMemcpyAsync(loc.data(), spec + static_cast<size_t>(m) * b, b * sizeof(double2), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    ctx->sync();
+    for (int r = 0; r < S; ++r)
+        for (int j = 0; j < N; ++j) {
+            const std::uint32_t f = static_cast<std::uint32_t>(r) + static_cast<std::uint32_t>(S) * bitrev(j, logN);
+            out[2 * f] = loc[static_cast<size_t>(r) * N + j].x;
+            out[2 * f + 1] = loc[static_cast<size_t>(r) * N + j].y;
+        }
+}
+
+int skc_sym_cached_transform(skc_sym_set* s, int m, double* out_host) {
+    return guard([&] {
+        check_vec(s, "set");
+        require(m >= 0 && m < s->B, "replicate index out of range");
+        s->ctx->use();
+        s->ensure_fresh();
+        spectrum_to_host(s->ctx, s->spec.p, m, s->b, s->N, s->logN, s->S, out_host);
+    });
+}
+
+// ---- RTPM ----
+// Runs T power steps on L restarts resident at ctx->U (device) and the median vvv of
+// the finals into ctx->values. Degenerate flags accumulate in ctx->flags.
+static void rtpm_restarts_device(skc_sym_set* s, int L, int T_iters, double tol) {
+    skc_context* ctx = s->ctx;
+    s->ensure_fresh();
+    ctx->flags.alloc(static_cast<size_t>(L));
+    CK(cudaMemsetAsync(ctx->flags.p, 0, sizeof(int) * L, ctx->stream));
+    ctx->part.alloc(static_cast<size_t>(L) * s->B * s->S * std::max(s->n, 3));
+    const SymView v = s->view();
+    for (int t = 0; t < T_iters; ++t) {
+        {
+            SKC_PROF(ctx, "sym_contract");
+            launch_sym_contract(ctx->stream, v, ctx->U.p, L, 0, ctx->part.p);
+        }
+        SKC_PROF(ctx, "median");
+        launch_median_rows(ctx->stream, ctx->part.p, L, s->B, s->S, s->n, nullptr, ctx->U.p, tol, ctx->flags.p);
+    }
+    ctx->check_launch();
+    launch_sym_contract(ctx->stream, v, ctx->U.p, L, 1, ctx->part.p);
+    ctx->values.alloc(static_cast<size_t>(L));
+    launch_sym_vvv_finish(ctx->stream, ctx->part.p, L, s->B, s->S, s->b, ctx->values.p);
+    ctx->check_launch();
+}
+
+static void check_degenerate(skc_context* ctx, int L) {
+    std::vector<int> f(L);
+    CK(cudaMemcpyAsync(f.data(), ctx->flags.p, sizeof(int) * L, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    for (int x : f)
+        if (x) fail(kDegenerate, "power update produced a vanishing iterate");  // decompose.cpp:37-38
+}
+
+int skc_sym_rtpm(skc_sym_set* s, int k, int L, int T_iters, uint64_t seed, double tol, const double* inits,
+                 double* lambda, double* V, int* best_tau) {
+    return guard([&] {
+        check_vec(s, "set");
+        check_vec(lambda, "rtpm: lambda");
+        check_vec(V, "rtpm: V");
+        // decompose.cpp:15-20
+        if (k < 1 || L < 1 || T_iters < 1) fail(kInvalidArgument, "power method: k, L and T must be positive");
+        if (k > s->n) fail(kInvalidArgument, "power method: target rank exceeds tensor dimension");
+        require(s->B <= 128, "median over more than 128 replicates is not supported");
+        skc_context* ctx = s->ctx;
+        ctx->use();
+        const int n = s->n;
+        std::vector<double> gen;
+        if (!inits) {
+            gen.resize(static_cast<size_t>(L) * n);
+        }
+        ctx->ints.alloc(16);
+        ctx->dbl.alloc(4);
+        ctx->X.alloc(static_cast<size_t>(n));
+        for (int c = 0; c < k; ++c) {
+            const double* U0;
+            if (inits) {
+                U0 = inits + static_cast<size_t>(c) * L * n;
+            } else {
+                for (int t = 0; t < L; ++t) {
+                    Rng rng(derive_seed(seed, seed_tag::kPowerInit, static_cast<std::uint64_t>(c),
+                                        static_cast<std::uint64_t>(t)));
+                    rng.unit_sphere(n, gen.data() + static_cast<size_t>(t) * n);
+                }
+                U0 = gen.data();
+            }
+            ctx->U.upload(U0, static_cast<size_t>(L) * n, ctx->stream);
+            rtpm_restarts_device(s, L, T_iters, tol);
+            launch_argmax_first(ctx->stream, ctx->values.p, L, ctx->ints.p + 2, ctx->dbl.p);
+            ctx->check_launch();
+            int bt = 0;
+            double lam = 0.0;
+            CK(cudaMemcpyAsync(&bt, ctx->ints.p + 2, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaMemcpyAsync(&lam, ctx->dbl.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+            check_degenerate(ctx, L);  // synchronises
+            lambda[c] = lam;
+            if (best_tau) best_tau[c] = bt;
+            CK(cudaMemcpyAsync(V + static_cast<size_t>(c) * n, ctx->U.p + static_cast<size_t>(bt) * n, n * 8,
+                               cudaMemcpyDeviceToHost, ctx->stream));
+            // deflation: add_scaled_rank1(v, -lambda) (decompose.cpp:112)
+            if (lam != 0.0) {
+                CK(cudaMemcpyAsync(ctx->X.p, ctx->U.p + static_cast<size_t>(bt) * n, n * 8, cudaMemcpyDeviceToDevice,
+                                   ctx->stream));
+                s->version++;
+                sym_moment_device(s, ctx->X.p, nullptr, -lam, 1);
+            }
+            ctx->sync();
+        }
+    });
+}
+
+int skc_sym_rtpm_restarts(skc_sym_set* s, const double* U0_host, int L, int T_iters, double tol, double* finals_out,
+                          double* values_out) {
+    return guard([&] {
+        check_vec(s, "set");
+        check_vec(U0_host, "rtpm_restarts: U0");
+        require(L >= 1 && T_iters >= 1, "power method: k, L and T must be positive");
+        require(s->B <= 128, "median over more than 128 replicates is not supported");
+        skc_context* ctx = s->ctx;
+        ctx->use();
+        ctx->U.upload(U0_host, static_cast<size_t>(L) * s->n, ctx->stream);
+        rtpm_restarts_device(s, L, T_iters, tol);
+        if (finals_out)
+            CK(cudaMemcpyAsync(finals_out, ctx->U.p, static_cast<size_t>(L) * s->n * 8, cudaMemcpyDeviceToHost,
+                               ctx->stream));
+        if (values_out)
+            CK(cudaMemcpyAsync(values_out, ctx->values.p, static_cast<size_t>(L) * 8, cudaMemcpyDeviceToHost,
+                               ctx->stream));
+        check_degenerate(ctx, L);
+    });
+}
+
+// ---- asymmetric set ----
+int skc_asym_create(skc_context* ctx, int n, uint32_t b, int B, uint64_t master_seed, skc_asym_set** out) {
+    return guard([&] {
+        check_vec(ctx, "context");
+        validate_set_args(n, b, B);
+        auto s = std::make_unique<skc_asym_set>();
+        s->ctx = ctx;
+        s->n = n;
+        s->b = b;
+        s->B = B;
+        s->seed = master_seed;
+        s->hcoef.resize(static_cast<size_t>(B) * 3 * 2);
+        s->xcoef.resize(static_cast<size_t>(B) * 3 * 6);
+        for (int m = 0; m < B; ++m)  // sketch.cpp:161-167
+            for (int sl = 0; sl < 3; ++sl) {
+                poly_coefficients(2, derive_seed(master_seed, seed_tag::kAsymBucketHash, m, sl),
+                                  &s->hcoef[(m * 3 + sl) * 2]);
+                poly_coefficients(6, derive_seed(master_seed, seed_tag::kAsymSign, m, sl), &s->xcoef[(m * 3 + sl) * 6]);
+            }
+        init_asym_device(s.get(), nullptr);
+        *out = s.release();
+    });
+}
+int skc_asym_create_from_coefficients(skc_context* ctx, int n, uint32_t b, int B, uint64_t master_seed,
+                                      const uint64_t* hcoef, const uint64_t* xcoef, const double* data_host,
+                                      skc_asym_set** out) {
+    return guard([&] {
+        check_vec(ctx, "context");
+        validate_set_args(n, b, B);
+        check_vec(hcoef, "hcoef");
+        check_vec(xcoef, "xcoef");
+        for (int x = 0; x < B * 6; ++x) require(hcoef[x] < kHashPrime, "PolyHash: coefficient out of range");
+        for (int x = 0; x < B * 18; ++x) require(xcoef[x] < kHashPrime, "PolyHash: coefficient out of range");
+        auto s = std::make_unique<skc_asym_set>();
+        s->ctx = ctx;
+        s->n = n;
+        s->b = b;
+        s->B = B;
+        s->seed = master_seed;
+        s->hcoef.assign(hcoef, hcoef + static_cast<size_t>(B) * 6);
+        s->xcoef.assign(xcoef, xcoef + static_cast<size_t>(B) * 18);
+        init_asym_device(s.get(), data_host);
+        *out = s.release();
+    });
+}
+int skc_asym_destroy(skc_asym_set* s) {
+    return guard([&] {
+        if (!s) return;
+        s->ctx->use();
+        s->ctx->sync();
+        delete s;
+    });
+}
+int skc_asym_info(const skc_asym_set* s, int* n, uint32_t* b, int* B, uint64_t* seed, uint64_t* version) {
+    return guard([&] {
+        check_vec(s, "set");
+        if (n) *n = s->n;
+        if (b) *b = s->b;
+        if (B) *B = s->B;
+        if (seed) *seed = s->seed;
+        if (version) *version = s->version;
+    });
+}
+int skc_asym_tables(const skc_asym_set* s, int m, uint32_t* bucket, double* sign) {
+    return guard([&] {
+        check_vec(s, "set");
+        require(m >= 0 && m < s->B, "replicate index out of range");
+        s->ctx->use();
+        const size_t off = static_cast<size_t>(m) * 3 * s->n, cnt = static_cast<size_t>(3) * s->n;
+        if (bucket) CK(cudaMemcpyAsync(bucket, s->bucket.p + off, cnt * 4, cudaMemcpyDeviceToHost, s->ctx->stream));
+        if (sign) CK(cudaMemcpyAsync(sign, s->sign.p + off, cnt * 8, cudaMemcpyDeviceToHost, s->ctx->stream));
+        s->ctx->sync();
+    });
+}
+int skc_asym_coefficients(const skc_asym_set* s, uint64_t* hcoef, uint64_t* xcoef) {
+    return guard([&] {
+        check_vec(s, "set");
+        if (hcoef) std::copy(s->hcoef.begin(), s->hcoef.end(), hcoef);
+        if (xcoef) std::copy(s->xcoef.begin(), s->xcoef.end(), xcoef);
+    });
+}
+int skc_asym_accumulate_dense(skc_asym_set* s, const void* T, int dtype, int location, int i0, int i1) {
+    return guard([&] {
+        check_vec(s, "set");
+        check_vec(T, "accumulate_dense: tensor");
+        require(dtype == SKC_F64 || dtype == SKC_F32, "accumulate_dense: dtype must be SKC_F64 or SKC_F32");
+        require(location == SKC_HOST || location == SKC_DEVICE, "accumulate_dense: bad location");
+        require(0 <= i0 && i0 <= i1 && i1 <= s->n, "accumulate_dense: slice out of range");
+        require(s->n <= 65535, "accumulate_dense: n above 65535 is not supported");
+        skc_context* ctx = s->ctx;
+        ctx->use();
+        const void* Td = stage_tensor(ctx, T, s->n, dtype, location);
+        s->version++;  // sketch.cpp:175
+        run_dense_build(ctx, Td, s->n, dtype, false, i0, i1, s->B, s->b, s->packed.p, s->data.p);
+        ctx->sync();
+    });
+}
+
+static void asym_factored_device(skc_asym_set* s, const double* ad, const double* Ud, const double* Vd,
+                                 const double* Wd, long long Ncomp, double alpha, int m_only, double2* dst,
+                                 bool overwrite) {
+    skc_context* ctx = s->ctx;
+    const int Bm = m_only >= 0 ? 1 : s->B;
+    const int per_rep = Bm * s->S;
+    int chunks = static_cast<int>(std::max<long long>(1, std::min<long long>(Ncomp, (4ll * ctx->sms + per_rep - 1) / per_rep)));
+    ctx->freq_acc.alloc(static_cast<size_t>(chunks) * per_rep * s->N * 2);
+    ctx->tmp.alloc(static_cast<size_t>(s->B) * s->b);
+    AsymView v = s->view();
+    launch_asym_factored_accumulate(ctx->stream, v, ad, Ud, Vd, Wd, Ncomp, chunks, m_only, ctx->freq_acc.p);
+    ctx->check_launch();
+    // reduce into tmp slot of replicate (m_only or all)
+    double2* tmp = ctx->tmp.p;
+    launch_freq_reduce_inverse(ctx->stream, ctx->freq_acc.p, chunks, Bm, s->S, s->N, s->logN, s->b, s->logb, v.tw,
+                               tmp);
+    ctx->check_launch();
+    // combine: for m_only the tmp holds one replicate at index 0
+    launch_combine_residues(ctx->stream, tmp, Bm, s->S, s->N, s->b, v.tw, alpha, -1, overwrite,
+                            dst + (m_only >= 0 ? static_cast<size_t>(m_only) * s->b * 0 : 0));
+    ctx->check_launch();
+}
+
+int skc_asym_add_rank1(skc_asym_set* s, double alpha, const double* u, const double* v, const double* w) {
+    return guard([&] {
+        check_vec(s, "set");
+        check_vec(u, "add_rank1: u");
+        check_vec(v, "add_rank1: v");
+        check_vec(w, "add_rank1: w");
+        skc_context* ctx = s->ctx;
+        ctx->use();
+        s->version++;  // sketch.cpp:216
+        const int n = s->n;
+        std::vector<double> h(3 * static_cast<size_t>(n));
+        std::copy(u, u + n, h.begin());
+        std::copy(v, v + n, h.begin() + n);
+        std::copy(w, w + n, h.begin() + 2 * n);
+        ctx->X.upload(h.data(), h.size(), ctx->stream);
+        asym_factored_device(s, nullptr, ctx->X.p, ctx->X.p + n, ctx->X.p + 2 * n, 1, alpha, -1, s->data.p, false);
+        ctx->sync();
+    });
+}
+int skc_asym_accumulate_factored(skc_asym_set* s, long long N, const double* a, const double* U, const double* V,
+                                 const double* W) {
+    return guard([&] {
+        check_vec(s, "set");
+        require(N >= 0, "accumulate_factored: negative component count");
+        skc_context* ctx = s->ctx;
+        ctx->use();
+        s->version++;  // sketch.cpp:226
+        if (N == 0) return;
+        check_vec(a, "accumulate_factored: a");
+        check_vec(U, "accumulate_factored: U");
+        check_vec(V, "accumulate_factored: V");
+        check_vec(W, "accumulate_factored: W");
+        const size_t Nn = static_cast<size_t>(N) * s->n;
+        std::vector<double> h(3 * Nn + static_cast<size_t>(N));
+        std::copy(U, U + Nn, h.begin());
+        std::copy(V, V + Nn, h.begin() + Nn);
+        std::copy(W, W + Nn, h.begin() + 2 * Nn);
+        std::copy(a, a + N, h.begin() + 3 * Nn);
+        ctx->X.upload(h.data(), h.size(), ctx->stream);
+        asym_factored_device(s, ctx->X.p + 3 * Nn, ctx->X.p, ctx->X.p + Nn, ctx->X.p + 2 * Nn, N, 1.0, -1, s->data.p,
+                             false);
+        ctx->sync();
+    });
+}
+int skc_asym_rank1_sketch(skc_asym_set* s, int m, const double* u, const double* v, const double* w,
+                          double* out_host) {
+    return guard([&] {
+        check_vec(s, "set");
+        require(m >= 0 && m < s->B, "replicate index out of range");
+        check_vec(u, "rank1_sketch: u");
+        check_vec(v, "rank1_sketch: v");
+        check_vec(w, "rank1_sketch: w");
+        skc_context* ctx = s->ctx;
+        ctx->use();
+        const int n = s->n;
+        std::vector<double> h(3 * static_cast<size_t>(n));
+        std::copy(u, u + n, h.begin());
+        std::copy(v, v + n, h.begin() + n);
+        std::copy(w, w + n, h.begin() + 2 * n);
+        ctx->X.upload(h.data(), h.size(), ctx->stream);
+        DevBuf<double2> out;
+        out.alloc(s->b);
+        asym_factored_device(s, nullptr, ctx->X.p, ctx->X.p + n, ctx->X.p + 2 * n, 1, 1.0, m, out.p, true);
+        CK(cudaMemcpyAsync(out_host, out.p, s->b * sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->sync();
+    });
+}
+int skc_asym_read_data(const skc_asym_set* s, int m, double* out_host) {
+    return guard([&] {
+        check_vec(s, "set");
+        require(m < s->B, "replicate index out of range");
+        s->ctx->use();
+        const size_t off = m < 0 ? 0 : static_cast<size_t>(m) * s->b;
+        const size_t cnt = m < 0 ? static_cast<size_t>(s->B) * s->b : s->b;
+        CK(cudaMemcpyAsync(out_host, s->data.p + off, cnt * sizeof(double2), cudaMemcpyDeviceToHost, s->ctx->stream));
+        s->ctx->sync();
+    });
+}
+int skc_asym_write_data(skc_asym_set* s, int m, const double* in_host) {
+    return guard([&] {
+        check_vec(s, "set");
+        require(m < s->B, "replicate index out of range");
+        s->ctx->use();
+        const size_t off = m < 0 ? 0 : static_cast<size_t>(m) * s->b;
+        const size_t cnt = m < 0 ? static_cast<size_t>(s->B) * s->b : s->b;
+        CK(cudaMemcpyAsync(s->data.p + off, in_host, cnt * sizeof(double2), cudaMemcpyHostToDevice, s->ctx->stream));
+        s->version++;
+        s->ctx->sync();
+    });
+}
+int skc_asym_data_device(skc_asym_set* s, void** dev_ptr, size_t* bytes) {
+    return guard([&] {
+        check_vec(s, "set");
+        *dev_ptr = s->data.p;
+        *bytes = static_cast<size_t>(s->B) * s->b * sizeof(double2);
+    });
+}
+int skc_asym_bump_version(skc_asym_set* s) {
+    return guard([&] {
+        check_vec(s, "set");
+        s->version++;
+    });
+}
+int skc_asym_recover_entry(const skc_asym_set* s, int i, int j, int k, double* out) {
+    return guard([&] {  // sketch.cpp:250-262
+        check_vec(s, "set");
+        const int n = s->n;
+        if (i < 0 || j < 0 || k < 0 || i >= n || j >= n || k >= n)
+            fail(kInvalidArgument, "recover_entry: index out of range");
+        s->ctx->use();
+        std::vector<double> est(s->B);
+        for (int m = 0; m < s->B; ++m) {
+            const int idx[3] = {i, j, k};
+            std::uint32_t bk[3];
+            double sg[3];
+            for (int q = 0; q < 3; ++q) {
+                const size_t off = (static_cast<size_t>(m) * 3 + q) * n + idx[q];
+                CK(cudaMemcpy(&bk[q], s->bucket.p + off, 4, cudaMemcpyDeviceToHost));
+                CK(cudaMemcpy(&sg[q], s->sign.p + off, 8, cudaMemcpyDeviceToHost));
+            }
+            const std::uint32_t t = static_cast<std::uint32_t>((std::uint64_t{bk[0]} + bk[1] + bk[2]) % s->b);
+            double2 z;
+            CK(cudaMemcpy(&z, s->data.p + static_cast<size_t>(m) * s->b + t, sizeof(double2), cudaMemcpyDeviceToHost));
+            est[m] = sg[0] * sg[1] * sg[2] * z.x;
+        }
+        std::size_t mid = est.size() / 2;
+        std::nth_element(est.begin(), est.begin() + mid, est.end());
+        double hi = est[mid];
+        if (est.size() % 2 == 1) {
+            *out = hi;
+        } else {
+            double lo = *std::max_element(est.begin(), est.begin() + mid);
+            *out = 0.5 * (lo + hi);
+        }
+    });
+}
+int skc_asym_mode_contraction(skc_asym_set* s, int free_mode, const double* X_host, const double* Y_host, int L,
+                              double* out_host) {
+    return guard([&] {
+        check_vec(s, "set");
+        check_vec(X_host, "mode_contraction: x");
+        check_vec(Y_host, "mode_contraction: y");
+        if (free_mode < 0 || free_mode > 2)
+            fail(kInvalidArgument, "mode_contraction: free_mode must be 0, 1 or 2");  // contraction.cpp:253-254
+        require(L >= 1, "mode_contraction: need at least one vector pair");
+        require(s->B <= 128, "median over more than 128 replicates is not supported");
+        skc_context* ctx = s->ctx;
+        ctx->use();
+        const size_t Ln = static_cast<size_t>(L) * s->n;
+        std::vector<double> h(2 * Ln);
+        std::copy(X_host, X_host + Ln, h.begin());
+        std::copy(Y_host, Y_host + Ln, h.begin() + Ln);
+        ctx->U.upload(h.data(), h.size(), ctx->stream);
+        s->ensure_fresh();
+        ctx->part.alloc(static_cast<size_t>(L) * s->B * s->S * s->n);
+        launch_asym_mode(ctx->stream, s->view(), free_mode, ctx->U.p, ctx->U.p + Ln, L, ctx->part.p);
+        ctx->check_launch();
+        ctx->values.alloc(Ln);
+        launch_median_rows(ctx->stream, ctx->part.p, L, s->B, s->S, s->n, ctx->values.p, nullptr, 0.0, nullptr);
+        ctx->check_launch();
+        CK(cudaMemcpyAsync(out_host, ctx->values.p, Ln * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->sync();
+    });
+}
+int skc_asym_vvv(skc_asym_set* s, const double* U_host, int L, double* out_host) {
+    return guard([&] {
+        check_vec(s, "set");
+        check_vec(U_host, "vvv: u");
+        require(L >= 1, "vvv: need at least one vector");
+        require(s->B <= 128, "median over more than 128 replicates is not supported");
+        skc_context* ctx = s->ctx;
+        ctx->use();
+        ctx->U.upload(U_host, static_cast<size_t>(L) * s->n, ctx->stream);
+        s->ensure_fresh();
+        ctx->part.alloc(static_cast<size_t>(L) * s->B * s->S);
+        launch_asym_vvv(ctx->stream, s->view(), ctx->U.p, L, ctx->part.p);
+        ctx->check_launch();
+        ctx->values.alloc(static_cast<size_t>(L));
+        launch_asym_vvv_finish(ctx->stream, ctx->part.p, L, s->B, s->S, s->b, ctx->values.p);
+        ctx->check_launch();
+        CK(cudaMemcpyAsync(out_host, ctx->values.p, static_cast<size_t>(L) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->sync();
+    });
+}
+int skc_asym_cached_transform(skc_asym_set* s, int m, double* out_host) {
+    return guard([&] {
+        check_vec(s, "set");
+        require(m >= 0 && m < s->B, "replicate index out of range");
+        s->ctx->use();
+        s->ensure_fresh();
+        spectrum_to_host(s->ctx, s->spec.p, m, s->b, s->N, s->logN, s->S, out_host);
+    });
+}
+
+// ---- generators ----
+static void planted_factors(int n, int rank, std::uint64_t seed, double* lambda, double* V) {
+    Rng lr(derive_seed(seed, seed_tag::kGenLambda));
+    for (int r = 0; r < rank; ++r) lambda[r] = 1.0 + lr.uniform();  // U[1,2]
+    Rng br(derive_seed(seed, seed_tag::kGenBasis));
+    for (int r = 0; r < rank; ++r)
+        for (int i = 0; i < n; ++i) V[static_cast<size_t>(r) * n + i] = br.gaussian();
+    // modified Gram-Schmidt, two passes (orthonormal columns = Q of a QR)
+    for (int pass = 0; pass < 2; ++pass)
+        for (int r = 0; r < rank; ++r) {
+            double* v = V + static_cast<size_t>(r) * n;
+            for (int q = 0; q < r; ++q) {
+                const double* w = V + static_cast<size_t>(q) * n;
+                double d = 0;
+                for (int i = 0; i < n; ++i) d += v[i] * w[i];
+                for (int i = 0; i < n; ++i) v[i] -= d * w[i];
+            }
+            double s = 0;
+            for (int i = 0; i < n; ++i) s += v[i] * v[i];
+            const double inv = 1.0 / std::sqrt(s);
+            for (int i = 0; i < n; ++i) v[i] *= inv;
+        }
+}
+
+int skc_gen_planted_tensor(int n, int rank, double sigma, uint64_t seed, int dtype, void* T_out, double* lambda_out,
+                           double* V_out) {
+    return guard([&] {
+        require(n >= 1 && rank >= 1 && rank <= n, "gen_planted_tensor: need 1 <= rank <= n");
+        require(dtype == SKC_F64 || dtype == SKC_F32, "gen_planted_tensor: bad dtype");
+        check_vec(T_out, "gen_planted_tensor: T");
+        std::vector<double> lam(rank), V(static_cast<size_t>(rank) * n);
+        planted_factors(n, rank, seed, lam.data(), V.data());
+        if (lambda_out) std::copy(lam.begin(), lam.end(), lambda_out);
+        if (V_out) std::copy(V.begin(), V.end(), V_out);
+        // noise for the sorted triples in loop order, mirrored (tensor.cpp:228-244 convention)
+        Rng nr(derive_seed(seed, seed_tag::kGenNoise));
+        auto put = [&](size_t off, double x) {
+            if (dtype == SKC_F64)
+                static_cast<double*>(T_out)[off] = x;
+            else
+                static_cast<float*>(T_out)[off] = static_cast<float>(x);
+        };
+        for (int i = 0; i < n; ++i)
+            for (int j = i; j < n; ++j)
+                for (int k = j; k < n; ++k) {
+                    double s = 0;
+                    for (int r = 0; r < rank; ++r)
+                        s += lam[r] * V[static_cast<size_t>(r) * n + i] * V[static_cast<size_t>(r) * n + j] *
+                             V[static_cast<size_t>(r) * n + k];
+                    if (sigma > 0) s += sigma * nr.gaussian();
+                    const int p[6][3] = {{i, j, k}, {i, k, j}, {j, i, k}, {j, k, i}, {k, i, j}, {k, j, i}};
+                    for (auto& q : p) put((static_cast<size_t>(q[0]) * n + q[1]) * n + q[2], s);
+                }
+    });
+}
+
+int skc_gen_planted_tensor_device(skc_context* ctx, int n, int rank, double sigma, uint64_t seed, int dtype,
+                                  void* dev_out, double* lambda_out, double* V_out) {
+    return guard([&] {
+        check_vec(ctx, "context");
+        require(n >= 1 && rank >= 1 && rank <= n, "gen_planted_tensor: need 1 <= rank <= n");
+        require(dtype == SKC_F64 || dtype == SKC_F32, "gen_planted_tensor: bad dtype");
+        ctx->use();
+        std::vector<double> lam(rank), V(static_cast<size_t>(rank) * n);
+        planted_factors(n, rank, seed, lam.data(), V.data());
+        if (lambda_out) std::copy(lam.begin(), lam.end(), lambda_out);
+        if (V_out) std::copy(V.begin(), V.end(), V_out);
+        DevBuf<double> dl, dv;
+        dl.upload(lam.data(), lam.size(), ctx->stream);
+        dv.upload(V.data(), V.size(), ctx->stream);
+        launch_gen_planted(ctx->stream, n, rank, dl.p, dv.p, sigma, derive_seed(seed, seed_tag::kGenNoise), dtype,
+                           dev_out);
+        ctx->check_launch();
+        ctx->sync();
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,228 @@
+// Residue-split, in-shared-memory radix-16 FFT used by every sketch kernel.
+//
+// A length-b transform (b = S * N, N = "local length") is split into S independent
+// CTA-local transforms of length N, one per frequency residue r in [0, S):
+//
+//   forward   F[r + S*f2] = sum_{t'} ( sum_{t = t' mod N} x[t] w_b^{-r t} ) w_N^{-f2 t'}
+//   inverse   z[t]        = sum_r w_b^{r t} v_r[t mod N],
+//             v_r[t']     = sum_{f2} Z[r + S*f2] w_N^{f2 t'}
+//
+// Sketch inputs are sparse (n nonzeros: count sketches of n-vectors) and contraction
+// outputs are read at n positions only, so the split needs no cross-CTA exchange:
+// the prologue scatters the n nonzeros with their residue twiddle and the epilogue
+// gathers n outputs. The local transform is an in-place decimation-in-frequency
+// (forward, natural -> bit-reversed order) and its mirror decimation-in-time
+// (inverse, bit-reversed -> natural); spectra are stored in that bit-reversed
+// local order, so no reorder pass is ever needed (pointwise products do not care).
+//
+// Everything here is __host__ __device__ so tests can emulate a CTA on the CPU
+// (tests/cpu_emulation/) and check the index algebra against the oracle FFT.
+// Semantics follow the reference wrapper proj/src/fft.cpp:48-77 (FFTW_FORWARD sign,
+// unnormalised forward, inverse unscaled unless the caller scales by 1/b).
+#pragma once
+
+#include <cstdint>
+
+#ifdef __CUDACC__
+#define SKC_HD __host__ __device__ __forceinline__
+#else
+#define SKC_HD inline
+#include <cmath>
+struct double2 {
+    double x, y;
+};
+#endif
+
+namespace skc {
+
+SKC_HD double2 mk(double x, double y) {
+    double2 r;
+    r.x = x;
+    r.y = y;
+    return r;
+}
+SKC_HD double2 cadd(double2 a, double2 b) { return mk(a.x + b.x, a.y + b.y); }
+SKC_HD double2 csub(double2 a, double2 b) { return mk(a.x - b.x, a.y - b.y); }
+SKC_HD double2 cmul(double2 a, double2 b) { return mk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+SKC_HD double2 conj(double2 a) { return mk(a.x, -a.y); }
+SKC_HD double2 cscale(double2 a, double s) { return mk(a.x * s, a.y * s); }
+// a * conj(b)
+SKC_HD double2 cmulc(double2 a, double2 b) { return mk(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y); }
+
+// omega^e with omega = i (complex4 signs, proj/src/sketch.cpp:38-45): e mod 4.
+SKC_HD double2 root4_times(unsigned e, double v) {
+    switch (e & 3u) {
+        case 0: return mk(v, 0.0);
+        case 1: return mk(0.0, v);
+        case 2: return mk(-v, 0.0);
+        default: return mk(0.0, -v);
+    }
+}
+// Re(omega^{-e} z) (proj/src/contraction.cpp:40-47)
+SKC_HD double re_rot_conj(unsigned e, double2 z) {
+    switch (e & 3u) {
+        case 0: return z.x;
+        case 1: return z.y;
+        case 2: return -z.x;
+        default: return -z.y;
+    }
+}
+
+// Padded shared-memory index: one pad slot per 16 complex values keeps the
+// radix-16 passes free of bank conflicts for 16-byte elements.
+SKC_HD int pad16(int x) { return x + (x >> 4); }
+SKC_HD int padded_len(int N) { return N + (N >> 4) + 1; }
+
+SKC_HD int ilog2(unsigned x) {
+    int r = 0;
+    while ((1u << r) < x) ++r;
+    return r;
+}
+
+// Constant roots w_M^{-q} for M in {2,4,8,16}, q < M/2 (forward sign).
+SKC_HD double2 const_root(int M, int q) {
+    // cos/sin of 2*pi*q/16 for q = 0..7
+    const double c16[8] = {1.0,
+                           0.92387953251128675613,
+                           0.70710678118654752440,
+                           0.38268343236508977173,
+                           0.0,
+                           -0.38268343236508977173,
+                           -0.70710678118654752440,
+                           -0.92387953251128675613};
+    const double s16[8] = {0.0,
+                           0.38268343236508977173,
+                           0.70710678118654752440,
+                           0.92387953251128675613,
+                           1.0,
+                           0.92387953251128675613,
+                           0.70710678118654752440,
+                           0.38268343236508977173};
+    int idx = q * (16 / M);
+    return mk(c16[idx], -s16[idx]);
+}
+
+// Pass plan for a local length N = 2^p: the first pass takes radix 2^(p mod 4)
+// (if nonzero), every later pass radix 16. Pass j starts at half-size h_j.
+struct PassPlan {
+    int npass;
+    int logr[8];  // log2 radix of pass j
+    int h[8];     // half-size at the start of pass j
+};
+
+SKC_HD PassPlan make_plan(int N) {
+    PassPlan pl;
+    pl.npass = 0;
+    int p = ilog2(static_cast<unsigned>(N));
+    int h = N >> 1;
+    int first = p % 4;
+    if (first == 0 && p > 0) first = 4;
+    int rem = p;
+    int lr = first;
+    while (rem > 0) {
+        pl.logr[pl.npass] = lr;
+        pl.h[pl.npass] = h;
+        pl.npass++;
+        h >>= lr;
+        rem -= lr;
+        lr = 4;
+    }
+    return pl;
+}
+
+// One forward (DIF) pass on item w of array x (length N, padded smem layout).
+// tw: table of w_b^k = (cos 2 pi k / b, sin 2 pi k / b), k in [0, b).
+// logb_over: log2(b) used to index tw for stage twiddles w_{2hs}^{-pos}.
+template <int LOGR>
+SKC_HD void dif_pass_item(double2* x, int w, int h, const double2* tw, int logb) {
+    constexpr int R = 1 << LOGR;
+    const int g = (2 * h) >> LOGR;  // element spacing
+    const int block = w / g;
+    const int pos = w - block * g;
+    const int base = block * 2 * h + pos;
+    double2 v[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) v[q] = x[pad16(base + q * g)];
+#pragma unroll
+    for (int s = 0; s < LOGR; ++s) {
+        const int hs = h >> s;
+        const int Hq = R >> (s + 1);
+        // w_{2hs}^{-pos} = conj(tw[pos * b / (2 hs)])
+        const int lg2hs = ilog2(static_cast<unsigned>(2 * hs));
+        double2 W = conj(tw[static_cast<unsigned>(pos) << (logb - lg2hs)]);
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            if (q & Hq) continue;
+            const int qp = q & (Hq - 1);  // position inside the (R>>s)-block, lower half
+            double2 a = v[q], c = v[q + Hq];
+            v[q] = cadd(a, c);
+            double2 d = csub(a, c);
+            double2 tw2 = (qp == 0) ? W : cmul(W, const_root(R >> s, qp));
+            v[q + Hq] = cmul(d, tw2);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) x[pad16(base + q * g)] = v[q];
+}
+
+// Mirror inverse (DIT) pass: unscaled, conjugate twiddles.
+template <int LOGR>
+SKC_HD void dit_pass_item(double2* x, int w, int h, const double2* tw, int logb) {
+    constexpr int R = 1 << LOGR;
+    const int g = (2 * h) >> LOGR;
+    const int block = w / g;
+    const int pos = w - block * g;
+    const int base = block * 2 * h + pos;
+    double2 v[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) v[q] = x[pad16(base + q * g)];
+#pragma unroll
+    for (int s = LOGR - 1; s >= 0; --s) {
+        const int hs = h >> s;
+        const int Hq = R >> (s + 1);
+        const int lg2hs = ilog2(static_cast<unsigned>(2 * hs));
+        double2 W = tw[static_cast<unsigned>(pos) << (logb - lg2hs)];
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            if (q & Hq) continue;
+            const int qp = q & (Hq - 1);
+            double2 tw2 = (qp == 0) ? W : cmul(W, conj(const_root(R >> s, qp)));
+            double2 a = v[q];
+            double2 c = cmul(v[q + Hq], tw2);
+            v[q] = cadd(a, c);
+            v[q + Hq] = csub(a, c);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) x[pad16(base + q * g)] = v[q];
+}
+
+SKC_HD void dif_pass_dispatch(int logr, double2* x, int w, int h, const double2* tw, int logb) {
+    switch (logr) {
+        case 1: dif_pass_item<1>(x, w, h, tw, logb); break;
+        case 2: dif_pass_item<2>(x, w, h, tw, logb); break;
+        case 3: dif_pass_item<3>(x, w, h, tw, logb); break;
+        default: dif_pass_item<4>(x, w, h, tw, logb); break;
+    }
+}
+SKC_HD void dit_pass_dispatch(int logr, double2* x, int w, int h, const double2* tw, int logb) {
+    switch (logr) {
+        case 1: dit_pass_item<1>(x, w, h, tw, logb); break;
+        case 2: dit_pass_item<2>(x, w, h, tw, logb); break;
+        case 3: dit_pass_item<3>(x, w, h, tw, logb); break;
+        default: dit_pass_item<4>(x, w, h, tw, logb); break;
+    }
+}
+
+// Bit reversal of j over `bits` bits: local spectrum slot j holds frequency
+// f = r + S * bitrev(j).
+SKC_HD unsigned bitrev(unsigned j, int bits) {
+    unsigned r = 0;
+    for (int i = 0; i < bits; ++i) {
+        r = (r << 1) | (j & 1u);
+        j >>= 1;
+    }
+    return r;
+}
+
+}  // namespace skc

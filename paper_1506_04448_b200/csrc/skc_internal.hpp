@@ -1,0 +1,128 @@
+// Internal interface between the C-ABI orchestration (skc_abi.cu) and the
+// kernels (skc_kernels.cu). Device pointers only; every launch goes on `st`.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "skc_fft.cuh"
+
+namespace skc {
+
+// Per-set device view used by the sketch kernels.
+struct SymView {
+    int n;
+    std::uint32_t b;
+    int logb;
+    int B;
+    const std::uint32_t* bucket1;  // B x n
+    const std::uint32_t* bucket2;
+    const std::uint32_t* bucket3;
+    const std::uint8_t* sexp;
+    const std::uint32_t* packed;  // h | e << 30
+    const double2* tw;            // w_b^k, k in [0, b)
+    // residue split
+    int N, logN, S;
+    const std::uint32_t* perm1;  // B x n: indices sorted by (bucket1 mod N, i)
+    const std::uint32_t* perm2;  // B x n: sorted by (bucket2 mod N, i)
+    const double2* data;         // B x b time domain
+    const double2* spec;         // B x S x N local bit-reversed spectra
+};
+
+struct AsymView {
+    int n;
+    std::uint32_t b;
+    int logb;
+    int B;
+    const std::uint32_t* bucket;  // B x 3 x n
+    const double* sign;           // B x 3 x n (+-1)
+    const std::uint32_t* packed;  // B x 3 x n: h | neg << 31
+    const double2* tw;
+    int N, logN, S;
+    const std::uint32_t* perm;  // B x 3 x n sorted by (bucket mod N, i)
+    const double2* data;
+    const double2* spec;
+};
+
+std::uint64_t launch_count();
+void count_launch();
+std::uint64_t transform_units();          // local FFTs executed, in units of length-N transforms
+void count_transforms(std::uint64_t local_ffts, int S);  // accumulate S-split counts
+
+// tables
+void launch_sym_tables(cudaStream_t st, const std::uint64_t* hcoef, const std::uint64_t* scoef, int n,
+                       std::uint32_t b, int B, std::uint32_t* b1, std::uint32_t* b2, std::uint32_t* b3,
+                       std::uint8_t* sexp, std::uint32_t* packed);
+void launch_asym_tables(cudaStream_t st, const std::uint64_t* hcoef, const std::uint64_t* xcoef, int n,
+                        std::uint32_t b, int B, std::uint32_t* bucket, double* sign, std::uint32_t* packed);
+// keys: nrep x n table; perm[rep][rank] = i sorted by (keys & mask, i)
+void launch_sort_perm(cudaStream_t st, const std::uint32_t* keys, int nrep, int n, std::uint32_t mask,
+                      std::uint32_t* perm);
+
+// dense build
+struct BuildPlan {
+    int n;
+    bool sym;
+    int dtype;  // 0 f64, 1 f32
+    const std::uint32_t* rowtab;
+    int nrows;
+    const int* chunk_begin;  // C+1, device
+    int C, G;
+    long long total_slots;
+    int slots_per_cta;
+    int threads;
+    std::uint32_t bmask;
+    int B;
+    const std::uint32_t* packed;
+    double* prepass_partials;  // kPrepassBlocks
+    int* scale_exp;            // device int
+    int* nonfinite;            // device int
+    long long* partials;       // C x total_slots
+    double* data_as_double;    // B x b x 2
+};
+constexpr int kPrepassBlocks = 1024;
+void launch_build_prepass(cudaStream_t st, const void* T, const BuildPlan& p);
+void launch_build_main(cudaStream_t st, const void* T, const BuildPlan& p);
+void launch_build_finalize(cudaStream_t st, const BuildPlan& p);
+
+// spectra: spec[m][r][j] = local DIF of residue r of data[m]
+void launch_spectrum(cudaStream_t st, const double2* data, std::uint32_t b, int logb, int B, int N, int logN,
+                     int S, const double2* tw, double2* spec);
+
+// symmetric contractions. mode 0: Ivv partials (L x B x S x n); mode 1: vvv
+// partials (L x B x S x 3: acc1, acc2, term3).
+void launch_sym_contract(cudaStream_t st, const SymView& v, const double* U, int L, int mode, double* out);
+// medians: part L x B x S x n -> out L x n (and optional normalisation into Unext)
+void launch_median_rows(cudaStream_t st, const double* part, int L, int B, int S, int n, double* out,
+                        double* Unext, double tol, int* flags);
+void launch_sym_vvv_finish(cudaStream_t st, const double* part, int L, int B, int S, std::uint32_t b,
+                           double* values);
+void launch_asym_vvv_finish(cudaStream_t st, const double* part, int L, int B, int S, std::uint32_t b,
+                            double* values);
+void launch_argmax_first(cudaStream_t st, const double* values, int L, int* best, double* best_value);
+
+// deflation / rank-1 / factored / moment accumulation (frequency domain)
+// acc[chunk][m][r][N] partial spectra; then reduce+DIT -> tmp[m][r][N]; combine -> data.
+// acc[chunk][m][r][j] = sum over samples s in chunk of wscale * w[s] * F_r(CS_m(x_s))[j]^3
+// (w may be null: weight 1). chunks * B * S CTAs.
+void launch_sym_moment_accumulate(cudaStream_t st, const SymView& v, const double* X, const double* w,
+                                  double wscale, long long Nsamp, int chunks, double* acc);
+void launch_freq_reduce_inverse(cudaStream_t st, const double* acc, int chunks, int B, int S, int N, int logN,
+                                std::uint32_t b, int logb, const double2* tw, double2* tmp);
+void launch_combine_residues(cudaStream_t st, const double2* tmp, int B, int S, int N, std::uint32_t b,
+                             const double2* tw, double alpha, int m_only, bool overwrite, double2* dst);
+void launch_asym_factored_accumulate(cudaStream_t st, const AsymView& v, const double* a, const double* U,
+                                     const double* V, const double* W, long long Ncomp, int chunks, int m_only,
+                                     double* acc);
+
+// asymmetric contractions
+void launch_asym_mode(cudaStream_t st, const AsymView& v, int free_mode, const double* X, const double* Y, int L,
+                      double* part);
+void launch_asym_vvv(cudaStream_t st, const AsymView& v, const double* U, int L, double* part);
+
+// generators
+void launch_gen_planted(cudaStream_t st, int n, int rank, const double* lambda, const double* V, double sigma,
+                        std::uint64_t seed, int dtype, void* out);
+
+}  // namespace skc

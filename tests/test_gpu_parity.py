@@ -1,0 +1,343 @@
+"""GPU parity of the sm_100a path against the CPU oracle, through the C-ABI.
+
+Tolerances (BASELINE.json north_star): hash tables bit-exact; sketches
+per-replicate ||d||_2/||s||_2 <= 1e-9 (fp64 input) and <= 1e-4 (fp32 input);
+contraction vectors ||d||_inf/||v||_inf <= 1e-9; RTPM (lambda_k, v_k) relative
+<= 1e-9 after sign/permutation alignment.
+"""
+import json
+import pathlib
+
+import numpy as np
+import pytest
+
+import oracle_py as O
+
+pytestmark = pytest.mark.gpu
+
+SKETCH_TOL = 1e-9
+SKETCH_TOL_F32 = 1e-4
+VEC_TOL = 1e-9
+GOLDEN = pathlib.Path(__file__).resolve().parent / "golden"
+
+
+def skb():
+    import paper_1506_04448_b200 as m
+
+    return m
+
+
+def sym_tensor(n, seed, scale=1.0):
+    rng = np.random.default_rng(seed)
+    A = rng.normal(size=(n, n, n)) * scale
+    return sum(A.transpose(p) for p in [(0, 1, 2), (0, 2, 1), (1, 0, 2), (1, 2, 0), (2, 0, 1), (2, 1, 0)]) / 6
+
+
+def rel_per_replicate(got, ref):
+    num = np.linalg.norm(got - ref, axis=-1)
+    den = np.maximum(np.linalg.norm(ref, axis=-1), 1e-300)
+    return float(np.max(num / den))
+
+
+def vec_rel(got, ref):
+    return float(np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-300))
+
+
+# ---------------------------------------------------------------- tables
+@pytest.mark.parametrize("n,b,B,seed", [(7, 16, 3, 1), (100, 4096, 20, 0), (257, 2, 2, 99), (33, 1 << 16, 4, 2**63 + 5)])
+def test_sym_tables_bit_exact(gpu_ctx, n, b, B, seed):
+    s = skb().SymTensorSketchSet(n, b, B, seed, gpu_ctx)
+    o = O.SymSet(n, b, B, seed)
+    hc, sc = s.coefficients()
+    for m in range(B):
+        b1, b2, b3, se = s.tables(m)
+        ob1, ob2, ob3, ose, ohc, osc = o.tables(m)
+        assert np.array_equal(b1, ob1) and np.array_equal(b2, ob2) and np.array_equal(b3, ob3)
+        assert np.array_equal(se, ose)
+        assert np.array_equal(hc[m], ohc) and np.array_equal(sc[m], osc)
+
+
+@pytest.mark.parametrize("n,b,B,seed", [(7, 16, 3, 1), (100, 4096, 20, 0), (50, 2, 2, 5)])
+def test_asym_tables_bit_exact(gpu_ctx, n, b, B, seed):
+    s = skb().AsymTensorSketchSet(n, b, B, seed, gpu_ctx)
+    o = O.AsymSet(n, b, B, seed)
+    hc, xc = s.coefficients()
+    for m in range(B):
+        bk, sg = s.tables(m)
+        obk, osg, ohc, oxc = o.tables(m)
+        assert np.array_equal(bk, obk) and np.array_equal(sg, osg)
+        assert np.array_equal(hc[m], ohc) and np.array_equal(xc[m], oxc)
+
+
+# ---------------------------------------------------------------- dense builds
+@pytest.mark.parametrize("n,b,B", [(12, 64, 3), (40, 1024, 5), (64, 4096, 20), (30, 16384, 4), (9, 2, 3), (1, 8, 2)])
+def test_sym_dense_build_matches_oracle(gpu_ctx, n, b, B):
+    T = sym_tensor(n, n + b)
+    s = skb().SymTensorSketchSet(n, b, B, 11, gpu_ctx)
+    o = O.SymSet(n, b, B, 11)
+    s.accumulate_dense(T, assume_symmetric=True)
+    o.accumulate_dense(T, assume_symmetric=True)
+    assert rel_per_replicate(s.data(), o.data()) <= SKETCH_TOL
+    assert s.version() == 1
+
+
+def test_sym_dense_build_is_deterministic(gpu_ctx):
+    T = sym_tensor(48, 3)
+    outs = []
+    for _ in range(2):
+        s = skb().SymTensorSketchSet(48, 2048, 6, 7, gpu_ctx)
+        s.accumulate_dense(T, assume_symmetric=True)
+        outs.append(s.data())
+    assert np.array_equal(outs[0], outs[1])
+
+
+def test_sym_dense_build_f32_input(gpu_ctx):
+    T = sym_tensor(36, 4).astype(np.float32)
+    s = skb().SymTensorSketchSet(36, 1 << 16, 3, 5, gpu_ctx)
+    o = O.SymSet(36, 1 << 16, 3, 5)
+    s.accumulate_dense(T, assume_symmetric=True)
+    o.accumulate_dense(T.astype(np.float64), assume_symmetric=True)
+    assert rel_per_replicate(s.data(), o.data()) <= SKETCH_TOL_F32
+
+
+def test_sym_dense_slices_sum_to_whole(gpu_ctx):
+    n = 30
+    T = sym_tensor(n, 8)
+    whole = skb().SymTensorSketchSet(n, 512, 4, 3, gpu_ctx)
+    whole.accumulate_dense(T, assume_symmetric=True)
+    parts = skb().SymTensorSketchSet(n, 512, 4, 3, gpu_ctx)
+    for i0, i1 in [(0, 5), (5, 17), (17, 30)]:
+        parts.accumulate_dense(T, assume_symmetric=True, i0=i0, i1=i1)
+    assert rel_per_replicate(parts.data(), whole.data()) <= 1e-12
+
+
+def test_sym_dense_device_tensor_and_accumulate(gpu_ctx):
+    import torch
+
+    n = 20
+    T = sym_tensor(n, 9)
+    s = skb().SymTensorSketchSet(n, 256, 3, 1, gpu_ctx)
+    o = O.SymSet(n, 256, 3, 1)
+    Td = torch.from_numpy(T).cuda()
+    s.accumulate_dense(Td, assume_symmetric=True)
+    s.accumulate_dense(Td, assume_symmetric=True)  # accumulates (+=)
+    o.accumulate_dense(T, True)
+    o.accumulate_dense(T, True)
+    assert rel_per_replicate(s.data(), o.data()) <= SKETCH_TOL
+
+
+def test_sym_dense_symmetry_check_message(gpu_ctx):
+    n = 6
+    T = sym_tensor(n, 1)
+    T[1, 3, 2] += 0.5
+    s = skb().SymTensorSketchSet(n, 64, 2, 1, gpu_ctx)
+    o = O.SymSet(n, 64, 2, 1)
+    with pytest.raises(ValueError) as e:
+        s.accumulate_dense(T)
+    with pytest.raises(O.OracleError) as eo:
+        o.accumulate_dense(T)
+    assert str(e.value) == str(eo.value)
+    assert s.version() == 0
+
+
+def test_sym_zero_and_single_entry(gpu_ctx):
+    n = 10
+    s = skb().SymTensorSketchSet(n, 128, 5, 3, gpu_ctx)
+    s.accumulate_dense(np.zeros((n, n, n)), assume_symmetric=True)
+    assert not np.any(s.data())
+    T = np.zeros((n, n, n))
+    for p in [(1, 2, 3), (1, 3, 2), (2, 1, 3), (2, 3, 1), (3, 1, 2), (3, 2, 1)]:
+        T[p] = 6.0
+    s.accumulate_dense(T, assume_symmetric=True)
+    assert s.recover_entry(1, 2, 3) == pytest.approx(6.0, abs=1e-12)
+    o = O.SymSet(n, 128, 5, 3)
+    o.accumulate_dense(T, True)
+    assert s.recover_entry(3, 1, 2) == o.recover_entry(3, 1, 2)
+
+
+def test_nonfinite_input_rejected(gpu_ctx):
+    n = 5
+    T = sym_tensor(n, 2)
+    T[0, 0, 0] = np.nan
+    s = skb().SymTensorSketchSet(n, 64, 2, 1, gpu_ctx)
+    with pytest.raises(ValueError):
+        s.accumulate_dense(T, assume_symmetric=True)
+
+
+@pytest.mark.parametrize("n,b,B", [(10, 64, 3), (24, 4096, 6), (16, 1 << 15, 2)])
+def test_asym_dense_build_matches_oracle(gpu_ctx, n, b, B):
+    T = np.random.default_rng(n).normal(size=(n, n, n))
+    s = skb().AsymTensorSketchSet(n, b, B, 17, gpu_ctx)
+    o = O.AsymSet(n, b, B, 17)
+    s.accumulate_dense(T)
+    o.accumulate_dense(T)
+    assert rel_per_replicate(s.data(), o.data()) <= SKETCH_TOL
+    for (i, j, k) in [(0, 1, 2), (n - 1, 0, n - 1)]:
+        assert s.recover_entry(i, j, k) == pytest.approx(o.recover_entry(i, j, k), abs=1e-12)
+
+
+# ---------------------------------------------------------------- spectra & contractions
+@pytest.mark.parametrize("n,b,B", [(12, 64, 3), (50, 4096, 8), (40, 16384, 4), (8, 2, 2), (9, 8, 3)])
+def test_sym_contractions_match_oracle(gpu_ctx, n, b, B):
+    T = sym_tensor(n, b + n)
+    s = skb().SymTensorSketchSet(n, b, B, 23, gpu_ctx)
+    o = O.SymSet(n, b, B, 23)
+    s.accumulate_dense(T, True)
+    o.accumulate_dense(T, True)
+    ws = skb().SymContractionWorkspace(s)
+    for m in range(B):
+        ref = o.cached_transform(m)
+        assert np.max(np.abs(ws.cached_transform(m) - ref)) <= 1e-12 * max(np.max(np.abs(ref)), 1e-300)
+    rng = np.random.default_rng(5)
+    U = rng.normal(size=(7, n))
+    U /= np.linalg.norm(U, axis=1, keepdims=True)
+    got = ws.Ivv(U)
+    for l in range(U.shape[0]):
+        assert vec_rel(got[l], o.ivv(U[l])) <= VEC_TOL
+    gv = ws.vvv(U)
+    for l in range(U.shape[0]):
+        ov = o.vvv(U[l])
+        assert abs(gv[l] - ov) <= VEC_TOL * max(abs(ov), np.max(np.abs(T)))
+
+
+def test_sym_golden_fixture(gpu_ctx):
+    g = json.loads((GOLDEN / "oracle_golden.json").read_text())["sym_small"]
+    n, b, B = g["n"], g["b"], g["B"]
+    s = skb().SymTensorSketchSet(n, b, B, g["seed"], gpu_ctx)
+    s.accumulate_dense(np.array(g["T"]).reshape(n, n, n))
+    ref = (np.array(g["data_re"]) + 1j * np.array(g["data_im"])).reshape(B, b)
+    assert rel_per_replicate(s.data(), ref) <= SKETCH_TOL
+    ws = skb().SymContractionWorkspace(s)
+    assert vec_rel(ws.Ivv(np.array(g["u"])), np.array(g["ivv"])) <= VEC_TOL
+    assert abs(ws.vvv(np.array(g["u"])) - g["vvv"]) <= 1e-9 * abs(g["vvv"])
+
+
+def test_cached_transform_refreshes_on_mutation(gpu_ctx):
+    n, b, B = 10, 256, 3
+    s = skb().SymTensorSketchSet(n, b, B, 1, gpu_ctx)
+    s.accumulate_dense(sym_tensor(n, 1), True)
+    ws = skb().SymContractionWorkspace(s)
+    f0 = ws.cached_transform(1)
+    d = s.data()
+    d[1] *= 2
+    s.set_data(None, d)
+    assert np.allclose(ws.cached_transform(1), 2 * f0, rtol=0, atol=1e-12 * np.max(np.abs(f0)))
+
+
+# ---------------------------------------------------------------- rank-1 / moment
+@pytest.mark.parametrize("n,b,B", [(9, 64, 3), (100, 4096, 20), (50, 16384, 4)])
+def test_add_scaled_rank1_matches_oracle(gpu_ctx, n, b, B):
+    T = sym_tensor(n, 2)
+    u = np.random.default_rng(3).normal(size=n)
+    s = skb().SymTensorSketchSet(n, b, B, 4, gpu_ctx)
+    o = O.SymSet(n, b, B, 4)
+    s.accumulate_dense(T, True)
+    o.accumulate_dense(T, True)
+    s.add_scaled_rank1(u, -1.75)
+    o.add_scaled_rank1(u, -1.75)
+    assert rel_per_replicate(s.data(), o.data()) <= SKETCH_TOL
+    v0 = s.version()
+    s.add_scaled_rank1(u, 0.0)  # alpha == 0 is a no-op (sketch.cpp:349)
+    assert s.version() == v0
+
+
+def test_moment_equals_sum_of_rank1(gpu_ctx):
+    n, b, B, N = 12, 512, 4, 37
+    rng = np.random.default_rng(8)
+    X = rng.normal(size=(N, n))
+    w = rng.uniform(size=N)
+    s = skb().SymTensorSketchSet(n, b, B, 9, gpu_ctx)
+    s.accumulate_moment(X, w)
+    o = O.SymSet(n, b, B, 9)
+    for i in range(N):
+        o.add_scaled_rank1(X[i], w[i])
+    assert rel_per_replicate(s.data(), o.data()) <= SKETCH_TOL
+    d = O.SymSet(n, b, B, 9)
+    d.accumulate_dense(np.einsum("s,si,sj,sk->ijk", w, X, X, X), True)
+    assert rel_per_replicate(s.data(), d.data()) <= 1e-9
+
+
+# ---------------------------------------------------------------- RTPM
+@pytest.mark.parametrize("n,b,B,k,L,T", [(20, 1024, 6, 3, 8, 10), (100, 4096, 20, 3, 12, 30)])
+def test_rtpm_matches_oracle(gpu_ctx, n, b, B, k, L, T):
+    Tn, lam_true, V_true = skb().gen_planted_tensor(n, k + 1, 0.01, 7)
+    s = skb().SymTensorSketchSet(n, b, B, 3, gpu_ctx)
+    o = O.SymSet(n, b, B, 3)
+    s.accumulate_dense(Tn, True)
+    o.accumulate_dense(Tn, True)
+    cfg = skb().PowerConfig(k=k, L=L, T_iters=T, b=b, B=B, seed=13)
+    d = skb().robust_tpm_fast(s, cfg)
+    lam_o, V_o, bt_o = o.rtpm(k, L, T, seed=13)
+    assert np.array_equal(d.best_tau, bt_o)
+    assert np.max(np.abs(d.lambda_ - lam_o) / np.abs(lam_o)) <= VEC_TOL
+    match = O.greedy_match(d.A, V_o)
+    assert np.all(match[:, 2] > 1 - 1e-12)
+    for r in range(k):
+        a, t = int(match[r, 0]), int(match[r, 1])
+        sgn = np.sign(d.A[:, a] @ V_o[:, t])
+        assert vec_rel(sgn * d.A[:, a], V_o[:, t]) <= VEC_TOL
+    # deflated sets agree too
+    assert rel_per_replicate(s.data(), o.data()) <= 1e-8
+
+
+def test_rtpm_validation(gpu_ctx):
+    s = skb().SymTensorSketchSet(4, 64, 2, 1, gpu_ctx)
+    with pytest.raises(ValueError, match="target rank exceeds"):
+        skb().robust_tpm_fast(s, skb().PowerConfig(k=5, L=2, T_iters=2))
+    with pytest.raises(ValueError, match="must be positive"):
+        skb().robust_tpm_fast(s, skb().PowerConfig(k=1, L=0, T_iters=2))
+
+
+def test_rtpm_degenerate_on_zero_sketch(gpu_ctx):
+    s = skb().SymTensorSketchSet(6, 64, 3, 1, gpu_ctx)
+    with pytest.raises(skb().DegenerateIterationError):
+        skb().robust_tpm_fast(s, skb().PowerConfig(k=1, L=2, T_iters=2))
+
+
+# ---------------------------------------------------------------- asymmetric contractions / factored
+@pytest.mark.parametrize("n,b,B", [(10, 64, 3), (40, 4096, 8), (24, 16384, 3)])
+def test_asym_contractions_match_oracle(gpu_ctx, n, b, B):
+    T = np.random.default_rng(b).normal(size=(n, n, n))
+    s = skb().AsymTensorSketchSet(n, b, B, 31, gpu_ctx)
+    o = O.AsymSet(n, b, B, 31)
+    s.accumulate_dense(T)
+    o.accumulate_dense(T)
+    ws = skb().AsymContractionWorkspace(s)
+    rng = np.random.default_rng(1)
+    X = rng.normal(size=(4, n))
+    Y = rng.normal(size=(4, n))
+    for fm in range(3):
+        got = ws.mode_contraction(fm, X, Y)
+        for l in range(4):
+            assert vec_rel(got[l], o.mode_contraction(fm, X[l], Y[l])) <= VEC_TOL
+    assert np.array_equal(ws.Ibc(X[0], X[0]), ws.Ivv(X[0]))
+    gv = ws.vvv(X)
+    for l in range(4):
+        ov = o.vvv(X[l])
+        assert abs(gv[l] - ov) <= VEC_TOL * max(abs(ov), 1.0)
+    with pytest.raises(ValueError, match="free_mode"):
+        ws.mode_contraction(3, X[0], Y[0])
+
+
+def test_asym_factored_rank1_match_oracle(gpu_ctx):
+    n, b, B, N = 8, 256, 3, 20
+    rng = np.random.default_rng(2)
+    a = rng.normal(size=N)
+    U, V, W = rng.normal(size=(3, N, n))
+    s = skb().AsymTensorSketchSet(n, b, B, 5, gpu_ctx)
+    o = O.AsymSet(n, b, B, 5)
+    s.accumulate_factored(a, U, V, W)
+    o.accumulate_factored(a, U, V, W)
+    assert rel_per_replicate(s.data(), o.data()) <= SKETCH_TOL
+    for m in range(B):
+        assert rel_per_replicate(s.rank1_sketch(m, U[0], V[0], W[0]), o.rank1_sketch(m, U[0], V[0], W[0])) <= SKETCH_TOL
+    s.add_rank1(0.5, U[1], V[1], W[1])
+    o.add_rank1(0.5, U[1], V[1], W[1])
+    assert rel_per_replicate(s.data(), o.data()) <= SKETCH_TOL
+
+
+def test_launches_are_counted(gpu_ctx):
+    before = skb().kernel_launch_count()
+    s = skb().SymTensorSketchSet(8, 64, 2, 1, gpu_ctx)
+    s.accumulate_dense(sym_tensor(8, 1), True)
+    assert skb().kernel_launch_count() > before

@@ -1,0 +1,94 @@
+"""CPU-only checks of the product library: it loads, exports every symbol the
+C-ABI header declares, and its host-side (bit-exact) helpers agree with the
+oracle. No device compute happens here."""
+import pathlib
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle_py as O
+
+ROOT = pathlib.Path(__file__).resolve().parents[1]
+HEADER = ROOT / "include" / "sketchcp_b200.h"
+
+
+def _declared():
+    txt = HEADER.read_text()
+    return sorted(set(re.findall(r"\b(skc_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1506_04448_b200 import _lib
+
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)], capture_output=True, text=True,
+                         check=True).stdout
+    exported = set(re.findall(r"\bT (skc_[a-z0-9_]+)", out))
+    missing = [s for s in _declared() if s not in exported]
+    assert not missing, missing
+    # and the ctypes table covers them all
+    assert set(_declared()) <= set(_lib.SIGNATURES)
+
+
+def test_library_is_sm100a():
+    from paper_1506_04448_b200 import _lib
+
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_derive_seed_matches_oracle():
+    import paper_1506_04448_b200 as skb
+
+    for args in [(0, 0x21, 0, 0), (42, 0x22, 5, 0), (2**63 + 17, 0x11, 3, 2), (7, 0x31, 9, 49)]:
+        assert skb.derive_seed(*args) == O.derive_seed(*args)
+
+
+def test_unit_sphere_and_power_inits_bit_exact():
+    import paper_1506_04448_b200 as skb
+
+    for seed in (1, 99, 2**40 + 3):
+        assert np.array_equal(skb.unit_sphere(seed, 37), O.unit_sphere(seed, 37))
+    inits = skb.power_inits(seed=5, n=11, k=3, L=4)
+    for c in range(3):
+        for t in range(4):
+            assert np.array_equal(inits[c, t], O.unit_sphere(O.derive_seed(5, 0x31, c, t), 11))
+
+
+def test_poly_coefficients_and_eval_bit_exact():
+    import ctypes as C
+
+    from paper_1506_04448_b200 import _lib
+
+    for k, b, seed in [(6, 1024, 42), (2, 16, 7), (6, 4, 1234)]:
+        out = np.empty(k, dtype=np.uint64)
+        _lib.check(_lib.lib.skc_poly_coefficients(k, seed, out.ctypes.data_as(C.POINTER(C.c_uint64))))
+        assert np.array_equal(out, O.polyhash_from_seed(k, b, seed))
+        for i in range(50):
+            v = _lib.lib.skc_poly_eval(out.ctypes.data_as(C.POINTER(C.c_uint64)), k, b, i)
+            assert v == O.polyhash_eval(out, b, [i])[0]
+
+
+def test_planted_generator_deterministic_and_symmetric():
+    import paper_1506_04448_b200 as skb
+
+    T1, lam1, V1 = skb.gen_planted_tensor(9, 3, 0.01, 7)
+    T2, lam2, V2 = skb.gen_planted_tensor(9, 3, 0.01, 7)
+    assert np.array_equal(T1, T2) and np.array_equal(lam1, lam2)
+    assert np.all((lam1 >= 1) & (lam1 <= 2))
+    assert np.allclose(V1.T @ V1, np.eye(3), atol=1e-12)
+    for p in [(0, 2, 1), (1, 0, 2), (2, 1, 0)]:
+        assert np.array_equal(T1, T1.transpose(p))
+    assert O.lib().orc_first_asymmetric_triple(O.dp(T1), 9, 0.0, (O.C.c_int * 3)()) == 0
+
+
+def test_no_gpu_means_loud_failure():
+    """Without a device the library must fail (no silent CPU fallback)."""
+    import paper_1506_04448_b200 as skb
+
+    if skb.device_count() > 0:
+        pytest.skip("a GPU is visible")
+    with pytest.raises(skb.CudaError):
+        skb.Context(0)
