@@ -1,0 +1,338 @@
+#!/usr/bin/env python
+"""Benchmark of the FFT tensor-sketch hot path (BASELINE.json metric:
+"tensor-sketch build entries/s (HBM GB/s) and sketched T(I,u,u) contractions/s").
+
+Workload (N=1 and every N): BASELINE config 1 — dense symmetric n=400 fp64 tensor,
+rank-50 planted + 0.01 mirrored Gaussian noise (host generator, seeded), symmetric
+sketch b=2^14, B=20. One step = one full sketch build of the tensor (sorted
+triples, sketch.cpp:315-345) resident in HBM; with N ranks the i-slices are split
+by equal work and the B x b sketches are summed with an NCCL all-reduce (strong
+scaling). `value` = n^3 logical entries per second for the whole job. The
+sketched-contraction throughput (batched T(I,u,u), L=100 restarts, the RTPM power
+step) is reported beside it.
+
+--impl reference times the reference algorithm's CPU implementation (the oracle
+restatement, oracle/; the reference itself cannot be built here) on the host
+cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "tensor-sketch build entries/s (HBM GB/s) and sketched T(I,u,u) contractions/s"
+CFG = dict(n=400, rank=50, sigma=0.01, b=1 << 14, B=20, seed=20150615, L=100)
+
+
+def simplex_entries(n, i0=0, i1=None):
+    i1 = n if i1 is None else i1
+    return sum((n - i) * (n - i + 1) // 2 for i in range(i0, i1))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if len(r) > 3 + k and r[3 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def traffic_from_profiles(kernel):
+    p = ROOT / "profiles" / "traffic.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        e = d.get(kernel)
+        if e and e.get("config") == "config1":
+            return e.get("dram_bytes_per_launch")
+    return None
+
+
+def oracle_build_seconds(T, reps):
+    """Oracle (CPU restatement) sym build of the whole tensor with all host threads."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_py as O
+
+    O.lib().orc_set_num_threads(os.cpu_count() or 1)
+    times = []
+    for _ in range(reps):
+        s = O.SymSet(CFG["n"], CFG["b"], CFG["B"], CFG["seed"])
+        t0 = time.perf_counter()
+        s.accumulate_dense(T, assume_symmetric=True)
+        times.append(time.perf_counter() - t0)
+    return times, O.lib().orc_num_threads()
+
+
+def make_tensor():
+    import paper_1506_04448_b200 as skb
+
+    T, lam, V = skb.gen_planted_tensor(CFG["n"], CFG["rank"], CFG["sigma"], CFG["seed"])
+    return T
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    T = make_tensor()
+    n = CFG["n"]
+    warm, _ = oracle_build_seconds(T, max(args.warmup, 0))
+    times, threads = oracle_build_seconds(T, args.steps)
+    tot = sum(times)
+    val = n ** 3 * args.steps / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "entries/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(args.gpus),
+        "cpu_baseline": {"value": val, "unit": "entries/s", "cores": threads, "kind": "port",
+                         "sample": "full config-1 build (n=400, b=2^14, B=20) per step, oracle restatement "
+                                   "of sketch.cpp:315-345 (reference not buildable: no Eigen3/FFTW3)"},
+        "e2e": {"value": val, "unit": "entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def config_dict(world):
+    return {"workload": "config1: dense symmetric n=400 fp64 tensor (rank-50 planted, sigma=0.01), "
+                        "sym sketch b=2^14 B=20; contractions: batched T(I,u,u) over L=100 restarts",
+            "n": CFG["n"], "rank": CFG["rank"], "sigma": CFG["sigma"], "b": CFG["b"], "B": CFG["B"],
+            "seed": CFG["seed"], "L": CFG["L"],
+            "l2": "flushed (256 MiB write) before every timed step",
+            "parallelism": f"i-slices x{world} + NCCL all-reduce" if world > 1 else "single GPU"}
+
+
+def run_b200(args):
+    import torch
+
+    import paper_1506_04448_b200 as skb
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    n, b, B = CFG["n"], CFG["b"], CFG["B"]
+    ctx = skb.Context(local)
+    ext = torch.cuda.ExternalStream(ctx.stream())
+    T_host = make_tensor()
+    T_pinned = torch.from_numpy(T_host).pin_memory()
+    T_dev = T_pinned.to(f"cuda:{local}")
+    from paper_1506_04448_b200.distributed import equal_work_slices
+
+    i0, i1 = equal_work_slices(n, world)[rank]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+    sset = skb.SymTensorSketchSet(n, b, B, CFG["seed"], ctx)
+    dptr, dbytes = sset.data_device()
+
+    class _CAI:  # zero-copy torch view of the set's device data for the collective
+        __cuda_array_interface__ = {"shape": (dbytes // 8,), "typestr": "<f8", "data": (dptr, False), "version": 3}
+
+    data_view = torch.as_tensor(_CAI(), device=f"cuda:{local}")
+
+    def step(T, host=False):
+        if world > 1 and rank != 0:
+            with torch.cuda.stream(ext):
+                data_view.zero_()  # prior sketch counted once by the all-reduce
+        sset.accumulate_dense(T, assume_symmetric=True, i0=i0, i1=i1)
+        if world > 1:
+            with torch.cuda.stream(ext):
+                dist.all_reduce(data_view)
+            sset.bump_version()
+        if host:
+            return sset.data()
+        return None
+
+    for _ in range(max(args.warmup, 3)):
+        step(T_dev)
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed region -------------------------------------------------
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ctx.profile(True)
+    ctx.profile_reset()
+    launches0 = skb.kernel_launch_count()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.fill_(k & 0xFF)
+            torch.cuda.synchronize()
+            ev[k][0].record(ext)
+            step(T_dev)
+            ev[k][1].record(ext)
+        torch.cuda.synchronize()
+    launches = skb.kernel_launch_count() - launches0
+    if dist:
+        dist.barrier()
+    ms = sum(a.elapsed_time(e) for a, e in ev)
+    main_ms, main_cnt = ctx.profile_get("build_main")
+    pre_ms, _ = ctx.profile_get("build_prepass")
+    fin_ms, _ = ctx.profile_get("build_finalize")
+    ctx.profile(False)
+    if dist:
+        t = torch.tensor([ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = n ** 3 / (ms_step * 1e-3)
+    simplex_bytes_job = simplex_entries(n) * 8
+    simplex_bytes_rank = simplex_entries(n, i0, i1) * 8
+
+    # ---- end-to-end through the public API: pinned host tensor in, sketch out ----------
+    T_np_pinned = T_pinned.numpy()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e2e_ev = []
+    for k in range(max(1, min(args.steps, 5))):
+        a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(ext)
+        step(T_np_pinned, host=True)
+        e.record(ext)
+        e2e_ev.append((a, e))
+    torch.cuda.synchronize()
+    e2e_ms = sum(a.elapsed_time(e) for a, e in e2e_ev) / len(e2e_ev)
+    if dist:
+        t = torch.tensor([e2e_ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    # ---- sketched contractions: batched T(I,u,u) power step over L restarts -----------
+    L = CFG["L"]
+    ws = skb.SymContractionWorkspace(sset)
+    U = skb.power_inits(1, n, 1, L)[0]
+    for _ in range(2):
+        ws.Ivv(U)
+    ctx.profile(True)
+    ctx.profile_reset()
+    reps = 10
+    for _ in range(reps):
+        ws.Ivv(U)
+    c_ms, _ = ctx.profile_get("sym_contract")
+    m_ms, _ = ctx.profile_get("median")
+    ctx.profile(False)
+    contr_per_s = L * reps / ((c_ms + m_ms) * 1e-3) if (c_ms + m_ms) > 0 else None
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_src = peaks()
+    achieved = simplex_bytes_rank / (main_ms / main_cnt * 1e-3) / 1e9 if main_cnt else None
+    clocks = clk.summary()
+    line = {
+        "metric": METRIC, "value": value, "unit": "entries/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded host generator, BASELINE config 1 shape)",
+        "config": config_dict(world),
+        "hbm_gbs_algorithmic": simplex_bytes_job / (ms_step * 1e-3) / 1e9,
+        "contractions_per_s": contr_per_s,
+        "contraction_step_ms": (c_ms + m_ms) / reps,
+        "e2e": {"value": n ** 3 / (e2e_ms * 1e-3), "unit": "entries/s",
+                # pinned input: the quantize pass reads the sorted-triple rows in place over the bus
+                "h2d_bytes_per_step": int(simplex_bytes_job), "d2h_bytes_per_step": int(B * b * 16),
+                "ms_per_step": e2e_ms,
+                "path": "accumulate_dense(pinned host tensor) + replicate data readback (public API)"},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "kernel": "k_build_main",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None,
+                     "traffic": traffic_from_profiles("k_build_main"),
+                     "algorithmic_bytes_per_launch": simplex_bytes_rank,
+                     "kernel_ms_per_launch": main_ms / main_cnt if main_cnt else None,
+                     "prepass_ms_per_launch": pre_ms / main_cnt if main_cnt else None,
+                     "finalize_ms_per_launch": fin_ms / main_cnt if main_cnt else None,
+                     "scatter_adds_per_s": (simplex_entries(n, i0, i1) * B) / (main_ms / main_cnt * 1e-3) if main_cnt else None,
+                     "peak_source": peak_src},
+        "clocks": clocks,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        times, threads = oracle_build_seconds(T_host, 2)
+        best = min(times)
+        line["cpu_baseline"] = {"value": n ** 3 / best, "unit": "entries/s", "cores": threads, "kind": "port",
+                                "sample": "full config-1 build (n=400, b=2^14, B=20), best of 2, oracle restatement"}
+    print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

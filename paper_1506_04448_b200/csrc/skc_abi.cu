@@ -114,13 +114,15 @@ struct skc_context {
     // dense-build row tables keyed by (n, i0, i1, sym)
     struct RowTab {
         DevBuf<std::uint32_t> rows;
+        DevBuf<long long> offs;  // packed-stream offset of each row (= cum[row])
         std::vector<long long> cum;  // cumulative entries per row (host)
         int nrows = 0;
     };
     std::map<std::tuple<int, int, int, bool>, std::unique_ptr<RowTab>> rowtabs;
     // scratch
     DevBuf<unsigned char> tensor_stage;
-    DevBuf<long long> build_partials;
+    DevBuf<long long> build_partials, qbuf;
+    DevBuf<short> rowF;
     DevBuf<double> prepass;
     DevBuf<int> ints;  // [0] scale exp, [1] nonfinite, [2] best tau, [3..] misc
     DevBuf<double> dbl;  // [0] best value
@@ -139,6 +141,9 @@ struct skc_context {
     std::vector<ProfRec> prof;
 
     void use() const { CK(cudaSetDevice(device)); }
+    // w_N^k tables for the CTA-local transforms (contiguous; the full-b table would be
+    // read at stride S)
+    const double2* twl(int N) { return tw(static_cast<std::uint32_t>(N)); }
     const double2* tw(std::uint32_t b) {
         auto it = twiddles.find(b);
         if (it != twiddles.end()) return it->second->p;
@@ -164,6 +169,7 @@ struct skc_context {
             }
         rt->nrows = static_cast<int>(rows.size());
         rt->rows.upload(rows.data(), rows.size(), stream);
+        rt->offs.upload(rt->cum.data(), rows.size(), stream);
         CK(cudaStreamSynchronize(stream));
         RowTab& ref = *rt;
         rowtabs[key] = std::move(rt);
@@ -207,6 +213,7 @@ struct skc_sym_set {
     std::vector<std::uint64_t> hcoef, scoef;  // B x 6 each
     DevBuf<std::uint64_t> d_hcoef, d_scoef;
     DevBuf<std::uint32_t> bucket1, bucket2, bucket3, packed, perm1, perm2;
+    DevBuf<uint2> plan1, plan2;
     DevBuf<std::uint8_t> sexp;
     DevBuf<double2> data, spec;
     int N = 2, logN = 1, S = 1;
@@ -225,11 +232,12 @@ struct skc_sym_set {
         v.sexp = sexp.p;
         v.packed = packed.p;
         v.tw = ctx->tw(b);
+        v.twl = ctx->twl(N);
         v.N = N;
         v.logN = logN;
         v.S = S;
-        v.perm1 = perm1.p;
-        v.perm2 = perm2.p;
+        v.plan1 = plan1.p;
+        v.plan2 = plan2.p;
         v.data = data.p;
         v.spec = spec.p;
         return v;
@@ -238,7 +246,7 @@ struct skc_sym_set {
     void ensure_fresh() {
         if (spec_valid && spec_version == version) return;
         SKC_PROF(ctx, "spectrum");
-        launch_spectrum(ctx->stream, data.p, b, logb, B, N, logN, S, ctx->tw(b), spec.p);
+        launch_spectrum(ctx->stream, data.p, b, logb, B, N, logN, S, ctx->tw(b), ctx->twl(N), spec.p);
         ctx->check_launch();
         spec_version = version;
         spec_valid = true;
@@ -256,6 +264,7 @@ struct skc_asym_set {
     std::vector<std::uint64_t> hcoef, xcoef;  // B x 3 x 2, B x 3 x 6
     DevBuf<std::uint64_t> d_hcoef, d_xcoef;
     DevBuf<std::uint32_t> bucket, packed, perm;
+    DevBuf<uint2> plan;
     DevBuf<double> sign;
     DevBuf<double2> data, spec;
     int N = 2, logN = 1, S = 1;
@@ -272,10 +281,11 @@ struct skc_asym_set {
         v.sign = sign.p;
         v.packed = packed.p;
         v.tw = ctx->tw(b);
+        v.twl = ctx->twl(N);
         v.N = N;
         v.logN = logN;
         v.S = S;
-        v.perm = perm.p;
+        v.plan = plan.p;
         v.data = data.p;
         v.spec = spec.p;
         return v;
@@ -283,7 +293,7 @@ struct skc_asym_set {
     void ensure_fresh() {
         if (spec_valid && spec_version == version) return;
         SKC_PROF(ctx, "spectrum");
-        launch_spectrum(ctx->stream, data.p, b, logb, B, N, logN, S, ctx->tw(b), spec.p);
+        launch_spectrum(ctx->stream, data.p, b, logb, B, N, logN, S, ctx->tw(b), ctx->twl(N), spec.p);
         ctx->check_launch();
         spec_version = version;
         spec_valid = true;
@@ -327,6 +337,10 @@ void init_sym_device(skc_sym_set* s, const double* data_host) {
     s->logb = ilog2(s->b);
     launch_sort_perm(st, s->bucket1.p, s->B, s->n, static_cast<std::uint32_t>(s->N - 1), s->perm1.p);
     launch_sort_perm(st, s->bucket2.p, s->B, s->n, static_cast<std::uint32_t>(s->N - 1), s->perm2.p);
+    s->plan1.alloc(Bn);
+    s->plan2.alloc(Bn);
+    launch_make_plan(st, s->perm1.p, s->bucket1.p, s->sexp.p, 1, nullptr, s->B, s->n, s->plan1.p);
+    launch_make_plan(st, s->perm2.p, s->bucket2.p, s->sexp.p, 2, nullptr, s->B, s->n, s->plan2.p);
     ctx->check_launch();
     const size_t Bb = static_cast<size_t>(s->B) * s->b;
     s->data.alloc(Bb);
@@ -357,6 +371,8 @@ void init_asym_device(skc_asym_set* s, const double* data_host) {
     s->S = static_cast<int>(s->b / static_cast<std::uint32_t>(s->N));
     s->logb = ilog2(s->b);
     launch_sort_perm(st, s->bucket.p, s->B * 3, s->n, static_cast<std::uint32_t>(s->N - 1), s->perm.p);
+    s->plan.alloc(B3n);
+    launch_make_plan(st, s->perm.p, s->bucket.p, nullptr, 0, s->packed.p, s->B * 3, s->n, s->plan.p);
     ctx->check_launch();
     const size_t Bb = static_cast<size_t>(s->B) * s->b;
     s->data.alloc(Bb);
@@ -370,12 +386,43 @@ void init_asym_device(skc_asym_set* s, const double* data_host) {
 }
 
 // ---- dense build orchestration ------------------------------------------------------
-const void* stage_tensor(skc_context* ctx, const void* T, int n, int dtype, int location) {
+// Device-visible view of the input tensor. Device pointers are used as is. Pinned
+// (page-locked, UVA-mapped) host memory is read in place by the quantize pass, so only
+// the bytes the build reads cross the bus. Pageable host memory is staged, copying only
+// the row blocks the build reads (sym: T[i][i:n][:], asym: T[i0:i1]) unless the full
+// tensor is needed by the symmetry check.
+const void* stage_tensor(skc_context* ctx, const void* T, int n, int dtype, int location, bool sym, int i0, int i1,
+                         bool need_full, size_t* h2d_bytes) {
+    if (h2d_bytes) *h2d_bytes = 0;
     if (location == SKC_DEVICE) return T;
-    const size_t bytes = static_cast<size_t>(n) * n * n * (dtype == SKC_F64 ? 8 : 4);
-    ctx->tensor_stage.alloc(bytes);
-    CK(cudaMemcpyAsync(ctx->tensor_stage.p, T, bytes, cudaMemcpyHostToDevice, ctx->stream));
-    return ctx->tensor_stage.p;
+    const size_t es = dtype == SKC_F64 ? 8 : 4;
+    const size_t n2 = static_cast<size_t>(n) * n;
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, T) == cudaSuccess && attr.type == cudaMemoryTypeHost &&
+        attr.devicePointer != nullptr) {
+        return attr.devicePointer;
+    }
+    cudaGetLastError();  // clear a failed attribute query on pageable memory
+    ctx->tensor_stage.alloc(n2 * n * es);
+    unsigned char* dst = ctx->tensor_stage.p;
+    const unsigned char* src = static_cast<const unsigned char*>(T);
+    size_t moved = 0;
+    if (need_full) {
+        CK(cudaMemcpyAsync(dst, src, n2 * n * es, cudaMemcpyHostToDevice, ctx->stream));
+        moved = n2 * n * es;
+    } else if (sym) {
+        for (int i = i0; i < i1; ++i) {
+            const size_t off = (static_cast<size_t>(i) * n + i) * n * es, len = static_cast<size_t>(n - i) * n * es;
+            CK(cudaMemcpyAsync(dst + off, src + off, len, cudaMemcpyHostToDevice, ctx->stream));
+            moved += len;
+        }
+    } else {
+        const size_t off = static_cast<size_t>(i0) * n2 * es, len = static_cast<size_t>(i1 - i0) * n2 * es;
+        CK(cudaMemcpyAsync(dst + off, src + off, len, cudaMemcpyHostToDevice, ctx->stream));
+        moved = len;
+    }
+    if (h2d_bytes) *h2d_bytes = moved;
+    return dst;
 }
 
 void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool sym, int i0, int i1, int B,
@@ -384,12 +431,30 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
     skc_context::RowTab& rt = ctx->rowtab(n, i0, i1, sym);
     if (rt.nrows == 0) return;
     const long long total_slots = static_cast<long long>(B) * (sym ? 2ll * b : static_cast<long long>(b));
-    const long long cap = std::max<long long>(1024, (ctx->smem_optin - 1024) / 8);
-    int G = static_cast<int>((total_slots + cap - 1) / cap);
+    // slots per CTA limited by shared memory (limbs + per-replicate hash tables)
+    int G = 1;
+    for (;; ++G) {
+        long long spc = ((total_slots + G - 1) / G + 31) / 32 * 32;
+        const long long spr0 = sym ? 2ll * b : static_cast<long long>(b);
+        int Rg = 1;
+        for (int g = 0; g < G; ++g) {
+            const long long lo = g * spc, hi = std::min(lo + spc, total_slots);
+            if (hi > lo) Rg = std::max(Rg, static_cast<int>((hi - 1) / spr0 - lo / spr0 + 1));
+        }
+        if (Rg <= 16 && build_smem_bytes(spc, Rg, n) <= static_cast<size_t>(ctx->smem_optin - 1024)) break;
+        if (G > 4096) fail(kInvalidArgument, "accumulate_dense: sketch set too large for the dense build");
+    }
     int C = std::max(1, ctx->sms / G);
     C = std::min(C, rt.nrows);
     long long spc = (total_slots + G - 1) / G;
     spc = (spc + 31) / 32 * 32;
+    const long long spr = sym ? 2ll * b : static_cast<long long>(b);
+    int R = 1;
+    for (int g = 0; g < G; ++g) {
+        const long long lo = g * spc, hi = std::min(lo + spc, total_slots);
+        if (hi > lo) R = std::max(R, static_cast<int>((hi - 1) / spr - lo / spr + 1));
+    }
+    require(R <= 16, "accumulate_dense: slot range spans too many replicates");
     // chunk boundaries balanced by entry count
     std::vector<int> cb(C + 1, 0);
     const long long tot = rt.cum.back();
@@ -401,6 +466,8 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
     cb[C] = rt.nrows;
     ctx->chunk_begin.upload(cb.data(), cb.size(), ctx->stream);
     ctx->build_partials.alloc(static_cast<size_t>(C) * total_slots);
+    ctx->qbuf.alloc(static_cast<size_t>(std::max<long long>(1, tot)));
+    ctx->rowF.alloc(static_cast<size_t>(rt.nrows));
     ctx->prepass.alloc(kPrepassBlocks);
     ctx->ints.alloc(16);
 
@@ -415,10 +482,13 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
     p.G = G;
     p.total_slots = total_slots;
     p.slots_per_cta = static_cast<int>(spc);
-    p.threads = 1024;
+    p.R = R;
     p.bmask = b - 1;
     p.B = B;
     p.packed = packed;
+    p.rowoff = rt.offs.p;
+    p.qbuf = ctx->qbuf.p;
+    p.rowF = ctx->rowF.p;
     p.prepass_partials = ctx->prepass.p;
     p.scale_exp = ctx->ints.p;
     p.nonfinite = ctx->ints.p + 1;
@@ -693,7 +763,7 @@ int skc_sym_accumulate_dense(skc_sym_set* s, const void* T, int dtype, int locat
         require(s->n <= 65535, "accumulate_dense: n above 65535 is not supported");
         skc_context* ctx = s->ctx;
         ctx->use();
-        const void* Td = stage_tensor(ctx, T, s->n, dtype, location);
+        const void* Td = stage_tensor(ctx, T, s->n, dtype, location, true, i0, i1, !assume_symmetric, nullptr);
         if (!assume_symmetric) {
             ctx->asym_key.alloc(1);
             unsigned long long init = ~0ull;
@@ -741,7 +811,7 @@ static void sym_moment_device(skc_sym_set* s, const double* Xd, const double* wd
     {
         SKC_PROF(ctx, "freq_inverse");
         launch_freq_reduce_inverse(ctx->stream, ctx->freq_acc.p, chunks, s->B, s->S, s->N, s->logN, s->b, s->logb,
-                                   v.tw, ctx->tmp.p);
+                                   v.twl, ctx->tmp.p);
     }
     ctx->check_launch();
     {
@@ -1149,7 +1219,7 @@ int skc_asym_accumulate_dense(skc_asym_set* s, const void* T, int dtype, int loc
         require(s->n <= 65535, "accumulate_dense: n above 65535 is not supported");
         skc_context* ctx = s->ctx;
         ctx->use();
-        const void* Td = stage_tensor(ctx, T, s->n, dtype, location);
+        const void* Td = stage_tensor(ctx, T, s->n, dtype, location, false, i0, i1, false, nullptr);
         s->version++;  // sketch.cpp:175
         run_dense_build(ctx, Td, s->n, dtype, false, i0, i1, s->B, s->b, s->packed.p, s->data.p);
         ctx->sync();
@@ -1170,7 +1240,7 @@ static void asym_factored_device(skc_asym_set* s, const double* ad, const double
     ctx->check_launch();
     // reduce into tmp slot of replicate (m_only or all)
     double2* tmp = ctx->tmp.p;
-    launch_freq_reduce_inverse(ctx->stream, ctx->freq_acc.p, chunks, Bm, s->S, s->N, s->logN, s->b, s->logb, v.tw,
+    launch_freq_reduce_inverse(ctx->stream, ctx->freq_acc.p, chunks, Bm, s->S, s->N, s->logN, s->b, s->logb, v.twl,
                                tmp);
     ctx->check_launch();
     // combine: for m_only the tmp holds one replicate at index 0

@@ -22,10 +22,11 @@ struct SymView {
     const std::uint8_t* sexp;
     const std::uint32_t* packed;  // h | e << 30
     const double2* tw;            // w_b^k, k in [0, b)
+    const double2* twl;           // w_N^k, k in [0, N) (local transforms)
     // residue split
     int N, logN, S;
-    const std::uint32_t* perm1;  // B x n: indices sorted by (bucket1 mod N, i)
-    const std::uint32_t* perm2;  // B x n: sorted by (bucket2 mod N, i)
+    const uint2* plan1;  // B x n: (i, h_i | e_i << 28) sorted by (h_i mod N, i)
+    const uint2* plan2;  // B x n: (i, 2h_i mod b | 2e_i << 28) sorted by (2h_i mod N, i)
     const double2* data;         // B x b time domain
     const double2* spec;         // B x S x N local bit-reversed spectra
 };
@@ -39,8 +40,9 @@ struct AsymView {
     const double* sign;           // B x 3 x n (+-1)
     const std::uint32_t* packed;  // B x 3 x n: h | neg << 31
     const double2* tw;
+    const double2* twl;
     int N, logN, S;
-    const std::uint32_t* perm;  // B x 3 x n sorted by (bucket mod N, i)
+    const uint2* plan;  // B x 3 x n: (i, h_s(i) | neg << 31) sorted by (h_s(i) mod N, i)
     const double2* data;
     const double2* spec;
 };
@@ -59,36 +61,43 @@ void launch_asym_tables(cudaStream_t st, const std::uint64_t* hcoef, const std::
 // keys: nrep x n table; perm[rep][rank] = i sorted by (keys & mask, i)
 void launch_sort_perm(cudaStream_t st, const std::uint32_t* keys, int nrep, int n, std::uint32_t mask,
                       std::uint32_t* perm);
+// plan[q] = (i, bucket_i | ((sexp_i * sexp_mult) & 3) << 28 | sign bit of packed_i) for i = perm[q]
+void launch_make_plan(cudaStream_t st, const std::uint32_t* perm, const std::uint32_t* bucket, const std::uint8_t* sexp,
+                      int sexp_mult, const std::uint32_t* packed, int nrep, int n, uint2* plan);
 
-// dense build
+// dense build (skc_build.cu)
 struct BuildPlan {
     int n;
     bool sym;
     int dtype;  // 0 f64, 1 f32
-    const std::uint32_t* rowtab;
+    const std::uint32_t* rowtab;  // packed (i << 16 | j) rows of the stream
     int nrows;
-    const int* chunk_begin;  // C+1, device
-    int C, G;
-    long long total_slots;
+    const int* chunk_begin;  // C+1 row boundaries, device
+    int C, G;                // row chunks x contiguous slot ranges
+    long long total_slots;   // B x 2b (sym) or B x b (asym)
     int slots_per_cta;
-    int threads;
+    int R;                   // max replicates a slot range overlaps
     std::uint32_t bmask;
     int B;
-    const std::uint32_t* packed;
-    double* prepass_partials;  // kPrepassBlocks
-    int* scale_exp;            // device int
-    int* nonfinite;            // device int
-    long long* partials;       // C x total_slots
-    double* data_as_double;    // B x b x 2
+    const std::uint32_t* packed;  // sym: B x n (h | e << 30); asym: B x 3 x n (h | neg << 31)
+    const long long* rowoff;      // packed-stream offset of each row
+    long long* qbuf;              // packed fixed-point stream (quantize pass)
+    short* rowF;                  // per-row exponent of qbuf
+    double* prepass_partials;     // kPrepassBlocks
+    int* scale_exp;               // device int
+    int* nonfinite;               // device int
+    long long* partials;          // C x total_slots
+    double* data_as_double;       // B x b x 2
 };
 constexpr int kPrepassBlocks = 1024;
+size_t build_smem_bytes(long long slots_per_cta, int R, int n);
 void launch_build_prepass(cudaStream_t st, const void* T, const BuildPlan& p);
 void launch_build_main(cudaStream_t st, const void* T, const BuildPlan& p);
 void launch_build_finalize(cudaStream_t st, const BuildPlan& p);
 
 // spectra: spec[m][r][j] = local DIF of residue r of data[m]
 void launch_spectrum(cudaStream_t st, const double2* data, std::uint32_t b, int logb, int B, int N, int logN,
-                     int S, const double2* tw, double2* spec);
+                     int S, const double2* tw, const double2* twl, double2* spec);
 
 // symmetric contractions. mode 0: Ivv partials (L x B x S x n); mode 1: vvv
 // partials (L x B x S x 3: acc1, acc2, term3).
@@ -109,7 +118,7 @@ void launch_argmax_first(cudaStream_t st, const double* values, int L, int* best
 void launch_sym_moment_accumulate(cudaStream_t st, const SymView& v, const double* X, const double* w,
                                   double wscale, long long Nsamp, int chunks, double* acc);
 void launch_freq_reduce_inverse(cudaStream_t st, const double* acc, int chunks, int B, int S, int N, int logN,
-                                std::uint32_t b, int logb, const double2* tw, double2* tmp);
+                                std::uint32_t b, int logb, const double2* twl, double2* tmp);
 void launch_combine_residues(cudaStream_t st, const double2* tmp, int B, int S, int N, std::uint32_t b,
                              const double2* tw, double alpha, int m_only, bool overwrite, double2* dst);
 void launch_asym_factored_accumulate(cudaStream_t st, const AsymView& v, const double* a, const double* U,

@@ -136,277 +136,87 @@ void launch_sort_perm(cudaStream_t st, const std::uint32_t* keys, int nrep, int 
     SKC_LAUNCHED();
 }
 
-// ============================ K1: dense build ====================================
-// Symmetric: sketch.cpp:315-345 — sorted triples i<=j<=k, weight kappa 1/3/6,
-// bucket (h_i+h_j+h_k) mod b, sign root4(e_i+e_j+e_k). Asymmetric: sketch.cpp:173-193.
-//
-// Exact fixed point: every contribution q = round(kappa*T*2^F) is an int64 and is
-// added into shared-memory (lo, hi) 32-bit limbs with two native ATOMS.ADD plus a
-// carry taken from the returned old lo value. Integer addition is associative, so
-// the build is bit-deterministic under any schedule; F is chosen from the L1 mass
-// of the stream so that no bucket can overflow (|sum q| < 2^62).
-
-template <typename TT, bool SYM>
-__global__ void __launch_bounds__(256) k_build_prepass(const TT* __restrict__ T, int n,
-                                                      const std::uint32_t* __restrict__ rowtab, int nrows,
-                                                      double* __restrict__ partials, int* __restrict__ nonfinite) {
-    __shared__ double red[8];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double acc = 0.0;
-    bool bad = false;
-    for (int row = blockIdx.x * 8 + warp; row < nrows; row += gridDim.x * 8) {
-        const std::uint32_t ij = rowtab[row];
-        const int i = static_cast<int>(ij >> 16), j = static_cast<int>(ij & 0xFFFFu);
-        const TT* rp = T + ((size_t)i * n + j) * n;
-        const int k0 = SYM ? j : 0;
-        for (int k = k0 + lane; k < n; k += 32) {
-            const double v = static_cast<double>(rp[k]);
-            double kap = 1.0;
-            if (SYM) kap = (i == j && j == k) ? 1.0 : ((i == j || j == k) ? 3.0 : 6.0);
-            acc += kap * fabs(v);
-            bad |= !isfinite(v);
-        }
-    }
-    if (bad) atomicOr(nonfinite, 1);
-    double s = block_sum<256>(acc, red);
-    if (threadIdx.x == 0) partials[blockIdx.x] = s;
-}
-
-__global__ void k_build_scale(const double* __restrict__ partials, int np, int* __restrict__ scale_exp) {
-    __shared__ double red[8];
-    double acc = 0.0;
-    for (int i = threadIdx.x; i < np; i += 256) acc += partials[i];
-    double s = block_sum<256>(acc, red);
-    if (threadIdx.x == 0) {
-        int F = 0;
-        if (s > 0.0 && isfinite(s)) {
-            int ex;
-            frexp(s, &ex);  // s <= 2^ex
-            F = 61 - ex;
-            F = F > 1000 ? 1000 : (F < -1000 ? -1000 : F);
-        }
-        *scale_exp = F;
-    }
-}
-
-__device__ __forceinline__ void add64(std::uint32_t* lo, std::uint32_t* hi, int s, long long q) {
-    const std::uint32_t ql = static_cast<std::uint32_t>(q);
-    const std::uint32_t qh = static_cast<std::uint32_t>(static_cast<unsigned long long>(q) >> 32);
-    const std::uint32_t old = atomicAdd(lo + s, ql);
-    const std::uint32_t carry = (old + ql) < old ? 1u : 0u;
-    atomicAdd(hi + s, qh + carry);
-}
-
-constexpr int kBuildThreads = 1024;
-constexpr int kBuildMR = 4;  // replicates handled per row pass
-
-template <typename TT, bool SYM>
-__global__ void __launch_bounds__(kBuildThreads, 1)
-    k_build_main(const TT* __restrict__ T, int n, const std::uint32_t* __restrict__ packed, std::uint32_t bmask,
-                 const std::uint32_t* __restrict__ rowtab, const int* __restrict__ chunk_begin, long long total_slots,
-                 int slots_per_cta, int G, const int* __restrict__ scale_exp, long long* __restrict__ partials) {
-    extern __shared__ std::uint32_t sacc[];
-    std::uint32_t* lo = sacc;
-    std::uint32_t* hi = sacc + slots_per_cta;
-    const int g = blockIdx.x % G, c = blockIdx.x / G;
-    const long long slot_lo = (long long)g * slots_per_cta;
-    const long long slot_hi = min(slot_lo + slots_per_cta, total_slots);
-    const int nslots = static_cast<int>(slot_hi - slot_lo);
-    for (int s = threadIdx.x; s < 2 * slots_per_cta; s += kBuildThreads) sacc[s] = 0u;
-    __syncthreads();
-    if (nslots > 0) {
-        const double scale = ldexp(1.0, *scale_exp);
-        const long long SPR = SYM ? 2ll * (bmask + 1) : (long long)(bmask + 1);  // slots per replicate
-        const int m_lo = static_cast<int>(slot_lo / SPR), m_hi = static_cast<int>((slot_hi - 1) / SPR);
-        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        const int row_end = chunk_begin[c + 1];
-        for (int row = chunk_begin[c] + warp; row < row_end; row += kBuildThreads / 32) {
-            const std::uint32_t ij = rowtab[row];
-            const int i = static_cast<int>(ij >> 16), j = static_cast<int>(ij & 0xFFFFu);
-            const TT* rp = T + ((size_t)i * n + j) * n;
-            const int k0 = SYM ? j : 0;
-            for (int mb = m_lo; mb <= m_hi; mb += kBuildMR) {
-                std::uint32_t pij[kBuildMR];
-                const std::uint32_t* pk[kBuildMR];
-#pragma unroll
-                for (int r = 0; r < kBuildMR; ++r) {
-                    const int m = min(mb + r, m_hi);
-                    if (SYM) {
-                        const std::uint32_t* pm = packed + (size_t)m * n;
-                        pij[r] = __ldg(pm + i) + __ldg(pm + j);
-                        pk[r] = pm;
-                    } else {
-                        const std::uint32_t* pm = packed + (size_t)m * 3 * n;
-                        pij[r] = __ldg(pm + i) + __ldg(pm + n + j);
-                        pk[r] = pm + 2 * n;
-                    }
-                }
-                for (int k = k0 + lane; k < n; k += 32) {
-                    const double v = static_cast<double>(rp[k]);
-                    if (v == 0.0) continue;
-                    double kap = 1.0;
-                    if (SYM) kap = (i == j && j == k) ? 1.0 : ((i == j || j == k) ? 3.0 : 6.0);
-                    const long long q = __double2ll_rn(kap * v * scale);
-#pragma unroll
-                    for (int r = 0; r < kBuildMR; ++r) {
-                        const int m = mb + r;
-                        if (m > m_hi) break;
-                        const std::uint32_t p = pij[r] + __ldg(pk[r] + k);
-                        long long slot;
-                        if (SYM)
-                            slot = (long long)m * SPR + 2ll * (p & bmask) + ((p >> 30) & 1u);
-                        else
-                            slot = (long long)m * SPR + (p & bmask);
-                        const long long ls = slot - slot_lo;
-                        if (ls < 0 || ls >= nslots) continue;
-                        add64(lo, hi, static_cast<int>(ls), (p >> 31) ? -q : q);
-                    }
-                }
-            }
-        }
-    }
-    __syncthreads();
-    long long* out = partials + (long long)c * total_slots + slot_lo;
-    for (int s = threadIdx.x; s < nslots; s += kBuildThreads)
-        out[s] = static_cast<long long>((static_cast<unsigned long long>(hi[s]) << 32) | lo[s]);
-}
-
-// data += (sum over chunks of partials) * 2^-F. For the symmetric set the slot
-// index equals the double index into interleaved (re,im) data; asym is real-only.
-template <bool SYM>
-__global__ void k_build_finalize(const long long* __restrict__ partials, int C, long long total_slots,
-                                 const int* __restrict__ scale_exp, double* __restrict__ data) {
-    long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (s >= total_slots) return;
-    unsigned long long acc = 0;
-    for (int c = 0; c < C; ++c) acc += static_cast<unsigned long long>(partials[(long long)c * total_slots + s]);
-    const long long q = static_cast<long long>(acc);
-    if (q == 0) return;
-    const double v = ldexp(static_cast<double>(q), -*scale_exp);
-    if (SYM)
-        data[s] += v;
-    else
-        data[2 * s] += v;
-}
-
-void launch_build_prepass(cudaStream_t st, const void* T, const BuildPlan& p) {
-    cudaMemsetAsync(p.nonfinite, 0, sizeof(int), st);
-    if (p.sym) {
-        if (p.dtype == 0)
-            k_build_prepass<double, true><<<kPrepassBlocks, 256, 0, st>>>((const double*)T, p.n, p.rowtab, p.nrows,
-                                                                         p.prepass_partials, p.nonfinite);
-        else
-            k_build_prepass<float, true><<<kPrepassBlocks, 256, 0, st>>>((const float*)T, p.n, p.rowtab, p.nrows,
-                                                                        p.prepass_partials, p.nonfinite);
-    } else {
-        if (p.dtype == 0)
-            k_build_prepass<double, false><<<kPrepassBlocks, 256, 0, st>>>((const double*)T, p.n, p.rowtab, p.nrows,
-                                                                          p.prepass_partials, p.nonfinite);
-        else
-            k_build_prepass<float, false><<<kPrepassBlocks, 256, 0, st>>>((const float*)T, p.n, p.rowtab, p.nrows,
-                                                                         p.prepass_partials, p.nonfinite);
-    }
-    SKC_LAUNCHED();
-    k_build_scale<<<1, 256, 0, st>>>(p.prepass_partials, kPrepassBlocks, p.scale_exp);
-    SKC_LAUNCHED();
-}
-
-template <typename TT, bool SYM>
-static void build_main_t(cudaStream_t st, const TT* T, const BuildPlan& p) {
-    size_t smem = sizeof(std::uint32_t) * 2 * (size_t)p.slots_per_cta;
-    cudaFuncSetAttribute(k_build_main<TT, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_build_main<TT, SYM><<<p.G * p.C, kBuildThreads, smem, st>>>(T, p.n, p.packed, p.bmask, p.rowtab, p.chunk_begin,
-                                                                   p.total_slots, p.slots_per_cta, p.G, p.scale_exp,
-                                                                   p.partials);
-    SKC_LAUNCHED();
-}
-void launch_build_main(cudaStream_t st, const void* T, const BuildPlan& p) {
-    if (p.sym) {
-        if (p.dtype == 0)
-            build_main_t<double, true>(st, (const double*)T, p);
-        else
-            build_main_t<float, true>(st, (const float*)T, p);
-    } else {
-        if (p.dtype == 0)
-            build_main_t<double, false>(st, (const double*)T, p);
-        else
-            build_main_t<float, false>(st, (const float*)T, p);
-    }
-}
-void launch_build_finalize(cudaStream_t st, const BuildPlan& p) {
-    if (p.sym)
-        k_build_finalize<true><<<cdiv(p.total_slots, 256), 256, 0, st>>>(p.partials, p.C, p.total_slots, p.scale_exp,
-                                                                         p.data_as_double);
-    else
-        k_build_finalize<false><<<cdiv(p.total_slots, 256), 256, 0, st>>>(p.partials, p.C, p.total_slots,
-                                                                          p.scale_exp, p.data_as_double);
-    SKC_LAUNCHED();
-}
-
 // ============================ local FFT drivers ==================================
 constexpr int kFftThreads = 256;
+#ifndef SKC_FFT_MINB
+#define SKC_FFT_MINB 2  // 128 registers: radix-16 passes stay in registers (minB 3 spills)
+#endif
 
-// Forward DIF on `na` arrays of length N laid out back to back (stride padded_len(N)).
-__device__ __forceinline__ void dif_arrays(double2* sm, int na, int N, const PassPlan& pl, const double2* tw,
-                                           int logb) {
-    const int stride = padded_len(N);
-    for (int p = 0; p < pl.npass; ++p) {
-        const int items = N >> pl.logr[p];
-        for (int w = threadIdx.x; w < na * items; w += blockDim.x) {
-            const int a = w / items;
-            dif_pass_dispatch(pl.logr[p], sm + a * stride, w - a * items, pl.h[p], tw, logb);
-        }
-        __syncthreads();
+#define SKC_LOGN_SWITCH(logN, X)    \
+    switch (logN) {                 \
+        case 1: X(1); break;        \
+        case 2: X(2); break;        \
+        case 3: X(3); break;        \
+        case 4: X(4); break;        \
+        case 5: X(5); break;        \
+        case 6: X(6); break;        \
+        case 7: X(7); break;        \
+        case 8: X(8); break;        \
+        case 9: X(9); break;        \
+        case 10: X(10); break;      \
+        case 11: X(11); break;      \
+        case 12: X(12); break;      \
+        default: break;             \
     }
-}
-__device__ __forceinline__ void dit_arrays(double2* sm, int na, int N, const PassPlan& pl, const double2* tw,
-                                           int logb) {
-    const int stride = padded_len(N);
-    for (int p = pl.npass - 1; p >= 0; --p) {
-        const int items = N >> pl.logr[p];
-        for (int w = threadIdx.x; w < na * items; w += blockDim.x) {
-            const int a = w / items;
-            dit_pass_dispatch(pl.logr[p], sm + a * stride, w - a * items, pl.h[p], tw, logb);
-        }
-        __syncthreads();
-    }
-}
-
-// Deterministic sparse scatter of a count sketch into a residue-r local array:
-// y[t mod N] += val(i) * w_b^{-r t} for t = bucket(i). perm lists indices sorted
-// by (bucket mod N, i); each run of equal keys is summed by its head thread.
-template <typename ValFn>
-__device__ __forceinline__ void scatter_sorted(double2* y, const std::uint32_t* perm, const std::uint32_t* bucket,
-                                               int n, int N, int r, std::uint32_t bmask, const double2* tw,
-                                               ValFn val) {
-    const std::uint32_t nmask = static_cast<std::uint32_t>(N - 1);
-    for (int q = threadIdx.x; q < n; q += blockDim.x) {
-        const int i = perm[q];
-        const std::uint32_t t = bucket[i];
-        const std::uint32_t key = t & nmask;
-        if (q > 0 && (bucket[perm[q - 1]] & nmask) == key) continue;
-        double2 acc = mk(0.0, 0.0);
-        for (int q2 = q; q2 < n; ++q2) {
-            const int i2 = (q2 == q) ? i : static_cast<int>(perm[q2]);
-            const std::uint32_t t2 = (q2 == q) ? t : bucket[i2];
-            if ((t2 & nmask) != key) break;
-            const double2 x = val(i2);
-            acc = cadd(acc, cmul(x, conj(tw[(static_cast<std::uint32_t>(r) * t2) & bmask])));
-        }
-        y[pad16(static_cast<int>(key))] = acc;
-    }
-}
 
 __device__ __forceinline__ void zero_smem(double2* sm, int count) {
     for (int x = threadIdx.x; x < count; x += blockDim.x) sm[x] = mk(0.0, 0.0);
 }
 
+// Deterministic sparse scatter of a count sketch into the residue-r local array:
+// y[t mod N] = sum over the run of equal keys of val(i) * w_b^{-r t}. `plan` holds
+// (i, t | tag) ordered by (t mod N, i); the head of each run sums it in ascending i,
+// so no atomics are needed and the result does not depend on scheduling.
+template <typename ValFn>
+__device__ __forceinline__ void scatter_plan(double2* y, const uint2* __restrict__ plan, int n, int N, int r,
+                                             std::uint32_t bmask, std::uint32_t tmask, const double2* __restrict__ tw,
+                                             ValFn val) {
+    const std::uint32_t nmask = static_cast<std::uint32_t>(N - 1);
+    for (int q = threadIdx.x; q < n; q += blockDim.x) {
+        uint2 e = plan[q];
+        const std::uint32_t key = e.y & nmask;
+        if (q > 0 && (plan[q - 1].y & nmask) == key) continue;
+        double2 acc = mk(0.0, 0.0);
+        for (int q2 = q;;) {
+            const std::uint32_t t = e.y & tmask;
+            acc = cadd(acc, cmul(val(e.x, e.y), conj(tw[(static_cast<std::uint32_t>(r) * t) & bmask])));
+            if (++q2 >= n) break;
+            e = plan[q2];
+            if ((e.y & nmask) != key) break;
+        }
+        y[pad16(static_cast<int>(key))] = acc;
+    }
+}
+
+// plan[m][q] = (i, t_i | tag_i << tag_shift) for i = perm[m][q]
+__global__ void k_make_plan(const std::uint32_t* __restrict__ perm, const std::uint32_t* __restrict__ bucket,
+                            const std::uint8_t* __restrict__ sexp, int sexp_mult, const std::uint32_t* __restrict__ packed,
+                            int n, long long total, uint2* __restrict__ plan) {
+    const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (idx >= total) return;
+    const long long rep = idx / n;
+    const std::uint32_t i = perm[idx];
+    const long long src = rep * n + i;
+    std::uint32_t y = bucket[src];
+    if (sexp) y |= ((static_cast<std::uint32_t>(sexp[src]) * sexp_mult) & 3u) << 28;
+    if (packed) y |= packed[src] & 0x80000000u;
+    plan[idx] = make_uint2(i, y);
+}
+void launch_make_plan(cudaStream_t st, const std::uint32_t* perm, const std::uint32_t* bucket, const std::uint8_t* sexp,
+                      int sexp_mult, const std::uint32_t* packed, int nrep, int n, uint2* plan) {
+    const long long tot = (long long)nrep * n;
+    k_make_plan<<<cdiv(tot, 256), 256, 0, st>>>(perm, bucket, sexp, sexp_mult, packed, n, tot, plan);
+    SKC_LAUNCHED();
+}
+
 // ============================ K4: spectra ========================================
 // contraction.cpp:62-72 (ensure_fresh): F(data_m) for all m, in local residue layout.
-__global__ void __launch_bounds__(kFftThreads) k_spectrum(const double2* __restrict__ data, std::uint32_t b, int logb,
-                                                          int N, int logN, int S, const double2* __restrict__ tw,
-                                                          double2* __restrict__ spec) {
+template <int LOGN>
+__global__ void __launch_bounds__(kFftThreads, SKC_FFT_MINB)
+    k_spectrum(const double2* __restrict__ data, std::uint32_t b, int S, const double2* __restrict__ tw,
+               const double2* __restrict__ twl, double2* __restrict__ spec) {
     extern __shared__ double2 sm[];
+    constexpr int N = 1 << LOGN;
     const int r = blockIdx.x % S, m = blockIdx.x / S;
     const double2* dm = data + (size_t)m * b;
     const std::uint32_t bmask = b - 1;
@@ -419,17 +229,23 @@ __global__ void __launch_bounds__(kFftThreads) k_spectrum(const double2* __restr
         sm[pad16(tp)] = y;
     }
     __syncthreads();
-    const PassPlan pl = make_plan(N);
-    dif_arrays(sm, 1, N, pl, tw, logb);
+    dif_local<LOGN>(sm, 1, twl);
     double2* out = spec + ((size_t)m * S + r) * N;
     for (int j = threadIdx.x; j < N; j += blockDim.x) out[j] = sm[pad16(j)];
 }
 
 void launch_spectrum(cudaStream_t st, const double2* data, std::uint32_t b, int logb, int B, int N, int logN, int S,
-                     const double2* tw, double2* spec) {
-    size_t smem = sizeof(double2) * padded_len(N);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_spectrum, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_spectrum<<<B * S, kFftThreads, smem, st>>>(data, b, logb, N, logN, S, tw, spec);
+                     const double2* tw, const double2* twl, double2* spec) {
+    (void)logb;
+    const size_t smem = sizeof(double2) * padded_len(N);
+#define L_(LG)                                                                                               \
+    {                                                                                                        \
+        if (smem > 48 * 1024)                                                                                \
+            cudaFuncSetAttribute(k_spectrum<LG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
+        k_spectrum<LG><<<B * S, kFftThreads, smem, st>>>(data, b, S, tw, twl, spec);                          \
+    }
+    SKC_LOGN_SWITCH(logN, L_)
+#undef L_
     SKC_LAUNCHED();
     count_transforms((std::uint64_t)B * S, S);
 }
@@ -437,36 +253,33 @@ void launch_spectrum(cudaStream_t st, const double2* data, std::uint32_t b, int 
 // ============================ K3: symmetric contractions ==========================
 // Ivv: contraction.cpp:128-181. vvv: contraction.cpp:83-126.
 // One CTA per (restart l, replicate m, residue r).
-__global__ void __launch_bounds__(kFftThreads) k_sym_contract(SymView v, const double* __restrict__ U, int L,
-                                                              int mode, double* __restrict__ out) {
+template <int LOGN>
+__global__ void __launch_bounds__(kFftThreads, SKC_FFT_MINB)
+    k_sym_contract(SymView v, const double* __restrict__ U, int L, int mode, double* __restrict__ out) {
     extern __shared__ double2 sm[];
     __shared__ double red[kFftThreads / 32];
-    const int N = v.N, S = v.S, n = v.n, B = v.B;
+    constexpr int N = 1 << LOGN;
+    constexpr int stride = N + (N >> 4) + 1;
+    const int S = v.S, n = v.n, B = v.B;
     const int r = blockIdx.x % S;
     const int m = (blockIdx.x / S) % B;
     const int l = blockIdx.x / (S * B);
-    const int stride = padded_len(N);
     double2* A = sm;
     double2* Bv = sm + stride;
     const double* u = U + (size_t)l * n;
-    const std::uint32_t* b1 = v.bucket1 + (size_t)m * n;
-    const std::uint32_t* b2 = v.bucket2 + (size_t)m * n;
-    const std::uint32_t* b3 = v.bucket3 + (size_t)m * n;
-    const std::uint8_t* se = v.sexp + (size_t)m * n;
     const std::uint32_t bmask = v.b - 1;
 
     zero_smem(sm, 2 * stride);
     __syncthreads();
     // f1[h_i] += sigma_i u_i ; f2[2h_i] += sigma_i^2 u_i^2   (contraction.cpp:150-154)
-    scatter_sorted(A, v.perm1 + (size_t)m * n, b1, n, N, r, bmask, v.tw,
-                   [&](int i) { return root4_times(se[i], u[i]); });
-    scatter_sorted(Bv, v.perm2 + (size_t)m * n, b2, n, N, r, bmask, v.tw, [&](int i) {
+    scatter_plan(A, v.plan1 + (size_t)m * n, n, N, r, bmask, 0x0FFFFFFFu, v.tw,
+                 [&](std::uint32_t i, std::uint32_t y) { return root4_times(y >> 28, u[i]); });
+    scatter_plan(Bv, v.plan2 + (size_t)m * n, n, N, r, bmask, 0x0FFFFFFFu, v.tw, [&](std::uint32_t i, std::uint32_t y) {
         const double ui = u[i];
-        return root4_times(2u * se[i], ui * ui);
+        return root4_times(y >> 28, ui * ui);
     });
     __syncthreads();
-    const PassPlan pl = make_plan(N);
-    dif_arrays(sm, 2, N, pl, v.tw, v.logb);
+    dif_local<LOGN>(sm, 2, v.twl);
     const double2* fT = v.spec + ((size_t)m * S + r) * N;
 
     if (mode == 0) {
@@ -479,11 +292,15 @@ __global__ void __launch_bounds__(kFftThreads) k_sym_contract(SymView v, const d
             Bv[pad16(j)] = cmulc(t, fu);
         }
         __syncthreads();
-        dit_arrays(sm, 2, N, pl, v.tw, v.logb);
+        dit_local<LOGN>(sm, 2, v.twl);
         const double inv_b = 1.0 / static_cast<double>(v.b);
         const std::uint32_t nmask = static_cast<std::uint32_t>(N - 1);
         double* o = out + (((size_t)l * B + m) * S + r) * n;
         const double2* dm = v.data + (size_t)m * v.b;
+        const std::uint32_t* b1 = v.bucket1 + (size_t)m * n;
+        const std::uint32_t* b2 = v.bucket2 + (size_t)m * n;
+        const std::uint32_t* b3 = v.bucket3 + (size_t)m * n;
+        const std::uint8_t* se = v.sexp + (size_t)m * n;
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
             const unsigned e = se[i];
             const double ui = u[i];
@@ -509,6 +326,8 @@ __global__ void __launch_bounds__(kFftThreads) k_sym_contract(SymView v, const d
         double term3 = 0.0;
         if (r == 0) {  // contraction.cpp:117-121
             const double2* dm = v.data + (size_t)m * v.b;
+            const std::uint32_t* b3 = v.bucket3 + (size_t)m * n;
+            const std::uint8_t* se = v.sexp + (size_t)m * n;
             for (int i = threadIdx.x; i < n; i += blockDim.x) {
                 const double u3 = u[i] * u[i] * u[i];
                 term3 += u3 * re_rot_conj(3u * se[i], dm[b3[i]]);
@@ -525,9 +344,16 @@ __global__ void __launch_bounds__(kFftThreads) k_sym_contract(SymView v, const d
 }
 
 void launch_sym_contract(cudaStream_t st, const SymView& v, const double* U, int L, int mode, double* out) {
-    size_t smem = sizeof(double2) * 2 * padded_len(v.N);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_sym_contract, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_sym_contract<<<(unsigned)((long long)L * v.B * v.S), kFftThreads, smem, st>>>(v, U, L, mode, out);
+    const size_t smem = sizeof(double2) * 2 * padded_len(v.N);
+    const unsigned grid = (unsigned)((long long)L * v.B * v.S);
+#define L_(LG)                                                                                                  \
+    {                                                                                                           \
+        if (smem > 48 * 1024)                                                                                   \
+            cudaFuncSetAttribute(k_sym_contract<LG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
+        k_sym_contract<LG><<<grid, kFftThreads, smem, st>>>(v, U, L, mode, out);                                \
+    }
+    SKC_LOGN_SWITCH(v.logN, L_)
+#undef L_
     SKC_LAUNCHED();
     count_transforms((std::uint64_t)L * v.B * v.S * (mode == 0 ? 4 : 2), v.S);
 }
@@ -662,31 +488,31 @@ void launch_argmax_first(cudaStream_t st, const double* values, int L, int* best
 
 // ============================ K2: frequency-domain accumulation ===================
 // Symmetric moment / rank-1: acc += w * F(CS(x))^3 (sketch.cpp:353-358; lda.cpp:201-207).
-__global__ void __launch_bounds__(kFftThreads) k_sym_moment(SymView v, const double* __restrict__ X,
-                                                            const double* __restrict__ w, double wscale,
-                                                            long long Nsamp, int chunks, double* __restrict__ acc) {
+template <int LOGN>
+__global__ void __launch_bounds__(kFftThreads, SKC_FFT_MINB)
+    k_sym_moment(SymView v, const double* __restrict__ X, const double* __restrict__ w, double wscale, long long Nsamp,
+                 int chunks, double* __restrict__ acc) {
     extern __shared__ double2 sm[];
-    const int N = v.N, S = v.S, n = v.n, B = v.B;
+    constexpr int N = 1 << LOGN;
+    constexpr int stride = N + (N >> 4) + 1;
+    const int S = v.S, n = v.n, B = v.B;
     const int r = blockIdx.x % S;
     const int m = (blockIdx.x / S) % B;
     const int ch = blockIdx.x / (S * B);
-    const int stride = padded_len(N);
     double2* A = sm;
     double2* ACC = sm + stride;
     const long long per = (Nsamp + chunks - 1) / chunks;
     const long long s0 = (long long)ch * per, s1 = min(Nsamp, s0 + per);
-    const std::uint32_t* b1 = v.bucket1 + (size_t)m * n;
-    const std::uint8_t* se = v.sexp + (size_t)m * n;
-    const std::uint32_t* perm = v.perm1 + (size_t)m * n;
-    const PassPlan pl = make_plan(N);
+    const uint2* plan = v.plan1 + (size_t)m * n;
     zero_smem(ACC, N + 8);
     for (long long s = s0; s < s1; ++s) {
         const double* x = X + (size_t)s * n;
         zero_smem(A, stride);
         __syncthreads();
-        scatter_sorted(A, perm, b1, n, N, r, v.b - 1, v.tw, [&](int i) { return root4_times(se[i], x[i]); });
+        scatter_plan(A, plan, n, N, r, v.b - 1, 0x0FFFFFFFu, v.tw,
+                     [&](std::uint32_t i, std::uint32_t y) { return root4_times(y >> 28, x[i]); });
         __syncthreads();
-        dif_arrays(A, 1, N, pl, v.tw, v.logb);
+        dif_local<LOGN>(A, 1, v.twl);
         const double ws = (w ? w[s] : 1.0) * wscale;
         for (int j = threadIdx.x; j < N; j += blockDim.x) {
             const double2 z = A[pad16(j)];
@@ -700,20 +526,27 @@ __global__ void __launch_bounds__(kFftThreads) k_sym_moment(SymView v, const dou
 }
 void launch_sym_moment_accumulate(cudaStream_t st, const SymView& v, const double* X, const double* w, double wscale,
                                   long long Nsamp, int chunks, double* acc) {
-    size_t smem = sizeof(double2) * (padded_len(v.N) + v.N + 8);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_sym_moment, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_sym_moment<<<(unsigned)((long long)chunks * v.B * v.S), kFftThreads, smem, st>>>(v, X, w, wscale, Nsamp, chunks,
-                                                                                       acc);
+    const size_t smem = sizeof(double2) * (padded_len(v.N) + v.N + 8);
+    const unsigned grid = (unsigned)((long long)chunks * v.B * v.S);
+#define L_(LG)                                                                                                \
+    {                                                                                                         \
+        if (smem > 48 * 1024)                                                                                 \
+            cudaFuncSetAttribute(k_sym_moment<LG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
+        k_sym_moment<LG><<<grid, kFftThreads, smem, st>>>(v, X, w, wscale, Nsamp, chunks, acc);               \
+    }
+    SKC_LOGN_SWITCH(v.logN, L_)
+#undef L_
     SKC_LAUNCHED();
     count_transforms((std::uint64_t)Nsamp * v.B * v.S, v.S);
 }
 
 // Sum the chunk partials (fixed order), inverse DIT -> tmp[m][r][t'] natural order.
-__global__ void __launch_bounds__(kFftThreads) k_freq_reduce_inverse(const double2* __restrict__ acc, int chunks, int B,
-                                                                     int S, int N, int logb,
-                                                                     const double2* __restrict__ tw,
-                                                                     double2* __restrict__ tmp) {
+template <int LOGN>
+__global__ void __launch_bounds__(kFftThreads, SKC_FFT_MINB)
+    k_freq_reduce_inverse(const double2* __restrict__ acc, int chunks, int B, int S, const double2* __restrict__ twl,
+                          double2* __restrict__ tmp) {
     extern __shared__ double2 sm[];
+    constexpr int N = 1 << LOGN;
     const int r = blockIdx.x % S, m = blockIdx.x / S;
     for (int j = threadIdx.x; j < N; j += blockDim.x) {
         double2 s = mk(0.0, 0.0);
@@ -721,20 +554,24 @@ __global__ void __launch_bounds__(kFftThreads) k_freq_reduce_inverse(const doubl
         sm[pad16(j)] = s;
     }
     __syncthreads();
-    const PassPlan pl = make_plan(N);
-    dit_arrays(sm, 1, N, pl, tw, logb);
+    dit_local<LOGN>(sm, 1, twl);
     double2* o = tmp + ((size_t)m * S + r) * N;
     for (int j = threadIdx.x; j < N; j += blockDim.x) o[j] = sm[pad16(j)];
 }
 void launch_freq_reduce_inverse(cudaStream_t st, const double* acc, int chunks, int B, int S, int N, int logN,
-                                std::uint32_t b, int logb, const double2* tw, double2* tmp) {
-    (void)logN;
+                                std::uint32_t b, int logb, const double2* twl, double2* tmp) {
     (void)b;
-    size_t smem = sizeof(double2) * padded_len(N);
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(k_freq_reduce_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_freq_reduce_inverse<<<B * S, kFftThreads, smem, st>>>(reinterpret_cast<const double2*>(acc), chunks, B, S, N,
-                                                            logb, tw, tmp);
+    (void)logb;
+    const size_t smem = sizeof(double2) * padded_len(N);
+#define L_(LG)                                                                                                    \
+    {                                                                                                             \
+        if (smem > 48 * 1024)                                                                                     \
+            cudaFuncSetAttribute(k_freq_reduce_inverse<LG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        k_freq_reduce_inverse<LG><<<B * S, kFftThreads, smem, st>>>(reinterpret_cast<const double2*>(acc), chunks, B, S, \
+                                                                    twl, tmp);                                   \
+    }
+    SKC_LOGN_SWITCH(logN, L_)
+#undef L_
     SKC_LAUNCHED();
     count_transforms((std::uint64_t)B * S, S);
 }
@@ -772,23 +609,23 @@ void launch_combine_residues(cudaStream_t st, const double2* tmp, int B, int S, 
 
 // Asymmetric factored accumulation (sketch.cpp:224-248, Eq. 2):
 // acc += a_c F(s1 u_c) F(s2 v_c) F(s3 w_c). m_only >= 0 restricts to one replicate.
-__global__ void __launch_bounds__(kFftThreads) k_asym_factored(AsymView v, const double* __restrict__ a,
-                                                               const double* __restrict__ U,
-                                                               const double* __restrict__ V,
-                                                               const double* __restrict__ W, long long Ncomp,
-                                                               int chunks, int m_only, double* __restrict__ acc) {
+template <int LOGN>
+__global__ void __launch_bounds__(kFftThreads, 1)
+    k_asym_factored(AsymView v, const double* __restrict__ a, const double* __restrict__ U,
+                    const double* __restrict__ V, const double* __restrict__ W, long long Ncomp, int chunks,
+                    int m_only, double* __restrict__ acc) {
     extern __shared__ double2 sm[];
-    const int N = v.N, S = v.S, n = v.n;
+    constexpr int N = 1 << LOGN;
+    constexpr int stride = N + (N >> 4) + 1;
+    const int S = v.S, n = v.n;
     const int Bm = (m_only >= 0) ? 1 : v.B;
     const int r = blockIdx.x % S;
     const int mm = (blockIdx.x / S) % Bm;
     const int m = (m_only >= 0) ? m_only : mm;
     const int ch = blockIdx.x / (S * Bm);
-    const int stride = padded_len(N);
     double2* ACC = sm + 3 * stride;
     const long long per = (Ncomp + chunks - 1) / chunks;
     const long long c0 = (long long)ch * per, c1 = min(Ncomp, c0 + per);
-    const PassPlan pl = make_plan(N);
     zero_smem(ACC, N + 8);
     for (long long c = c0; c < c1; ++c) {
         zero_smem(sm, 3 * stride);
@@ -796,14 +633,12 @@ __global__ void __launch_bounds__(kFftThreads) k_asym_factored(AsymView v, const
         const double* vecs[3] = {U + (size_t)c * n, V + (size_t)c * n, W + (size_t)c * n};
 #pragma unroll
         for (int sl = 0; sl < 3; ++sl) {
-            const std::uint32_t* bk = v.bucket + ((size_t)m * 3 + sl) * n;
-            const double* sg = v.sign + ((size_t)m * 3 + sl) * n;
             const double* x = vecs[sl];
-            scatter_sorted(sm + sl * stride, v.perm + ((size_t)m * 3 + sl) * n, bk, n, N, r, v.b - 1, v.tw,
-                           [&](int i) { return mk(sg[i] * x[i], 0.0); });
+            scatter_plan(sm + sl * stride, v.plan + ((size_t)m * 3 + sl) * n, n, N, r, v.b - 1, 0x7FFFFFFFu, v.tw,
+                         [&](std::uint32_t i, std::uint32_t y) { return mk((y >> 31) ? -x[i] : x[i], 0.0); });
         }
         __syncthreads();
-        dif_arrays(sm, 3, N, pl, v.tw, v.logb);
+        dif_local<LOGN>(sm, 3, v.twl);
         const double ac = a ? a[c] : 1.0;
         for (int j = threadIdx.x; j < N; j += blockDim.x) {
             const double2 pr = cmul(sm[pad16(j)], cmul(sm[stride + pad16(j)], sm[2 * stride + pad16(j)]));
@@ -817,27 +652,34 @@ __global__ void __launch_bounds__(kFftThreads) k_asym_factored(AsymView v, const
 void launch_asym_factored_accumulate(cudaStream_t st, const AsymView& v, const double* a, const double* U,
                                      const double* V, const double* W, long long Ncomp, int chunks, int m_only,
                                      double* acc) {
-    size_t smem = sizeof(double2) * (3 * padded_len(v.N) + v.N + 8);
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(k_asym_factored, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = sizeof(double2) * (3 * padded_len(v.N) + v.N + 8);
     const int Bm = (m_only >= 0) ? 1 : v.B;
-    k_asym_factored<<<(unsigned)((long long)chunks * Bm * v.S), kFftThreads, smem, st>>>(v, a, U, V, W, Ncomp, chunks,
-                                                                                         m_only, acc);
+    const unsigned grid = (unsigned)((long long)chunks * Bm * v.S);
+#define L_(LG)                                                                                                   \
+    {                                                                                                            \
+        if (smem > 48 * 1024)                                                                                    \
+            cudaFuncSetAttribute(k_asym_factored<LG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
+        k_asym_factored<LG><<<grid, kFftThreads, smem, st>>>(v, a, U, V, W, Ncomp, chunks, m_only, acc);         \
+    }
+    SKC_LOGN_SWITCH(v.logN, L_)
+#undef L_
     SKC_LAUNCHED();
     count_transforms((std::uint64_t)Ncomp * Bm * v.S * 3, v.S);
 }
 
 // ============================ K3a: asymmetric contractions ========================
 // mode_contraction: contraction.cpp:248-295 (slots at :256-257).
-__global__ void __launch_bounds__(kFftThreads) k_asym_mode(AsymView v, int free_mode, const double* __restrict__ X,
-                                                           const double* __restrict__ Y, int L,
-                                                           double* __restrict__ out) {
+template <int LOGN>
+__global__ void __launch_bounds__(kFftThreads, SKC_FFT_MINB)
+    k_asym_mode(AsymView v, int free_mode, const double* __restrict__ X, const double* __restrict__ Y, int L,
+                double* __restrict__ out) {
     extern __shared__ double2 sm[];
-    const int N = v.N, S = v.S, n = v.n, B = v.B;
+    constexpr int N = 1 << LOGN;
+    constexpr int stride = N + (N >> 4) + 1;
+    const int S = v.S, n = v.n, B = v.B;
     const int r = blockIdx.x % S;
     const int m = (blockIdx.x / S) % B;
     const int l = blockIdx.x / (S * B);
-    const int stride = padded_len(N);
     const int slot_x = free_mode == 0 ? 1 : 0;
     const int slot_y = free_mode == 2 ? 1 : 2;
     const double* x = X + (size_t)l * n;
@@ -845,26 +687,17 @@ __global__ void __launch_bounds__(kFftThreads) k_asym_mode(AsymView v, int free_
     const std::uint32_t bmask = v.b - 1;
     zero_smem(sm, 2 * stride);
     __syncthreads();
-    {
-        const std::uint32_t* bk = v.bucket + ((size_t)m * 3 + slot_x) * n;
-        const double* sg = v.sign + ((size_t)m * 3 + slot_x) * n;
-        scatter_sorted(sm, v.perm + ((size_t)m * 3 + slot_x) * n, bk, n, N, r, bmask, v.tw,
-                       [&](int i) { return mk(sg[i] * x[i], 0.0); });
-    }
-    {
-        const std::uint32_t* bk = v.bucket + ((size_t)m * 3 + slot_y) * n;
-        const double* sg = v.sign + ((size_t)m * 3 + slot_y) * n;
-        scatter_sorted(sm + stride, v.perm + ((size_t)m * 3 + slot_y) * n, bk, n, N, r, bmask, v.tw,
-                       [&](int i) { return mk(sg[i] * y[i], 0.0); });
-    }
+    scatter_plan(sm, v.plan + ((size_t)m * 3 + slot_x) * n, n, N, r, bmask, 0x7FFFFFFFu, v.tw,
+                 [&](std::uint32_t i, std::uint32_t tg) { return mk((tg >> 31) ? -x[i] : x[i], 0.0); });
+    scatter_plan(sm + stride, v.plan + ((size_t)m * 3 + slot_y) * n, n, N, r, bmask, 0x7FFFFFFFu, v.tw,
+                 [&](std::uint32_t i, std::uint32_t tg) { return mk((tg >> 31) ? -y[i] : y[i], 0.0); });
     __syncthreads();
-    const PassPlan pl = make_plan(N);
-    dif_arrays(sm, 2, N, pl, v.tw, v.logb);
+    dif_local<LOGN>(sm, 2, v.twl);
     const double2* fT = v.spec + ((size_t)m * S + r) * N;
     for (int j = threadIdx.x; j < N; j += blockDim.x)
         sm[pad16(j)] = cmulc(fT[j], cmul(sm[pad16(j)], sm[stride + pad16(j)]));
     __syncthreads();
-    dit_arrays(sm, 1, N, pl, v.tw, v.logb);
+    dit_local<LOGN>(sm, 1, v.twl);
     const double inv_b = 1.0 / static_cast<double>(v.b);
     const std::uint32_t nmask = static_cast<std::uint32_t>(N - 1);
     const std::uint32_t* bf = v.bucket + ((size_t)m * 3 + free_mode) * n;
@@ -878,37 +711,42 @@ __global__ void __launch_bounds__(kFftThreads) k_asym_mode(AsymView v, int free_
 }
 void launch_asym_mode(cudaStream_t st, const AsymView& v, int free_mode, const double* X, const double* Y, int L,
                       double* part) {
-    size_t smem = sizeof(double2) * 2 * padded_len(v.N);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_asym_mode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_asym_mode<<<(unsigned)((long long)L * v.B * v.S), kFftThreads, smem, st>>>(v, free_mode, X, Y, L, part);
+    const size_t smem = sizeof(double2) * 2 * padded_len(v.N);
+    const unsigned grid = (unsigned)((long long)L * v.B * v.S);
+#define L_(LG)                                                                                               \
+    {                                                                                                        \
+        if (smem > 48 * 1024)                                                                                \
+            cudaFuncSetAttribute(k_asym_mode<LG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
+        k_asym_mode<LG><<<grid, kFftThreads, smem, st>>>(v, free_mode, X, Y, L, part);                       \
+    }
+    SKC_LOGN_SWITCH(v.logN, L_)
+#undef L_
     SKC_LAUNCHED();
     count_transforms((std::uint64_t)L * v.B * v.S * 3, v.S);
 }
 
 // vvv: contraction.cpp:209-246. Partial sums of Re(fT conj(fx fy fz)) per residue.
-__global__ void __launch_bounds__(kFftThreads) k_asym_vvv(AsymView v, const double* __restrict__ U, int L,
-                                                          double* __restrict__ out) {
+template <int LOGN>
+__global__ void __launch_bounds__(kFftThreads, 2)
+    k_asym_vvv(AsymView v, const double* __restrict__ U, int L, double* __restrict__ out) {
     extern __shared__ double2 sm[];
     __shared__ double red[kFftThreads / 32];
-    const int N = v.N, S = v.S, n = v.n, B = v.B;
+    constexpr int N = 1 << LOGN;
+    constexpr int stride = N + (N >> 4) + 1;
+    const int S = v.S, n = v.n, B = v.B;
     const int r = blockIdx.x % S;
     const int m = (blockIdx.x / S) % B;
     const int l = blockIdx.x / (S * B);
-    const int stride = padded_len(N);
     const double* u = U + (size_t)l * n;
     const std::uint32_t bmask = v.b - 1;
     zero_smem(sm, 3 * stride);
     __syncthreads();
 #pragma unroll
-    for (int sl = 0; sl < 3; ++sl) {
-        const std::uint32_t* bk = v.bucket + ((size_t)m * 3 + sl) * n;
-        const double* sg = v.sign + ((size_t)m * 3 + sl) * n;
-        scatter_sorted(sm + sl * stride, v.perm + ((size_t)m * 3 + sl) * n, bk, n, N, r, bmask, v.tw,
-                       [&](int i) { return mk(sg[i] * u[i], 0.0); });
-    }
+    for (int sl = 0; sl < 3; ++sl)
+        scatter_plan(sm + sl * stride, v.plan + ((size_t)m * 3 + sl) * n, n, N, r, bmask, 0x7FFFFFFFu, v.tw,
+                     [&](std::uint32_t i, std::uint32_t tg) { return mk((tg >> 31) ? -u[i] : u[i], 0.0); });
     __syncthreads();
-    const PassPlan pl = make_plan(N);
-    dif_arrays(sm, 3, N, pl, v.tw, v.logb);
+    dif_local<LOGN>(sm, 3, v.twl);
     const double2* fT = v.spec + ((size_t)m * S + r) * N;
     double acc = 0.0;
     for (int j = threadIdx.x; j < N; j += blockDim.x) {
@@ -919,9 +757,16 @@ __global__ void __launch_bounds__(kFftThreads) k_asym_vvv(AsymView v, const doub
     if (threadIdx.x == 0) out[((size_t)l * B + m) * S + r] = s;
 }
 void launch_asym_vvv(cudaStream_t st, const AsymView& v, const double* U, int L, double* part) {
-    size_t smem = sizeof(double2) * 3 * padded_len(v.N);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_asym_vvv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_asym_vvv<<<(unsigned)((long long)L * v.B * v.S), kFftThreads, smem, st>>>(v, U, L, part);
+    const size_t smem = sizeof(double2) * 3 * padded_len(v.N);
+    const unsigned grid = (unsigned)((long long)L * v.B * v.S);
+#define L_(LG)                                                                                              \
+    {                                                                                                       \
+        if (smem > 48 * 1024)                                                                               \
+            cudaFuncSetAttribute(k_asym_vvv<LG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
+        k_asym_vvv<LG><<<grid, kFftThreads, smem, st>>>(v, U, L, part);                                     \
+    }
+    SKC_LOGN_SWITCH(v.logN, L_)
+#undef L_
     SKC_LAUNCHED();
     count_transforms((std::uint64_t)L * v.B * v.S * 3, v.S);
 }

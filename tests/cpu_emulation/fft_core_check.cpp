@@ -34,6 +34,10 @@ int main() {
                 F[f] = {(double)s.real(), (double)s.imag()};
             }
             PassPlan pl = make_plan(N);
+            // local table w_N^k as used by the templated device drivers (index with logN)
+            std::vector<double2> twl(N);
+            for (int k = 0; k < N; ++k) twl[k] = tw[static_cast<size_t>(k) * S];
+            const bool use_local = (logN % 2) == 1 || N == b;  // exercise both indexings
             double maxerr = 0, maxinv = 0;
             std::vector<std::complex<double>> back(b, 0.0);
             for (int r = 0; r < S; ++r) {
@@ -46,7 +50,9 @@ int main() {
                 }
                 for (int p = 0; p < pl.npass; ++p) {
                     int items = N >> pl.logr[p];
-                    for (int w = 0; w < items; ++w) dif_pass_dispatch(pl.logr[p], sm.data(), w, pl.h[p], tw.data(), logb);
+                    for (int w = 0; w < items; ++w)
+                        dif_pass_dispatch(pl.logr[p], sm.data(), w, pl.h[p], use_local ? twl.data() : tw.data(),
+                                          use_local ? logN : logb);
                 }
                 for (int j = 0; j < N; ++j) {
                     int f = r + S * (int)bitrev(j, logN);
@@ -55,7 +61,9 @@ int main() {
                 }
                 for (int p = pl.npass - 1; p >= 0; --p) {
                     int items = N >> pl.logr[p];
-                    for (int w = 0; w < items; ++w) dit_pass_dispatch(pl.logr[p], sm.data(), w, pl.h[p], tw.data(), logb);
+                    for (int w = 0; w < items; ++w)
+                        dit_pass_dispatch(pl.logr[p], sm.data(), w, pl.h[p], use_local ? twl.data() : tw.data(),
+                                          use_local ? logN : logb);
                 }
                 for (int t = 0; t < b; ++t) {
                     double2 v = cmul(sm[pad16(t % N)], tw[((long long)r * t) % b]);
@@ -65,6 +73,9 @@ int main() {
             for (int t = 0; t < b; ++t) maxinv = std::max(maxinv, std::abs(back[t] / (double)b - x[t]));
             bool ok = maxerr < 1e-13 && maxinv < 1e-13;
             if (!ok) ++fails;
+            if (plan_npass(logN) != pl.npass) { ++fails; std::printf("constexpr plan mismatch\n"); }
+            for (int p = 0; p < pl.npass; ++p)
+                if (plan_logr(logN, p) != pl.logr[p] || plan_h(logN, p) != pl.h[p]) { ++fails; std::printf("plan mismatch\n"); }
             std::printf("b=%6d N=%6d S=%3d passes=%d fwd_err=%.2e inv_err=%.2e %s\n", b, N, S, pl.npass, maxerr, maxinv, ok ? "ok" : "FAIL");
         }
     }

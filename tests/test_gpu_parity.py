@@ -126,6 +126,26 @@ def test_sym_dense_device_tensor_and_accumulate(gpu_ctx):
     assert rel_per_replicate(s.data(), o.data()) <= SKETCH_TOL
 
 
+def test_sym_dense_pinned_and_pageable_host_inputs(gpu_ctx):
+    """Pinned host tensors are read in place over the bus, pageable ones staged by row
+    blocks; both must give the device-resident result (and the oracle's)."""
+    import torch
+
+    n = 33
+    T = sym_tensor(n, 12)
+    pinned = torch.from_numpy(T.copy()).pin_memory().numpy()
+    ref = O.SymSet(n, 1024, 4, 9)
+    ref.accumulate_dense(T, True)
+    for src in (T, pinned):
+        s = skb().SymTensorSketchSet(n, 1024, 4, 9, gpu_ctx)
+        s.accumulate_dense(src, assume_symmetric=True)
+        assert rel_per_replicate(s.data(), ref.data()) <= SKETCH_TOL
+    sl = skb().SymTensorSketchSet(n, 1024, 4, 9, gpu_ctx)
+    sl.accumulate_dense(pinned, assume_symmetric=True, i0=0, i1=10)
+    sl.accumulate_dense(T, assume_symmetric=True, i0=10, i1=n)
+    assert rel_per_replicate(sl.data(), ref.data()) <= SKETCH_TOL
+
+
 def test_sym_dense_symmetry_check_message(gpu_ctx):
     n = 6
     T = sym_tensor(n, 1)
