@@ -124,6 +124,13 @@ int skc_sym_add_scaled_rank1(skc_sym_set* s, const double* u_host, double alpha)
  * Mathematically N calls of add_scaled_rank1(x_i, w_i) with one inverse transform
  * per replicate at the end, the pattern of lda.cpp:195-223. */
 int skc_sym_accumulate_moment(skc_sym_set* s, const double* X, const double* w, long long N, int location);
+/* sketch_whitened_m3(corpus, W, alpha0, set) (lda.cpp:145-226). Corpus in CSR form
+ * (doc_ptr[D+1] with doc_ptr[0] = 0, word[nnz], count[nnz]) and the whitening map W
+ * (V x k row-major, k == set n), all host arrays. used/skipped receive StreamStats
+ * (lda.hpp:57-60). Documents shorter than 3 tokens are skipped (lda.cpp:164-167). */
+int skc_sym_sketch_whitened_m3(skc_sym_set* s, int V, long long D, const long long* doc_ptr, const int* word,
+                               const int* count, const double* W, double alpha0, long long* used,
+                               long long* skipped);
 /* replicate(m).data -> host (B-major when m < 0: all replicates, B*b complex). */
 int skc_sym_read_data(const skc_sym_set* s, int m, double* out_host);
 /* mutable_replicate(m).data = in (bumps version, sketch.hpp:105-108); m < 0: all. */
@@ -131,6 +138,12 @@ int skc_sym_write_data(skc_sym_set* s, int m, const double* in_host);
 /* Device pointer to the B*b complex data (for collectives); bump version after writes. */
 int skc_sym_data_device(skc_sym_set* s, void** dev_ptr, size_t* bytes);
 int skc_sym_bump_version(skc_sym_set* s);
+/* sym_aux_sketches(rep(m), b, u) (sketch.cpp:412-425): s1/s2/s3 host arrays of 2*b doubles
+ * (any may be NULL). */
+int skc_sym_aux_sketches(const skc_sym_set* s, int m, const double* u_host, double* s1, double* s2, double* s3);
+/* sketch_rank1_sym(set, m, u) (sketch.cpp:427-443): sketch of the upper-triangular
+ * truncation of u^(x)3, (1/6) s1*s1*s1 + (1/2) s2*s1 + (1/3) s3 -> out 2*b doubles. */
+int skc_sym_rank1_truncated(const skc_sym_set* s, int m, const double* u_host, double* out_host);
 /* recover_entry(i,j,k) (sketch.cpp:363-377) */
 int skc_sym_recover_entry(const skc_sym_set* s, int i, int j, int k, double* out);
 

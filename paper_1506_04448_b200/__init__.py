@@ -332,6 +332,36 @@ class SymTensorSketchSet:
         wa = None if w is None else _f64(w, (X.shape[0],))
         check(lib.skc_sym_accumulate_moment(self._h, _dp(X), None if wa is None else _dp(wa), X.shape[0], SKC_HOST))
 
+    def sketch_whitened_m3(self, V: int, doc_ptr, word, count, W, alpha0: float):
+        """lda.cpp:145-226 on this set (n == whitening rank k). Corpus in CSR form; returns
+        StreamStats as (used, skipped)."""
+        dp = np.ascontiguousarray(doc_ptr, dtype=np.int64)
+        wd = np.ascontiguousarray(word, dtype=np.int32)
+        ct = np.ascontiguousarray(count, dtype=np.int32)
+        Wm = _f64(W)
+        if Wm.shape != (V, self.n()):
+            raise ValueError("sketch_whitened_m3: vocabulary mismatch")
+        used, skipped = C.c_longlong(), C.c_longlong()
+        check(lib.skc_sym_sketch_whitened_m3(self._h, int(V), dp.size - 1, dp.ctypes.data_as(C.POINTER(C.c_longlong)),
+                                             wd.ctypes.data_as(C.POINTER(C.c_int)), ct.ctypes.data_as(C.POINTER(C.c_int)),
+                                             _dp(Wm), float(alpha0), C.byref(used), C.byref(skipped)))
+        return used.value, skipped.value
+
+    def aux_sketches(self, m: int, u):
+        """sym_aux_sketches(replicate(m), b, u) (sketch.cpp:412-425) -> (s1, s2, s3)."""
+        u = _f64(u, (self.n(),))
+        b = self.b()
+        out = [np.empty(b, dtype=np.complex128) for _ in range(3)]
+        check(lib.skc_sym_aux_sketches(self._h, int(m), _dp(u), *[o.ctypes.data_as(C.POINTER(C.c_double)) for o in out]))
+        return tuple(out)
+
+    def rank1_truncated(self, m: int, u) -> np.ndarray:
+        """sketch_rank1_sym(set, m, u) (sketch.cpp:427-443)."""
+        u = _f64(u, (self.n(),))
+        out = np.empty(self.b(), dtype=np.complex128)
+        check(lib.skc_sym_rank1_truncated(self._h, int(m), _dp(u), out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
     def recover_entry(self, i: int, j: int, k: int) -> float:
         """sketch.cpp:363-377"""
         out = C.c_double()

@@ -859,6 +859,154 @@ int skc_sym_accumulate_moment(skc_sym_set* s, const double* X, const double* w, 
     });
 }
 
+int skc_sym_sketch_whitened_m3(skc_sym_set* s, int V, long long D, const long long* doc_ptr, const int* word,
+                               const int* count, const double* W, double alpha0, long long* used_out,
+                               long long* skipped_out) {
+    return guard([&] {
+        check_vec(s, "set");
+        require(V >= 1 && D >= 0, "sketch_whitened_m3: invalid corpus dimensions");
+        check_vec(doc_ptr, "sketch_whitened_m3: doc_ptr");
+        check_vec(W, "sketch_whitened_m3: W");
+        const int k = s->n;  // lda.cpp:149-151: set dimension must equal the whitening rank
+        const long long nnz = doc_ptr[D] - doc_ptr[0];
+        require(doc_ptr[0] == 0 && nnz >= 0, "sketch_whitened_m3: doc_ptr must start at 0");
+        if (nnz > 0) {
+            check_vec(word, "sketch_whitened_m3: word");
+            check_vec(count, "sketch_whitened_m3: count");
+        }
+        // host: document totals, StreamStats and the word-major transpose (docs ascending)
+        long long used = 0, skipped = 0, used1 = 0;
+        std::vector<long long> cptr(static_cast<size_t>(V) + 1, 0);
+        for (long long d = 0; d < D; ++d) {
+            long long tot = 0;
+            for (long long q = doc_ptr[d]; q < doc_ptr[d + 1]; ++q) {
+                require(word[q] >= 0 && word[q] < V, "sketch_whitened_m3: word id out of range");
+                tot += count[q];
+                cptr[static_cast<size_t>(word[q]) + 1]++;
+            }
+            if (tot < 3) ++skipped; else ++used;   // lda.cpp:164-168
+            if (tot >= 1) ++used1;                 // lda.cpp:93-96
+        }
+        if (used == 0) fail(kNumericalError, "sketch_whitened_m3: no documents with >= 3 words");  // lda.cpp:186
+        for (int w = 0; w < V; ++w) cptr[w + 1] += cptr[w];
+        std::vector<long long> cdoc(static_cast<size_t>(nnz));
+        std::vector<int> ccount(static_cast<size_t>(nnz));
+        {
+            std::vector<long long> fillp(cptr.begin(), cptr.end() - 1);
+            for (long long d = 0; d < D; ++d)
+                for (long long q = doc_ptr[d]; q < doc_ptr[d + 1]; ++q) {
+                    const long long pos = fillp[word[q]]++;
+                    cdoc[pos] = d;
+                    ccount[pos] = count[q];
+                }
+        }
+        skc_context* ctx = s->ctx;
+        ctx->use();
+        const cudaStream_t st = ctx->stream;
+        DevBuf<long long> d_ptr, d_cptr, d_cdoc, d_total;
+        DevBuf<int> d_word, d_count, d_ccount;
+        DevBuf<double> d_W, d_P, d_s1, d_s2, d_coeff1, d_sumwn, d_m1, d_q, d_acc, d_cross;
+        d_ptr.upload(doc_ptr, static_cast<size_t>(D) + 1, st);
+        d_word.upload(word, static_cast<size_t>(std::max<long long>(nnz, 1)), st);
+        d_count.upload(count, static_cast<size_t>(std::max<long long>(nnz, 1)), st);
+        d_cptr.upload(cptr.data(), cptr.size(), st);
+        d_cdoc.upload(cdoc.data(), std::max<size_t>(cdoc.size(), 1), st);
+        d_ccount.upload(ccount.data(), std::max<size_t>(ccount.size(), 1), st);
+        d_W.upload(W, static_cast<size_t>(V) * k, st);
+        d_P.alloc(static_cast<size_t>(std::max<long long>(D, 1)) * k);
+        d_s1.alloc(static_cast<size_t>(std::max<long long>(D, 1)));
+        d_s2.alloc(static_cast<size_t>(std::max<long long>(D, 1)));
+        d_total.alloc(static_cast<size_t>(std::max<long long>(D, 1)));
+        d_coeff1.alloc(static_cast<size_t>(V));
+        d_sumwn.alloc(static_cast<size_t>(V) * k);
+        d_m1.alloc(static_cast<size_t>(V));
+        d_q.alloc(static_cast<size_t>(k));
+        {
+            SKC_PROF(ctx, "lda_docs");
+            launch_lda_docs(st, k, D, d_ptr.p, d_word.p, d_count.p, d_W.p, alpha0, d_P.p, d_s1.p, d_s2.p, d_total.p);
+        }
+        {
+            SKC_PROF(ctx, "lda_vocab");
+            launch_lda_vocab(st, k, V, d_cptr.p, d_cdoc.p, d_ccount.p, d_P.p, d_s1.p, d_total.p, d_coeff1.p,
+                             d_sumwn.p, d_m1.p);
+        }
+        launch_lda_q(st, k, V, d_W.p, d_m1.p, 1.0 / static_cast<double>(used1), d_q.p);
+        ctx->check_launch();
+        const int per_rep = s->B * s->S;
+        const int chunks = std::max(1, (ctx->sms + per_rep - 1) / per_rep);
+        d_acc.alloc(static_cast<size_t>(chunks) * per_rep * s->N * 2);
+        d_cross.alloc(static_cast<size_t>(chunks) * per_rep * s->N * 2);
+        SymView v = s->view();
+        {
+            SKC_PROF(ctx, "lda_accumulate");
+            launch_lda_accumulate(st, v, D, d_P.p, d_s1.p, d_s2.p, V, d_W.p, d_coeff1.p, d_sumwn.p, chunks, d_acc.p,
+                                  d_cross.p);
+        }
+        ctx->check_launch();
+        ctx->tmp.alloc(static_cast<size_t>(s->B) * s->b);
+        const double inv_docs = 1.0 / static_cast<double>(used);
+        const double m1_coeff = 2.0 * alpha0 * alpha0 / ((alpha0 + 1.0) * (alpha0 + 2.0));  // lda.cpp:191
+        launch_lda_finish(st, v, d_acc.p, d_cross.p, chunks, d_q.p, inv_docs, m1_coeff, ctx->tmp.p);
+        ctx->check_launch();
+        launch_combine_residues(st, ctx->tmp.p, s->B, s->S, s->N, s->b, v.tw, 1.0, -1, false, s->data.p);
+        ctx->check_launch();
+        s->version += static_cast<std::uint64_t>(s->B);  // mutable_replicate(m) per replicate (lda.cpp:197)
+        ctx->sync();
+        if (used_out) *used_out = used;
+        if (skipped_out) *skipped_out = skipped;
+    });
+}
+
+int skc_sym_aux_sketches(const skc_sym_set* s, int m, const double* u_host, double* s1, double* s2, double* s3) {
+    return guard([&] {  // sketch.cpp:412-425
+        check_vec(s, "set");
+        check_vec(u_host, "sym_aux_sketches: u");
+        require(m >= 0 && m < s->B, "replicate index out of range");
+        skc_context* ctx = s->ctx;
+        ctx->use();
+        ctx->X.upload(u_host, s->n, ctx->stream);
+        ctx->tmp.alloc(3 * static_cast<size_t>(s->b));
+        launch_sym_aux(ctx->stream, s->view(), m, ctx->X.p, ctx->tmp.p);
+        ctx->check_launch();
+        const size_t bytes = s->b * sizeof(double2);
+        if (s1) CK(cudaMemcpyAsync(s1, ctx->tmp.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        if (s2) CK(cudaMemcpyAsync(s2, ctx->tmp.p + s->b, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        if (s3) CK(cudaMemcpyAsync(s3, ctx->tmp.p + 2 * static_cast<size_t>(s->b), bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->sync();
+    });
+}
+
+int skc_sym_rank1_truncated(const skc_sym_set* s, int m, const double* u_host, double* out_host) {
+    return guard([&] {  // sketch.cpp:427-443
+        check_vec(s, "set");
+        check_vec(u_host, "sketch_rank1_sym: u");
+        check_vec(out_host, "sketch_rank1_sym: out");
+        require(m >= 0 && m < s->B, "replicate index out of range");
+        skc_context* ctx = s->ctx;
+        ctx->use();
+        const cudaStream_t st = ctx->stream;
+        const SymView v = s->view();
+        ctx->X.upload(u_host, s->n, st);
+        DevBuf<double2> aux, spec2, acc, tmp, out;
+        aux.alloc(3 * static_cast<size_t>(s->b));
+        spec2.alloc(2 * static_cast<size_t>(s->b));
+        acc.alloc(s->b);
+        tmp.alloc(s->b);
+        out.alloc(s->b);
+        launch_sym_aux(st, v, m, ctx->X.p, aux.p);
+        // forward transforms of s1 and s2 (two "replicates" in local residue layout)
+        launch_spectrum(st, aux.p, s->b, s->logb, 2, s->N, s->logN, s->S, v.tw, v.twl, spec2.p);
+        launch_rank1_trunc_product(st, spec2.p, static_cast<long long>(s->b), acc.p);
+        launch_freq_reduce_inverse(st, reinterpret_cast<const double*>(acc.p), 1, 1, s->S, s->N, s->logN, s->b,
+                                   s->logb, v.twl, tmp.p);
+        launch_combine_residues(st, tmp.p, 1, s->S, s->N, s->b, v.tw, 1.0, -1, true, out.p);
+        launch_add_third(st, aux.p + 2 * static_cast<size_t>(s->b), s->b, out.p);
+        ctx->check_launch();
+        CK(cudaMemcpyAsync(out_host, out.p, s->b * sizeof(double2), cudaMemcpyDeviceToHost, st));
+        ctx->sync();
+    });
+}
+
 int skc_sym_read_data(const skc_sym_set* s, int m, double* out_host) {
     return guard([&] {
         check_vec(s, "set");

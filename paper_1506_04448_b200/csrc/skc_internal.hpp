@@ -130,6 +130,25 @@ void launch_asym_mode(cudaStream_t st, const AsymView& v, int free_mode, const d
                       double* part);
 void launch_asym_vvv(cudaStream_t st, const AsymView& v, const double* U, int L, double* part);
 
+// sym_aux_sketches / sketch_rank1_sym (sketch.cpp:412-443)
+void launch_sym_aux(cudaStream_t st, const SymView& v, int m, const double* u, double2* out /* 3 x b */);
+void launch_rank1_trunc_product(cudaStream_t st, const double2* spec2, long long len, double2* acc);
+void launch_add_third(cudaStream_t st, const double2* s3, std::uint32_t b, double2* out);
+
+// LDA whitened third moment (skc_lda.cu)
+void launch_lda_docs(cudaStream_t st, int k, long long D, const long long* doc_ptr, const int* word, const int* count,
+                     const double* W, double alpha0, double* P, double* s1, double* s2, long long* total);
+void launch_lda_vocab(cudaStream_t st, int k, int V, const long long* cptr, const long long* cdoc, const int* ccount,
+                      const double* P, const double* s1, const long long* total, double* coeff1, double* sumwn,
+                      double* m1_partial);
+void launch_lda_q(cudaStream_t st, int k, int V, const double* W, const double* m1_partial, double inv_used1,
+                  double* q);
+void launch_lda_accumulate(cudaStream_t st, const SymView& v, long long Dn, const double* P, const double* s1,
+                           const double* s2, int V, const double* W, const double* coeff1, const double* sumwn,
+                           int chunks, double* acc, double* cross);
+void launch_lda_finish(cudaStream_t st, const SymView& v, const double* acc, const double* cross, int chunks,
+                       const double* q, double inv_docs, double m1_coeff, double2* tmp);
+
 // generators
 void launch_gen_planted(cudaStream_t st, int n, int rank, const double* lambda, const double* V, double sigma,
                         std::uint64_t seed, int dtype, void* out);

@@ -771,6 +771,53 @@ void launch_asym_vvv(cudaStream_t st, const AsymView& v, const double* U, int L,
     count_transforms((std::uint64_t)L * v.B * v.S * 3, v.S);
 }
 
+// ============================ sym_aux_sketches / sketch_rank1_sym ===================
+// sketch.cpp:412-425: s1[h] += sigma u, s2[2h] += sigma^2 u^2, s3[3h] += sigma^3 u^3,
+// accumulated in ascending i by one thread (exact reference order; a test hook).
+__global__ void k_sym_aux(const std::uint32_t* __restrict__ b1, const std::uint32_t* __restrict__ b2,
+                          const std::uint32_t* __restrict__ b3, const std::uint8_t* __restrict__ se,
+                          const double* __restrict__ u, int n, std::uint32_t b, double2* __restrict__ out) {
+    double2* s1 = out;
+    double2* s2 = out + b;
+    double2* s3 = out + 2 * (size_t)b;
+    for (std::uint32_t t = threadIdx.x; t < 3 * b; t += blockDim.x) out[t] = mk(0.0, 0.0);
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    for (int i = 0; i < n; ++i) {
+        const double ui = u[i];
+        const unsigned e = se[i];
+        s1[b1[i]] = cadd(s1[b1[i]], root4_times(e, ui));
+        s2[b2[i]] = cadd(s2[b2[i]], root4_times(2u * e, ui * ui));
+        s3[b3[i]] = cadd(s3[b3[i]], root4_times(3u * e, ui * ui * ui));
+    }
+}
+void launch_sym_aux(cudaStream_t st, const SymView& v, int m, const double* u, double2* out) {
+    const size_t off = (size_t)m * v.n;
+    k_sym_aux<<<1, 256, 0, st>>>(v.bucket1 + off, v.bucket2 + off, v.bucket3 + off, v.sexp + off, u, v.n, v.b, out);
+    SKC_LAUNCHED();
+}
+// sketch.cpp:438-439: acc = f1 (f1 f1 / 6 + f2 / 2) on the local spectra of [s1; s2]
+__global__ void k_rank1_trunc_product(const double2* __restrict__ spec2, long long len, double2* __restrict__ acc) {
+    const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (j >= len) return;
+    const double2 f1 = spec2[j], f2 = spec2[len + j];
+    acc[j] = cmul(f1, cadd(cscale(cmul(f1, f1), 1.0 / 6.0), cscale(f2, 0.5)));
+}
+void launch_rank1_trunc_product(cudaStream_t st, const double2* spec2, long long len, double2* acc) {
+    k_rank1_trunc_product<<<cdiv(len, 256), 256, 0, st>>>(spec2, len, acc);
+    SKC_LAUNCHED();
+}
+// out += s3 / 3 (sketch.cpp:441)
+__global__ void k_add_third(const double2* __restrict__ s3, std::uint32_t b, double2* __restrict__ out) {
+    const std::uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= b) return;
+    out[t] = cadd(out[t], cscale(s3[t], 1.0 / 3.0));
+}
+void launch_add_third(cudaStream_t st, const double2* s3, std::uint32_t b, double2* out) {
+    k_add_third<<<cdiv(b, 256), 256, 0, st>>>(s3, b, out);
+    SKC_LAUNCHED();
+}
+
 // ============================ synthetic inputs ====================================
 // Planted symmetric tensor on the device: sum_r lambda_r V[a,r]V[b,r]V[c,r] over the
 // sorted index triple (bitwise symmetric) plus sigma * N(0,1) noise from a

@@ -1,0 +1,295 @@
+// LDA whitened third-moment sketch on sm_100a — sketch_whitened_m3
+// (proj/src/lda.cpp:145-226, with compute_m1 lda.cpp:88-100).
+//
+//   doc pass      p_d = W^T n_d (k-vector), s1_d = 1/(m(m-1)(m-2)), s2_d = a0/((a0+2) m(m-1))
+//                 for documents with m >= 3 (lda.cpp:163-185)      -> k_lda_docs (warp/doc)
+//   vocab sums    coeff1_w = sum_d 2 s1_d c_dw, sumwn_w = sum_d s1_d c_dw p_d, in ascending d
+//                 through the word-major transpose (deterministic)  -> k_lda_vocab (warp/word)
+//   m1, q         m1 = mean_d n_d/m_d (m_d >= 1), q = W^T m1        -> k_lda_m1, k_lda_q
+//   spectra       acc = sum_d s1 F(p)^3 + sum_w F(w)^2 (coeff1 F(w) - 3 F(sumwn_w)),
+//                 cross = sum_d s2 F(p)^2                          -> k_lda_accumulate
+//                 acc = (acc - 3 cross F(q)) / D + c_m1 F(q)^3; data += IFFT(acc) -> k_lda_finish
+// All transforms use the residue-split local FFT of skc_fft.cuh.
+#include <cuda_runtime.h>
+
+#include "skc_fft.cuh"
+#include "skc_host.hpp"
+#include "skc_internal.hpp"
+
+namespace skc {
+
+namespace {
+inline unsigned cdiv_l(long long a, long long b) { return static_cast<unsigned>((a + b - 1) / b); }
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ void zero_sm(double2* sm, int count) {
+    for (int x = threadIdx.x; x < count; x += blockDim.x) sm[x] = mk(0.0, 0.0);
+}
+
+// scatter of a dense k-vector through the set's bucket1 plan (cf. skc_kernels.cu)
+template <typename ValFn>
+__device__ __forceinline__ void scatter_dense(double2* y, const uint2* __restrict__ plan, int n, int N, int r,
+                                              std::uint32_t bmask, const double2* __restrict__ tw, ValFn val) {
+    const std::uint32_t nmask = static_cast<std::uint32_t>(N - 1);
+    for (int q = threadIdx.x; q < n; q += blockDim.x) {
+        uint2 e = plan[q];
+        const std::uint32_t key = e.y & nmask;
+        if (q > 0 && (plan[q - 1].y & nmask) == key) continue;
+        double2 acc = mk(0.0, 0.0);
+        for (int q2 = q;;) {
+            const std::uint32_t t = e.y & 0x0FFFFFFFu;
+            acc = cadd(acc, cmul(root4_times(e.y >> 28, val(e.x)), conj(tw[(static_cast<std::uint32_t>(r) * t) & bmask])));
+            if (++q2 >= n) break;
+            e = plan[q2];
+            if ((e.y & nmask) != key) break;
+        }
+        y[pad16(static_cast<int>(key))] = acc;
+    }
+}
+}  // namespace
+
+// ---- document pass: one warp per document ------------------------------------------
+__global__ void k_lda_docs(int k, long long D, const long long* __restrict__ doc_ptr, const int* __restrict__ word,
+                           const int* __restrict__ count, const double* __restrict__ W, double alpha0,
+                           double* __restrict__ P, double* __restrict__ s1, double* __restrict__ s2,
+                           long long* __restrict__ total_out) {
+    const long long d = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (d >= D) return;
+    const long long b0 = doc_ptr[d], b1 = doc_ptr[d + 1];
+    long long tot = 0;
+    for (long long q = b0 + lane; q < b1; q += 32) tot += count[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    if (lane == 0) total_out[d] = tot;
+    const double m = static_cast<double>(tot);
+    const bool used = tot >= 3;
+    if (lane == 0) {
+        s1[d] = used ? 1.0 / (m * (m - 1.0) * (m - 2.0)) : 0.0;
+        s2[d] = used ? alpha0 / ((alpha0 + 2.0) * m * (m - 1.0)) : 0.0;
+    }
+    // p = sum_q c_q W[word_q]  (lda.cpp:172-174, words in document order)
+    for (int a = lane; a < k; a += 32) {
+        double acc = 0.0;
+        if (used)
+            for (long long q = b0; q < b1; ++q) acc += static_cast<double>(count[q]) * W[(size_t)word[q] * k + a];
+        P[(size_t)d * k + a] = acc;
+    }
+}
+
+// ---- vocabulary accumulators through the word-major transpose ------------------------
+// cptr[V+1], cdoc[nnz] (ascending d per word), ccount[nnz]
+__global__ void k_lda_vocab(int k, int V, const long long* __restrict__ cptr, const long long* __restrict__ cdoc,
+                            const int* __restrict__ ccount, const double* __restrict__ P, const double* __restrict__ s1,
+                            const long long* __restrict__ total, double* __restrict__ coeff1,
+                            double* __restrict__ sumwn, double* __restrict__ m1_partial) {
+    const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= V) return;
+    const long long b0 = cptr[w], b1 = cptr[w + 1];
+    for (int a = lane; a < k; a += 32) {
+        double acc = 0.0;
+        for (long long q = b0; q < b1; ++q) {
+            const long long d = cdoc[q];
+            const double c = s1[d] * static_cast<double>(ccount[q]);
+            if (c != 0.0) acc += c * P[(size_t)d * k + a];
+        }
+        sumwn[(size_t)w * k + a] = acc;
+    }
+    if (lane == 0) {
+        double c1 = 0.0, m1 = 0.0;
+        for (long long q = b0; q < b1; ++q) {
+            const long long d = cdoc[q];
+            c1 += 2.0 * s1[d] * static_cast<double>(ccount[q]);                                       // lda.cpp:178
+            if (total[d] >= 1) m1 += (1.0 / static_cast<double>(total[d])) * static_cast<double>(ccount[q]);  // lda.cpp:94-95
+        }
+        coeff1[w] = c1;
+        m1_partial[w] = m1;
+    }
+}
+
+// q[a] = sum_w W[w][a] * m1[w] / used1 (lda.cpp:188-189); one block per a, fixed order.
+__global__ void k_lda_q(int k, int V, const double* __restrict__ W, const double* __restrict__ m1_partial,
+                        double inv_used1, double* __restrict__ q) {
+    __shared__ double red[kThreads / 32];
+    const int a = blockIdx.x;
+    double acc = 0.0;
+    for (int w = threadIdx.x; w < V; w += blockDim.x) acc += W[(size_t)w * k + a] * (m1_partial[w] * inv_used1);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int i = 0; i < kThreads / 32; ++i) s += red[i];
+        q[a] = s;
+    }
+}
+
+// ---- frequency-domain accumulation: CTA per (chunk, m, r) -----------------------------
+// items [0, Dn) are documents (P rows with weights s1, s2), items [Dn, Dn + V) are
+// vocabulary words (W rows with coeff1 and sumwn rows).
+template <int LOGN>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_lda_accumulate(SymView v, long long Dn, const double* __restrict__ P, const double* __restrict__ s1,
+                     const double* __restrict__ s2, int V, const double* __restrict__ W,
+                     const double* __restrict__ coeff1, const double* __restrict__ sumwn, int chunks,
+                     double* __restrict__ acc_out, double* __restrict__ cross_out) {
+    extern __shared__ double2 sm[];
+    constexpr int N = 1 << LOGN;
+    constexpr int stride = N + (N >> 4) + 1;
+    const int S = v.S, n = v.n, B = v.B;
+    const int r = blockIdx.x % S;
+    const int m = (blockIdx.x / S) % B;
+    const int ch = blockIdx.x / (S * B);
+    double2* A = sm;
+    double2* Bw = sm + stride;
+    double2* ACC = sm + 2 * stride;
+    double2* CR = ACC + N;
+    const uint2* plan = v.plan1 + (size_t)m * n;
+    const std::uint32_t bmask = v.b - 1;
+    const long long items = Dn + V;
+    const long long per = (items + chunks - 1) / chunks;
+    const long long i0 = (long long)ch * per, i1 = min(items, i0 + per);
+    zero_sm(ACC, 2 * N);
+    for (long long it = i0; it < i1; ++it) {
+        const bool doc = it < Dn;
+        if (doc && s1[it] == 0.0 && s2[it] == 0.0) continue;  // skipped document (m < 3)
+        zero_sm(sm, 2 * stride);
+        __syncthreads();
+        if (doc) {
+            const double* p = P + (size_t)it * n;
+            scatter_dense(A, plan, n, N, r, bmask, v.tw, [&](std::uint32_t i) { return p[i]; });
+        } else {
+            const long long w = it - Dn;
+            const double* wr = W + (size_t)w * n;
+            const double* sr = sumwn + (size_t)w * n;
+            scatter_dense(A, plan, n, N, r, bmask, v.tw, [&](std::uint32_t i) { return wr[i]; });
+            scatter_dense(Bw, plan, n, N, r, bmask, v.tw, [&](std::uint32_t i) { return sr[i]; });
+        }
+        __syncthreads();
+        dif_local<LOGN>(sm, doc ? 1 : 2, v.twl);
+        if (doc) {
+            const double a1 = s1[it], a2 = s2[it];
+            for (int j = threadIdx.x; j < N; j += blockDim.x) {
+                const double2 f = A[pad16(j)];
+                const double2 sq = cmul(f, f);
+                ACC[j] = cadd(ACC[j], cscale(cmul(sq, f), a1));  // lda.cpp:205
+                CR[j] = cadd(CR[j], cscale(sq, a2));              // lda.cpp:206
+            }
+        } else {
+            const double c1 = coeff1[it - Dn];
+            for (int j = threadIdx.x; j < N; j += blockDim.x) {
+                const double2 fw = A[pad16(j)];
+                const double2 w2 = cmul(fw, fw);
+                ACC[j] = cadd(ACC[j], cmul(w2, csub(cscale(fw, c1), cscale(Bw[pad16(j)], 3.0))));  // lda.cpp:216-217
+            }
+        }
+        __syncthreads();
+    }
+    double2* ao = reinterpret_cast<double2*>(acc_out) + (((size_t)ch * B + m) * S + r) * N;
+    double2* co = reinterpret_cast<double2*>(cross_out) + (((size_t)ch * B + m) * S + r) * N;
+    for (int j = threadIdx.x; j < N; j += blockDim.x) {
+        ao[j] = ACC[j];
+        co[j] = CR[j];
+    }
+}
+
+// acc = (sum acc - 3 sum cross F(q)) / D + c_m1 F(q)^3 (lda.cpp:211, 220-221), inverse DIT.
+template <int LOGN>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_lda_finish(SymView v, const double* __restrict__ acc_in, const double* __restrict__ cross_in, int chunks,
+                 const double* __restrict__ q, double inv_docs, double m1_coeff, double2* __restrict__ tmp) {
+    extern __shared__ double2 sm[];
+    constexpr int N = 1 << LOGN;
+    const int S = v.S, n = v.n, B = v.B;
+    const int r = blockIdx.x % S, m = blockIdx.x / S;
+    zero_sm(sm, N + (N >> 4) + 1);
+    __syncthreads();
+    scatter_dense(sm, v.plan1 + (size_t)m * n, n, N, r, v.b - 1, v.tw, [&](std::uint32_t i) { return q[i]; });
+    __syncthreads();
+    dif_local<LOGN>(sm, 1, v.twl);
+    const double2* ai = reinterpret_cast<const double2*>(acc_in);
+    const double2* ci = reinterpret_cast<const double2*>(cross_in);
+    for (int j = threadIdx.x; j < N; j += blockDim.x) {
+        double2 a = mk(0.0, 0.0), c = mk(0.0, 0.0);
+        for (int h = 0; h < chunks; ++h) {
+            const size_t off = (((size_t)h * B + m) * S + r) * N + j;
+            a = cadd(a, ai[off]);
+            c = cadd(c, ci[off]);
+        }
+        const double2 fq = sm[pad16(j)];
+        a = csub(a, cscale(cmul(c, fq), 3.0));
+        sm[pad16(j)] = cadd(cscale(a, inv_docs), cscale(cmul(cmul(fq, fq), fq), m1_coeff));
+    }
+    __syncthreads();
+    dit_local<LOGN>(sm, 1, v.twl);
+    double2* o = tmp + ((size_t)m * S + r) * N;
+    for (int j = threadIdx.x; j < N; j += blockDim.x) o[j] = sm[pad16(j)];
+}
+
+void launch_lda_docs(cudaStream_t st, int k, long long D, const long long* doc_ptr, const int* word, const int* count,
+                     const double* W, double alpha0, double* P, double* s1, double* s2, long long* total) {
+    k_lda_docs<<<cdiv_l(D * 32, kThreads), kThreads, 0, st>>>(k, D, doc_ptr, word, count, W, alpha0, P, s1, s2, total);
+    count_launch();
+}
+void launch_lda_vocab(cudaStream_t st, int k, int V, const long long* cptr, const long long* cdoc, const int* ccount,
+                      const double* P, const double* s1, const long long* total, double* coeff1, double* sumwn,
+                      double* m1_partial) {
+    k_lda_vocab<<<cdiv_l((long long)V * 32, kThreads), kThreads, 0, st>>>(k, V, cptr, cdoc, ccount, P, s1, total,
+                                                                        coeff1, sumwn, m1_partial);
+    count_launch();
+}
+void launch_lda_q(cudaStream_t st, int k, int V, const double* W, const double* m1_partial, double inv_used1,
+                  double* q) {
+    k_lda_q<<<k, kThreads, 0, st>>>(k, V, W, m1_partial, inv_used1, q);
+    count_launch();
+}
+
+#define SKC_LOGN_SWITCH_L(logN, X) \
+    switch (logN) {                \
+        case 1: X(1); break;       \
+        case 2: X(2); break;       \
+        case 3: X(3); break;       \
+        case 4: X(4); break;       \
+        case 5: X(5); break;       \
+        case 6: X(6); break;       \
+        case 7: X(7); break;       \
+        case 8: X(8); break;       \
+        case 9: X(9); break;       \
+        case 10: X(10); break;     \
+        case 11: X(11); break;     \
+        case 12: X(12); break;     \
+        default: break;            \
+    }
+
+void launch_lda_accumulate(cudaStream_t st, const SymView& v, long long Dn, const double* P, const double* s1,
+                           const double* s2, int V, const double* W, const double* coeff1, const double* sumwn,
+                           int chunks, double* acc, double* cross) {
+    const size_t smem = sizeof(double2) * (2 * padded_len(v.N) + 2 * v.N);
+    const unsigned grid = (unsigned)((long long)chunks * v.B * v.S);
+#define L_(LG)                                                                                                    \
+    {                                                                                                             \
+        cudaFuncSetAttribute(k_lda_accumulate<LG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
+        k_lda_accumulate<LG><<<grid, kThreads, smem, st>>>(v, Dn, P, s1, s2, V, W, coeff1, sumwn, chunks, acc, cross); \
+    }
+    SKC_LOGN_SWITCH_L(v.logN, L_)
+#undef L_
+    count_launch();
+    count_transforms((std::uint64_t)(Dn + 2ll * V) * v.B * v.S, v.S);
+}
+void launch_lda_finish(cudaStream_t st, const SymView& v, const double* acc, const double* cross, int chunks,
+                       const double* q, double inv_docs, double m1_coeff, double2* tmp) {
+    const size_t smem = sizeof(double2) * padded_len(v.N);
+#define L_(LG)                                                                                               \
+    {                                                                                                        \
+        cudaFuncSetAttribute(k_lda_finish<LG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
+        k_lda_finish<LG><<<v.B * v.S, kThreads, smem, st>>>(v, acc, cross, chunks, q, inv_docs, m1_coeff, tmp); \
+    }
+    SKC_LOGN_SWITCH_L(v.logN, L_)
+#undef L_
+    count_launch();
+    count_transforms((std::uint64_t)v.B * v.S * 2, v.S);
+}
+
+}  // namespace skc

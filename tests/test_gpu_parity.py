@@ -361,3 +361,49 @@ def test_launches_are_counted(gpu_ctx):
     s = skb().SymTensorSketchSet(8, 64, 2, 1, gpu_ctx)
     s.accumulate_dense(sym_tensor(8, 1), True)
     assert skb().kernel_launch_count() > before
+
+
+# ---------------------------------------------------------------- LDA whitened moment (a26)
+@pytest.mark.parametrize("alpha0", [1.0, 0.5])
+def test_lda_sketch_whitened_m3_matches_oracle(gpu_ctx, alpha0):
+    from lda_fixtures import synthetic_corpus
+
+    V = 80
+    doc_ptr, word, count, W = synthetic_corpus(V=V, k=10, D=300, mean_len=10, seed=5)
+    k = W.shape[1]
+    for b, B in [(256, 4), (16384, 3)]:
+        s = skb().SymTensorSketchSet(k, b, B, 7, gpu_ctx)
+        o = O.SymSet(k, b, B, 7)
+        got = s.sketch_whitened_m3(V, doc_ptr, word, count, W, alpha0)
+        ref = o.sketch_whitened_m3(V, doc_ptr, word, count, W, alpha0)
+        assert got == ref
+        assert rel_per_replicate(s.data(), o.data()) <= SKETCH_TOL
+        assert s.version() == B
+
+
+def test_lda_rejects_short_corpus(gpu_ctx):
+    s = skb().SymTensorSketchSet(4, 64, 2, 1, gpu_ctx)
+    with pytest.raises(skb().NumericalError, match="no documents with >= 3 words"):
+        s.sketch_whitened_m3(5, [0, 1, 2], [0, 1], [1, 2], np.ones((5, 4)), 1.0)
+
+
+# ---------------------------------------------------------------- sym_aux / truncated rank-1 (a16)
+@pytest.mark.parametrize("n,b", [(9, 64), (30, 16384)])
+def test_sym_aux_and_truncated_rank1_match_oracle(gpu_ctx, n, b):
+    u = np.random.default_rng(4).normal(size=n)
+    s = skb().SymTensorSketchSet(n, b, 3, 8, gpu_ctx)
+    o = O.SymSet(n, b, 3, 8)
+    for m in range(3):
+        s1, s2, s3 = s.aux_sketches(m, u)
+        b1, b2, b3, se, _, _ = o.tables(m)
+        r1 = np.zeros(b, complex)
+        r2 = np.zeros(b, complex)
+        r3 = np.zeros(b, complex)
+        for i in range(n):  # sketch.cpp:418-423, direct
+            r1[b1[i]] += (1j ** int(se[i])) * u[i]
+            r2[b2[i]] += (1j ** int(2 * se[i])) * u[i] ** 2
+            r3[b3[i]] += (1j ** int(3 * se[i])) * u[i] ** 3
+        for got, ref in ((s1, r1), (s2, r2), (s3, r3)):
+            assert np.max(np.abs(got - ref)) <= 1e-13 * max(1.0, np.max(np.abs(ref)))
+        tr = s.rank1_truncated(m, u)
+        assert rel_per_replicate(tr, o.rank1_truncated(m, u)) <= SKETCH_TOL

@@ -306,3 +306,21 @@ def test_golden_vectors_reproduce():
     u = np.array(sc["u"])
     assert np.max(np.abs(s.ivv(u) - np.array(sc["ivv"]))) < 1e-13
     assert abs(s.vvv(u) - sc["vvv"]) < 1e-13
+
+
+# ---- lda.cpp:145-226 algebra: the frequency-domain accumulation equals the sketch of
+# the explicit (symmetrised) whitened moment tensor ---------------------------------------
+def test_lda_sketch_whitened_m3_equals_dense_sketch_of_moment():
+    from lda_fixtures import explicit_whitened_m3, synthetic_corpus
+
+    V = 50
+    doc_ptr, word, count, W = synthetic_corpus(V=V, k=6, D=60, mean_len=5, seed=3)
+    k = W.shape[1]
+    for alpha0 in (1.0, 0.0):
+        s = O.SymSet(k, 256, 4, 11)
+        used, skipped = s.sketch_whitened_m3(V, doc_ptr, word, count, W, alpha0)
+        T, u_ref, s_ref = explicit_whitened_m3(V, doc_ptr, word, count, W, alpha0)
+        assert (used, skipped) == (u_ref, s_ref) and skipped > 0
+        d = O.SymSet(k, 256, 4, 11)
+        d.accumulate_dense(T, assume_symmetric=True)
+        assert np.max(np.abs(s.data() - d.data())) <= 1e-10 * np.max(np.abs(d.data()))
