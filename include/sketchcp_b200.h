@@ -207,6 +207,21 @@ int skc_asym_mode_contraction(skc_asym_set* s, int free_mode, const double* X_ho
 int skc_asym_vvv(skc_asym_set* s, const double* U_host, int L, double* out_host);
 int skc_asym_cached_transform(skc_asym_set* s, int m, double* out_host);
 
+/* ---- standalone transforms: fft::forward_inplace / inverse_inplace /
+ * inverse_inplace_unscaled (fft.hpp:15-20, fft.cpp:48-66) on the device of a process-wide
+ * context. x: 2*b doubles (interleaved complex) transformed in place; dir -1 forward,
+ * +1 inverse scaled by 1/b, +2 inverse unscaled. b must be a power of two. */
+int skc_fft(double* x_host, size_t b, int dir);
+
+/* ---- sketch file container (sketch.cpp:47-141, 264-296, 379-410, 445-449) ------ */
+/* save/load and peek_sketch_mode; little-endian, magic SKCPSKT\0, version 1. Loading
+ * rebuilds the tables from the stored coefficients; errors are SKC_FORMAT_ERROR. */
+int skc_peek_sketch_mode(const char* path, int* mode /* 0 asym, 1 sym */);
+int skc_sym_save(const skc_sym_set* s, const char* path);
+int skc_sym_load(skc_context* ctx, const char* path, skc_sym_set** out);
+int skc_asym_save(const skc_asym_set* s, const char* path);
+int skc_asym_load(skc_context* ctx, const char* path, skc_asym_set** out);
+
 /* ---- synthetic inputs for the benchmark configs (host generators) ---------- */
 /* Planted symmetric tensor T = sum_r lambda_r v_r^(x)3 + sigma*E (BASELINE configs 0-2):
  * lambda_r ~ U[1,2], V = Q of a Gram-Schmidt QR of an n x rank N(0,1) matrix, E

@@ -40,6 +40,8 @@ __all__ = [
     "unit_sphere",
     "power_inits",
     "gen_planted_tensor",
+    "fft",
+    "peek_sketch_mode",
     "kernel_launch_count",
     "transform_count",
     "NumericalError",
@@ -88,6 +90,44 @@ def kernel_launch_count() -> int:
 def transform_count() -> int:
     """Analogue of fft::transform_count() (fft.hpp:25), in length-b transforms."""
     return int(lib.skc_transform_count())
+
+
+class fft:  # noqa: N801 — mirrors namespace sketchcp::fft (fft.hpp:15-26)
+    """In-place complex transforms of power-of-two length on the device."""
+
+    @staticmethod
+    def _run(x, direction):
+        a = np.ascontiguousarray(np.asarray(x, dtype=np.complex128)).copy()
+        check(lib.skc_fft(a.ctypes.data_as(C.POINTER(C.c_double)), a.size, direction))
+        return a
+
+    @staticmethod
+    def forward(x):
+        return fft._run(x, -1)
+
+    @staticmethod
+    def inverse(x):
+        return fft._run(x, 1)
+
+    @staticmethod
+    def inverse_unscaled(x):
+        return fft._run(x, 2)
+
+    @staticmethod
+    def circular_convolve(x, y):
+        """fft.cpp:62-71"""
+        x = np.asarray(x, dtype=np.complex128)
+        y = np.asarray(y, dtype=np.complex128)
+        if x.size != y.size:
+            raise ValueError("circular_convolve: length mismatch")
+        return fft.inverse(fft.forward(x) * fft.forward(y))
+
+
+def peek_sketch_mode(path) -> str:
+    """'sym' or 'asym' (sketch.cpp:445-449)."""
+    m = C.c_int()
+    check(lib.skc_peek_sketch_mode(str(path).encode(), C.byref(m)))
+    return "sym" if m.value == 1 else "asym"
 
 
 def device_count() -> int:
@@ -377,6 +417,21 @@ class SymTensorSketchSet:
     def bump_version(self) -> None:
         check(lib.skc_sym_bump_version(self._h))
 
+    def save(self, path) -> None:
+        """sketch.cpp:379-389"""
+        check(lib.skc_sym_save(self._h, str(path).encode()))
+
+    @classmethod
+    def load(cls, path, ctx: Context | None = None) -> "SymTensorSketchSet":
+        """sketch.cpp:391-410"""
+        ctx = ctx or default_context()
+        h = C.c_void_p()
+        check(lib.skc_sym_load(ctx.handle, str(path).encode(), C.byref(h)))
+        obj = cls.__new__(cls)
+        obj.ctx = ctx
+        obj._h = h
+        return obj
+
 
 class SymContractionWorkspace:
     """contraction.hpp:14-41. Calls accept one n-vector or an (L, n) batch."""
@@ -593,6 +648,21 @@ class AsymTensorSketchSet:
 
     def bump_version(self) -> None:
         check(lib.skc_asym_bump_version(self._h))
+
+    def save(self, path) -> None:
+        """sketch.cpp:264-274"""
+        check(lib.skc_asym_save(self._h, str(path).encode()))
+
+    @classmethod
+    def load(cls, path, ctx: Context | None = None) -> "AsymTensorSketchSet":
+        """sketch.cpp:276-296"""
+        ctx = ctx or default_context()
+        h = C.c_void_p()
+        check(lib.skc_asym_load(ctx.handle, str(path).encode(), C.byref(h)))
+        obj = cls.__new__(cls)
+        obj.ctx = ctx
+        obj._h = h
+        return obj
 
 
 class AsymContractionWorkspace:

@@ -98,6 +98,12 @@ SIGNATURES = {
     "skc_asym_mode_contraction": (c_int, [p_void, c_int, p_double, p_double, c_int, p_double]),
     "skc_asym_vvv": (c_int, [p_void, p_double, c_int, p_double]),
     "skc_asym_cached_transform": (c_int, [p_void, c_int, p_double]),
+    "skc_fft": (c_int, [p_double, c_size, c_int]),
+    "skc_peek_sketch_mode": (c_int, [C.c_char_p, p_int]),
+    "skc_sym_save": (c_int, [p_void, C.c_char_p]),
+    "skc_sym_load": (c_int, [p_void, C.c_char_p, pp_void]),
+    "skc_asym_save": (c_int, [p_void, C.c_char_p]),
+    "skc_asym_load": (c_int, [p_void, C.c_char_p, pp_void]),
     "skc_gen_planted_tensor": (c_int, [c_int, c_int, c_double, c_u64, c_int, p_void, p_double, p_double]),
     "skc_gen_planted_tensor_device": (
         c_int,

@@ -14,6 +14,7 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <fstream>
 #include <tuple>
 #include <vector>
 
@@ -1588,6 +1589,242 @@ int skc_asym_cached_transform(skc_asym_set* s, int m, double* out_host) {
         s->ctx->use();
         s->ensure_fresh();
         spectrum_to_host(s->ctx, s->spec.p, m, s->b, s->N, s->logN, s->S, out_host);
+    });
+}
+
+// ---- standalone transforms: fft::* (fft.hpp:15-26) on the device -------------------------
+static skc_context* process_context() {
+    static std::mutex mu;
+    static skc_context* ctx = nullptr;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!ctx) {
+        skc_context* c = nullptr;
+        const int st = skc_context_create(0, &c);
+        if (st != kOk) fail(st, g_last_error);
+        ctx = c;
+    }
+    return ctx;
+}
+
+// dir: -1 forward (unnormalised, e^{-2 pi i}), +1 inverse scaled by 1/b, +2 inverse unscaled.
+static void device_fft(skc_context* ctx, double* x, std::size_t b, int dir) {
+    if (!is_pow2(b))  // fft.cpp:40-44
+        fail(kInvalidArgument, "fft: length must be a power of two, got " + std::to_string(b));
+    require(b <= (1u << 28), "fft: length above 2^28 is not supported");
+    require(dir == -1 || dir == 1 || dir == 2, "fft: direction must be -1, +1 or +2");
+    ctx->use();
+    const cudaStream_t st = ctx->stream;
+    const std::uint32_t bb = static_cast<std::uint32_t>(b);
+    if (bb == 1) return;  // length-1 transform is the identity
+    const int N = local_length(bb), logN = ilog2(static_cast<unsigned>(N)), S = static_cast<int>(bb / N);
+    const int logb = ilog2(bb);
+    DevBuf<double2> in, out;
+    in.alloc(b);
+    out.alloc(b);
+    if (dir == -1) {
+        in.upload(reinterpret_cast<const double2*>(x), b, st);
+        launch_spectrum(st, in.p, bb, logb, 1, N, logN, S, ctx->tw(bb), ctx->twl(N), out.p);
+        ctx->check_launch();
+        spectrum_to_host(ctx, out.p, 0, bb, N, logN, S, x);
+    } else {
+        std::vector<double2> lay(b);
+        for (int r = 0; r < S; ++r)
+            for (int j = 0; j < N; ++j) {
+                const std::size_t f = static_cast<std::size_t>(r) + static_cast<std::size_t>(S) * bitrev(j, logN);
+                lay[static_cast<std::size_t>(r) * N + j] = double2{x[2 * f], x[2 * f + 1]};
+            }
+        in.upload(lay.data(), b, st);
+        launch_freq_reduce_inverse(st, reinterpret_cast<const double*>(in.p), 1, 1, S, N, logN, bb, logb, ctx->twl(N),
+                                   out.p);
+        launch_combine_residues(st, out.p, 1, S, N, bb, ctx->tw(bb), 1.0, -1, true, in.p, dir == 1);
+        ctx->check_launch();
+        CK(cudaMemcpyAsync(x, in.p, b * sizeof(double2), cudaMemcpyDeviceToHost, st));
+        ctx->sync();
+    }
+}
+
+int skc_fft(double* x_host, size_t b, int dir) {
+    return guard([&] {
+        check_vec(x_host, "fft: x");
+        device_fft(process_context(), x_host, b, dir);
+    });
+}
+
+// ---- sketch file container (sketch.cpp:47-141, 264-296, 379-410, 445-449) -----------------
+// little-endian: magic "SKCPSKT\0", u64 version 1, mode (0 asym, 1 sym), n, b, B, seed; then
+// per replicate the hash coefficient lists (count + values) and the complex data.
+namespace {
+const char kMagic[8] = {'S', 'K', 'C', 'P', 'S', 'K', 'T', '\0'};
+void put_u64(std::ostream& os, std::uint64_t v) {
+    unsigned char buf[8];
+    for (int i = 0; i < 8; ++i) buf[i] = static_cast<unsigned char>(v >> (8 * i));
+    os.write(reinterpret_cast<const char*>(buf), 8);
+}
+std::uint64_t get_u64(std::istream& is) {
+    unsigned char buf[8];
+    is.read(reinterpret_cast<char*>(buf), 8);
+    if (!is) fail(kFormatError, "sketch file: truncated");
+    std::uint64_t v = 0;
+    for (int i = 0; i < 8; ++i) v |= static_cast<std::uint64_t>(buf[i]) << (8 * i);
+    return v;
+}
+void put_coeffs(std::ostream& os, const std::uint64_t* c, int k) {
+    put_u64(os, static_cast<std::uint64_t>(k));
+    for (int d = 0; d < k; ++d) put_u64(os, c[d]);
+}
+void get_coeffs(std::istream& is, int expect, std::uint64_t* out) {
+    const std::uint64_t cnt = get_u64(is);
+    if (cnt == 0 || cnt > 16) fail(kFormatError, "sketch file: bad hash coefficient count");
+    if (cnt != static_cast<std::uint64_t>(expect))
+        fail(kFormatError, "sketch file: unexpected hash independence for this sketch kind");
+    for (std::uint64_t d = 0; d < cnt; ++d) {
+        out[d] = get_u64(is);
+        if (out[d] >= kHashPrime) fail(kInvalidArgument, "PolyHash: coefficient out of range");
+    }
+}
+void put_data(std::ostream& os, const std::vector<double>& d) {
+    for (double x : d) {
+        std::uint64_t bits;
+        std::memcpy(&bits, &x, 8);
+        put_u64(os, bits);
+    }
+}
+void get_data(std::istream& is, std::vector<double>& d) {
+    for (double& x : d) {
+        const std::uint64_t bits = get_u64(is);
+        std::memcpy(&x, &bits, 8);
+    }
+}
+struct FileHeader {
+    std::uint64_t mode, n, b, B, seed;
+};
+FileHeader read_header(std::istream& is) {
+    char magic[8];
+    is.read(magic, 8);
+    if (!is || std::memcmp(magic, kMagic, 8) != 0) fail(kFormatError, "sketch file: bad magic");
+    if (get_u64(is) != 1) fail(kFormatError, "sketch file: unsupported version");
+    FileHeader h;
+    h.mode = get_u64(is);
+    if (h.mode > 1) fail(kFormatError, "sketch file: unknown mode");
+    h.n = get_u64(is);
+    h.b = get_u64(is);
+    h.B = get_u64(is);
+    h.seed = get_u64(is);
+    if (h.n == 0 || h.B == 0 || !is_pow2(h.b)) fail(kFormatError, "sketch file: invalid header");
+    return h;
+}
+void write_header(std::ostream& os, std::uint64_t mode, std::uint64_t n, std::uint64_t b, std::uint64_t B,
+                  std::uint64_t seed) {
+    os.write(kMagic, 8);
+    put_u64(os, 1);
+    put_u64(os, mode);
+    put_u64(os, n);
+    put_u64(os, b);
+    put_u64(os, B);
+    put_u64(os, seed);
+}
+}  // namespace
+
+int skc_peek_sketch_mode(const char* path, int* mode) {
+    return guard([&] {
+        check_vec(path, "path");
+        std::ifstream is(path, std::ios::binary);
+        if (!is) fail(kFormatError, std::string("cannot open sketch file: ") + path);
+        *mode = static_cast<int>(read_header(is).mode);
+    });
+}
+
+int skc_sym_save(const skc_sym_set* s, const char* path) {
+    return guard([&] {
+        check_vec(s, "set");
+        check_vec(path, "path");
+        std::vector<double> data(static_cast<size_t>(s->B) * s->b * 2);
+        s->ctx->use();
+        CK(cudaMemcpyAsync(data.data(), s->data.p, data.size() * 8, cudaMemcpyDeviceToHost, s->ctx->stream));
+        s->ctx->sync();
+        std::ofstream os(path, std::ios::binary);
+        if (!os) fail(kFormatError, std::string("cannot write sketch file: ") + path);
+        write_header(os, 1, s->n, s->b, s->B, s->seed);
+        std::vector<double> rep(2 * static_cast<size_t>(s->b));
+        for (int m = 0; m < s->B; ++m) {
+            put_coeffs(os, &s->hcoef[m * 6], 6);
+            put_coeffs(os, &s->scoef[m * 6], 6);
+            std::copy(data.begin() + static_cast<long>(m) * 2 * s->b, data.begin() + static_cast<long>(m + 1) * 2 * s->b,
+                      rep.begin());
+            put_data(os, rep);
+        }
+        if (!os) fail(kFormatError, std::string("write failure on sketch file: ") + path);
+    });
+}
+
+int skc_sym_load(skc_context* ctx, const char* path, skc_sym_set** out) {
+    return guard([&] {
+        check_vec(ctx, "context");
+        check_vec(path, "path");
+        std::ifstream is(path, std::ios::binary);
+        if (!is) fail(kFormatError, std::string("cannot open sketch file: ") + path);
+        const FileHeader h = read_header(is);
+        if (h.mode != 1) fail(kFormatError, std::string(path) + ": not a symmetric sketch file");
+        require(h.n <= 0x7fffffffull && h.B <= 0x7fffffffull && h.b <= (1ull << 28), "sketch file: dimensions too large");
+        const int n = static_cast<int>(h.n), B = static_cast<int>(h.B);
+        const std::uint32_t b = static_cast<std::uint32_t>(h.b);
+        std::vector<std::uint64_t> hc(static_cast<size_t>(B) * 6), sc(static_cast<size_t>(B) * 6);
+        std::vector<double> data(static_cast<size_t>(B) * b * 2), rep(2 * static_cast<size_t>(b));
+        for (int m = 0; m < B; ++m) {
+            get_coeffs(is, 6, &hc[m * 6]);
+            get_coeffs(is, 6, &sc[m * 6]);
+            get_data(is, rep);
+            std::copy(rep.begin(), rep.end(), data.begin() + static_cast<long>(m) * 2 * b);
+        }
+        const int st = skc_sym_create_from_coefficients(ctx, n, b, B, h.seed, hc.data(), sc.data(), data.data(), out);
+        if (st != kOk) fail(st, g_last_error);
+    });
+}
+
+int skc_asym_save(const skc_asym_set* s, const char* path) {
+    return guard([&] {
+        check_vec(s, "set");
+        check_vec(path, "path");
+        std::vector<double> data(static_cast<size_t>(s->B) * s->b * 2);
+        s->ctx->use();
+        CK(cudaMemcpyAsync(data.data(), s->data.p, data.size() * 8, cudaMemcpyDeviceToHost, s->ctx->stream));
+        s->ctx->sync();
+        std::ofstream os(path, std::ios::binary);
+        if (!os) fail(kFormatError, std::string("cannot write sketch file: ") + path);
+        write_header(os, 0, s->n, s->b, s->B, s->seed);
+        std::vector<double> rep(2 * static_cast<size_t>(s->b));
+        for (int m = 0; m < s->B; ++m) {
+            for (int sl = 0; sl < 3; ++sl) put_coeffs(os, &s->hcoef[(m * 3 + sl) * 2], 2);
+            for (int sl = 0; sl < 3; ++sl) put_coeffs(os, &s->xcoef[(m * 3 + sl) * 6], 6);
+            std::copy(data.begin() + static_cast<long>(m) * 2 * s->b, data.begin() + static_cast<long>(m + 1) * 2 * s->b,
+                      rep.begin());
+            put_data(os, rep);
+        }
+        if (!os) fail(kFormatError, std::string("write failure on sketch file: ") + path);
+    });
+}
+
+int skc_asym_load(skc_context* ctx, const char* path, skc_asym_set** out) {
+    return guard([&] {
+        check_vec(ctx, "context");
+        check_vec(path, "path");
+        std::ifstream is(path, std::ios::binary);
+        if (!is) fail(kFormatError, std::string("cannot open sketch file: ") + path);
+        const FileHeader h = read_header(is);
+        if (h.mode != 0) fail(kFormatError, std::string(path) + ": not an asymmetric sketch file");
+        require(h.n <= 0x7fffffffull && h.B <= 0x7fffffffull && h.b <= (1ull << 28), "sketch file: dimensions too large");
+        const int n = static_cast<int>(h.n), B = static_cast<int>(h.B);
+        const std::uint32_t b = static_cast<std::uint32_t>(h.b);
+        std::vector<std::uint64_t> hc(static_cast<size_t>(B) * 6), xc(static_cast<size_t>(B) * 18);
+        std::vector<double> data(static_cast<size_t>(B) * b * 2), rep(2 * static_cast<size_t>(b));
+        for (int m = 0; m < B; ++m) {
+            for (int sl = 0; sl < 3; ++sl) get_coeffs(is, 2, &hc[(m * 3 + sl) * 2]);
+            for (int sl = 0; sl < 3; ++sl) get_coeffs(is, 6, &xc[(m * 3 + sl) * 6]);
+            get_data(is, rep);
+            std::copy(rep.begin(), rep.end(), data.begin() + static_cast<long>(m) * 2 * b);
+        }
+        const int st = skc_asym_create_from_coefficients(ctx, n, b, B, h.seed, hc.data(), xc.data(), data.data(), out);
+        if (st != kOk) fail(st, g_last_error);
     });
 }
 

@@ -214,13 +214,15 @@ SKC_HD void dit_pass_dispatch(int logr, double2* x, int w, int h, const double2*
     }
 }
 
-// ---- compile-time pass plans (same decomposition as make_plan) -------------------------
-constexpr int plan_first(int logN) { return (logN % 4) ? (logN % 4) : 4; }
-constexpr int plan_npass(int logN) { return logN == 0 ? 0 : 1 + (logN - plan_first(logN)) / 4; }
-constexpr int plan_logr(int logN, int p) { return p == 0 ? plan_first(logN) : 4; }
-constexpr int plan_h(int logN, int p) {
+// ---- compile-time pass plans ----------------------------------------------------------
+// Max radix 2^LR per pass (LR = 4: radix-16, the make_plan decomposition; LR = 3:
+// radix-8, fewer registers per thread at the cost of one more pass over shared memory).
+constexpr int plan_first(int logN, int LR = 4) { return (logN % LR) ? (logN % LR) : LR; }
+constexpr int plan_npass(int logN, int LR = 4) { return logN == 0 ? 0 : 1 + (logN - plan_first(logN, LR)) / LR; }
+constexpr int plan_logr(int logN, int p, int LR = 4) { return p == 0 ? plan_first(logN, LR) : LR; }
+constexpr int plan_h(int logN, int p, int LR = 4) {
     int h = (1 << logN) >> 1;
-    for (int q = 0; q < p; ++q) h >>= plan_logr(logN, q);
+    for (int q = 0; q < p; ++q) h >>= plan_logr(logN, q, LR);
     return h;
 }
 
@@ -228,52 +230,52 @@ constexpr int plan_h(int logN, int p) {
 // Forward DIF over `na` back-to-back padded arrays of length 2^LOGN. `twl` is the local
 // table w_N^k (k < N): stage twiddles are twl[pos << (LOGN - log2(2 hs))], contiguous,
 // so a CTA's whole twiddle working set is N*16 bytes.
-template <int LOGN, int P, int NP = plan_npass(LOGN)>
+template <int LOGN, int LR, int P, int NP = plan_npass(LOGN, LR)>
 struct DifPasses {
     __device__ __forceinline__ static void run(double2* sm, int na, const double2* twl) {
-        constexpr int LR = plan_logr(LOGN, P);
-        constexpr int H = plan_h(LOGN, P);
-        constexpr int items = (1 << LOGN) >> LR;
+        constexpr int R_ = plan_logr(LOGN, P, LR);
+        constexpr int H = plan_h(LOGN, P, LR);
+        constexpr int items = (1 << LOGN) >> R_;
         constexpr int stride = (1 << LOGN) + ((1 << LOGN) >> 4) + 1;
         for (int w = threadIdx.x; w < na * items; w += blockDim.x) {
             const int a = w / items;
-            dif_pass_item<LR>(sm + a * stride, w - a * items, H, twl, LOGN);
+            dif_pass_item<R_>(sm + a * stride, w - a * items, H, twl, LOGN);
         }
         __syncthreads();
-        DifPasses<LOGN, P + 1, NP>::run(sm, na, twl);
+        DifPasses<LOGN, LR, P + 1, NP>::run(sm, na, twl);
     }
 };
-template <int LOGN, int NP>
-struct DifPasses<LOGN, NP, NP> {
+template <int LOGN, int LR, int NP>
+struct DifPasses<LOGN, LR, NP, NP> {
     __device__ __forceinline__ static void run(double2*, int, const double2*) {}
 };
 // Mirror inverse (DIT, unscaled), passes in reverse order.
-template <int LOGN, int P>
+template <int LOGN, int LR, int P>
 struct DitPasses {
     __device__ __forceinline__ static void run(double2* sm, int na, const double2* twl) {
-        constexpr int LR = plan_logr(LOGN, P);
-        constexpr int H = plan_h(LOGN, P);
-        constexpr int items = (1 << LOGN) >> LR;
+        constexpr int R_ = plan_logr(LOGN, P, LR);
+        constexpr int H = plan_h(LOGN, P, LR);
+        constexpr int items = (1 << LOGN) >> R_;
         constexpr int stride = (1 << LOGN) + ((1 << LOGN) >> 4) + 1;
         for (int w = threadIdx.x; w < na * items; w += blockDim.x) {
             const int a = w / items;
-            dit_pass_item<LR>(sm + a * stride, w - a * items, H, twl, LOGN);
+            dit_pass_item<R_>(sm + a * stride, w - a * items, H, twl, LOGN);
         }
         __syncthreads();
-        DitPasses<LOGN, P - 1>::run(sm, na, twl);
+        DitPasses<LOGN, LR, P - 1>::run(sm, na, twl);
     }
 };
-template <int LOGN>
-struct DitPasses<LOGN, -1> {
+template <int LOGN, int LR>
+struct DitPasses<LOGN, LR, -1> {
     __device__ __forceinline__ static void run(double2*, int, const double2*) {}
 };
-template <int LOGN>
+template <int LOGN, int LR = 4>
 __device__ __forceinline__ void dif_local(double2* sm, int na, const double2* twl) {
-    DifPasses<LOGN, 0>::run(sm, na, twl);
+    DifPasses<LOGN, LR, 0>::run(sm, na, twl);
 }
-template <int LOGN>
+template <int LOGN, int LR = 4>
 __device__ __forceinline__ void dit_local(double2* sm, int na, const double2* twl) {
-    DitPasses<LOGN, plan_npass(LOGN) - 1>::run(sm, na, twl);
+    DitPasses<LOGN, LR, plan_npass(LOGN, LR) - 1>::run(sm, na, twl);
 }
 #endif
 

@@ -120,7 +120,8 @@ void launch_sym_moment_accumulate(cudaStream_t st, const SymView& v, const doubl
 void launch_freq_reduce_inverse(cudaStream_t st, const double* acc, int chunks, int B, int S, int N, int logN,
                                 std::uint32_t b, int logb, const double2* twl, double2* tmp);
 void launch_combine_residues(cudaStream_t st, const double2* tmp, int B, int S, int N, std::uint32_t b,
-                             const double2* tw, double alpha, int m_only, bool overwrite, double2* dst);
+                             const double2* tw, double alpha, int m_only, bool overwrite, double2* dst,
+                             bool scaled = true);
 void launch_asym_factored_accumulate(cudaStream_t st, const AsymView& v, const double* a, const double* U,
                                      const double* V, const double* W, long long Ncomp, int chunks, int m_only,
                                      double* acc);

@@ -15,6 +15,8 @@
 
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
+#include <string>
 
 #include "skc_fft.cuh"
 #include "skc_host.hpp"
@@ -188,6 +190,64 @@ __device__ __forceinline__ void scatter_plan(double2* y, const uint2* __restrict
     }
 }
 
+// Two-phase deterministic scatter of up to two count sketches at once (latency-tolerant):
+// phase 1 computes every contribution val(i) w_b^{-r t} independently into shared
+// scratch (all loads in flight), phase 2 lets each run head sum its run in plan order.
+// scratch: 2*n double2 + 2*n keys; n <= kScatterMax.
+constexpr int kScatterMax = 1024;
+template <typename ValA, typename ValB>
+__device__ __forceinline__ void scatter2(double2* yA, const uint2* __restrict__ planA, ValA valA, double2* yB,
+                                         const uint2* __restrict__ planB, ValB valB, int n, int N, int r,
+                                         std::uint32_t bmask, std::uint32_t tmask, const double2* __restrict__ tw,
+                                         double2* scr, std::uint32_t* keys) {
+    const std::uint32_t nmask = static_cast<std::uint32_t>(N - 1);
+    const int tot = yB ? 2 * n : n;
+    for (int x = threadIdx.x; x < tot; x += blockDim.x) {
+        const bool b = x >= n;
+        const uint2 e = b ? planB[x - n] : planA[x];
+        const double2 v = b ? valB(e.x, e.y) : valA(e.x, e.y);
+        const std::uint32_t t = e.y & tmask;
+        scr[x] = cmul(v, conj(tw[(static_cast<std::uint32_t>(r) * t) & bmask]));
+        keys[x] = e.y & nmask;
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < tot; x += blockDim.x) {
+        const int lo = (x >= n) ? n : 0;
+        const std::uint32_t key = keys[x];
+        if (x > lo && keys[x - 1] == key) continue;
+        double2 acc = scr[x];
+        for (int x2 = x + 1; x2 < lo + n && keys[x2] == key; ++x2) acc = cadd(acc, scr[x2]);
+        ((x >= n) ? yB : yA)[pad16(static_cast<int>(key))] = acc;
+    }
+}
+
+// Scratch-free variant: every thread computes its own contribution with independent
+// loads; a run head writes it (plus, rarely, its run's followers recomputed in plan
+// order), non-heads write nothing. Deterministic, no extra shared memory or barrier.
+template <typename ValA, typename ValB>
+__device__ __forceinline__ void scatter2_direct(double2* yA, const uint2* __restrict__ planA, ValA valA, double2* yB,
+                                                const uint2* __restrict__ planB, ValB valB, int n, int N, int r,
+                                                std::uint32_t bmask, std::uint32_t tmask, const double2* __restrict__ tw) {
+    const std::uint32_t nmask = static_cast<std::uint32_t>(N - 1);
+    const int tot = yB ? 2 * n : n;
+    for (int x = threadIdx.x; x < tot; x += blockDim.x) {
+        const bool b = x >= n;
+        const int q = b ? x - n : x;
+        const uint2* plan = b ? planB : planA;
+        const uint2 e = plan[q];
+        const std::uint32_t key = e.y & nmask;
+        const bool head = (q == 0) || ((plan[q - 1].y & nmask) != key);
+        double2 acc = cmul(b ? valB(e.x, e.y) : valA(e.x, e.y), conj(tw[(static_cast<std::uint32_t>(r) * (e.y & tmask)) & bmask]));
+        if (!head) continue;
+        for (int q2 = q + 1; q2 < n; ++q2) {
+            const uint2 f = plan[q2];
+            if ((f.y & nmask) != key) break;
+            acc = cadd(acc, cmul(b ? valB(f.x, f.y) : valA(f.x, f.y), conj(tw[(static_cast<std::uint32_t>(r) * (f.y & tmask)) & bmask])));
+        }
+        (b ? yB : yA)[pad16(static_cast<int>(key))] = acc;
+    }
+}
+
 // plan[m][q] = (i, t_i | tag_i << tag_shift) for i = perm[m][q]
 __global__ void k_make_plan(const std::uint32_t* __restrict__ perm, const std::uint32_t* __restrict__ bucket,
                             const std::uint8_t* __restrict__ sexp, int sexp_mult, const std::uint32_t* __restrict__ packed,
@@ -252,10 +312,13 @@ void launch_spectrum(cudaStream_t st, const double2* data, std::uint32_t b, int 
 
 // ============================ K3: symmetric contractions ==========================
 // Ivv: contraction.cpp:128-181. vvv: contraction.cpp:83-126.
-// One CTA per (restart l, replicate m, residue r).
-template <int LOGN>
-__global__ void __launch_bounds__(kFftThreads, SKC_FFT_MINB)
+// One CTA per (restart block, replicate m, residue r): kLPB restarts per CTA share the
+// spectrum slice F_r(T_m) (L1-resident across restarts) and amortise CTA start-up.
+constexpr int kLPB = 4;
+template <int LOGN, int VAR, int LR, int MINB>
+__global__ void __launch_bounds__(kFftThreads, MINB)
     k_sym_contract(SymView v, const double* __restrict__ U, int L, int mode, double* __restrict__ out) {
+    constexpr bool SCR = VAR == 1;
     extern __shared__ double2 sm[];
     __shared__ double red[kFftThreads / 32];
     constexpr int N = 1 << LOGN;
@@ -263,94 +326,132 @@ __global__ void __launch_bounds__(kFftThreads, SKC_FFT_MINB)
     const int S = v.S, n = v.n, B = v.B;
     const int r = blockIdx.x % S;
     const int m = (blockIdx.x / S) % B;
-    const int l = blockIdx.x / (S * B);
+    const int l0 = (blockIdx.x / (S * B)) * kLPB;
     double2* A = sm;
     double2* Bv = sm + stride;
-    const double* u = U + (size_t)l * n;
+    double2* scr = sm + 2 * stride;  // 2n (SCR only)
+    std::uint32_t* keys = reinterpret_cast<std::uint32_t*>(scr + (SCR ? 2 * n : 0));
     const std::uint32_t bmask = v.b - 1;
+    const double2* fT = v.spec + ((size_t)m * S + r) * N;  // re-read per restart (L1/L2 resident)
+    const uint2* p1 = v.plan1 + (size_t)m * n;
+    const uint2* p2 = v.plan2 + (size_t)m * n;
+    const std::uint32_t* b1 = v.bucket1 + (size_t)m * n;
+    const std::uint32_t* b2 = v.bucket2 + (size_t)m * n;
+    const std::uint32_t* b3 = v.bucket3 + (size_t)m * n;
+    const std::uint8_t* se = v.sexp + (size_t)m * n;
+    const double2* dm = v.data + (size_t)m * v.b;
 
-    zero_smem(sm, 2 * stride);
-    __syncthreads();
-    // f1[h_i] += sigma_i u_i ; f2[2h_i] += sigma_i^2 u_i^2   (contraction.cpp:150-154)
-    scatter_plan(A, v.plan1 + (size_t)m * n, n, N, r, bmask, 0x0FFFFFFFu, v.tw,
-                 [&](std::uint32_t i, std::uint32_t y) { return root4_times(y >> 28, u[i]); });
-    scatter_plan(Bv, v.plan2 + (size_t)m * n, n, N, r, bmask, 0x0FFFFFFFu, v.tw, [&](std::uint32_t i, std::uint32_t y) {
-        const double ui = u[i];
-        return root4_times(y >> 28, ui * ui);
-    });
-    __syncthreads();
-    dif_local<LOGN>(sm, 2, v.twl);
-    const double2* fT = v.spec + ((size_t)m * S + r) * N;
-
-    if (mode == 0) {
-        // z1 = fT conj(f1^2 + f2), z2 = fT conj(f1)   (contraction.cpp:158-162)
-        for (int j = threadIdx.x; j < N; j += blockDim.x) {
-            const double2 t = fT[j];
-            const double2 fu = A[pad16(j)];
-            const double2 f2 = Bv[pad16(j)];
-            A[pad16(j)] = cmulc(t, cadd(cmul(fu, fu), f2));
-            Bv[pad16(j)] = cmulc(t, fu);
+    for (int l = l0; l < min(L, l0 + kLPB); ++l) {
+        const double* u = U + (size_t)l * n;
+        zero_smem(sm, 2 * stride);
+        __syncthreads();
+        // f1[h_i] += sigma_i u_i ; f2[2h_i] += sigma_i^2 u_i^2   (contraction.cpp:150-154)
+        auto v1 = [&](std::uint32_t i, std::uint32_t y) { return root4_times(y >> 28, u[i]); };
+        auto v2 = [&](std::uint32_t i, std::uint32_t y) {
+            const double ui = u[i];
+            return root4_times(y >> 28, ui * ui);
+        };
+        if (VAR == 1) {
+            scatter2(A, p1, v1, Bv, p2, v2, n, N, r, bmask, 0x0FFFFFFFu, v.tw, scr, keys);
+        } else if (VAR == 2) {
+            scatter2_direct(A, p1, v1, Bv, p2, v2, n, N, r, bmask, 0x0FFFFFFFu, v.tw);
+        } else {
+            scatter_plan(A, p1, n, N, r, bmask, 0x0FFFFFFFu, v.tw, v1);
+            scatter_plan(Bv, p2, n, N, r, bmask, 0x0FFFFFFFu, v.tw, v2);
         }
         __syncthreads();
-        dit_local<LOGN>(sm, 2, v.twl);
-        const double inv_b = 1.0 / static_cast<double>(v.b);
-        const std::uint32_t nmask = static_cast<std::uint32_t>(N - 1);
-        double* o = out + (((size_t)l * B + m) * S + r) * n;
-        const double2* dm = v.data + (size_t)m * v.b;
-        const std::uint32_t* b1 = v.bucket1 + (size_t)m * n;
-        const std::uint32_t* b2 = v.bucket2 + (size_t)m * n;
-        const std::uint32_t* b3 = v.bucket3 + (size_t)m * n;
-        const std::uint8_t* se = v.sexp + (size_t)m * n;
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            const unsigned e = se[i];
-            const double ui = u[i];
-            const std::uint32_t t1 = b1[i], t2 = b2[i];
-            const double2 z1 = cmul(A[pad16(static_cast<int>(t1 & nmask))], v.tw[(static_cast<std::uint32_t>(r) * t1) & bmask]);
-            const double2 z2 = cmul(Bv[pad16(static_cast<int>(t2 & nmask))], v.tw[(static_cast<std::uint32_t>(r) * t2) & bmask]);
-            double val = re_rot_conj(e, z1) * (1.0 / 6.0) * inv_b;
-            val += ui * re_rot_conj(2u * e, z2) * (1.0 / 3.0) * inv_b;
-            if (r == 0) val += ui * ui * re_rot_conj(3u * e, dm[b3[i]]) * (1.0 / 3.0);
-            o[i] = val;
-        }
-    } else {
-        // acc1 += Re(fT conj(f1)^3), acc2 += Re(fT conj(f1) conj(f2))   (contraction.cpp:111-116)
-        double acc1 = 0.0, acc2 = 0.0;
-        for (int j = threadIdx.x; j < N; j += blockDim.x) {
-            const double2 c1 = conj(A[pad16(j)]);
-            const double2 w1 = cmul(fT[j], c1);
-            acc1 += cmul(cmul(w1, c1), c1).x;
-            acc2 += cmul(w1, conj(Bv[pad16(j)])).x;
-        }
-        const double s1 = block_sum<kFftThreads>(acc1, red);
-        const double s2 = block_sum<kFftThreads>(acc2, red);
-        double term3 = 0.0;
-        if (r == 0) {  // contraction.cpp:117-121
-            const double2* dm = v.data + (size_t)m * v.b;
-            const std::uint32_t* b3 = v.bucket3 + (size_t)m * n;
-            const std::uint8_t* se = v.sexp + (size_t)m * n;
+        dif_local<LOGN, LR>(sm, 2, v.twl);
+
+        if (mode == 0) {
+            // z1 = fT conj(f1^2 + f2), z2 = fT conj(f1)   (contraction.cpp:158-162)
+            for (int j = threadIdx.x; j < N; j += blockDim.x) {
+                const double2 t = fT[j];
+                const double2 fu = A[pad16(j)];
+                const double2 f2 = Bv[pad16(j)];
+                A[pad16(j)] = cmulc(t, cadd(cmul(fu, fu), f2));
+                Bv[pad16(j)] = cmulc(t, fu);
+            }
+            __syncthreads();
+            dit_local<LOGN, LR>(sm, 2, v.twl);
+            const double inv_b = 1.0 / static_cast<double>(v.b);
+            const std::uint32_t nmask = static_cast<std::uint32_t>(N - 1);
+            double* o = out + (((size_t)l * B + m) * S + r) * n;
             for (int i = threadIdx.x; i < n; i += blockDim.x) {
-                const double u3 = u[i] * u[i] * u[i];
-                term3 += u3 * re_rot_conj(3u * se[i], dm[b3[i]]);
+                const unsigned e = se[i];
+                const double ui = u[i];
+                const std::uint32_t t1 = b1[i], t2 = b2[i];
+                const double2 z1 = cmul(A[pad16(static_cast<int>(t1 & nmask))], v.tw[(static_cast<std::uint32_t>(r) * t1) & bmask]);
+                const double2 z2 = cmul(Bv[pad16(static_cast<int>(t2 & nmask))], v.tw[(static_cast<std::uint32_t>(r) * t2) & bmask]);
+                double val = re_rot_conj(e, z1) * (1.0 / 6.0) * inv_b;
+                val += ui * re_rot_conj(2u * e, z2) * (1.0 / 3.0) * inv_b;
+                if (r == 0) val += ui * ui * re_rot_conj(3u * e, dm[b3[i]]) * (1.0 / 3.0);
+                o[i] = val;
+            }
+        } else {
+            // acc1 += Re(fT conj(f1)^3), acc2 += Re(fT conj(f1) conj(f2))   (contraction.cpp:111-116)
+            double acc1 = 0.0, acc2 = 0.0;
+            for (int j = threadIdx.x; j < N; j += blockDim.x) {
+                const double2 c1 = conj(A[pad16(j)]);
+                const double2 w1 = cmul(fT[j], c1);
+                acc1 += cmul(cmul(w1, c1), c1).x;
+                acc2 += cmul(w1, conj(Bv[pad16(j)])).x;
+            }
+            const double s1 = block_sum<kFftThreads>(acc1, red);
+            const double s2 = block_sum<kFftThreads>(acc2, red);
+            double term3 = 0.0;
+            if (r == 0) {  // contraction.cpp:117-121
+                for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                    const double u3 = u[i] * u[i] * u[i];
+                    term3 += u3 * re_rot_conj(3u * se[i], dm[b3[i]]);
+                }
+            }
+            const double s3 = block_sum<kFftThreads>(term3, red);
+            if (threadIdx.x == 0) {
+                double* o = out + (((size_t)l * B + m) * S + r) * 3;
+                o[0] = s1;
+                o[1] = s2;
+                o[2] = s3;
             }
         }
-        const double s3 = block_sum<kFftThreads>(term3, red);
-        if (threadIdx.x == 0) {
-            double* o = out + (((size_t)l * B + m) * S + r) * 3;
-            o[0] = s1;
-            o[1] = s2;
-            o[2] = s3;
-        }
+        __syncthreads();
     }
 }
 
+// Variant selection (A/B measured on B200, see profiles/): SKC_CONTRACT_VARIANT =
+//   "16s" radix-16 + scratch scatter (2 CTAs/SM), "16d" radix-16 + direct scatter,
+//   "8d" radix-8 + direct scatter (3 CTAs/SM).
+static int contract_variant() {
+    static int v = [] {
+        const char* e = std::getenv("SKC_CONTRACT_VARIANT");
+        if (!e) return 0;
+        std::string s(e);
+        return s == "16s" ? 0 : s == "16d" ? 1 : s == "8d" ? 2 : 0;
+    }();
+    return v;
+}
+
+template <int LG, int VAR, int LR, int MINB>
+static void sym_contract_launch(cudaStream_t st, const SymView& v, const double* U, int L, int mode, double* out,
+                                unsigned grid, size_t smem) {
+    cudaFuncSetAttribute(k_sym_contract<LG, VAR, LR, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_sym_contract<LG, VAR, LR, MINB><<<grid, kFftThreads, smem, st>>>(v, U, L, mode, out);
+}
+
 void launch_sym_contract(cudaStream_t st, const SymView& v, const double* U, int L, int mode, double* out) {
-    const size_t smem = sizeof(double2) * 2 * padded_len(v.N);
-    const unsigned grid = (unsigned)((long long)L * v.B * v.S);
-#define L_(LG)                                                                                                  \
-    {                                                                                                           \
-        if (smem > 48 * 1024)                                                                                   \
-            cudaFuncSetAttribute(k_sym_contract<LG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
-        k_sym_contract<LG><<<grid, kFftThreads, smem, st>>>(v, U, L, mode, out);                                \
+    const bool scr_ok = v.n <= kScatterMax;
+    int var = contract_variant();
+    if (var == 0 && !scr_ok) var = 1;
+    const size_t smem = sizeof(double2) * 2 * padded_len(v.N) +
+                        (var == 0 ? (sizeof(double2) + sizeof(std::uint32_t)) * 2 * (size_t)v.n : 0);
+    const unsigned grid = (unsigned)((long long)((L + kLPB - 1) / kLPB) * v.B * v.S);
+#define L_(LG)                                                                                         \
+    {                                                                                                  \
+        if (var == 0)                                                                                  \
+            sym_contract_launch<LG, 1, 4, 2>(st, v, U, L, mode, out, grid, smem);                      \
+        else if (var == 1)                                                                             \
+            sym_contract_launch<LG, 2, 4, 2>(st, v, U, L, mode, out, grid, smem);                      \
+        else                                                                                           \
+            sym_contract_launch<LG, 2, 3, 3>(st, v, U, L, mode, out, grid, smem);                      \
     }
     SKC_LOGN_SWITCH(v.logN, L_)
 #undef L_
@@ -579,7 +680,7 @@ void launch_freq_reduce_inverse(cudaStream_t st, const double* acc, int chunks, 
 // dst[m][t] (+)= alpha * (1/b) * sum_r w_b^{r t} tmp[m][r][t mod N]
 // (inverse_inplace scaling, fft.cpp:62-66; data += alpha*su, sketch.cpp:359).
 __global__ void k_combine_residues(const double2* __restrict__ tmp, int B, int S, int N, std::uint32_t b,
-                                   const double2* __restrict__ tw, double alpha, int m_only, int overwrite,
+                                   const double2* __restrict__ tw, double alpha, int m_only, int overwrite, int scaled,
                                    double2* __restrict__ dst) {
     long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     const int Bm = (m_only >= 0) ? 1 : B;
@@ -593,7 +694,7 @@ __global__ void k_combine_residues(const double2* __restrict__ tmp, int B, int S
     for (int r = 0; r < S; ++r)
         s = cadd(s, cmul(tm[(size_t)r * N + (t & nmask)], tw[(static_cast<std::uint32_t>(r) * t) & bmask]));
     const double inv_b = 1.0 / static_cast<double>(b);
-    const double2 su = cscale(s, inv_b);
+    const double2 su = scaled ? cscale(s, inv_b) : s;
     double2* d = dst + idx;
     if (overwrite)
         *d = cscale(su, alpha);
@@ -601,9 +702,10 @@ __global__ void k_combine_residues(const double2* __restrict__ tmp, int B, int S
         *d = cadd(*d, cscale(su, alpha));
 }
 void launch_combine_residues(cudaStream_t st, const double2* tmp, int B, int S, int N, std::uint32_t b,
-                             const double2* tw, double alpha, int m_only, bool overwrite, double2* dst) {
+                             const double2* tw, double alpha, int m_only, bool overwrite, double2* dst, bool scaled) {
     long long tot = (long long)((m_only >= 0) ? 1 : B) * b;
-    k_combine_residues<<<cdiv(tot, 256), 256, 0, st>>>(tmp, B, S, N, b, tw, alpha, m_only, overwrite ? 1 : 0, dst);
+    k_combine_residues<<<cdiv(tot, 256), 256, 0, st>>>(tmp, B, S, N, b, tw, alpha, m_only, overwrite ? 1 : 0,
+                                                       scaled ? 1 : 0, dst);
     SKC_LAUNCHED();
 }
 

@@ -407,3 +407,60 @@ def test_sym_aux_and_truncated_rank1_match_oracle(gpu_ctx, n, b):
             assert np.max(np.abs(got - ref)) <= 1e-13 * max(1.0, np.max(np.abs(ref)))
         tr = s.rank1_truncated(m, u)
         assert rel_per_replicate(tr, o.rank1_truncated(m, u)) <= SKETCH_TOL
+
+
+# ---------------------------------------------------------------- fft:: (fft.hpp:15-26) on the device
+@pytest.mark.parametrize("b", [1, 2, 16, 64, 1024, 4096, 16384, 1 << 16])
+def test_device_fft_matches_numpy_and_oracle(gpu_ctx, b):
+    rng = np.random.default_rng(b)
+    x = rng.normal(size=b) + 1j * rng.normal(size=b)
+    F = skb().fft
+    assert np.max(np.abs(F.forward(x) - np.fft.fft(x))) <= 1e-12 * max(1.0, np.max(np.abs(np.fft.fft(x))))
+    assert np.max(np.abs(F.inverse(F.forward(x)) - x)) < 1e-12  # test_fft.cpp:37-46
+    assert np.max(np.abs(F.inverse_unscaled(x) - np.fft.ifft(x) * b)) <= 1e-12 * b
+    if b >= 2:
+        assert np.max(np.abs(F.forward(x) - O.fft(x, -1))) <= 1e-12 * max(1.0, np.max(np.abs(np.fft.fft(x))))
+
+
+def test_device_fft_rejects_non_power_of_two(gpu_ctx):  # test_fft.cpp:77-82
+    with pytest.raises(ValueError, match="power of two"):
+        skb().fft.forward(np.ones(12))
+
+
+def test_device_circular_convolution_worked_examples(gpu_ctx):  # test_fft.cpp:48-75
+    x = np.array([1, 2, 3, 4], dtype=complex)
+    y = np.array([1, 0, 0, 1], dtype=complex)
+    assert np.allclose(skb().fft.circular_convolve(x, y).real, [3, 5, 7, 5], atol=1e-12)
+
+
+# ---------------------------------------------------------------- sketch file container (next row)
+def test_sketch_save_load_round_trip(gpu_ctx, tmp_path):  # SPEC.md:307 bit-exact round trip
+    n, b, B = 11, 512, 3
+    s = skb().SymTensorSketchSet(n, b, B, 42, gpu_ctx)
+    s.accumulate_dense(sym_tensor(n, 2), True)
+    p = tmp_path / "s.skt"
+    s.save(p)
+    assert skb().peek_sketch_mode(p) == "sym"
+    t = skb().SymTensorSketchSet.load(p, gpu_ctx)
+    assert np.array_equal(t.data(), s.data())
+    for m in range(B):
+        assert all(np.array_equal(x, y) for x, y in zip(t.tables(m), s.tables(m)))
+    u = np.random.default_rng(1).normal(size=n)
+    ws1, ws2 = skb().SymContractionWorkspace(s), skb().SymContractionWorkspace(t)
+    assert np.array_equal(ws1.Ivv(u), ws2.Ivv(u))
+    a = skb().AsymTensorSketchSet(n, b, B, 43, gpu_ctx)
+    a.accumulate_dense(np.random.default_rng(3).normal(size=(n, n, n)))
+    pa = tmp_path / "a.skt"
+    a.save(pa)
+    assert skb().peek_sketch_mode(pa) == "asym"
+    assert np.array_equal(skb().AsymTensorSketchSet.load(pa, gpu_ctx).data(), a.data())
+    with pytest.raises(skb().FormatError, match="not a symmetric"):
+        skb().SymTensorSketchSet.load(pa, gpu_ctx)
+    bad = tmp_path / "bad.skt"
+    bad.write_bytes(b"NOTASKETCH" + bytes(60))
+    with pytest.raises(skb().FormatError, match="bad magic"):
+        skb().peek_sketch_mode(bad)
+    trunc = tmp_path / "t.skt"
+    trunc.write_bytes(p.read_bytes()[:200])
+    with pytest.raises(skb().FormatError, match="truncated"):
+        skb().SymTensorSketchSet.load(trunc, gpu_ctx)
