@@ -800,7 +800,8 @@ int skc_sym_accumulate_dense(skc_sym_set* s, const void* T, int dtype, int locat
 static void sym_moment_device(skc_sym_set* s, const double* Xd, const double* wd, double alpha, long long Nsamp) {
     skc_context* ctx = s->ctx;
     const int per_rep = s->B * s->S;
-    int chunks = static_cast<int>(std::max<long long>(1, std::min<long long>(Nsamp, (4ll * ctx->sms + per_rep - 1) / per_rep)));
+    // ~4 waves of 2 resident CTAs per SM; one sample per chunk at most
+    int chunks = static_cast<int>(std::max<long long>(1, std::min<long long>(Nsamp, (8ll * ctx->sms) / per_rep)));
     ctx->freq_acc.alloc(static_cast<size_t>(chunks) * per_rep * s->N * 2);
     ctx->tmp.alloc(static_cast<size_t>(s->B) * s->b);
     SymView v = s->view();
@@ -869,6 +870,7 @@ int skc_sym_sketch_whitened_m3(skc_sym_set* s, int V, long long D, const long lo
         check_vec(doc_ptr, "sketch_whitened_m3: doc_ptr");
         check_vec(W, "sketch_whitened_m3: W");
         const int k = s->n;  // lda.cpp:149-151: set dimension must equal the whitening rank
+        require(k <= 2048, "sketch_whitened_m3: whitening rank above 2048 is not supported on the device path");
         const long long nnz = doc_ptr[D] - doc_ptr[0];
         require(doc_ptr[0] == 0 && nnz >= 0, "sketch_whitened_m3: doc_ptr must start at 0");
         if (nnz > 0) {
@@ -934,7 +936,7 @@ int skc_sym_sketch_whitened_m3(skc_sym_set* s, int V, long long D, const long lo
         launch_lda_q(st, k, V, d_W.p, d_m1.p, 1.0 / static_cast<double>(used1), d_q.p);
         ctx->check_launch();
         const int per_rep = s->B * s->S;
-        const int chunks = std::max(1, (ctx->sms + per_rep - 1) / per_rep);
+        const int chunks = std::max(1, static_cast<int>(std::min<long long>(D + V, (4ll * ctx->sms) / per_rep)));
         d_acc.alloc(static_cast<size_t>(chunks) * per_rep * s->N * 2);
         d_cross.alloc(static_cast<size_t>(chunks) * per_rep * s->N * 2);
         SymView v = s->view();

@@ -589,7 +589,7 @@ void launch_argmax_first(cudaStream_t st, const double* values, int L, int* best
 
 // ============================ K2: frequency-domain accumulation ===================
 // Symmetric moment / rank-1: acc += w * F(CS(x))^3 (sketch.cpp:353-358; lda.cpp:201-207).
-template <int LOGN>
+template <int LOGN, bool SCR>
 __global__ void __launch_bounds__(kFftThreads, SKC_FFT_MINB)
     k_sym_moment(SymView v, const double* __restrict__ X, const double* __restrict__ w, double wscale, long long Nsamp,
                  int chunks, double* __restrict__ acc) {
@@ -602,16 +602,22 @@ __global__ void __launch_bounds__(kFftThreads, SKC_FFT_MINB)
     const int ch = blockIdx.x / (S * B);
     double2* A = sm;
     double2* ACC = sm + stride;
+    double2* scr = ACC + N + 8;                                        // n (SCR)
+    std::uint32_t* keys = reinterpret_cast<std::uint32_t*>(scr + n);  // n (SCR)
     const long long per = (Nsamp + chunks - 1) / chunks;
     const long long s0 = (long long)ch * per, s1 = min(Nsamp, s0 + per);
     const uint2* plan = v.plan1 + (size_t)m * n;
+    const std::uint32_t bmask = v.b - 1;
     zero_smem(ACC, N + 8);
     for (long long s = s0; s < s1; ++s) {
         const double* x = X + (size_t)s * n;
         zero_smem(A, stride);
         __syncthreads();
-        scatter_plan(A, plan, n, N, r, v.b - 1, 0x0FFFFFFFu, v.tw,
-                     [&](std::uint32_t i, std::uint32_t y) { return root4_times(y >> 28, x[i]); });
+        auto vx = [&](std::uint32_t i, std::uint32_t y) { return root4_times(y >> 28, x[i]); };
+        if (SCR)
+            scatter2(A, plan, vx, static_cast<double2*>(nullptr), plan, vx, n, N, r, bmask, 0x0FFFFFFFu, v.tw, scr, keys);
+        else
+            scatter_plan(A, plan, n, N, r, bmask, 0x0FFFFFFFu, v.tw, vx);
         __syncthreads();
         dif_local<LOGN>(A, 1, v.twl);
         const double ws = (w ? w[s] : 1.0) * wscale;
@@ -627,13 +633,19 @@ __global__ void __launch_bounds__(kFftThreads, SKC_FFT_MINB)
 }
 void launch_sym_moment_accumulate(cudaStream_t st, const SymView& v, const double* X, const double* w, double wscale,
                                   long long Nsamp, int chunks, double* acc) {
-    const size_t smem = sizeof(double2) * (padded_len(v.N) + v.N + 8);
+    const bool scr = v.n <= kScatterMax;
+    const size_t smem = sizeof(double2) * (padded_len(v.N) + v.N + 8) +
+                        (scr ? (sizeof(double2) + sizeof(std::uint32_t)) * (size_t)v.n : 0);
     const unsigned grid = (unsigned)((long long)chunks * v.B * v.S);
-#define L_(LG)                                                                                                \
-    {                                                                                                         \
-        if (smem > 48 * 1024)                                                                                 \
-            cudaFuncSetAttribute(k_sym_moment<LG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
-        k_sym_moment<LG><<<grid, kFftThreads, smem, st>>>(v, X, w, wscale, Nsamp, chunks, acc);               \
+#define L_(LG)                                                                                                     \
+    {                                                                                                              \
+        if (scr) {                                                                                                 \
+            cudaFuncSetAttribute(k_sym_moment<LG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
+            k_sym_moment<LG, true><<<grid, kFftThreads, smem, st>>>(v, X, w, wscale, Nsamp, chunks, acc);          \
+        } else {                                                                                                   \
+            cudaFuncSetAttribute(k_sym_moment<LG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+            k_sym_moment<LG, false><<<grid, kFftThreads, smem, st>>>(v, X, w, wscale, Nsamp, chunks, acc);         \
+        }                                                                                                          \
     }
     SKC_LOGN_SWITCH(v.logN, L_)
 #undef L_

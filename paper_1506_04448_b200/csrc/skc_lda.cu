@@ -26,25 +26,38 @@ __device__ __forceinline__ void zero_sm(double2* sm, int count) {
     for (int x = threadIdx.x; x < count; x += blockDim.x) sm[x] = mk(0.0, 0.0);
 }
 
-// scatter of a dense k-vector through the set's bucket1 plan (cf. skc_kernels.cu)
+// Deterministic scatter of a dense k-vector through the set's bucket1 plan: every
+// contribution is computed independently (all loads in flight), then each run head sums
+// its run in plan order. Two vectors (A: valA, B: valB) may be scattered at once.
+// scratch: up to 2k double2 + 2k keys.
+template <typename ValA, typename ValB>
+__device__ __forceinline__ void scatter_dense2(double2* yA, ValA valA, double2* yB, ValB valB, const uint2* __restrict__ plan,
+                                               int n, int N, int r, std::uint32_t bmask, const double2* __restrict__ tw,
+                                               double2* scr, std::uint32_t* keys) {
+    const std::uint32_t nmask = static_cast<std::uint32_t>(N - 1);
+    const int tot = yB ? 2 * n : n;
+    for (int x = threadIdx.x; x < tot; x += blockDim.x) {
+        const bool b = x >= n;
+        const uint2 e = plan[b ? x - n : x];
+        const double val = b ? valB(e.x) : valA(e.x);
+        scr[x] = cmul(root4_times(e.y >> 28, val), conj(tw[(static_cast<std::uint32_t>(r) * (e.y & 0x0FFFFFFFu)) & bmask]));
+        keys[x] = e.y & nmask;
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < tot; x += blockDim.x) {
+        const int lo = (x >= n) ? n : 0;
+        const std::uint32_t key = keys[x];
+        if (x > lo && keys[x - 1] == key) continue;
+        double2 acc = scr[x];
+        for (int x2 = x + 1; x2 < lo + n && keys[x2] == key; ++x2) acc = cadd(acc, scr[x2]);
+        ((x >= n) ? yB : yA)[pad16(static_cast<int>(key))] = acc;
+    }
+}
 template <typename ValFn>
 __device__ __forceinline__ void scatter_dense(double2* y, const uint2* __restrict__ plan, int n, int N, int r,
-                                              std::uint32_t bmask, const double2* __restrict__ tw, ValFn val) {
-    const std::uint32_t nmask = static_cast<std::uint32_t>(N - 1);
-    for (int q = threadIdx.x; q < n; q += blockDim.x) {
-        uint2 e = plan[q];
-        const std::uint32_t key = e.y & nmask;
-        if (q > 0 && (plan[q - 1].y & nmask) == key) continue;
-        double2 acc = mk(0.0, 0.0);
-        for (int q2 = q;;) {
-            const std::uint32_t t = e.y & 0x0FFFFFFFu;
-            acc = cadd(acc, cmul(root4_times(e.y >> 28, val(e.x)), conj(tw[(static_cast<std::uint32_t>(r) * t) & bmask])));
-            if (++q2 >= n) break;
-            e = plan[q2];
-            if ((e.y & nmask) != key) break;
-        }
-        y[pad16(static_cast<int>(key))] = acc;
-    }
+                                              std::uint32_t bmask, const double2* __restrict__ tw, ValFn val,
+                                              double2* scr, std::uint32_t* keys) {
+    scatter_dense2(y, val, static_cast<double2*>(nullptr), val, plan, n, N, r, bmask, tw, scr, keys);
 }
 }  // namespace
 
@@ -146,6 +159,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     double2* Bw = sm + stride;
     double2* ACC = sm + 2 * stride;
     double2* CR = ACC + N;
+    double2* scr = CR + N;                                                 // 2n
+    std::uint32_t* keys = reinterpret_cast<std::uint32_t*>(scr + 2 * n);  // 2n
     const uint2* plan = v.plan1 + (size_t)m * n;
     const std::uint32_t bmask = v.b - 1;
     const long long items = Dn + V;
@@ -159,13 +174,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncthreads();
         if (doc) {
             const double* p = P + (size_t)it * n;
-            scatter_dense(A, plan, n, N, r, bmask, v.tw, [&](std::uint32_t i) { return p[i]; });
+            scatter_dense(A, plan, n, N, r, bmask, v.tw, [&](std::uint32_t i) { return p[i]; }, scr, keys);
         } else {
             const long long w = it - Dn;
             const double* wr = W + (size_t)w * n;
             const double* sr = sumwn + (size_t)w * n;
-            scatter_dense(A, plan, n, N, r, bmask, v.tw, [&](std::uint32_t i) { return wr[i]; });
-            scatter_dense(Bw, plan, n, N, r, bmask, v.tw, [&](std::uint32_t i) { return sr[i]; });
+            scatter_dense2(A, [&](std::uint32_t i) { return wr[i]; }, Bw, [&](std::uint32_t i) { return sr[i]; }, plan, n, N,
+                           r, bmask, v.tw, scr, keys);
         }
         __syncthreads();
         dif_local<LOGN>(sm, doc ? 1 : 2, v.twl);
@@ -204,9 +219,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int N = 1 << LOGN;
     const int S = v.S, n = v.n, B = v.B;
     const int r = blockIdx.x % S, m = blockIdx.x / S;
+    double2* scr = sm + (N + (N >> 4) + 1);
+    std::uint32_t* keys = reinterpret_cast<std::uint32_t*>(scr + 2 * n);
     zero_sm(sm, N + (N >> 4) + 1);
     __syncthreads();
-    scatter_dense(sm, v.plan1 + (size_t)m * n, n, N, r, v.b - 1, v.tw, [&](std::uint32_t i) { return q[i]; });
+    scatter_dense(sm, v.plan1 + (size_t)m * n, n, N, r, v.b - 1, v.tw, [&](std::uint32_t i) { return q[i]; }, scr, keys);
     __syncthreads();
     dif_local<LOGN>(sm, 1, v.twl);
     const double2* ai = reinterpret_cast<const double2*>(acc_in);
@@ -266,7 +283,7 @@ void launch_lda_q(cudaStream_t st, int k, int V, const double* W, const double* 
 void launch_lda_accumulate(cudaStream_t st, const SymView& v, long long Dn, const double* P, const double* s1,
                            const double* s2, int V, const double* W, const double* coeff1, const double* sumwn,
                            int chunks, double* acc, double* cross) {
-    const size_t smem = sizeof(double2) * (2 * padded_len(v.N) + 2 * v.N);
+    const size_t smem = sizeof(double2) * (2 * padded_len(v.N) + 2 * v.N) + (sizeof(double2) + 4) * 2 * (size_t)v.n;
     const unsigned grid = (unsigned)((long long)chunks * v.B * v.S);
 #define L_(LG)                                                                                                    \
     {                                                                                                             \
@@ -280,7 +297,7 @@ void launch_lda_accumulate(cudaStream_t st, const SymView& v, long long Dn, cons
 }
 void launch_lda_finish(cudaStream_t st, const SymView& v, const double* acc, const double* cross, int chunks,
                        const double* q, double inv_docs, double m1_coeff, double2* tmp) {
-    const size_t smem = sizeof(double2) * padded_len(v.N);
+    const size_t smem = sizeof(double2) * padded_len(v.N) + (sizeof(double2) + 4) * 2 * (size_t)v.n;
 #define L_(LG)                                                                                               \
     {                                                                                                        \
         cudaFuncSetAttribute(k_lda_finish<LG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
