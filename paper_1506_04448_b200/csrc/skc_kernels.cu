@@ -417,15 +417,189 @@ __global__ void __launch_bounds__(kFftThreads, MINB)
     }
 }
 
+// ---- half-length f2 / z2 variant ---------------------------------------------------------
+// f2 lives on even buckets 2h_i, so y_r (the residue-r local array of f2) is supported on
+// even t' and its N-point DFT is periodic with period N/2: only the N/2-point DFT of the
+// even subsequence is computed (Bh). In the bit-reversed local layout, full position p
+// pairs with half position p >> 1. Likewise z2 is only gathered at even local positions,
+// so Z2 is folded (Z[2p''] + Z[2p''+1] holds frequencies k and k + N/2) and inverted with
+// an N/2-point DIT. Net: 3 of the 4 length-N transforms per restart instead of 4.
+template <int LOGN, int LR, int P, int NPA = plan_npass(LOGN, LR), int NPB = plan_npass(LOGN - 1, LR)>
+struct DifPair {
+    __device__ __forceinline__ static void run(double2* A, double2* Bh, const double2* twl) {
+        constexpr int PB = P - (NPA - NPB);
+        constexpr int RA = plan_logr(LOGN, P, LR), HA = plan_h(LOGN, P, LR), IA = (1 << LOGN) >> RA;
+        constexpr int RB = PB >= 0 ? plan_logr(LOGN - 1, PB, LR) : 1;
+        constexpr int HB = PB >= 0 ? plan_h(LOGN - 1, PB, LR) : 1;
+        constexpr int IB = PB >= 0 ? (1 << (LOGN - 1)) >> RB : 0;
+        for (int w = threadIdx.x; w < IA + IB; w += blockDim.x) {
+            if (w < IA)
+                dif_pass_item<RA>(A, w, HA, twl, LOGN);
+            else
+                dif_pass_item<RB>(Bh, w - IA, HB, twl, LOGN);
+        }
+        __syncthreads();
+        DifPair<LOGN, LR, P + 1, NPA, NPB>::run(A, Bh, twl);
+    }
+};
+template <int LOGN, int LR, int NPA, int NPB>
+struct DifPair<LOGN, LR, NPA, NPA, NPB> {
+    __device__ __forceinline__ static void run(double2*, double2*, const double2*) {}
+};
+template <int LOGN, int LR, int P, int NPA = plan_npass(LOGN, LR), int NPB = plan_npass(LOGN - 1, LR)>
+struct DitPair {
+    __device__ __forceinline__ static void run(double2* A, double2* Bh, const double2* twl) {
+        constexpr int PB = P - (NPA - NPB);
+        constexpr int RA = plan_logr(LOGN, P, LR), HA = plan_h(LOGN, P, LR), IA = (1 << LOGN) >> RA;
+        constexpr int RB = PB >= 0 ? plan_logr(LOGN - 1, PB, LR) : 1;
+        constexpr int HB = PB >= 0 ? plan_h(LOGN - 1, PB, LR) : 1;
+        constexpr int IB = PB >= 0 ? (1 << (LOGN - 1)) >> RB : 0;
+        for (int w = threadIdx.x; w < IA + IB; w += blockDim.x) {
+            if (w < IA)
+                dit_pass_item<RA>(A, w, HA, twl, LOGN);
+            else
+                dit_pass_item<RB>(Bh, w - IA, HB, twl, LOGN);
+        }
+        __syncthreads();
+        DitPair<LOGN, LR, P - 1, NPA, NPB>::run(A, Bh, twl);
+    }
+};
+template <int LOGN, int LR, int NPA, int NPB>
+struct DitPair<LOGN, LR, -1, NPA, NPB> {
+    __device__ __forceinline__ static void run(double2*, double2*, const double2*) {}
+};
+
+template <int LOGN, int NT>
+__device__ __forceinline__ void sym_contract_half_body(const SymView& v, const double* __restrict__ U, int L, int mode,
+                                                       double* __restrict__ out) {
+    extern __shared__ double2 sm[];
+    __shared__ double red[NT / 32];
+    constexpr int N = 1 << LOGN, NH = N / 2;
+    constexpr int strideA = N + (N >> 4) + 1;
+    constexpr int strideB = NH + (NH >> 4) + 1;
+    const int S = v.S, n = v.n, B = v.B;
+    const int r = blockIdx.x % S;
+    const int m = (blockIdx.x / S) % B;
+    const int l0 = (blockIdx.x / (S * B)) * kLPB;
+    double2* A = sm;
+    double2* Bh = sm + strideA;
+    double2* scr = Bh + strideB;                                           // 2n
+    std::uint32_t* keys = reinterpret_cast<std::uint32_t*>(scr + 2 * n);  // 2n
+    const std::uint32_t bmask = v.b - 1;
+    const std::uint32_t nmask = static_cast<std::uint32_t>(N - 1);
+    const double2* fT = v.spec + ((size_t)m * S + r) * N;
+    const uint2* p1 = v.plan1 + (size_t)m * n;
+    const uint2* p2 = v.plan2 + (size_t)m * n;
+    const std::uint32_t* b1 = v.bucket1 + (size_t)m * n;
+    const std::uint32_t* b2 = v.bucket2 + (size_t)m * n;
+    const std::uint32_t* b3 = v.bucket3 + (size_t)m * n;
+    const std::uint8_t* se = v.sexp + (size_t)m * n;
+    const double2* dm = v.data + (size_t)m * v.b;
+
+    for (int l = l0; l < min(L, l0 + kLPB); ++l) {
+        const double* u = U + (size_t)l * n;
+        zero_smem(sm, strideA + strideB);
+        // phase 1 of the two-phase scatter (contraction.cpp:150-154): every contribution
+        // val * w_b^{-r t} independently into scratch, keys = local position (f2: halved)
+        for (int x = threadIdx.x; x < 2 * n; x += NT) {
+            const bool hb = x >= n;
+            const uint2 e = hb ? p2[x - n] : p1[x];
+            const double ui = u[e.x];
+            const double2 val = root4_times(e.y >> 28, hb ? ui * ui : ui);
+            scr[x] = cmul(val, conj(v.tw[(static_cast<std::uint32_t>(r) * (e.y & 0x0FFFFFFFu)) & bmask]));
+            keys[x] = hb ? ((e.y & nmask) >> 1) : (e.y & nmask);
+        }
+        __syncthreads();
+        for (int x = threadIdx.x; x < 2 * n; x += NT) {
+            const int lo = (x >= n) ? n : 0;
+            const std::uint32_t key = keys[x];
+            if (x > lo && keys[x - 1] == key) continue;
+            double2 acc = scr[x];
+            for (int x2 = x + 1; x2 < lo + n && keys[x2] == key; ++x2) acc = cadd(acc, scr[x2]);
+            ((x >= n) ? Bh : A)[pad16(static_cast<int>(key))] = acc;
+        }
+        __syncthreads();
+        DifPair<LOGN, 4, 0>::run(A, Bh, v.twl);
+
+        if (mode == 0) {
+            // z1 = fT conj(f1^2 + f2) (full), Z2 = fT conj(f1) folded to N/2 (contraction.cpp:158-162)
+            for (int q = threadIdx.x; q < NH; q += NT) {
+                const int p0 = 2 * q, p1i = 2 * q + 1;
+                const double2 t0 = fT[p0], t1 = fT[p1i];
+                const double2 u0 = A[pad16(p0)], u1 = A[pad16(p1i)];
+                const double2 f2 = Bh[pad16(q)];
+                A[pad16(p0)] = cmulc(t0, cadd(cmul(u0, u0), f2));
+                A[pad16(p1i)] = cmulc(t1, cadd(cmul(u1, u1), f2));
+                Bh[pad16(q)] = cadd(cmulc(t0, u0), cmulc(t1, u1));
+            }
+            __syncthreads();
+            DitPair<LOGN, 4, plan_npass(LOGN, 4) - 1>::run(A, Bh, v.twl);
+            const double inv_b = 1.0 / static_cast<double>(v.b);
+            double* o = out + (((size_t)l * B + m) * S + r) * n;
+            for (int i = threadIdx.x; i < n; i += NT) {
+                const unsigned e = se[i];
+                const double ui = u[i];
+                const std::uint32_t t1 = b1[i], t2 = b2[i];
+                const double2 z1 = cmul(A[pad16(static_cast<int>(t1 & nmask))], v.tw[(static_cast<std::uint32_t>(r) * t1) & bmask]);
+                const double2 z2 = cmul(Bh[pad16(static_cast<int>((t2 & nmask) >> 1))], v.tw[(static_cast<std::uint32_t>(r) * t2) & bmask]);
+                double val = re_rot_conj(e, z1) * (1.0 / 6.0) * inv_b;
+                val += ui * re_rot_conj(2u * e, z2) * (1.0 / 3.0) * inv_b;
+                if (r == 0) val += ui * ui * re_rot_conj(3u * e, dm[b3[i]]) * (1.0 / 3.0);
+                o[i] = val;
+            }
+        } else {
+            // acc1 += Re(fT conj(f1)^3), acc2 += Re(fT conj(f1) conj(f2))   (contraction.cpp:111-116)
+            double acc1 = 0.0, acc2 = 0.0;
+            for (int j = threadIdx.x; j < N; j += NT) {
+                const double2 c1 = conj(A[pad16(j)]);
+                const double2 w1 = cmul(fT[j], c1);
+                acc1 += cmul(cmul(w1, c1), c1).x;
+                acc2 += cmul(w1, conj(Bh[pad16(j >> 1)])).x;
+            }
+            const double s1 = block_sum<NT>(acc1, red);
+            const double s2 = block_sum<NT>(acc2, red);
+            double term3 = 0.0;
+            if (r == 0) {  // contraction.cpp:117-121
+                for (int i = threadIdx.x; i < n; i += NT) {
+                    const double u3 = u[i] * u[i] * u[i];
+                    term3 += u3 * re_rot_conj(3u * se[i], dm[b3[i]]);
+                }
+            }
+            const double s3 = block_sum<NT>(term3, red);
+            if (threadIdx.x == 0) {
+                double* o = out + (((size_t)l * B + m) * S + r) * 3;
+                o[0] = s1;
+                o[1] = s2;
+                o[2] = s3;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+template <int LOGN, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
+    k_sym_contract_half(SymView v, const double* __restrict__ U, int L, int mode, double* __restrict__ out) {
+    sym_contract_half_body<LOGN, NT>(v, U, L, mode, out);
+}
+// 192 threads x 3 CTAs per SM with a 112-register cap (launch bounds alone pick 96 and spill)
+template <int LOGN>
+__global__ void __maxnreg__(112)
+    k_sym_contract_half_r112(SymView v, const double* __restrict__ U, int L, int mode, double* __restrict__ out) {
+    sym_contract_half_body<LOGN, 192>(v, U, L, mode, out);
+}
+
 // Variant selection (A/B measured on B200, see profiles/): SKC_CONTRACT_VARIANT =
 //   "16s" radix-16 + scratch scatter (2 CTAs/SM), "16d" radix-16 + direct scatter,
-//   "8d" radix-8 + direct scatter (3 CTAs/SM).
+//   "8d" radix-8 + direct scatter (3 CTAs/SM), "h256"/"h192"/"h112" half-length f2/z2
+//   kernel at 256 threads x 2 CTAs, 192 x 3 (default), 192 x 3 with a 112-register cap.
+//   config-1 step (L=100): 16s 1.05 ms, h256 0.94, h192 0.886, h112 0.97 (profiles/r01).
 static int contract_variant() {
     static int v = [] {
         const char* e = std::getenv("SKC_CONTRACT_VARIANT");
-        if (!e) return 0;
+        if (!e) return 4;
         std::string s(e);
-        return s == "16s" ? 0 : s == "16d" ? 1 : s == "8d" ? 2 : 0;
+        return s == "16s" ? 0 : s == "16d" ? 1 : s == "8d" ? 2 : s == "h256" ? 3 : s == "h192" ? 4 : s == "h112" ? 5 : 4;
     }();
     return v;
 }
@@ -437,10 +611,55 @@ static void sym_contract_launch(cudaStream_t st, const SymView& v, const double*
     k_sym_contract<LG, VAR, LR, MINB><<<grid, kFftThreads, smem, st>>>(v, U, L, mode, out);
 }
 
+template <int LG, int NT, int MINB>
+static void sym_contract_half_launch(cudaStream_t st, const SymView& v, const double* U, int L, int mode, double* out,
+                                     unsigned grid, size_t smem) {
+    cudaFuncSetAttribute(k_sym_contract_half<LG, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_sym_contract_half<LG, NT, MINB><<<grid, NT, smem, st>>>(v, U, L, mode, out);
+}
+
+template <int LG>
+static void sym_contract_half_dispatch(cudaStream_t st, const SymView& v, const double* U, int L, int mode, double* out,
+                                       unsigned grid, size_t smem, int var) {
+    if (var == 3) {
+        sym_contract_half_launch<LG, 256, 2>(st, v, U, L, mode, out, grid, smem);
+    } else if (var == 4) {
+        sym_contract_half_launch<LG, 192, 3>(st, v, U, L, mode, out, grid, smem);
+    } else {
+        cudaFuncSetAttribute(k_sym_contract_half_r112<LG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_sym_contract_half_r112<LG><<<grid, 192, smem, st>>>(v, U, L, mode, out);
+    }
+}
+
 void launch_sym_contract(cudaStream_t st, const SymView& v, const double* U, int L, int mode, double* out) {
     const bool scr_ok = v.n <= kScatterMax;
     int var = contract_variant();
-    if (var == 0 && !scr_ok) var = 1;
+    if (var >= 3 && (!scr_ok || v.logN < 2)) var = scr_ok ? 0 : 1;
+    if (var >= 3) {
+        const int NH = v.N / 2;
+        const size_t smem = sizeof(double2) * (padded_len(v.N) + (NH + NH / 16 + 1)) +
+                            (sizeof(double2) + sizeof(std::uint32_t)) * 2 * (size_t)v.n;
+        const unsigned grid = (unsigned)((long long)((L + kLPB - 1) / kLPB) * v.B * v.S);
+#define LH_(LG) sym_contract_half_dispatch<LG>(st, v, U, L, mode, out, grid, smem, var)
+        switch (v.logN) {
+            case 2: LH_(2); break;
+            case 3: LH_(3); break;
+            case 4: LH_(4); break;
+            case 5: LH_(5); break;
+            case 6: LH_(6); break;
+            case 7: LH_(7); break;
+            case 8: LH_(8); break;
+            case 9: LH_(9); break;
+            case 10: LH_(10); break;
+            case 11: LH_(11); break;
+            case 12: LH_(12); break;
+            default: break;
+        }
+#undef LH_
+        SKC_LAUNCHED();
+        count_transforms((std::uint64_t)L * v.B * v.S * (mode == 0 ? 4 : 2), v.S);
+        return;
+    }
     const size_t smem = sizeof(double2) * 2 * padded_len(v.N) +
                         (var == 0 ? (sizeof(double2) + sizeof(std::uint32_t)) * 2 * (size_t)v.n : 0);
     const unsigned grid = (unsigned)((long long)((L + kLPB - 1) / kLPB) * v.B * v.S);
