@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -122,12 +123,13 @@ struct skc_context {
     std::map<std::tuple<int, int, int, bool>, std::unique_ptr<RowTab>> rowtabs;
     // scratch
     DevBuf<unsigned char> tensor_stage;
-    DevBuf<long long> build_partials, qbuf;
+    DevBuf<long long> qbuf;
     DevBuf<short> rowF;
     DevBuf<double> prepass;
     DevBuf<int> ints;  // [0] scale exp, [1] nonfinite, [2] best tau, [3..] misc
     DevBuf<double> dbl;  // [0] best value
-    DevBuf<int> chunk_begin;
+    DevBuf<int> build_ints;                // per-type row counters of the dense build
+    DevBuf<unsigned long long> build_acc;  // exact fixed-point slot accumulators
     DevBuf<double> U, part, values, freq_acc, X;
     DevBuf<double2> tmp;
     DevBuf<int> flags;
@@ -445,28 +447,28 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
         if (Rg <= 16 && build_smem_bytes(spc, Rg, n) <= static_cast<size_t>(ctx->smem_optin - 1024)) break;
         if (G > 4096) fail(kInvalidArgument, "accumulate_dense: sketch set too large for the dense build");
     }
-    int C = std::max(1, ctx->sms / G);
-    C = std::min(C, rt.nrows);
     long long spc = (total_slots + G - 1) / G;
     spc = (spc + 31) / 32 * 32;
+    if (const char* e = std::getenv("SKC_BUILD_SPC")) {  // experiment hook: forced window size
+        const long long f = std::atoll(e) / 32 * 32;
+        if (f >= 32 && f <= spc * 4 && build_smem_bytes(f, 16, n) <= static_cast<size_t>(ctx->smem_optin - 1024)) {
+            spc = f;
+            G = static_cast<int>((total_slots + spc - 1) / spc);
+        }
+    }
     const long long spr = sym ? 2ll * b : static_cast<long long>(b);
     int R = 1;
+    std::vector<int> Rg(G, 1);
     for (int g = 0; g < G; ++g) {
         const long long lo = g * spc, hi = std::min(lo + spc, total_slots);
-        if (hi > lo) R = std::max(R, static_cast<int>((hi - 1) / spr - lo / spr + 1));
+        if (hi > lo) Rg[g] = static_cast<int>((hi - 1) / spr - lo / spr + 1);
+        R = std::max(R, Rg[g]);
     }
     require(R <= 16, "accumulate_dense: slot range spans too many replicates");
-    // chunk boundaries balanced by entry count
-    std::vector<int> cb(C + 1, 0);
     const long long tot = rt.cum.back();
-    for (int c = 1; c < C; ++c) {
-        const long long target = tot * c / C;
-        cb[c] = static_cast<int>(std::lower_bound(rt.cum.begin(), rt.cum.end(), target) - rt.cum.begin());
-        cb[c] = std::max(cb[c], cb[c - 1]);
-    }
-    cb[C] = rt.nrows;
-    ctx->chunk_begin.upload(cb.data(), cb.size(), ctx->stream);
-    ctx->build_partials.alloc(static_cast<size_t>(C) * total_slots);
+    const int P = std::max(1, ctx->sms);  // one persistent CTA per SM, rows handed out dynamically
+    ctx->build_ints.alloc(static_cast<size_t>(G));
+    ctx->build_acc.alloc(static_cast<size_t>(total_slots));
     ctx->qbuf.alloc(static_cast<size_t>(std::max<long long>(1, tot)));
     ctx->rowF.alloc(static_cast<size_t>(rt.nrows));
     ctx->prepass.alloc(kPrepassBlocks);
@@ -478,9 +480,17 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
     p.dtype = dtype;
     p.rowtab = rt.rows.p;
     p.nrows = rt.nrows;
-    p.chunk_begin = ctx->chunk_begin.p;
-    p.C = C;
+    p.P = P;
     p.G = G;
+    p.next_row = ctx->build_ints.p;
+    p.acc = ctx->build_acc.p;
+    static const bool trace_on = std::getenv("SKC_BUILD_TRACE") != nullptr;
+    DevBuf<unsigned long long> trace;
+    p.trace = nullptr;
+    if (trace_on) {
+        trace.alloc(3 * static_cast<size_t>(P));
+        p.trace = trace.p;
+    }
     p.total_slots = total_slots;
     p.slots_per_cta = static_cast<int>(spc);
     p.R = R;
@@ -493,11 +503,20 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
     p.prepass_partials = ctx->prepass.p;
     p.scale_exp = ctx->ints.p;
     p.nonfinite = ctx->ints.p + 1;
-    p.partials = ctx->build_partials.p;
     p.data_as_double = reinterpret_cast<double*>(data);
     {
         SKC_PROF(ctx, "build_prepass");
         launch_build_prepass(ctx->stream, Tdev, p);
+    }
+    ctx->check_launch();
+    {
+        SKC_PROF(ctx, "build_main");
+        launch_build_main(ctx->stream, Tdev, p);
+    }
+    ctx->check_launch();
+    {
+        SKC_PROF(ctx, "build_finalize");
+        launch_build_finalize(ctx->stream, p);  // device-side no-op when nonfinite
     }
     ctx->check_launch();
     int nonfinite = 0;
@@ -506,16 +525,16 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
     // Fixed-point accumulation cannot carry NaN/Inf the way the reference's
     // floating-point sum would; reject instead of producing a wrong sketch.
     if (nonfinite) fail(kInvalidArgument, "accumulate_dense: tensor has a non-finite entry");
-    {
-        SKC_PROF(ctx, "build_main");
-        launch_build_main(ctx->stream, Tdev, p);
+    if (trace_on) {
+        std::vector<unsigned long long> t(3 * static_cast<size_t>(P));
+        CK(cudaMemcpy(t.data(), trace.p, t.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        unsigned long long t0 = ~0ull;
+        for (int x = 0; x < P; ++x) t0 = std::min(t0, t[3 * x]);
+        std::fprintf(stderr, "build trace: G=%d spc=%lld P=%d\n", G, spc, P);
+        for (int x = 0; x < P; ++x)
+            std::fprintf(stderr, "cta %3d start %7.1f us dur %7.1f us switches %llu\n", x, (t[3 * x] - t0) * 1e-3,
+                         (t[3 * x + 1] - t[3 * x]) * 1e-3, t[3 * x + 2]);
     }
-    ctx->check_launch();
-    {
-        SKC_PROF(ctx, "build_finalize");
-        launch_build_finalize(ctx->stream, p);
-    }
-    ctx->check_launch();
 }
 
 // Symmetry check of the reference (tensor.cpp:32-43) — first failing (i,j,k,perm) in

@@ -8,13 +8,14 @@
 //
 // Layout of the work. The B x b complex sketch set (5.2 MB at config 1) does not fit one
 // SM's shared memory and each tensor entry lands in B random buckets, so the slot space
-// (replicate, bucket, re/im) is cut into G contiguous ranges of ~29K slots (~227 KB of
-// limbs) and the sorted-triple rows into C chunks, G*C ~= #SMs. CTA (g, c) streams the
-// rows of chunk c with coalesced loads (a warp per row segment, a lane per k),
-// converts each entry to fixed point once, and evaluates it against the 1-2 replicates
-// its range overlaps; in-range contributions go to shared memory. The measured
-// alternative that enumerated only owned contributions through per-class suffix
-// tables executed 3x more instructions (profiles/).
+// (replicate, bucket, re/im) is cut into G contiguous ranges ("types") of ~27K slots
+// (~220 KB of limbs). One persistent 1024-thread CTA per SM holds one type's window and
+// streams the sorted-triple rows (coalesced, a lane per k), evaluating each entry
+// against the 1-2 replicates the window overlaps. Rows are handed out dynamically from
+// per-type atomic counters and CTAs migrate between types, so the SMs finish together
+// (a static split measured 1.3x max/avg imbalance from R=1 vs R=2 windows and short
+// rows). The measured alternative that enumerated only owned contributions through
+// per-class suffix tables executed 3x more instructions (profiles/).
 //
 // Accumulation is exact 64-bit fixed point: q = round(kappa*T*2^F) is split into two
 // 32-bit limbs added with native ATOMS.ADD (shared fp64 atomics are CAS loops on
@@ -159,119 +160,220 @@ void launch_build_prepass(cudaStream_t st, const void* T, const BuildPlan& p) {
 
 // ---- main pass -----------------------------------------------------------------------
 constexpr int kBuildThreads = 1024;
+constexpr int kWarps = kBuildThreads / 32;
+constexpr int kChunkRows = 16;  // rows per warp-level grab
 
-__device__ __forceinline__ std::uint32_t atom_add_shared(std::uint32_t addr, std::uint32_t v) {
-    std::uint32_t old;
-    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
-    return old;
-}
-__device__ __forceinline__ void red_add_shared(std::uint32_t addr, std::uint32_t v) {
-    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
-}
-// Exact 64-bit add into an interleaved (lo, hi) limb pair at addr, addr+4: the carry
-// out of lo is recovered from the returned old value.
-__device__ __forceinline__ void add64(std::uint32_t addr, long long q) {
-    const std::uint32_t ql = static_cast<std::uint32_t>(q);
-    const std::uint32_t qh = static_cast<std::uint32_t>(static_cast<unsigned long long>(q) >> 32);
-    const std::uint32_t old = atom_add_shared(addr, ql);
-    const std::uint32_t carry = static_cast<std::uint32_t>((static_cast<unsigned long long>(old) + ql) >> 32);
-    red_add_shared(addr + 4u, qh + carry);
+// Exact 64-bit add of (ql, qh) into the limb pair (lo at addr_lo, hi at addr_hi). The
+// limbs live in separate planes (4-byte stride: random slots spread over all 32 banks).
+// The carry out of the low limb comes from the returned old value (add.cc / addc).
+// Branch-free: callers redirect out-of-window contributions to a per-lane trash pair,
+// which costs two extra ATOMS but no divergence or reconvergence barriers.
+__device__ __forceinline__ void add64(std::uint32_t addr_lo, std::uint32_t addr_hi, std::uint32_t ql,
+                                      std::uint32_t qh) {
+    asm volatile(
+        "{\n\t.reg .u32 old, c;\n\t"
+        "atom.shared.add.u32 old, [%0], %2;\n\t"
+        "add.cc.u32 c, old, %2;\n\t"
+        "addc.u32 c, %3, 0;\n\t"
+        "red.shared.add.u32 [%1], c;\n\t}" ::"r"(addr_lo),
+        "r"(addr_hi), "r"(ql), "r"(qh));
 }
 
 struct BuildArgs {
-    int n, B;
+    int n, B, G, nrows;
     std::uint32_t bmask;
     long long total_slots;
-    int slots_per_cta, G;
+    int slots_per_cta;
     const std::uint32_t* rowtab;
     const long long* rowoff;
     const short* rowF;
     const long long* qbuf;
-    const int* chunk_begin;
     const std::uint32_t* packed;
     const int* scale_exp;
-    long long* partials;  // C x total_slots (natural slot order)
+    int* next_row;                 // G row counters (zeroed per build)
+    unsigned long long* acc;       // total_slots exact accumulators (zeroed per build)
+    unsigned long long* trace;     // optional: per-CTA (start, end, switches)
 };
 
-// CTA (g, c): contiguous slot range g of the B x (2b | b) slot space, rows of chunk c.
-// Every streamed entry is evaluated against the (1..RMAX) replicates the range
-// overlaps; in-range contributions go to the shared-memory limbs.
+struct RowMeta {
+    int i, j, k0, d;
+    const long long* qrow;  // qbuf + rowoff - k0: entry k of the row at qrow[k]
+};
+template <bool SYM>
+__device__ __forceinline__ RowMeta load_meta(const BuildArgs& a, int row, int F) {
+    const std::uint32_t ij = __ldg(a.rowtab + row);
+    const long long off = __ldg(a.rowoff + row);
+    const int rf = __ldg(a.rowF + row);
+    RowMeta m;
+    m.i = static_cast<int>(ij >> 16);
+    m.j = static_cast<int>(ij & 0xFFFFu);
+    m.k0 = SYM ? m.j : 0;
+    m.d = rf - F;  // >= 0
+    m.qrow = a.qbuf + off - m.k0;
+    return m;
+}
+__device__ __forceinline__ void load_block(long long (&q)[4], const long long* qrow, int kb, int n) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) q[u] = (kb + 32 * u < n) ? __ldg(qrow + kb + 32 * u) : 0ll;
+}
+
+// Persistent CTAs with dynamic load balancing. A CTA holds the limb window of one slot
+// range ("type" g: ~27K contiguous slots of the B x (2b | b) slot space); its warps grab
+// 16-row chunks of the sorted-triple row stream from the type's atomic counter and
+// evaluate every streamed entry against the (1..RMAX) replicates the range overlaps:
+// in-range contributions go to the window, the rest to a per-lane trash pair. When a
+// type's rows run out, the CTA adds its window into the global exact accumulators
+// (integer RED.64: order-independent, so the sketch stays bit-deterministic) and moves
+// to the type with the most rows left. Each warp walks its rows software-pipelined: the
+// next 128-entry block's loads are issued before the current block is processed, the
+// next row's metadata one row ahead and the next chunk grab one chunk ahead.
 template <bool SYM, int RMAX>
-__global__ void __launch_bounds__(kBuildThreads, 1) k_build_range(BuildArgs a) {
+__global__ void __launch_bounds__(kBuildThreads, 1) k_build_dyn(BuildArgs a) {
     extern __shared__ std::uint32_t sacc[];
-    const int g = blockIdx.x % a.G, c = blockIdx.x / a.G;
-    const long long slot_lo = (long long)g * a.slots_per_cta;
-    const long long slot_hi = min(slot_lo + a.slots_per_cta, a.total_slots);
-    const int nslots = static_cast<int>(slot_hi - slot_lo);
-    const int n = a.n;
+    __shared__ int s_next_g;
+    const int spc = a.slots_per_cta;
+    const int plane = spc + 32;                  // limbs + 32 trash slots
+    std::uint32_t* ptab = sacc + 2 * plane;      // RMAX x n (streamed-mode hashes)
+    std::uint32_t* pij_tab = ptab + RMAX * a.n;  // RMAX x 2n (row-pair hashes)
+    const int n = a.n, nrows = a.nrows;
     const long long spr = SYM ? 2ll * (a.bmask + 1) : static_cast<long long>(a.bmask + 1);
-    const int m_lo = static_cast<int>(slot_lo / spr);
-    const int R = static_cast<int>((slot_hi - 1) / spr) - m_lo + 1;
-    std::uint32_t* lo = sacc;
-    std::uint32_t* ptab = sacc + 2 * a.slots_per_cta;  // RMAX x n (streamed-mode hashes)
-    std::uint32_t* pij_tab = ptab + RMAX * n;          // RMAX x 2n (row-pair hashes)
-    for (int s = threadIdx.x; s < 2 * a.slots_per_cta; s += kBuildThreads) lo[s] = 0u;
     const int prow = SYM ? n : 3 * n;
-    for (int x = threadIdx.x; x < RMAX * n; x += kBuildThreads) {
-        const int r = x / n, k = x - r * n;
-        const std::uint32_t* pm = a.packed + (size_t)(m_lo + min(r, R - 1)) * prow;
-        ptab[x] = pm[(SYM ? 0 : 2 * n) + k];
-        pij_tab[r * 2 * n + k] = pm[k];
-        pij_tab[r * 2 * n + n + k] = pm[(SYM ? 0 : n) + k];
-    }
-    __syncthreads();
     const int F = *a.scale_exp;
     const std::uint32_t sbase = static_cast<std::uint32_t>(__cvta_generic_to_shared(sacc));
+    const std::uint32_t hioff = 4u * static_cast<std::uint32_t>(plane);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int row_end = a.chunk_begin[c + 1];
-    int base[RMAX];
-#pragma unroll
-    for (int r = 0; r < RMAX; ++r) base[r] = static_cast<int>((long long)(m_lo + r) * spr - slot_lo);
+    const std::uint32_t trash_idx = static_cast<std::uint32_t>(spc + lane);
+    unsigned long long t_start = 0, switches = 0;
+    if (a.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 
-    for (int row = a.chunk_begin[c] + warp; row < row_end; row += kBuildThreads / 32) {
-        const std::uint32_t ij = __ldg(a.rowtab + row);
-        const int i = static_cast<int>(ij >> 16), j = static_cast<int>(ij & 0xFFFFu);
-        const int k0 = SYM ? j : 0;
-        const long long* qrow = a.qbuf + __ldg(a.rowoff + row) - k0;
-        const int d = static_cast<int>(__ldg(a.rowF + row)) - F;  // >= 0
-        std::uint32_t pij[RMAX];
+    int g = static_cast<int>((static_cast<long long>(blockIdx.x) * a.G) / gridDim.x);
+    while (g >= 0) {
+        const long long slot_lo = (long long)g * spc;
+        const long long slot_hi = min(slot_lo + spc, a.total_slots);
+        const int nslots = static_cast<int>(slot_hi - slot_lo);
+        const int m_lo = static_cast<int>(slot_lo / spr);
+        const int R = static_cast<int>((slot_hi - 1) / spr) - m_lo + 1;
+        for (int s = threadIdx.x; s < 2 * plane; s += kBuildThreads) sacc[s] = 0u;
+        for (int x = threadIdx.x; x < RMAX * n; x += kBuildThreads) {
+            const int r = x / n, k = x - r * n;
+            const std::uint32_t* pm = a.packed + (size_t)(m_lo + min(r, R - 1)) * prow;
+            ptab[x] = pm[(SYM ? 0 : 2 * n) + k];
+            pij_tab[r * 2 * n + k] = pm[k];
+            pij_tab[r * 2 * n + n + k] = pm[(SYM ? 0 : n) + k];
+        }
+        __syncthreads();
+        int base[RMAX];
 #pragma unroll
-        for (int r = 0; r < RMAX; ++r) pij[r] = pij_tab[r * 2 * n + i] + pij_tab[r * 2 * n + n + j];
-        // 4 independent loads in flight per lane before any use (latency hiding)
-        for (int kb = k0 + lane; kb < n; kb += 128) {
-            long long qv[4];
+        for (int r = 0; r < RMAX; ++r) base[r] = static_cast<int>((long long)(m_lo + r) * spr - slot_lo);
+
+        // ---- warp row iterator: current chunk [c0, c1), next chunk start (prefetched grab)
+        int c0 = 0, c1 = 0, ncs = 0;
+        if (lane == 0) c0 = atomicAdd(a.next_row + g, kChunkRows);
+        c0 = __shfl_sync(0xffffffffu, c0, 0);
+        if (c0 < nrows) {
+            c1 = min(c0 + kChunkRows, nrows);
+            if (lane == 0) ncs = atomicAdd(a.next_row + g, kChunkRows);  // one chunk ahead
+            ncs = __shfl_sync(0xffffffffu, ncs, 0);
+            int row = c0;
+            RowMeta mc = load_meta<SYM>(a, row, F), mn{};
+            // next row: same chunk, else the prefetched chunk
+            int nrow = (row + 1 < c1) ? row + 1 : ncs;
+            bool has_next = nrow < nrows;
+            if (has_next) mn = load_meta<SYM>(a, nrow, F);
+            int kb = mc.k0 + lane;
+            long long qc[4];
+            load_block(qc, mc.qrow, kb, n);
+            std::uint32_t pij[RMAX];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) qv[u] = (kb + 32 * u < n) ? __ldg(qrow + kb + 32 * u) : 0ll;
+            for (int r = 0; r < RMAX; ++r) pij[r] = pij_tab[r * 2 * n + mc.i] + pij_tab[r * 2 * n + n + mc.j];
+            for (;;) {
+                const bool same_row = kb - lane + 128 < n;
+                const bool nvalid = same_row || has_next;
+                const int nkb = same_row ? kb + 128 : mn.k0 + lane;
+                long long qn[4];
+                if (nvalid) load_block(qn, same_row ? mc.qrow : mn.qrow, nkb, n);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int k = kb + 32 * u;
-                if (k >= n) break;
-                const long long q = qv[u] >> d;  // zero entries add nothing (sketch.cpp:337 skips them)
-                const long long nq = -q;
+                for (int u = 0; u < 4; ++u) {
+                    const int k = kb + 32 * u;
+                    if (k - lane >= n) break;  // warp-uniform: no lane of this group is in the row
+                    if (k < n) {
+                        // zero entries add nothing (sketch.cpp:337 skips them)
+                        const unsigned long long q = static_cast<unsigned long long>(qc[u] >> mc.d);
+                        const unsigned long long nq = 0ull - q;
+                        const std::uint32_t ql = static_cast<std::uint32_t>(q), qh = static_cast<std::uint32_t>(q >> 32);
+                        const std::uint32_t nql = static_cast<std::uint32_t>(nq), nqh = static_cast<std::uint32_t>(nq >> 32);
 #pragma unroll
-                for (int r = 0; r < RMAX; ++r) {
-                    if (r < R) {
-                        const std::uint32_t p = pij[r] + ptab[r * n + k];
-                        const int s = base[r] + (SYM ? static_cast<int>(((p & a.bmask) << 1) | ((p >> 30) & 1u))
-                                                     : static_cast<int>(p & a.bmask));
-                        if (static_cast<unsigned>(s) < static_cast<unsigned>(nslots))
-                            add64(sbase + 8u * static_cast<std::uint32_t>(s), (p >> 31) ? nq : q);
+                        for (int r = 0; r < RMAX; ++r) {
+                            if (r < R) {  // CTA-uniform
+                                const std::uint32_t p = pij[r] + ptab[r * n + k];
+                                const std::uint32_t s = static_cast<std::uint32_t>(base[r]) +
+                                                        (SYM ? (((p & a.bmask) << 1) | ((p >> 30) & 1u)) : (p & a.bmask));
+                                const bool neg = static_cast<int>(p) < 0;
+                                const std::uint32_t addr =
+                                    sbase + 4u * (s < static_cast<std::uint32_t>(nslots) ? s : trash_idx);
+                                add64(addr, addr + hioff, neg ? nql : ql, neg ? nqh : qh);
+                            }
+                        }
                     }
                 }
+                if (!nvalid) break;
+                if (!same_row) {
+                    if (row + 1 >= c1) {  // entering the prefetched chunk: grab the one after
+                        c0 = nrow;
+                        c1 = min(c0 + kChunkRows, nrows);
+                        if (lane == 0) ncs = atomicAdd(a.next_row + g, kChunkRows);
+                        ncs = __shfl_sync(0xffffffffu, ncs, 0);
+                    }
+                    row = nrow;
+                    mc = mn;
+                    nrow = (row + 1 < c1) ? row + 1 : ncs;
+                    has_next = nrow < nrows;
+                    if (has_next) mn = load_meta<SYM>(a, nrow, F);
+#pragma unroll
+                    for (int r = 0; r < RMAX; ++r) pij[r] = pij_tab[r * 2 * n + mc.i] + pij_tab[r * 2 * n + n + mc.j];
+                }
+                kb = nkb;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) qc[u] = qn[u];
             }
         }
+        __syncthreads();
+        // flush the window into the exact global accumulators
+        unsigned long long* out = a.acc + slot_lo;
+        for (int s = threadIdx.x; s < nslots; s += kBuildThreads) {
+            const unsigned long long v = (static_cast<unsigned long long>(sacc[plane + s]) << 32) | sacc[s];
+            if (v) atomicAdd(out + s, v);
+        }
+        // next type: the one with the most rows left (ties: lowest index)
+        if (threadIdx.x == 0) {
+            int best = -1, left = 0;
+            for (int t = 0; t < a.G; ++t) {
+                const int l = nrows - *((volatile int*)(a.next_row + t));
+                if (l > left) {
+                    left = l;
+                    best = t;
+                }
+            }
+            s_next_g = best;
+            ++switches;
+        }
+        __syncthreads();
+        g = s_next_g;
     }
-    __syncthreads();
-    long long* out = a.partials + (long long)c * a.total_slots + slot_lo;
-    const unsigned long long* limbs = reinterpret_cast<const unsigned long long*>(sacc);  // (lo, hi) pairs
-    for (int s = threadIdx.x; s < nslots; s += kBuildThreads) out[s] = static_cast<long long>(limbs[s]);
+    if (a.trace && threadIdx.x == 0) {
+        unsigned long long t_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        a.trace[3 * blockIdx.x] = t_start;
+        a.trace[3 * blockIdx.x + 1] = t_end;
+        a.trace[3 * blockIdx.x + 2] = switches;
+    }
 }
 
 template <bool SYM, int RMAX>
 static void build_launch(cudaStream_t st, const BuildPlan& p, const BuildArgs& a) {
-    const size_t smem = sizeof(std::uint32_t) * (2 * (size_t)p.slots_per_cta + 3 * (size_t)RMAX * p.n);
-    cudaFuncSetAttribute(k_build_range<SYM, RMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_build_range<SYM, RMAX><<<p.G * p.C, kBuildThreads, smem, st>>>(a);
+    const size_t smem = build_smem_bytes(p.slots_per_cta, RMAX, p.n);
+    cudaFuncSetAttribute(k_build_dyn<SYM, RMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_build_dyn<SYM, RMAX><<<p.P, kBuildThreads, smem, st>>>(a);
     count_launch();
 }
 
@@ -290,27 +392,31 @@ static void build_dispatch(cudaStream_t st, const BuildPlan& p, const BuildArgs&
 }
 
 size_t build_smem_bytes(long long slots_per_cta, int R, int n) {
-    int rm = R <= 1 ? 1 : R <= 2 ? 2 : R <= 4 ? 4 : R <= 8 ? 8 : 16;
-    return sizeof(std::uint32_t) * (2 * (size_t)slots_per_cta + 3 * (size_t)rm * n);
+    const int rm = R <= 1 ? 1 : R <= 2 ? 2 : R <= 4 ? 4 : R <= 8 ? 8 : 16;
+    return sizeof(std::uint32_t) * (2 * ((size_t)slots_per_cta + 32) + 3 * (size_t)rm * n);
 }
 
 void launch_build_main(cudaStream_t st, const void* T, const BuildPlan& p) {
     (void)T;
+    cudaMemsetAsync(p.next_row, 0, sizeof(int) * (size_t)p.G, st);
+    cudaMemsetAsync(p.acc, 0, sizeof(unsigned long long) * (size_t)p.total_slots, st);
     BuildArgs a;
     a.n = p.n;
     a.B = p.B;
+    a.G = p.G;
+    a.nrows = p.nrows;
     a.bmask = p.bmask;
     a.total_slots = p.total_slots;
     a.slots_per_cta = p.slots_per_cta;
-    a.G = p.G;
     a.rowtab = p.rowtab;
     a.rowoff = p.rowoff;
     a.rowF = p.rowF;
     a.qbuf = p.qbuf;
-    a.chunk_begin = p.chunk_begin;
     a.packed = p.packed;
     a.scale_exp = p.scale_exp;
-    a.partials = p.partials;
+    a.next_row = p.next_row;
+    a.acc = p.acc;
+    a.trace = p.trace;
     if (p.sym)
         build_dispatch<true>(st, p, a);
     else
@@ -318,16 +424,16 @@ void launch_build_main(cudaStream_t st, const void* T, const BuildPlan& p) {
 }
 
 // ---- finalize --------------------------------------------------------------------------
-// data += (sum over chunks of partials) * 2^-F. For the symmetric set the slot index is
-// the double index into interleaved (re, im) data; the asymmetric set is real-only.
+// data += acc * 2^-F, skipped entirely when the pre-pass flagged a non-finite entry (the
+// caller then reports the error with the set untouched). For the symmetric set the slot
+// index is the double index into interleaved (re, im) data; the asymmetric set is real-only.
 template <bool SYM>
-__global__ void k_build_finalize(const long long* __restrict__ partials, int C, long long total_slots,
-                                 const int* __restrict__ scale_exp, double* __restrict__ data) {
+__global__ void k_build_finalize(const unsigned long long* __restrict__ acc, long long total_slots,
+                                 const int* __restrict__ scale_exp, const int* __restrict__ nonfinite,
+                                 double* __restrict__ data) {
     const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (s >= total_slots) return;
-    unsigned long long acc = 0;
-    for (int c = 0; c < C; ++c) acc += static_cast<unsigned long long>(partials[(long long)c * total_slots + s]);
-    const long long q = static_cast<long long>(acc);
+    if (s >= total_slots || *nonfinite) return;
+    const long long q = static_cast<long long>(acc[s]);
     if (q == 0) return;
     const double v = ldexp(static_cast<double>(q), -*scale_exp);
     if (SYM)
@@ -338,11 +444,11 @@ __global__ void k_build_finalize(const long long* __restrict__ partials, int C, 
 
 void launch_build_finalize(cudaStream_t st, const BuildPlan& p) {
     if (p.sym)
-        k_build_finalize<true><<<cdiv(p.total_slots, 256), 256, 0, st>>>(p.partials, p.C, p.total_slots, p.scale_exp,
-                                                                         p.data_as_double);
+        k_build_finalize<true><<<cdiv(p.total_slots, 256), 256, 0, st>>>(p.acc, p.total_slots, p.scale_exp,
+                                                                         p.nonfinite, p.data_as_double);
     else
-        k_build_finalize<false><<<cdiv(p.total_slots, 256), 256, 0, st>>>(p.partials, p.C, p.total_slots,
-                                                                          p.scale_exp, p.data_as_double);
+        k_build_finalize<false><<<cdiv(p.total_slots, 256), 256, 0, st>>>(p.acc, p.total_slots, p.scale_exp,
+                                                                          p.nonfinite, p.data_as_double);
     count_launch();
 }
 

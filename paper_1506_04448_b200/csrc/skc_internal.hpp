@@ -72,8 +72,12 @@ struct BuildPlan {
     int dtype;  // 0 f64, 1 f32
     const std::uint32_t* rowtab;  // packed (i << 16 | j) rows of the stream
     int nrows;
-    const int* chunk_begin;  // C+1 row boundaries, device
-    int C, G;                // row chunks x contiguous slot ranges
+    // work split: G contiguous slot ranges ("types"), P persistent CTAs with dynamic
+    // row hand-out per type (next_row counters) and migration between types
+    int P, G;
+    int* next_row;               // G counters
+    unsigned long long* acc;     // total_slots exact fixed-point accumulators
+    unsigned long long* trace;   // optional per-CTA (start, end, switches) (SKC_BUILD_TRACE)
     long long total_slots;   // B x 2b (sym) or B x b (asym)
     int slots_per_cta;
     int R;                   // max replicates a slot range overlaps
@@ -86,7 +90,6 @@ struct BuildPlan {
     double* prepass_partials;     // kPrepassBlocks
     int* scale_exp;               // device int
     int* nonfinite;               // device int
-    long long* partials;          // C x total_slots
     double* data_as_double;       // B x b x 2
 };
 constexpr int kPrepassBlocks = 1024;
