@@ -119,6 +119,7 @@ struct skc_context {
         DevBuf<long long> offs;  // packed-stream offset of each row (= cum[row])
         std::vector<long long> cum;  // cumulative entries per row (host)
         int nrows = 0;
+
     };
     std::map<std::tuple<int, int, int, bool>, std::unique_ptr<RowTab>> rowtabs;
     // scratch
@@ -484,6 +485,11 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
     p.G = G;
     p.next_row = ctx->build_ints.p;
     p.acc = ctx->build_acc.p;
+    static const bool row_variant = [] {
+        const char* e = std::getenv("SKC_BUILD_KERNEL");
+        return e && std::string(e) == "rows";
+    }();
+    p.flat = !row_variant;
     static const bool trace_on = std::getenv("SKC_BUILD_TRACE") != nullptr;
     DevBuf<unsigned long long> trace;
     p.trace = nullptr;

@@ -24,6 +24,8 @@
 // F = 61 - ceil(log2(sum kappa|T|)) from a deterministic pre-pass bounds every bucket.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "skc_host.hpp"
 #include "skc_internal.hpp"
 
@@ -159,8 +161,6 @@ void launch_build_prepass(cudaStream_t st, const void* T, const BuildPlan& p) {
 }
 
 // ---- main pass -----------------------------------------------------------------------
-constexpr int kBuildThreads = 1024;
-constexpr int kWarps = kBuildThreads / 32;
 constexpr int kChunkRows = 16;  // rows per warp-level grab
 
 // Exact 64-bit add of (ql, qh) into the limb pair (lo at addr_lo, hi at addr_hi). The
@@ -179,6 +179,31 @@ __device__ __forceinline__ void add64(std::uint32_t addr_lo, std::uint32_t addr_
         "r"(addr_hi), "r"(ql), "r"(qh));
 }
 
+// Same add with the limb addresses formed inside the asm block from an opaque window
+// base (the compiler otherwise re-derives the shared-window base per use).
+__device__ __forceinline__ void add64_idx(std::uint32_t idx, std::uint32_t sbase, std::uint32_t hioff, std::uint32_t ql,
+                                          std::uint32_t qh) {
+    asm volatile(
+        "{\n\t.reg .u32 al, ah, old, c;\n\t"
+        "mad.lo.u32 al, %0, 4, %1;\n\t"
+        "add.u32 ah, al, %2;\n\t"
+        "atom.shared.add.u32 old, [al], %3;\n\t"
+        "add.cc.u32 c, old, %3;\n\t"
+        "addc.u32 c, %4, 0;\n\t"
+        "red.shared.add.u32 [ah], c;\n\t}" ::"r"(idx),
+        "r"(sbase), "r"(hioff), "r"(ql), "r"(qh));
+}
+__device__ __forceinline__ std::uint32_t lds_u32(std::uint32_t addr) {
+    std::uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+template <typename T>
+__device__ __forceinline__ T pin(T v) {  // opaque copy: keeps a kernel constant in a register
+    asm volatile("mov.b32 %0, %0;" : "+r"(v));
+    return v;
+}
+
 struct BuildArgs {
     int n, B, G, nrows;
     std::uint32_t bmask;
@@ -190,7 +215,8 @@ struct BuildArgs {
     const long long* qbuf;
     const std::uint32_t* packed;
     const int* scale_exp;
-    int* next_row;                 // G row counters (zeroed per build)
+    int* next_row;                 // G row (or tile) counters (zeroed per build)
+
     unsigned long long* acc;       // total_slots exact accumulators (zeroed per build)
     unsigned long long* trace;     // optional: per-CTA (start, end, switches)
 };
@@ -227,8 +253,9 @@ __device__ __forceinline__ void load_block(long long (&q)[4], const long long* q
 // to the type with the most rows left. Each warp walks its rows software-pipelined: the
 // next 128-entry block's loads are issued before the current block is processed, the
 // next row's metadata one row ahead and the next chunk grab one chunk ahead.
-template <bool SYM, int RMAX>
-__global__ void __launch_bounds__(kBuildThreads, 1) k_build_dyn(BuildArgs a) {
+template <bool SYM, int RMAX, int NT>
+__global__ void __launch_bounds__(NT, 1) k_build_dyn(BuildArgs a) {
+    constexpr int kBuildThreads = NT;
     extern __shared__ std::uint32_t sacc[];
     __shared__ int s_next_g;
     const int spc = a.slots_per_cta;
@@ -239,7 +266,8 @@ __global__ void __launch_bounds__(kBuildThreads, 1) k_build_dyn(BuildArgs a) {
     const long long spr = SYM ? 2ll * (a.bmask + 1) : static_cast<long long>(a.bmask + 1);
     const int prow = SYM ? n : 3 * n;
     const int F = *a.scale_exp;
-    const std::uint32_t sbase = static_cast<std::uint32_t>(__cvta_generic_to_shared(sacc));
+    std::uint32_t sbase = static_cast<std::uint32_t>(__cvta_generic_to_shared(sacc));
+    asm volatile("mov.b32 %0, %0;" : "+r"(sbase));  // keep in a register (no per-use S2UR/ULEA)
     const std::uint32_t hioff = 4u * static_cast<std::uint32_t>(plane);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const std::uint32_t trash_idx = static_cast<std::uint32_t>(spc + lane);
@@ -369,11 +397,200 @@ __global__ void __launch_bounds__(kBuildThreads, 1) k_build_dyn(BuildArgs a) {
     }
 }
 
+// Flat-chunk variant of the persistent build (default). A warp grabs a chunk of up to 16
+// consecutive rows, stages their metadata (relative start, k offset, exponent shift,
+// row-pair hash words) in its slice of shared memory, and then streams the chunk's
+// entries as one contiguous run of qbuf: lane e handles entries e, e+32, ... regardless
+// of row boundaries, advancing its row cursor when it crosses one. Short rows no longer
+// leave lanes idle, the 128-entry loads are independent of row bookkeeping (the next
+// block is prefetched before the current one is processed), and the per-row work is a
+// few shared-memory reads per crossing lane.
+constexpr int kFlatRows = 16;
+__host__ __device__ constexpr int flat_meta_words(int rmax) { return (kFlatRows + 1) + 2 * kFlatRows + rmax * kFlatRows; }
+
+template <bool SYM, int RMAX>
+__global__ void __launch_bounds__(1024, 1) k_build_flat(BuildArgs a) {
+    constexpr int NT = 1024;
+    extern __shared__ std::uint32_t sacc[];
+    __shared__ int s_next_g;
+    const int spc = a.slots_per_cta;
+    const int plane = spc + 32;
+    std::uint32_t* ptab = sacc + 2 * plane;
+    std::uint32_t* pij_tab = ptab + RMAX * a.n;
+    const int n = a.n, nrows = a.nrows;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // per-warp chunk metadata
+    std::uint32_t* wm = pij_tab + RMAX * 2 * n + warp * flat_meta_words(RMAX);
+    std::uint32_t* m_start = wm;                       // kFlatRows + 1 (relative starts, last = E)
+    int* m_kofs = reinterpret_cast<int*>(wm + kFlatRows + 1);
+    int* m_d = m_kofs + kFlatRows;
+    std::uint32_t* m_pij = reinterpret_cast<std::uint32_t*>(m_d + kFlatRows);  // RMAX x kFlatRows
+    const long long spr = SYM ? 2ll * (a.bmask + 1) : static_cast<long long>(a.bmask + 1);
+    const int prow = SYM ? n : 3 * n;
+    const int F = *a.scale_exp;
+    std::uint32_t sbase = static_cast<std::uint32_t>(__cvta_generic_to_shared(sacc));
+    asm volatile("mov.b32 %0, %0;" : "+r"(sbase));  // keep in a register (no per-use S2UR/ULEA)
+    const std::uint32_t hioff = 4u * static_cast<std::uint32_t>(plane);
+    const std::uint32_t trash_idx = static_cast<std::uint32_t>(spc + lane);
+    unsigned long long t_start = 0, switches = 0;
+    if (a.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+
+    int g = static_cast<int>((static_cast<long long>(blockIdx.x) * a.G) / gridDim.x);
+    while (g >= 0) {
+        const long long slot_lo = (long long)g * spc;
+        const long long slot_hi = min(slot_lo + spc, a.total_slots);
+        const int nslots = static_cast<int>(slot_hi - slot_lo);
+        const int m_lo = static_cast<int>(slot_lo / spr);
+        const int R = static_cast<int>((slot_hi - 1) / spr) - m_lo + 1;
+        for (int s = threadIdx.x; s < 2 * plane; s += NT) sacc[s] = 0u;
+        for (int x = threadIdx.x; x < RMAX * n; x += NT) {
+            const int r = x / n, k = x - r * n;
+            const std::uint32_t* pm = a.packed + (size_t)(m_lo + min(r, R - 1)) * prow;
+            ptab[x] = pm[(SYM ? 0 : 2 * n) + k];
+            pij_tab[r * 2 * n + k] = pm[k];
+            pij_tab[r * 2 * n + n + k] = pm[(SYM ? 0 : n) + k];
+        }
+        __syncthreads();
+        std::uint32_t base[RMAX];
+#pragma unroll
+        for (int r = 0; r < RMAX; ++r) base[r] = pin(static_cast<std::uint32_t>((long long)(m_lo + r) * spr - slot_lo));
+        const std::uint32_t nsl = pin(static_cast<std::uint32_t>(nslots));
+        const std::uint32_t bmask = pin(a.bmask);
+        const std::uint32_t n4 = pin(4u * static_cast<std::uint32_t>(n));
+        const std::uint32_t ptab_s = pin(sbase + 4u * static_cast<std::uint32_t>(2 * plane));
+
+        int c0 = 0;
+        if (lane == 0) c0 = atomicAdd(a.next_row + g, kFlatRows);
+        c0 = __shfl_sync(0xffffffffu, c0, 0);
+        while (c0 < nrows) {
+            int cn = 0;  // next grab, one chunk ahead
+            if (lane == 0) cn = atomicAdd(a.next_row + g, kFlatRows);
+            const int nr = min(kFlatRows, nrows - c0);
+            // stage the chunk's row metadata (lane l -> row c0 + l)
+            long long off = 0;
+            int len = 0;
+            if (lane < nr) {
+                const int row = c0 + lane;
+                const std::uint32_t ij = __ldg(a.rowtab + row);
+                off = __ldg(a.rowoff + row);
+                const int i = static_cast<int>(ij >> 16), j = static_cast<int>(ij & 0xFFFFu);
+                len = SYM ? n - j : n;
+                m_d[lane] = static_cast<int>(__ldg(a.rowF + row)) - F;
+#pragma unroll
+                for (int r = 0; r < RMAX; ++r) m_pij[r * kFlatRows + lane] = pij_tab[r * 2 * n + i] + pij_tab[r * 2 * n + n + j];
+                m_kofs[lane] = SYM ? j : 0;  // relative start subtracted below
+            }
+            const long long off0 = __shfl_sync(0xffffffffu, off, 0);
+            const int rel = static_cast<int>(off - off0);
+            const int E = __shfl_sync(0xffffffffu, rel + len, nr - 1);
+            if (lane < nr) {
+                m_start[lane] = static_cast<std::uint32_t>(rel);
+                m_kofs[lane] -= rel;
+            }
+            if (lane == 0) m_start[nr] = static_cast<std::uint32_t>(E);
+            __syncwarp();
+            const long long* qch = a.qbuf + off0;
+            int t = 0;
+            int cur_end = static_cast<int>(m_start[1]);
+            int kofs = m_kofs[0], d = m_d[0];
+            std::uint32_t pij[RMAX];
+#pragma unroll
+            for (int r = 0; r < RMAX; ++r) pij[r] = m_pij[r * kFlatRows];
+            long long qc[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) qc[u] = (lane + 32 * u < E) ? __ldg(qch + lane + 32 * u) : 0ll;
+            for (int eb = 0; eb < E; eb += 128) {
+                long long qn[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int e = eb + 128 + lane + 32 * u;
+                    qn[u] = (e < E) ? __ldg(qch + e) : 0ll;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int e = eb + lane + 32 * u;
+                    if (eb + 32 * u >= E) break;  // warp-uniform
+                    if (e < E) {
+                        while (e >= cur_end) {  // crossed into the next row of the chunk
+                            ++t;
+                            cur_end = static_cast<int>(m_start[t + 1]);
+                            kofs = m_kofs[t];
+                            d = m_d[t];
+#pragma unroll
+                            for (int r = 0; r < RMAX; ++r) pij[r] = m_pij[r * kFlatRows + t];
+                        }
+                        const std::uint32_t kaddr = ptab_s + 4u * static_cast<std::uint32_t>(e + kofs);
+                        // zero entries add nothing (sketch.cpp:337 skips them)
+                        const unsigned long long qq = static_cast<unsigned long long>(qc[u] >> d);
+                        const unsigned long long nq = 0ull - qq;
+                        const std::uint32_t ql = static_cast<std::uint32_t>(qq), qh = static_cast<std::uint32_t>(qq >> 32);
+                        const std::uint32_t nql = static_cast<std::uint32_t>(nq), nqh = static_cast<std::uint32_t>(nq >> 32);
+#pragma unroll
+                        for (int r = 0; r < RMAX; ++r) {
+                            if (r < R) {  // CTA-uniform
+                                const std::uint32_t p = pij[r] + lds_u32(kaddr + static_cast<std::uint32_t>(r) * n4);
+                                const std::uint32_t s = base[r] + (SYM ? (((p & bmask) << 1) | ((p >> 30) & 1u)) : (p & bmask));
+                                const bool neg = static_cast<int>(p) < 0;
+                                add64_idx(s < nsl ? s : trash_idx, sbase, hioff, neg ? nql : ql, neg ? nqh : qh);
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) qc[u] = qn[u];
+            }
+            __syncwarp();  // metadata slice reused by the next chunk
+            c0 = __shfl_sync(0xffffffffu, cn, 0);
+        }
+        __syncthreads();
+        unsigned long long* out = a.acc + slot_lo;
+        for (int s = threadIdx.x; s < nslots; s += NT) {
+            const unsigned long long v = (static_cast<unsigned long long>(sacc[plane + s]) << 32) | sacc[s];
+            if (v) atomicAdd(out + s, v);
+        }
+        if (threadIdx.x == 0) {
+            int best = -1, left = 0;
+            for (int tt = 0; tt < a.G; ++tt) {
+                const int l = nrows - *((volatile int*)(a.next_row + tt));
+                if (l > left) {
+                    left = l;
+                    best = tt;
+                }
+            }
+            s_next_g = best;
+            ++switches;
+        }
+        __syncthreads();
+        g = s_next_g;
+    }
+    if (a.trace && threadIdx.x == 0) {
+        unsigned long long t_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        a.trace[3 * blockIdx.x] = t_start;
+        a.trace[3 * blockIdx.x + 1] = t_end;
+        a.trace[3 * blockIdx.x + 2] = switches;
+    }
+}
+
+// Threads per CTA: 1024 (32 warps, 64 registers) by default; SKC_BUILD_NT=512 trades
+// warps for registers (experiment hook).
 template <bool SYM, int RMAX>
 static void build_launch(cudaStream_t st, const BuildPlan& p, const BuildArgs& a) {
+    static const int nt = [] {
+        const char* e = std::getenv("SKC_BUILD_NT");
+        return (e && std::atoi(e) == 512) ? 512 : 1024;
+    }();
     const size_t smem = build_smem_bytes(p.slots_per_cta, RMAX, p.n);
-    cudaFuncSetAttribute(k_build_dyn<SYM, RMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_build_dyn<SYM, RMAX><<<p.P, kBuildThreads, smem, st>>>(a);
+    if (p.flat) {
+        cudaFuncSetAttribute(k_build_flat<SYM, RMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_build_flat<SYM, RMAX><<<p.P, 1024, smem, st>>>(a);
+    } else if (nt == 512) {
+        cudaFuncSetAttribute(k_build_dyn<SYM, RMAX, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_build_dyn<SYM, RMAX, 512><<<p.P, 512, smem, st>>>(a);
+    } else {
+        cudaFuncSetAttribute(k_build_dyn<SYM, RMAX, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_build_dyn<SYM, RMAX, 1024><<<p.P, 1024, smem, st>>>(a);
+    }
     count_launch();
 }
 
@@ -393,7 +610,8 @@ static void build_dispatch(cudaStream_t st, const BuildPlan& p, const BuildArgs&
 
 size_t build_smem_bytes(long long slots_per_cta, int R, int n) {
     const int rm = R <= 1 ? 1 : R <= 2 ? 2 : R <= 4 ? 4 : R <= 8 ? 8 : 16;
-    return sizeof(std::uint32_t) * (2 * ((size_t)slots_per_cta + 32) + 3 * (size_t)rm * n);
+    return sizeof(std::uint32_t) *
+           (2 * ((size_t)slots_per_cta + 32) + 3 * (size_t)rm * n + 32 * (size_t)flat_meta_words(rm));
 }
 
 void launch_build_main(cudaStream_t st, const void* T, const BuildPlan& p) {
@@ -416,6 +634,7 @@ void launch_build_main(cudaStream_t st, const void* T, const BuildPlan& p) {
     a.scale_exp = p.scale_exp;
     a.next_row = p.next_row;
     a.acc = p.acc;
+
     a.trace = p.trace;
     if (p.sym)
         build_dispatch<true>(st, p, a);

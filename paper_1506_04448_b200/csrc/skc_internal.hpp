@@ -76,6 +76,7 @@ struct BuildPlan {
     // row hand-out per type (next_row counters) and migration between types
     int P, G;
     int* next_row;               // G counters
+    bool flat;                   // flat-chunk kernel (default) or the row-walk kernel
     unsigned long long* acc;     // total_slots exact fixed-point accumulators
     unsigned long long* trace;   // optional per-CTA (start, end, switches) (SKC_BUILD_TRACE)
     long long total_slots;   // B x 2b (sym) or B x b (asym)
