@@ -218,6 +218,7 @@ struct skc_sym_set {
     DevBuf<std::uint64_t> d_hcoef, d_scoef;
     DevBuf<std::uint32_t> bucket1, bucket2, bucket3, packed, perm1, perm2;
     DevBuf<uint2> plan1, plan2;
+    DevBuf<double2> stw1, stw2, gtw1, gtw2;  // residue twiddle tables (may stay empty)
     DevBuf<std::uint8_t> sexp;
     DevBuf<double2> data, spec;
     int N = 2, logN = 1, S = 1;
@@ -244,6 +245,10 @@ struct skc_sym_set {
         v.plan2 = plan2.p;
         v.data = data.p;
         v.spec = spec.p;
+        v.stw1 = stw1.p;
+        v.stw2 = stw2.p;
+        v.gtw1 = gtw1.p;
+        v.gtw2 = gtw2.p;
         return v;
     }
     // contraction.cpp:62-72: refresh cached spectra when the version moved.
@@ -346,6 +351,23 @@ void init_sym_device(skc_sym_set* s, const double* data_host) {
     launch_make_plan(st, s->perm1.p, s->bucket1.p, s->sexp.p, 1, nullptr, s->B, s->n, s->plan1.p);
     launch_make_plan(st, s->perm2.p, s->bucket2.p, s->sexp.p, 2, nullptr, s->B, s->n, s->plan2.p);
     ctx->check_launch();
+    {
+        // residue twiddles for the contraction scatter/gather (coalesced instead of
+        // dependent random reads of the b-entry table); skipped above 256 MB
+        const size_t cnt = static_cast<size_t>(s->B) * s->S * s->n;
+        if (4 * cnt * sizeof(double2) <= (size_t(256) << 20)) {
+            s->stw1.alloc(cnt);
+            s->stw2.alloc(cnt);
+            s->gtw1.alloc(cnt);
+            s->gtw2.alloc(cnt);
+            ctx->tw(s->b);
+            SymView v = s->view();
+            v.data = nullptr;
+            v.spec = nullptr;
+            launch_sym_twiddle_tables(st, v, s->stw1.p, s->stw2.p, s->gtw1.p, s->gtw2.p);
+            ctx->check_launch();
+        }
+    }
     const size_t Bb = static_cast<size_t>(s->B) * s->b;
     s->data.alloc(Bb);
     s->spec.alloc(Bb);

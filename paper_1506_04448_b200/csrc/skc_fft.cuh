@@ -143,13 +143,13 @@ SKC_HD void dif_pass_item(double2* x, int w, int h, const double2* tw, int logb)
     double2 v[R];
 #pragma unroll
     for (int q = 0; q < R; ++q) v[q] = x[pad16(base + q * g)];
+    // stage twiddles: w_{2h}^{-pos} from the table, then w_{2hs}^{-pos} = (w_{2h}^{-pos})^(2^s)
+    // by repeated squaring (one table read per item instead of LOGR)
+    double2 W = conj(tw[static_cast<unsigned>(pos) << (logb - ilog2(static_cast<unsigned>(2 * h)))]);
 #pragma unroll
     for (int s = 0; s < LOGR; ++s) {
-        const int hs = h >> s;
         const int Hq = R >> (s + 1);
-        // w_{2hs}^{-pos} = conj(tw[pos * b / (2 hs)])
-        const int lg2hs = ilog2(static_cast<unsigned>(2 * hs));
-        double2 W = conj(tw[static_cast<unsigned>(pos) << (logb - lg2hs)]);
+        if (s > 0) W = cmul(W, W);
 #pragma unroll
         for (int q = 0; q < R; ++q) {
             if (q & Hq) continue;
@@ -176,12 +176,15 @@ SKC_HD void dit_pass_item(double2* x, int w, int h, const double2* tw, int logb)
     double2 v[R];
 #pragma unroll
     for (int q = 0; q < R; ++q) v[q] = x[pad16(base + q * g)];
+    // stage twiddles w_{2hs}^{pos}, s = 0..LOGR-1, by repeated squaring of w_{2h}^{pos}
+    double2 Ws[LOGR];
+    Ws[0] = tw[static_cast<unsigned>(pos) << (logb - ilog2(static_cast<unsigned>(2 * h)))];
+#pragma unroll
+    for (int s = 1; s < LOGR; ++s) Ws[s] = cmul(Ws[s - 1], Ws[s - 1]);
 #pragma unroll
     for (int s = LOGR - 1; s >= 0; --s) {
-        const int hs = h >> s;
         const int Hq = R >> (s + 1);
-        const int lg2hs = ilog2(static_cast<unsigned>(2 * hs));
-        double2 W = tw[static_cast<unsigned>(pos) << (logb - lg2hs)];
+        const double2 W = Ws[s];
 #pragma unroll
         for (int q = 0; q < R; ++q) {
             if (q & Hq) continue;

@@ -29,6 +29,12 @@ struct SymView {
     const uint2* plan2;  // B x n: (i, 2h_i mod b | 2e_i << 28) sorted by (2h_i mod N, i)
     const double2* data;         // B x b time domain
     const double2* spec;         // B x S x N local bit-reversed spectra
+    // residue twiddles per (m, r): scatter (plan order) conj(w_b^{r t}), gather (index
+    // order) w_b^{r t}; B x S x n each, or null (then taken from tw on the fly)
+    const double2* stw1;
+    const double2* stw2;
+    const double2* gtw1;
+    const double2* gtw2;
 };
 
 struct AsymView {
@@ -98,6 +104,10 @@ size_t build_smem_bytes(long long slots_per_cta, int R, int n);
 void launch_build_prepass(cudaStream_t st, const void* T, const BuildPlan& p);
 void launch_build_main(cudaStream_t st, const void* T, const BuildPlan& p);
 void launch_build_finalize(cudaStream_t st, const BuildPlan& p);
+
+// residue twiddle tables of a symmetric set (SymView::stw*/gtw*)
+void launch_sym_twiddle_tables(cudaStream_t st, const SymView& v, double2* stw1, double2* stw2, double2* gtw1,
+                               double2* gtw2);
 
 // spectra: spec[m][r][j] = local DIF of residue r of data[m]
 void launch_spectrum(cudaStream_t st, const double2* data, std::uint32_t b, int logb, int B, int N, int logN,

@@ -269,6 +269,29 @@ void launch_make_plan(cudaStream_t st, const std::uint32_t* perm, const std::uin
     SKC_LAUNCHED();
 }
 
+// Residue twiddles of the symmetric contraction scatter/gather, per (m, r, q).
+__global__ void k_sym_twiddle_tables(SymView v, double2* __restrict__ stw1, double2* __restrict__ stw2,
+                                     double2* __restrict__ gtw1, double2* __restrict__ gtw2) {
+    const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long tot = (long long)v.B * v.S * v.n;
+    if (idx >= tot) return;
+    const int q = static_cast<int>(idx % v.n);
+    const int r = static_cast<int>((idx / v.n) % v.S);
+    const int m = static_cast<int>(idx / ((long long)v.n * v.S));
+    const std::uint32_t bmask = v.b - 1, ur = static_cast<std::uint32_t>(r);
+    const size_t mq = (size_t)m * v.n + q;
+    stw1[idx] = conj(v.tw[(ur * (v.plan1[mq].y & 0x0FFFFFFFu)) & bmask]);
+    stw2[idx] = conj(v.tw[(ur * (v.plan2[mq].y & 0x0FFFFFFFu)) & bmask]);
+    gtw1[idx] = v.tw[(ur * v.bucket1[mq]) & bmask];
+    gtw2[idx] = v.tw[(ur * v.bucket2[mq]) & bmask];
+}
+void launch_sym_twiddle_tables(cudaStream_t st, const SymView& v, double2* stw1, double2* stw2, double2* gtw1,
+                               double2* gtw2) {
+    const long long tot = (long long)v.B * v.S * v.n;
+    k_sym_twiddle_tables<<<cdiv(tot, 256), 256, 0, st>>>(v, stw1, stw2, gtw1, gtw2);
+    SKC_LAUNCHED();
+}
+
 // ============================ K4: spectra ========================================
 // contraction.cpp:62-72 (ensure_fresh): F(data_m) for all m, in local residue layout.
 template <int LOGN>
@@ -485,6 +508,7 @@ __device__ __forceinline__ void sym_contract_half_body(const SymView& v, const d
     double2* Bh = sm + strideA;
     double2* scr = Bh + strideB;                                           // 2n
     std::uint32_t* keys = reinterpret_cast<std::uint32_t*>(scr + 2 * n);  // 2n
+    double* us = reinterpret_cast<double*>(keys + 2 * n);  // n (2n u32 keep 8-byte alignment)
     const std::uint32_t bmask = v.b - 1;
     const std::uint32_t nmask = static_cast<std::uint32_t>(N - 1);
     const double2* fT = v.spec + ((size_t)m * S + r) * N;
@@ -496,17 +520,24 @@ __device__ __forceinline__ void sym_contract_half_body(const SymView& v, const d
     const std::uint8_t* se = v.sexp + (size_t)m * n;
     const double2* dm = v.data + (size_t)m * v.b;
 
+    const size_t mr = ((size_t)m * S + r) * n;  // residue-twiddle table offset of (m, r)
+    const bool ttab = v.stw1 != nullptr;
     for (int l = l0; l < min(L, l0 + kLPB); ++l) {
-        const double* u = U + (size_t)l * n;
+        const double* ug = U + (size_t)l * n;
+        for (int x = threadIdx.x; x < n; x += NT) us[x] = ug[x];  // u staged once per restart
         zero_smem(sm, strideA + strideB);
+        __syncthreads();
         // phase 1 of the two-phase scatter (contraction.cpp:150-154): every contribution
         // val * w_b^{-r t} independently into scratch, keys = local position (f2: halved)
         for (int x = threadIdx.x; x < 2 * n; x += NT) {
             const bool hb = x >= n;
-            const uint2 e = hb ? p2[x - n] : p1[x];
-            const double ui = u[e.x];
+            const int q = hb ? x - n : x;
+            const uint2 e = hb ? p2[q] : p1[q];
+            const double ui = us[e.x];
             const double2 val = root4_times(e.y >> 28, hb ? ui * ui : ui);
-            scr[x] = cmul(val, conj(v.tw[(static_cast<std::uint32_t>(r) * (e.y & 0x0FFFFFFFu)) & bmask]));
+            const double2 w = ttab ? (hb ? v.stw2 : v.stw1)[mr + q]
+                                   : conj(v.tw[(static_cast<std::uint32_t>(r) * (e.y & 0x0FFFFFFFu)) & bmask]);
+            scr[x] = cmul(val, w);
             keys[x] = hb ? ((e.y & nmask) >> 1) : (e.y & nmask);
         }
         __syncthreads();
@@ -538,10 +569,12 @@ __device__ __forceinline__ void sym_contract_half_body(const SymView& v, const d
             double* o = out + (((size_t)l * B + m) * S + r) * n;
             for (int i = threadIdx.x; i < n; i += NT) {
                 const unsigned e = se[i];
-                const double ui = u[i];
+                const double ui = us[i];
                 const std::uint32_t t1 = b1[i], t2 = b2[i];
-                const double2 z1 = cmul(A[pad16(static_cast<int>(t1 & nmask))], v.tw[(static_cast<std::uint32_t>(r) * t1) & bmask]);
-                const double2 z2 = cmul(Bh[pad16(static_cast<int>((t2 & nmask) >> 1))], v.tw[(static_cast<std::uint32_t>(r) * t2) & bmask]);
+                const double2 w1 = ttab ? v.gtw1[mr + i] : v.tw[(static_cast<std::uint32_t>(r) * t1) & bmask];
+                const double2 w2 = ttab ? v.gtw2[mr + i] : v.tw[(static_cast<std::uint32_t>(r) * t2) & bmask];
+                const double2 z1 = cmul(A[pad16(static_cast<int>(t1 & nmask))], w1);
+                const double2 z2 = cmul(Bh[pad16(static_cast<int>((t2 & nmask) >> 1))], w2);
                 double val = re_rot_conj(e, z1) * (1.0 / 6.0) * inv_b;
                 val += ui * re_rot_conj(2u * e, z2) * (1.0 / 3.0) * inv_b;
                 if (r == 0) val += ui * ui * re_rot_conj(3u * e, dm[b3[i]]) * (1.0 / 3.0);
@@ -561,7 +594,7 @@ __device__ __forceinline__ void sym_contract_half_body(const SymView& v, const d
             double term3 = 0.0;
             if (r == 0) {  // contraction.cpp:117-121
                 for (int i = threadIdx.x; i < n; i += NT) {
-                    const double u3 = u[i] * u[i] * u[i];
+                    const double u3 = us[i] * us[i] * us[i];
                     term3 += u3 * re_rot_conj(3u * se[i], dm[b3[i]]);
                 }
             }
@@ -638,7 +671,8 @@ void launch_sym_contract(cudaStream_t st, const SymView& v, const double* U, int
     if (var >= 3) {
         const int NH = v.N / 2;
         const size_t smem = sizeof(double2) * (padded_len(v.N) + (NH + NH / 16 + 1)) +
-                            (sizeof(double2) + sizeof(std::uint32_t)) * 2 * (size_t)v.n;
+                            (sizeof(double2) + sizeof(std::uint32_t)) * 2 * (size_t)v.n +
+                            sizeof(double) * ((size_t)v.n + 1);
         const unsigned grid = (unsigned)((long long)((L + kLPB - 1) / kLPB) * v.B * v.S);
 #define LH_(LG) sym_contract_half_dispatch<LG>(st, v, U, L, mode, out, grid, smem, var)
         switch (v.logN) {
