@@ -195,11 +195,14 @@ __device__ __forceinline__ void scatter_plan(double2* y, const uint2* __restrict
 // scratch (all loads in flight), phase 2 lets each run head sum its run in plan order.
 // scratch: 2*n double2 + 2*n keys; n <= kScatterMax.
 constexpr int kScatterMax = 1024;
+// stwA/stwB (optional): the plan-order residue twiddles conj(w_b^{r t}) of this (m, r)
+// (SymView::stw*), read coalesced instead of from the b-entry table.
 template <typename ValA, typename ValB>
 __device__ __forceinline__ void scatter2(double2* yA, const uint2* __restrict__ planA, ValA valA, double2* yB,
                                          const uint2* __restrict__ planB, ValB valB, int n, int N, int r,
                                          std::uint32_t bmask, std::uint32_t tmask, const double2* __restrict__ tw,
-                                         double2* scr, std::uint32_t* keys) {
+                                         double2* scr, std::uint32_t* keys, const double2* __restrict__ stwA = nullptr,
+                                         const double2* __restrict__ stwB = nullptr) {
     const std::uint32_t nmask = static_cast<std::uint32_t>(N - 1);
     const int tot = yB ? 2 * n : n;
     for (int x = threadIdx.x; x < tot; x += blockDim.x) {
@@ -207,7 +210,9 @@ __device__ __forceinline__ void scatter2(double2* yA, const uint2* __restrict__ 
         const uint2 e = b ? planB[x - n] : planA[x];
         const double2 v = b ? valB(e.x, e.y) : valA(e.x, e.y);
         const std::uint32_t t = e.y & tmask;
-        scr[x] = cmul(v, conj(tw[(static_cast<std::uint32_t>(r) * t) & bmask]));
+        const double2* st = b ? stwB : stwA;
+        const double2 w = st ? st[b ? x - n : x] : conj(tw[(static_cast<std::uint32_t>(r) * t) & bmask]);
+        scr[x] = cmul(v, w);
         keys[x] = e.y & nmask;
     }
     __syncthreads();
@@ -868,7 +873,8 @@ __global__ void __launch_bounds__(kFftThreads, SKC_FFT_MINB)
         __syncthreads();
         auto vx = [&](std::uint32_t i, std::uint32_t y) { return root4_times(y >> 28, x[i]); };
         if (SCR)
-            scatter2(A, plan, vx, static_cast<double2*>(nullptr), plan, vx, n, N, r, bmask, 0x0FFFFFFFu, v.tw, scr, keys);
+            scatter2(A, plan, vx, static_cast<double2*>(nullptr), plan, vx, n, N, r, bmask, 0x0FFFFFFFu, v.tw, scr, keys,
+                     v.stw1 ? v.stw1 + ((size_t)m * S + r) * n : nullptr);
         else
             scatter_plan(A, plan, n, N, r, bmask, 0x0FFFFFFFu, v.tw, vx);
         __syncthreads();

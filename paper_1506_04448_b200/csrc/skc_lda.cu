@@ -33,14 +33,17 @@ __device__ __forceinline__ void zero_sm(double2* sm, int count) {
 template <typename ValA, typename ValB>
 __device__ __forceinline__ void scatter_dense2(double2* yA, ValA valA, double2* yB, ValB valB, const uint2* __restrict__ plan,
                                                int n, int N, int r, std::uint32_t bmask, const double2* __restrict__ tw,
-                                               double2* scr, std::uint32_t* keys) {
+                                               double2* scr, std::uint32_t* keys, const double2* __restrict__ stw) {
     const std::uint32_t nmask = static_cast<std::uint32_t>(N - 1);
     const int tot = yB ? 2 * n : n;
     for (int x = threadIdx.x; x < tot; x += blockDim.x) {
         const bool b = x >= n;
-        const uint2 e = plan[b ? x - n : x];
+        const int q = b ? x - n : x;
+        const uint2 e = plan[q];
         const double val = b ? valB(e.x) : valA(e.x);
-        scr[x] = cmul(root4_times(e.y >> 28, val), conj(tw[(static_cast<std::uint32_t>(r) * (e.y & 0x0FFFFFFFu)) & bmask]));
+        // plan-order residue twiddle of this (m, r) when the set has the table (coalesced)
+        const double2 w = stw ? stw[q] : conj(tw[(static_cast<std::uint32_t>(r) * (e.y & 0x0FFFFFFFu)) & bmask]);
+        scr[x] = cmul(root4_times(e.y >> 28, val), w);
         keys[x] = e.y & nmask;
     }
     __syncthreads();
@@ -56,8 +59,8 @@ __device__ __forceinline__ void scatter_dense2(double2* yA, ValA valA, double2* 
 template <typename ValFn>
 __device__ __forceinline__ void scatter_dense(double2* y, const uint2* __restrict__ plan, int n, int N, int r,
                                               std::uint32_t bmask, const double2* __restrict__ tw, ValFn val,
-                                              double2* scr, std::uint32_t* keys) {
-    scatter_dense2(y, val, static_cast<double2*>(nullptr), val, plan, n, N, r, bmask, tw, scr, keys);
+                                              double2* scr, std::uint32_t* keys, const double2* __restrict__ stw) {
+    scatter_dense2(y, val, static_cast<double2*>(nullptr), val, plan, n, N, r, bmask, tw, scr, keys, stw);
 }
 }  // namespace
 
@@ -162,6 +165,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     double2* scr = CR + N;                                                 // 2n
     std::uint32_t* keys = reinterpret_cast<std::uint32_t*>(scr + 2 * n);  // 2n
     const uint2* plan = v.plan1 + (size_t)m * n;
+    const double2* stw = v.stw1 ? v.stw1 + ((size_t)m * S + r) * n : nullptr;
     const std::uint32_t bmask = v.b - 1;
     const long long items = Dn + V;
     const long long per = (items + chunks - 1) / chunks;
@@ -174,13 +178,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncthreads();
         if (doc) {
             const double* p = P + (size_t)it * n;
-            scatter_dense(A, plan, n, N, r, bmask, v.tw, [&](std::uint32_t i) { return p[i]; }, scr, keys);
+            scatter_dense(A, plan, n, N, r, bmask, v.tw, [&](std::uint32_t i) { return p[i]; }, scr, keys, stw);
         } else {
             const long long w = it - Dn;
             const double* wr = W + (size_t)w * n;
             const double* sr = sumwn + (size_t)w * n;
             scatter_dense2(A, [&](std::uint32_t i) { return wr[i]; }, Bw, [&](std::uint32_t i) { return sr[i]; }, plan, n, N,
-                           r, bmask, v.tw, scr, keys);
+                           r, bmask, v.tw, scr, keys, stw);
         }
         __syncthreads();
         dif_local<LOGN>(sm, doc ? 1 : 2, v.twl);
@@ -223,7 +227,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     std::uint32_t* keys = reinterpret_cast<std::uint32_t*>(scr + 2 * n);
     zero_sm(sm, N + (N >> 4) + 1);
     __syncthreads();
-    scatter_dense(sm, v.plan1 + (size_t)m * n, n, N, r, v.b - 1, v.tw, [&](std::uint32_t i) { return q[i]; }, scr, keys);
+    scatter_dense(sm, v.plan1 + (size_t)m * n, n, N, r, v.b - 1, v.tw, [&](std::uint32_t i) { return q[i]; }, scr, keys,
+                  v.stw1 ? v.stw1 + ((size_t)m * S + r) * n : nullptr);
     __syncthreads();
     dif_local<LOGN>(sm, 1, v.twl);
     const double2* ai = reinterpret_cast<const double2*>(acc_in);
