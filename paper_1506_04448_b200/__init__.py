@@ -320,10 +320,15 @@ class SymTensorSketchSet:
         hc, sc = self.coefficients()
         return SymReplicate(b1, b2, b3, se, hc[m], sc[m], self.data(m))
 
-    def data(self, m: int | None = None) -> np.ndarray:
-        """replicate(m).data (or all B replicates as a (B, b) array)."""
+    def data(self, m: int | None = None, out: np.ndarray | None = None) -> np.ndarray:
+        """replicate(m).data (or all B replicates as a (B, b) array). `out`: optional
+        preallocated complex128 array of that shape (e.g. pinned host memory)."""
         b, B = self.b(), self.replicates()
-        out = np.empty((b,) if m is not None else (B, b), dtype=np.complex128)
+        shape = (b,) if m is not None else (B, b)
+        if out is None:
+            out = np.empty(shape, dtype=np.complex128)
+        elif out.shape != shape or out.dtype != np.complex128 or not out.flags.c_contiguous:
+            raise ValueError(f"data: out must be a C-contiguous complex128 array of shape {shape}")
         check(lib.skc_sym_read_data(self._h, -1 if m is None else int(m), out.ctypes.data_as(C.POINTER(C.c_double))))
         return out
 

@@ -83,6 +83,13 @@ struct DevBuf {
     }
 };
 
+// integer knob from the environment, clamped to [lo, hi] (A/B experiment hooks)
+int env_int(const char* name, int dflt, int lo, int hi) {
+    const char* e = std::getenv(name);
+    if (!e) return dflt;
+    return std::min(hi, std::max(lo, std::atoi(e)));
+}
+
 int local_length(std::uint32_t b) {
     static int pref = [] {
         const char* e = std::getenv("SKC_LOCAL_N");
@@ -110,6 +117,8 @@ std::vector<double> host_twiddles(std::uint32_t b) {
 struct skc_context {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t stream2 = nullptr;  // pipelined zero-copy builds: main pass of chunk c
+    cudaEvent_t ev_q[5] = {};        // chunk c quantized / all chunks done
     int sms = 148;
     int smem_optin = 227 * 1024;
     std::map<std::uint32_t, std::unique_ptr<DevBuf<double2>>> twiddles;
@@ -418,14 +427,16 @@ void init_asym_device(skc_asym_set* s, const double* data_host) {
 // the row blocks the build reads (sym: T[i][i:n][:], asym: T[i0:i1]) unless the full
 // tensor is needed by the symmetry check.
 const void* stage_tensor(skc_context* ctx, const void* T, int n, int dtype, int location, bool sym, int i0, int i1,
-                         bool need_full, size_t* h2d_bytes) {
+                         bool need_full, size_t* h2d_bytes, bool* zero_copy = nullptr) {
     if (h2d_bytes) *h2d_bytes = 0;
+    if (zero_copy) *zero_copy = false;
     if (location == SKC_DEVICE) return T;
     const size_t es = dtype == SKC_F64 ? 8 : 4;
     const size_t n2 = static_cast<size_t>(n) * n;
     cudaPointerAttributes attr;
     if (cudaPointerGetAttributes(&attr, T) == cudaSuccess && attr.type == cudaMemoryTypeHost &&
         attr.devicePointer != nullptr) {
+        if (zero_copy) *zero_copy = true;
         return attr.devicePointer;
     }
     cudaGetLastError();  // clear a failed attribute query on pageable memory
@@ -452,7 +463,7 @@ const void* stage_tensor(skc_context* ctx, const void* T, int n, int dtype, int 
 }
 
 void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool sym, int i0, int i1, int B,
-                     std::uint32_t b, const std::uint32_t* packed, double2* data) {
+                     std::uint32_t b, const std::uint32_t* packed, double2* data, bool zero_copy) {
     if (i0 >= i1) return;
     skc_context::RowTab& rt = ctx->rowtab(n, i0, i1, sym);
     if (rt.nrows == 0) return;
@@ -532,21 +543,85 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
     p.scale_exp = ctx->ints.p;
     p.nonfinite = ctx->ints.p + 1;
     p.data_as_double = reinterpret_cast<double*>(data);
-    {
-        SKC_PROF(ctx, "build_prepass");
-        launch_build_prepass(ctx->stream, Tdev, p);
+    // Zero-copy host input: the quantize pass is bus-bound, so the rows are cut into K
+    // chunks and chunk c+1 is read over PCIe (a few SMs, wide blocks) while the main pass
+    // of chunk c runs on the other SMs (second stream). Each chunk keeps its own exponent
+    // and exact accumulator; the finalize sums the K chunk sketches in order.
+    static const bool pipe_on = [] {
+        const char* e = std::getenv("SKC_BUILD_PIPELINE");  // "0": A/B switch for the chunked path
+        return !(e && std::string(e) == "0");
+    }();
+    const int K = (pipe_on && zero_copy && rt.nrows >= 4096 &&
+                   sizeof(double) * 32 * (size_t)n <= (size_t)ctx->smem_optin - 1024)
+                      ? env_int("SKC_BUILD_K", 4, 2, 4)
+                      : 1;
+    if (K > 1) {
+        const int qsms = env_int("SKC_BUILD_QSMS", 16, 1, 64);  // SMs given to the bus-bound quantize pass
+        p.P = std::max(1, ctx->sms - qsms);
+        p.prepass_threads = 1024;
+        p.prepass_blocks = qsms;
+        p.prepass_warps = 32;
+        ctx->build_acc.alloc(static_cast<size_t>(K) * total_slots);
+        ctx->build_ints.alloc(static_cast<size_t>(K) * G);
+        ctx->ints.alloc(16);
+        ctx->prepass.alloc(static_cast<size_t>(K) * qsms);
+        if (!ctx->stream2) CK(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
+        if (!ctx->ev_q[0])
+            for (int c = 0; c < 5; ++c) CK(cudaEventCreateWithFlags(&ctx->ev_q[c], cudaEventDisableTiming));
+        std::vector<int> rb(K + 1, 0);
+        for (int c = 1; c < K; ++c) {
+            const long long target = tot * c / K;
+            rb[c] = static_cast<int>(std::lower_bound(rt.cum.begin(), rt.cum.end(), target) - rt.cum.begin());
+            rb[c] = std::min(std::max(rb[c], rb[c - 1]), rt.nrows);
+        }
+        rb[K] = rt.nrows;
+        CK(cudaMemsetAsync(p.nonfinite, 0, sizeof(int), ctx->stream));
+        {
+            SKC_PROF(ctx, "build_pipelined");
+            for (int c = 0; c < K; ++c) {
+                BuildPlan pc = p;
+                pc.rowtab = rt.rows.p + rb[c];
+                pc.rowoff = rt.offs.p + rb[c];
+                pc.rowF = ctx->rowF.p + rb[c];
+                pc.nrows = rb[c + 1] - rb[c];
+                pc.prepass_partials = ctx->prepass.p + static_cast<size_t>(c) * qsms;
+                pc.scale_exp = ctx->ints.p + 4 + c;
+                pc.reset_nonfinite = false;
+                pc.acc = ctx->build_acc.p + static_cast<size_t>(c) * total_slots;
+                pc.next_row = ctx->build_ints.p + static_cast<size_t>(c) * G;
+                if (pc.nrows > 0) launch_build_prepass(ctx->stream, Tdev, pc);
+                CK(cudaEventRecord(ctx->ev_q[c], ctx->stream));
+                CK(cudaStreamWaitEvent(ctx->stream2, ctx->ev_q[c], 0));
+                if (pc.nrows > 0) {
+                    launch_build_main(ctx->stream2, Tdev, pc);
+                } else {
+                    CK(cudaMemsetAsync(pc.acc, 0, sizeof(unsigned long long) * (size_t)total_slots, ctx->stream2));
+                }
+            }
+            CK(cudaEventRecord(ctx->ev_q[K], ctx->stream2));
+            CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_q[K], 0));
+            BuildPlan pf = p;
+            pf.acc = ctx->build_acc.p;
+            launch_build_finalize_multi(ctx->stream, pf, K, ctx->ints.p + 4);
+        }
+        ctx->check_launch();
+    } else {
+        {
+            SKC_PROF(ctx, "build_prepass");
+            launch_build_prepass(ctx->stream, Tdev, p);
+        }
+        ctx->check_launch();
+        {
+            SKC_PROF(ctx, "build_main");
+            launch_build_main(ctx->stream, Tdev, p);
+        }
+        ctx->check_launch();
+        {
+            SKC_PROF(ctx, "build_finalize");
+            launch_build_finalize(ctx->stream, p);  // device-side no-op when nonfinite
+        }
+        ctx->check_launch();
     }
-    ctx->check_launch();
-    {
-        SKC_PROF(ctx, "build_main");
-        launch_build_main(ctx->stream, Tdev, p);
-    }
-    ctx->check_launch();
-    {
-        SKC_PROF(ctx, "build_finalize");
-        launch_build_finalize(ctx->stream, p);  // device-side no-op when nonfinite
-    }
-    ctx->check_launch();
     int nonfinite = 0;
     CK(cudaMemcpyAsync(&nonfinite, p.nonfinite, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     ctx->sync();
@@ -632,9 +707,15 @@ int skc_context_destroy(skc_context* ctx) {
         if (!ctx) return;
         cudaSetDevice(ctx->device);
         cudaStreamSynchronize(ctx->stream);
-        cudaStream_t st = ctx->stream;
+        if (ctx->stream2) cudaStreamSynchronize(ctx->stream2);
+        cudaStream_t st = ctx->stream, st2 = ctx->stream2;
+        cudaEvent_t ev[5];
+        for (int c = 0; c < 5; ++c) ev[c] = ctx->ev_q[c];
         delete ctx;
         cudaStreamDestroy(st);
+        if (st2) cudaStreamDestroy(st2);
+        for (int c = 0; c < 5; ++c)
+            if (ev[c]) cudaEventDestroy(ev[c]);
     });
 }
 int skc_context_synchronize(skc_context* ctx) {
@@ -811,7 +892,8 @@ int skc_sym_accumulate_dense(skc_sym_set* s, const void* T, int dtype, int locat
         require(s->n <= 65535, "accumulate_dense: n above 65535 is not supported");
         skc_context* ctx = s->ctx;
         ctx->use();
-        const void* Td = stage_tensor(ctx, T, s->n, dtype, location, true, i0, i1, !assume_symmetric, nullptr);
+        bool zc = false;
+        const void* Td = stage_tensor(ctx, T, s->n, dtype, location, true, i0, i1, !assume_symmetric, nullptr, &zc);
         if (!assume_symmetric) {
             ctx->asym_key.alloc(1);
             unsigned long long init = ~0ull;
@@ -837,7 +919,7 @@ int skc_sym_accumulate_dense(skc_sym_set* s, const void* T, int dtype, int locat
             }
         }
         s->version++;  // sketch.cpp:324
-        run_dense_build(ctx, Td, s->n, dtype, true, i0, i1, s->B, s->b, s->packed.p, s->data.p);
+        run_dense_build(ctx, Td, s->n, dtype, true, i0, i1, s->B, s->b, s->packed.p, s->data.p, zc);
         ctx->sync();
     });
 }
@@ -1417,9 +1499,10 @@ int skc_asym_accumulate_dense(skc_asym_set* s, const void* T, int dtype, int loc
         require(s->n <= 65535, "accumulate_dense: n above 65535 is not supported");
         skc_context* ctx = s->ctx;
         ctx->use();
-        const void* Td = stage_tensor(ctx, T, s->n, dtype, location, false, i0, i1, false, nullptr);
+        bool zc = false;
+        const void* Td = stage_tensor(ctx, T, s->n, dtype, location, false, i0, i1, false, nullptr, &zc);
         s->version++;  // sketch.cpp:175
-        run_dense_build(ctx, Td, s->n, dtype, false, i0, i1, s->B, s->b, s->packed.p, s->data.p);
+        run_dense_build(ctx, Td, s->n, dtype, false, i0, i1, s->B, s->b, s->packed.p, s->data.p, zc);
         ctx->sync();
     });
 }

@@ -58,19 +58,21 @@ __device__ double block_sum_b(double v, double* red) {
 // stream qbuf[rowoff + e] = round(kappa T 2^Frow) with Frow = 61 - ceil(log2 rowL1).
 // The main pass rescales q >> (Frow - F) to the global exponent F, so T is read from
 // HBM once per build. Per-block L1 partials are summed in a fixed order (deterministic).
-template <typename TT, bool SYM>
-__global__ void __launch_bounds__(256) k_build_quantize(const TT* __restrict__ T, int n,
+template <typename TT, bool SYM, int NTQ>
+__global__ void __launch_bounds__(NTQ) k_build_quantize(const TT* __restrict__ T, int n,
                                                        const std::uint32_t* __restrict__ rowtab,
                                                        const long long* __restrict__ rowoff, int nrows,
                                                        long long* __restrict__ qbuf, short* __restrict__ rowF,
-                                                       double* __restrict__ partials, int* __restrict__ nonfinite) {
-    extern __shared__ double stage[];  // 8 warps x n: each element of T is read exactly once
-    __shared__ double red[8];
+                                                       double* __restrict__ partials, int* __restrict__ nonfinite,
+                                                       bool vec16) {
+    constexpr int W = NTQ / 32;
+    extern __shared__ double stage[];  // W warps x n: each element of T is read exactly once
+    __shared__ double red[W];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double* st = stage + (size_t)warp * n;
     double blk = 0.0;
     bool bad = false;
-    for (int row = blockIdx.x * 8 + warp; row < nrows; row += gridDim.x * 8) {
+    for (int row = blockIdx.x * W + warp; row < nrows; row += gridDim.x * W) {
         const std::uint32_t ij = rowtab[row];
         const int i = static_cast<int>(ij >> 16), j = static_cast<int>(ij & 0xFFFFu);
         const TT* rp = T + ((size_t)i * n + j) * n;
@@ -78,19 +80,51 @@ __global__ void __launch_bounds__(256) k_build_quantize(const TT* __restrict__ T
         const double kdiag = SYM ? ((i == j) ? 1.0 : 3.0) : 1.0;
         const double koff = SYM ? ((i == j) ? 3.0 : 6.0) : 1.0;
         double a0 = 0.0;
-        // 4 loads in flight per lane (T may be host memory read over PCIe)
-        for (int kb = k0 + lane; kb < n; kb += 128) {
-            double v[4];
+        if (sizeof(TT) == 8 && vec16) {
+            // 16-byte loads from a 16-byte aligned base covering the row segment: T may be
+            // pinned host memory read in place over PCIe, where wider requests carry less
+            // header overhead per byte. 4 pair-loads in flight per lane.
+            const size_t e0 = ((size_t)i * n + j) * n + k0;  // element index of (i, j, k0)
+            const size_t ea = e0 & ~(size_t)1;
+            const int npair = static_cast<int>((e0 + (n - k0) - ea + 1) >> 1);
+            const double2* tp = reinterpret_cast<const double2*>(T) + (ea >> 1);
+            const int off = static_cast<int>(e0 - ea);  // 0 or 1: leading element to skip
+            for (int pb = lane; pb < npair; pb += 128) {
+                double2 v[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = (kb + 32 * u < n) ? static_cast<double>(rp[kb + 32 * u]) : 0.0;
+                for (int u = 0; u < 4; ++u) v[u] = (pb + 32 * u < npair) ? tp[pb + 32 * u] : make_double2(0.0, 0.0);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int k = kb + 32 * u;
-                if (k < n) {
-                    const double kv = ((SYM && k == j) ? kdiag : koff) * v[u];
-                    st[k - k0] = kv;
-                    a0 += fabs(kv);
-                    bad |= !isfinite(v[u]);
+                for (int u = 0; u < 4; ++u) {
+                    const int q = 2 * (pb + 32 * u) - off;  // row-relative index of v[u].x
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int kk = q + h;
+                        if (kk >= 0 && kk < n - k0) {
+                            const double x = h ? v[u].y : v[u].x;
+                            const int k = k0 + kk;
+                            const double kv = ((SYM && k == j) ? kdiag : koff) * x;
+                            st[kk] = kv;
+                            a0 += fabs(kv);
+                            bad |= !isfinite(x);
+                        }
+                    }
+                }
+            }
+        } else {
+            // 4 loads in flight per lane
+            for (int kb = k0 + lane; kb < n; kb += 128) {
+                double v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[u] = (kb + 32 * u < n) ? static_cast<double>(rp[kb + 32 * u]) : 0.0;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int k = kb + 32 * u;
+                    if (k < n) {
+                        const double kv = ((SYM && k == j) ? kdiag : koff) * v[u];
+                        st[k - k0] = kv;
+                        a0 += fabs(kv);
+                        bad |= !isfinite(v[u]);
+                    }
                 }
             }
         }
@@ -115,7 +149,7 @@ __global__ void __launch_bounds__(256) k_build_quantize(const TT* __restrict__ T
         blk += (lane == 0) ? a0 : 0.0;
     }
     if (bad) atomicOr(nonfinite, 1);
-    const double s = block_sum_b<256>(blk, red);
+    const double s = block_sum_b<NTQ>(blk, red);
     if (threadIdx.x == 0) partials[blockIdx.x] = s;
 }
 
@@ -137,15 +171,32 @@ __global__ void k_build_scale(const double* __restrict__ partials, int np, int* 
     }
 }
 
+// Default: kPrepassBlocks x 256 threads over all SMs (HBM-bound). Pipelined zero-copy
+// builds use p.prepass_blocks x 1024-thread blocks on a few SMs (PCIe-bound), leaving the
+// rest to the concurrent main pass of the previous chunk.
 void launch_build_prepass(cudaStream_t st, const void* T, const BuildPlan& p) {
-    cudaMemsetAsync(p.nonfinite, 0, sizeof(int), st);
-#define QUANT(TT, SY)                                                                                             \
-    {                                                                                                             \
-        const size_t smem = sizeof(double) * 8 * (size_t)p.n;                                                     \
-        if (smem > 48 * 1024)                                                                                     \
-            cudaFuncSetAttribute(k_build_quantize<TT, SY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-        k_build_quantize<TT, SY><<<kPrepassBlocks, 256, smem, st>>>((const TT*)T, p.n, p.rowtab, p.rowoff, p.nrows,  \
-                                                                   p.qbuf, p.rowF, p.prepass_partials, p.nonfinite); \
+    if (p.reset_nonfinite) cudaMemsetAsync(p.nonfinite, 0, sizeof(int), st);
+    const bool wide = p.prepass_threads == 1024;
+    const int blocks = p.prepass_blocks;
+    const bool vec16 = (reinterpret_cast<std::uintptr_t>(T) & 15) == 0;
+#define QUANT(TT, SY)                                                                                                 \
+    {                                                                                                                 \
+        if (wide) {                                                                                                   \
+            const int w = p.prepass_warps;                                                                            \
+            const size_t smem = sizeof(double) * 32 * (size_t)p.n;                                                    \
+            (void)w;                                                                                                  \
+            cudaFuncSetAttribute(k_build_quantize<TT, SY, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+            k_build_quantize<TT, SY, 1024><<<blocks, 1024, smem, st>>>((const TT*)T, p.n, p.rowtab, p.rowoff, p.nrows,  \
+                                                                       p.qbuf, p.rowF, p.prepass_partials,             \
+                                                                       p.nonfinite, vec16);                            \
+        } else {                                                                                                      \
+            const size_t smem = sizeof(double) * 8 * (size_t)p.n;                                                     \
+            if (smem > 48 * 1024)                                                                                     \
+                cudaFuncSetAttribute(k_build_quantize<TT, SY, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+            k_build_quantize<TT, SY, 256><<<blocks, 256, smem, st>>>((const TT*)T, p.n, p.rowtab, p.rowoff, p.nrows,    \
+                                                                     p.qbuf, p.rowF, p.prepass_partials, p.nonfinite,  \
+                                                                     vec16);                                           \
+        }                                                                                                             \
     }
     if (p.sym) {
         if (p.dtype == 0) QUANT(double, true)
@@ -156,7 +207,7 @@ void launch_build_prepass(cudaStream_t st, const void* T, const BuildPlan& p) {
     }
 #undef QUANT
     count_launch();
-    k_build_scale<<<1, 256, 0, st>>>(p.prepass_partials, kPrepassBlocks, p.scale_exp);
+    k_build_scale<<<1, 256, 0, st>>>(p.prepass_partials, blocks, p.scale_exp);
     count_launch();
 }
 
@@ -659,6 +710,38 @@ __global__ void k_build_finalize(const unsigned long long* __restrict__ acc, lon
         data[s] += v;
     else
         data[2 * s] += v;
+}
+
+// Pipelined builds: K chunk accumulators with their own exponents, summed in chunk order.
+template <bool SYM>
+__global__ void k_build_finalize_multi(const unsigned long long* __restrict__ acc, int K, long long total_slots,
+                                       const int* __restrict__ scale_exps, const int* __restrict__ nonfinite,
+                                       double* __restrict__ data) {
+    const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (s >= total_slots || *nonfinite) return;
+    double v = 0.0;
+    bool any = false;
+    for (int c = 0; c < K; ++c) {
+        const long long q = static_cast<long long>(acc[(long long)c * total_slots + s]);
+        if (q) {
+            v += ldexp(static_cast<double>(q), -scale_exps[c]);
+            any = true;
+        }
+    }
+    if (!any) return;
+    if (SYM)
+        data[s] += v;
+    else
+        data[2 * s] += v;
+}
+void launch_build_finalize_multi(cudaStream_t st, const BuildPlan& p, int K, const int* scale_exps) {
+    if (p.sym)
+        k_build_finalize_multi<true><<<cdiv(p.total_slots, 256), 256, 0, st>>>(p.acc, K, p.total_slots, scale_exps,
+                                                                               p.nonfinite, p.data_as_double);
+    else
+        k_build_finalize_multi<false><<<cdiv(p.total_slots, 256), 256, 0, st>>>(p.acc, K, p.total_slots, scale_exps,
+                                                                                p.nonfinite, p.data_as_double);
+    count_launch();
 }
 
 void launch_build_finalize(cudaStream_t st, const BuildPlan& p) {

@@ -94,7 +94,9 @@ struct BuildPlan {
     const long long* rowoff;      // packed-stream offset of each row
     long long* qbuf;              // packed fixed-point stream (quantize pass)
     short* rowF;                  // per-row exponent of qbuf
-    double* prepass_partials;     // kPrepassBlocks
+    double* prepass_partials;     // prepass_blocks
+    int prepass_blocks = 1024, prepass_threads = 256, prepass_warps = 8;
+    bool reset_nonfinite = true;
     int* scale_exp;               // device int
     int* nonfinite;               // device int
     double* data_as_double;       // B x b x 2
@@ -104,6 +106,7 @@ size_t build_smem_bytes(long long slots_per_cta, int R, int n);
 void launch_build_prepass(cudaStream_t st, const void* T, const BuildPlan& p);
 void launch_build_main(cudaStream_t st, const void* T, const BuildPlan& p);
 void launch_build_finalize(cudaStream_t st, const BuildPlan& p);
+void launch_build_finalize_multi(cudaStream_t st, const BuildPlan& p, int K, const int* scale_exps);
 
 // residue twiddle tables of a symmetric set (SymView::stw*/gtw*)
 void launch_sym_twiddle_tables(cudaStream_t st, const SymView& v, double2* stw1, double2* stw2, double2* gtw1,

@@ -146,6 +146,45 @@ def test_sym_dense_pinned_and_pageable_host_inputs(gpu_ctx):
     assert rel_per_replicate(sl.data(), ref.data()) <= SKETCH_TOL
 
 
+@pytest.mark.parametrize("sym", [True, False])
+def test_dense_pinned_pipelined_build(gpu_ctx, sym):
+    """Large enough pinned inputs take the chunked zero-copy pipeline (bus-bound quantize
+    of chunk c+1 overlapping the main pass of chunk c, per-chunk exponents); the result
+    must match the oracle and the device-resident build, including a NaN rejection that
+    leaves the set untouched."""
+    import torch
+
+    n = 140 if sym else 48  # sym: 9870 rows; asym: 2304 rows -> also the unpipelined branch
+    T = sym_tensor(n, 31)
+    pinned = torch.from_numpy(T.copy()).pin_memory().numpy()
+    if sym:
+        ref = O.SymSet(n, 2048, 6, 4)
+        ref.accumulate_dense(T, True)
+        s = skb().SymTensorSketchSet(n, 2048, 6, 4, gpu_ctx)
+        d = skb().SymTensorSketchSet(n, 2048, 6, 4, gpu_ctx)
+        s.accumulate_dense(pinned, assume_symmetric=True)
+        d.accumulate_dense(torch.from_numpy(T).cuda(), assume_symmetric=True)
+    else:
+        ref = O.AsymSet(n, 2048, 6, 4)
+        ref.accumulate_dense(T)
+        s = skb().AsymTensorSketchSet(n, 2048, 6, 4, gpu_ctx)
+        d = skb().AsymTensorSketchSet(n, 2048, 6, 4, gpu_ctx)
+        s.accumulate_dense(pinned)
+        d.accumulate_dense(torch.from_numpy(T).cuda())
+    assert rel_per_replicate(s.data(), ref.data()) <= SKETCH_TOL
+    assert rel_per_replicate(s.data(), d.data()) <= 1e-13
+    bad = pinned.copy()
+    bad[n - 1, n - 1, n - 1] = np.nan
+    bad = torch.from_numpy(bad).pin_memory().numpy()
+    before = s.data().copy()
+    with pytest.raises(ValueError):
+        if sym:
+            s.accumulate_dense(bad, assume_symmetric=True)
+        else:
+            s.accumulate_dense(bad)
+    assert np.array_equal(s.data(), before)
+
+
 def test_sym_dense_symmetry_check_message(gpu_ctx):
     n = 6
     T = sym_tensor(n, 1)
