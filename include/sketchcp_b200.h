@@ -131,6 +131,29 @@ int skc_sym_accumulate_moment(skc_sym_set* s, const double* X, const double* w, 
 int skc_sym_sketch_whitened_m3(skc_sym_set* s, int V, long long D, const long long* doc_ptr, const int* word,
                                const int* count, const double* W, double alpha0, long long* used,
                                long long* skipped);
+/* ---- LDA moments and whitening (lda.cpp:88-143) -------------------------------------
+ * Corpus arguments as for skc_sym_sketch_whitened_m3 (host CSR). Matrices are row-major.
+ * compute_m1 (lda.cpp:88-100): m1[V] = mean over documents with >= 1 token of n_d / m_d. */
+int skc_lda_compute_m1(skc_context* ctx, int V, long long D, const long long* doc_ptr, const int* word,
+                       const int* count, double* m1_out);
+/* Y = M2 X for X, Y host V x p, where M2 is compute_m2(corpus, alpha0) (lda.cpp:102-123)
+ * applied without forming it (the V x V matrix of the reference). */
+int skc_lda_m2_apply(skc_context* ctx, int V, long long D, const long long* doc_ptr, const int* word,
+                     const int* count, double alpha0, int p, const double* X, double* Y);
+/* whiten(compute_m2(corpus, alpha0), k) (lda.cpp:125-143) by randomized subspace
+ * iteration on the implicit M2 (block p = k + oversample rounded up to 32, `iters`
+ * power steps, Gaussian start from derive_seed(seed, 0x68)) and a Rayleigh-Ritz
+ * projection. Outputs: W and unwhiten V x k, singular_values k (descending eigenvalues).
+ * oversample < 0 / iters < 0 select the defaults (max(16, k/4), 12). Errors follow the
+ * reference: invalid rank -> SKC_INVALID_ARGUMENT, eigenvalue <= 1e-10 ->
+ * SKC_NUMERICAL_ERROR "whiten: moment matrix is rank deficient at component c (...)". */
+int skc_lda_whiten_corpus(skc_context* ctx, int V, long long D, const long long* doc_ptr, const int* word,
+                          const int* count, double alpha0, int k, int oversample, int iters, uint64_t seed,
+                          double* W, double* unwhiten, double* singular_values);
+/* whiten(m2hat, k) for a dense symmetric host V x V matrix (same algorithm, DGEMM operator). */
+int skc_lda_whiten_dense(skc_context* ctx, int V, const double* m2, int k, int oversample, int iters, uint64_t seed,
+                         double* W, double* unwhiten, double* singular_values);
+
 /* replicate(m).data -> host (B-major when m < 0: all replicates, B*b complex). */
 int skc_sym_read_data(const skc_sym_set* s, int m, double* out_host);
 /* mutable_replicate(m).data = in (bumps version, sketch.hpp:105-108); m < 0: all. */

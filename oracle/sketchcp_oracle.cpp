@@ -875,6 +875,106 @@ void lda_compute_m1(int V, int D, const long long* doc_ptr, const int* word, con
     for (int w = 0; w < V; ++w) m1[w] /= static_cast<double>(used);
 }
 
+// --- lda.cpp:102-123: dense M2 = (1/used2) sum_d pair(d)/(m(m-1)) - a0/(a0+1) m1 m1^T --
+// pair(a, b) over document positions: c_a c_b, and c_a (c_a - 1) on the diagonal a == b.
+void lda_compute_m2(int V, int D, const long long* doc_ptr, const int* word, const int* count, double alpha0,
+                    double* m2 /* V x V row-major */) {
+    std::vector<double> m1(V);
+    lda_compute_m1(V, D, doc_ptr, word, count, m1.data());
+    std::fill(m2, m2 + static_cast<std::size_t>(V) * V, 0.0);
+    long long used = 0;
+    for (int d = 0; d < D; ++d) {
+        long long total = 0;
+        for (long long q = doc_ptr[d]; q < doc_ptr[d + 1]; ++q) total += count[q];
+        if (total < 2) continue;
+        ++used;
+        const double scale = 1.0 / (static_cast<double>(total) * (total - 1));
+        for (long long a = doc_ptr[d]; a < doc_ptr[d + 1]; ++a)
+            for (long long b = doc_ptr[d]; b < doc_ptr[d + 1]; ++b) {
+                const double pair = (a == b) ? static_cast<double>(count[a]) * (count[a] - 1)
+                                             : static_cast<double>(count[a]) * count[b];
+                m2[static_cast<std::size_t>(word[a]) * V + word[b]] += scale * pair;
+            }
+    }
+    if (used == 0) throw std::runtime_error("compute_m2: no documents with at least 2 words");
+    const double c = alpha0 / (alpha0 + 1.0);
+    for (int i = 0; i < V; ++i)
+        for (int j = 0; j < V; ++j) {
+            double& e = m2[static_cast<std::size_t>(i) * V + j];
+            e /= static_cast<double>(used);
+            e -= c * m1[i] * m1[j];
+        }
+}
+
+// Cyclic Jacobi eigensolver for a symmetric matrix: the test oracle standing in for
+// Eigen::SelfAdjointEigenSolver (lda.cpp:128). Eigenvalues ascending; column c of the
+// row-major evecs is the eigenvector of evals[c] (sign unpinned, as in Eigen).
+void sym_eigen_jacobi(int n, const double* A, double* evals, double* evecs) {
+    std::vector<long double> a(A, A + static_cast<std::size_t>(n) * n), v(static_cast<std::size_t>(n) * n, 0.0L);
+    for (int i = 0; i < n; ++i) v[static_cast<std::size_t>(i) * n + i] = 1.0L;
+    auto at = [&](std::vector<long double>& m, int i, int j) -> long double& { return m[static_cast<std::size_t>(i) * n + j]; };
+    for (int sweep = 0; sweep < 100; ++sweep) {
+        long double off = 0, tot = 0;
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j) {
+                tot += at(a, i, j) * at(a, i, j);
+                if (i != j) off += at(a, i, j) * at(a, i, j);
+            }
+        if (off <= 1e-30L * tot) break;
+        for (int p = 0; p < n - 1; ++p)
+            for (int q = p + 1; q < n; ++q) {
+                const long double apq = at(a, p, q);
+                if (apq == 0.0L) continue;
+                const long double theta = (at(a, q, q) - at(a, p, p)) / (2.0L * apq);
+                const long double t = (theta >= 0 ? 1.0L : -1.0L) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0L));
+                const long double c = 1.0L / std::sqrt(t * t + 1.0L), s = t * c;
+                for (int k = 0; k < n; ++k) {  // A <- A J (columns p, q)
+                    const long double akp = at(a, k, p), akq = at(a, k, q);
+                    at(a, k, p) = c * akp - s * akq;
+                    at(a, k, q) = s * akp + c * akq;
+                }
+                for (int k = 0; k < n; ++k) {  // A <- J^T A (rows p, q)
+                    const long double apk = at(a, p, k), aqk = at(a, q, k);
+                    at(a, p, k) = c * apk - s * aqk;
+                    at(a, q, k) = s * apk + c * aqk;
+                }
+                for (int k = 0; k < n; ++k) {
+                    const long double vkp = at(v, k, p), vkq = at(v, k, q);
+                    at(v, k, p) = c * vkp - s * vkq;
+                    at(v, k, q) = s * vkp + c * vkq;
+                }
+            }
+    }
+    std::vector<int> ord(n);
+    for (int i = 0; i < n; ++i) ord[i] = i;
+    std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return at(a, x, x) < at(a, y, y); });
+    for (int c = 0; c < n; ++c) {
+        evals[c] = static_cast<double>(at(a, ord[c], ord[c]));
+        for (int i = 0; i < n; ++i) evecs[static_cast<std::size_t>(i) * n + c] = static_cast<double>(at(v, i, ord[c]));
+    }
+}
+
+// --- lda.cpp:125-143: whiten(m2hat, k) ---------------------------------------------------
+// W[:, c] = u_c / sqrt(ev_c), unwhiten[:, c] = u_c sqrt(ev_c) for the k largest eigenpairs
+// (descending); W and unwhiten V x k row-major.
+void lda_whiten(int V, const double* m2, int k, double* W, double* unwhiten, double* sv) {
+    if (k < 1 || k > V) throw std::invalid_argument("whiten: invalid target rank");
+    std::vector<double> ev(V), U(static_cast<std::size_t>(V) * V);
+    sym_eigen_jacobi(V, m2, ev.data(), U.data());
+    for (int c = 0; c < k; ++c) {
+        const double e = ev[V - 1 - c];
+        if (!(e > 1e-10))
+            throw std::runtime_error("whiten: moment matrix is rank deficient at component " + std::to_string(c + 1) +
+                                 " (eigenvalue " + std::to_string(e) + ")");
+        sv[c] = e;
+        for (int i = 0; i < V; ++i) {
+            const double u = U[static_cast<std::size_t>(i) * V + (V - 1 - c)];
+            W[static_cast<std::size_t>(i) * k + c] = u / std::sqrt(e);
+            unwhiten[static_cast<std::size_t>(i) * k + c] = u * std::sqrt(e);
+        }
+    }
+}
+
 void fourier_sketch(const SymRep& rep, std::uint32_t b, const double* v, int k, cvec& out) {
     out.assign(b, {0.0, 0.0});
     for (int i = 0; i < k; ++i) out[rep.bucket1[i]] += root4(rep.sexp[i]) * v[i];
@@ -1299,6 +1399,20 @@ int orc_first_asymmetric_triple(const double* T, int n, double tol, int* out) {
 }
 int orc_greedy_match(const double* rec, int r, const double* truth, int g, int n, double* out) {
     return guard([&] { greedy_match(rec, r, truth, g, n, out); });
+}
+
+int orc_lda_compute_m1(int V, int D, const long long* doc_ptr, const int* word, const int* count, double* m1) {
+    return guard([&] { lda_compute_m1(V, D, doc_ptr, word, count, m1); });
+}
+int orc_lda_compute_m2(int V, int D, const long long* doc_ptr, const int* word, const int* count, double alpha0,
+                       double* m2) {
+    return guard([&] { lda_compute_m2(V, D, doc_ptr, word, count, alpha0, m2); });
+}
+int orc_sym_eigen(int n, const double* A, double* evals, double* evecs) {
+    return guard([&] { sym_eigen_jacobi(n, A, evals, evecs); });
+}
+int orc_lda_whiten(int V, const double* m2, int k, double* W, double* unwhiten, double* sv) {
+    return guard([&] { lda_whiten(V, m2, k, W, unwhiten, sv); });
 }
 
 }  // extern "C"

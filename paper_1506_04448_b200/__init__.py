@@ -715,6 +715,71 @@ class AsymContractionWorkspace:
         return out
 
 
+# ---- LDA moments and whitening (lda.hpp:49-57, lda.cpp:88-143) ---------------------------
+def _corpus_args(doc_ptr, word, count):
+    dp = np.ascontiguousarray(doc_ptr, dtype=np.int64)
+    wd = np.ascontiguousarray(word, dtype=np.int32)
+    ct = np.ascontiguousarray(count, dtype=np.int32)
+    return (dp, wd, ct), (dp.size - 1, dp.ctypes.data_as(C.POINTER(C.c_longlong)), wd.ctypes.data_as(C.POINTER(C.c_int)),
+                          ct.ctypes.data_as(C.POINTER(C.c_int)))
+
+
+class WhiteningMap:
+    """lda.hpp:42-46: W (V x k, W' M2 W = I), unwhiten (V x k), singular_values (k)."""
+
+    def __init__(self, W, unwhiten, singular_values):
+        self.W, self.unwhiten, self.singular_values = W, unwhiten, singular_values
+
+
+def compute_m1(V: int, doc_ptr, word, count, ctx: Context | None = None) -> np.ndarray:
+    """lda.cpp:88-100 on the GPU (corpus in CSR form)."""
+    ctx = ctx or default_context()
+    keep, (D, dpp, wdp, ctp) = _corpus_args(doc_ptr, word, count)
+    out = np.empty(V)
+    check(lib.skc_lda_compute_m1(ctx.handle, int(V), D, dpp, wdp, ctp, _dp(out)))
+    return out
+
+
+def m2_apply(V: int, doc_ptr, word, count, alpha0: float, X, ctx: Context | None = None) -> np.ndarray:
+    """M2 @ X for the implicit compute_m2(corpus, alpha0) (lda.cpp:102-123); X is V x p."""
+    ctx = ctx or default_context()
+    X = _f64(X)
+    if X.ndim == 1:
+        X = X.reshape(-1, 1)
+    if X.shape[0] != V:
+        raise ValueError("m2_apply: X must have V rows")
+    keep, (D, dpp, wdp, ctp) = _corpus_args(doc_ptr, word, count)
+    Y = np.empty_like(X)
+    check(lib.skc_lda_m2_apply(ctx.handle, int(V), D, dpp, wdp, ctp, float(alpha0), X.shape[1], _dp(X), _dp(Y)))
+    return Y
+
+
+def whiten_corpus(V: int, doc_ptr, word, count, alpha0: float, k: int, oversample: int = -1, iters: int = -1,
+                  seed: int = 0x5EED, ctx: Context | None = None) -> WhiteningMap:
+    """whiten(compute_m2(corpus, alpha0), k) (lda.cpp:102-143) without forming M2:
+    randomized subspace iteration + Rayleigh-Ritz on the GPU."""
+    ctx = ctx or default_context()
+    keep, (D, dpp, wdp, ctp) = _corpus_args(doc_ptr, word, count)
+    W, U, sv = np.empty((V, k)), np.empty((V, k)), np.empty(k)
+    check(lib.skc_lda_whiten_corpus(ctx.handle, int(V), D, dpp, wdp, ctp, float(alpha0), int(k), int(oversample),
+                                    int(iters), C.c_uint64(seed), _dp(W), _dp(U), _dp(sv)))
+    return WhiteningMap(W, U, sv)
+
+
+def whiten(m2hat, k: int, oversample: int = -1, iters: int = -1, seed: int = 0x5EED,
+           ctx: Context | None = None) -> WhiteningMap:
+    """whiten(m2hat, k) (lda.cpp:125-143) for a dense symmetric matrix (lower triangle read)."""
+    ctx = ctx or default_context()
+    M = _f64(m2hat)
+    if M.ndim != 2 or M.shape[0] != M.shape[1]:
+        raise ValueError("whiten: matrix must be square")
+    V = M.shape[0]
+    W, U, sv = np.empty((V, k)), np.empty((V, k)), np.empty(k)
+    check(lib.skc_lda_whiten_dense(ctx.handle, V, _dp(M), int(k), int(oversample), int(iters), C.c_uint64(seed),
+                                   _dp(W), _dp(U), _dp(sv)))
+    return WhiteningMap(W, U, sv)
+
+
 def gen_planted_tensor(n: int, rank: int, sigma: float, seed: int, dtype=np.float64):
     """Host generator of the BASELINE planted tensors (configs 0-2). Returns (T, lambda, V)."""
     T = np.empty((n, n, n), dtype=dtype)

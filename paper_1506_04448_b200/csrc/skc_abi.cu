@@ -2,6 +2,7 @@
 // sm_100a kernels in skc_kernels.cu. Mirrors the reference classes in
 // proj/include/sketchcp/{sketch,contraction,decompose}.hpp: validation, error
 // messages and exception taxonomy follow the reference; compute runs only on the GPU.
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -119,6 +120,7 @@ struct skc_context {
     cudaStream_t stream = nullptr;
     cudaStream_t stream2 = nullptr;  // pipelined zero-copy builds: main pass of chunk c
     cudaEvent_t ev_q[5] = {};        // chunk c quantized / all chunks done
+    cublasHandle_t cublas = nullptr;  // LDA whitening block products (lazy)
     int sms = 148;
     int smem_optin = 227 * 1024;
     std::map<std::uint32_t, std::unique_ptr<DevBuf<double2>>> twiddles;
@@ -662,6 +664,312 @@ __global__ void k_first_asym(const void* T, int dtype, int n, double tol, unsign
         }
 }
 
+
+// ---- LDA moments and whitening (lda.cpp:88-143; kernels in skc_whiten.cu) ---------------
+#define CB(call)                                                                                      \
+    do {                                                                                              \
+        cublasStatus_t st_ = (call);                                                                  \
+        if (st_ != CUBLAS_STATUS_SUCCESS)                                                             \
+            fail(kCudaError, std::string("cuBLAS error ") + std::to_string(static_cast<int>(st_)) + " at " #call); \
+    } while (0)
+
+cublasHandle_t cublas_of(skc_context* ctx) {
+    if (!ctx->cublas) CB(cublasCreate(&ctx->cublas));
+    CB(cublasSetStream(ctx->cublas, ctx->stream));
+    return ctx->cublas;
+}
+
+// Corpus on the device: CSR (document-major) and its word-major transpose, per-document
+// weights and per-word diagonal / M1 sums.
+struct CorpusDev {
+    int V = 0;
+    long long D = 0, nnz = 0, used1 = 0, used2 = 0;
+    DevBuf<long long> doc_ptr, cptr, cdoc, total;
+    DevBuf<int> word, count, ccount;
+    DevBuf<double> s2, invm, diag, m1p;
+};
+
+void upload_corpus(skc_context* ctx, int V, long long D, const long long* doc_ptr, const int* word, const int* count,
+                   CorpusDev& c) {
+    require(V >= 1 && D >= 0, "lda: invalid corpus dimensions");
+    check_vec(doc_ptr, "lda: doc_ptr");
+    const long long nnz = doc_ptr[D];
+    require(doc_ptr[0] == 0 && nnz >= 0, "lda: doc_ptr must start at 0");
+    if (nnz > 0) {
+        check_vec(word, "lda: word");
+        check_vec(count, "lda: count");
+    }
+    std::vector<long long> cptr(static_cast<size_t>(V) + 1, 0);
+    for (long long d = 0; d < D; ++d) {
+        require(doc_ptr[d + 1] >= doc_ptr[d], "lda: doc_ptr must be non-decreasing");
+        long long tot = 0;
+        for (long long q = doc_ptr[d]; q < doc_ptr[d + 1]; ++q) {
+            require(word[q] >= 0 && word[q] < V, "lda: word id out of range");
+            require(count[q] >= 0, "lda: negative count");
+            tot += count[q];
+            cptr[static_cast<size_t>(word[q]) + 1]++;
+        }
+        if (tot >= 1) ++c.used1;
+        if (tot >= 2) ++c.used2;
+    }
+    for (int w = 0; w < V; ++w) cptr[w + 1] += cptr[w];
+    std::vector<long long> cdoc(static_cast<size_t>(std::max<long long>(nnz, 1)));
+    std::vector<int> ccount(static_cast<size_t>(std::max<long long>(nnz, 1)));
+    {
+        std::vector<long long> fillp(cptr.begin(), cptr.end() - 1);
+        for (long long d = 0; d < D; ++d)
+            for (long long q = doc_ptr[d]; q < doc_ptr[d + 1]; ++q) {
+                const long long pos = fillp[word[q]]++;
+                cdoc[pos] = d;
+                ccount[pos] = count[q];
+            }
+    }
+    c.V = V;
+    c.D = D;
+    c.nnz = nnz;
+    const cudaStream_t st = ctx->stream;
+    c.doc_ptr.upload(doc_ptr, static_cast<size_t>(D) + 1, st);
+    const int zero = 0;
+    c.word.upload(nnz > 0 ? word : &zero, static_cast<size_t>(std::max<long long>(nnz, 1)), st);
+    c.count.upload(nnz > 0 ? count : &zero, static_cast<size_t>(std::max<long long>(nnz, 1)), st);
+    c.cptr.upload(cptr.data(), cptr.size(), st);
+    c.cdoc.upload(cdoc.data(), cdoc.size(), st);
+    c.ccount.upload(ccount.data(), ccount.size(), st);
+    c.total.alloc(static_cast<size_t>(std::max<long long>(D, 1)));
+    c.s2.alloc(static_cast<size_t>(std::max<long long>(D, 1)));
+    c.invm.alloc(static_cast<size_t>(std::max<long long>(D, 1)));
+    c.diag.alloc(static_cast<size_t>(V));
+    c.m1p.alloc(static_cast<size_t>(V));
+    launch_corpus_prep(st, V, D, c.doc_ptr.p, c.count.p, c.cptr.p, c.cdoc.p, c.ccount.p, c.total.p, c.s2.p, c.invm.p,
+                       c.diag.p, c.m1p.p);
+    ctx->check_launch();
+}
+
+// reference error order: compute_m2 calls compute_m1 first (lda.cpp:89-99, 103, 120)
+void check_corpus_m1(const CorpusDev& c) {
+    if (c.D == 0) fail(kNumericalError, "compute_m1: empty corpus");
+    if (c.used1 == 0) fail(kNumericalError, "compute_m1: no nonempty documents");
+}
+void check_corpus_m2(const CorpusDev& c) {
+    check_corpus_m1(c);
+    if (c.used2 == 0) fail(kNumericalError, "compute_m2: no documents with at least 2 words");
+}
+
+struct M2Work {
+    DevBuf<double> Z, mx;
+};
+void m2_apply(skc_context* ctx, const CorpusDev& c, double alpha0, int p, const double* Xd, double* Yd, M2Work& w) {
+    w.Z.alloc(static_cast<size_t>(std::max<long long>(c.D, 1)) * p);
+    w.mx.alloc(static_cast<size_t>(p));
+    launch_m2_apply(ctx->stream, c.V, c.D, p, c.doc_ptr.p, c.word.p, c.count.p, c.cptr.p, c.cdoc.p, c.ccount.p, c.s2.p,
+                    c.diag.p, c.m1p.p, 1.0 / static_cast<double>(c.used1), 1.0 / static_cast<double>(c.used2),
+                    alpha0 / (alpha0 + 1.0), Xd, w.Z.p, w.mx.p, Yd);
+    ctx->check_launch();
+}
+
+// Cyclic Jacobi for a small symmetric matrix (col-major p x p): ascending eigenvalues,
+// column c of vecs the eigenvector of vals[c].
+void jacobi_eigen(int p, std::vector<double> a, std::vector<double>& vals, std::vector<double>& vecs) {
+    vecs.assign(static_cast<size_t>(p) * p, 0.0);
+    for (int i = 0; i < p; ++i) vecs[static_cast<size_t>(i) * p + i] = 1.0;
+    auto A = [&](int i, int j) -> double& { return a[static_cast<size_t>(j) * p + i]; };
+    auto Vv = [&](int i, int j) -> double& { return vecs[static_cast<size_t>(j) * p + i]; };
+    for (int sweep = 0; sweep < 60; ++sweep) {
+        double off = 0.0, tot = 0.0;
+        for (int j = 0; j < p; ++j)
+            for (int i = 0; i < p; ++i) {
+                tot += A(i, j) * A(i, j);
+                if (i != j) off += A(i, j) * A(i, j);
+            }
+        if (off <= 1e-30 * tot) break;
+        for (int P = 0; P < p - 1; ++P)
+            for (int Q = P + 1; Q < p; ++Q) {
+                const double apq = A(P, Q);
+                if (apq == 0.0) continue;
+                const double theta = (A(Q, Q) - A(P, P)) / (2.0 * apq);
+                const double t = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
+                const double cs = 1.0 / std::sqrt(t * t + 1.0), sn = t * cs;
+                for (int k = 0; k < p; ++k) {
+                    const double akp = A(k, P), akq = A(k, Q);
+                    A(k, P) = cs * akp - sn * akq;
+                    A(k, Q) = sn * akp + cs * akq;
+                }
+                for (int k = 0; k < p; ++k) {
+                    const double apk = A(P, k), aqk = A(Q, k);
+                    A(P, k) = cs * apk - sn * aqk;
+                    A(Q, k) = sn * apk + cs * aqk;
+                }
+                for (int k = 0; k < p; ++k) {
+                    const double vkp = Vv(k, P), vkq = Vv(k, Q);
+                    Vv(k, P) = cs * vkp - sn * vkq;
+                    Vv(k, Q) = sn * vkp + cs * vkq;
+                }
+            }
+    }
+    std::vector<int> ord(p);
+    for (int i = 0; i < p; ++i) ord[i] = i;
+    std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return A(x, x) < A(y, y); });
+    std::vector<double> sorted(static_cast<size_t>(p) * p);
+    vals.resize(p);
+    for (int c = 0; c < p; ++c) {
+        vals[c] = A(ord[c], ord[c]);
+        for (int i = 0; i < p; ++i) sorted[static_cast<size_t>(c) * p + i] = Vv(i, ord[c]);
+    }
+    vecs.swap(sorted);
+}
+
+// Q (V x p row-major = p x V col-major) = orthonormal basis of range(Y): CholeskyQR2 with
+// DGEMM Gram products; modified Gram-Schmidt on the host (with random completion) when
+// the Gram matrix is not numerically positive definite (rank-deficient block).
+struct OrthWork {
+    DevBuf<double> G, Rinv, tmp;
+};
+void orthonormalize(skc_context* ctx, int V, int p, const double* Yd, double* Qd, OrthWork& w, Rng& rng) {
+    cublasHandle_t h = cublas_of(ctx);
+    const double one = 1.0, zero = 0.0;
+    w.G.alloc(static_cast<size_t>(p) * p);
+    w.Rinv.alloc(static_cast<size_t>(p) * p);
+    w.tmp.alloc(static_cast<size_t>(V) * p);
+    std::vector<double> G(static_cast<size_t>(p) * p), Ri(static_cast<size_t>(p) * p);
+    const double* src = Yd;
+    for (int pass = 0; pass < 2; ++pass) {
+        CB(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, p, p, V, &one, src, p, src, p, &zero, w.G.p, p));
+        CK(cudaMemcpyAsync(G.data(), w.G.p, G.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->sync();
+        // Cholesky G = R^T R (R upper, col-major)
+        bool ok = true;
+        double gmax = 0.0;
+        for (int i = 0; i < p; ++i) gmax = std::max(gmax, G[static_cast<size_t>(i) * p + i]);
+        std::vector<double> R(static_cast<size_t>(p) * p, 0.0);
+        for (int j = 0; j < p && ok; ++j) {
+            for (int i = 0; i <= j; ++i) {
+                double s = G[static_cast<size_t>(j) * p + i];
+                for (int k = 0; k < i; ++k) s -= R[static_cast<size_t>(i) * p + k] * R[static_cast<size_t>(j) * p + k];
+                if (i == j) {
+                    if (!(s > 1e-12 * gmax)) {
+                        ok = false;
+                        break;
+                    }
+                    R[static_cast<size_t>(j) * p + j] = std::sqrt(s);
+                } else {
+                    R[static_cast<size_t>(j) * p + i] = s / R[static_cast<size_t>(i) * p + i];
+                }
+            }
+        }
+        if (!ok) {
+            // host modified Gram-Schmidt (twice) with random completion of null directions
+            std::vector<double> Y(static_cast<size_t>(V) * p);
+            CK(cudaMemcpyAsync(Y.data(), src, Y.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+            ctx->sync();
+            auto col = [&](int c, int r) -> double& { return Y[static_cast<size_t>(r) * p + c]; };
+            double ymax = 0.0;
+            for (double x : Y) ymax = std::max(ymax, std::fabs(x));
+            for (int c = 0; c < p; ++c) {
+                for (int attempt = 0; attempt < 8; ++attempt) {
+                    for (int rep = 0; rep < 2; ++rep)
+                        for (int c2 = 0; c2 < c; ++c2) {
+                            double d = 0.0;
+                            for (int r = 0; r < V; ++r) d += col(c2, r) * col(c, r);
+                            for (int r = 0; r < V; ++r) col(c, r) -= d * col(c2, r);
+                        }
+                    double nr = 0.0;
+                    for (int r = 0; r < V; ++r) nr += col(c, r) * col(c, r);
+                    nr = std::sqrt(nr);
+                    if (nr > 1e-10 * std::max(ymax, 1e-300) && nr > 0.0) {
+                        for (int r = 0; r < V; ++r) col(c, r) /= nr;
+                        break;
+                    }
+                    for (int r = 0; r < V; ++r) col(c, r) = rng.gaussian();
+                    ymax = 1.0;
+                }
+            }
+            CK(cudaMemcpyAsync(Qd, Y.data(), Y.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+            ctx->sync();
+            return;
+        }
+        // Rinv (upper) by back substitution, col-major
+        std::fill(Ri.begin(), Ri.end(), 0.0);
+        for (int j = 0; j < p; ++j) {
+            Ri[static_cast<size_t>(j) * p + j] = 1.0 / R[static_cast<size_t>(j) * p + j];
+            for (int i = j - 1; i >= 0; --i) {
+                double s = 0.0;
+                for (int k = i + 1; k <= j; ++k) s += R[static_cast<size_t>(k) * p + i] * Ri[static_cast<size_t>(j) * p + k];
+                Ri[static_cast<size_t>(j) * p + i] = -s / R[static_cast<size_t>(i) * p + i];
+            }
+        }
+        CK(cudaMemcpyAsync(w.Rinv.p, Ri.data(), Ri.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        // Q^T = Rinv^T Y^T  (col-major: (p x V) = (p x p)^T (p x V))
+        double* dst = (pass == 0) ? w.tmp.p : Qd;
+        CB(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, p, V, p, &one, w.Rinv.p, p, src, p, &zero, dst, p));
+        src = dst;
+    }
+}
+
+// whiten (lda.cpp:125-143) for an operator apply(X, Y): Y = M2 X on V x p device blocks.
+template <typename Apply>
+void whiten_randomized(skc_context* ctx, int V, int k, int oversample, int iters, std::uint64_t seed, Apply apply,
+                       double* W_out, double* U_out, double* sv_out) {
+    require(k >= 1 && k <= V, "whiten: invalid target rank");
+    if (oversample < 0) oversample = std::max(16, k / 4);
+    if (iters < 0) iters = 12;
+    const int p = std::min(V, (k + oversample + 31) / 32 * 32);
+    Rng rng(derive_seed(seed, seed_tag::kWhitenProbe));
+    std::vector<double> om(static_cast<size_t>(V) * p);
+    for (double& x : om) x = rng.gaussian();
+    DevBuf<double> Q, Y;
+    Q.alloc(om.size());
+    Y.upload(om.data(), om.size(), ctx->stream);
+    OrthWork ow;
+    orthonormalize(ctx, V, p, Y.p, Q.p, ow, rng);
+    for (int it = 0; it < iters; ++it) {
+        apply(Q.p, Y.p, p);
+        orthonormalize(ctx, V, p, Y.p, Q.p, ow, rng);
+    }
+    apply(Q.p, Y.p, p);
+    // Rayleigh-Ritz: H = Q^T M2 Q (p x p)
+    cublasHandle_t h = cublas_of(ctx);
+    const double one = 1.0, zero = 0.0;
+    DevBuf<double> Hd;
+    Hd.alloc(static_cast<size_t>(p) * p);
+    CB(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, p, p, V, &one, Q.p, p, Y.p, p, &zero, Hd.p, p));
+    std::vector<double> H(static_cast<size_t>(p) * p);
+    CK(cudaMemcpyAsync(H.data(), Hd.p, H.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    for (int i = 0; i < p; ++i)
+        for (int j = i + 1; j < p; ++j) {
+            const double s = 0.5 * (H[static_cast<size_t>(j) * p + i] + H[static_cast<size_t>(i) * p + j]);
+            H[static_cast<size_t>(j) * p + i] = H[static_cast<size_t>(i) * p + j] = s;
+        }
+    std::vector<double> ev, U;
+    jacobi_eigen(p, H, ev, U);
+    std::vector<double> Uk(static_cast<size_t>(p) * k), fw(k), fu(k);
+    for (int c = 0; c < k; ++c) {
+        const double e = ev[p - 1 - c];
+        if (!(e > 1e-10))  // lda.cpp:133-136
+            fail(kNumericalError, "whiten: moment matrix is rank deficient at component " + std::to_string(c + 1) +
+                                      " (eigenvalue " + std::to_string(e) + ")");
+        sv_out[c] = e;
+        fw[c] = 1.0 / std::sqrt(e);
+        fu[c] = std::sqrt(e);
+        std::copy(U.begin() + static_cast<size_t>(p - 1 - c) * p, U.begin() + static_cast<size_t>(p - c) * p,
+                  Uk.begin() + static_cast<size_t>(c) * p);
+    }
+    DevBuf<double> Ukd, Vk, fwd, fud, out;
+    Ukd.upload(Uk.data(), Uk.size(), ctx->stream);
+    Vk.alloc(static_cast<size_t>(V) * k);
+    // Vk (V x k row-major = k x V col-major) = Uk^T (k x p) Q^T (p x V)
+    CB(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, k, V, p, &one, Ukd.p, p, Q.p, p, &zero, Vk.p, k));
+    fwd.upload(fw.data(), fw.size(), ctx->stream);
+    fud.upload(fu.data(), fu.size(), ctx->stream);
+    out.alloc(static_cast<size_t>(V) * k);
+    launch_scale_cols(ctx->stream, V, k, Vk.p, fwd.p, out.p);
+    CK(cudaMemcpyAsync(W_out, out.p, static_cast<size_t>(V) * k * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    launch_scale_cols(ctx->stream, V, k, Vk.p, fud.p, out.p);
+    CK(cudaMemcpyAsync(U_out, out.p, static_cast<size_t>(V) * k * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+}
+
 }  // namespace
 
 // ============================ C-ABI ==============================================
@@ -708,6 +1016,7 @@ int skc_context_destroy(skc_context* ctx) {
         cudaSetDevice(ctx->device);
         cudaStreamSynchronize(ctx->stream);
         if (ctx->stream2) cudaStreamSynchronize(ctx->stream2);
+        if (ctx->cublas) cublasDestroy(ctx->cublas);
         cudaStream_t st = ctx->stream, st2 = ctx->stream2;
         cudaEvent_t ev[5];
         for (int c = 0; c < 5; ++c) ev[c] = ctx->ev_q[c];
@@ -2034,6 +2343,97 @@ int skc_gen_planted_tensor_device(skc_context* ctx, int n, int rank, double sigm
                            dev_out);
         ctx->check_launch();
         ctx->sync();
+    });
+}
+
+
+// ---- LDA moments and whitening (lda.cpp:88-143) ----------------------------------------
+int skc_lda_compute_m1(skc_context* ctx, int V, long long D, const long long* doc_ptr, const int* word,
+                       const int* count, double* m1_out) {
+    return guard([&] {
+        check_vec(ctx, "context");
+        check_vec(m1_out, "compute_m1: out");
+        ctx->use();
+        CorpusDev c;
+        upload_corpus(ctx, V, D, doc_ptr, word, count, c);
+        check_corpus_m1(c);
+        CK(cudaMemcpyAsync(m1_out, c.m1p.p, static_cast<size_t>(V) * sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        ctx->sync();
+        for (int w = 0; w < V; ++w) m1_out[w] /= static_cast<double>(c.used1);  // lda.cpp:99
+    });
+}
+
+int skc_lda_m2_apply(skc_context* ctx, int V, long long D, const long long* doc_ptr, const int* word,
+                     const int* count, double alpha0, int p, const double* X, double* Y) {
+    return guard([&] {
+        check_vec(ctx, "context");
+        check_vec(X, "m2_apply: X");
+        check_vec(Y, "m2_apply: Y");
+        require(p >= 1, "m2_apply: p must be positive");
+        ctx->use();
+        CorpusDev c;
+        upload_corpus(ctx, V, D, doc_ptr, word, count, c);
+        check_corpus_m2(c);
+        DevBuf<double> Xd, Yd;
+        Xd.upload(X, static_cast<size_t>(V) * p, ctx->stream);
+        Yd.alloc(static_cast<size_t>(V) * p);
+        M2Work w;
+        m2_apply(ctx, c, alpha0, p, Xd.p, Yd.p, w);
+        CK(cudaMemcpyAsync(Y, Yd.p, static_cast<size_t>(V) * p * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->sync();
+    });
+}
+
+int skc_lda_whiten_corpus(skc_context* ctx, int V, long long D, const long long* doc_ptr, const int* word,
+                          const int* count, double alpha0, int k, int oversample, int iters, uint64_t seed,
+                          double* W, double* unwhiten, double* singular_values) {
+    return guard([&] {
+        check_vec(ctx, "context");
+        check_vec(W, "whiten: W");
+        check_vec(unwhiten, "whiten: unwhiten");
+        check_vec(singular_values, "whiten: singular_values");
+        ctx->use();
+        CorpusDev c;
+        upload_corpus(ctx, V, D, doc_ptr, word, count, c);
+        check_corpus_m2(c);
+        require(k >= 1 && k <= V, "whiten: invalid target rank");
+        M2Work w;
+        SKC_PROF(ctx, "lda_whiten");
+        whiten_randomized(
+            ctx, V, k, oversample, iters, seed,
+            [&](const double* Xd, double* Yd, int p) { m2_apply(ctx, c, alpha0, p, Xd, Yd, w); }, W, unwhiten,
+            singular_values);
+    });
+}
+
+int skc_lda_whiten_dense(skc_context* ctx, int V, const double* m2, int k, int oversample, int iters, uint64_t seed,
+                         double* W, double* unwhiten, double* singular_values) {
+    return guard([&] {
+        check_vec(ctx, "context");
+        check_vec(m2, "whiten: m2hat");
+        check_vec(W, "whiten: W");
+        check_vec(unwhiten, "whiten: unwhiten");
+        check_vec(singular_values, "whiten: singular_values");
+        require(V >= 1, "whiten: matrix must be square");
+        require(k >= 1 && k <= V, "whiten: invalid target rank");
+        ctx->use();
+        // SelfAdjointEigenSolver reads the lower triangle: symmetrise from it
+        std::vector<double> M(static_cast<size_t>(V) * V);
+        for (int i = 0; i < V; ++i)
+            for (int j = 0; j <= i; ++j)
+                M[static_cast<size_t>(i) * V + j] = M[static_cast<size_t>(j) * V + i] = m2[static_cast<size_t>(i) * V + j];
+        DevBuf<double> Md;
+        Md.upload(M.data(), M.size(), ctx->stream);
+        cublasHandle_t h = cublas_of(ctx);
+        const double one = 1.0, zero = 0.0;
+        whiten_randomized(
+            ctx, V, k, oversample, iters, seed,
+            [&](const double* Xd, double* Yd, int p) {
+                // Y^T (p x V) = X^T (p x V) M2 (V x V)
+                CB(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, p, V, V, &one, Xd, p, Md.p, V, &zero, Yd, p));
+            },
+            W, unwhiten, singular_values);
     });
 }
 

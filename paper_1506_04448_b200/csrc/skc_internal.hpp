@@ -108,6 +108,16 @@ void launch_build_main(cudaStream_t st, const void* T, const BuildPlan& p);
 void launch_build_finalize(cudaStream_t st, const BuildPlan& p);
 void launch_build_finalize_multi(cudaStream_t st, const BuildPlan& p, int K, const int* scale_exps);
 
+// LDA moments / whitening (skc_whiten.cu)
+void launch_corpus_prep(cudaStream_t st, int V, long long D, const long long* doc_ptr, const int* count,
+                        const long long* cptr, const long long* cdoc, const int* ccount, long long* total, double* s2,
+                        double* invm, double* diag, double* m1p);
+void launch_m2_apply(cudaStream_t st, int V, long long D, int p, const long long* doc_ptr, const int* word,
+                     const int* count, const long long* cptr, const long long* cdoc, const int* ccount,
+                     const double* s2, const double* diag, const double* m1p, double inv_used1, double inv_used2,
+                     double a, const double* X, double* Z, double* mx, double* Y);
+void launch_scale_cols(cudaStream_t st, long long rows, int k, const double* in, const double* f, double* out);
+
 // residue twiddle tables of a symmetric set (SymView::stw*/gtw*)
 void launch_sym_twiddle_tables(cudaStream_t st, const SymView& v, double2* stw1, double2* stw2, double2* gtw1,
                                double2* gtw2);

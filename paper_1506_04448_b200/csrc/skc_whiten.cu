@@ -1,0 +1,175 @@
+// K6: LDA moments and whitening on sm_100a (lda.cpp:88-143).
+//
+// The reference forms M2 densely (V x V, 20 GB at V = 5e4) and calls a full
+// SelfAdjointEigenSolver. Here M2 is never formed. It is applied to a V x p block as
+//
+//   M2 X = (1/used2) [ C^T (S2 (C X)) - diag(sum_d s2_d n_d) X ] - a0/(a0+1) m1 (m1^T X),
+//
+// where C is the D x V count matrix, S2 = diag(1/(m_d (m_d - 1))) over documents with
+// m_d >= 2, and m1 = (1/used1) sum_{m_d >= 1} n_d / m_d. This equals the reference's
+// position-pair sum, pair(a, a) = c_a (c_a - 1), exactly, duplicates included. Top-k
+// eigenpairs come from randomized subspace iteration with Rayleigh-Ritz (host code in
+// skc_abi.cu; the block products use cuBLAS DGEMM).
+//
+//   k_corpus_docs   per document: m_d, s2_d, 1/m_d                       (thread/doc)
+//   k_m2_word_prep  per word: diag_w = sum s2_d c_dw, m1_w (CSC, fixed order)  (thread/word)
+//   k_m2_docs       Z[d, :] = s2_d sum_q c_q X[w_q, :]                     (warp/doc)
+//   k_colsum        mx = m1^T X                                           (block/32 cols)
+//   k_m2_words      Y[w, :] = (sum_{d in w} c Z[d, :] - diag_w X[w, :]) / used2
+//                             - a m1_w mx                                  (warp/word)
+// Every sum runs in a fixed order, so the operator is deterministic.
+#include <cuda_runtime.h>
+
+#include "skc_host.hpp"
+#include "skc_internal.hpp"
+
+namespace skc {
+
+namespace {
+inline unsigned cdiv_w(long long a, long long b) { return static_cast<unsigned>((a + b - 1) / b); }
+}  // namespace
+
+__global__ void k_corpus_docs(long long D, const long long* __restrict__ doc_ptr, const int* __restrict__ count,
+                              long long* __restrict__ total, double* __restrict__ s2, double* __restrict__ invm) {
+    const long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (d >= D) return;
+    long long t = 0;
+    for (long long q = doc_ptr[d]; q < doc_ptr[d + 1]; ++q) t += count[q];
+    total[d] = t;
+    const double m = static_cast<double>(t);
+    s2[d] = t >= 2 ? 1.0 / (m * (m - 1.0)) : 0.0;  // lda.cpp:111
+    invm[d] = t >= 1 ? 1.0 / m : 0.0;              // lda.cpp:94
+}
+
+__global__ void k_m2_word_prep(int V, const long long* __restrict__ cptr, const long long* __restrict__ cdoc,
+                               const int* __restrict__ ccount, const double* __restrict__ s2,
+                               const double* __restrict__ invm, double* __restrict__ diag, double* __restrict__ m1p) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= V) return;
+    double dg = 0.0, m = 0.0;
+    for (long long q = cptr[w]; q < cptr[w + 1]; ++q) {
+        const long long d = cdoc[q];
+        const double c = static_cast<double>(ccount[q]);
+        dg += s2[d] * c;
+        m += invm[d] * c;
+    }
+    diag[w] = dg;
+    m1p[w] = m;
+}
+
+__global__ void k_m2_docs(long long D, int p, const long long* __restrict__ doc_ptr, const int* __restrict__ word,
+                          const int* __restrict__ count, const double* __restrict__ s2, const double* __restrict__ X,
+                          double* __restrict__ Z) {
+    const long long d = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (d >= D) return;
+    const double sd = s2[d];
+    const long long q0 = doc_ptr[d], q1 = doc_ptr[d + 1];
+    for (int c0 = 0; c0 < p; c0 += 128) {
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        if (sd != 0.0) {
+            for (long long q = q0; q < q1; ++q) {
+                const double cnt = static_cast<double>(count[q]);
+                const double* xr = X + (size_t)word[q] * p;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int c = c0 + lane + 32 * u;
+                    if (c < p) acc[u] += cnt * xr[c];
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int c = c0 + lane + 32 * u;
+            if (c < p) Z[(size_t)d * p + c] = sd * acc[u];
+        }
+    }
+}
+
+// mx[c] = sum_w m1_w X[w, c] with m1_w = m1p_w / used1; block per 32 columns, 8 warps
+// striding the rows, warp partials combined in a fixed order.
+__global__ void k_colsum(int V, int p, const double* __restrict__ m1p, double inv_used1, const double* __restrict__ X,
+                         double* __restrict__ mx) {
+    __shared__ double part[8][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int c = blockIdx.x * 32 + lane;
+    double acc = 0.0;
+    if (c < p)
+        for (int w = warp; w < V; w += 8) acc += (m1p[w] * inv_used1) * X[(size_t)w * p + c];
+    part[warp][lane] = acc;
+    __syncthreads();
+    if (warp == 0 && c < p) {
+        double s = 0.0;
+        for (int i = 0; i < 8; ++i) s += part[i][lane];
+        mx[c] = s;
+    }
+}
+
+__global__ void k_m2_words(int V, int p, const long long* __restrict__ cptr, const long long* __restrict__ cdoc,
+                           const int* __restrict__ ccount, const double* __restrict__ Z, const double* __restrict__ diag,
+                           const double* __restrict__ m1p, double inv_used1, double inv_used2, double a,
+                           const double* __restrict__ mx, const double* __restrict__ X, double* __restrict__ Y) {
+    const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= V) return;
+    const long long q0 = cptr[w], q1 = cptr[w + 1];
+    const double dg = diag[w];
+    const double m1w = m1p[w] * inv_used1;
+    for (int c0 = 0; c0 < p; c0 += 128) {
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (long long q = q0; q < q1; ++q) {
+            const double cnt = static_cast<double>(ccount[q]);
+            const double* zr = Z + (size_t)cdoc[q] * p;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int c = c0 + lane + 32 * u;
+                if (c < p) acc[u] += cnt * zr[c];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int c = c0 + lane + 32 * u;
+            if (c < p) {
+                const size_t idx = (size_t)w * p + c;
+                Y[idx] = (acc[u] - dg * X[idx]) * inv_used2 - a * m1w * mx[c];
+            }
+        }
+    }
+}
+
+// W[w, c] = Vk[w, c] * f[c] (row-major V x k): scaling of the Ritz vectors
+__global__ void k_scale_cols(long long rows, int k, const double* __restrict__ in, const double* __restrict__ f,
+                             double* __restrict__ out) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= rows * k) return;
+    out[i] = in[i] * f[i % k];
+}
+
+void launch_corpus_prep(cudaStream_t st, int V, long long D, const long long* doc_ptr, const int* count,
+                        const long long* cptr, const long long* cdoc, const int* ccount, long long* total, double* s2,
+                        double* invm, double* diag, double* m1p) {
+    if (D > 0) k_corpus_docs<<<cdiv_w(D, 256), 256, 0, st>>>(D, doc_ptr, count, total, s2, invm);
+    k_m2_word_prep<<<cdiv_w(V, 256), 256, 0, st>>>(V, cptr, cdoc, ccount, s2, invm, diag, m1p);
+    count_launch();
+    count_launch();
+}
+
+void launch_m2_apply(cudaStream_t st, int V, long long D, int p, const long long* doc_ptr, const int* word,
+                     const int* count, const long long* cptr, const long long* cdoc, const int* ccount,
+                     const double* s2, const double* diag, const double* m1p, double inv_used1, double inv_used2,
+                     double a, const double* X, double* Z, double* mx, double* Y) {
+    if (D > 0) k_m2_docs<<<cdiv_w(D * 32, 256), 256, 0, st>>>(D, p, doc_ptr, word, count, s2, X, Z);
+    k_colsum<<<cdiv_w(p, 32), 256, 0, st>>>(V, p, m1p, inv_used1, X, mx);
+    k_m2_words<<<cdiv_w((long long)V * 32, 256), 256, 0, st>>>(V, p, cptr, cdoc, ccount, Z, diag, m1p, inv_used1,
+                                                               inv_used2, a, mx, X, Y);
+    count_launch();
+    count_launch();
+    count_launch();
+}
+
+void launch_scale_cols(cudaStream_t st, long long rows, int k, const double* in, const double* f, double* out) {
+    k_scale_cols<<<cdiv_w(rows * k, 256), 256, 0, st>>>(rows, k, in, f, out);
+    count_launch();
+}
+
+}  // namespace skc

@@ -89,6 +89,10 @@ def _setup(L):
         "orc_contract_Ivv_exact": (None, [d_p, C.c_int, d_p, d_p, d_p]),
         "orc_first_asymmetric_triple": (C.c_int, [d_p, C.c_int, C.c_double, i_p]),
         "orc_greedy_match": (C.c_int, [d_p, C.c_int, d_p, C.c_int, C.c_int, d_p]),
+        "orc_lda_compute_m1": (C.c_int, [C.c_int, C.c_int, ll_p, i_p, i_p, d_p]),
+        "orc_lda_compute_m2": (C.c_int, [C.c_int, C.c_int, ll_p, i_p, i_p, C.c_double, d_p]),
+        "orc_sym_eigen": (C.c_int, [C.c_int, d_p, d_p, d_p]),
+        "orc_lda_whiten": (C.c_int, [C.c_int, d_p, C.c_int, d_p, d_p, d_p]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -329,6 +333,49 @@ def contract_Ivv_exact(T, u, v):
     out = np.empty(T.shape[0])
     lib().orc_contract_Ivv_exact(dp(T), T.shape[0], dp(f64(u)), dp(f64(v)), dp(out))
     return out
+
+
+def _corpus(doc_ptr, word, count):
+    dpn = np.ascontiguousarray(doc_ptr, dtype=np.int64)
+    wd = np.ascontiguousarray(word, dtype=np.int32)
+    ct = np.ascontiguousarray(count, dtype=np.int32)
+    return dpn, wd, ct
+
+
+def lda_compute_m1(V, doc_ptr, word, count):
+    """lda.cpp:88-100"""
+    dpn, wd, ct = _corpus(doc_ptr, word, count)
+    out = np.zeros(V)
+    _chk(lib().orc_lda_compute_m1(V, dpn.size - 1, dpn.ctypes.data_as(ll_p), wd.ctypes.data_as(i_p),
+                                  ct.ctypes.data_as(i_p), dp(out)))
+    return out
+
+
+def lda_compute_m2(V, doc_ptr, word, count, alpha0):
+    """lda.cpp:102-123 (dense V x V)"""
+    dpn, wd, ct = _corpus(doc_ptr, word, count)
+    out = np.zeros((V, V))
+    _chk(lib().orc_lda_compute_m2(V, dpn.size - 1, dpn.ctypes.data_as(ll_p), wd.ctypes.data_as(i_p),
+                                  ct.ctypes.data_as(i_p), float(alpha0), dp(out)))
+    return out
+
+
+def sym_eigen(A):
+    """Jacobi eigensolver (ascending), stand-in for Eigen::SelfAdjointEigenSolver."""
+    A = f64(A)
+    n = A.shape[0]
+    ev, U = np.zeros(n), np.zeros((n, n))
+    _chk(lib().orc_sym_eigen(n, dp(A), dp(ev), dp(U)))
+    return ev, U
+
+
+def lda_whiten(m2, k):
+    """lda.cpp:125-143: (W, unwhiten, singular_values), W and unwhiten V x k."""
+    m2 = f64(m2)
+    V = m2.shape[0]
+    W, Uw, sv = np.zeros((V, k)), np.zeros((V, k)), np.zeros(k)
+    _chk(lib().orc_lda_whiten(V, dp(m2), k, dp(W), dp(Uw), dp(sv)))
+    return W, Uw, sv
 
 
 def greedy_match(rec, truth):

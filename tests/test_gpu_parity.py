@@ -426,6 +426,72 @@ def test_lda_rejects_short_corpus(gpu_ctx):
         s.sketch_whitened_m3(5, [0, 1, 2], [0, 1], [1, 2], np.ones((5, 4)), 1.0)
 
 
+# ---------------------------------------------------------------- LDA moments / whitening (§8f rank 1)
+def _align_cols(A, ref):
+    """Flip column signs of A to match ref (eigenvector signs are unpinned, lda.cpp:128)."""
+    s = np.sign(np.sum(A * ref, axis=0))
+    s[s == 0] = 1
+    return A * s
+
+
+@pytest.mark.parametrize("alpha0", [1.0, 0.3])
+def test_lda_m1_and_m2_operator_match_oracle(gpu_ctx, alpha0):
+    from lda_fixtures import synthetic_corpus
+
+    V = 120
+    doc_ptr, word, count, _ = synthetic_corpus(V=V, k=6, D=500, mean_len=9, seed=11)
+    m1 = skb().compute_m1(V, doc_ptr, word, count, gpu_ctx)
+    m1_ref = O.lda_compute_m1(V, doc_ptr, word, count)
+    assert np.max(np.abs(m1 - m1_ref)) <= 1e-14 * np.max(np.abs(m1_ref))
+    M2 = O.lda_compute_m2(V, doc_ptr, word, count, alpha0)
+    X = np.random.default_rng(2).normal(size=(V, 37))
+    Y = skb().m2_apply(V, doc_ptr, word, count, alpha0, X, gpu_ctx)
+    assert np.max(np.abs(Y - M2 @ X)) <= 1e-12 * np.max(np.abs(M2 @ X))
+
+
+@pytest.mark.parametrize("dense", [False, True])
+def test_lda_whiten_matches_dense_eigensolver_oracle(gpu_ctx, dense):
+    """Randomized subspace iteration on the implicit (or dense) M2 reproduces whiten's
+    top-k eigenpairs (lda.cpp:125-143) from the oracle's full Jacobi eigendecomposition."""
+    from lda_fixtures import synthetic_corpus
+
+    V, k, alpha0 = 150, 6, 1.0
+    doc_ptr, word, count, _ = synthetic_corpus(V=V, k=k, D=3000, mean_len=30, seed=3)
+    M2 = O.lda_compute_m2(V, doc_ptr, word, count, alpha0)
+    W_ref, U_ref, sv_ref = O.lda_whiten(M2, k)
+    if dense:
+        wm = skb().whiten(M2, k, iters=40, ctx=gpu_ctx)
+    else:
+        wm = skb().whiten_corpus(V, doc_ptr, word, count, alpha0, k, iters=40, ctx=gpu_ctx)
+    assert np.max(np.abs(wm.singular_values - sv_ref) / sv_ref) <= 1e-9
+    W = _align_cols(wm.W, W_ref)
+    U = _align_cols(wm.unwhiten, U_ref)
+    assert np.max(np.abs(W - W_ref)) <= 1e-6 * np.max(np.abs(W_ref))
+    assert np.max(np.abs(U - U_ref)) <= 1e-6 * np.max(np.abs(U_ref))
+    # W' M2 W = I on the input moment (lda.hpp:43)
+    assert np.max(np.abs(wm.W.T @ M2 @ wm.W - np.eye(k))) <= 1e-8
+
+
+def test_lda_whiten_errors_follow_reference(gpu_ctx):
+    from lda_fixtures import synthetic_corpus
+
+    V = 40
+    doc_ptr, word, count, _ = synthetic_corpus(V=V, k=3, D=200, mean_len=12, seed=4)
+    with pytest.raises(ValueError, match="whiten: invalid target rank"):
+        skb().whiten_corpus(V, doc_ptr, word, count, 1.0, V + 1, ctx=gpu_ctx)
+    with pytest.raises(skb().NumericalError, match="compute_m1: empty corpus"):
+        skb().compute_m1(V, [0], [], [], gpu_ctx)
+    with pytest.raises(skb().NumericalError, match="compute_m2: no documents with at least 2 words"):
+        skb().m2_apply(V, [0, 1, 2], [0, 1], [1, 1], 1.0, np.ones((V, 1)), gpu_ctx)
+    # a PSD matrix of rank 3 cannot be whitened to k = 5 (lda.cpp:133-136)
+    Q = np.linalg.qr(np.random.default_rng(0).normal(size=(V, 3)))[0]
+    M = Q @ np.diag([3.0, 2.0, 1.0]) @ Q.T
+    with pytest.raises(skb().NumericalError, match="rank deficient at component 4"):
+        skb().whiten(M, 5, ctx=gpu_ctx)
+    with pytest.raises(O.OracleError, match="rank deficient at component 4"):
+        O.lda_whiten(M, 5)
+
+
 # ---------------------------------------------------------------- sym_aux / truncated rank-1 (a16)
 @pytest.mark.parametrize("n,b", [(9, 64), (30, 16384)])
 def test_sym_aux_and_truncated_rank1_match_oracle(gpu_ctx, n, b):

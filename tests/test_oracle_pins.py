@@ -324,3 +324,45 @@ def test_lda_sketch_whitened_m3_equals_dense_sketch_of_moment():
         d = O.SymSet(k, 256, 4, 11)
         d.accumulate_dense(T, assume_symmetric=True)
         assert np.max(np.abs(s.data() - d.data())) <= 1e-10 * np.max(np.abs(d.data()))
+
+
+# ---- LDA moments / whitening oracle (lda.cpp:88-143) pinned against numpy -------------
+def test_oracle_m2_and_whiten_match_numpy_restatement():
+    from lda_fixtures import synthetic_corpus
+
+    V, k, alpha0 = 60, 4, 0.7
+    doc_ptr, word, count, _ = synthetic_corpus(V=V, k=k, D=400, mean_len=15, seed=9)
+    D = doc_ptr.size - 1
+    m1 = np.zeros(V)
+    used1 = 0
+    M2 = np.zeros((V, V))
+    used2 = 0
+    for d in range(D):
+        ws = word[doc_ptr[d]:doc_ptr[d + 1]]
+        cs = count[doc_ptr[d]:doc_ptr[d + 1]].astype(float)
+        tot = cs.sum()
+        if tot >= 1:
+            m1[ws] += cs / tot
+            used1 += 1
+        if tot >= 2:
+            used2 += 1
+            nd = np.zeros(V)
+            np.add.at(nd, ws, cs)
+            M2 += (np.outer(nd, nd) - np.diag(nd)) / (tot * (tot - 1))
+    m1 /= used1
+    M2 = M2 / used2 - alpha0 / (alpha0 + 1) * np.outer(m1, m1)
+    assert np.max(np.abs(O.lda_compute_m1(V, doc_ptr, word, count) - m1)) <= 1e-15
+    M2o = O.lda_compute_m2(V, doc_ptr, word, count, alpha0)
+    assert np.max(np.abs(M2o - M2)) <= 1e-14 * np.max(np.abs(M2))
+    ev, U = np.linalg.eigh(M2o)
+    W, Uw, sv = O.lda_whiten(M2o, k)
+    assert np.allclose(sv, ev[::-1][:k], rtol=1e-12, atol=0)
+    top = U[:, ::-1][:, :k]
+    sgn = np.sign(np.sum(top * W, axis=0))
+    assert np.max(np.abs(W - top * sgn / np.sqrt(sv))) <= 1e-10
+    assert np.max(np.abs(Uw - top * sgn * np.sqrt(sv))) <= 1e-10
+
+
+def test_oracle_whiten_rejects_bad_rank():
+    with pytest.raises(O.OracleError, match="whiten: invalid target rank"):
+        O.lda_whiten(np.eye(4), 5)
