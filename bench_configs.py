@@ -10,7 +10,8 @@ on the host cores (bounded samples, stated in each line).
   C3  factored third moment, n=1000, K=50 Dirichlet(0.1) mixtures + 0.1 N(0,I), b=2^14 B=10:
       frequency-domain accumulation (reduced N, linear in N), then RTPM k=50 L=T=30
   C4  LDA V=50000 K=100, Dirichlet(0.01) topics, Poisson(150) docs (reduced D), b=2^14 B=10:
-      sketch_whitened_m3 given W, then RTPM L=100 k=100 T=30
+      whitening from the corpus M2 (implicit, randomized), sketch_whitened_m3, then RTPM
+      L=100 k=100 T=30
 
 Usage: python bench_configs.py [--configs 0,1,2,3,4] [--quick]
 """
@@ -180,12 +181,24 @@ def c4(skb, ctx, quick):
         doc_ptr.append(doc_ptr[-1] + nz.size)
     words = np.concatenate(words)
     counts = np.concatenate(counts)
-    W, _ = np.linalg.qr(rng.normal(size=(V, K)))
+    # whitening from the corpus' own second moment (lda.cpp:102-143, implicit M2 on the GPU)
+    alpha0 = 1.0
+    t0 = time.perf_counter()
+    ctx.profile(True)
+    ctx.profile_reset()
+    wm = skb.whiten_corpus(V, np.array(doc_ptr), words, counts, alpha0, K, ctx=ctx)
+    whiten_s = time.perf_counter() - t0
+    whiten_dev = ctx.profile_get("lda_whiten")[0]
+    ctx.profile(False)
+    emit({"config": 4, "what": "whiten(compute_m2(corpus), K) by randomized subspace iteration on the implicit M2",
+          "V": V, "K": K, "D": D, "nnz": int(words.size), "seconds": whiten_s, "device_ms": whiten_dev,
+          "top_eigenvalues": wm.singular_values[:3].tolist(), "kth_eigenvalue": float(wm.singular_values[-1])})
+    W = wm.W
     s = skb.SymTensorSketchSet(K, b, B, 9, ctx)
     t0 = time.perf_counter()
     ctx.profile(True)
     ctx.profile_reset()
-    used, skipped = s.sketch_whitened_m3(V, np.array(doc_ptr), words, counts, W, 1.0)
+    used, skipped = s.sketch_whitened_m3(V, np.array(doc_ptr), words, counts, W, alpha0)
     wall = time.perf_counter() - t0
     dev = {x: ctx.profile_get(x)[0] for x in ["lda_docs", "lda_vocab", "lda_accumulate"]}
     ctx.profile(False)
@@ -194,8 +207,23 @@ def c4(skb, ctx, quick):
           "device_ms_by_kernel": dev, "docs_per_s_device": D / (sum(dev.values()) * 1e-3)})
     k = 5 if quick else 100
     t0 = time.perf_counter()
-    skb.robust_tpm_fast(s, skb.PowerConfig(k=k, L=100, T_iters=30, seed=2))
-    emit({"config": 4, "what": f"RTPM k={k} L=100 T=30 on the whitened sketch", "seconds": time.perf_counter() - t0})
+    dec = skb.robust_tpm_fast(s, skb.PowerConfig(k=k, L=100, T_iters=30, seed=2))
+    rtpm_s = time.perf_counter() - t0
+    # recover_params (lda.cpp:228-248) and the recovery quality against the generating topics
+    model = skb.recover_params(dec, wm, alpha0)
+    Pn = model.Phi / np.linalg.norm(model.Phi, axis=0, keepdims=True)
+    Tn = topics.T / np.linalg.norm(topics.T, axis=0, keepdims=True)
+    cos = Pn.T @ Tn  # k x K
+    best = []
+    used_t = set()
+    for c in np.argsort(-cos.max(axis=1)):
+        order = np.argsort(-cos[c])
+        t = next(t for t in order if t not in used_t)
+        used_t.add(t)
+        best.append(cos[c, t])
+    emit({"config": 4, "what": f"RTPM k={k} L=100 T=30 on the whitened sketch + recover_params", "seconds": rtpm_s,
+          "topic_cos_median": float(np.median(best)), "topic_cos_min": float(np.min(best)),
+          "alpha0_recovered": float(model.alpha.sum())})
 
 
 def main():

@@ -154,6 +154,16 @@ int skc_lda_whiten_corpus(skc_context* ctx, int V, long long D, const long long*
 int skc_lda_whiten_dense(skc_context* ctx, int V, const double* m2, int k, int oversample, int iters, uint64_t seed,
                          double* W, double* unwhiten, double* singular_values);
 
+/* recover_params(D, wm, alpha0) (lda.cpp:228-248), host math: lambda[k], A = D.A (k x k
+ * row-major, column i = component i), unwhiten V x k -> Phi V x k (columns projected onto
+ * the simplex, lda.cpp:250-271) and alpha[k]. */
+int skc_lda_recover_params(int V, int k, const double* lambda, const double* A, const double* unwhiten, double alpha0,
+                           double* Phi, double* alpha);
+/* heldout_likelihood(model, held) (lda.cpp:273-320): Phi V x k, held-out corpus CSR over
+ * vocabulary Vh <= V; documents fitted in parallel, summed in document order. */
+int skc_lda_heldout_likelihood(int V, int k, const double* Phi, int Vh, long long D, const long long* doc_ptr,
+                               const int* word, const int* count, double* ll_out, long long* floored_words);
+
 /* replicate(m).data -> host (B-major when m < 0: all replicates, B*b complex). */
 int skc_sym_read_data(const skc_sym_set* s, int m, double* out_host);
 /* mutable_replicate(m).data = in (bumps version, sketch.hpp:105-108); m < 0: all. */

@@ -780,6 +780,40 @@ def whiten(m2hat, k: int, oversample: int = -1, iters: int = -1, seed: int = 0x5
     return WhiteningMap(W, U, sv)
 
 
+class LdaModel:
+    """lda.hpp:33-39: Phi (V x k, column-stochastic) and alpha (k)."""
+
+    def __init__(self, Phi, alpha):
+        self.Phi, self.alpha = Phi, alpha
+
+    def alpha0(self) -> float:
+        return float(self.alpha.sum())
+
+
+def recover_params(dec: "CpDecomposition", wm: WhiteningMap, alpha0: float) -> LdaModel:
+    """lda.cpp:228-248 (host math)."""
+    A = _f64(dec.A)
+    k = A.shape[1]
+    if A.shape[0] != wm.W.shape[1]:
+        raise ValueError("recover_params: decomposition/whitening rank mismatch")
+    lam = _f64(dec.lambda_)
+    V = wm.unwhiten.shape[0]
+    Phi, alpha = np.empty((V, k)), np.empty(k)
+    check(lib.skc_lda_recover_params(V, k, _dp(lam), _dp(A), _dp(_f64(wm.unwhiten)), float(alpha0), _dp(Phi),
+                                     _dp(alpha)))
+    return LdaModel(Phi, alpha)
+
+
+def heldout_likelihood(model: LdaModel, V_held: int, doc_ptr, word, count):
+    """lda.cpp:273-320 -> (mean per-word log-likelihood, floored word count)."""
+    Phi = _f64(model.Phi)
+    keep, (D, dpp, wdp, ctp) = _corpus_args(doc_ptr, word, count)
+    ll, fl = C.c_double(), C.c_longlong()
+    check(lib.skc_lda_heldout_likelihood(Phi.shape[0], Phi.shape[1], _dp(Phi), int(V_held), D, dpp, wdp, ctp,
+                                         C.byref(ll), C.byref(fl)))
+    return ll.value, fl.value
+
+
 def gen_planted_tensor(n: int, rank: int, sigma: float, seed: int, dtype=np.float64):
     """Host generator of the BASELINE planted tensors (configs 0-2). Returns (T, lambda, V)."""
     T = np.empty((n, n, n), dtype=dtype)

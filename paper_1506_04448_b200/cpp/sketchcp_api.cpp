@@ -559,6 +559,124 @@ long long Corpus::total_tokens() const {
     for (const auto& d : docs) t += d.total;
     return t;
 }
+namespace {
+struct CorpusCsr {
+    std::vector<long long> doc_ptr{0};
+    std::vector<int> word, count;
+    explicit CorpusCsr(const Corpus& c) {
+        for (const auto& d : c.docs) {
+            word.insert(word.end(), d.word.begin(), d.word.end());
+            count.insert(count.end(), d.count.begin(), d.count.end());
+            doc_ptr.push_back(static_cast<long long>(word.size()));
+        }
+    }
+    long long D() const { return static_cast<long long>(doc_ptr.size()) - 1; }
+};
+WhiteningMap whitening_from_rowmajor(int V, int k, const std::vector<double>& W, const std::vector<double>& U,
+                                     const std::vector<double>& sv) {
+    WhiteningMap wm;
+    wm.W.resize(V, k);
+    wm.unwhiten.resize(V, k);
+    wm.singular_values.resize(k);
+    for (int w = 0; w < V; ++w)
+        for (int a = 0; a < k; ++a) {
+            wm.W(w, a) = W[static_cast<std::size_t>(w) * k + a];
+            wm.unwhiten(w, a) = U[static_cast<std::size_t>(w) * k + a];
+        }
+    for (int a = 0; a < k; ++a) wm.singular_values[a] = sv[a];
+    return wm;
+}
+}  // namespace
+
+Eigen::VectorXd compute_m1(const Corpus& c) {
+    CorpusCsr csr(c);
+    Eigen::VectorXd m1(c.V);
+    check(skc_lda_compute_m1(context(), c.V, csr.D(), csr.doc_ptr.data(), csr.word.data(), csr.count.data(), m1.data()));
+    return m1;
+}
+
+Eigen::MatrixXd compute_m2(const Corpus& c, double alpha0) {
+    CorpusCsr csr(c);
+    const int V = c.V;
+    Eigen::MatrixXd m2(V, V);
+    const int blk = std::min(V, 256);
+    std::vector<double> X(static_cast<std::size_t>(V) * blk), Y(X.size());
+    for (int c0 = 0; c0 < V; c0 += blk) {
+        const int p = std::min(blk, V - c0);
+        std::fill(X.begin(), X.end(), 0.0);
+        for (int j = 0; j < p; ++j) X[static_cast<std::size_t>(c0 + j) * p + j] = 1.0;
+        check(skc_lda_m2_apply(context(), V, csr.D(), csr.doc_ptr.data(), csr.word.data(), csr.count.data(), alpha0, p,
+                               X.data(), Y.data()));
+        for (int w = 0; w < V; ++w)
+            for (int j = 0; j < p; ++j) m2(w, c0 + j) = Y[static_cast<std::size_t>(w) * p + j];
+    }
+    return m2;
+}
+
+WhiteningMap whiten(const Eigen::MatrixXd& m2hat, int k) {
+    if (m2hat.rows() != m2hat.cols()) throw std::invalid_argument("whiten: matrix must be square");
+    const int V = static_cast<int>(m2hat.rows());
+    if (k < 1 || k > V) throw std::invalid_argument("whiten: invalid target rank");
+    std::vector<double> M(static_cast<std::size_t>(V) * V);
+    for (int i = 0; i < V; ++i)
+        for (int j = 0; j < V; ++j) M[static_cast<std::size_t>(i) * V + j] = m2hat(i, j);
+    std::vector<double> W(static_cast<std::size_t>(V) * k), U(W.size()), sv(k);
+    check(skc_lda_whiten_dense(context(), V, M.data(), k, -1, -1, 0x5EED, W.data(), U.data(), sv.data()));
+    return whitening_from_rowmajor(V, k, W, U, sv);
+}
+
+WhiteningMap whiten_corpus(const Corpus& c, double alpha0, int k) {
+    CorpusCsr csr(c);
+    const int V = c.V;
+    if (k < 1 || k > V) throw std::invalid_argument("whiten: invalid target rank");
+    std::vector<double> W(static_cast<std::size_t>(V) * k), U(W.size()), sv(k);
+    check(skc_lda_whiten_corpus(context(), V, csr.D(), csr.doc_ptr.data(), csr.word.data(), csr.count.data(), alpha0, k,
+                                -1, -1, 0x5EED, W.data(), U.data(), sv.data()));
+    return whitening_from_rowmajor(V, k, W, U, sv);
+}
+
+LdaModel recover_params(const CpDecomposition& D, const WhiteningMap& wm, double alpha0) {
+    const int k = D.rank();
+    if (k < 1) throw std::invalid_argument("recover_params: empty decomposition");
+    if (D.A.rows() != wm.W.cols()) throw std::invalid_argument("recover_params: decomposition/whitening rank mismatch");
+    const int V = static_cast<int>(wm.W.rows()), r = static_cast<int>(D.A.rows());
+    std::vector<double> A(static_cast<std::size_t>(r) * k), U(static_cast<std::size_t>(V) * r), Phi(static_cast<std::size_t>(V) * k);
+    for (int i = 0; i < r; ++i)
+        for (int j = 0; j < k; ++j) A[static_cast<std::size_t>(i) * k + j] = D.A(i, j);
+    for (int w = 0; w < V; ++w)
+        for (int j = 0; j < r; ++j) U[static_cast<std::size_t>(w) * r + j] = wm.unwhiten(w, j);
+    LdaModel m;
+    m.alpha.resize(k);
+    check(skc_lda_recover_params(V, k, D.lambda.data(), A.data(), U.data(), alpha0, Phi.data(), m.alpha.data()));
+    m.Phi.resize(V, k);
+    for (int w = 0; w < V; ++w)
+        for (int j = 0; j < k; ++j) m.Phi(w, j) = Phi[static_cast<std::size_t>(w) * k + j];
+    return m;
+}
+
+Eigen::VectorXd project_to_simplex(const Eigen::VectorXd& y) {
+    // one-column recover_params with lambda chosen so mu = y: 0.5 (a0 + 2) lam = 1 at a0 = 0, lam = 1
+    const int n = static_cast<int>(y.size());
+    double one = 1.0, a = 1.0, alpha = 0.0;
+    Eigen::VectorXd out(n);
+    check(skc_lda_recover_params(n, 1, &one, &a, y.data(), 0.0, out.data(), &alpha));
+    return out;
+}
+
+double heldout_likelihood(const LdaModel& m, const Corpus& held, long long* floored_words) {
+    CorpusCsr csr(held);
+    const int V = m.vocab(), k = m.topics();
+    std::vector<double> Phi(static_cast<std::size_t>(V) * k);
+    for (int w = 0; w < V; ++w)
+        for (int j = 0; j < k; ++j) Phi[static_cast<std::size_t>(w) * k + j] = m.Phi(w, j);
+    double ll = 0.0;
+    long long fl = 0;
+    check(skc_lda_heldout_likelihood(V, k, Phi.data(), held.V, csr.D(), csr.doc_ptr.data(), csr.word.data(),
+                                     csr.count.data(), &ll, &fl));
+    if (floored_words) *floored_words = fl;
+    return ll;
+}
+
 StreamStats sketch_whitened_m3(const Corpus& c, const WhiteningMap& wm, double alpha0, SymTensorSketchSet& set) {
     const int k = static_cast<int>(wm.W.cols()), V = c.V;
     if (wm.W.rows() != V) throw std::invalid_argument("sketch_whitened_m3: vocabulary mismatch");

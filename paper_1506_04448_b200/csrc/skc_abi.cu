@@ -970,6 +970,30 @@ void whiten_randomized(skc_context* ctx, int V, int k, int oversample, int iters
     ctx->sync();
 }
 
+
+// lda.cpp:250-271: Euclidean projection onto the probability simplex (sort-based)
+std::vector<double> project_to_simplex(const double* y, int n) {
+    std::vector<double> u(y, y + n);
+    std::sort(u.begin(), u.end(), std::greater<double>());
+    double css = 0, theta = 0;
+    int rho = 0;
+    for (int i = 0; i < n; ++i) {
+        css += u[i];
+        const double t = (css - 1.0) / (i + 1);
+        if (u[i] - t > 0) {
+            rho = i + 1;
+            theta = t;
+        }
+    }
+    std::vector<double> x(n);
+    if (rho == 0) {  // all mass collapsed: uniform (lda.cpp:262-265)
+        std::fill(x.begin(), x.end(), 1.0 / n);
+        return x;
+    }
+    for (int i = 0; i < n; ++i) x[i] = std::max(y[i] - theta, 0.0);
+    return x;
+}
+
 }  // namespace
 
 // ============================ C-ABI ==============================================
@@ -2434,6 +2458,112 @@ int skc_lda_whiten_dense(skc_context* ctx, int V, const double* m2, int k, int o
                 CB(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, p, V, V, &one, Xd, p, Md.p, V, &zero, Yd, p));
             },
             W, unwhiten, singular_values);
+    });
+}
+
+
+// lda.cpp:228-248: topics and prior from the whitened CP decomposition (host math, O(V k)).
+int skc_lda_recover_params(int V, int k, const double* lambda, const double* A, const double* unwhiten, double alpha0,
+                           double* Phi, double* alpha) {
+    return guard([&] {
+        require(k >= 1, "recover_params: empty decomposition");
+        check_vec(lambda, "recover_params: lambda");
+        check_vec(A, "recover_params: A");
+        check_vec(unwhiten, "recover_params: unwhiten");
+        check_vec(Phi, "recover_params: Phi");
+        check_vec(alpha, "recover_params: alpha");
+        require(V >= 1, "recover_params: decomposition/whitening rank mismatch");
+        std::vector<double> mu(V);
+        for (int i = 0; i < k; ++i) {
+            const double lam = lambda[i];
+            if (lam == 0.0) fail(kNumericalError, "recover_params: zero eigenvalue at component " + std::to_string(i + 1));
+            alpha[i] = 4.0 * alpha0 * (alpha0 + 1.0) / ((alpha0 + 2.0) * (alpha0 + 2.0) * lam * lam);
+            for (int w = 0; w < V; ++w) {  // mu = 0.5 (a0 + 2) lam * unwhiten A[:, i]
+                double s = 0.0;
+                for (int c = 0; c < k; ++c) s += unwhiten[static_cast<size_t>(w) * k + c] * A[static_cast<size_t>(c) * k + i];
+                mu[w] = 0.5 * (alpha0 + 2.0) * lam * s;
+            }
+            const std::vector<double> ph = project_to_simplex(mu.data(), V);
+            for (int w = 0; w < V; ++w) Phi[static_cast<size_t>(w) * k + i] = ph[w];
+        }
+    });
+}
+
+// lda.cpp:273-320: mean per-document held-out log-likelihood, mixtures by simplex-
+// projected gradient (500 steps, stop at |step| <= 1e-8). Documents in parallel
+// (each is independent; the final sum runs in document order).
+int skc_lda_heldout_likelihood(int V, int k, const double* Phi, int Vh, long long D, const long long* doc_ptr,
+                               const int* word, const int* count, double* ll_out, long long* floored_out) {
+    return guard([&] {
+        check_vec(Phi, "heldout_likelihood: Phi");
+        check_vec(doc_ptr, "heldout_likelihood: doc_ptr");
+        check_vec(ll_out, "heldout_likelihood: out");
+        require(Vh <= V, "heldout_likelihood: corpus vocabulary exceeds the model's");
+        std::vector<double> gram(static_cast<size_t>(k) * k, 0.0);
+        for (int a = 0; a < k; ++a)
+            for (int b = 0; b < k; ++b) {
+                double s = 0.0;
+                for (int w = 0; w < V; ++w) s += Phi[static_cast<size_t>(w) * k + a] * Phi[static_cast<size_t>(w) * k + b];
+                gram[static_cast<size_t>(b) * k + a] = s;
+            }
+        std::vector<double> ev, U;
+        jacobi_eigen(k, gram, ev, U);
+        const double lips = ev.empty() ? 0.0 : ev.back();
+        const double step = lips > 0 ? 1.0 / lips : 1.0;
+        std::vector<double> per(static_cast<size_t>(std::max<long long>(D, 1)), 0.0);
+        std::vector<long long> fl(static_cast<size_t>(std::max<long long>(D, 1)), 0);
+        std::vector<char> used(static_cast<size_t>(std::max<long long>(D, 1)), 0);
+#pragma omp parallel for schedule(dynamic, 16)
+        for (long long d = 0; d < D; ++d) {
+            long long tot = 0;
+            for (long long q = doc_ptr[d]; q < doc_ptr[d + 1]; ++q) tot += count[q];
+            if (tot < 1) continue;
+            used[d] = 1;
+            std::vector<double> pi(k, 1.0 / k);
+            if (k > 1) {
+                std::vector<double> phi_tw(k, 0.0), grad(k), next(k);
+                const double inv_m = 1.0 / static_cast<double>(tot);
+                for (long long q = doc_ptr[d]; q < doc_ptr[d + 1]; ++q)
+                    for (int a = 0; a < k; ++a)
+                        phi_tw[a] += (inv_m * count[q]) * Phi[static_cast<size_t>(word[q]) * k + a];
+                for (int it = 0; it < 500; ++it) {
+                    for (int a = 0; a < k; ++a) {
+                        double s = 0.0;
+                        for (int b = 0; b < k; ++b) s += gram[static_cast<size_t>(b) * k + a] * pi[b];
+                        grad[a] = pi[a] - step * (s - phi_tw[a]);
+                    }
+                    next = project_to_simplex(grad.data(), k);
+                    double moved = 0.0;
+                    for (int a = 0; a < k; ++a) moved += (next[a] - pi[a]) * (next[a] - pi[a]);
+                    pi.swap(next);
+                    if (std::sqrt(moved) <= 1e-8) break;
+                }
+            } else {
+                pi.assign(1, 1.0);
+            }
+            double ll = 0.0;
+            for (long long q = doc_ptr[d]; q < doc_ptr[d + 1]; ++q) {
+                double pw = 0.0;
+                for (int a = 0; a < k; ++a) pw += Phi[static_cast<size_t>(word[q]) * k + a] * pi[a];
+                if (pw < 1e-12) {
+                    pw = 1e-12;
+                    ++fl[d];
+                }
+                ll += count[q] * std::log(pw);
+            }
+            per[d] = ll / static_cast<double>(tot);
+        }
+        double total = 0.0;
+        long long nused = 0, floored = 0;
+        for (long long d = 0; d < D; ++d)
+            if (used[d]) {
+                total += per[d];
+                ++nused;
+                floored += fl[d];
+            }
+        if (floored_out) *floored_out = floored;
+        if (nused == 0) fail(kNumericalError, "heldout_likelihood: empty held-out corpus");
+        *ll_out = total / static_cast<double>(nused);
     });
 }
 

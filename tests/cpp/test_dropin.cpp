@@ -252,6 +252,60 @@ TEST_CASE("sketch_whitened_m3 stream statistics (lda.cpp:145-226)", lda_stats) {
     CHECK_THROWS_AS(sketch_whitened_m3(c, wm, 1.0, wrong), std::invalid_argument);
 }
 
+TEST_CASE("lda moments, whitening, recovery", lda_whitening_pipeline) {
+    // lda.cpp:88-320 through the reference-named API: dense M2 + whiten equals the
+    // corpus (implicit-M2) whitening; recover_params yields column-stochastic topics.
+    Rng rng(77);
+    Corpus c;
+    c.V = 40;
+    for (int d = 0; d < 400; ++d) {
+        Document doc;
+        const int topic = d % 3;
+        for (int t = 0; t < 20; ++t) {
+            int w = (rng.uniform() < 0.8) ? topic * 10 + static_cast<int>(rng.uniform_below(10))
+                                          : static_cast<int>(rng.uniform_below(40));
+            auto it = std::find(doc.word.begin(), doc.word.end(), w);
+            if (it == doc.word.end()) {
+                doc.word.push_back(w);
+                doc.count.push_back(1);
+            } else {
+                ++doc.count[it - doc.word.begin()];
+            }
+            doc.total += 1;
+        }
+        c.docs.push_back(doc);
+    }
+    const Eigen::VectorXd m1 = compute_m1(c);
+    CHECK(std::abs(m1.sum() - 1.0) < 1e-12);
+    const Eigen::MatrixXd m2 = compute_m2(c, 1.0);
+    const WhiteningMap a = whiten(m2, 3), b = whiten_corpus(c, 1.0, 3);
+    for (int i = 0; i < 3; ++i) CHECK(std::abs(a.singular_values[i] - b.singular_values[i]) < 1e-9 * a.singular_values[i]);
+    // W' M2 W = I
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double s = 0.0;
+            for (int u = 0; u < c.V; ++u)
+                for (int v = 0; v < c.V; ++v) s += b.W(u, i) * m2(u, v) * b.W(v, j);
+            CHECK(std::abs(s - (i == j ? 1.0 : 0.0)) < 1e-8);
+        }
+    CHECK_THROWS_AS(whiten(m2, 41), std::invalid_argument);
+    CpDecomposition D = CpDecomposition::symmetric_of(Eigen::VectorXd::Constant(3, 1.5), Eigen::MatrixXd::Identity(3, 3));
+    const LdaModel m = recover_params(D, b, 1.0);
+    for (int i = 0; i < 3; ++i) {
+        double s = 0.0;
+        for (int w = 0; w < c.V; ++w) {
+            CHECK(m.Phi(w, i) >= 0.0);
+            s += m.Phi(w, i);
+        }
+        CHECK(std::abs(s - 1.0) < 1e-12);
+    }
+    long long floored = -1;
+    const double ll = heldout_likelihood(m, c, &floored);
+    CHECK(std::isfinite(ll) && ll < 0.0 && floored >= 0);
+    const Eigen::VectorXd y = project_to_simplex(Eigen::VectorXd{0.5, 0.5, 0.5});
+    CHECK(std::abs(y[0] - 1.0 / 3.0) < 1e-15);
+}
+
 int main() {
     for (auto& [name, fn] : registry()) {
         try {

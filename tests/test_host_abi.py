@@ -92,3 +92,67 @@ def test_no_gpu_means_loud_failure():
         pytest.skip("a GPU is visible")
     with pytest.raises(skb.CudaError):
         skb.Context(0)
+
+
+# ---- LDA recover_params / heldout_likelihood (lda.cpp:228-320): host math, no GPU -------
+def _np_project_to_simplex(y):
+    u = np.sort(y)[::-1]
+    css = np.cumsum(u)
+    t = (css - 1.0) / np.arange(1, y.size + 1)
+    ok = np.nonzero(u - t > 0)[0]
+    if ok.size == 0:
+        return np.full(y.size, 1.0 / y.size)
+    return np.maximum(y - t[ok[-1]], 0.0)
+
+
+def test_lda_recover_params_matches_restatement():
+    import paper_1506_04448_b200 as skb
+
+    rng = np.random.default_rng(1)
+    V, k, alpha0 = 30, 4, 0.8
+    lam = rng.uniform(0.5, 2.0, size=k)
+    A = np.linalg.qr(rng.normal(size=(k, k)))[0]
+    Uw = rng.normal(size=(V, k))
+    wm = skb.WhiteningMap(np.zeros((V, k)), Uw, np.ones(k))
+    dec = skb.CpDecomposition.symmetric_of(lam, A)
+    m = skb.recover_params(dec, wm, alpha0)
+    for i in range(k):
+        mu = 0.5 * (alpha0 + 2.0) * lam[i] * (Uw @ A[:, i])
+        assert np.allclose(m.Phi[:, i], _np_project_to_simplex(mu), rtol=0, atol=1e-14)
+        assert np.isclose(m.alpha[i], 4 * alpha0 * (alpha0 + 1) / ((alpha0 + 2) ** 2 * lam[i] ** 2), rtol=1e-15)
+    with pytest.raises(skb.NumericalError, match="zero eigenvalue at component 2"):
+        skb.recover_params(skb.CpDecomposition.symmetric_of(np.array([1.0, 0.0, 1.0, 1.0]), A), wm, alpha0)
+
+
+def test_lda_heldout_likelihood_matches_restatement():
+    import paper_1506_04448_b200 as skb
+    from lda_fixtures import synthetic_corpus
+
+    V, k = 25, 3
+    doc_ptr, word, count, _ = synthetic_corpus(V=V, k=k, D=30, mean_len=10, seed=8)
+    Phi = np.random.default_rng(3).dirichlet(np.full(V, 0.5), size=k).T
+    ll, fl = skb.heldout_likelihood(skb.LdaModel(Phi, np.ones(k)), V, doc_ptr, word, count)
+    gram = Phi.T @ Phi
+    step = 1.0 / np.linalg.eigvalsh(gram).max()
+    tot_ll, used, floored = 0.0, 0, 0
+    for d in range(doc_ptr.size - 1):
+        ws = word[doc_ptr[d]:doc_ptr[d + 1]]
+        cs = count[doc_ptr[d]:doc_ptr[d + 1]].astype(float)
+        m = cs.sum()
+        if m < 1:
+            continue
+        used += 1
+        phi_tw = (cs / m) @ Phi[ws]
+        pi = np.full(k, 1.0 / k)
+        for _ in range(500):
+            nxt = _np_project_to_simplex(pi - step * (gram @ pi - phi_tw))
+            moved = np.linalg.norm(nxt - pi)
+            pi = nxt
+            if moved <= 1e-8:
+                break
+        p = Phi[ws] @ pi
+        floored += int(np.sum(p < 1e-12))
+        p = np.maximum(p, 1e-12)
+        tot_ll += float(cs @ np.log(p)) / m
+    assert abs(ll - tot_ll / used) <= 1e-10 * abs(tot_ll / used)
+    assert fl == floored
