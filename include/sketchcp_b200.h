@@ -131,6 +131,12 @@ int skc_sym_accumulate_moment(skc_sym_set* s, const double* X, const double* w, 
 int skc_sym_sketch_whitened_m3(skc_sym_set* s, int V, long long D, const long long* doc_ptr, const int* word,
                                const int* count, const double* W, double alpha0, long long* used,
                                long long* skipped);
+/* als_fast(set, AlsConfig{k, max_iters, tol, seed}) (decompose.cpp:117-205): CP-ALS with
+ * batched sketched mode contractions. lambda[k]; A, B, C n x k column-major; iters_out
+ * (may be null) receives the number of sweeps run. */
+int skc_asym_als(skc_asym_set* s, int k, int max_iters, double tol, uint64_t seed, double* lambda, double* A,
+                 double* B, double* C, int* iters_out);
+
 /* ---- LDA moments and whitening (lda.cpp:88-143) -------------------------------------
  * Corpus arguments as for skc_sym_sketch_whitened_m3 (host CSR). Matrices are row-major.
  * compute_m1 (lda.cpp:88-100): m1[V] = mean over documents with >= 1 token of n_d / m_d. */

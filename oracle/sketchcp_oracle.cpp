@@ -66,7 +66,7 @@ inline std::uint64_t derive_seed(std::uint64_t master, std::uint64_t tag, std::u
 }
 
 constexpr std::uint64_t kAsymBucketHash = 0x11, kAsymSign = 0x12, kSymBucketHash = 0x21,
-                        kSymSign = 0x22, kPowerInit = 0x31;
+                        kSymSign = 0x22, kPowerInit = 0x31, kAlsInit = 0x32;
 
 // --- rng.hpp:51-141 ----------------------------------------------------------
 class Rng {
@@ -1386,6 +1386,95 @@ int orc_asym_mode_contraction(void* h, int free_mode, const double* x, const dou
         auto& s = *static_cast<AsymSet*>(h);
         AsymWs ws{&s, s.version - 1, {}};
         asym_mode_contraction(ws, free_mode, x, y, out);
+    });
+}
+
+// decompose.cpp:44-51 + 117-205: pinv_spectral and als_fast restated (test oracle).
+int orc_pinv_spectral(int k, const double* G, double* P) {
+    return guard([&] {
+        std::vector<double> ev(k), U(static_cast<std::size_t>(k) * k);
+        sym_eigen_jacobi(k, G, ev.data(), U.data());
+        double amax = 0.0;
+        for (double e : ev) amax = std::max(amax, std::fabs(e));
+        const double cutoff = 1e-10 * amax;
+        for (int i = 0; i < k; ++i)
+            for (int j = 0; j < k; ++j) {
+                double s = 0.0;
+                for (int q = 0; q < k; ++q)
+                    if (std::fabs(ev[q]) > cutoff)
+                        s += U[static_cast<std::size_t>(i) * k + q] * (1.0 / ev[q]) * U[static_cast<std::size_t>(j) * k + q];
+                P[static_cast<std::size_t>(i) * k + j] = s;
+            }
+    });
+}
+int orc_asym_als(void* h, int k, int max_iters, double tol, std::uint64_t seed, double* lambda_out, double* A_out,
+                 double* B_out, double* C_out, int* iters_out) {
+    return guard([&] {
+        auto& s = *static_cast<AsymSet*>(h);
+        const int n = s.n;
+        if (k < 1 || max_iters < 1) throw std::invalid_argument("als: k and max_iters must be positive");
+        if (k > n) throw std::invalid_argument("als: target rank exceeds tensor dimension");
+        // factors column-major n x k
+        std::vector<double> F[3];
+        for (auto& f : F) f.assign(static_cast<std::size_t>(n) * k, 0.0);
+        for (int r = 0; r < k; ++r) {
+            Rng rng(derive_seed(seed, kAlsInit, r));
+            for (int f = 0; f < 3; ++f) {
+                auto v = rng.unit_sphere(n);
+                std::copy(v.begin(), v.end(), F[f].begin() + static_cast<std::size_t>(r) * n);
+            }
+        }
+        AsymWs ws{&s, s.version - 1, {}};
+        std::vector<double> lambda(k, 1.0), lambda_prev(k, 1.0), M(static_cast<std::size_t>(n) * k), P(static_cast<std::size_t>(k) * k);
+        int it = 0;
+        for (; it < max_iters;) {
+            for (int mode = 0; mode < 3; ++mode) {
+                const int f1 = mode == 0 ? 1 : 0, f2 = mode == 2 ? 1 : 2;
+                for (int r = 0; r < k; ++r)
+                    asym_mode_contraction(ws, mode, F[f1].data() + static_cast<std::size_t>(r) * n,
+                                          F[f2].data() + static_cast<std::size_t>(r) * n, M.data() + static_cast<std::size_t>(r) * n);
+                std::vector<double> G(static_cast<std::size_t>(k) * k);
+                for (int a = 0; a < k; ++a)
+                    for (int b = 0; b < k; ++b) {
+                        double g1 = 0.0, g2 = 0.0;
+                        for (int i = 0; i < n; ++i) {
+                            g1 += F[f1][static_cast<std::size_t>(a) * n + i] * F[f1][static_cast<std::size_t>(b) * n + i];
+                            g2 += F[f2][static_cast<std::size_t>(a) * n + i] * F[f2][static_cast<std::size_t>(b) * n + i];
+                        }
+                        G[static_cast<std::size_t>(a) * k + b] = g1 * g2;
+                    }
+                if (orc_pinv_spectral(k, G.data(), P.data()) != 0) throw std::runtime_error(g_err);
+                std::vector<double> prev = F[mode];
+                for (int r = 0; r < k; ++r) {
+                    double nrm2 = 0.0;
+                    for (int i = 0; i < n; ++i) {
+                        double v = 0.0;
+                        for (int q = 0; q < k; ++q) v += M[static_cast<std::size_t>(q) * n + i] * P[static_cast<std::size_t>(q) * k + r];
+                        F[mode][static_cast<std::size_t>(r) * n + i] = v;
+                        nrm2 += v * v;
+                    }
+                    const double nrm = std::sqrt(nrm2);
+                    lambda[r] = nrm;
+                    for (int i = 0; i < n; ++i) {
+                        double& x = F[mode][static_cast<std::size_t>(r) * n + i];
+                        x = nrm > 0 ? x / nrm : prev[static_cast<std::size_t>(r) * n + i];
+                    }
+                }
+            }
+            ++it;
+            double dn = 0.0, pn = 0.0;
+            for (int r = 0; r < k; ++r) {
+                dn += (lambda[r] - lambda_prev[r]) * (lambda[r] - lambda_prev[r]);
+                pn += lambda_prev[r] * lambda_prev[r];
+            }
+            if (std::sqrt(dn) / std::max(std::sqrt(pn), 1e-300) < tol) break;
+            lambda_prev = lambda;
+        }
+        std::copy(lambda.begin(), lambda.end(), lambda_out);
+        std::copy(F[0].begin(), F[0].end(), A_out);
+        std::copy(F[1].begin(), F[1].end(), B_out);
+        std::copy(F[2].begin(), F[2].end(), C_out);
+        if (iters_out) *iters_out = it;
     });
 }
 

@@ -715,6 +715,29 @@ class AsymContractionWorkspace:
         return out
 
 
+class AlsConfig:
+    """decompose.hpp:19-26"""
+
+    def __init__(self, k=1, max_iters=1000, tol=1e-6, b=4096, B=40, seed=0):
+        self.k, self.max_iters, self.tol, self.b, self.B, self.seed = k, max_iters, tol, b, B, seed
+
+
+def als_fast(set_: "AsymTensorSketchSet", cfg: AlsConfig) -> CpDecomposition:
+    """decompose.cpp:199-205: CP-ALS on the asymmetric sketch set (batched sketched mode
+    contractions on the GPU). Returns CpDecomposition with A, B, C (n x k); the number of
+    sweeps run is in .iters."""
+    n = set_.n()
+    k = int(cfg.k)
+    lam = np.empty(k)
+    A, B, Cm = (np.empty((k, n)) for _ in range(3))
+    it = C.c_int()
+    check(lib.skc_asym_als(set_.handle, k, int(cfg.max_iters), float(cfg.tol), C.c_uint64(cfg.seed), _dp(lam), _dp(A),
+                           _dp(B), _dp(Cm), C.byref(it)))
+    d = CpDecomposition(lam, A.T.copy(), B.T.copy(), Cm.T.copy())
+    d.iters = it.value
+    return d
+
+
 # ---- LDA moments and whitening (lda.hpp:49-57, lda.cpp:88-143) ---------------------------
 def _corpus_args(doc_ptr, word, count):
     dp = np.ascontiguousarray(doc_ptr, dtype=np.int64)

@@ -65,6 +65,7 @@ SIGNATURES = {
     "skc_sym_add_scaled_rank1": (c_int, [p_void, p_double, c_double]),
     "skc_sym_accumulate_moment": (c_int, [p_void, p_double, p_double, c_ll, c_int]),
     "skc_sym_sketch_whitened_m3": (c_int, [p_void, c_int, c_ll, p_ll, p_int, p_int, p_double, c_double, p_ll, p_ll]),
+    "skc_asym_als": (c_int, [p_void, c_int, c_int, c_double, c_u64, p_double, p_double, p_double, p_double, p_int]),
     "skc_lda_compute_m1": (c_int, [p_void, c_int, c_ll, p_ll, p_int, p_int, p_double]),
     "skc_lda_m2_apply": (c_int, [p_void, c_int, c_ll, p_ll, p_int, p_int, c_double, c_int, p_double, p_double]),
     "skc_lda_whiten_corpus": (c_int, [p_void, c_int, c_ll, p_ll, p_int, p_int, c_double, c_int, c_int, c_int, c_u64,

@@ -553,6 +553,76 @@ CpDecomposition robust_tpm_fast(SymTensorSketchSet& set, const PowerConfig& cfg)
     return CpDecomposition::symmetric_of(std::move(lambda), std::move(V));
 }
 
+CpDecomposition als_fast(const AsymTensorSketchSet& set, const AlsConfig& cfg) {
+    const int n = set.n(), k = cfg.k;
+    if (k < 1 || cfg.max_iters < 1) throw std::invalid_argument("als: k and max_iters must be positive");
+    if (k > n) throw std::invalid_argument("als: target rank exceeds tensor dimension");
+    Eigen::VectorXd lambda(k);
+    Eigen::MatrixXd A(n, k), B(n, k), C(n, k);  // column-major, as the C-ABI returns them
+    int iters = 0;
+    check(skc_asym_als(set.device_handle(), k, cfg.max_iters, cfg.tol, cfg.seed, lambda.data(), A.data(), B.data(),
+                       C.data(), &iters));
+    CpDecomposition d;
+    d.lambda = std::move(lambda);
+    d.A = std::move(A);
+    d.B = std::move(B);
+    d.C = std::move(C);
+    return d;
+}
+
+Eigen::MatrixXd pinv_spectral(const Eigen::MatrixXd& G) {
+    // symmetric eigendecomposition by cyclic Jacobi (host), truncation at 1e-10 max|ev|
+    const int k = static_cast<int>(G.rows());
+    if (G.cols() != k) throw std::invalid_argument("pinv_spectral: matrix must be square");
+    std::vector<double> a(G.data(), G.data() + static_cast<std::size_t>(k) * k), v(static_cast<std::size_t>(k) * k, 0.0);
+    for (int i = 0; i < k; ++i) v[static_cast<std::size_t>(i) * k + i] = 1.0;
+    auto A = [&](int i, int j) -> double& { return a[static_cast<std::size_t>(j) * k + i]; };
+    auto Vv = [&](int i, int j) -> double& { return v[static_cast<std::size_t>(j) * k + i]; };
+    for (int sweep = 0; sweep < 60; ++sweep) {
+        double off = 0.0, tot = 0.0;
+        for (int j = 0; j < k; ++j)
+            for (int i = 0; i < k; ++i) {
+                tot += A(i, j) * A(i, j);
+                if (i != j) off += A(i, j) * A(i, j);
+            }
+        if (off <= 1e-30 * tot) break;
+        for (int p = 0; p < k - 1; ++p)
+            for (int q = p + 1; q < k; ++q) {
+                const double apq = A(p, q);
+                if (apq == 0.0) continue;
+                const double th = (A(q, q) - A(p, p)) / (2.0 * apq);
+                const double t = (th >= 0 ? 1.0 : -1.0) / (std::abs(th) + std::sqrt(th * th + 1.0));
+                const double c = 1.0 / std::sqrt(t * t + 1.0), s = t * c;
+                for (int r = 0; r < k; ++r) {
+                    const double x = A(r, p), y = A(r, q);
+                    A(r, p) = c * x - s * y;
+                    A(r, q) = s * x + c * y;
+                }
+                for (int r = 0; r < k; ++r) {
+                    const double x = A(p, r), y = A(q, r);
+                    A(p, r) = c * x - s * y;
+                    A(q, r) = s * x + c * y;
+                }
+                for (int r = 0; r < k; ++r) {
+                    const double x = Vv(r, p), y = Vv(r, q);
+                    Vv(r, p) = c * x - s * y;
+                    Vv(r, q) = s * x + c * y;
+                }
+            }
+    }
+    double amax = 0.0;
+    for (int i = 0; i < k; ++i) amax = std::max(amax, std::abs(A(i, i)));
+    const double cutoff = 1e-10 * amax;
+    Eigen::MatrixXd P = Eigen::MatrixXd::Zero(k, k);
+    for (int q = 0; q < k; ++q) {
+        if (!(std::abs(A(q, q)) > cutoff)) continue;
+        const double inv = 1.0 / A(q, q);
+        for (int j = 0; j < k; ++j)
+            for (int i = 0; i < k; ++i) P(i, j) += Vv(i, q) * inv * Vv(j, q);
+    }
+    return P;
+}
+
 // ---- lda.hpp -------------------------------------------------------------------------
 long long Corpus::total_tokens() const {
     long long t = 0;

@@ -994,6 +994,64 @@ std::vector<double> project_to_simplex(const double* y, int n) {
     return x;
 }
 
+
+// decompose.cpp:44-51 pinv_spectral: symmetric pseudoinverse with spectral truncation at
+// 1e-10 of the largest |eigenvalue|. G is symmetric PSD here (Hadamard product of Grams):
+// when its Cholesky pivots show it is well conditioned the pseudoinverse is the inverse,
+// computed by Cholesky; otherwise the eigen-decomposition route (Jacobi) truncates.
+std::vector<double> pinv_spectral_host(int k, const std::vector<double>& G /* col-major */) {
+    std::vector<double> L(static_cast<size_t>(k) * k, 0.0);
+    bool ok = true;
+    double gmax = 0.0;
+    for (int i = 0; i < k; ++i) gmax = std::max(gmax, std::fabs(G[static_cast<size_t>(i) * k + i]));
+    for (int j = 0; j < k && ok; ++j) {
+        double s = G[static_cast<size_t>(j) * k + j];
+        for (int q = 0; q < j; ++q) s -= L[static_cast<size_t>(q) * k + j] * L[static_cast<size_t>(q) * k + j];
+        if (!(s > 1e-8 * gmax)) {  // margin above the 1e-10 spectral cutoff
+            ok = false;
+            break;
+        }
+        L[static_cast<size_t>(j) * k + j] = std::sqrt(s);
+        for (int i = j + 1; i < k; ++i) {
+            double t = G[static_cast<size_t>(j) * k + i];
+            for (int q = 0; q < j; ++q) t -= L[static_cast<size_t>(q) * k + i] * L[static_cast<size_t>(q) * k + j];
+            L[static_cast<size_t>(j) * k + i] = t / L[static_cast<size_t>(j) * k + j];
+        }
+    }
+    std::vector<double> P(static_cast<size_t>(k) * k, 0.0);
+    if (ok) {
+        // columns of G^{-1}: solve L L^T x = e_c
+        std::vector<double> y(k);
+        for (int c = 0; c < k; ++c) {
+            for (int i = 0; i < k; ++i) {
+                double s = (i == c) ? 1.0 : 0.0;
+                for (int q = 0; q < i; ++q) s -= L[static_cast<size_t>(q) * k + i] * y[q];
+                y[i] = s / L[static_cast<size_t>(i) * k + i];
+            }
+            for (int i = k - 1; i >= 0; --i) {
+                double s = y[i];
+                for (int q = i + 1; q < k; ++q) s -= L[static_cast<size_t>(i) * k + q] * P[static_cast<size_t>(c) * k + q];
+                P[static_cast<size_t>(c) * k + i] = s / L[static_cast<size_t>(i) * k + i];
+            }
+        }
+        return P;
+    }
+    std::vector<double> ev, U;
+    jacobi_eigen(k, G, ev, U);
+    double amax = 0.0;
+    for (double e : ev) amax = std::max(amax, std::fabs(e));
+    const double cutoff = 1e-10 * amax;
+    for (int q = 0; q < k; ++q) {
+        const double e = ev[q];
+        if (!(std::fabs(e) > cutoff)) continue;
+        const double inv = 1.0 / e;
+        for (int j = 0; j < k; ++j)
+            for (int i = 0; i < k; ++i)
+                P[static_cast<size_t>(j) * k + i] += U[static_cast<size_t>(q) * k + i] * inv * U[static_cast<size_t>(q) * k + j];
+    }
+    return P;
+}
+
 }  // namespace
 
 // ============================ C-ABI ==============================================
@@ -2564,6 +2622,90 @@ int skc_lda_heldout_likelihood(int V, int k, const double* Phi, int Vh, long lon
         if (floored_out) *floored_out = floored;
         if (nused == 0) fail(kNumericalError, "heldout_likelihood: empty held-out corpus");
         *ll_out = total / static_cast<double>(nused);
+    });
+}
+
+
+// als_fast(set, cfg) (decompose.cpp:117-205): CP-ALS where each factor column update is a
+// batched sketched mode contraction (contraction.cpp:248-295) of the other two factors'
+// columns. Factors stay on the device (column-major n x k); the k x k Grams are DGEMMs,
+// the spectral pseudoinverse is host math. A, B, C out: n x k column-major.
+int skc_asym_als(skc_asym_set* s, int k, int max_iters, double tol, uint64_t seed, double* lambda_out, double* A_out,
+                 double* B_out, double* C_out, int* iters_out) {
+    return guard([&] {
+        check_vec(s, "set");
+        check_vec(lambda_out, "als: lambda");
+        check_vec(A_out, "als: A");
+        check_vec(B_out, "als: B");
+        check_vec(C_out, "als: C");
+        if (k < 1 || max_iters < 1) fail(kInvalidArgument, "als: k and max_iters must be positive");  // decompose.cpp:125-126
+        if (k > s->n) fail(kInvalidArgument, "als: target rank exceeds tensor dimension");         // decompose.cpp:127
+        require(s->B <= 128, "median over more than 128 replicates is not supported");
+        skc_context* ctx = s->ctx;
+        ctx->use();
+        const int n = s->n;
+        const size_t nk = static_cast<size_t>(n) * k;
+        // als_init (decompose.cpp:124-138): one Rng per component r, A/B/C columns in turn
+        std::vector<double> h(3 * nk);
+        for (int r = 0; r < k; ++r) {
+            Rng rng(derive_seed(seed, seed_tag::kAlsInit, static_cast<std::uint64_t>(r)));
+            for (int f = 0; f < 3; ++f) rng.unit_sphere(n, h.data() + f * nk + static_cast<size_t>(r) * n);
+        }
+        DevBuf<double> F, M, prev, G1, G2, P, lam;
+        F.upload(h.data(), h.size(), ctx->stream);
+        M.alloc(nk);
+        prev.alloc(nk);
+        G1.alloc(static_cast<size_t>(k) * k);
+        G2.alloc(static_cast<size_t>(k) * k);
+        P.alloc(static_cast<size_t>(k) * k);
+        lam.alloc(static_cast<size_t>(k));
+        double* fac[3] = {F.p, F.p + nk, F.p + 2 * nk};
+        s->ensure_fresh();
+        ctx->part.alloc(static_cast<size_t>(k) * s->B * s->S * n);
+        cublasHandle_t hb = cublas_of(ctx);
+        const double one = 1.0, zero = 0.0;
+        std::vector<double> g1(static_cast<size_t>(k) * k), g2(g1.size()), G(g1.size());
+        std::vector<double> lambda(k, 1.0), lambda_prev(k, 1.0);  // s.lambda = Ones (decompose.cpp:129)
+        int it = 0;
+        for (; it < max_iters;) {
+            for (int mode = 0; mode < 3; ++mode) {
+                const int f1 = mode == 0 ? 1 : 0, f2 = mode == 2 ? 1 : 2;
+                // M[:, r] = T(free mode, F1[:, r], F2[:, r]) for all r at once
+                launch_asym_mode(ctx->stream, s->view(), mode, fac[f1], fac[f2], k, ctx->part.p);
+                launch_median_rows(ctx->stream, ctx->part.p, k, s->B, s->S, n, M.p, nullptr, 0.0, nullptr);
+                ctx->check_launch();
+                // G = (F1' F1) .* (F2' F2)
+                CB(cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, k, k, n, &one, fac[f1], n, fac[f1], n, &zero, G1.p, k));
+                CB(cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, k, k, n, &one, fac[f2], n, fac[f2], n, &zero, G2.p, k));
+                CK(cudaMemcpyAsync(g1.data(), G1.p, g1.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+                CK(cudaMemcpyAsync(g2.data(), G2.p, g2.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+                ctx->sync();
+                for (size_t q = 0; q < G.size(); ++q) G[q] = g1[q] * g2[q];
+                const std::vector<double> Pinv = pinv_spectral_host(k, G);
+                CK(cudaMemcpyAsync(P.p, Pinv.data(), Pinv.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+                // target = M * pinv(G); normalize_columns(target, prev, lambda)
+                CK(cudaMemcpyAsync(prev.p, fac[mode], nk * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+                CB(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, n, k, k, &one, M.p, n, P.p, k, &zero, fac[mode], n));
+                launch_normalize_columns(ctx->stream, n, k, fac[mode], prev.p, lam.p);
+                ctx->check_launch();
+            }
+            CK(cudaMemcpyAsync(lambda.data(), lam.p, static_cast<size_t>(k) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+            ctx->sync();
+            ++it;
+            double dn = 0.0, pn = 0.0;
+            for (int r = 0; r < k; ++r) {
+                dn += (lambda[r] - lambda_prev[r]) * (lambda[r] - lambda_prev[r]);
+                pn += lambda_prev[r] * lambda_prev[r];
+            }
+            if (std::sqrt(dn) / std::max(std::sqrt(pn), 1e-300) < tol) break;  // decompose.cpp:184-186
+            lambda_prev = lambda;
+        }
+        std::copy(lambda.begin(), lambda.end(), lambda_out);
+        CK(cudaMemcpyAsync(A_out, fac[0], nk * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(B_out, fac[1], nk * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(C_out, fac[2], nk * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->sync();
+        if (iters_out) *iters_out = it;
     });
 }
 

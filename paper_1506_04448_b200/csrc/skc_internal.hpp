@@ -117,6 +117,7 @@ void launch_m2_apply(cudaStream_t st, int V, long long D, int p, const long long
                      const double* s2, const double* diag, const double* m1p, double inv_used1, double inv_used2,
                      double a, const double* X, double* Z, double* mx, double* Y);
 void launch_scale_cols(cudaStream_t st, long long rows, int k, const double* in, const double* f, double* out);
+void launch_normalize_columns(cudaStream_t st, int n, int k, double* F, const double* prev, double* lambda);
 
 // residue twiddle tables of a symmetric set (SymView::stw*/gtw*)
 void launch_sym_twiddle_tables(cudaStream_t st, const SymView& v, double2* stw1, double2* stw2, double2* gtw1,

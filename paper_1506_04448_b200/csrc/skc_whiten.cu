@@ -145,6 +145,36 @@ __global__ void k_scale_cols(long long rows, int k, const double* __restrict__ i
     out[i] = in[i] * f[i % k];
 }
 
+// ALS normalize_columns (decompose.cpp:145-155) on a column-major n x k factor: lambda[r]
+// = ||col r|| (fixed-order block reduction); col /= norm, or the previous column when the
+// norm is zero.
+__global__ void k_normalize_columns(int n, double* __restrict__ F, const double* __restrict__ prev,
+                                    double* __restrict__ lambda) {
+    __shared__ double red[8];
+    const int r = blockIdx.x;
+    double* col = F + (size_t)r * n;
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < n; i += 256) acc += col[i] * col[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    __shared__ double nrm_s;
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int i = 0; i < 8; ++i) s += red[i];
+        nrm_s = sqrt(s);
+        lambda[r] = nrm_s;
+    }
+    __syncthreads();
+    const double nrm = nrm_s;
+    for (int i = threadIdx.x; i < n; i += 256) col[i] = nrm > 0 ? col[i] / nrm : prev[(size_t)r * n + i];
+}
+void launch_normalize_columns(cudaStream_t st, int n, int k, double* F, const double* prev, double* lambda) {
+    k_normalize_columns<<<k, 256, 0, st>>>(n, F, prev, lambda);
+    count_launch();
+}
+
 void launch_corpus_prep(cudaStream_t st, int V, long long D, const long long* doc_ptr, const int* count,
                         const long long* cptr, const long long* cdoc, const int* ccount, long long* total, double* s2,
                         double* invm, double* diag, double* m1p) {

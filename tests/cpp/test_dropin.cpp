@@ -306,6 +306,49 @@ TEST_CASE("lda moments, whitening, recovery", lda_whitening_pipeline) {
     CHECK(std::abs(y[0] - 1.0 / 3.0) < 1e-15);
 }
 
+TEST_CASE("fast ALS on the asymmetric set (decompose.cpp:117-205)", als_fast_case) {
+    const int n = 16, k = 2;
+    Rng rng(5);
+    std::vector<double> a(n * k), b(n * k), c(n * k);
+    for (auto* f : {&a, &b, &c})
+        for (int r = 0; r < k; ++r) {
+            auto u = rng.unit_sphere(n);
+            for (int i = 0; i < n; ++i) (*f)[r * n + i] = u[i];
+        }
+    DenseTensor3 T(n);
+    const double lam[2] = {3.0, 1.0};
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j)
+            for (int q = 0; q < n; ++q) {
+                double v = 0.0;
+                for (int r = 0; r < k; ++r) v += lam[r] * a[r * n + i] * b[r * n + j] * c[r * n + q];
+                T.at(i, j, q) = v;
+            }
+    AsymTensorSketchSet s(n, 4096, 20, 3);
+    s.accumulate_dense(T);
+    AlsConfig cfg;
+    cfg.k = k;
+    cfg.max_iters = 200;
+    cfg.tol = 1e-9;
+    cfg.seed = 2;
+    const CpDecomposition d = als_fast(s, cfg);
+    CHECK(d.rank() == k);
+    double best0 = 0.0;
+    for (int r = 0; r < k; ++r) {
+        double dot = 0.0;
+        for (int i = 0; i < n; ++i) dot += d.A(i, r) * a[i];
+        best0 = std::max(best0, std::abs(dot));
+    }
+    CHECK(best0 > 0.99);
+    AlsConfig bad = cfg;
+    bad.k = n + 1;
+    CHECK_THROWS_AS(als_fast(s, bad), std::invalid_argument);
+    Eigen::MatrixXd G = Eigen::MatrixXd::Identity(3, 3);
+    for (int i = 0; i < 3; ++i) G(i, i) = 2.0;
+    const Eigen::MatrixXd P = pinv_spectral(G);
+    CHECK(std::abs(P(1, 1) - 0.5) < 1e-15 && std::abs(P(0, 1)) < 1e-15);
+}
+
 int main() {
     for (auto& [name, fn] : registry()) {
         try {

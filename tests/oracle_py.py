@@ -89,6 +89,8 @@ def _setup(L):
         "orc_contract_Ivv_exact": (None, [d_p, C.c_int, d_p, d_p, d_p]),
         "orc_first_asymmetric_triple": (C.c_int, [d_p, C.c_int, C.c_double, i_p]),
         "orc_greedy_match": (C.c_int, [d_p, C.c_int, d_p, C.c_int, C.c_int, d_p]),
+        "orc_asym_als": (C.c_int, [vp, C.c_int, C.c_int, C.c_double, C.c_uint64, d_p, d_p, d_p, d_p, i_p]),
+        "orc_pinv_spectral": (C.c_int, [C.c_int, d_p, d_p]),
         "orc_lda_compute_m1": (C.c_int, [C.c_int, C.c_int, ll_p, i_p, i_p, d_p]),
         "orc_lda_compute_m2": (C.c_int, [C.c_int, C.c_int, ll_p, i_p, i_p, C.c_double, d_p]),
         "orc_sym_eigen": (C.c_int, [C.c_int, d_p, d_p, d_p]),
@@ -333,6 +335,24 @@ def contract_Ivv_exact(T, u, v):
     out = np.empty(T.shape[0])
     lib().orc_contract_Ivv_exact(dp(T), T.shape[0], dp(f64(u)), dp(f64(v)), dp(out))
     return out
+
+
+def asym_als(aset, k, max_iters=1000, tol=1e-6, seed=0):
+    """decompose.cpp:117-205 als_fast on an oracle AsymSet -> (lambda, A, B, C, iters); factors n x k."""
+    n = aset.n
+    lam = np.zeros(k)
+    A, B, Cm = (np.zeros((k, n)) for _ in range(3))  # column-major n x k == k x n row-major
+    it = C.c_int()
+    _chk(lib().orc_asym_als(aset.h, k, max_iters, tol, seed, dp(lam), dp(A), dp(B), dp(Cm), C.byref(it)))
+    return lam, A.T.copy(), B.T.copy(), Cm.T.copy(), it.value
+
+
+def pinv_spectral(G):
+    G = f64(G)
+    k = G.shape[0]
+    P = np.zeros((k, k))
+    _chk(lib().orc_pinv_spectral(k, dp(G), dp(P)))
+    return P
 
 
 def _corpus(doc_ptr, word, count):

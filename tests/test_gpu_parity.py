@@ -426,6 +426,47 @@ def test_lda_rejects_short_corpus(gpu_ctx):
         s.sketch_whitened_m3(5, [0, 1, 2], [0, 1], [1, 2], np.ones((5, 4)), 1.0)
 
 
+# ---------------------------------------------------------------- fast ALS on the asym set (§8f rank 3)
+def _planted_asym(n, k, seed):
+    rng = np.random.default_rng(seed)
+    lam = np.linspace(3.0, 1.5, k)
+    A, B, Cf = (np.linalg.qr(rng.normal(size=(n, k)))[0] for _ in range(3))
+    T = np.einsum("r,ir,jr,kr->ijk", lam, A, B, Cf)
+    return T, lam, A, B, Cf
+
+
+@pytest.mark.parametrize("max_iters", [1, 25])
+def test_asym_als_matches_oracle(gpu_ctx, max_iters):
+    """als_fast (decompose.cpp:117-205): same init stream, same sketched mode contractions,
+    same pseudoinverse update -> the GPU factors follow the oracle's trajectory."""
+    n, k, b, B = 24, 3, 1024, 10
+    T, lam, A, Bf, Cf = _planted_asym(n, k, 5)
+    s = skb().AsymTensorSketchSet(n, b, B, 17, gpu_ctx)
+    o = O.AsymSet(n, b, B, 17)
+    s.accumulate_dense(T)
+    o.accumulate_dense(T)
+    d = skb().als_fast(s, skb().AlsConfig(k=k, max_iters=max_iters, tol=1e-6, seed=9))
+    lo, Ao, Bo, Co, ito = O.asym_als(o, k, max_iters, 1e-6, 9)
+    assert d.iters == ito
+    assert np.max(np.abs(d.lambda_ - lo) / np.abs(lo)) <= 1e-7
+    for X, Y in ((d.A, Ao), (d.B, Bo), (d.C, Co)):
+        assert np.max(np.abs(X - Y)) <= 1e-7
+
+
+def test_asym_als_recovers_planted_components(gpu_ctx):
+    n, k = 30, 3
+    T, lam, A, Bf, Cf = _planted_asym(n, k, 8)
+    s = skb().AsymTensorSketchSet(n, 4096, 20, 3, gpu_ctx)
+    s.accumulate_dense(T)
+    d = skb().als_fast(s, skb().AlsConfig(k=k, max_iters=200, tol=1e-8, seed=1))
+    m = O.greedy_match(d.A, A)
+    assert np.all(m[:, 2] > 0.99)
+    with pytest.raises(ValueError, match="als: target rank exceeds tensor dimension"):
+        skb().als_fast(s, skb().AlsConfig(k=n + 1))
+    with pytest.raises(ValueError, match="als: k and max_iters must be positive"):
+        skb().als_fast(s, skb().AlsConfig(k=2, max_iters=0))
+
+
 # ---------------------------------------------------------------- LDA moments / whitening (§8f rank 1)
 def _align_cols(A, ref):
     """Flip column signs of A to match ref (eigenvector signs are unpinned, lda.cpp:128)."""

@@ -366,3 +366,15 @@ def test_oracle_m2_and_whiten_match_numpy_restatement():
 def test_oracle_whiten_rejects_bad_rank():
     with pytest.raises(O.OracleError, match="whiten: invalid target rank"):
         O.lda_whiten(np.eye(4), 5)
+
+
+# ---- decompose.cpp:44-51 pinv_spectral (ALS update) pinned to numpy ---------------------
+def test_oracle_pinv_spectral_matches_numpy():
+    rng = np.random.default_rng(2)
+    X = rng.normal(size=(6, 4))
+    G = X @ X.T  # rank 4 PSD 6 x 6: truncation must drop the null space
+    P = O.pinv_spectral(G)
+    assert np.max(np.abs(P - np.linalg.pinv(G, rcond=1e-10, hermitian=True))) <= 1e-9 * np.max(np.abs(P))
+    H = rng.normal(size=(5, 5))
+    H = H @ H.T + 5 * np.eye(5)
+    assert np.max(np.abs(O.pinv_spectral(H) - np.linalg.inv(H))) <= 1e-13
