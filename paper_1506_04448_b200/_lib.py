@@ -11,7 +11,9 @@ import os
 import pathlib
 
 _HERE = pathlib.Path(__file__).resolve().parent
-LIB_PATH = _HERE / "_lib" / "libsketchcp_b200.so"
+# SKC_LIB_DIR: alternate build directory (instrumented experiment builds); default _lib/
+LIB_PATH = pathlib.Path(os.environ["SKC_LIB_DIR"]) / "libsketchcp_b200.so" if os.environ.get("SKC_LIB_DIR") \
+    else _HERE / "_lib" / "libsketchcp_b200.so"
 
 if not LIB_PATH.exists():
     raise ImportError(

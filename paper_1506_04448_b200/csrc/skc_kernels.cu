@@ -287,8 +287,14 @@ __global__ void k_sym_twiddle_tables(SymView v, double2* __restrict__ stw1, doub
     const size_t mq = (size_t)m * v.n + q;
     stw1[idx] = conj(v.tw[(ur * (v.plan1[mq].y & 0x0FFFFFFFu)) & bmask]);
     stw2[idx] = conj(v.tw[(ur * (v.plan2[mq].y & 0x0FFFFFFFu)) & bmask]);
-    gtw1[idx] = v.tw[(ur * v.bucket1[mq]) & bmask];
-    gtw2[idx] = v.tw[(ur * v.bucket2[mq]) & bmask];
+    // gather weights with the sign rotation and the 1/(6b), 1/(3b) scalings folded in
+    // (contraction.cpp:170-175): Re(z1 conj(sigma)) / (6b) = Re(A[h] * gtw1) etc.
+    const unsigned e = v.sexp[mq];
+    const double inv_b = 1.0 / static_cast<double>(v.b);
+    const double2 r1 = root4_times((4u - (e & 3u)) & 3u, inv_b / 6.0);
+    const double2 r2 = root4_times((4u - ((2u * e) & 3u)) & 3u, inv_b / 3.0);
+    gtw1[idx] = cmul(v.tw[(ur * v.bucket1[mq]) & bmask], r1);
+    gtw2[idx] = cmul(v.tw[(ur * v.bucket2[mq]) & bmask], r2);
 }
 void launch_sym_twiddle_tables(cudaStream_t st, const SymView& v, double2* stw1, double2* stw2, double2* gtw1,
                                double2* gtw2) {
@@ -497,6 +503,9 @@ struct DitPair<LOGN, LR, -1, NPA, NPB> {
     __device__ __forceinline__ static void run(double2*, double2*, const double2*) {}
 };
 
+#ifdef SKC_TRACE_CONTRACT
+__device__ unsigned long long g_contract_phase[8];
+#endif
 template <int LOGN, int NT>
 __device__ __forceinline__ void sym_contract_half_body(const SymView& v, const double* __restrict__ U, int L, int mode,
                                                        double* __restrict__ out) {
@@ -511,9 +520,14 @@ __device__ __forceinline__ void sym_contract_half_body(const SymView& v, const d
     const int l0 = (blockIdx.x / (S * B)) * kLPB;
     double2* A = sm;
     double2* Bh = sm + strideA;
-    double2* scr = Bh + strideB;                                           // 2n
-    std::uint32_t* keys = reinterpret_cast<std::uint32_t*>(scr + 2 * n);  // 2n
-    double* us = reinterpret_cast<double*>(keys + 2 * n);  // n (2n u32 keep 8-byte alignment)
+    // restart-invariant scatter metadata of this (m, r), built once per CTA: the complex
+    // weight root4(e) conj(w_b^{r t}), the local key (f2: halved) and the index i of each
+    // plan entry. Per restart only u (staged in us) changes, so a run head sums
+    // wv[q] * u[idx[q]] (f2: u^2) over its run straight from shared memory.
+    double2* wv = Bh + strideB;                                               // 2n
+    std::uint32_t* keys = reinterpret_cast<std::uint32_t*>(wv + 2 * n);      // 2n
+    std::uint32_t* idx = keys + 2 * n;                                        // 2n
+    double* us = reinterpret_cast<double*>(idx + 2 * n);  // n (4n u32 keep 8-byte alignment)
     const std::uint32_t bmask = v.b - 1;
     const std::uint32_t nmask = static_cast<std::uint32_t>(N - 1);
     const double2* fT = v.spec + ((size_t)m * S + r) * N;
@@ -526,36 +540,55 @@ __device__ __forceinline__ void sym_contract_half_body(const SymView& v, const d
     const double2* dm = v.data + (size_t)m * v.b;
 
     const size_t mr = ((size_t)m * S + r) * n;  // residue-twiddle table offset of (m, r)
+#ifdef SKC_TRACE_CONTRACT
+    unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tp = clock64();
+#define PH(q)                                   \
+    {                                           \
+        const unsigned long long t_ = clock64(); \
+        ph[q] += t_ - tp;                        \
+        tp = t_;                                 \
+    }
+#else
+#define PH(q)
+#endif
     const bool ttab = v.stw1 != nullptr;
+    for (int x = threadIdx.x; x < 2 * n; x += NT) {
+        const bool hb = x >= n;
+        const int q = hb ? x - n : x;
+        const uint2 e = hb ? p2[q] : p1[q];
+        const double2 w = ttab ? (hb ? v.stw2 : v.stw1)[mr + q]
+                               : conj(v.tw[(static_cast<std::uint32_t>(r) * (e.y & 0x0FFFFFFFu)) & bmask]);
+        wv[x] = cmul(root4_times(e.y >> 28, 1.0), w);
+        keys[x] = hb ? ((e.y & nmask) >> 1) : (e.y & nmask);
+        idx[x] = e.x;
+    }
     for (int l = l0; l < min(L, l0 + kLPB); ++l) {
         const double* ug = U + (size_t)l * n;
         for (int x = threadIdx.x; x < n; x += NT) us[x] = ug[x];  // u staged once per restart
         zero_smem(sm, strideA + strideB);
         __syncthreads();
-        // phase 1 of the two-phase scatter (contraction.cpp:150-154): every contribution
-        // val * w_b^{-r t} independently into scratch, keys = local position (f2: halved)
-        for (int x = threadIdx.x; x < 2 * n; x += NT) {
-            const bool hb = x >= n;
-            const int q = hb ? x - n : x;
-            const uint2 e = hb ? p2[q] : p1[q];
-            const double ui = us[e.x];
-            const double2 val = root4_times(e.y >> 28, hb ? ui * ui : ui);
-            const double2 w = ttab ? (hb ? v.stw2 : v.stw1)[mr + q]
-                                   : conj(v.tw[(static_cast<std::uint32_t>(r) * (e.y & 0x0FFFFFFFu)) & bmask]);
-            scr[x] = cmul(val, w);
-            keys[x] = hb ? ((e.y & nmask) >> 1) : (e.y & nmask);
-        }
-        __syncthreads();
+        PH(0)
+        // deterministic scatter (contraction.cpp:150-154): the head of each run of equal
+        // keys sums its run in plan order; f1 values u_i, f2 values u_i^2
         for (int x = threadIdx.x; x < 2 * n; x += NT) {
             const int lo = (x >= n) ? n : 0;
             const std::uint32_t key = keys[x];
             if (x > lo && keys[x - 1] == key) continue;
-            double2 acc = scr[x];
-            for (int x2 = x + 1; x2 < lo + n && keys[x2] == key; ++x2) acc = cadd(acc, scr[x2]);
-            ((x >= n) ? Bh : A)[pad16(static_cast<int>(key))] = acc;
+            const bool hb = x >= n;
+            double2 acc = mk(0.0, 0.0);
+            for (int x2 = x; x2 < lo + n && keys[x2] == key; ++x2) {
+                const double ui = us[idx[x2]];
+                const double2 w = wv[x2];
+                const double val = hb ? ui * ui : ui;
+                acc = cadd(acc, mk(w.x * val, w.y * val));
+            }
+            (hb ? Bh : A)[pad16(static_cast<int>(key))] = acc;
         }
         __syncthreads();
+        PH(1)
+        PH(2)
         DifPair<LOGN, 4, 0>::run(A, Bh, v.twl);
+        PH(3)
 
         if (mode == 0) {
             // z1 = fT conj(f1^2 + f2) (full), Z2 = fT conj(f1) folded to N/2 (contraction.cpp:158-162)
@@ -569,20 +602,28 @@ __device__ __forceinline__ void sym_contract_half_body(const SymView& v, const d
                 Bh[pad16(q)] = cadd(cmulc(t0, u0), cmulc(t1, u1));
             }
             __syncthreads();
+            PH(4)
             DitPair<LOGN, 4, plan_npass(LOGN, 4) - 1>::run(A, Bh, v.twl);
+            PH(5)
             const double inv_b = 1.0 / static_cast<double>(v.b);
             double* o = out + (((size_t)l * B + m) * S + r) * n;
             for (int i = threadIdx.x; i < n; i += NT) {
-                const unsigned e = se[i];
                 const double ui = us[i];
                 const std::uint32_t t1 = b1[i], t2 = b2[i];
-                const double2 w1 = ttab ? v.gtw1[mr + i] : v.tw[(static_cast<std::uint32_t>(r) * t1) & bmask];
-                const double2 w2 = ttab ? v.gtw2[mr + i] : v.tw[(static_cast<std::uint32_t>(r) * t2) & bmask];
-                const double2 z1 = cmul(A[pad16(static_cast<int>(t1 & nmask))], w1);
-                const double2 z2 = cmul(Bh[pad16(static_cast<int>((t2 & nmask) >> 1))], w2);
-                double val = re_rot_conj(e, z1) * (1.0 / 6.0) * inv_b;
-                val += ui * re_rot_conj(2u * e, z2) * (1.0 / 3.0) * inv_b;
-                if (r == 0) val += ui * ui * re_rot_conj(3u * e, dm[b3[i]]) * (1.0 / 3.0);
+                const double2 a1 = A[pad16(static_cast<int>(t1 & nmask))];
+                const double2 a2 = Bh[pad16(static_cast<int>((t2 & nmask) >> 1))];
+                double val;
+                if (ttab) {  // folded gather weights (k_sym_twiddle_tables)
+                    const double2 g1 = v.gtw1[mr + i], g2 = v.gtw2[mr + i];
+                    val = (a1.x * g1.x - a1.y * g1.y) + ui * (a2.x * g2.x - a2.y * g2.y);
+                } else {
+                    const unsigned e = se[i];
+                    const double2 z1 = cmul(a1, v.tw[(static_cast<std::uint32_t>(r) * t1) & bmask]);
+                    const double2 z2 = cmul(a2, v.tw[(static_cast<std::uint32_t>(r) * t2) & bmask]);
+                    val = re_rot_conj(e, z1) * (1.0 / 6.0) * inv_b;
+                    val += ui * re_rot_conj(2u * e, z2) * (1.0 / 3.0) * inv_b;
+                }
+                if (r == 0) val += ui * ui * re_rot_conj(3u * se[i], dm[b3[i]]) * (1.0 / 3.0);
                 o[i] = val;
             }
         } else {
@@ -612,7 +653,13 @@ __device__ __forceinline__ void sym_contract_half_body(const SymView& v, const d
             }
         }
         __syncthreads();
+        PH(6)
     }
+#ifdef SKC_TRACE_CONTRACT
+    if (threadIdx.x == 0)
+        for (int q = 0; q < 8; ++q) atomicAdd(&g_contract_phase[q], ph[q]);
+#endif
+#undef PH
 }
 
 template <int LOGN, int NT, int MINB>
@@ -676,7 +723,7 @@ void launch_sym_contract(cudaStream_t st, const SymView& v, const double* U, int
     if (var >= 3) {
         const int NH = v.N / 2;
         const size_t smem = sizeof(double2) * (padded_len(v.N) + (NH + NH / 16 + 1)) +
-                            (sizeof(double2) + sizeof(std::uint32_t)) * 2 * (size_t)v.n +
+                            (sizeof(double2) + 2 * sizeof(std::uint32_t)) * 2 * (size_t)v.n +
                             sizeof(double) * ((size_t)v.n + 1);
         const unsigned grid = (unsigned)((long long)((L + kLPB - 1) / kLPB) * v.B * v.S);
 #define LH_(LG) sym_contract_half_dispatch<LG>(st, v, U, L, mode, out, grid, smem, var)
@@ -1233,3 +1280,15 @@ void launch_gen_planted(cudaStream_t st, int n, int rank, const double* lambda, 
 }
 
 }  // namespace skc
+
+#ifdef SKC_TRACE_CONTRACT
+// experiment build only: per-phase cycle sums of k_sym_contract_half (thread 0 per CTA)
+extern "C" int skc_debug_contract_phases(unsigned long long* out, int reset) {
+    cudaMemcpyFromSymbol(out, skc::g_contract_phase, sizeof(unsigned long long) * 8);
+    if (reset) {
+        unsigned long long z[8] = {};
+        cudaMemcpyToSymbol(skc::g_contract_phase, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
