@@ -37,5 +37,29 @@ def main():
     (HERE / "oracle_golden.json").write_text(json.dumps(out, indent=1))
 
 
+def rtpm_c0():
+    """BASELINE config 0 in full (n=100, rank 10 + 0.01 noise, b=2^12, B=20, RTPM k=10,
+    L=50, T=30) through the oracle: the full-size RTPM parity fixture (rtpm_c0.json).
+    The tensor comes from the repository's host generator (bit-exact, no GPU)."""
+    import os
+
+    sys.path.insert(0, str(HERE.parents[1]))
+    import paper_1506_04448_b200 as skb
+
+    n, rank, b, B, k, L, T = 100, 10, 1 << 12, 20, 10, 50, 30
+    Tt, lam, V = skb.gen_planted_tensor(n, rank, 0.01, 11)
+    O.lib().orc_set_num_threads(os.cpu_count() or 1)
+    o = O.SymSet(n, b, B, 5)
+    o.accumulate_dense(Tt, True)
+    lo, Vo, bto = o.rtpm(k, L, T, seed=3)
+    (HERE / "rtpm_c0.json").write_text(json.dumps({
+        "config": {"n": n, "rank": rank, "sigma": 0.01, "gen_seed": 11, "b": b, "B": B, "set_seed": 5, "k": k, "L": L,
+                   "T": T, "rtpm_seed": 3},
+        "lambda": lo.tolist(), "V": Vo.tolist(), "best_tau": [int(x) for x in bto]}))
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "--rtpm-c0":
+        rtpm_c0()
+    else:
+        main()
