@@ -907,28 +907,74 @@ __global__ void __launch_bounds__(kFftThreads, SKC_FFT_MINB)
     const int ch = blockIdx.x / (S * B);
     double2* A = sm;
     double2* ACC = sm + stride;
-    double2* scr = ACC + N + 8;                                        // n (SCR)
-    std::uint32_t* keys = reinterpret_cast<std::uint32_t*>(scr + n);  // n (SCR)
+    // SCR: the sample-invariant scatter metadata of this (m, r) (weight root4(e)
+    // conj(w_b^{r t}), local key, index i) is built once; per sample a run head sums
+    // wv[q] x[idx[q]] over its run.
+    double2* wv = ACC + N + 8;                                         // n (SCR)
+    std::uint32_t* keys = reinterpret_cast<std::uint32_t*>(wv + n);   // n (SCR)
+    std::uint32_t* idx = keys + n;                                     // n (SCR)
+    double* xs = reinterpret_cast<double*>(idx + n);  // 2 x n (SCR): sample double buffer (2n u32: 8-byte aligned)
     const long long per = (Nsamp + chunks - 1) / chunks;
     const long long s0 = (long long)ch * per, s1 = min(Nsamp, s0 + per);
     const uint2* plan = v.plan1 + (size_t)m * n;
     const std::uint32_t bmask = v.b - 1;
+    const std::uint32_t nmask = static_cast<std::uint32_t>(N - 1);
     zero_smem(ACC, N + 8);
+    zero_smem(A, stride);
+    if (SCR) {
+        const double2* stw = v.stw1 ? v.stw1 + ((size_t)m * S + r) * n : nullptr;
+        for (int q = threadIdx.x; q < n; q += blockDim.x) {
+            const uint2 e = plan[q];
+            const double2 w = stw ? stw[q] : conj(v.tw[(static_cast<std::uint32_t>(r) * (e.y & 0x0FFFFFFFu)) & bmask]);
+            wv[q] = cmul(root4_times(e.y >> 28, 1.0), w);
+            keys[q] = e.y & nmask;
+            idx[q] = e.x;
+        }
+    }
+    // the next sample's row is copied into the other half of xs (cp.async) while the
+    // current one is transformed
+    auto prefetch = [&](long long smp) {
+        if (!SCR || smp >= s1) return;
+        const double* src = X + (size_t)smp * n;
+        double* dst = xs + (size_t)(smp & 1) * n;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const std::uint32_t da = static_cast<std::uint32_t>(__cvta_generic_to_shared(dst + i));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(da), "l"(src + i) : "memory");
+        }
+    };
+    prefetch(s0);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    __syncthreads();
     for (long long s = s0; s < s1; ++s) {
         const double* x = X + (size_t)s * n;
-        zero_smem(A, stride);
+        prefetch(s + 1);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");  // this sample's row has landed
         __syncthreads();
-        auto vx = [&](std::uint32_t i, std::uint32_t y) { return root4_times(y >> 28, x[i]); };
-        if (SCR)
-            scatter2(A, plan, vx, static_cast<double2*>(nullptr), plan, vx, n, N, r, bmask, 0x0FFFFFFFu, v.tw, scr, keys,
-                     v.stw1 ? v.stw1 + ((size_t)m * S + r) * n : nullptr);
-        else
+        // A is all-zero here (initially, then re-zeroed by the accumulate pass below)
+        if (SCR) {
+            const double* xr = xs + (size_t)(s & 1) * n;
+            for (int q = threadIdx.x; q < n; q += blockDim.x) {
+                const std::uint32_t key = keys[q];
+                if (q > 0 && keys[q - 1] == key) continue;
+                double2 a = mk(0.0, 0.0);
+                for (int q2 = q; q2 < n && keys[q2] == key; ++q2) {
+                    const double xi = xr[idx[q2]];
+                    const double2 wq = wv[q2];
+                    a = cadd(a, mk(wq.x * xi, wq.y * xi));
+                }
+                A[pad16(static_cast<int>(key))] = a;
+            }
+        } else {
+            auto vx = [&](std::uint32_t i, std::uint32_t y) { return root4_times(y >> 28, x[i]); };
             scatter_plan(A, plan, n, N, r, bmask, 0x0FFFFFFFu, v.tw, vx);
+        }
         __syncthreads();
         dif_local<LOGN>(A, 1, v.twl);
         const double ws = (w ? w[s] : 1.0) * wscale;
         for (int j = threadIdx.x; j < N; j += blockDim.x) {
             const double2 z = A[pad16(j)];
+            A[pad16(j)] = mk(0.0, 0.0);  // ready for the next sample's scatter
             const double2 z3 = cmul(cmul(z, z), z);
             ACC[j] = cadd(ACC[j], cscale(z3, ws));
         }
@@ -941,7 +987,7 @@ void launch_sym_moment_accumulate(cudaStream_t st, const SymView& v, const doubl
                                   long long Nsamp, int chunks, double* acc) {
     const bool scr = v.n <= kScatterMax;
     const size_t smem = sizeof(double2) * (padded_len(v.N) + v.N + 8) +
-                        (scr ? (sizeof(double2) + sizeof(std::uint32_t)) * (size_t)v.n : 0);
+                        (scr ? (sizeof(double2) + 2 * sizeof(std::uint32_t) + 2 * sizeof(double)) * (size_t)v.n + 8 : 0);
     const unsigned grid = (unsigned)((long long)chunks * v.B * v.S);
 #define L_(LG)                                                                                                     \
     {                                                                                                              \
