@@ -1400,6 +1400,7 @@ int skc_sym_sketch_whitened_m3(skc_sym_set* s, int V, long long D, const long lo
         // host: document totals, StreamStats and the word-major transpose (docs ascending)
         long long used = 0, skipped = 0, used1 = 0;
         std::vector<long long> cptr(static_cast<size_t>(V) + 1, 0);
+        std::vector<long long> used_docs;
         for (long long d = 0; d < D; ++d) {
             long long tot = 0;
             for (long long q = doc_ptr[d]; q < doc_ptr[d + 1]; ++q) {
@@ -1407,7 +1408,12 @@ int skc_sym_sketch_whitened_m3(skc_sym_set* s, int V, long long D, const long lo
                 tot += count[q];
                 cptr[static_cast<size_t>(word[q]) + 1]++;
             }
-            if (tot < 3) ++skipped; else ++used;   // lda.cpp:164-168
+            if (tot < 3) {  // lda.cpp:164-168
+                ++skipped;
+            } else {
+                ++used;
+                used_docs.push_back(d);
+            }
             if (tot >= 1) ++used1;                 // lda.cpp:93-96
         }
         if (used == 0) fail(kNumericalError, "sketch_whitened_m3: no documents with >= 3 words");  // lda.cpp:186
@@ -1456,20 +1462,25 @@ int skc_sym_sketch_whitened_m3(skc_sym_set* s, int V, long long D, const long lo
         launch_lda_q(st, k, V, d_W.p, d_m1.p, 1.0 / static_cast<double>(used1), d_q.p);
         ctx->check_launch();
         const int per_rep = s->B * s->S;
-        const int chunks = std::max(1, static_cast<int>(std::min<long long>(D + V, (4ll * ctx->sms) / per_rep)));
-        d_acc.alloc(static_cast<size_t>(chunks) * per_rep * s->N * 2);
-        d_cross.alloc(static_cast<size_t>(chunks) * per_rep * s->N * 2);
+        // ~4 waves of 2 resident CTAs per SM for each of the two item kinds
+        const int chunks_d = std::max(1, static_cast<int>(std::min<long long>(used, (8ll * ctx->sms) / per_rep)));
+        const int chunks_v = std::max(1, static_cast<int>(std::min<long long>(V, (8ll * ctx->sms) / per_rep)));
+        d_acc.alloc(static_cast<size_t>(chunks_d + chunks_v) * per_rep * s->N * 2);
+        d_cross.alloc(static_cast<size_t>(chunks_d) * per_rep * s->N * 2);
+        DevBuf<long long> d_used;
+        d_used.upload(used_docs.data(), used_docs.size(), st);
         SymView v = s->view();
         {
             SKC_PROF(ctx, "lda_accumulate");
-            launch_lda_accumulate(st, v, D, d_P.p, d_s1.p, d_s2.p, V, d_W.p, d_coeff1.p, d_sumwn.p, chunks, d_acc.p,
-                                  d_cross.p);
+            launch_lda_accumulate(st, v, used, d_used.p, d_P.p, d_s1.p, d_s2.p, V, d_W.p, d_coeff1.p, d_sumwn.p,
+                                  chunks_d, chunks_v, d_acc.p, d_cross.p);
         }
         ctx->check_launch();
         ctx->tmp.alloc(static_cast<size_t>(s->B) * s->b);
         const double inv_docs = 1.0 / static_cast<double>(used);
         const double m1_coeff = 2.0 * alpha0 * alpha0 / ((alpha0 + 1.0) * (alpha0 + 2.0));  // lda.cpp:191
-        launch_lda_finish(st, v, d_acc.p, d_cross.p, chunks, d_q.p, inv_docs, m1_coeff, ctx->tmp.p);
+        launch_lda_finish(st, v, d_acc.p, d_cross.p, chunks_d + chunks_v, chunks_d, d_q.p, inv_docs, m1_coeff,
+                          ctx->tmp.p);
         ctx->check_launch();
         launch_combine_residues(st, ctx->tmp.p, s->B, s->S, s->N, s->b, v.tw, 1.0, -1, false, s->data.p);
         ctx->check_launch();

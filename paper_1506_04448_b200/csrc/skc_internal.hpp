@@ -172,11 +172,11 @@ void launch_lda_vocab(cudaStream_t st, int k, int V, const long long* cptr, cons
                       double* m1_partial);
 void launch_lda_q(cudaStream_t st, int k, int V, const double* W, const double* m1_partial, double inv_used1,
                   double* q);
-void launch_lda_accumulate(cudaStream_t st, const SymView& v, long long Dn, const double* P, const double* s1,
-                           const double* s2, int V, const double* W, const double* coeff1, const double* sumwn,
-                           int chunks, double* acc, double* cross);
-void launch_lda_finish(cudaStream_t st, const SymView& v, const double* acc, const double* cross, int chunks,
-                       const double* q, double inv_docs, double m1_coeff, double2* tmp);
+void launch_lda_accumulate(cudaStream_t st, const SymView& v, long long Du, const long long* used_docs, const double* P,
+                           const double* s1, const double* s2, int V, const double* W, const double* coeff1,
+                           const double* sumwn, int chunks_d, int chunks_v, double* acc, double* cross);
+void launch_lda_finish(cudaStream_t st, const SymView& v, const double* acc, const double* cross, int chunks_acc,
+                       int chunks_cross, const double* q, double inv_docs, double m1_coeff, double2* tmp);
 
 // generators
 void launch_gen_planted(cudaStream_t st, int n, int rank, const double* lambda, const double* V, double sigma,

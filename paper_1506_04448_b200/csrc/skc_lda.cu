@@ -143,14 +143,110 @@ __global__ void k_lda_q(int k, int V, const double* __restrict__ W, const double
 }
 
 // ---- frequency-domain accumulation: CTA per (chunk, m, r) -----------------------------
-// items [0, Dn) are documents (P rows with weights s1, s2), items [Dn, Dn + V) are
-// vocabulary words (W rows with coeff1 and sumwn rows).
+// Two kernels, two resident CTAs per SM each:
+//   documents (used ones only, via the host-built index list): ACC += s1 F(p)^3,
+//                                                               CR  += s2 F(p)^2
+//   vocabulary words: ACC += F(w)^2 (coeff1 F(w) - 3 F(sumwn))
+// The item-invariant scatter metadata of (m, r) (weight, local key, index) is built once
+// per CTA; item rows are double-buffered into shared memory with cp.async; the local
+// arrays are re-zeroed by the accumulate pass, so each item costs one barrier before and
+// one after its transform.
+struct ScatterMeta {
+    double2* wv;
+    std::uint32_t* keys;
+    std::uint32_t* idx;
+};
+__device__ __forceinline__ void build_meta(const ScatterMeta& mt, const uint2* __restrict__ plan,
+                                           const double2* __restrict__ stw, const double2* __restrict__ tw, int n, int N,
+                                           int r, std::uint32_t bmask) {
+    const std::uint32_t nmask = static_cast<std::uint32_t>(N - 1);
+    for (int q = threadIdx.x; q < n; q += blockDim.x) {
+        const uint2 e = plan[q];
+        const double2 w = stw ? stw[q] : conj(tw[(static_cast<std::uint32_t>(r) * (e.y & 0x0FFFFFFFu)) & bmask]);
+        mt.wv[q] = cmul(root4_times(e.y >> 28, 1.0), w);
+        mt.keys[q] = e.y & nmask;
+        mt.idx[q] = e.x;
+    }
+}
+// run heads sum wv[q] val[idx[q]] in plan order (deterministic) into y (all-zero before)
+__device__ __forceinline__ void scatter_meta(double2* y, const ScatterMeta& mt, const double* val, int n) {
+    for (int q = threadIdx.x; q < n; q += blockDim.x) {
+        const std::uint32_t key = mt.keys[q];
+        if (q > 0 && mt.keys[q - 1] == key) continue;
+        double2 a = mk(0.0, 0.0);
+        for (int q2 = q; q2 < n && mt.keys[q2] == key; ++q2) {
+            const double x = val[mt.idx[q2]];
+            const double2 w = mt.wv[q2];
+            a = cadd(a, mk(w.x * x, w.y * x));
+        }
+        y[pad16(static_cast<int>(key))] = a;
+    }
+}
+__device__ __forceinline__ void async_row(double* dst, const double* src, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const std::uint32_t da = static_cast<std::uint32_t>(__cvta_generic_to_shared(dst + i));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(da), "l"(src + i) : "memory");
+    }
+}
+
 template <int LOGN>
-__global__ void __launch_bounds__(kThreads, 1)
-    k_lda_accumulate(SymView v, long long Dn, const double* __restrict__ P, const double* __restrict__ s1,
-                     const double* __restrict__ s2, int V, const double* __restrict__ W,
-                     const double* __restrict__ coeff1, const double* __restrict__ sumwn, int chunks,
-                     double* __restrict__ acc_out, double* __restrict__ cross_out) {
+__global__ void __launch_bounds__(kThreads, 2)
+    k_lda_acc_docs(SymView v, long long Du, const long long* __restrict__ used_docs, const double* __restrict__ P,
+                   const double* __restrict__ s1, const double* __restrict__ s2, int chunks, double* __restrict__ acc_out,
+                   double* __restrict__ cross_out) {
+    extern __shared__ double2 sm[];
+    constexpr int N = 1 << LOGN;
+    constexpr int stride = N + (N >> 4) + 1;
+    const int S = v.S, n = v.n, B = v.B;
+    const int r = blockIdx.x % S;
+    const int m = (blockIdx.x / S) % B;
+    const int ch = blockIdx.x / (S * B);
+    double2* A = sm;
+    double2* ACC = sm + stride;
+    double2* CR = ACC + N;
+    ScatterMeta mt{CR + N, nullptr, nullptr};
+    mt.keys = reinterpret_cast<std::uint32_t*>(mt.wv + n);
+    mt.idx = mt.keys + n;
+    double* rows = reinterpret_cast<double*>(mt.idx + n);  // 2 x n (2n u32: 8-byte aligned)
+    const long long per = (Du + chunks - 1) / chunks;
+    const long long i0 = (long long)ch * per, i1 = min(Du, i0 + per);
+    zero_sm(A, stride);
+    zero_sm(ACC, 2 * N);
+    build_meta(mt, v.plan1 + (size_t)m * n, v.stw1 ? v.stw1 + ((size_t)m * S + r) * n : nullptr, v.tw, n, N, r,
+               v.b - 1);
+    if (i0 < i1) async_row(rows, P + (size_t)used_docs[i0] * n, n);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    for (long long it = i0; it < i1; ++it) {
+        if (it + 1 < i1) async_row(rows + (size_t)((it + 1 - i0) & 1) * n, P + (size_t)used_docs[it + 1] * n, n);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncthreads();
+        const long long d = used_docs[it];
+        scatter_meta(A, mt, rows + (size_t)((it - i0) & 1) * n, n);
+        __syncthreads();
+        dif_local<LOGN>(A, 1, v.twl);
+        const double a1 = s1[d], a2 = s2[d];
+        for (int j = threadIdx.x; j < N; j += blockDim.x) {
+            const double2 f = A[pad16(j)];
+            A[pad16(j)] = mk(0.0, 0.0);
+            const double2 sq = cmul(f, f);
+            ACC[j] = cadd(ACC[j], cscale(cmul(sq, f), a1));  // lda.cpp:205
+            CR[j] = cadd(CR[j], cscale(sq, a2));              // lda.cpp:206
+        }
+    }
+    __syncthreads();
+    double2* ao = reinterpret_cast<double2*>(acc_out) + (((size_t)ch * B + m) * S + r) * N;
+    double2* co = reinterpret_cast<double2*>(cross_out) + (((size_t)ch * B + m) * S + r) * N;
+    for (int j = threadIdx.x; j < N; j += blockDim.x) {
+        ao[j] = ACC[j];
+        co[j] = CR[j];
+    }
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(kThreads, 2)
+    k_lda_acc_vocab(SymView v, int V, const double* __restrict__ W, const double* __restrict__ coeff1,
+                    const double* __restrict__ sumwn, int chunks, double* __restrict__ acc_out) {
     extern __shared__ double2 sm[];
     constexpr int N = 1 << LOGN;
     constexpr int stride = N + (N >> 4) + 1;
@@ -161,64 +257,52 @@ __global__ void __launch_bounds__(kThreads, 1)
     double2* A = sm;
     double2* Bw = sm + stride;
     double2* ACC = sm + 2 * stride;
-    double2* CR = ACC + N;
-    double2* scr = CR + N;                                                 // 2n
-    std::uint32_t* keys = reinterpret_cast<std::uint32_t*>(scr + 2 * n);  // 2n
-    const uint2* plan = v.plan1 + (size_t)m * n;
-    const double2* stw = v.stw1 ? v.stw1 + ((size_t)m * S + r) * n : nullptr;
-    const std::uint32_t bmask = v.b - 1;
-    const long long items = Dn + V;
-    const long long per = (items + chunks - 1) / chunks;
-    const long long i0 = (long long)ch * per, i1 = min(items, i0 + per);
-    zero_sm(ACC, 2 * N);
-    for (long long it = i0; it < i1; ++it) {
-        const bool doc = it < Dn;
-        if (doc && s1[it] == 0.0 && s2[it] == 0.0) continue;  // skipped document (m < 3)
-        zero_sm(sm, 2 * stride);
+    ScatterMeta mt{ACC + N, nullptr, nullptr};
+    mt.keys = reinterpret_cast<std::uint32_t*>(mt.wv + n);
+    mt.idx = mt.keys + n;
+    double* rows = reinterpret_cast<double*>(mt.idx + n);  // 2 x (W row, sumwn row)
+    const long long per = ((long long)V + chunks - 1) / chunks;
+    const long long i0 = (long long)ch * per, i1 = min((long long)V, i0 + per);
+    zero_sm(A, 2 * stride);
+    zero_sm(ACC, N);
+    build_meta(mt, v.plan1 + (size_t)m * n, v.stw1 ? v.stw1 + ((size_t)m * S + r) * n : nullptr, v.tw, n, N, r,
+               v.b - 1);
+    auto fetch = [&](long long w, int buf) {
+        async_row(rows + (size_t)buf * 2 * n, W + (size_t)w * n, n);
+        async_row(rows + (size_t)buf * 2 * n + n, sumwn + (size_t)w * n, n);
+    };
+    if (i0 < i1) fetch(i0, 0);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    for (long long w = i0; w < i1; ++w) {
+        if (w + 1 < i1) fetch(w + 1, static_cast<int>((w + 1 - i0) & 1));
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
         __syncthreads();
-        if (doc) {
-            const double* p = P + (size_t)it * n;
-            scatter_dense(A, plan, n, N, r, bmask, v.tw, [&](std::uint32_t i) { return p[i]; }, scr, keys, stw);
-        } else {
-            const long long w = it - Dn;
-            const double* wr = W + (size_t)w * n;
-            const double* sr = sumwn + (size_t)w * n;
-            scatter_dense2(A, [&](std::uint32_t i) { return wr[i]; }, Bw, [&](std::uint32_t i) { return sr[i]; }, plan, n, N,
-                           r, bmask, v.tw, scr, keys, stw);
+        const double* row = rows + (size_t)((w - i0) & 1) * 2 * n;
+        scatter_meta(A, mt, row, n);
+        scatter_meta(Bw, mt, row + n, n);
+        __syncthreads();
+        dif_local<LOGN>(sm, 2, v.twl);
+        const double c1 = coeff1[w];
+        for (int j = threadIdx.x; j < N; j += blockDim.x) {
+            const double2 fw = A[pad16(j)], fs = Bw[pad16(j)];
+            A[pad16(j)] = mk(0.0, 0.0);
+            Bw[pad16(j)] = mk(0.0, 0.0);
+            const double2 w2 = cmul(fw, fw);
+            ACC[j] = cadd(ACC[j], cmul(w2, csub(cscale(fw, c1), cscale(fs, 3.0))));  // lda.cpp:216-217
         }
-        __syncthreads();
-        dif_local<LOGN>(sm, doc ? 1 : 2, v.twl);
-        if (doc) {
-            const double a1 = s1[it], a2 = s2[it];
-            for (int j = threadIdx.x; j < N; j += blockDim.x) {
-                const double2 f = A[pad16(j)];
-                const double2 sq = cmul(f, f);
-                ACC[j] = cadd(ACC[j], cscale(cmul(sq, f), a1));  // lda.cpp:205
-                CR[j] = cadd(CR[j], cscale(sq, a2));              // lda.cpp:206
-            }
-        } else {
-            const double c1 = coeff1[it - Dn];
-            for (int j = threadIdx.x; j < N; j += blockDim.x) {
-                const double2 fw = A[pad16(j)];
-                const double2 w2 = cmul(fw, fw);
-                ACC[j] = cadd(ACC[j], cmul(w2, csub(cscale(fw, c1), cscale(Bw[pad16(j)], 3.0))));  // lda.cpp:216-217
-            }
-        }
-        __syncthreads();
     }
+    __syncthreads();
     double2* ao = reinterpret_cast<double2*>(acc_out) + (((size_t)ch * B + m) * S + r) * N;
-    double2* co = reinterpret_cast<double2*>(cross_out) + (((size_t)ch * B + m) * S + r) * N;
-    for (int j = threadIdx.x; j < N; j += blockDim.x) {
-        ao[j] = ACC[j];
-        co[j] = CR[j];
-    }
+    for (int j = threadIdx.x; j < N; j += blockDim.x) ao[j] = ACC[j];
 }
 
 // acc = (sum acc - 3 sum cross F(q)) / D + c_m1 F(q)^3 (lda.cpp:211, 220-221), inverse DIT.
 template <int LOGN>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_lda_finish(SymView v, const double* __restrict__ acc_in, const double* __restrict__ cross_in, int chunks,
-                 const double* __restrict__ q, double inv_docs, double m1_coeff, double2* __restrict__ tmp) {
+    k_lda_finish(SymView v, const double* __restrict__ acc_in, const double* __restrict__ cross_in, int chunks_acc,
+                 int chunks_cross, const double* __restrict__ q, double inv_docs, double m1_coeff,
+                 double2* __restrict__ tmp) {
     extern __shared__ double2 sm[];
     constexpr int N = 1 << LOGN;
     const int S = v.S, n = v.n, B = v.B;
@@ -235,11 +319,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const double2* ci = reinterpret_cast<const double2*>(cross_in);
     for (int j = threadIdx.x; j < N; j += blockDim.x) {
         double2 a = mk(0.0, 0.0), c = mk(0.0, 0.0);
-        for (int h = 0; h < chunks; ++h) {
-            const size_t off = (((size_t)h * B + m) * S + r) * N + j;
-            a = cadd(a, ai[off]);
-            c = cadd(c, ci[off]);
-        }
+        for (int h = 0; h < chunks_acc; ++h) a = cadd(a, ai[(((size_t)h * B + m) * S + r) * N + j]);
+        for (int h = 0; h < chunks_cross; ++h) c = cadd(c, ci[(((size_t)h * B + m) * S + r) * N + j]);
         const double2 fq = sm[pad16(j)];
         a = csub(a, cscale(cmul(c, fq), 3.0));
         sm[pad16(j)] = cadd(cscale(a, inv_docs), cscale(cmul(cmul(fq, fq), fq), m1_coeff));
@@ -285,28 +366,37 @@ void launch_lda_q(cudaStream_t st, int k, int V, const double* W, const double* 
         default: break;            \
     }
 
-void launch_lda_accumulate(cudaStream_t st, const SymView& v, long long Dn, const double* P, const double* s1,
-                           const double* s2, int V, const double* W, const double* coeff1, const double* sumwn,
-                           int chunks, double* acc, double* cross) {
-    const size_t smem = sizeof(double2) * (2 * padded_len(v.N) + 2 * v.N) + (sizeof(double2) + 4) * 2 * (size_t)v.n;
-    const unsigned grid = (unsigned)((long long)chunks * v.B * v.S);
-#define L_(LG)                                                                                                    \
-    {                                                                                                             \
-        cudaFuncSetAttribute(k_lda_accumulate<LG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
-        k_lda_accumulate<LG><<<grid, kThreads, smem, st>>>(v, Dn, P, s1, s2, V, W, coeff1, sumwn, chunks, acc, cross); \
+// acc: (chunks_d + chunks_v) partial spectra (documents first), cross: chunks_d.
+void launch_lda_accumulate(cudaStream_t st, const SymView& v, long long Du, const long long* used_docs, const double* P,
+                           const double* s1, const double* s2, int V, const double* W, const double* coeff1,
+                           const double* sumwn, int chunks_d, int chunks_v, double* acc, double* cross) {
+    const size_t meta = (sizeof(double2) + 2 * sizeof(std::uint32_t)) * (size_t)v.n;
+    const size_t smem_d = sizeof(double2) * (padded_len(v.N) + 2 * v.N) + meta + 2 * sizeof(double) * (size_t)v.n;
+    const size_t smem_v = sizeof(double2) * (2 * padded_len(v.N) + v.N) + meta + 4 * sizeof(double) * (size_t)v.n;
+    const unsigned grid_d = (unsigned)((long long)chunks_d * v.B * v.S);
+    const unsigned grid_v = (unsigned)((long long)chunks_v * v.B * v.S);
+    double* acc_v = acc + (size_t)chunks_d * v.B * v.S * v.N * 2;
+#define L_(LG)                                                                                                      \
+    {                                                                                                               \
+        cudaFuncSetAttribute(k_lda_acc_docs<LG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_d);         \
+        cudaFuncSetAttribute(k_lda_acc_vocab<LG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_v);        \
+        if (Du > 0) k_lda_acc_docs<LG><<<grid_d, kThreads, smem_d, st>>>(v, Du, used_docs, P, s1, s2, chunks_d, acc, cross); \
+        if (V > 0) k_lda_acc_vocab<LG><<<grid_v, kThreads, smem_v, st>>>(v, V, W, coeff1, sumwn, chunks_v, acc_v);          \
     }
     SKC_LOGN_SWITCH_L(v.logN, L_)
 #undef L_
     count_launch();
-    count_transforms((std::uint64_t)(Dn + 2ll * V) * v.B * v.S, v.S);
+    count_launch();
+    count_transforms((std::uint64_t)(Du + 2ll * V) * v.B * v.S, v.S);
 }
-void launch_lda_finish(cudaStream_t st, const SymView& v, const double* acc, const double* cross, int chunks,
-                       const double* q, double inv_docs, double m1_coeff, double2* tmp) {
+void launch_lda_finish(cudaStream_t st, const SymView& v, const double* acc, const double* cross, int chunks_acc,
+                       int chunks_cross, const double* q, double inv_docs, double m1_coeff, double2* tmp) {
     const size_t smem = sizeof(double2) * padded_len(v.N) + (sizeof(double2) + 4) * 2 * (size_t)v.n;
 #define L_(LG)                                                                                               \
     {                                                                                                        \
         cudaFuncSetAttribute(k_lda_finish<LG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
-        k_lda_finish<LG><<<v.B * v.S, kThreads, smem, st>>>(v, acc, cross, chunks, q, inv_docs, m1_coeff, tmp); \
+        k_lda_finish<LG><<<v.B * v.S, kThreads, smem, st>>>(v, acc, cross, chunks_acc, chunks_cross, q, inv_docs,   \
+                                                            m1_coeff, tmp);                                          \
     }
     SKC_LOGN_SWITCH_L(v.logN, L_)
 #undef L_
