@@ -1715,7 +1715,9 @@ static void rtpm_restarts_device(skc_sym_set* s, int L, int T_iters, double tol)
             launch_sym_contract(ctx->stream, v, ctx->U.p, L, 0, ctx->part.p);
         }
         SKC_PROF(ctx, "median");
-        launch_median_rows(ctx->stream, ctx->part.p, L, s->B, s->S, s->n, nullptr, ctx->U.p, tol, ctx->flags.p);
+        ctx->values.alloc(static_cast<size_t>(L) * s->n);
+        launch_median_rows(ctx->stream, ctx->part.p, L, s->B, s->S, s->n, nullptr, ctx->U.p, tol, ctx->flags.p,
+                           ctx->values.p);
     }
     ctx->check_launch();
     launch_sym_contract(ctx->stream, v, ctx->U.p, L, 1, ctx->part.p);

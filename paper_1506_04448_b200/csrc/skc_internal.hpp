@@ -132,7 +132,7 @@ void launch_spectrum(cudaStream_t st, const double2* data, std::uint32_t b, int 
 void launch_sym_contract(cudaStream_t st, const SymView& v, const double* U, int L, int mode, double* out);
 // medians: part L x B x S x n -> out L x n (and optional normalisation into Unext)
 void launch_median_rows(cudaStream_t st, const double* part, int L, int B, int S, int n, double* out,
-                        double* Unext, double tol, int* flags);
+                        double* Unext, double tol, int* flags, double* scratch = nullptr);
 void launch_sym_vvv_finish(cudaStream_t st, const double* part, int L, int B, int S, std::uint32_t b,
                            double* values);
 void launch_asym_vvv_finish(cudaStream_t st, const double* part, int L, int B, int S, std::uint32_t b,

@@ -785,48 +785,85 @@ __device__ __forceinline__ double median_of(const double* est, int B) {
     return (B & 1) ? hi : 0.5 * (lo + hi);
 }
 
-// part: L x B x S x n. out (may be null): L x n medians. Unext (may be null):
-// normalised medians (decompose.cpp:35-40), flags[l] set when ||.|| <= tol.
-__global__ void __launch_bounds__(256) k_median_rows(const double* __restrict__ part, int B, int S, int n,
-                                                      double* __restrict__ out, double* __restrict__ Unext,
-                                                      double tol, int* __restrict__ flags) {
-    extern __shared__ double med[];  // n
-    __shared__ double red[8];
-    const int l = blockIdx.x;
-    double est[kMaxB];
-    double ss = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        for (int m = 0; m < B; ++m) {
-            const double* p = part + (((size_t)l * B + m) * S) * n + i;
+// part: L x B x S x n -> med: L x n medians over B of the residue sums (fixed order).
+// One thread per (l, i), grid over all L*n; BT > 0 keeps the B estimates in registers.
+template <int BT>
+__global__ void __launch_bounds__(256) k_median_cols(const double* __restrict__ part, int L, int B, int S, int n,
+                                                      double* __restrict__ med) {
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t >= (long long)L * n) return;
+    const int l = static_cast<int>(t / n), i = static_cast<int>(t - (long long)l * n);
+    constexpr int CAP = BT > 0 ? BT : kMaxB;
+    double est[CAP];
+    const int Bn = BT > 0 ? BT : B;
+#pragma unroll
+    for (int m = 0; m < CAP; ++m) {
+        if (m < Bn) {
+            const double* p = part + (((size_t)l * Bn + m) * S) * n + i;
             double s = p[0];
             for (int r = 1; r < S; ++r) s += p[(size_t)r * n];
             est[m] = s;
         }
-        const double md = median_of(est, B);
-        med[i] = md;
-        if (out) out[(size_t)l * n + i] = md;
-        ss += md * md;
     }
-    if (Unext) {
-        const double tot = block_sum<256>(ss, red);
-        __shared__ double nrm_s;
-        if (threadIdx.x == 0) {
-            const double nrm = sqrt(tot);
-            nrm_s = nrm;
-            if (!(nrm > tol)) flags[l] = 1;
+    // rank selection, ties by index: the (B/2-1)-th and (B/2)-th order statistics
+    const int hiR = Bn / 2, loR = Bn / 2 - 1;
+    double hi = 0.0, lo = 0.0;
+#pragma unroll
+    for (int a = 0; a < CAP; ++a) {
+        if (a >= Bn) break;
+        const double x = est[a];
+        int rank = 0;
+#pragma unroll
+        for (int c = 0; c < CAP; ++c) {
+            if (c >= Bn) break;
+            const double y = est[c];
+            rank += (y < x) || (y == x && c < a);
         }
-        __syncthreads();
-        const double nrm = nrm_s;
-        for (int i = threadIdx.x; i < n; i += blockDim.x) Unext[(size_t)l * n + i] = med[i] / nrm;
+        if (rank == hiR) hi = x;
+        if (rank == loR) lo = x;
     }
+    med[t] = (Bn & 1) ? hi : 0.5 * (lo + hi);
 }
 
+// Unext[l] = med[l] / ||med[l]|| (decompose.cpp:35-40), flags[l] set when ||.|| <= tol.
+__global__ void __launch_bounds__(256) k_normalize_rows(const double* __restrict__ med, int n,
+                                                         double* __restrict__ Unext, double tol,
+                                                         int* __restrict__ flags) {
+    __shared__ double red[8];
+    const int l = blockIdx.x;
+    const double* row = med + (size_t)l * n;
+    double ss = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) ss += row[i] * row[i];
+    const double tot = block_sum<256>(ss, red);
+    __shared__ double nrm_s;
+    if (threadIdx.x == 0) {
+        const double nrm = sqrt(tot);
+        nrm_s = nrm;
+        if (!(nrm > tol)) flags[l] = 1;
+    }
+    __syncthreads();
+    const double nrm = nrm_s;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) Unext[(size_t)l * n + i] = row[i] / nrm;
+}
+
+// out (may be null): L x n medians; Unext (may be null): normalised medians + flags.
+// When out is null a library scratch buffer holds the medians (scratch: L x n).
 void launch_median_rows(cudaStream_t st, const double* part, int L, int B, int S, int n, double* out, double* Unext,
-                        double tol, int* flags) {
-    size_t smem = sizeof(double) * n;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_median_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_median_rows<<<L, 256, smem, st>>>(part, B, S, n, out, Unext, tol, flags);
+                        double tol, int* flags, double* scratch) {
+    double* med = out ? out : scratch;
+    const long long tot = (long long)L * n;
+    const unsigned grid = cdiv(tot, 256);
+    switch (B) {
+        case 10: k_median_cols<10><<<grid, 256, 0, st>>>(part, L, B, S, n, med); break;
+        case 20: k_median_cols<20><<<grid, 256, 0, st>>>(part, L, B, S, n, med); break;
+        case 40: k_median_cols<40><<<grid, 256, 0, st>>>(part, L, B, S, n, med); break;
+        default: k_median_cols<0><<<grid, 256, 0, st>>>(part, L, B, S, n, med); break;
+    }
     SKC_LAUNCHED();
+    if (Unext) {
+        k_normalize_rows<<<L, 256, 0, st>>>(med, n, Unext, tol, flags);
+        SKC_LAUNCHED();
+    }
 }
 
 // vvv: est_m = (acc1/6 + acc2/2)/b + term3/3  (contraction.cpp:122), median over m.
