@@ -4,6 +4,7 @@
 // messages and exception taxonomy follow the reference; compute runs only on the GPU.
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
+#include <omp.h>
 
 #include <algorithm>
 #include <array>
@@ -679,6 +680,76 @@ cublasHandle_t cublas_of(skc_context* ctx) {
     return ctx->cublas;
 }
 
+// Word-major transpose of a CSR corpus, stable (documents ascending within each word),
+// plus per-document token totals: a parallel counting sort over document blocks (per-
+// block word histograms, block-major offsets), deterministic for any thread count.
+struct CorpusT {
+    std::vector<long long> cptr, cdoc, total;
+    std::vector<int> ccount;
+};
+void corpus_transpose(int V, long long D, const long long* doc_ptr, const int* word, const int* count, CorpusT& c,
+                      const std::string& who, bool check_counts) {
+    const long long nnz = doc_ptr[D];
+    const int T = std::max(1, std::min(omp_get_max_threads(), static_cast<int>(std::max<long long>(D / 256, 1))));
+    std::vector<long long> blk(T + 1, 0);
+    for (int t = 1; t < T; ++t) {  // equal-nnz document blocks
+        const long long target = nnz * t / T;
+        blk[t] = std::lower_bound(doc_ptr, doc_ptr + D + 1, target) - doc_ptr;
+        blk[t] = std::min(std::max(blk[t], blk[t - 1]), D);
+    }
+    blk[T] = D;
+    std::vector<std::vector<long long>> hist(T, std::vector<long long>(static_cast<size_t>(V), 0));
+    c.total.assign(static_cast<size_t>(std::max<long long>(D, 1)), 0);
+    int bad_word = 0, bad_count = 0, bad_ptr = 0;
+#pragma omp parallel for num_threads(T) schedule(static, 1) reduction(| : bad_word, bad_count, bad_ptr)
+    for (int t = 0; t < T; ++t) {
+        auto& h = hist[t];
+        for (long long d = blk[t]; d < blk[t + 1]; ++d) {
+            if (doc_ptr[d + 1] < doc_ptr[d]) {
+                bad_ptr = 1;
+                continue;
+            }
+            long long tot = 0;
+            for (long long q = doc_ptr[d]; q < doc_ptr[d + 1]; ++q) {
+                const int w = word[q];
+                if (w < 0 || w >= V) {
+                    bad_word = 1;
+                    continue;
+                }
+                if (check_counts && count[q] < 0) bad_count = 1;
+                tot += count[q];
+                h[w]++;
+            }
+            c.total[d] = tot;
+        }
+    }
+    if (bad_ptr) fail(kInvalidArgument, who + ": doc_ptr must be non-decreasing");
+    if (bad_word) fail(kInvalidArgument, who + ": word id out of range");
+    if (bad_count) fail(kInvalidArgument, who + ": negative count");
+    c.cptr.assign(static_cast<size_t>(V) + 1, 0);
+    for (int w = 0; w < V; ++w) {
+        long long base = c.cptr[w];
+        for (int t = 0; t < T; ++t) {
+            const long long cnt = hist[t][w];
+            hist[t][w] = base;  // becomes block t's first slot for word w
+            base += cnt;
+        }
+        c.cptr[w + 1] = base;
+    }
+    c.cdoc.assign(static_cast<size_t>(std::max<long long>(nnz, 1)), 0);
+    c.ccount.assign(static_cast<size_t>(std::max<long long>(nnz, 1)), 0);
+#pragma omp parallel for num_threads(T) schedule(static, 1)
+    for (int t = 0; t < T; ++t) {
+        auto& pos = hist[t];
+        for (long long d = blk[t]; d < blk[t + 1]; ++d)
+            for (long long q = doc_ptr[d]; q < doc_ptr[d + 1]; ++q) {
+                const long long at = pos[word[q]]++;
+                c.cdoc[at] = d;
+                c.ccount[at] = count[q];
+            }
+    }
+}
+
 // Corpus on the device: CSR (document-major) and its word-major transpose, per-document
 // weights and per-word diagonal / M1 sums.
 struct CorpusDev {
@@ -699,31 +770,15 @@ void upload_corpus(skc_context* ctx, int V, long long D, const long long* doc_pt
         check_vec(word, "lda: word");
         check_vec(count, "lda: count");
     }
-    std::vector<long long> cptr(static_cast<size_t>(V) + 1, 0);
+    CorpusT ct;
+    corpus_transpose(V, D, doc_ptr, word, count, ct, "lda", true);
     for (long long d = 0; d < D; ++d) {
-        require(doc_ptr[d + 1] >= doc_ptr[d], "lda: doc_ptr must be non-decreasing");
-        long long tot = 0;
-        for (long long q = doc_ptr[d]; q < doc_ptr[d + 1]; ++q) {
-            require(word[q] >= 0 && word[q] < V, "lda: word id out of range");
-            require(count[q] >= 0, "lda: negative count");
-            tot += count[q];
-            cptr[static_cast<size_t>(word[q]) + 1]++;
-        }
-        if (tot >= 1) ++c.used1;
-        if (tot >= 2) ++c.used2;
+        if (ct.total[d] >= 1) ++c.used1;
+        if (ct.total[d] >= 2) ++c.used2;
     }
-    for (int w = 0; w < V; ++w) cptr[w + 1] += cptr[w];
-    std::vector<long long> cdoc(static_cast<size_t>(std::max<long long>(nnz, 1)));
-    std::vector<int> ccount(static_cast<size_t>(std::max<long long>(nnz, 1)));
-    {
-        std::vector<long long> fillp(cptr.begin(), cptr.end() - 1);
-        for (long long d = 0; d < D; ++d)
-            for (long long q = doc_ptr[d]; q < doc_ptr[d + 1]; ++q) {
-                const long long pos = fillp[word[q]]++;
-                cdoc[pos] = d;
-                ccount[pos] = count[q];
-            }
-    }
+    std::vector<long long>& cptr = ct.cptr;
+    std::vector<long long>& cdoc = ct.cdoc;
+    std::vector<int>& ccount = ct.ccount;
     c.V = V;
     c.D = D;
     c.nnz = nnz;
@@ -1398,37 +1453,24 @@ int skc_sym_sketch_whitened_m3(skc_sym_set* s, int V, long long D, const long lo
             check_vec(count, "sketch_whitened_m3: count");
         }
         // host: document totals, StreamStats and the word-major transpose (docs ascending)
+        CorpusT ct;
+        corpus_transpose(V, D, doc_ptr, word, count, ct, "sketch_whitened_m3", false);
         long long used = 0, skipped = 0, used1 = 0;
-        std::vector<long long> cptr(static_cast<size_t>(V) + 1, 0);
         std::vector<long long> used_docs;
         for (long long d = 0; d < D; ++d) {
-            long long tot = 0;
-            for (long long q = doc_ptr[d]; q < doc_ptr[d + 1]; ++q) {
-                require(word[q] >= 0 && word[q] < V, "sketch_whitened_m3: word id out of range");
-                tot += count[q];
-                cptr[static_cast<size_t>(word[q]) + 1]++;
-            }
+            const long long tot = ct.total[d];
             if (tot < 3) {  // lda.cpp:164-168
                 ++skipped;
             } else {
                 ++used;
                 used_docs.push_back(d);
             }
-            if (tot >= 1) ++used1;                 // lda.cpp:93-96
+            if (tot >= 1) ++used1;  // lda.cpp:93-96
         }
         if (used == 0) fail(kNumericalError, "sketch_whitened_m3: no documents with >= 3 words");  // lda.cpp:186
-        for (int w = 0; w < V; ++w) cptr[w + 1] += cptr[w];
-        std::vector<long long> cdoc(static_cast<size_t>(nnz));
-        std::vector<int> ccount(static_cast<size_t>(nnz));
-        {
-            std::vector<long long> fillp(cptr.begin(), cptr.end() - 1);
-            for (long long d = 0; d < D; ++d)
-                for (long long q = doc_ptr[d]; q < doc_ptr[d + 1]; ++q) {
-                    const long long pos = fillp[word[q]]++;
-                    cdoc[pos] = d;
-                    ccount[pos] = count[q];
-                }
-        }
+        std::vector<long long>& cptr = ct.cptr;
+        std::vector<long long>& cdoc = ct.cdoc;
+        std::vector<int>& ccount = ct.ccount;
         skc_context* ctx = s->ctx;
         ctx->use();
         const cudaStream_t st = ctx->stream;
