@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <array>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -758,6 +759,10 @@ struct CorpusDev {
     DevBuf<long long> doc_ptr, cptr, cdoc, total;
     DevBuf<int> word, count, ccount;
     DevBuf<double> s2, invm, diag, m1p;
+    // word-pass chunks (load balance over Zipf-heavy words): [chunk_lo, chunk_hi) CSC
+    // ranges, word w owns chunks [word_chunk[w], word_chunk[w+1])
+    long long nchunks = 0;
+    DevBuf<long long> chunk_lo, chunk_hi, word_chunk;
 };
 
 void upload_corpus(skc_context* ctx, int V, long long D, const long long* doc_ptr, const int* word, const int* count,
@@ -779,6 +784,21 @@ void upload_corpus(skc_context* ctx, int V, long long D, const long long* doc_pt
     std::vector<long long>& cptr = ct.cptr;
     std::vector<long long>& cdoc = ct.cdoc;
     std::vector<int>& ccount = ct.ccount;
+    {
+        constexpr long long kWordChunk = 64;
+        std::vector<long long> lo, hi, wc(static_cast<size_t>(V) + 1, 0);
+        for (int w = 0; w < V; ++w) {
+            for (long long q = cptr[w]; q < cptr[w + 1]; q += kWordChunk) {
+                lo.push_back(q);
+                hi.push_back(std::min(q + kWordChunk, cptr[w + 1]));
+            }
+            wc[w + 1] = static_cast<long long>(lo.size());
+        }
+        c.nchunks = static_cast<long long>(lo.size());
+        c.chunk_lo.upload(lo.empty() ? wc.data() : lo.data(), std::max<size_t>(lo.size(), 1), ctx->stream);
+        c.chunk_hi.upload(hi.empty() ? wc.data() : hi.data(), std::max<size_t>(hi.size(), 1), ctx->stream);
+        c.word_chunk.upload(wc.data(), wc.size(), ctx->stream);
+    }
     c.V = V;
     c.D = D;
     c.nnz = nnz;
@@ -811,15 +831,147 @@ void check_corpus_m2(const CorpusDev& c) {
 }
 
 struct M2Work {
-    DevBuf<double> Z, mx;
+    DevBuf<double> Z, part, mx;
 };
 void m2_apply(skc_context* ctx, const CorpusDev& c, double alpha0, int p, const double* Xd, double* Yd, M2Work& w) {
     w.Z.alloc(static_cast<size_t>(std::max<long long>(c.D, 1)) * p);
+    w.part.alloc(static_cast<size_t>(std::max<long long>(std::max<long long>(c.nchunks, (c.V + 511) / 512), 1)) * p);
     w.mx.alloc(static_cast<size_t>(p));
-    launch_m2_apply(ctx->stream, c.V, c.D, p, c.doc_ptr.p, c.word.p, c.count.p, c.cptr.p, c.cdoc.p, c.ccount.p, c.s2.p,
-                    c.diag.p, c.m1p.p, 1.0 / static_cast<double>(c.used1), 1.0 / static_cast<double>(c.used2),
-                    alpha0 / (alpha0 + 1.0), Xd, w.Z.p, w.mx.p, Yd);
+    launch_m2_apply(ctx->stream, c.V, c.D, p, c.doc_ptr.p, c.word.p, c.count.p, c.cdoc.p, c.ccount.p, c.nchunks,
+                    c.chunk_lo.p, c.chunk_hi.p, c.word_chunk.p, c.s2.p, c.diag.p, c.m1p.p,
+                    1.0 / static_cast<double>(c.used1), 1.0 / static_cast<double>(c.used2), alpha0 / (alpha0 + 1.0),
+                    Xd, w.Z.p, w.part.p, w.mx.p, Yd);
     ctx->check_launch();
+}
+
+// Householder tridiagonalisation + implicit shifted QL (O(p^3); the textbook method),
+// symmetric row-major input; vecs[i*n + c] = component i of the eigenvector of vals[c]
+// (ascending). Returns false if an eigenvalue fails to converge.
+bool sym_eigen_ql_rowmajor(int n, std::vector<double> a, std::vector<double>& vals, std::vector<double>& vecs) {
+    auto A = [&](int i, int j) -> double& { return a[(size_t)i * n + j]; };
+    std::vector<double> d(n), e(n);
+    for (int i = n - 1; i > 0; --i) {
+        const int l = i - 1;
+        double h = 0.0, scale = 0.0;
+        if (l > 0) {
+            for (int k = 0; k <= l; ++k) scale += std::fabs(A(i, k));
+            if (scale == 0.0) {
+                e[i] = A(i, l);
+            } else {
+                for (int k = 0; k <= l; ++k) {
+                    A(i, k) /= scale;
+                    h += A(i, k) * A(i, k);
+                }
+                double f = A(i, l);
+                double g = (f >= 0.0) ? -std::sqrt(h) : std::sqrt(h);
+                e[i] = scale * g;
+                h -= f * g;
+                A(i, l) = f - g;
+                f = 0.0;
+                for (int j = 0; j <= l; ++j) {
+                    A(j, i) = A(i, j) / h;
+                    g = 0.0;
+                    for (int k = 0; k <= j; ++k) g += A(j, k) * A(i, k);
+                    for (int k = j + 1; k <= l; ++k) g += A(k, j) * A(i, k);
+                    e[j] = g / h;
+                    f += e[j] * A(i, j);
+                }
+                const double hh = f / (h + h);
+                for (int j = 0; j <= l; ++j) {
+                    f = A(i, j);
+                    e[j] = g = e[j] - hh * f;
+                    for (int k = 0; k <= j; ++k) A(j, k) -= (f * e[k] + g * A(i, k));
+                }
+            }
+        } else {
+            e[i] = A(i, l);
+        }
+        d[i] = h;
+    }
+    d[0] = 0.0;
+    e[0] = 0.0;
+    for (int i = 0; i < n; ++i) {
+        const int l = i - 1;
+        if (d[i] != 0.0) {
+            for (int j = 0; j <= l; ++j) {
+                double g = 0.0;
+                for (int k = 0; k <= l; ++k) g += A(i, k) * A(k, j);
+                for (int k = 0; k <= l; ++k) A(k, j) -= g * A(k, i);
+            }
+        }
+        d[i] = A(i, i);
+        A(i, i) = 1.0;
+        for (int j = 0; j <= l; ++j) A(j, i) = A(i, j) = 0.0;
+    }
+    // implicit QL on (d, e) accumulating into A (columns = eigenvectors)
+    for (int i = 1; i < n; ++i) e[i - 1] = e[i];
+    e[n - 1] = 0.0;
+    for (int l = 0; l < n; ++l) {
+        int iter = 0, m;
+        do {
+            for (m = l; m < n - 1; ++m) {
+                const double dd = std::fabs(d[m]) + std::fabs(d[m + 1]);
+                if (std::fabs(e[m]) <= 1e-16 * dd) break;
+            }
+            if (m != l) {
+                if (iter++ == 100) return false;
+                double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+                double r = std::hypot(g, 1.0);
+                g = d[m] - d[l] + e[l] / (g + (g >= 0.0 ? std::fabs(r) : -std::fabs(r)));
+                double s = 1.0, c = 1.0, p = 0.0;
+                int i;
+                for (i = m - 1; i >= l; --i) {
+                    double f = s * e[i];
+                    const double b = c * e[i];
+                    e[i + 1] = (r = std::hypot(f, g));
+                    if (r == 0.0) {
+                        d[i + 1] -= p;
+                        e[m] = 0.0;
+                        break;
+                    }
+                    s = f / r;
+                    c = g / r;
+                    g = d[i + 1] - p;
+                    r = (d[i] - g) * s + 2.0 * c * b;
+                    d[i + 1] = g + (p = s * r);
+                    g = c * r - b;
+                    for (int k = 0; k < n; ++k) {
+                        f = A(k, i + 1);
+                        A(k, i + 1) = s * A(k, i) + c * f;
+                        A(k, i) = c * A(k, i) - s * f;
+                    }
+                }
+                if (r == 0.0 && i >= l) continue;
+                d[l] -= p;
+                e[l] = g;
+                e[m] = 0.0;
+            }
+        } while (m != l);
+    }
+    std::vector<int> ord(n);
+    for (int i = 0; i < n; ++i) ord[i] = i;
+    std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return d[x] < d[y]; });
+    vals.resize(n);
+    vecs.assign((size_t)n * n, 0.0);
+    for (int c = 0; c < n; ++c) {
+        vals[c] = d[ord[c]];
+        for (int i = 0; i < n; ++i) vecs[(size_t)i * n + c] = A(i, ord[c]);
+    }
+    return true;
+}
+
+// Symmetric eigensolver used by the host-side small problems (col-major output like
+// jacobi_eigen): tridiagonal QL, with the Jacobi sweep as fallback.
+void jacobi_eigen(int p, std::vector<double> a, std::vector<double>& vals, std::vector<double>& vecs);
+void sym_eigen_host(int p, const std::vector<double>& a, std::vector<double>& vals, std::vector<double>& vecs) {
+    std::vector<double> rm;
+    if (sym_eigen_ql_rowmajor(p, a, vals, rm)) {  // symmetric: row-major == col-major input
+        vecs.assign(static_cast<size_t>(p) * p, 0.0);
+        for (int c = 0; c < p; ++c)
+            for (int i = 0; i < p; ++i) vecs[static_cast<size_t>(c) * p + i] = rm[static_cast<size_t>(i) * p + c];
+        return;
+    }
+    jacobi_eigen(p, a, vals, vecs);
 }
 
 // Cyclic Jacobi for a small symmetric matrix (col-major p x p): ascending eigenvalues,
@@ -968,17 +1120,30 @@ void whiten_randomized(skc_context* ctx, int V, int k, int oversample, int iters
     if (oversample < 0) oversample = std::max(16, k / 4);
     if (iters < 0) iters = 12;
     const int p = std::min(V, (k + oversample + 31) / 32 * 32);
-    Rng rng(derive_seed(seed, seed_tag::kWhitenProbe));
-    std::vector<double> om(static_cast<size_t>(V) * p);
-    for (double& x : om) x = rng.gaussian();
+    static const bool trace = std::getenv("SKC_WHITEN_TRACE") != nullptr;
+    auto t_last = std::chrono::steady_clock::now();
+    auto tick = [&](const char* what) {
+        if (!trace) return;
+        ctx->sync();
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "whiten %-12s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(now - t_last).count());
+        t_last = now;
+    };
+    Rng rng(derive_seed(seed, seed_tag::kWhitenProbe));  // host stream: MGS completion only
     DevBuf<double> Q, Y;
-    Q.alloc(om.size());
-    Y.upload(om.data(), om.size(), ctx->stream);
+    Q.alloc(static_cast<size_t>(V) * p);
+    Y.alloc(static_cast<size_t>(V) * p);
+    // Gaussian start block on the device (counter-based, deterministic)
+    launch_gaussian_fill(ctx->stream, derive_seed(seed, seed_tag::kWhitenProbe), static_cast<long long>(V) * p, Y.p);
+    tick("omega");
     OrthWork ow;
     orthonormalize(ctx, V, p, Y.p, Q.p, ow, rng);
+    tick("orth0");
     for (int it = 0; it < iters; ++it) {
         apply(Q.p, Y.p, p);
+        tick("apply");
         orthonormalize(ctx, V, p, Y.p, Q.p, ow, rng);
+        tick("orth");
     }
     apply(Q.p, Y.p, p);
     // Rayleigh-Ritz: H = Q^T M2 Q (p x p)
@@ -995,8 +1160,10 @@ void whiten_randomized(skc_context* ctx, int V, int k, int oversample, int iters
             const double s = 0.5 * (H[static_cast<size_t>(j) * p + i] + H[static_cast<size_t>(i) * p + j]);
             H[static_cast<size_t>(j) * p + i] = H[static_cast<size_t>(i) * p + j] = s;
         }
+    tick("rayleigh");
     std::vector<double> ev, U;
-    jacobi_eigen(p, H, ev, U);
+    sym_eigen_host(p, H, ev, U);
+    tick("eigen");
     std::vector<double> Uk(static_cast<size_t>(p) * k), fw(k), fu(k);
     for (int c = 0; c < k; ++c) {
         const double e = ev[p - 1 - c];
@@ -1092,7 +1259,7 @@ std::vector<double> pinv_spectral_host(int k, const std::vector<double>& G /* co
         return P;
     }
     std::vector<double> ev, U;
-    jacobi_eigen(k, G, ev, U);
+    sym_eigen_host(k, G, ev, U);
     double amax = 0.0;
     for (double e : ev) amax = std::max(amax, std::fabs(e));
     const double cutoff = 1e-10 * amax;
@@ -2620,7 +2787,7 @@ int skc_lda_heldout_likelihood(int V, int k, const double* Phi, int Vh, long lon
                 gram[static_cast<size_t>(b) * k + a] = s;
             }
         std::vector<double> ev, U;
-        jacobi_eigen(k, gram, ev, U);
+        sym_eigen_host(k, gram, ev, U);
         const double lips = ev.empty() ? 0.0 : ev.back();
         const double step = lips > 0 ? 1.0 / lips : 1.0;
         std::vector<double> per(static_cast<size_t>(std::max<long long>(D, 1)), 0.0);

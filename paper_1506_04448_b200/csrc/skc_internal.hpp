@@ -113,11 +113,13 @@ void launch_corpus_prep(cudaStream_t st, int V, long long D, const long long* do
                         const long long* cptr, const long long* cdoc, const int* ccount, long long* total, double* s2,
                         double* invm, double* diag, double* m1p);
 void launch_m2_apply(cudaStream_t st, int V, long long D, int p, const long long* doc_ptr, const int* word,
-                     const int* count, const long long* cptr, const long long* cdoc, const int* ccount,
+                     const int* count, const long long* cdoc, const int* ccount, long long nchunks,
+                     const long long* chunk_lo, const long long* chunk_hi, const long long* word_chunk,
                      const double* s2, const double* diag, const double* m1p, double inv_used1, double inv_used2,
-                     double a, const double* X, double* Z, double* mx, double* Y);
+                     double a, const double* X, double* Z, double* part, double* mx, double* Y);
 void launch_scale_cols(cudaStream_t st, long long rows, int k, const double* in, const double* f, double* out);
 void launch_normalize_columns(cudaStream_t st, int n, int k, double* F, const double* prev, double* lambda);
+void launch_gaussian_fill(cudaStream_t st, unsigned long long seed, long long count, double* out);
 
 // residue twiddle tables of a symmetric set (SymView::stw*/gtw*)
 void launch_sym_twiddle_tables(cudaStream_t st, const SymView& v, double2* stw1, double2* stw2, double2* gtw1,

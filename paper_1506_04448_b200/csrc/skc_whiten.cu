@@ -15,8 +15,9 @@
 //   k_m2_word_prep  per word: diag_w = sum s2_d c_dw, m1_w (CSC, fixed order)  (thread/word)
 //   k_m2_docs       Z[d, :] = s2_d sum_q c_q X[w_q, :]                     (warp/doc)
 //   k_colsum        mx = m1^T X                                           (block/32 cols)
-//   k_m2_words      Y[w, :] = (sum_{d in w} c Z[d, :] - diag_w X[w, :]) / used2
-//                             - a m1_w mx                                  (warp/word)
+//   k_m2_word_chunks / k_m2_word_finish
+//                   Y[w, :] = (sum_{d in w} c Z[d, :] - diag_w X[w, :]) / used2 - a m1_w mx
+//                   (warp per <= 64-entry chunk of a word's CSC range, then warp per word)
 // Every sum runs in a fixed order, so the operator is deterministic.
 #include <cuda_runtime.h>
 
@@ -86,35 +87,48 @@ __global__ void k_m2_docs(long long D, int p, const long long* __restrict__ doc_
     }
 }
 
-// mx[c] = sum_w m1_w X[w, c] with m1_w = m1p_w / used1; block per 32 columns, 8 warps
-// striding the rows, warp partials combined in a fixed order.
+// mx[c] = sum_w m1_w X[w, c] with m1_w = m1p_w / used1, in two deterministic stages:
+// block (rb, cg) sums rows [rb*RB, (rb+1)*RB) of column group cg (8 warps striding the
+// rows, warp partials combined in order) into part[rb][c]; then k_colsum_final adds the
+// row-block partials in order.
+constexpr int kColsumRows = 512;
 __global__ void k_colsum(int V, int p, const double* __restrict__ m1p, double inv_used1, const double* __restrict__ X,
-                         double* __restrict__ mx) {
-    __shared__ double part[8][32];
+                         double* __restrict__ part) {
+    __shared__ double sp[8][32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int c = blockIdx.x * 32 + lane;
+    const int c = blockIdx.y * 32 + lane;
+    const int r0 = blockIdx.x * kColsumRows, r1 = min(V, r0 + kColsumRows);
     double acc = 0.0;
     if (c < p)
-        for (int w = warp; w < V; w += 8) acc += (m1p[w] * inv_used1) * X[(size_t)w * p + c];
-    part[warp][lane] = acc;
+        for (int w = r0 + warp; w < r1; w += 8) acc += (m1p[w] * inv_used1) * X[(size_t)w * p + c];
+    sp[warp][lane] = acc;
     __syncthreads();
     if (warp == 0 && c < p) {
         double s = 0.0;
-        for (int i = 0; i < 8; ++i) s += part[i][lane];
-        mx[c] = s;
+        for (int i = 0; i < 8; ++i) s += sp[i][lane];
+        part[(size_t)blockIdx.x * p + c] = s;
     }
 }
+__global__ void k_colsum_final(int nb, int p, const double* __restrict__ part, double* __restrict__ mx) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= p) return;
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += part[(size_t)b * p + c];
+    mx[c] = s;
+}
 
-__global__ void k_m2_words(int V, int p, const long long* __restrict__ cptr, const long long* __restrict__ cdoc,
-                           const int* __restrict__ ccount, const double* __restrict__ Z, const double* __restrict__ diag,
-                           const double* __restrict__ m1p, double inv_used1, double inv_used2, double a,
-                           const double* __restrict__ mx, const double* __restrict__ X, double* __restrict__ Y) {
-    const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+// Word pass split for load balance: a word's CSC range is cut into chunks of at most
+// kWordChunk entries (frequent words are Zipf-heavy); a warp per chunk writes its partial
+// sum, and a warp per word adds its chunks in order and applies the diagonal and rank-1
+// terms. Deterministic for any chunking of the same corpus.
+__global__ void k_m2_word_chunks(long long nchunks, int p, const long long* __restrict__ chunk_lo,
+                                 const long long* __restrict__ chunk_hi, const long long* __restrict__ cdoc,
+                                 const int* __restrict__ ccount, const double* __restrict__ Z,
+                                 double* __restrict__ part) {
+    const long long ck = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (w >= V) return;
-    const long long q0 = cptr[w], q1 = cptr[w + 1];
-    const double dg = diag[w];
-    const double m1w = m1p[w] * inv_used1;
+    if (ck >= nchunks) return;
+    const long long q0 = chunk_lo[ck], q1 = chunk_hi[ck];
     for (int c0 = 0; c0 < p; c0 += 128) {
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
         for (long long q = q0; q < q1; ++q) {
@@ -129,11 +143,24 @@ __global__ void k_m2_words(int V, int p, const long long* __restrict__ cptr, con
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int c = c0 + lane + 32 * u;
-            if (c < p) {
-                const size_t idx = (size_t)w * p + c;
-                Y[idx] = (acc[u] - dg * X[idx]) * inv_used2 - a * m1w * mx[c];
-            }
+            if (c < p) part[(size_t)ck * p + c] = acc[u];
         }
+    }
+}
+__global__ void k_m2_word_finish(int V, int p, const long long* __restrict__ word_chunk, const double* __restrict__ part,
+                                 const double* __restrict__ diag, const double* __restrict__ m1p, double inv_used1,
+                                 double inv_used2, double a, const double* __restrict__ mx, const double* __restrict__ X,
+                                 double* __restrict__ Y) {
+    const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= V) return;
+    const double dg = diag[w];
+    const double m1w = m1p[w] * inv_used1;
+    for (int c = lane; c < p; c += 32) {
+        double acc = 0.0;
+        for (long long ck = word_chunk[w]; ck < word_chunk[w + 1]; ++ck) acc += part[(size_t)ck * p + c];
+        const size_t idx = (size_t)w * p + c;
+        Y[idx] = (acc - dg * X[idx]) * inv_used2 - a * m1w * mx[c];
     }
 }
 
@@ -170,6 +197,29 @@ __global__ void k_normalize_columns(int n, double* __restrict__ F, const double*
     const double nrm = nrm_s;
     for (int i = threadIdx.x; i < n; i += 256) col[i] = nrm > 0 ? col[i] / nrm : prev[(size_t)r * n + i];
 }
+// Counter-based Gaussian block: element t from two splitmix64 draws keyed by (seed, t)
+// and the Box-Muller cosine branch (deterministic; only the start of the subspace
+// iteration, so device libm rounding is immaterial).
+__device__ __forceinline__ unsigned long long smix(unsigned long long z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__global__ void k_gaussian_fill(unsigned long long seed, long long count, double* __restrict__ out) {
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t >= count) return;
+    const unsigned long long a = smix(seed ^ smix(2ull * (unsigned long long)t));
+    const unsigned long long b = smix(seed ^ smix(2ull * (unsigned long long)t + 1ull));
+    const double u1 = (static_cast<double>(a >> 11) + 1.0) * 0x1.0p-53;  // (0, 1]
+    const double u2 = static_cast<double>(b >> 11) * 0x1.0p-53;          // [0, 1)
+    out[t] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+}
+void launch_gaussian_fill(cudaStream_t st, unsigned long long seed, long long count, double* out) {
+    k_gaussian_fill<<<cdiv_w(count, 256), 256, 0, st>>>(seed, count, out);
+    count_launch();
+}
+
 void launch_normalize_columns(cudaStream_t st, int n, int k, double* F, const double* prev, double* lambda) {
     k_normalize_columns<<<k, 256, 0, st>>>(n, F, prev, lambda);
     count_launch();
@@ -185,13 +235,24 @@ void launch_corpus_prep(cudaStream_t st, int V, long long D, const long long* do
 }
 
 void launch_m2_apply(cudaStream_t st, int V, long long D, int p, const long long* doc_ptr, const int* word,
-                     const int* count, const long long* cptr, const long long* cdoc, const int* ccount,
+                     const int* count, const long long* cdoc, const int* ccount, long long nchunks,
+                     const long long* chunk_lo, const long long* chunk_hi, const long long* word_chunk,
                      const double* s2, const double* diag, const double* m1p, double inv_used1, double inv_used2,
-                     double a, const double* X, double* Z, double* mx, double* Y) {
+                     double a, const double* X, double* Z, double* part, double* mx, double* Y) {
     if (D > 0) k_m2_docs<<<cdiv_w(D * 32, 256), 256, 0, st>>>(D, p, doc_ptr, word, count, s2, X, Z);
-    k_colsum<<<cdiv_w(p, 32), 256, 0, st>>>(V, p, m1p, inv_used1, X, mx);
-    k_m2_words<<<cdiv_w((long long)V * 32, 256), 256, 0, st>>>(V, p, cptr, cdoc, ccount, Z, diag, m1p, inv_used1,
-                                                               inv_used2, a, mx, X, Y);
+    {
+        const int nb = static_cast<int>(cdiv_w(V, kColsumRows));
+        // (part is free here: the chunk pass below overwrites it after mx is final)
+        k_colsum<<<dim3(nb, cdiv_w(p, 32)), 256, 0, st>>>(V, p, m1p, inv_used1, X, part);
+        k_colsum_final<<<cdiv_w(p, 128), 128, 0, st>>>(nb, p, part, mx);
+        count_launch();
+    }
+    if (nchunks > 0)
+        k_m2_word_chunks<<<cdiv_w(nchunks * 32, 256), 256, 0, st>>>(nchunks, p, chunk_lo, chunk_hi, cdoc, ccount, Z,
+                                                                    part);
+    k_m2_word_finish<<<cdiv_w((long long)V * 32, 256), 256, 0, st>>>(V, p, word_chunk, part, diag, m1p, inv_used1,
+                                                                     inv_used2, a, mx, X, Y);
+    count_launch();
     count_launch();
     count_launch();
     count_launch();
