@@ -572,9 +572,12 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
         if (!ctx->stream2) CK(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
         if (!ctx->ev_q[0])
             for (int c = 0; c < 5; ++c) CK(cudaEventCreateWithFlags(&ctx->ev_q[c], cudaEventDisableTiming));
+        // decreasing chunk sizes: chunk c's main pass (~0.4x the bus time of its rows) hides
+        // under chunk c+1's bus reads, and the exposed tail (last main pass) stays short
+        static const double kFrac4[5] = {0.0, 0.42, 0.72, 0.90, 1.0};
         std::vector<int> rb(K + 1, 0);
         for (int c = 1; c < K; ++c) {
-            const long long target = tot * c / K;
+            const long long target = (K == 4) ? static_cast<long long>(static_cast<double>(tot) * kFrac4[c]) : tot * c / K;
             rb[c] = static_cast<int>(std::lower_bound(rt.cum.begin(), rt.cum.end(), target) - rt.cum.begin());
             rb[c] = std::min(std::max(rb[c], rb[c - 1]), rt.nrows);
         }
@@ -582,6 +585,12 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
         CK(cudaMemsetAsync(p.nonfinite, 0, sizeof(int), ctx->stream));
         {
             SKC_PROF(ctx, "build_pipelined");
+            static const bool ptrace = std::getenv("SKC_PIPE_TRACE") != nullptr;
+            cudaEvent_t te[4][5];
+            if (ptrace)
+                for (auto& row : te)
+                    for (auto& e : row) CK(cudaEventCreate(&e));
+            if (ptrace) CK(cudaEventRecord(te[0][0], ctx->stream));
             for (int c = 0; c < K; ++c) {
                 BuildPlan pc = p;
                 pc.rowtab = rt.rows.p + rb[c];
@@ -593,11 +602,15 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
                 pc.reset_nonfinite = false;
                 pc.acc = ctx->build_acc.p + static_cast<size_t>(c) * total_slots;
                 pc.next_row = ctx->build_ints.p + static_cast<size_t>(c) * G;
+                if (ptrace) CK(cudaEventRecord(te[0][c + 1 < 5 ? c + 1 : 4], ctx->stream));
                 if (pc.nrows > 0) launch_build_prepass(ctx->stream, Tdev, pc);
+                if (ptrace) CK(cudaEventRecord(te[1][c], ctx->stream));
                 CK(cudaEventRecord(ctx->ev_q[c], ctx->stream));
                 CK(cudaStreamWaitEvent(ctx->stream2, ctx->ev_q[c], 0));
                 if (pc.nrows > 0) {
+                    if (ptrace) CK(cudaEventRecord(te[2][c], ctx->stream2));
                     launch_build_main(ctx->stream2, Tdev, pc);
+                    if (ptrace) CK(cudaEventRecord(te[3][c], ctx->stream2));
                 } else {
                     CK(cudaMemsetAsync(pc.acc, 0, sizeof(unsigned long long) * (size_t)total_slots, ctx->stream2));
                 }
@@ -607,6 +620,19 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
             BuildPlan pf = p;
             pf.acc = ctx->build_acc.p;
             launch_build_finalize_multi(ctx->stream, pf, K, ctx->ints.p + 4);
+            if (ptrace) {
+                ctx->sync();
+                for (int c = 0; c < K && c < 4; ++c) {
+                    float q0, q1, m0, m1;
+                    cudaEventElapsedTime(&q0, te[0][0], te[0][c + 1 < 5 ? c + 1 : 4]);
+                    cudaEventElapsedTime(&q1, te[0][0], te[1][c]);
+                    cudaEventElapsedTime(&m0, te[0][0], te[2][c]);
+                    cudaEventElapsedTime(&m1, te[0][0], te[3][c]);
+                    std::fprintf(stderr, "chunk %d quantize %.3f-%.3f ms main %.3f-%.3f ms\n", c, q0, q1, m0, m1);
+                }
+                for (auto& row : te)
+                    for (auto& e : row) cudaEventDestroy(e);
+            }
         }
         ctx->check_launch();
     } else {
