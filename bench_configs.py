@@ -7,11 +7,11 @@ on the host cores (bounded samples, stated in each line).
   C0  n=100 fp64 rank 10, b=2^12 B=20: sym + asym dense build, RTPM k=10 L=50 T=30
   C1  n=400 fp64 rank 50, b=2^14 B=20: full RTPM k=50 L=100 T=30
   C2  n=1000 fp32 rank 100 (4 GB, generated on device), b=2^16 B=10: dense build
-  C3  factored third moment, n=1000, K=50 Dirichlet(0.1) mixtures + 0.1 N(0,I), b=2^14 B=10:
-      frequency-domain accumulation (reduced N, linear in N), then RTPM k=50 L=T=30
-  C4  LDA V=50000 K=100, Dirichlet(0.01) topics, Poisson(150) docs (reduced D), b=2^14 B=10:
-      whitening from the corpus M2 (implicit, randomized), sketch_whitened_m3, then RTPM
-      L=100 k=100 T=30
+  C3  factored third moment, N=2^22 samples (device-generated blocks), n=1000, K=50
+      Dirichlet(0.1) mixtures + 0.1 N(0,I), b=2^14 B=10, then RTPM k=50 L=T=30
+  C4  LDA V=50000 K=100, Dirichlet(0.01) topics, D=1e6 Poisson(150) docs (device-generated
+      corpus), b=2^14 B=10: whitening from the corpus M2 (implicit, randomized),
+      sketch_whitened_m3, RTPM L=100 k=100 T=30, recover_params
 
   C5  (paper Table 4) fast ALS: n=1000 rank 10 fp32 tensor on device, asym b=2^14 B=40,
       k=10, exactly 30 sweeps
@@ -143,71 +143,123 @@ def c2(skb, ctx, quick):
 
 
 def c3(skb, ctx, quick):
-    n, K, b, B = 1000, 50, 1 << 14, 10
-    N = 1 << (14 if quick else 17)
-    rng = np.random.default_rng(3)
-    A, _ = np.linalg.qr(rng.normal(size=(n, K)))
-    Wm = rng.dirichlet(np.full(K, 0.1), size=N)
-    X = Wm @ A.T + 0.1 * rng.normal(size=(N, n))
+    """Factored third moment at BASELINE size: N = 2^22 samples x_i = A w_i + 0.1 g_i
+    (n=1000, K=50, w ~ Dirichlet(0.1)), generated on the device in 2^18-sample blocks
+    (seeded torch generator) and accumulated block by block (the sketch is linear)."""
     import torch
 
-    Xd = torch.from_numpy(X).cuda()
-    w = torch.full((N,), 1.0 / N, dtype=torch.float64, device="cuda")
+    n, K, b, B = 1000, 50, 1 << 14, 10
+    N = 1 << (16 if quick else 22)
+    blk = min(N, 1 << 18)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    A = torch.linalg.qr(torch.randn(n, K, generator=g, device="cuda", dtype=torch.float64))[0]
+    conc = torch.full((K,), 0.1, device="cuda", dtype=torch.float64)
     s = skb.SymTensorSketchSet(n, b, B, 4, ctx)
-    s.accumulate_moment(Xd[:256], w[:256])
-    _, dev = timed(ctx, lambda: s.accumulate_moment(Xd, w), ["moment", "freq_inverse", "combine"])
-    ms = sum(dev.values())
-    emit({"config": 3, "what": "factored moment sketch (frequency-domain accumulation)", "N": N, "n": n, "b": b,
-          "B": B, "device_ms": ms, "samples_per_s": N / (ms * 1e-3),
-          "extrapolated_seconds_for_N=2^22": (1 << 22) / (N / (ms * 1e-3))})
+    ctx.profile(True)
+    ctx.profile_reset()
+    gen_s = 0.0
+    for start in range(0, N, blk):
+        t0 = time.perf_counter()
+        gam = torch._standard_gamma(conc.expand(blk, K).contiguous())
+        Wm = gam / gam.sum(dim=1, keepdim=True)
+        X = Wm @ A.T + 0.1 * torch.randn(blk, n, generator=g, device="cuda", dtype=torch.float64)
+        torch.cuda.synchronize()
+        gen_s += time.perf_counter() - t0
+        s.accumulate_moment(X, torch.full((blk,), 1.0 / N, device="cuda", dtype=torch.float64))
+    ctx.synchronize()
+    ms = sum(ctx.profile_get(k)[0] for k in ["moment", "freq_inverse", "combine"])
+    ctx.profile(False)
+    emit({"config": 3, "what": "factored moment sketch (frequency-domain accumulation), device-resident samples",
+          "N": N, "n": n, "b": b, "B": B, "device_ms": ms, "samples_per_s": N / (ms * 1e-3),
+          "sample_generation_s_not_timed": gen_s})
     k = 5 if quick else 50
     t0 = time.perf_counter()
     dec = skb.robust_tpm_fast(s, skb.PowerConfig(k=k, L=30, T_iters=30, seed=1))
+    A_h = A.cpu().numpy()
+    cos = np.abs(A_h.T @ (dec.A / np.linalg.norm(dec.A, axis=0)))
     emit({"config": 3, "what": f"RTPM k={k} L=30 T=30 on the moment sketch", "seconds": time.perf_counter() - t0,
-          "lambda_top3": dec.lambda_[:3].tolist()})
+          "lambda_top3": dec.lambda_[:3].tolist(), "best_cos_to_planted_median": float(np.median(cos.max(axis=0)))})
+
+
+def _lda_corpus_device(V, K, D, seed):
+    """Synthetic LDA corpus on the device: topics ~ Dirichlet(0.01 1_V), theta_d ~
+    Dirichlet(alpha0/K 1_K) with alpha0 = 1, m_d ~ Poisson(150), topic-then-word token
+    draws (inverse CDF); returns host CSR (doc_ptr, word, count) and the topics."""
+    import torch
+
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    dev = "cuda"
+    topics = torch._standard_gamma(torch.full((K, V), 0.01, device=dev, dtype=torch.float64), generator=g)
+    topics = topics / topics.sum(dim=1, keepdim=True)
+    cdf = torch.cumsum(topics, dim=1)
+    cdf[:, -1] = 1.0
+    lens = torch.poisson(torch.full((D,), 150.0, device=dev), generator=g).to(torch.int64)
+    theta = torch._standard_gamma(torch.full((D, K), 1.0 / K, device=dev, dtype=torch.float64), generator=g)
+    theta = theta / theta.sum(dim=1, keepdim=True).clamp_min(1e-300)
+    theta = torch.nan_to_num(theta, nan=1.0 / K)
+    keys = []
+    for d0 in range(0, D, 50000):
+        d1 = min(D, d0 + 50000)
+        L = lens[d0:d1]
+        mx = int(L.max().item()) if d1 > d0 else 0
+        if mx == 0:
+            continue
+        z = torch.multinomial(theta[d0:d1].float().clamp_min(1e-30), mx, replacement=True, generator=g)  # (nd, mx)
+        mask = torch.arange(mx, device=dev)[None, :] < L[:, None]
+        doc = (torch.arange(d0, d1, device=dev)[:, None].expand(-1, mx))[mask]
+        zt = z[mask]
+        u = torch.rand(zt.numel(), device=dev, dtype=torch.float64, generator=g)
+        w = torch.empty_like(zt)
+        for k in range(K):
+            sel = zt == k
+            if sel.any():
+                w[sel] = torch.searchsorted(cdf[k], u[sel]).clamp_max(V - 1)
+        keys.append(doc * V + w)
+    keys = torch.cat(keys)
+    uk, cnt = torch.unique(keys, return_counts=True)
+    docs = uk // V
+    words = (uk % V).to(torch.int32)
+    doc_ptr = torch.zeros(D + 1, dtype=torch.int64, device=dev)
+    doc_ptr[1:] = torch.cumsum(torch.bincount(docs, minlength=D), dim=0)
+    return (doc_ptr.cpu().numpy(), words.cpu().numpy(), cnt.to(torch.int32).cpu().numpy(), topics.cpu().numpy())
 
 
 def c4(skb, ctx, quick):
+    """Spectral LDA at BASELINE size: V=5e4, K=100, D=1e6 documents (device-generated
+    corpus), whitening from the corpus M2, sketch_whitened_m3, RTPM, recover_params."""
     V, K, b, B = 50000, 100, 1 << 14, 10
-    D = 2000 if quick else 100000
-    rng = np.random.default_rng(4)
-    topics = rng.dirichlet(np.full(V, 0.01), size=K)
-    lens = rng.poisson(150, size=D)
-    doc_ptr, words, counts = [0], [], []
-    for d in range(D):
-        theta = rng.dirichlet(np.full(K, 1.0 / K))
-        p = theta @ topics
-        c = rng.multinomial(lens[d], p / p.sum())
-        nz = np.nonzero(c)[0]
-        words.append(nz.astype(np.int32))
-        counts.append(c[nz].astype(np.int32))
-        doc_ptr.append(doc_ptr[-1] + nz.size)
-    words = np.concatenate(words)
-    counts = np.concatenate(counts)
-    # whitening from the corpus' own second moment (lda.cpp:102-143, implicit M2 on the GPU)
+    D = 20000 if quick else 1000000
+    t0 = time.perf_counter()
+    doc_ptr, words, counts, topics = _lda_corpus_device(V, K, D, 4)
+    gen_s = time.perf_counter() - t0
     alpha0 = 1.0
+    t0 = time.perf_counter()
+    corpus = skb.LdaCorpus(V, doc_ptr, words, counts, ctx)  # upload + transpose once
+    corpus_s = time.perf_counter() - t0
     t0 = time.perf_counter()
     ctx.profile(True)
     ctx.profile_reset()
-    wm = skb.whiten_corpus(V, np.array(doc_ptr), words, counts, alpha0, K, ctx=ctx)
+    wm = corpus.whiten(alpha0, K)
     whiten_s = time.perf_counter() - t0
     whiten_dev = ctx.profile_get("lda_whiten")[0]
     ctx.profile(False)
     emit({"config": 4, "what": "whiten(compute_m2(corpus), K) by randomized subspace iteration on the implicit M2",
-          "V": V, "K": K, "D": D, "nnz": int(words.size), "seconds": whiten_s, "device_ms": whiten_dev,
+          "V": V, "K": K, "D": D, "nnz": int(words.size), "tokens": int(counts.sum()),
+          "corpus_upload_transpose_s": corpus_s, "seconds": whiten_s, "device_section_ms": whiten_dev,
+          "corpus_generation_s_not_timed": gen_s,
           "top_eigenvalues": wm.singular_values[:3].tolist(), "kth_eigenvalue": float(wm.singular_values[-1])})
     W = wm.W
     s = skb.SymTensorSketchSet(K, b, B, 9, ctx)
     t0 = time.perf_counter()
     ctx.profile(True)
     ctx.profile_reset()
-    used, skipped = s.sketch_whitened_m3(V, np.array(doc_ptr), words, counts, W, alpha0)
+    used, skipped = s.sketch_whitened_m3_corpus(corpus, W, alpha0)
     wall = time.perf_counter() - t0
     dev = {x: ctx.profile_get(x)[0] for x in ["lda_docs", "lda_vocab", "lda_accumulate"]}
     ctx.profile(False)
-    emit({"config": 4, "what": "sketch_whitened_m3 given W (host CSR in, includes host transpose + H2D)", "V": V,
+    emit({"config": 4, "what": "sketch_whitened_m3 given W on the device-resident corpus", "V": V,
           "K": K, "D": D, "nnz": int(words.size), "used": used, "skipped": skipped, "seconds": wall,
-          "device_ms_by_kernel": dev, "docs_per_s_device": D / (sum(dev.values()) * 1e-3)})
+          "device_ms_by_kernel": dev, "docs_per_s_device": used / (sum(dev.values()) * 1e-3)})
     k = 5 if quick else 100
     t0 = time.perf_counter()
     dec = skb.robust_tpm_fast(s, skb.PowerConfig(k=k, L=100, T_iters=30, seed=2))

@@ -160,6 +160,18 @@ int skc_lda_whiten_corpus(skc_context* ctx, int V, long long D, const long long*
 int skc_lda_whiten_dense(skc_context* ctx, int V, const double* m2, int k, int oversample, int iters, uint64_t seed,
                          double* W, double* unwhiten, double* singular_values);
 
+/* Device-resident corpus (B200 extension): upload + validate + word-major transpose once,
+ * then whiten and sketch without re-uploading (the reference passes Corpus& to each). */
+typedef struct skc_lda_corpus skc_lda_corpus;
+int skc_lda_corpus_create(skc_context* ctx, int V, long long D, const long long* doc_ptr, const int* word,
+                          const int* count, skc_lda_corpus** out);
+int skc_lda_corpus_destroy(skc_lda_corpus* c);
+int skc_lda_corpus_info(const skc_lda_corpus* c, int* V, long long* D, long long* nnz, long long* used3);
+int skc_lda_whiten_corpus_handle(skc_lda_corpus* c, double alpha0, int k, int oversample, int iters, uint64_t seed,
+                                 double* W, double* unwhiten, double* singular_values);
+int skc_sym_sketch_whitened_m3_corpus(skc_sym_set* s, skc_lda_corpus* c, const double* W, double alpha0,
+                                      long long* used, long long* skipped);
+
 /* recover_params(D, wm, alpha0) (lda.cpp:228-248), host math: lambda[k], A = D.A (k x k
  * row-major, column i = component i), unwhiten V x k -> Phi V x k (columns projected onto
  * the simplex, lda.cpp:250-271) and alpha[k]. */

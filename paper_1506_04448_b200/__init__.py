@@ -377,6 +377,16 @@ class SymTensorSketchSet:
         wa = None if w is None else _f64(w, (X.shape[0],))
         check(lib.skc_sym_accumulate_moment(self._h, _dp(X), None if wa is None else _dp(wa), X.shape[0], SKC_HOST))
 
+    def sketch_whitened_m3_corpus(self, corpus: "LdaCorpus", W, alpha0: float):
+        """sketch_whitened_m3 on a device-resident LdaCorpus (no re-upload)."""
+        Wm = _f64(W)
+        if Wm.shape != (corpus.V, self.n()):
+            raise ValueError("sketch_whitened_m3: vocabulary mismatch")
+        used, skipped = C.c_longlong(), C.c_longlong()
+        check(lib.skc_sym_sketch_whitened_m3_corpus(self._h, corpus.handle, _dp(Wm), float(alpha0), C.byref(used),
+                                                    C.byref(skipped)))
+        return used.value, skipped.value
+
     def sketch_whitened_m3(self, V: int, doc_ptr, word, count, W, alpha0: float):
         """lda.cpp:145-226 on this set (n == whitening rank k). Corpus in CSR form; returns
         StreamStats as (used, skipped)."""
@@ -801,6 +811,39 @@ def whiten(m2hat, k: int, oversample: int = -1, iters: int = -1, seed: int = 0x5
     check(lib.skc_lda_whiten_dense(ctx.handle, V, _dp(M), int(k), int(oversample), int(iters), C.c_uint64(seed),
                                    _dp(W), _dp(U), _dp(sv)))
     return WhiteningMap(W, U, sv)
+
+
+class LdaCorpus:
+    """Device-resident corpus (B200 extension): CSR uploaded, validated and transposed
+    once; whiten() and SymTensorSketchSet.sketch_whitened_m3(corpus=...) reuse it."""
+
+    def __init__(self, V: int, doc_ptr, word, count, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        keep, (D, dpp, wdp, ctp) = _corpus_args(doc_ptr, word, count)
+        h = C.c_void_p()
+        check(lib.skc_lda_corpus_create(self.ctx.handle, int(V), D, dpp, wdp, ctp, C.byref(h)))
+        self._h = h
+        self.V = int(V)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.skc_lda_corpus_destroy(self._h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self):
+        V, D, nnz, u3 = C.c_int(), C.c_longlong(), C.c_longlong(), C.c_longlong()
+        check(lib.skc_lda_corpus_info(self._h, C.byref(V), C.byref(D), C.byref(nnz), C.byref(u3)))
+        return {"V": V.value, "D": D.value, "nnz": nnz.value, "docs_ge3": u3.value}
+
+    def whiten(self, alpha0: float, k: int, oversample: int = -1, iters: int = -1, seed: int = 0x5EED):
+        W, U, sv = np.empty((self.V, k)), np.empty((self.V, k)), np.empty(k)
+        check(lib.skc_lda_whiten_corpus_handle(self._h, float(alpha0), int(k), int(oversample), int(iters),
+                                               C.c_uint64(seed), _dp(W), _dp(U), _dp(sv)))
+        return WhiteningMap(W, U, sv)
 
 
 class LdaModel:

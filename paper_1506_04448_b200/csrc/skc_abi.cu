@@ -781,7 +781,8 @@ void corpus_transpose(int V, long long D, const long long* doc_ptr, const int* w
 // weights and per-word diagonal / M1 sums.
 struct CorpusDev {
     int V = 0;
-    long long D = 0, nnz = 0, used1 = 0, used2 = 0;
+    long long D = 0, nnz = 0, used1 = 0, used2 = 0, used3 = 0;
+    DevBuf<long long> used_docs;  // documents with >= 3 tokens (sketch_whitened_m3, lda.cpp:164-168)
     DevBuf<long long> doc_ptr, cptr, cdoc, total;
     DevBuf<int> word, count, ccount;
     DevBuf<double> s2, invm, diag, m1p;
@@ -792,21 +793,25 @@ struct CorpusDev {
 };
 
 void upload_corpus(skc_context* ctx, int V, long long D, const long long* doc_ptr, const int* word, const int* count,
-                   CorpusDev& c) {
-    require(V >= 1 && D >= 0, "lda: invalid corpus dimensions");
-    check_vec(doc_ptr, "lda: doc_ptr");
+                   CorpusDev& c, const std::string& who = "lda", bool check_counts = true) {
+    require(V >= 1 && D >= 0, who + ": invalid corpus dimensions");
+    check_vec(doc_ptr, (who + ": doc_ptr").c_str());
     const long long nnz = doc_ptr[D];
-    require(doc_ptr[0] == 0 && nnz >= 0, "lda: doc_ptr must start at 0");
+    require(doc_ptr[0] == 0 && nnz >= 0, who + ": doc_ptr must start at 0");
     if (nnz > 0) {
-        check_vec(word, "lda: word");
-        check_vec(count, "lda: count");
+        check_vec(word, (who + ": word").c_str());
+        check_vec(count, (who + ": count").c_str());
     }
     CorpusT ct;
-    corpus_transpose(V, D, doc_ptr, word, count, ct, "lda", true);
+    corpus_transpose(V, D, doc_ptr, word, count, ct, who, check_counts);
+    std::vector<long long> used3;
     for (long long d = 0; d < D; ++d) {
         if (ct.total[d] >= 1) ++c.used1;
         if (ct.total[d] >= 2) ++c.used2;
+        if (ct.total[d] >= 3) used3.push_back(d);
     }
+    c.used3 = static_cast<long long>(used3.size());
+    c.used_docs.upload(used3.empty() ? doc_ptr : used3.data(), std::max<size_t>(used3.size(), 1), ctx->stream);
     std::vector<long long>& cptr = ct.cptr;
     std::vector<long long>& cdoc = ct.cdoc;
     std::vector<int>& ccount = ct.ccount;
@@ -1300,9 +1305,75 @@ std::vector<double> pinv_spectral_host(int k, const std::vector<double>& G /* co
     return P;
 }
 
+// sketch_whitened_m3 (lda.cpp:145-226) on an uploaded corpus.
+void sketch_whitened_m3_dev(skc_sym_set* s, CorpusDev& c, const double* W, double alpha0, long long* used_out,
+                            long long* skipped_out) {
+    check_vec(W, "sketch_whitened_m3: W");
+    const int k = s->n;  // lda.cpp:149-151: set dimension must equal the whitening rank
+    require(k <= 2048, "sketch_whitened_m3: whitening rank above 2048 is not supported on the device path");
+    const long long used = c.used3, skipped = c.D - c.used3, used1 = c.used1;
+    if (used == 0) fail(kNumericalError, "sketch_whitened_m3: no documents with >= 3 words");  // lda.cpp:186
+    const int V = c.V;
+    const long long D = c.D;
+    skc_context* ctx = s->ctx;
+    ctx->use();
+    const cudaStream_t st = ctx->stream;
+    DevBuf<long long> d_total;
+    DevBuf<double> d_W, d_P, d_s1, d_s2, d_coeff1, d_sumwn, d_m1, d_q, d_acc, d_cross;
+    d_W.upload(W, static_cast<size_t>(V) * k, st);
+    d_P.alloc(static_cast<size_t>(std::max<long long>(D, 1)) * k);
+    d_s1.alloc(static_cast<size_t>(std::max<long long>(D, 1)));
+    d_s2.alloc(static_cast<size_t>(std::max<long long>(D, 1)));
+    d_total.alloc(static_cast<size_t>(std::max<long long>(D, 1)));
+    d_coeff1.alloc(static_cast<size_t>(V));
+    d_sumwn.alloc(static_cast<size_t>(V) * k);
+    d_m1.alloc(static_cast<size_t>(V));
+    d_q.alloc(static_cast<size_t>(k));
+    {
+        SKC_PROF(ctx, "lda_docs");
+        launch_lda_docs(st, k, D, c.doc_ptr.p, c.word.p, c.count.p, d_W.p, alpha0, d_P.p, d_s1.p, d_s2.p, d_total.p);
+    }
+    {
+        SKC_PROF(ctx, "lda_vocab");
+        launch_lda_vocab(st, k, V, c.cptr.p, c.cdoc.p, c.ccount.p, d_P.p, d_s1.p, d_total.p, d_coeff1.p, d_sumwn.p,
+                         d_m1.p);
+    }
+    launch_lda_q(st, k, V, d_W.p, d_m1.p, 1.0 / static_cast<double>(used1), d_q.p);
+    ctx->check_launch();
+    const int per_rep = s->B * s->S;
+    // ~4 waves of 2 resident CTAs per SM for each of the two item kinds
+    const int chunks_d = std::max(1, static_cast<int>(std::min<long long>(used, (8ll * ctx->sms) / per_rep)));
+    const int chunks_v = std::max(1, static_cast<int>(std::min<long long>(V, (8ll * ctx->sms) / per_rep)));
+    d_acc.alloc(static_cast<size_t>(chunks_d + chunks_v) * per_rep * s->N * 2);
+    d_cross.alloc(static_cast<size_t>(chunks_d) * per_rep * s->N * 2);
+    SymView v = s->view();
+    {
+        SKC_PROF(ctx, "lda_accumulate");
+        launch_lda_accumulate(st, v, used, c.used_docs.p, d_P.p, d_s1.p, d_s2.p, V, d_W.p, d_coeff1.p, d_sumwn.p,
+                              chunks_d, chunks_v, d_acc.p, d_cross.p);
+    }
+    ctx->check_launch();
+    ctx->tmp.alloc(static_cast<size_t>(s->B) * s->b);
+    const double inv_docs = 1.0 / static_cast<double>(used);
+    const double m1_coeff = 2.0 * alpha0 * alpha0 / ((alpha0 + 1.0) * (alpha0 + 2.0));  // lda.cpp:191
+    launch_lda_finish(st, v, d_acc.p, d_cross.p, chunks_d + chunks_v, chunks_d, d_q.p, inv_docs, m1_coeff, ctx->tmp.p);
+    ctx->check_launch();
+    launch_combine_residues(st, ctx->tmp.p, s->B, s->S, s->N, s->b, v.tw, 1.0, -1, false, s->data.p);
+    ctx->check_launch();
+    s->version += static_cast<std::uint64_t>(s->B);  // mutable_replicate(m) per replicate (lda.cpp:197)
+    ctx->sync();
+    if (used_out) *used_out = used;
+    if (skipped_out) *skipped_out = skipped;
+}
+
 }  // namespace
 
 // ============================ C-ABI ==============================================
+struct skc_lda_corpus {
+    skc_context* ctx = nullptr;
+    CorpusDev dev;
+};
+
 extern "C" {
 
 const char* skc_last_error(void) { return g_last_error.c_str(); }
@@ -1634,95 +1705,11 @@ int skc_sym_sketch_whitened_m3(skc_sym_set* s, int V, long long D, const long lo
                                long long* skipped_out) {
     return guard([&] {
         check_vec(s, "set");
-        require(V >= 1 && D >= 0, "sketch_whitened_m3: invalid corpus dimensions");
-        check_vec(doc_ptr, "sketch_whitened_m3: doc_ptr");
         check_vec(W, "sketch_whitened_m3: W");
-        const int k = s->n;  // lda.cpp:149-151: set dimension must equal the whitening rank
-        require(k <= 2048, "sketch_whitened_m3: whitening rank above 2048 is not supported on the device path");
-        const long long nnz = doc_ptr[D] - doc_ptr[0];
-        require(doc_ptr[0] == 0 && nnz >= 0, "sketch_whitened_m3: doc_ptr must start at 0");
-        if (nnz > 0) {
-            check_vec(word, "sketch_whitened_m3: word");
-            check_vec(count, "sketch_whitened_m3: count");
-        }
-        // host: document totals, StreamStats and the word-major transpose (docs ascending)
-        CorpusT ct;
-        corpus_transpose(V, D, doc_ptr, word, count, ct, "sketch_whitened_m3", false);
-        long long used = 0, skipped = 0, used1 = 0;
-        std::vector<long long> used_docs;
-        for (long long d = 0; d < D; ++d) {
-            const long long tot = ct.total[d];
-            if (tot < 3) {  // lda.cpp:164-168
-                ++skipped;
-            } else {
-                ++used;
-                used_docs.push_back(d);
-            }
-            if (tot >= 1) ++used1;  // lda.cpp:93-96
-        }
-        if (used == 0) fail(kNumericalError, "sketch_whitened_m3: no documents with >= 3 words");  // lda.cpp:186
-        std::vector<long long>& cptr = ct.cptr;
-        std::vector<long long>& cdoc = ct.cdoc;
-        std::vector<int>& ccount = ct.ccount;
-        skc_context* ctx = s->ctx;
-        ctx->use();
-        const cudaStream_t st = ctx->stream;
-        DevBuf<long long> d_ptr, d_cptr, d_cdoc, d_total;
-        DevBuf<int> d_word, d_count, d_ccount;
-        DevBuf<double> d_W, d_P, d_s1, d_s2, d_coeff1, d_sumwn, d_m1, d_q, d_acc, d_cross;
-        d_ptr.upload(doc_ptr, static_cast<size_t>(D) + 1, st);
-        d_word.upload(word, static_cast<size_t>(std::max<long long>(nnz, 1)), st);
-        d_count.upload(count, static_cast<size_t>(std::max<long long>(nnz, 1)), st);
-        d_cptr.upload(cptr.data(), cptr.size(), st);
-        d_cdoc.upload(cdoc.data(), std::max<size_t>(cdoc.size(), 1), st);
-        d_ccount.upload(ccount.data(), std::max<size_t>(ccount.size(), 1), st);
-        d_W.upload(W, static_cast<size_t>(V) * k, st);
-        d_P.alloc(static_cast<size_t>(std::max<long long>(D, 1)) * k);
-        d_s1.alloc(static_cast<size_t>(std::max<long long>(D, 1)));
-        d_s2.alloc(static_cast<size_t>(std::max<long long>(D, 1)));
-        d_total.alloc(static_cast<size_t>(std::max<long long>(D, 1)));
-        d_coeff1.alloc(static_cast<size_t>(V));
-        d_sumwn.alloc(static_cast<size_t>(V) * k);
-        d_m1.alloc(static_cast<size_t>(V));
-        d_q.alloc(static_cast<size_t>(k));
-        {
-            SKC_PROF(ctx, "lda_docs");
-            launch_lda_docs(st, k, D, d_ptr.p, d_word.p, d_count.p, d_W.p, alpha0, d_P.p, d_s1.p, d_s2.p, d_total.p);
-        }
-        {
-            SKC_PROF(ctx, "lda_vocab");
-            launch_lda_vocab(st, k, V, d_cptr.p, d_cdoc.p, d_ccount.p, d_P.p, d_s1.p, d_total.p, d_coeff1.p,
-                             d_sumwn.p, d_m1.p);
-        }
-        launch_lda_q(st, k, V, d_W.p, d_m1.p, 1.0 / static_cast<double>(used1), d_q.p);
-        ctx->check_launch();
-        const int per_rep = s->B * s->S;
-        // ~4 waves of 2 resident CTAs per SM for each of the two item kinds
-        const int chunks_d = std::max(1, static_cast<int>(std::min<long long>(used, (8ll * ctx->sms) / per_rep)));
-        const int chunks_v = std::max(1, static_cast<int>(std::min<long long>(V, (8ll * ctx->sms) / per_rep)));
-        d_acc.alloc(static_cast<size_t>(chunks_d + chunks_v) * per_rep * s->N * 2);
-        d_cross.alloc(static_cast<size_t>(chunks_d) * per_rep * s->N * 2);
-        DevBuf<long long> d_used;
-        d_used.upload(used_docs.data(), used_docs.size(), st);
-        SymView v = s->view();
-        {
-            SKC_PROF(ctx, "lda_accumulate");
-            launch_lda_accumulate(st, v, used, d_used.p, d_P.p, d_s1.p, d_s2.p, V, d_W.p, d_coeff1.p, d_sumwn.p,
-                                  chunks_d, chunks_v, d_acc.p, d_cross.p);
-        }
-        ctx->check_launch();
-        ctx->tmp.alloc(static_cast<size_t>(s->B) * s->b);
-        const double inv_docs = 1.0 / static_cast<double>(used);
-        const double m1_coeff = 2.0 * alpha0 * alpha0 / ((alpha0 + 1.0) * (alpha0 + 2.0));  // lda.cpp:191
-        launch_lda_finish(st, v, d_acc.p, d_cross.p, chunks_d + chunks_v, chunks_d, d_q.p, inv_docs, m1_coeff,
-                          ctx->tmp.p);
-        ctx->check_launch();
-        launch_combine_residues(st, ctx->tmp.p, s->B, s->S, s->N, s->b, v.tw, 1.0, -1, false, s->data.p);
-        ctx->check_launch();
-        s->version += static_cast<std::uint64_t>(s->B);  // mutable_replicate(m) per replicate (lda.cpp:197)
-        ctx->sync();
-        if (used_out) *used_out = used;
-        if (skipped_out) *skipped_out = skipped;
+        s->ctx->use();
+        CorpusDev c;
+        upload_corpus(s->ctx, V, D, doc_ptr, word, count, c, "sketch_whitened_m3", false);
+        sketch_whitened_m3_dev(s, c, W, alpha0, used_out, skipped_out);
     });
 }
 
@@ -2954,6 +2941,66 @@ int skc_asym_als(skc_asym_set* s, int k, int max_iters, double tol, uint64_t see
         CK(cudaMemcpyAsync(C_out, fac[2], nk * 8, cudaMemcpyDeviceToHost, ctx->stream));
         ctx->sync();
         if (iters_out) *iters_out = it;
+    });
+}
+
+
+// ---- device-resident corpus handle (upload + transpose once, reuse across calls) ------
+int skc_lda_corpus_create(skc_context* ctx, int V, long long D, const long long* doc_ptr, const int* word,
+                          const int* count, skc_lda_corpus** out) {
+    return guard([&] {
+        check_vec(ctx, "context");
+        check_vec(out, "lda_corpus_create: out");
+        ctx->use();
+        auto c = std::make_unique<skc_lda_corpus>();
+        c->ctx = ctx;
+        upload_corpus(ctx, V, D, doc_ptr, word, count, c->dev, "lda", true);
+        ctx->sync();
+        *out = c.release();
+    });
+}
+int skc_lda_corpus_destroy(skc_lda_corpus* c) {
+    return guard([&] {
+        if (!c) return;
+        c->ctx->use();
+        delete c;
+    });
+}
+int skc_lda_corpus_info(const skc_lda_corpus* c, int* V, long long* D, long long* nnz, long long* used3) {
+    return guard([&] {
+        check_vec(c, "corpus");
+        if (V) *V = c->dev.V;
+        if (D) *D = c->dev.D;
+        if (nnz) *nnz = c->dev.nnz;
+        if (used3) *used3 = c->dev.used3;
+    });
+}
+int skc_lda_whiten_corpus_handle(skc_lda_corpus* c, double alpha0, int k, int oversample, int iters, uint64_t seed,
+                                 double* W, double* unwhiten, double* singular_values) {
+    return guard([&] {
+        check_vec(c, "corpus");
+        check_vec(W, "whiten: W");
+        check_vec(unwhiten, "whiten: unwhiten");
+        check_vec(singular_values, "whiten: singular_values");
+        skc_context* ctx = c->ctx;
+        ctx->use();
+        check_corpus_m2(c->dev);
+        require(k >= 1 && k <= c->dev.V, "whiten: invalid target rank");
+        M2Work w;
+        SKC_PROF(ctx, "lda_whiten");
+        whiten_randomized(
+            ctx, c->dev.V, k, oversample, iters, seed,
+            [&](const double* Xd, double* Yd, int p) { m2_apply(ctx, c->dev, alpha0, p, Xd, Yd, w); }, W, unwhiten,
+            singular_values);
+    });
+}
+int skc_sym_sketch_whitened_m3_corpus(skc_sym_set* s, skc_lda_corpus* c, const double* W, double alpha0,
+                                      long long* used_out, long long* skipped_out) {
+    return guard([&] {
+        check_vec(s, "set");
+        check_vec(c, "corpus");
+        require(s->ctx == c->ctx, "sketch_whitened_m3: set and corpus belong to different contexts");
+        sketch_whitened_m3_dev(s, c->dev, W, alpha0, used_out, skipped_out);
     });
 }
 

@@ -540,6 +540,26 @@ def test_lda_whiten_matches_dense_eigensolver_oracle(gpu_ctx, dense):
     assert np.max(np.abs(wm.W.T @ M2 @ wm.W - np.eye(k))) <= 1e-8
 
 
+def test_lda_device_corpus_handle_matches_per_call_path(gpu_ctx):
+    """The device-resident corpus gives the same whitening and sketch as the per-call
+    entry points (same operator, same order), bit for bit."""
+    from lda_fixtures import synthetic_corpus
+
+    V, k, alpha0 = 90, 5, 1.0
+    doc_ptr, word, count, _ = synthetic_corpus(V=V, k=k, D=800, mean_len=20, seed=6)
+    corpus = skb().LdaCorpus(V, doc_ptr, word, count, gpu_ctx)
+    info = corpus.info()
+    assert info["V"] == V and info["D"] == doc_ptr.size - 1 and info["nnz"] == word.size
+    a = corpus.whiten(alpha0, k, iters=20)
+    b = skb().whiten_corpus(V, doc_ptr, word, count, alpha0, k, iters=20, ctx=gpu_ctx)
+    assert np.array_equal(a.W, b.W) and np.array_equal(a.singular_values, b.singular_values)
+    s1 = skb().SymTensorSketchSet(k, 1024, 4, 3, gpu_ctx)
+    s2 = skb().SymTensorSketchSet(k, 1024, 4, 3, gpu_ctx)
+    assert s1.sketch_whitened_m3_corpus(corpus, a.W, alpha0) == s2.sketch_whitened_m3(V, doc_ptr, word, count, a.W,
+                                                                                       alpha0)
+    assert np.array_equal(s1.data(), s2.data())
+
+
 def test_lda_whiten_errors_follow_reference(gpu_ctx):
     from lda_fixtures import synthetic_corpus
 
