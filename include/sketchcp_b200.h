@@ -160,6 +160,15 @@ int skc_lda_whiten_corpus(skc_context* ctx, int V, long long D, const long long*
 int skc_lda_whiten_dense(skc_context* ctx, int V, const double* m2, int k, int oversample, int iters, uint64_t seed,
                          double* W, double* unwhiten, double* singular_values);
 
+/* Document shard of sketch_whitened_m3 for multi-GPU runs: document sums over this
+ * shard, normalised by the whole corpus' global_used (documents with >= 3 tokens) and
+ * using its averaged M1 (global_m1, V); add_q_cubed != 0 on exactly one shard. Summing
+ * the shards' data (all-reduce) gives the full sketch (the sketch is linear in the
+ * per-document terms). */
+int skc_sym_sketch_whitened_m3_shard(skc_sym_set* s, int V, long long D, const long long* doc_ptr, const int* word,
+                                     const int* count, const double* W, double alpha0, long long global_used,
+                                     const double* global_m1, int add_q_cubed, long long* used, long long* skipped);
+
 /* Device-resident corpus (B200 extension): upload + validate + word-major transpose once,
  * then whiten and sketch without re-uploading (the reference passes Corpus& to each). */
 typedef struct skc_lda_corpus skc_lda_corpus;

@@ -377,6 +377,19 @@ class SymTensorSketchSet:
         wa = None if w is None else _f64(w, (X.shape[0],))
         check(lib.skc_sym_accumulate_moment(self._h, _dp(X), None if wa is None else _dp(wa), X.shape[0], SKC_HOST))
 
+    def sketch_whitened_m3_shard(self, V: int, doc_ptr, word, count, W, alpha0: float, global_used: int, global_m1,
+                                 add_q_cubed: bool):
+        """Document-shard form (multi-GPU): sums over these documents, normalised by the
+        whole corpus' global_used and M1; add_q_cubed on exactly one shard."""
+        keep, (D, dpp, wdp, ctp) = _corpus_args(doc_ptr, word, count)
+        Wm = _f64(W)
+        m1 = _f64(global_m1, (int(V),))
+        used, skipped = C.c_longlong(), C.c_longlong()
+        check(lib.skc_sym_sketch_whitened_m3_shard(self._h, int(V), D, dpp, wdp, ctp, _dp(Wm), float(alpha0),
+                                                   int(global_used), _dp(m1), 1 if add_q_cubed else 0,
+                                                   C.byref(used), C.byref(skipped)))
+        return used.value, skipped.value
+
     def sketch_whitened_m3_corpus(self, corpus: "LdaCorpus", W, alpha0: float):
         """sketch_whitened_m3 on a device-resident LdaCorpus (no re-upload)."""
         Wm = _f64(W)

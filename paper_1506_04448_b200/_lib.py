@@ -68,6 +68,8 @@ SIGNATURES = {
     "skc_sym_accumulate_moment": (c_int, [p_void, p_double, p_double, c_ll, c_int]),
     "skc_sym_sketch_whitened_m3": (c_int, [p_void, c_int, c_ll, p_ll, p_int, p_int, p_double, c_double, p_ll, p_ll]),
     "skc_asym_als": (c_int, [p_void, c_int, c_int, c_double, c_u64, p_double, p_double, p_double, p_double, p_int]),
+    "skc_sym_sketch_whitened_m3_shard": (c_int, [p_void, c_int, c_ll, p_ll, p_int, p_int, p_double, c_double, c_ll,
+                                                 p_double, c_int, p_ll, p_ll]),
     "skc_lda_corpus_create": (c_int, [p_void, c_int, c_ll, p_ll, p_int, p_int, C.POINTER(p_void)]),
     "skc_lda_corpus_destroy": (c_int, [p_void]),
     "skc_lda_corpus_info": (c_int, [p_void, p_int, p_ll, p_ll, p_ll]),

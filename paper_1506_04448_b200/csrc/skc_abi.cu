@@ -1306,13 +1306,21 @@ std::vector<double> pinv_spectral_host(int k, const std::vector<double>& G /* co
 }
 
 // sketch_whitened_m3 (lda.cpp:145-226) on an uploaded corpus.
+// Shard mode (global_m1 != null): the document sums run over this corpus only, while the
+// normalisation 1/D_used (global_used) and q = W^T m1 (global_m1, V, already averaged)
+// are the whole corpus'; add_q_cubed selects the one shard that adds c_m1 F(q)^3. The
+// sketch is linear in the per-document terms, so summing the shards' data reproduces the
+// full sketch_whitened_m3.
 void sketch_whitened_m3_dev(skc_sym_set* s, CorpusDev& c, const double* W, double alpha0, long long* used_out,
-                            long long* skipped_out) {
+                            long long* skipped_out, long long global_used = -1, const double* global_m1 = nullptr,
+                            bool add_q_cubed = true) {
     check_vec(W, "sketch_whitened_m3: W");
     const int k = s->n;  // lda.cpp:149-151: set dimension must equal the whitening rank
     require(k <= 2048, "sketch_whitened_m3: whitening rank above 2048 is not supported on the device path");
+    const bool shard = global_m1 != nullptr;
     const long long used = c.used3, skipped = c.D - c.used3, used1 = c.used1;
-    if (used == 0) fail(kNumericalError, "sketch_whitened_m3: no documents with >= 3 words");  // lda.cpp:186
+    const long long norm_used = shard ? global_used : used;
+    if (norm_used <= 0) fail(kNumericalError, "sketch_whitened_m3: no documents with >= 3 words");  // lda.cpp:186
     const int V = c.V;
     const long long D = c.D;
     skc_context* ctx = s->ctx;
@@ -1338,11 +1346,16 @@ void sketch_whitened_m3_dev(skc_sym_set* s, CorpusDev& c, const double* W, doubl
         launch_lda_vocab(st, k, V, c.cptr.p, c.cdoc.p, c.ccount.p, d_P.p, d_s1.p, d_total.p, d_coeff1.p, d_sumwn.p,
                          d_m1.p);
     }
-    launch_lda_q(st, k, V, d_W.p, d_m1.p, 1.0 / static_cast<double>(used1), d_q.p);
+    if (shard) {
+        d_m1.upload(global_m1, static_cast<size_t>(V), st);
+        launch_lda_q(st, k, V, d_W.p, d_m1.p, 1.0, d_q.p);
+    } else {
+        launch_lda_q(st, k, V, d_W.p, d_m1.p, 1.0 / static_cast<double>(used1), d_q.p);
+    }
     ctx->check_launch();
     const int per_rep = s->B * s->S;
     // ~4 waves of 2 resident CTAs per SM for each of the two item kinds
-    const int chunks_d = std::max(1, static_cast<int>(std::min<long long>(used, (8ll * ctx->sms) / per_rep)));
+    const int chunks_d = std::max(1, static_cast<int>(std::min<long long>(std::max<long long>(used, 1), (8ll * ctx->sms) / per_rep)));
     const int chunks_v = std::max(1, static_cast<int>(std::min<long long>(V, (8ll * ctx->sms) / per_rep)));
     d_acc.alloc(static_cast<size_t>(chunks_d + chunks_v) * per_rep * s->N * 2);
     d_cross.alloc(static_cast<size_t>(chunks_d) * per_rep * s->N * 2);
@@ -1354,8 +1367,9 @@ void sketch_whitened_m3_dev(skc_sym_set* s, CorpusDev& c, const double* W, doubl
     }
     ctx->check_launch();
     ctx->tmp.alloc(static_cast<size_t>(s->B) * s->b);
-    const double inv_docs = 1.0 / static_cast<double>(used);
-    const double m1_coeff = 2.0 * alpha0 * alpha0 / ((alpha0 + 1.0) * (alpha0 + 2.0));  // lda.cpp:191
+    const double inv_docs = 1.0 / static_cast<double>(norm_used);
+    const double m1_coeff =
+        add_q_cubed ? 2.0 * alpha0 * alpha0 / ((alpha0 + 1.0) * (alpha0 + 2.0)) : 0.0;  // lda.cpp:191
     launch_lda_finish(st, v, d_acc.p, d_cross.p, chunks_d + chunks_v, chunks_d, d_q.p, inv_docs, m1_coeff, ctx->tmp.p);
     ctx->check_launch();
     launch_combine_residues(st, ctx->tmp.p, s->B, s->S, s->N, s->b, v.tw, 1.0, -1, false, s->data.p);
@@ -3001,6 +3015,24 @@ int skc_sym_sketch_whitened_m3_corpus(skc_sym_set* s, skc_lda_corpus* c, const d
         check_vec(c, "corpus");
         require(s->ctx == c->ctx, "sketch_whitened_m3: set and corpus belong to different contexts");
         sketch_whitened_m3_dev(s, c->dev, W, alpha0, used_out, skipped_out);
+    });
+}
+
+
+// Document-shard form of sketch_whitened_m3 for multi-GPU runs (distributed.py).
+int skc_sym_sketch_whitened_m3_shard(skc_sym_set* s, int V, long long D, const long long* doc_ptr, const int* word,
+                                     const int* count, const double* W, double alpha0, long long global_used,
+                                     const double* global_m1, int add_q_cubed, long long* used_out,
+                                     long long* skipped_out) {
+    return guard([&] {
+        check_vec(s, "set");
+        check_vec(W, "sketch_whitened_m3: W");
+        check_vec(global_m1, "sketch_whitened_m3: global m1");
+        require(global_used >= 1, "sketch_whitened_m3: no documents with >= 3 words");
+        s->ctx->use();
+        CorpusDev c;
+        upload_corpus(s->ctx, V, D, doc_ptr, word, count, c, "sketch_whitened_m3", false);
+        sketch_whitened_m3_dev(s, c, W, alpha0, used_out, skipped_out, global_used, global_m1, add_q_cubed != 0);
     });
 }
 

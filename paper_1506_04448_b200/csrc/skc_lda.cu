@@ -376,6 +376,10 @@ void launch_lda_accumulate(cudaStream_t st, const SymView& v, long long Du, cons
     const unsigned grid_d = (unsigned)((long long)chunks_d * v.B * v.S);
     const unsigned grid_v = (unsigned)((long long)chunks_v * v.B * v.S);
     double* acc_v = acc + (size_t)chunks_d * v.B * v.S * v.N * 2;
+    if (Du <= 0) {  // a document shard with no used documents contributes nothing
+        cudaMemsetAsync(acc, 0, sizeof(double) * (size_t)chunks_d * v.B * v.S * v.N * 2, st);
+        cudaMemsetAsync(cross, 0, sizeof(double) * (size_t)chunks_d * v.B * v.S * v.N * 2, st);
+    }
 #define L_(LG)                                                                                                      \
     {                                                                                                               \
         cudaFuncSetAttribute(k_lda_acc_docs<LG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_d);         \

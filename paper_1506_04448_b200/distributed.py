@@ -6,6 +6,10 @@ Where the path shards:
     (sketch.cpp:328-343); sketches are linear, so one all-reduce(sum) of the
     B x b complex data finishes the build;
   * factored / moment build — samples are split across ranks, same all-reduce;
+  * LDA whitened moment — documents are split across ranks; the per-document terms are
+    linear, the corpus-wide M1 and document count are all-reduced first (sums of the
+    shards' partials), each rank sketches its shard with those globals, and one
+    all-reduce of the B x b data completes sketch_whitened_m3 (lda.cpp:145-226);
   * RTPM — every rank holds the full sketch, the L restarts of a component are
     split across ranks; selection is an all-gather of (value, global tau) with the
     reference's strict '>' over ascending tau (decompose.cpp:105-109), the owner
@@ -196,3 +200,83 @@ def sharded_dense_build(sset, T, group=None, assume_symmetric: bool = True) -> N
         dist.all_reduce(view, group=group)
         torch.cuda.synchronize()
         sset.bump_version()
+
+
+def _allreduce_data(sset, group=None) -> None:
+    import torch
+    import torch.distributed as dist
+
+    ptr, nbytes = sset.data_device()
+    sset.ctx.synchronize()
+
+    class _CAI:
+        __cuda_array_interface__ = {"shape": (nbytes // 8,), "typestr": "<f8", "data": (ptr, False), "version": 3}
+
+    view = torch.as_tensor(_CAI(), device=torch.device("cuda", torch.cuda.current_device()))
+    dist.all_reduce(view, group=group)
+    torch.cuda.synchronize()
+    sset.bump_version()
+
+
+def sharded_moment(sset, X_local, w_local=None, group=None) -> None:
+    """accumulate_moment over the samples split across ranks (each passes its own rows
+    with globally normalised weights); one all-reduce of the data."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if world > 1 and rank != 0:
+        sset.set_data(None, np.zeros((sset.replicates(), sset.b()), dtype=np.complex128))
+    sset.accumulate_moment(X_local, w_local)
+    if world > 1:
+        _allreduce_data(sset, group)
+
+
+def lda_shard_globals(V: int, doc_ptr, word, count, group=None):
+    """Corpus-wide (documents with >= 3 tokens, averaged M1) from this rank's document
+    shard: local sums (lda.cpp:88-100) combined by one all-reduce. Returns
+    (global_used, global_m1, local_used1, local_used3)."""
+    import torch
+    import torch.distributed as dist
+
+    doc_ptr = np.asarray(doc_ptr, dtype=np.int64)
+    word = np.asarray(word, dtype=np.int64)
+    count = np.asarray(count, dtype=np.float64)
+    D = doc_ptr.size - 1
+    tot = np.add.reduceat(count, doc_ptr[:-1]) if word.size else np.zeros(D)
+    tot[doc_ptr[:-1] == doc_ptr[1:]] = 0.0
+    lens = np.diff(doc_ptr)
+    m1 = np.zeros(V)
+    doc_of = np.repeat(np.arange(D), lens)
+    ok = tot[doc_of] >= 1
+    np.add.at(m1, word[ok], count[ok] / tot[doc_of[ok]])
+    used1 = float(np.sum(tot >= 1))
+    used3 = float(np.sum(tot >= 3))
+    buf = torch.from_numpy(np.concatenate([m1, [used1, used3]]))
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(buf, group=group)
+    g = buf.numpy()
+    if g[V] <= 0:
+        raise ValueError("compute_m1: no nonempty documents")
+    return int(round(g[V + 1])), g[:V] / g[V], int(used1), int(used3)
+
+
+def sharded_sketch_whitened_m3(sset, V: int, doc_ptr, word, count, W, alpha0: float, group=None):
+    """sketch_whitened_m3 with the documents split across ranks (each passes its shard in
+    CSR form); returns the corpus-wide (used, skipped) StreamStats."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    g_used, g_m1, _, _ = lda_shard_globals(V, doc_ptr, word, count, group)
+    if world > 1 and rank != 0:
+        sset.set_data(None, np.zeros((sset.replicates(), sset.b()), dtype=np.complex128))
+    used, skipped = sset.sketch_whitened_m3_shard(V, doc_ptr, word, count, W, alpha0, g_used, g_m1, rank == 0)
+    if world > 1:
+        _allreduce_data(sset, group)
+    import torch
+
+    stats = torch.tensor([used, skipped], dtype=torch.int64)
+    if world > 1:
+        dist.all_reduce(stats, group=group)
+    return int(stats[0]), int(stats[1])

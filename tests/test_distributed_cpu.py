@@ -116,3 +116,50 @@ def test_gloo_world2_build_and_rtpm():
     assert np.array_equal(taus, bt_o)
     assert np.allclose(lam, lam_o, rtol=1e-12, atol=0)
     assert np.allclose(V, V_o, rtol=0, atol=1e-12)
+
+
+def _lda_worker(rank, world, port, out):
+    import torch.distributed as dist
+
+    from lda_fixtures import synthetic_corpus
+    from paper_1506_04448_b200.distributed import lda_shard_globals
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    V = 40
+    doc_ptr, word, count, _ = synthetic_corpus(V=V, k=4, D=90, mean_len=6, seed=3)
+    cut = 37
+    if rank == 0:
+        dp_, w_, c_ = doc_ptr[:cut + 1], word[:doc_ptr[cut]], count[:doc_ptr[cut]]
+    else:
+        dp_, w_, c_ = doc_ptr[cut:] - doc_ptr[cut], word[doc_ptr[cut]:], count[doc_ptr[cut]:]
+    g_used, g_m1, _, _ = lda_shard_globals(V, dp_, w_, c_)
+    if rank == 0:
+        out.put((g_used, g_m1))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_lda_shard_globals():
+    """Each rank passes its document shard; both see the corpus-wide document count and
+    averaged M1 (compute_m1, lda.cpp:88-100) of the whole corpus."""
+    from lda_fixtures import synthetic_corpus
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_lda_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    g_used, g_m1 = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    V = 40
+    doc_ptr, word, count, _ = synthetic_corpus(V=V, k=4, D=90, mean_len=6, seed=3)
+    m1 = O.lda_compute_m1(V, doc_ptr, word, count)
+    tot = np.array([count[doc_ptr[d]:doc_ptr[d + 1]].sum() for d in range(doc_ptr.size - 1)])
+    assert g_used == int(np.sum(tot >= 3))
+    assert np.max(np.abs(g_m1 - m1)) <= 1e-15

@@ -560,6 +560,35 @@ def test_lda_device_corpus_handle_matches_per_call_path(gpu_ctx):
     assert np.array_equal(s1.data(), s2.data())
 
 
+def test_lda_document_shards_sum_to_full_sketch(gpu_ctx):
+    """Multi-GPU decomposition of sketch_whitened_m3 (distributed.py), run shard by shard
+    on one GPU: the shards' sketches with corpus-wide normalisation and M1 sum to the
+    full sketch (one shard adds the c_m1 F(q)^3 term); a shard without usable documents
+    contributes only its vocabulary terms."""
+    from lda_fixtures import synthetic_corpus
+
+    from paper_1506_04448_b200.distributed import lda_shard_globals
+
+    V, k, alpha0 = 70, 6, 0.8
+    doc_ptr, word, count, W = synthetic_corpus(V=V, k=k, D=400, mean_len=12, seed=12)
+    full = skb().SymTensorSketchSet(k, 2048, 5, 21, gpu_ctx)
+    used, skipped = full.sketch_whitened_m3(V, doc_ptr, word, count, W, alpha0)
+    g_used, g_m1, _, _ = lda_shard_globals(V, doc_ptr, word, count)
+    assert g_used == used
+    cut = 173
+    shards = [(doc_ptr[:cut + 1], word[:doc_ptr[cut]], count[:doc_ptr[cut]]),
+              (doc_ptr[cut:] - doc_ptr[cut], word[doc_ptr[cut]:], count[doc_ptr[cut]:])]
+    total = np.zeros_like(full.data())
+    tot_used = 0
+    for r, (dp_, w_, c_) in enumerate(shards):
+        s = skb().SymTensorSketchSet(k, 2048, 5, 21, gpu_ctx)
+        u, _ = s.sketch_whitened_m3_shard(V, dp_, w_, c_, W, alpha0, g_used, g_m1, r == 0)
+        tot_used += u
+        total += s.data()
+    assert tot_used == used
+    assert rel_per_replicate(total, full.data()) <= 1e-11
+
+
 def test_lda_whiten_errors_follow_reference(gpu_ctx):
     from lda_fixtures import synthetic_corpus
 
