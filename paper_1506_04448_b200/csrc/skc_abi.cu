@@ -526,7 +526,9 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
         const char* e = std::getenv("SKC_BUILD_KERNEL");
         return e && std::string(e) == "rows";
     }();
-    p.flat = !row_variant;
+    // flat kernel's doubled SYM tables need bucket sums below bit 30: b <= 2^27 (larger
+    // sets take the row-walk kernel, which uses the plain packed form)
+    p.flat = !row_variant && (!sym || b <= (1u << 27));
     static const bool trace_on = std::getenv("SKC_BUILD_TRACE") != nullptr;
     DevBuf<unsigned long long> trace;
     p.trace = nullptr;

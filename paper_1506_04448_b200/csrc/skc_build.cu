@@ -494,12 +494,17 @@ __global__ void __launch_bounds__(1024, 1) k_build_flat(BuildArgs a) {
         const int m_lo = static_cast<int>(slot_lo / spr);
         const int R = static_cast<int>((slot_hi - 1) / spr) - m_lo + 1;
         for (int s = threadIdx.x; s < 2 * plane; s += NT) sacc[s] = 0u;
+        // SYM: tables in the doubled form 2h | e<<30 (from h | e<<30): the sum q of a row-pair
+        // word and a k word carries 2*(bucket sum) in bits 1.. and the exponent mod 4 in bits
+        // 30-31, so the slot 2*bucket + parity is one funnel of q and q >> 30 and the sign is
+        // q's sign bit (b <= 2^27 keeps the bucket carries below bit 30).
+        auto cv = [](std::uint32_t x) { return SYM ? (((x & 0x3FFFFFFFu) << 1) | (x & 0xC0000000u)) : x; };
         for (int x = threadIdx.x; x < RMAX * n; x += NT) {
             const int r = x / n, k = x - r * n;
             const std::uint32_t* pm = a.packed + (size_t)(m_lo + min(r, R - 1)) * prow;
-            ptab[x] = pm[(SYM ? 0 : 2 * n) + k];
-            pij_tab[r * 2 * n + k] = pm[k];
-            pij_tab[r * 2 * n + n + k] = pm[(SYM ? 0 : n) + k];
+            ptab[x] = cv(pm[(SYM ? 0 : 2 * n) + k]);
+            pij_tab[r * 2 * n + k] = cv(pm[k]);
+            pij_tab[r * 2 * n + n + k] = cv(pm[(SYM ? 0 : n) + k]);
         }
         __syncthreads();
         std::uint32_t base[RMAX];
@@ -507,6 +512,7 @@ __global__ void __launch_bounds__(1024, 1) k_build_flat(BuildArgs a) {
         for (int r = 0; r < RMAX; ++r) base[r] = pin(static_cast<std::uint32_t>((long long)(m_lo + r) * spr - slot_lo));
         const std::uint32_t nsl = pin(static_cast<std::uint32_t>(nslots));
         const std::uint32_t bmask = pin(a.bmask);
+        const std::uint32_t m1 = pin(2u * a.bmask);  // SYM: 2*bucket mask in the doubled form
         const std::uint32_t n4 = pin(4u * static_cast<std::uint32_t>(n));
         const std::uint32_t ptab_s = pin(sbase + 4u * static_cast<std::uint32_t>(2 * plane));
 
@@ -580,7 +586,7 @@ __global__ void __launch_bounds__(1024, 1) k_build_flat(BuildArgs a) {
                         for (int r = 0; r < RMAX; ++r) {
                             if (r < R) {  // CTA-uniform
                                 const std::uint32_t p = pij[r] + lds_u32(kaddr + static_cast<std::uint32_t>(r) * n4);
-                                const std::uint32_t s = base[r] + (SYM ? (((p & bmask) << 1) | ((p >> 30) & 1u)) : (p & bmask));
+                                const std::uint32_t s = base[r] + (SYM ? ((p & m1) | ((p >> 30) & ~m1)) : (p & bmask));
                                 const bool neg = static_cast<int>(p) < 0;
                                 add64_idx(s < nsl ? s : trash_idx, sbase, hioff, neg ? nql : ql, neg ? nqh : qh);
                             }
