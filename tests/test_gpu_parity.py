@@ -426,6 +426,31 @@ def test_lda_rejects_short_corpus(gpu_ctx):
         s.sketch_whitened_m3(5, [0, 1, 2], [0, 1], [1, 2], np.ones((5, 4)), 1.0)
 
 
+# ---------------------------------------------------------------- BASELINE config 1 at full size
+def test_config1_full_size_build_and_contractions_match_oracle(gpu_ctx):
+    """BASELINE config 1 exactly (n=400 fp64, rank 50 + 0.01 noise, b=2^14, B=20): the
+    full dense build from pinned host memory (the chunked zero-copy pipeline) and from
+    device memory, and T(I,u,u) / T(u,u,u) for a batch of restarts, against the oracle."""
+    import torch
+
+    n, b, B, seed = 400, 1 << 14, 20, 20150615
+    T, lam, V = skb().gen_planted_tensor(n, 50, 0.01, seed)
+    o = O.SymSet(n, b, B, seed)
+    o.accumulate_dense(T, True)
+    pinned = torch.from_numpy(T).pin_memory()
+    for src in (pinned.numpy(), pinned.cuda()):
+        s = skb().SymTensorSketchSet(n, b, B, seed, gpu_ctx)
+        s.accumulate_dense(src, assume_symmetric=True)
+        assert rel_per_replicate(s.data(), o.data()) <= SKETCH_TOL
+    ws = skb().SymContractionWorkspace(s)
+    U = skb().power_inits(7, n, 1, 6)[0]
+    iv = ws.Ivv(U)
+    for l in range(U.shape[0]):
+        ref = o.ivv(U[l])
+        assert np.max(np.abs(iv[l] - ref)) <= 1e-9 * np.max(np.abs(ref))
+        assert abs(ws.vvv(U[l]) - o.vvv(U[l])) <= 1e-9 * abs(o.vvv(U[l]))
+
+
 # ---------------------------------------------------------------- RTPM at BASELINE config 0, full size
 def test_rtpm_config0_full_size_matches_oracle_fixture(gpu_ctx):
     """BASELINE config 0 in full (n=100, b=2^12, B=20, k=10, L=50, T=30) against the
