@@ -553,16 +553,14 @@ __global__ void __launch_bounds__(1024, 1) k_build_flat(BuildArgs a) {
             std::uint32_t pij[RMAX];
 #pragma unroll
             for (int r = 0; r < RMAX; ++r) pij[r] = m_pij[r * kFlatRows];
-            long long qc[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) qc[u] = (lane + 32 * u < E) ? __ldg(qch + lane + 32 * u) : 0ll;
-            for (int eb = 0; eb < E; eb += 128) {
-                long long qn[4];
+            auto load4 = [&](long long (&q)[4], int eb) {
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const int e = eb + 128 + lane + 32 * u;
-                    qn[u] = (e < E) ? __ldg(qch + e) : 0ll;
+                    const int e = eb + lane + 32 * u;
+                    q[u] = (e < E) ? __ldg(qch + e) : 0ll;
                 }
+            };
+            auto process = [&](const long long (&qc)[4], int eb) {
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const int e = eb + lane + 32 * u;
@@ -593,8 +591,17 @@ __global__ void __launch_bounds__(1024, 1) k_build_flat(BuildArgs a) {
                         }
                     }
                 }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) qc[u] = qn[u];
+            };
+            // ping-pong over 128-entry blocks: the next block's loads are in flight while the
+            // current one is processed, with no register copies between iterations
+            long long qa[4], qb[4];
+            load4(qa, 0);
+            for (int eb = 0; eb < E; eb += 256) {
+                load4(qb, eb + 128);
+                process(qa, eb);
+                if (eb + 128 >= E) break;
+                load4(qa, eb + 256);
+                process(qb, eb + 128);
             }
             __syncwarp();  // metadata slice reused by the next chunk
             c0 = __shfl_sync(0xffffffffu, cn, 0);
