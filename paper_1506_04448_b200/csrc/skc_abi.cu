@@ -709,76 +709,6 @@ cublasHandle_t cublas_of(skc_context* ctx) {
     return ctx->cublas;
 }
 
-// Word-major transpose of a CSR corpus, stable (documents ascending within each word),
-// plus per-document token totals: a parallel counting sort over document blocks (per-
-// block word histograms, block-major offsets), deterministic for any thread count.
-struct CorpusT {
-    std::vector<long long> cptr, cdoc, total;
-    std::vector<int> ccount;
-};
-void corpus_transpose(int V, long long D, const long long* doc_ptr, const int* word, const int* count, CorpusT& c,
-                      const std::string& who, bool check_counts) {
-    const long long nnz = doc_ptr[D];
-    const int T = std::max(1, std::min(omp_get_max_threads(), static_cast<int>(std::max<long long>(D / 256, 1))));
-    std::vector<long long> blk(T + 1, 0);
-    for (int t = 1; t < T; ++t) {  // equal-nnz document blocks
-        const long long target = nnz * t / T;
-        blk[t] = std::lower_bound(doc_ptr, doc_ptr + D + 1, target) - doc_ptr;
-        blk[t] = std::min(std::max(blk[t], blk[t - 1]), D);
-    }
-    blk[T] = D;
-    std::vector<std::vector<long long>> hist(T, std::vector<long long>(static_cast<size_t>(V), 0));
-    c.total.assign(static_cast<size_t>(std::max<long long>(D, 1)), 0);
-    int bad_word = 0, bad_count = 0, bad_ptr = 0;
-#pragma omp parallel for num_threads(T) schedule(static, 1) reduction(| : bad_word, bad_count, bad_ptr)
-    for (int t = 0; t < T; ++t) {
-        auto& h = hist[t];
-        for (long long d = blk[t]; d < blk[t + 1]; ++d) {
-            if (doc_ptr[d + 1] < doc_ptr[d]) {
-                bad_ptr = 1;
-                continue;
-            }
-            long long tot = 0;
-            for (long long q = doc_ptr[d]; q < doc_ptr[d + 1]; ++q) {
-                const int w = word[q];
-                if (w < 0 || w >= V) {
-                    bad_word = 1;
-                    continue;
-                }
-                if (check_counts && count[q] < 0) bad_count = 1;
-                tot += count[q];
-                h[w]++;
-            }
-            c.total[d] = tot;
-        }
-    }
-    if (bad_ptr) fail(kInvalidArgument, who + ": doc_ptr must be non-decreasing");
-    if (bad_word) fail(kInvalidArgument, who + ": word id out of range");
-    if (bad_count) fail(kInvalidArgument, who + ": negative count");
-    c.cptr.assign(static_cast<size_t>(V) + 1, 0);
-    for (int w = 0; w < V; ++w) {
-        long long base = c.cptr[w];
-        for (int t = 0; t < T; ++t) {
-            const long long cnt = hist[t][w];
-            hist[t][w] = base;  // becomes block t's first slot for word w
-            base += cnt;
-        }
-        c.cptr[w + 1] = base;
-    }
-    c.cdoc.assign(static_cast<size_t>(std::max<long long>(nnz, 1)), 0);
-    c.ccount.assign(static_cast<size_t>(std::max<long long>(nnz, 1)), 0);
-#pragma omp parallel for num_threads(T) schedule(static, 1)
-    for (int t = 0; t < T; ++t) {
-        auto& pos = hist[t];
-        for (long long d = blk[t]; d < blk[t + 1]; ++d)
-            for (long long q = doc_ptr[d]; q < doc_ptr[d + 1]; ++q) {
-                const long long at = pos[word[q]]++;
-                c.cdoc[at] = d;
-                c.ccount[at] = count[q];
-            }
-    }
-}
-
 // Corpus on the device: CSR (document-major) and its word-major transpose, per-document
 // weights and per-word diagonal / M1 sums.
 struct CorpusDev {
@@ -804,45 +734,51 @@ void upload_corpus(skc_context* ctx, int V, long long D, const long long* doc_pt
         check_vec(word, (who + ": word").c_str());
         check_vec(count, (who + ": count").c_str());
     }
-    CorpusT ct;
-    corpus_transpose(V, D, doc_ptr, word, count, ct, who, check_counts);
-    std::vector<long long> used3;
-    for (long long d = 0; d < D; ++d) {
-        if (ct.total[d] >= 1) ++c.used1;
-        if (ct.total[d] >= 2) ++c.used2;
-        if (ct.total[d] >= 3) used3.push_back(d);
-    }
-    c.used3 = static_cast<long long>(used3.size());
-    c.used_docs.upload(used3.empty() ? doc_ptr : used3.data(), std::max<size_t>(used3.size(), 1), ctx->stream);
-    std::vector<long long>& cptr = ct.cptr;
-    std::vector<long long>& cdoc = ct.cdoc;
-    std::vector<int>& ccount = ct.ccount;
-    {
-        constexpr long long kWordChunk = 64;
-        std::vector<long long> lo, hi, wc(static_cast<size_t>(V) + 1, 0);
-        for (int w = 0; w < V; ++w) {
-            for (long long q = cptr[w]; q < cptr[w + 1]; q += kWordChunk) {
-                lo.push_back(q);
-                hi.push_back(std::min(q + kWordChunk, cptr[w + 1]));
-            }
-            wc[w + 1] = static_cast<long long>(lo.size());
-        }
-        c.nchunks = static_cast<long long>(lo.size());
-        c.chunk_lo.upload(lo.empty() ? wc.data() : lo.data(), std::max<size_t>(lo.size(), 1), ctx->stream);
-        c.chunk_hi.upload(hi.empty() ? wc.data() : hi.data(), std::max<size_t>(hi.size(), 1), ctx->stream);
-        c.word_chunk.upload(wc.data(), wc.size(), ctx->stream);
-    }
+    for (long long d = 0; d < D; ++d)  // O(D) host check keeps device reads in bounds
+        if (doc_ptr[d + 1] < doc_ptr[d]) fail(kInvalidArgument, who + ": doc_ptr must be non-decreasing");
+    // device-side validation, totals, stable word-major transpose, used-document list
+    // and word-pass chunks (corpus_gpu_build, skc_whiten.cu)
+    constexpr long long kWordChunk = 64;
+    const cudaStream_t st = ctx->stream;
+    const size_t nz = static_cast<size_t>(std::max<long long>(nnz, 1));
+    const size_t Dz = static_cast<size_t>(std::max<long long>(D, 1));
     c.V = V;
     c.D = D;
     c.nnz = nnz;
-    const cudaStream_t st = ctx->stream;
     c.doc_ptr.upload(doc_ptr, static_cast<size_t>(D) + 1, st);
     const int zero = 0;
-    c.word.upload(nnz > 0 ? word : &zero, static_cast<size_t>(std::max<long long>(nnz, 1)), st);
-    c.count.upload(nnz > 0 ? count : &zero, static_cast<size_t>(std::max<long long>(nnz, 1)), st);
-    c.cptr.upload(cptr.data(), cptr.size(), st);
-    c.cdoc.upload(cdoc.data(), cdoc.size(), st);
-    c.ccount.upload(ccount.data(), ccount.size(), st);
+    c.word.upload(nnz > 0 ? word : &zero, nz, st);
+    c.count.upload(nnz > 0 ? count : &zero, nz, st);
+    c.cptr.alloc(static_cast<size_t>(V) + 1);
+    c.cdoc.alloc(nz);
+    c.ccount.alloc(nz);
+    c.total.alloc(Dz);
+    c.used_docs.alloc(Dz);
+    c.word_chunk.alloc(static_cast<size_t>(V) + 1);
+    const size_t max_chunks = static_cast<size_t>(nnz / kWordChunk + V + 1);
+    c.chunk_lo.alloc(max_chunks);
+    c.chunk_hi.alloc(max_chunks);
+    DevBuf<unsigned long long> stats;
+    stats.alloc(8);
+    DevBuf<unsigned char> temp;
+    const size_t tb = corpus_gpu_temp_bytes(V, D, nnz);
+    temp.alloc(tb);
+    corpus_gpu_build(st, V, D, nnz, c.doc_ptr.p, c.word.p, c.count.p, check_counts, c.total.p, c.cptr.p, c.cdoc.p,
+                     c.ccount.p, c.used_docs.p, stats.p, kWordChunk, c.word_chunk.p, c.chunk_lo.p, c.chunk_hi.p,
+                     temp.p, tb);
+    ctx->check_launch();
+    unsigned long long hs[8];
+    CK(cudaMemcpyAsync(hs, stats.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    long long nchunks = 0;
+    CK(cudaMemcpyAsync(&nchunks, c.word_chunk.p + V, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    ctx->sync();
+    if (hs[0]) fail(kInvalidArgument, who + ": doc_ptr must be non-decreasing");
+    if (hs[1]) fail(kInvalidArgument, who + ": word id out of range");
+    if (hs[2]) fail(kInvalidArgument, who + ": negative count");
+    c.used1 = static_cast<long long>(hs[3]);
+    c.used2 = static_cast<long long>(hs[4]);
+    c.used3 = static_cast<long long>(hs[5]);
+    c.nchunks = nchunks;
     c.total.alloc(static_cast<size_t>(std::max<long long>(D, 1)));
     c.s2.alloc(static_cast<size_t>(std::max<long long>(D, 1)));
     c.invm.alloc(static_cast<size_t>(std::max<long long>(D, 1)));

@@ -120,6 +120,13 @@ void launch_m2_apply(cudaStream_t st, int V, long long D, int p, const long long
 void launch_scale_cols(cudaStream_t st, long long rows, int k, const double* in, const double* f, double* out);
 void launch_normalize_columns(cudaStream_t st, int n, int k, double* F, const double* prev, double* lambda);
 void launch_gaussian_fill(cudaStream_t st, unsigned long long seed, long long count, double* out);
+// device corpus preparation (skc_whiten.cu): stats[0..5] = bad doc_ptr, bad word, negative
+// count, docs >= 1 token, docs >= 2 tokens, docs >= 3 tokens
+size_t corpus_gpu_temp_bytes(int V, long long D, long long nnz);
+void corpus_gpu_build(cudaStream_t st, int V, long long D, long long nnz, const long long* doc_ptr, const int* word,
+                      const int* count, bool check_counts, long long* total, long long* cptr, long long* cdoc,
+                      int* ccount, long long* used_docs, unsigned long long* stats, long long chunk,
+                      long long* word_chunk, long long* chunk_lo, long long* chunk_hi, void* temp, size_t temp_bytes);
 
 // residue twiddle tables of a symmetric set (SymView::stw*/gtw*)
 void launch_sym_twiddle_tables(cudaStream_t st, const SymView& v, double2* stw1, double2* stw2, double2* gtw1,

@@ -21,6 +21,9 @@
 // Every sum runs in a fixed order, so the operator is deterministic.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cub/cub.cuh>
+
 #include "skc_host.hpp"
 #include "skc_internal.hpp"
 
@@ -261,6 +264,148 @@ void launch_m2_apply(cudaStream_t st, int V, long long D, int p, const long long
 void launch_scale_cols(cudaStream_t st, long long rows, int k, const double* in, const double* f, double* out) {
     k_scale_cols<<<cdiv_w(rows * k, 256), 256, 0, st>>>(rows, k, in, f, out);
     count_launch();
+}
+
+}  // namespace skc
+
+// ---- device corpus preparation (replaces the host transpose for large corpora) -------
+// Validation, per-document totals and the word histogram in one document pass; a stable
+// radix sort of (word, entry index) pairs gives the word-major transpose with documents
+// ascending inside each word (the order of the host counting sort), so every per-word sum
+// downstream runs in the same order as before. cub is used for the scan / sort / select
+// primitives of this setup step only.
+
+namespace skc {
+namespace {
+__global__ void k_corpus_docs_scan(long long D, int V, const long long* __restrict__ doc_ptr, const int* __restrict__ word,
+                                   const int* __restrict__ count, int check_counts, long long* __restrict__ total,
+                                   unsigned int* __restrict__ doc_of, unsigned long long* __restrict__ hist,
+                                   unsigned long long* __restrict__ stats, unsigned char* __restrict__ used3_flag) {
+    const long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (d >= D) return;
+    const long long q0 = doc_ptr[d], q1 = doc_ptr[d + 1];
+    if (q1 < q0) {
+        atomicAdd(&stats[0], 1ull);
+        total[d] = 0;
+        used3_flag[d] = 0;
+        return;
+    }
+    long long t = 0;
+    bool bw = false, bc = false;
+    for (long long q = q0; q < q1; ++q) {
+        const int w = word[q];
+        doc_of[q] = static_cast<unsigned int>(d);
+        if (w < 0 || w >= V) {
+            bw = true;
+            continue;
+        }
+        if (check_counts && count[q] < 0) bc = true;
+        t += count[q];
+        atomicAdd(&hist[w], 1ull);
+    }
+    if (bw) atomicAdd(&stats[1], 1ull);
+    if (bc) atomicAdd(&stats[2], 1ull);
+    total[d] = t;
+    if (t >= 1) atomicAdd(&stats[3], 1ull);
+    if (t >= 2) atomicAdd(&stats[4], 1ull);
+    used3_flag[d] = t >= 3;
+}
+__global__ void k_iota_u32(long long n, unsigned int* __restrict__ out) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < n) out[i] = static_cast<unsigned int>(i);
+}
+__global__ void k_corpus_gather(long long nnz, const unsigned int* __restrict__ order,
+                                const unsigned int* __restrict__ doc_of, const int* __restrict__ count,
+                                long long* __restrict__ cdoc, int* __restrict__ ccount) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= nnz) return;
+    const unsigned int q = order[i];
+    cdoc[i] = doc_of[q];
+    ccount[i] = count[q];
+}
+__global__ void k_word_nchunks(int V, const long long* __restrict__ cptr, long long chunk, long long* __restrict__ nch) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= V) return;
+    nch[w] = (cptr[w + 1] - cptr[w] + chunk - 1) / chunk;
+}
+__global__ void k_word_chunks(int V, const long long* __restrict__ cptr, const long long* __restrict__ wc, long long chunk,
+                              long long* __restrict__ lo, long long* __restrict__ hi) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= V) return;
+    long long k = wc[w];
+    for (long long q = cptr[w]; q < cptr[w + 1]; q += chunk, ++k) {
+        lo[k] = q;
+        hi[k] = min(q + chunk, cptr[w + 1]);
+    }
+}
+template <typename T>
+__global__ void k_cast_to_ll(long long n, const T* __restrict__ in, long long* __restrict__ out) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < n) out[i] = static_cast<long long>(in[i]);
+}
+}  // namespace
+
+// temp layout: [doc_of u32 nnz][order_in u32 nnz][keys_out u32 nnz][order_out u32 nnz]
+//              [hist u64 V+1][nch ll V+1][flags u8 D][cub temp]
+size_t corpus_gpu_temp_bytes(int V, long long D, long long nnz) {
+    size_t sort_b = 0, scan_b = 0, sel_b = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, sort_b, (const unsigned int*)nullptr, (unsigned int*)nullptr,
+                                    (const unsigned int*)nullptr, (unsigned int*)nullptr, static_cast<int>(std::max<long long>(nnz, 1)));
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_b, (const long long*)nullptr, (long long*)nullptr, V + 1);
+    cub::DeviceSelect::Flagged(nullptr, sel_b, cub::CountingInputIterator<long long>(0), (const unsigned char*)nullptr,
+                               (long long*)nullptr, (long long*)nullptr, static_cast<int>(std::max<long long>(D, 1)));
+    const size_t nz = static_cast<size_t>(std::max<long long>(nnz, 1));
+    // + 256-byte alignment slack for each of the 8 carved regions
+    return 16 * nz + 2 * 8 * (static_cast<size_t>(V) + 1) + static_cast<size_t>(std::max<long long>(D, 1)) +
+           std::max(sort_b, std::max(scan_b, sel_b)) + 8 * 256;
+}
+
+void corpus_gpu_build(cudaStream_t st, int V, long long D, long long nnz, const long long* doc_ptr, const int* word,
+                      const int* count, bool check_counts, long long* total, long long* cptr, long long* cdoc,
+                      int* ccount, long long* used_docs, unsigned long long* stats, long long chunk,
+                      long long* word_chunk, long long* chunk_lo, long long* chunk_hi, void* temp, size_t temp_bytes) {
+    const size_t nz = static_cast<size_t>(std::max<long long>(nnz, 1));
+    unsigned char* t = static_cast<unsigned char*>(temp);
+    auto carve = [&](size_t bytes) {
+        unsigned char* p = t;
+        t += (bytes + 255) / 256 * 256;
+        return p;
+    };
+    unsigned int* doc_of = reinterpret_cast<unsigned int*>(carve(4 * nz));
+    unsigned int* order_in = reinterpret_cast<unsigned int*>(carve(4 * nz));
+    unsigned int* keys_out = reinterpret_cast<unsigned int*>(carve(4 * nz));
+    unsigned int* order_out = reinterpret_cast<unsigned int*>(carve(4 * nz));
+    unsigned long long* hist = reinterpret_cast<unsigned long long*>(carve(8 * (static_cast<size_t>(V) + 1)));
+    long long* nch = reinterpret_cast<long long*>(carve(8 * (static_cast<size_t>(V) + 1)));
+    unsigned char* flags = carve(static_cast<size_t>(std::max<long long>(D, 1)));
+    void* cub_tmp = t;
+    size_t cub_b = temp_bytes - static_cast<size_t>(t - static_cast<unsigned char*>(temp));
+    cudaMemsetAsync(hist, 0, 8 * (static_cast<size_t>(V) + 1), st);
+    cudaMemsetAsync(stats, 0, 8 * 8, st);
+    if (D > 0)
+        k_corpus_docs_scan<<<cdiv_w(D, 256), 256, 0, st>>>(D, V, doc_ptr, word, count, check_counts ? 1 : 0, total,
+                                                            doc_of, hist, stats, flags);
+    // cptr = exclusive scan of the histogram (V + 1 entries, last = nnz of valid words)
+    k_cast_to_ll<unsigned long long><<<cdiv_w(V + 1, 256), 256, 0, st>>>(V + 1, hist, nch);
+    cub::DeviceScan::ExclusiveSum(cub_tmp, cub_b, nch, cptr, V + 1, st);
+    if (nnz > 0) {
+        // stable sort of entry indices by word: documents stay ascending within each word
+        k_iota_u32<<<cdiv_w(nnz, 256), 256, 0, st>>>(nnz, order_in);
+        int bits = 1;
+        while ((1ll << bits) < V) ++bits;
+        cub::DeviceRadixSort::SortPairs(cub_tmp, cub_b, reinterpret_cast<const unsigned int*>(word), keys_out, order_in,
+                                        order_out, static_cast<int>(nnz), 0, bits, st);
+        k_corpus_gather<<<cdiv_w(nnz, 256), 256, 0, st>>>(nnz, order_out, doc_of, count, cdoc, ccount);
+    }
+    // used-document list (>= 3 tokens), ascending
+    if (D > 0)
+        cub::DeviceSelect::Flagged(cub_tmp, cub_b, cub::CountingInputIterator<long long>(0), flags, used_docs,
+                                   reinterpret_cast<long long*>(&stats[5]), static_cast<int>(D), st);
+    // word-pass chunk lists
+    k_word_nchunks<<<cdiv_w(V, 256), 256, 0, st>>>(V, cptr, chunk, nch);
+    cub::DeviceScan::ExclusiveSum(cub_tmp, cub_b, nch, word_chunk, V + 1, st);
+    k_word_chunks<<<cdiv_w(V, 256), 256, 0, st>>>(V, cptr, word_chunk, chunk, chunk_lo, chunk_hi);
+    for (int i = 0; i < 8; ++i) count_launch();
 }
 
 }  // namespace skc
