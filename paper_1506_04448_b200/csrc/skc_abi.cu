@@ -1265,8 +1265,9 @@ void sketch_whitened_m3_dev(skc_sym_set* s, CorpusDev& c, const double* W, doubl
     ctx->use();
     const cudaStream_t st = ctx->stream;
     DevBuf<long long> d_total;
-    DevBuf<double> d_W, d_P, d_s1, d_s2, d_coeff1, d_sumwn, d_m1, d_q, d_acc, d_cross;
+    DevBuf<double> d_W, d_P, d_s1, d_s2, d_coeff1, d_sumwn, d_m1, d_q, d_acc, d_cross, d_vpart;
     d_W.upload(W, static_cast<size_t>(V) * k, st);
+    d_vpart.alloc(static_cast<size_t>(std::max<long long>(c.nchunks, 1)) * (k + 2));
     d_P.alloc(static_cast<size_t>(std::max<long long>(D, 1)) * k);
     d_s1.alloc(static_cast<size_t>(std::max<long long>(D, 1)));
     d_s2.alloc(static_cast<size_t>(std::max<long long>(D, 1)));
@@ -1281,8 +1282,8 @@ void sketch_whitened_m3_dev(skc_sym_set* s, CorpusDev& c, const double* W, doubl
     }
     {
         SKC_PROF(ctx, "lda_vocab");
-        launch_lda_vocab(st, k, V, c.cptr.p, c.cdoc.p, c.ccount.p, d_P.p, d_s1.p, d_total.p, d_coeff1.p, d_sumwn.p,
-                         d_m1.p);
+        launch_lda_vocab_chunked(st, k, V, c.nchunks, c.chunk_lo.p, c.chunk_hi.p, c.word_chunk.p, c.cdoc.p, c.ccount.p,
+                                 d_P.p, d_s1.p, d_total.p, d_vpart.p, d_coeff1.p, d_sumwn.p, d_m1.p);
     }
     if (shard) {
         d_m1.upload(global_m1, static_cast<size_t>(V), st);

@@ -176,6 +176,10 @@ void launch_add_third(cudaStream_t st, const double2* s3, std::uint32_t b, doubl
 // LDA whitened third moment (skc_lda.cu)
 void launch_lda_docs(cudaStream_t st, int k, long long D, const long long* doc_ptr, const int* word, const int* count,
                      const double* W, double alpha0, double* P, double* s1, double* s2, long long* total);
+void launch_lda_vocab_chunked(cudaStream_t st, int k, int V, long long nchunks, const long long* chunk_lo,
+                              const long long* chunk_hi, const long long* word_chunk, const long long* cdoc,
+                              const int* ccount, const double* P, const double* s1, const long long* total,
+                              double* part, double* coeff1, double* sumwn, double* m1_partial);
 void launch_lda_vocab(cudaStream_t st, int k, int V, const long long* cptr, const long long* cdoc, const int* ccount,
                       const double* P, const double* s1, const long long* total, double* coeff1, double* sumwn,
                       double* m1_partial);

@@ -124,6 +124,70 @@ __global__ void k_lda_vocab(int k, int V, const long long* __restrict__ cptr, co
     }
 }
 
+// Chunked vocabulary pass (load balance over Zipf-heavy words): a warp per <= 64-entry
+// chunk of a word's CSC range writes partial (sumwn[0..k), coeff1, m1); a warp per word
+// adds its chunks in order. Same sums as k_lda_vocab in a fixed chunked order.
+__global__ void k_lda_vocab_chunks(int k, long long nchunks, const long long* __restrict__ chunk_lo,
+                                   const long long* __restrict__ chunk_hi, const long long* __restrict__ cdoc,
+                                   const int* __restrict__ ccount, const double* __restrict__ P,
+                                   const double* __restrict__ s1, const long long* __restrict__ total,
+                                   double* __restrict__ part) {
+    const long long ck = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (ck >= nchunks) return;
+    const long long q0 = chunk_lo[ck], q1 = chunk_hi[ck];
+    double* o = part + (size_t)ck * (k + 2);
+    for (int a = lane; a < k; a += 32) {
+        double acc = 0.0;
+        for (long long q = q0; q < q1; ++q) {
+            const long long d = cdoc[q];
+            const double c = s1[d] * static_cast<double>(ccount[q]);
+            if (c != 0.0) acc += c * P[(size_t)d * k + a];
+        }
+        o[a] = acc;
+    }
+    if (lane == 0) {
+        double c1 = 0.0, m1 = 0.0;
+        for (long long q = q0; q < q1; ++q) {
+            const long long d = cdoc[q];
+            c1 += 2.0 * s1[d] * static_cast<double>(ccount[q]);                                       // lda.cpp:178
+            if (total[d] >= 1) m1 += (1.0 / static_cast<double>(total[d])) * static_cast<double>(ccount[q]);  // lda.cpp:94-95
+        }
+        o[k] = c1;
+        o[k + 1] = m1;
+    }
+}
+__global__ void k_lda_vocab_finish(int k, int V, const long long* __restrict__ word_chunk,
+                                   const double* __restrict__ part, double* __restrict__ coeff1,
+                                   double* __restrict__ sumwn, double* __restrict__ m1_partial) {
+    const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= V) return;
+    const long long c0 = word_chunk[w], c1e = word_chunk[w + 1];
+    for (int a = lane; a < k + 2; a += 32) {
+        double acc = 0.0;
+        for (long long ck = c0; ck < c1e; ++ck) acc += part[(size_t)ck * (k + 2) + a];
+        if (a < k)
+            sumwn[(size_t)w * k + a] = acc;
+        else if (a == k)
+            coeff1[w] = acc;
+        else
+            m1_partial[w] = acc;
+    }
+}
+void launch_lda_vocab_chunked(cudaStream_t st, int k, int V, long long nchunks, const long long* chunk_lo,
+                              const long long* chunk_hi, const long long* word_chunk, const long long* cdoc,
+                              const int* ccount, const double* P, const double* s1, const long long* total,
+                              double* part, double* coeff1, double* sumwn, double* m1_partial) {
+    if (nchunks > 0)
+        k_lda_vocab_chunks<<<cdiv_l(nchunks * 32, kThreads), kThreads, 0, st>>>(k, nchunks, chunk_lo, chunk_hi, cdoc,
+                                                                              ccount, P, s1, total, part);
+    k_lda_vocab_finish<<<cdiv_l((long long)V * 32, kThreads), kThreads, 0, st>>>(k, V, word_chunk, part, coeff1,
+                                                                                 sumwn, m1_partial);
+    count_launch();
+    count_launch();
+}
+
 // q[a] = sum_w W[w][a] * m1[w] / used1 (lda.cpp:188-189); one block per a, fixed order.
 __global__ void k_lda_q(int k, int V, const double* __restrict__ W, const double* __restrict__ m1_partial,
                         double inv_used1, double* __restrict__ q) {
