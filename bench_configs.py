@@ -160,7 +160,7 @@ def c3(skb, ctx, quick):
     gen_s = 0.0
     for start in range(0, N, blk):
         t0 = time.perf_counter()
-        gam = torch._standard_gamma(conc.expand(blk, K).contiguous())
+        gam = torch._standard_gamma(conc.expand(blk, K).contiguous(), generator=g)
         Wm = gam / gam.sum(dim=1, keepdim=True)
         X = Wm @ A.T + 0.1 * torch.randn(blk, n, generator=g, device="cuda", dtype=torch.float64)
         torch.cuda.synchronize()
