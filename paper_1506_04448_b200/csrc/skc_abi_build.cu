@@ -1,0 +1,255 @@
+// Dense sketch builds (sketch.cpp accumulate_dense): input staging and the
+// quantize / scatter / finalize orchestration of skc_build.cu.
+#include "skc_abi_impl.hpp"
+
+namespace skcabi {
+
+// ---- dense build orchestration ------------------------------------------------------
+// Device-visible view of the input tensor. Device pointers are used as is. Pinned
+// (page-locked, UVA-mapped) host memory is read in place by the quantize pass, so only
+// the bytes the build reads cross the bus. Pageable host memory is staged, copying only
+// the row blocks the build reads (sym: T[i][i:n][:], asym: T[i0:i1]) unless the full
+// tensor is needed by the symmetry check.
+const void* stage_tensor(skc_context* ctx, const void* T, int n, int dtype, int location, bool sym, int i0, int i1,
+                         bool need_full, size_t* h2d_bytes, bool* zero_copy) {
+    if (h2d_bytes) *h2d_bytes = 0;
+    if (zero_copy) *zero_copy = false;
+    if (location == SKC_DEVICE) return T;
+    const size_t es = dtype == SKC_F64 ? 8 : 4;
+    const size_t n2 = static_cast<size_t>(n) * n;
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, T) == cudaSuccess && attr.type == cudaMemoryTypeHost &&
+        attr.devicePointer != nullptr) {
+        if (zero_copy) *zero_copy = true;
+        return attr.devicePointer;
+    }
+    cudaGetLastError();  // clear a failed attribute query on pageable memory
+    ctx->tensor_stage.alloc(n2 * n * es);
+    unsigned char* dst = ctx->tensor_stage.p;
+    const unsigned char* src = static_cast<const unsigned char*>(T);
+    size_t moved = 0;
+    if (need_full) {
+        CK(cudaMemcpyAsync(dst, src, n2 * n * es, cudaMemcpyHostToDevice, ctx->stream));
+        moved = n2 * n * es;
+    } else if (sym) {
+        for (int i = i0; i < i1; ++i) {
+            const size_t off = (static_cast<size_t>(i) * n + i) * n * es, len = static_cast<size_t>(n - i) * n * es;
+            CK(cudaMemcpyAsync(dst + off, src + off, len, cudaMemcpyHostToDevice, ctx->stream));
+            moved += len;
+        }
+    } else {
+        const size_t off = static_cast<size_t>(i0) * n2 * es, len = static_cast<size_t>(i1 - i0) * n2 * es;
+        CK(cudaMemcpyAsync(dst + off, src + off, len, cudaMemcpyHostToDevice, ctx->stream));
+        moved = len;
+    }
+    if (h2d_bytes) *h2d_bytes = moved;
+    return dst;
+}
+
+void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool sym, int i0, int i1, int B,
+                     std::uint32_t b, const std::uint32_t* packed, double2* data, bool zero_copy) {
+    if (i0 >= i1) return;
+    skc_context::RowTab& rt = ctx->rowtab(n, i0, i1, sym);
+    if (rt.nrows == 0) return;
+    const long long total_slots = static_cast<long long>(B) * (sym ? 2ll * b : static_cast<long long>(b));
+    // slots per CTA limited by shared memory (limbs + per-replicate hash tables)
+    int G = 1;
+    for (;; ++G) {
+        long long spc = ((total_slots + G - 1) / G + 31) / 32 * 32;
+        const long long spr0 = sym ? 2ll * b : static_cast<long long>(b);
+        int Rg = 1;
+        for (int g = 0; g < G; ++g) {
+            const long long lo = g * spc, hi = std::min(lo + spc, total_slots);
+            if (hi > lo) Rg = std::max(Rg, static_cast<int>((hi - 1) / spr0 - lo / spr0 + 1));
+        }
+        if (Rg <= 16 && build_smem_bytes(spc, Rg, n) <= static_cast<size_t>(ctx->smem_optin - 1024)) break;
+        if (G > 4096) fail(kInvalidArgument, "accumulate_dense: sketch set too large for the dense build");
+    }
+    long long spc = (total_slots + G - 1) / G;
+    spc = (spc + 31) / 32 * 32;
+    if (const char* e = std::getenv("SKC_BUILD_SPC")) {  // experiment hook: forced window size
+        const long long f = std::atoll(e) / 32 * 32;
+        if (f >= 32 && f <= spc * 4 && build_smem_bytes(f, 16, n) <= static_cast<size_t>(ctx->smem_optin - 1024)) {
+            spc = f;
+            G = static_cast<int>((total_slots + spc - 1) / spc);
+        }
+    }
+    const long long spr = sym ? 2ll * b : static_cast<long long>(b);
+    int R = 1;
+    std::vector<int> Rg(G, 1);
+    for (int g = 0; g < G; ++g) {
+        const long long lo = g * spc, hi = std::min(lo + spc, total_slots);
+        if (hi > lo) Rg[g] = static_cast<int>((hi - 1) / spr - lo / spr + 1);
+        R = std::max(R, Rg[g]);
+    }
+    require(R <= 16, "accumulate_dense: slot range spans too many replicates");
+    const long long tot = rt.cum.back();
+    const int P = std::max(1, ctx->sms);  // one persistent CTA per SM, rows handed out dynamically
+    ctx->build_ints.alloc(static_cast<size_t>(G));
+    ctx->build_acc.alloc(static_cast<size_t>(total_slots));
+    ctx->qbuf.alloc(static_cast<size_t>(std::max<long long>(1, tot)));
+    ctx->rowF.alloc(static_cast<size_t>(rt.nrows));
+    ctx->prepass.alloc(kPrepassBlocks);
+    ctx->ints.alloc(16);
+
+    BuildPlan p;
+    p.n = n;
+    p.sym = sym;
+    p.dtype = dtype;
+    p.rowtab = rt.rows.p;
+    p.nrows = rt.nrows;
+    p.P = P;
+    p.G = G;
+    p.next_row = ctx->build_ints.p;
+    p.acc = ctx->build_acc.p;
+    static const bool row_variant = [] {
+        const char* e = std::getenv("SKC_BUILD_KERNEL");
+        return e && std::string(e) == "rows";
+    }();
+    // flat kernel's doubled SYM tables need bucket sums below bit 30: b <= 2^27 (larger
+    // sets take the row-walk kernel, which uses the plain packed form)
+    p.flat = !row_variant && (!sym || b <= (1u << 27));
+    static const bool trace_on = std::getenv("SKC_BUILD_TRACE") != nullptr;
+    DevBuf<unsigned long long> trace;
+    p.trace = nullptr;
+    if (trace_on) {
+        trace.alloc(3 * static_cast<size_t>(P));
+        p.trace = trace.p;
+    }
+    p.total_slots = total_slots;
+    p.slots_per_cta = static_cast<int>(spc);
+    p.R = R;
+    p.bmask = b - 1;
+    p.B = B;
+    p.packed = packed;
+    p.rowoff = rt.offs.p;
+    p.qbuf = ctx->qbuf.p;
+    p.rowF = ctx->rowF.p;
+    p.prepass_partials = ctx->prepass.p;
+    p.scale_exp = ctx->ints.p;
+    p.nonfinite = ctx->ints.p + 1;
+    p.data_as_double = reinterpret_cast<double*>(data);
+    // Zero-copy host input: the quantize pass is bus-bound, so the rows are cut into K
+    // chunks and chunk c+1 is read over PCIe (a few SMs, wide blocks) while the main pass
+    // of chunk c runs on the other SMs (second stream). Each chunk keeps its own exponent
+    // and exact accumulator; the finalize sums the K chunk sketches in order.
+    static const bool pipe_on = [] {
+        const char* e = std::getenv("SKC_BUILD_PIPELINE");  // "0": A/B switch for the chunked path
+        return !(e && std::string(e) == "0");
+    }();
+    const int K = (pipe_on && zero_copy && rt.nrows >= 4096 &&
+                   sizeof(double) * 32 * (size_t)n <= (size_t)ctx->smem_optin - 1024)
+                      ? env_int("SKC_BUILD_K", 4, 2, 4)
+                      : 1;
+    if (K > 1) {
+        const int qsms = env_int("SKC_BUILD_QSMS", 16, 1, 64);  // SMs given to the bus-bound quantize pass
+        p.P = std::max(1, ctx->sms - qsms);
+        p.prepass_threads = 1024;
+        p.prepass_blocks = qsms;
+        p.prepass_warps = 32;
+        ctx->build_acc.alloc(static_cast<size_t>(K) * total_slots);
+        ctx->build_ints.alloc(static_cast<size_t>(K) * G);
+        ctx->ints.alloc(16);
+        ctx->prepass.alloc(static_cast<size_t>(K) * qsms);
+        if (!ctx->stream2) CK(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
+        if (!ctx->ev_q[0])
+            for (int c = 0; c < 5; ++c) CK(cudaEventCreateWithFlags(&ctx->ev_q[c], cudaEventDisableTiming));
+        // decreasing chunk sizes: chunk c's main pass (~0.4x the bus time of its rows) hides
+        // under chunk c+1's bus reads, and the exposed tail (last main pass) stays short
+        static const double kFrac4[5] = {0.0, 0.42, 0.72, 0.90, 1.0};
+        std::vector<int> rb(K + 1, 0);
+        for (int c = 1; c < K; ++c) {
+            const long long target = (K == 4) ? static_cast<long long>(static_cast<double>(tot) * kFrac4[c]) : tot * c / K;
+            rb[c] = static_cast<int>(std::lower_bound(rt.cum.begin(), rt.cum.end(), target) - rt.cum.begin());
+            rb[c] = std::min(std::max(rb[c], rb[c - 1]), rt.nrows);
+        }
+        rb[K] = rt.nrows;
+        CK(cudaMemsetAsync(p.nonfinite, 0, sizeof(int), ctx->stream));
+        {
+            SKC_PROF(ctx, "build_pipelined");
+            static const bool ptrace = std::getenv("SKC_PIPE_TRACE") != nullptr;
+            cudaEvent_t te[4][5];
+            if (ptrace)
+                for (auto& row : te)
+                    for (auto& e : row) CK(cudaEventCreate(&e));
+            if (ptrace) CK(cudaEventRecord(te[0][0], ctx->stream));
+            for (int c = 0; c < K; ++c) {
+                BuildPlan pc = p;
+                pc.rowtab = rt.rows.p + rb[c];
+                pc.rowoff = rt.offs.p + rb[c];
+                pc.rowF = ctx->rowF.p + rb[c];
+                pc.nrows = rb[c + 1] - rb[c];
+                pc.prepass_partials = ctx->prepass.p + static_cast<size_t>(c) * qsms;
+                pc.scale_exp = ctx->ints.p + 4 + c;
+                pc.reset_nonfinite = false;
+                pc.acc = ctx->build_acc.p + static_cast<size_t>(c) * total_slots;
+                pc.next_row = ctx->build_ints.p + static_cast<size_t>(c) * G;
+                if (ptrace) CK(cudaEventRecord(te[0][c + 1 < 5 ? c + 1 : 4], ctx->stream));
+                if (pc.nrows > 0) launch_build_prepass(ctx->stream, Tdev, pc);
+                if (ptrace) CK(cudaEventRecord(te[1][c], ctx->stream));
+                CK(cudaEventRecord(ctx->ev_q[c], ctx->stream));
+                CK(cudaStreamWaitEvent(ctx->stream2, ctx->ev_q[c], 0));
+                if (pc.nrows > 0) {
+                    if (ptrace) CK(cudaEventRecord(te[2][c], ctx->stream2));
+                    launch_build_main(ctx->stream2, Tdev, pc);
+                    if (ptrace) CK(cudaEventRecord(te[3][c], ctx->stream2));
+                } else {
+                    CK(cudaMemsetAsync(pc.acc, 0, sizeof(unsigned long long) * (size_t)total_slots, ctx->stream2));
+                }
+            }
+            CK(cudaEventRecord(ctx->ev_q[K], ctx->stream2));
+            CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_q[K], 0));
+            BuildPlan pf = p;
+            pf.acc = ctx->build_acc.p;
+            launch_build_finalize_multi(ctx->stream, pf, K, ctx->ints.p + 4);
+            if (ptrace) {
+                ctx->sync();
+                for (int c = 0; c < K && c < 4; ++c) {
+                    float q0, q1, m0, m1;
+                    cudaEventElapsedTime(&q0, te[0][0], te[0][c + 1 < 5 ? c + 1 : 4]);
+                    cudaEventElapsedTime(&q1, te[0][0], te[1][c]);
+                    cudaEventElapsedTime(&m0, te[0][0], te[2][c]);
+                    cudaEventElapsedTime(&m1, te[0][0], te[3][c]);
+                    std::fprintf(stderr, "chunk %d quantize %.3f-%.3f ms main %.3f-%.3f ms\n", c, q0, q1, m0, m1);
+                }
+                for (auto& row : te)
+                    for (auto& e : row) cudaEventDestroy(e);
+            }
+        }
+        ctx->check_launch();
+    } else {
+        {
+            SKC_PROF(ctx, "build_prepass");
+            launch_build_prepass(ctx->stream, Tdev, p);
+        }
+        ctx->check_launch();
+        {
+            SKC_PROF(ctx, "build_main");
+            launch_build_main(ctx->stream, Tdev, p);
+        }
+        ctx->check_launch();
+        {
+            SKC_PROF(ctx, "build_finalize");
+            launch_build_finalize(ctx->stream, p);  // device-side no-op when nonfinite
+        }
+        ctx->check_launch();
+    }
+    int nonfinite = 0;
+    CK(cudaMemcpyAsync(&nonfinite, p.nonfinite, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    // Fixed-point accumulation cannot carry NaN/Inf the way the reference's
+    // floating-point sum would; reject instead of producing a wrong sketch.
+    if (nonfinite) fail(kInvalidArgument, "accumulate_dense: tensor has a non-finite entry");
+    if (trace_on) {
+        std::vector<unsigned long long> t(3 * static_cast<size_t>(P));
+        CK(cudaMemcpy(t.data(), trace.p, t.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        unsigned long long t0 = ~0ull;
+        for (int x = 0; x < P; ++x) t0 = std::min(t0, t[3 * x]);
+        std::fprintf(stderr, "build trace: G=%d spc=%lld P=%d\n", G, spc, P);
+        for (int x = 0; x < P; ++x)
+            std::fprintf(stderr, "cta %3d start %7.1f us dur %7.1f us switches %llu\n", x, (t[3 * x] - t0) * 1e-3,
+                         (t[3 * x + 1] - t[3 * x]) * 1e-3, t[3 * x + 2]);
+    }
+}
+
+}  // namespace skcabi

@@ -1,4 +1,4 @@
-// Internal interface between the C-ABI orchestration (skc_abi.cu) and the
+// Internal interface between the C-ABI orchestration (skc_abi*.cu) and the
 // kernels (skc_kernels.cu). Device pointers only; every launch goes on `st`.
 #pragma once
 
