@@ -456,7 +456,10 @@ int skc_sym_vvv(skc_sym_set* s, const double* U_host, int L, double* out_host) {
         ctx->U.upload(U_host, static_cast<size_t>(L) * s->n, ctx->stream);
         sym_contract_batch(s, ctx->U.p, L, 1);
         ctx->values.alloc(static_cast<size_t>(L));
-        launch_sym_vvv_finish(ctx->stream, ctx->part.p, L, s->B, s->S, s->b, ctx->values.p);
+        {
+            SKC_PROF(ctx, "vvv_finish");
+            launch_sym_vvv_finish(ctx->stream, ctx->part.p, L, s->B, s->S, s->b, ctx->values.p);
+        }
         ctx->check_launch();
         CK(cudaMemcpyAsync(out_host, ctx->values.p, static_cast<size_t>(L) * 8, cudaMemcpyDeviceToHost, ctx->stream));
         ctx->sync();

@@ -1,12 +1,14 @@
 """Full config-0 RTPM (n=100, b=2^12, B=20, k=10, L=50, T=30) on the GPU and in the
-oracle (host threads) with the same seeds; prints the component-wise differences."""
+oracle (host threads) with the same seeds; prints the component-wise differences.
+Test infrastructure: the oracle is the checker here (run from the repo root)."""
 import json
 import os
 import sys
 import time
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+_ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, _ROOT)
+sys.path.insert(0, os.path.join(_ROOT, "tests"))
 import numpy as np  # noqa: E402
 
 import oracle_py as O  # noqa: E402
