@@ -103,6 +103,18 @@ def traffic_from_profiles(kernel):
     return None
 
 
+def pcie_link(device):
+    """Current / max PCIe generation and width of the GPU's link (the e2e leg is bus-bound)."""
+    try:
+        out = subprocess.run(["nvidia-smi", "-i", str(device), "--query-gpu=pcie.link.gen.current,pcie.link.gen.max,"
+                              "pcie.link.width.current,pcie.link.width.max", "--format=csv,noheader,nounits"],
+                             capture_output=True, text=True, timeout=5)
+        g, gm, w, wm = [x.strip() for x in out.stdout.strip().split(",")]
+        return {"gen": g, "gen_max": gm, "width": w, "width_max": wm}
+    except Exception:
+        return None
+
+
 def contraction_roofline(per_s, n, b, B):
     """SURVEY 8(d) model of one median-of-B T(I,u,u): 4B length-b transforms at 5 b log2 b
     nominal flops each plus B(5n + 40b); shared memory moves 32b bytes per radix-2 pass
@@ -263,18 +275,23 @@ def run_b200(args):
 
     # ---- end-to-end through the public API: pinned host tensor in, sketch out ----------
     T_np_pinned = T_pinned.numpy()
+    for _ in range(max(args.warmup, 3)):  # warm the pinned (chunked pipeline) path too
+        step(T_np_pinned, host=True)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     e2e_ev = []
-    for k in range(max(1, min(args.steps, 5))):
+    for k in range(max(1, args.steps)):
         a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(ext)
         step(T_np_pinned, host=True)
         e.record(ext)
         e2e_ev.append((a, e))
     torch.cuda.synchronize()
-    e2e_ms = sum(a.elapsed_time(e) for a, e in e2e_ev) / len(e2e_ev)
+    pcie = pcie_link(local)  # right after the bus-bound loop (idle links downshift)
+    e2e_list = [a.elapsed_time(e) for a, e in e2e_ev]
+    e2e_ms = sum(e2e_list) / len(e2e_list)
+    e2e_med = statistics.median(e2e_list)
     if dist:
         t = torch.tensor([e2e_ms], device=f"cuda:{local}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -327,7 +344,7 @@ def run_b200(args):
         "e2e": {"value": n ** 3 / (e2e_ms * 1e-3), "unit": "entries/s",
                 # pinned input: the quantize pass reads the sorted-triple rows in place over the bus
                 "h2d_bytes_per_step": int(simplex_bytes_job), "d2h_bytes_per_step": int(B * b * 16),
-                "ms_per_step": e2e_ms,
+                "ms_per_step": e2e_ms, "ms_per_step_median": e2e_med, "pcie": pcie,
                 "path": "accumulate_dense(pinned host tensor) + replicate data readback into pinned host memory (public API)"},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "kernel": "k_build_flat",
