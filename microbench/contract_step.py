@@ -9,7 +9,7 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1506_04448_b200 as skb  # noqa: E402
 
-n, b, B, L = int(os.environ.get("N_", 400)), int(os.environ.get("B_", 1 << 14)), 20, 100
+n, b, B, L = int(os.environ.get("N_", 400)), int(os.environ.get("B_", 1 << 14)), 20, int(os.environ.get("L_", 100))
 ctx = skb.default_context(0)
 s = skb.SymTensorSketchSet(n, b, B, 5, ctx)
 rng = np.random.default_rng(0)
@@ -25,5 +25,5 @@ for _ in range(10):
     ws.Ivv(U)
 c, _ = ctx.profile_get("sym_contract")
 ctx.profile(False)
-print(json.dumps({"variant": os.environ.get("SKC_CONTRACT_VARIANT", "default"), "n": n, "b": b,
-                  "contract_ms_per_step": c / 10, "local_N": os.environ.get("SKC_LOCAL_N", "2048")}))
+print(json.dumps({"variant": os.environ.get("SKC_CONTRACT_VARIANT", "default"), "n": n, "b": b, "L": L,
+                  "contract_ms_per_step": c / 10, "us_per_restart": c / 10 / L * 1e3, "local_N": os.environ.get("SKC_LOCAL_N", "2048")}))

@@ -365,6 +365,26 @@ struct CorpusDev {
     DevBuf<long long> chunk_lo, chunk_hi, word_chunk;
 };
 
+// Sample/document chunks of the frequency-domain accumulation kernels (2 resident
+// 256-thread CTAs per SM, per_rep = B*S CTAs per chunk): at least ~4 waves, rounded up
+// to a chunk count whose grid fills its last wave to >= 99% (config 3: 14 chunks = 3.78
+// waves -> 22 = 5.95 waves; a 10-full-wave grid measured 6% faster than 14 chunks).
+// At most `cap` chunks (one sample or document per chunk).
+inline int wave_chunks(int sms, int per_rep, long long cap) {
+    const long long resident = 2ll * sms;
+    const long long c0 = std::max<long long>(1, (8ll * sms) / per_rep);
+    const long long w0 = (c0 * per_rep + resident - 1) / resident;
+    long long chunks = c0;
+    for (long long w = w0; w <= 4 * w0; ++w) {
+        const long long c = (w * resident) / per_rep;
+        if (c >= c0 && static_cast<double>(c * per_rep) >= 0.99 * static_cast<double>(w * resident)) {
+            chunks = c;
+            break;
+        }
+    }
+    return static_cast<int>(std::max<long long>(1, std::min<long long>(std::max<long long>(cap, 1), chunks)));
+}
+
 // ---- cross-unit helpers ----------------------------------------------------------------
 // skc_abi_build.cu
 const void* stage_tensor(skc_context* ctx, const void* T, int n, int dtype, int location, bool sym, int i0, int i1,

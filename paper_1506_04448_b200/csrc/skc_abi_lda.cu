@@ -312,7 +312,7 @@ void sketch_whitened_m3_dev(skc_sym_set* s, CorpusDev& c, const double* W, doubl
     ctx->check_launch();
     const int per_rep = s->B * s->S;
     // ~4 waves of 2 resident CTAs per SM for each of the two item kinds
-    const int chunks_d = std::max(1, static_cast<int>(std::min<long long>(std::max<long long>(used, 1), (8ll * ctx->sms) / per_rep)));
+    const int chunks_d = wave_chunks(ctx->sms, per_rep, used);
     const int chunks_v = std::max(1, static_cast<int>(std::min<long long>(V, (8ll * ctx->sms) / per_rep)));
     d_acc.alloc(static_cast<size_t>(chunks_d + chunks_v) * per_rep * s->N * 2);
     d_cross.alloc(static_cast<size_t>(chunks_d) * per_rep * s->N * 2);

@@ -219,8 +219,8 @@ int skc_sym_accumulate_dense(skc_sym_set* s, const void* T, int dtype, int locat
 static void sym_moment_device(skc_sym_set* s, const double* Xd, const double* wd, double alpha, long long Nsamp) {
     skc_context* ctx = s->ctx;
     const int per_rep = s->B * s->S;
-    // ~4 waves of 2 resident CTAs per SM; one sample per chunk at most
-    int chunks = static_cast<int>(std::max<long long>(1, std::min<long long>(Nsamp, (8ll * ctx->sms) / per_rep)));
+    int chunks = wave_chunks(ctx->sms, per_rep, Nsamp);
+    chunks = static_cast<int>(std::min<long long>(Nsamp, env_int("SKC_MOMENT_CHUNKS", chunks, 1, 1 << 16)));  // A/B hook
     ctx->freq_acc.alloc(static_cast<size_t>(chunks) * per_rep * s->N * 2);
     ctx->tmp.alloc(static_cast<size_t>(s->B) * s->b);
     SymView v = s->view();

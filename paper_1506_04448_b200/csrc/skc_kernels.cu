@@ -931,7 +931,7 @@ void launch_argmax_first(cudaStream_t st, const double* values, int L, int* best
 
 // ============================ K2: frequency-domain accumulation ===================
 // Symmetric moment / rank-1: acc += w * F(CS(x))^3 (sketch.cpp:353-358; lda.cpp:201-207).
-template <int LOGN, bool SCR>
+template <int LOGN, bool SCR, int LR>
 __global__ void __launch_bounds__(kFftThreads, SKC_FFT_MINB)
     k_sym_moment(SymView v, const double* __restrict__ X, const double* __restrict__ w, double wscale, long long Nsamp,
                  int chunks, double* __restrict__ acc) {
@@ -1007,7 +1007,7 @@ __global__ void __launch_bounds__(kFftThreads, SKC_FFT_MINB)
             scatter_plan(A, plan, n, N, r, bmask, 0x0FFFFFFFu, v.tw, vx);
         }
         __syncthreads();
-        dif_local<LOGN>(A, 1, v.twl);
+        dif_local<LOGN, LR>(A, 1, v.twl);
         const double ws = (w ? w[s] : 1.0) * wscale;
         for (int j = threadIdx.x; j < N; j += blockDim.x) {
             const double2 z = A[pad16(j)];
@@ -1020,24 +1020,38 @@ __global__ void __launch_bounds__(kFftThreads, SKC_FFT_MINB)
     double2* o = reinterpret_cast<double2*>(acc) + (((size_t)ch * B + m) * S + r) * N;
     for (int j = threadIdx.x; j < N; j += blockDim.x) o[j] = ACC[j];
 }
+// Max radix of the local DIF passes (A/B hook): 4 = radix-16 (make_plan), 3 = radix-8.
+static int env_lr(const char* name) {
+    const char* e = std::getenv(name);
+    return (e && std::atoi(e) == 3) ? 3 : 4;
+}
+template <int LR>
+static void moment_launch(cudaStream_t st, const SymView& v, const double* X, const double* w, double wscale,
+                          long long Nsamp, int chunks, double* acc, bool scr, size_t smem, unsigned grid) {
+#define L_(LG)                                                                                                         \
+    {                                                                                                                  \
+        if (scr) {                                                                                                     \
+            cudaFuncSetAttribute(k_sym_moment<LG, true, LR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
+            k_sym_moment<LG, true, LR><<<grid, kFftThreads, smem, st>>>(v, X, w, wscale, Nsamp, chunks, acc);          \
+        } else {                                                                                                       \
+            cudaFuncSetAttribute(k_sym_moment<LG, false, LR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+            k_sym_moment<LG, false, LR><<<grid, kFftThreads, smem, st>>>(v, X, w, wscale, Nsamp, chunks, acc);         \
+        }                                                                                                              \
+    }
+    SKC_LOGN_SWITCH(v.logN, L_)
+#undef L_
+}
 void launch_sym_moment_accumulate(cudaStream_t st, const SymView& v, const double* X, const double* w, double wscale,
                                   long long Nsamp, int chunks, double* acc) {
     const bool scr = v.n <= kScatterMax;
     const size_t smem = sizeof(double2) * (padded_len(v.N) + v.N + 8) +
                         (scr ? (sizeof(double2) + 2 * sizeof(std::uint32_t) + 2 * sizeof(double)) * (size_t)v.n + 8 : 0);
     const unsigned grid = (unsigned)((long long)chunks * v.B * v.S);
-#define L_(LG)                                                                                                     \
-    {                                                                                                              \
-        if (scr) {                                                                                                 \
-            cudaFuncSetAttribute(k_sym_moment<LG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
-            k_sym_moment<LG, true><<<grid, kFftThreads, smem, st>>>(v, X, w, wscale, Nsamp, chunks, acc);          \
-        } else {                                                                                                   \
-            cudaFuncSetAttribute(k_sym_moment<LG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-            k_sym_moment<LG, false><<<grid, kFftThreads, smem, st>>>(v, X, w, wscale, Nsamp, chunks, acc);         \
-        }                                                                                                          \
-    }
-    SKC_LOGN_SWITCH(v.logN, L_)
-#undef L_
+    static const int lr = env_lr("SKC_MOMENT_LR");
+    if (lr == 3)
+        moment_launch<3>(st, v, X, w, wscale, Nsamp, chunks, acc, scr, smem, grid);
+    else
+        moment_launch<4>(st, v, X, w, wscale, Nsamp, chunks, acc, scr, smem, grid);
     SKC_LAUNCHED();
     count_transforms((std::uint64_t)Nsamp * v.B * v.S, v.S);
 }
