@@ -74,6 +74,21 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
             G = static_cast<int>((total_slots + spc - 1) / spc);
         }
     }
+    // Symmetric sets take the class-list kernel when a (replicate, parity, bucket class)
+    // window fits: the fewest bucket-class bits t <= 3 whose window + tables fit.
+    static const int kernel_choice = [] {
+        const char* e = std::getenv("SKC_BUILD_KERNEL");  // "flat" / "rows": A/B switches
+        return (e && (std::string(e) == "flat" || std::string(e) == "rows")) ? 1 : 0;
+    }();
+    int cls_bits = -1;
+    if (sym && kernel_choice == 0 && b <= (1u << 22) && b >= 64) {
+        for (int t = 0; t <= 3; ++t)
+            if (cls_smem_bytes(b, t, n) <= static_cast<size_t>(ctx->smem_optin - 1024)) {
+                cls_bits = t;
+                break;
+            }
+    }
+    if (cls_bits >= 0) G = B * (2 << cls_bits);
     const long long spr = sym ? 2ll * b : static_cast<long long>(b);
     int R = 1;
     std::vector<int> Rg(G, 1);
@@ -109,6 +124,7 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
     // flat kernel's doubled SYM tables need bucket sums below bit 30: b <= 2^27 (larger
     // sets take the row-walk kernel, which uses the plain packed form)
     p.flat = !row_variant && (!sym || b <= (1u << 27));
+    p.cls_bits = cls_bits;
     static const bool trace_on = std::getenv("SKC_BUILD_TRACE") != nullptr;
     DevBuf<unsigned long long> trace;
     p.trace = nullptr;

@@ -636,6 +636,219 @@ __global__ void __launch_bounds__(1024, 1) k_build_flat(BuildArgs a) {
     }
 }
 
+// ---- class-list build (symmetric sets, default when a window fits) -----------------------
+// A window ("type") is one (replicate m, parity P, bucket residue r mod 2^TB) class of the
+// slot space: the b/2^TB buckets t = r (mod 2^TB) of replicate m in the real (P = 0) or
+// imaginary (P = 1) plane. The destination of entry (i, j, k) under replicate m has
+// bucket (c_ij + h_k) mod b and parity (e_ij + e_k) & 1, so for a fixed row (i, j) the
+// entries that land in the window are exactly those k in one class of the k index set:
+// e_k & 1 = P ^ (e_ij & 1) and h_k = r - c_ij (mod 2^TB). Each window keeps its k indices
+// grouped by class (stable, so ascending k within a class) with a suffix table giving the
+// first list position with k >= j. The rows' in-window entries are then one contiguous run
+// of the class list, gathered from the row in qbuf: every (entry, replicate) pair is
+// evaluated once, in the one window it lands in (no out-of-window evaluations, no trash
+// atomics), against ~2.2 evaluations per pair for the contiguous-slot windows above.
+constexpr int kClsRows = 16;
+__host__ __device__ constexpr int cls_meta_words() { return 4 * kClsRows + 4; }  // int4 per row (+ align)
+__host__ __device__ constexpr int cls_sfx_words(int C, int n) { return (C * (n + 1) + 1) / 2; }
+
+size_t cls_smem_bytes(std::uint32_t b, int tbits, int n) {
+    const int C = 2 << tbits;
+    const size_t W = static_cast<size_t>(b) >> tbits;
+    return sizeof(std::uint32_t) * (2 * W + 3 * (size_t)n + cls_sfx_words(C, n) + 4 + 32 * (size_t)cls_meta_words());
+}
+
+template <int TB>
+__global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
+    constexpr int NT = 1024, C = 2 << TB;
+    constexpr std::uint32_t tmask = (1u << TB) - 1u;
+    extern __shared__ __align__(16) std::uint32_t sm[];
+    __shared__ int s_next_g;
+    __shared__ int s_cend[C];
+    const int n = a.n, nrows = a.nrows;
+    const int W = static_cast<int>((a.bmask + 1u) >> TB);  // slots per plane
+    uint2* lst = reinterpret_cast<uint2*>(sm + 2 * W);   // n: (word, k) grouped by class
+    std::uint32_t* pw = reinterpret_cast<std::uint32_t*>(lst + n);  // n: h | e << 30
+    unsigned short* sfx = reinterpret_cast<unsigned short*>(pw + n);  // C x (n + 1)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // per-warp row metadata, one int4 per row: (end entry, list position - entry index,
+    // qbuf index - k relative to the chunk, c_ij | d << 24 | e_ij << 30)
+    int4* meta = reinterpret_cast<int4*>(
+        sm + ((static_cast<size_t>(2 * W + 3 * n + cls_sfx_words(C, n)) + 3) & ~static_cast<size_t>(3))) + warp * kClsRows;
+    const int F = *a.scale_exp;
+    std::uint32_t sbase = static_cast<std::uint32_t>(__cvta_generic_to_shared(sm));
+    asm volatile("mov.b32 %0, %0;" : "+r"(sbase));
+    const std::uint32_t hioff = pin(4u * static_cast<std::uint32_t>(W));
+    const std::uint32_t bmask = pin(a.bmask);
+    const std::uint32_t lst_s = pin(sbase + 8u * static_cast<std::uint32_t>(W));
+    unsigned long long t_start = 0, switches = 0;
+    if (a.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+
+    int g = static_cast<int>((static_cast<long long>(blockIdx.x) * a.G) / gridDim.x);
+    while (g >= 0) {
+        const int m = g / C, P = (g >> TB) & 1, r = g & static_cast<int>(tmask);
+        for (int s = threadIdx.x; s < 2 * W; s += NT) sm[s] = 0u;
+        for (int k = threadIdx.x; k < n; k += NT) pw[k] = a.packed[(size_t)m * n + k];
+        __syncthreads();
+        if (warp == 0) {  // stable class grouping of k and the suffix tables
+            auto cls_of = [&](std::uint32_t w) { return static_cast<int>((((w >> 30) & 1u) << TB) | (w & tmask)); };
+            int cnt = 0;  // lane c: size of class c
+            for (int base = 0; base < n; base += 32) {
+                const int k = base + lane;
+                const int c = k < n ? cls_of(pw[k]) : -1;
+#pragma unroll
+                for (int cc = 0; cc < C; ++cc) {
+                    const int pc = __popc(__ballot_sync(0xffffffffu, c == cc));
+                    if (lane == cc) cnt += pc;
+                }
+            }
+            int run = cnt;  // exclusive scan over the class lanes
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, run, o);
+                if (lane >= o) run += v;
+            }
+            run -= cnt;  // lane c: start of class c
+            if (lane < C) s_cend[lane] = run + cnt;
+            const std::uint32_t lt = (1u << lane) - 1u;
+            for (int base = 0; base < n; base += 32) {
+                const int k = base + lane;
+                const std::uint32_t w = k < n ? pw[k] : 0u;
+                const int c = k < n ? cls_of(w) : -1;
+#pragma unroll
+                for (int cc = 0; cc < C; ++cc) {
+                    const std::uint32_t mk = __ballot_sync(0xffffffffu, c == cc);
+                    const int rc = __shfl_sync(0xffffffffu, run, cc);
+                    const int pos = rc + __popc(mk & lt);
+                    if (k < n) sfx[cc * (n + 1) + k] = static_cast<unsigned short>(pos);
+                    if (c == cc) lst[pos] = make_uint2(w, static_cast<std::uint32_t>(k));
+                    if (lane == cc) run += __popc(mk);
+                }
+            }
+            if (lane < C) sfx[lane * (n + 1) + n] = static_cast<unsigned short>(run);
+        }
+        __syncthreads();
+
+        int c0 = 0;
+        if (lane == 0) c0 = atomicAdd(a.next_row + g, kClsRows);
+        c0 = __shfl_sync(0xffffffffu, c0, 0);
+        while (c0 < nrows) {
+            int cn = 0;  // next grab, one chunk ahead
+            if (lane == 0) cn = atomicAdd(a.next_row + g, kClsRows);
+            const int nr = min(kClsRows, nrows - c0);
+            long long off = 0;
+            int cnt = 0, pos0 = 0, j = 0;
+            std::uint32_t pwd = 0;
+            if (lane < nr) {
+                const int row = c0 + lane;
+                const std::uint32_t ij = __ldg(a.rowtab + row);
+                off = __ldg(a.rowoff + row);
+                const int i = static_cast<int>(ij >> 16);
+                j = static_cast<int>(ij & 0xFFFFu);
+                const std::uint32_t pij = pw[i] + pw[j];
+                const int cl = static_cast<int>(((((pij >> 30) & 1u) ^ static_cast<std::uint32_t>(P)) << TB) |
+                                                ((static_cast<std::uint32_t>(r) - pij) & tmask));
+                pos0 = sfx[cl * (n + 1) + j];
+                cnt = s_cend[cl] - pos0;
+                int d = static_cast<int>(__ldg(a.rowF + row)) - F;
+                d = d < 0 ? 0 : (d > 63 ? 63 : d);  // zero rows may sit below F; q >> 63 of |q| < 2^62 is 0 / -1
+                pwd = pij + (static_cast<std::uint32_t>(d) << 24);  // bucket sums < 3b <= 2^24 stay below bit 24
+            }
+            int incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            const long long off0 = __shfl_sync(0xffffffffu, off, 0);
+            const int E = __shfl_sync(0xffffffffu, incl, 31);
+            if (lane < nr) meta[lane] = make_int4(incl, pos0 - (incl - cnt), static_cast<int>(off - off0) - j, static_cast<int>(pwd));
+            __syncwarp();
+            const long long* qch = a.qbuf + off0;
+            int t = 0;
+            int4 cur = meta[0];
+            // load stage: list entry, gathered q and the packed word p = c_ij + h_k | d | e.
+            // Lanes past the chunk end get q = 0 and a private slot (their add is a no-op).
+            auto load4 = [&](long long (&q)[4], std::uint32_t (&p)[4], int eb) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int e = eb + lane + 32 * u;
+                    q[u] = 0;
+                    p[u] = static_cast<std::uint32_t>(lane);
+                    if (e < E) {
+                        while (e >= cur.x) cur = meta[++t];
+                        uint2 lw;
+                        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
+                                     : "=r"(lw.x), "=r"(lw.y)
+                                     : "r"(lst_s + 8u * static_cast<std::uint32_t>(e + cur.y)));
+                        q[u] = __ldg(qch + static_cast<std::uint32_t>(cur.z + static_cast<int>(lw.y)));
+                        p[u] = static_cast<std::uint32_t>(cur.w) + lw.x;
+                    }
+                }
+            };
+            auto process = [&](const long long (&q)[4], const std::uint32_t (&p)[4], int eb) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (eb + 32 * u >= E) break;  // warp-uniform
+                    const unsigned long long qq = static_cast<unsigned long long>(q[u] >> ((p[u] >> 24) & 63u));
+                    const bool neg = static_cast<int>(p[u]) < 0;
+                    const unsigned long long v = neg ? 0ull - qq : qq;
+                    const std::uint32_t s = (p[u] & bmask) >> TB;
+                    add64_idx(s, sbase, hioff, static_cast<std::uint32_t>(v), static_cast<std::uint32_t>(v >> 32));
+                }
+            };
+            long long qa[4], qb[4];
+            std::uint32_t pa[4], pb[4];
+            load4(qa, pa, 0);
+            for (int eb = 0; eb < E; eb += 256) {
+                load4(qb, pb, eb + 128);
+                process(qa, pa, eb);
+                if (eb + 128 >= E) break;
+                load4(qa, pa, eb + 256);
+                process(qb, pb, eb + 128);
+            }
+            __syncwarp();
+            c0 = __shfl_sync(0xffffffffu, cn, 0);
+        }
+        __syncthreads();
+        // flush: window slot s is bucket (s << TB) | r of replicate m, parity P
+        unsigned long long* out = a.acc + (long long)m * 2ll * (a.bmask + 1) + P;
+        for (int s = threadIdx.x; s < W; s += NT) {
+            const unsigned long long v = (static_cast<unsigned long long>(sm[W + s]) << 32) | sm[s];
+            if (v) atomicAdd(out + 2ll * ((static_cast<long long>(s) << TB) | r), v);
+        }
+        if (threadIdx.x == 0) {
+            int best = -1, left = 0;
+            for (int tt = 0; tt < a.G; ++tt) {
+                const int l = nrows - *((volatile int*)(a.next_row + tt));
+                if (l > left) {
+                    left = l;
+                    best = tt;
+                }
+            }
+            s_next_g = best;
+            ++switches;
+        }
+        __syncthreads();
+        g = s_next_g;
+    }
+    if (a.trace && threadIdx.x == 0) {
+        unsigned long long t_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        a.trace[3 * blockIdx.x] = t_start;
+        a.trace[3 * blockIdx.x + 1] = t_end;
+        a.trace[3 * blockIdx.x + 2] = switches;
+    }
+}
+
+template <int TB>
+static void cls_launch(cudaStream_t st, const BuildPlan& p, const BuildArgs& a) {
+    const size_t smem = cls_smem_bytes(p.bmask + 1u, TB, p.n);
+    cudaFuncSetAttribute(k_build_cls<TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_build_cls<TB><<<p.P, 1024, smem, st>>>(a);
+    count_launch();
+}
+
 // Threads per CTA: 1024 (32 warps, 64 registers) by default; SKC_BUILD_NT=512 trades
 // warps for registers (experiment hook).
 template <bool SYM, int RMAX>
@@ -700,7 +913,14 @@ void launch_build_main(cudaStream_t st, const void* T, const BuildPlan& p) {
     a.acc = p.acc;
 
     a.trace = p.trace;
-    if (p.sym)
+    if (p.sym && p.cls_bits >= 0) {
+        switch (p.cls_bits) {
+            case 0: cls_launch<0>(st, p, a); break;
+            case 1: cls_launch<1>(st, p, a); break;
+            case 2: cls_launch<2>(st, p, a); break;
+            default: cls_launch<3>(st, p, a); break;
+        }
+    } else if (p.sym)
         build_dispatch<true>(st, p, a);
     else
         build_dispatch<false>(st, p, a);

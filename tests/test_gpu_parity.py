@@ -81,6 +81,45 @@ def test_sym_dense_build_matches_oracle(gpu_ctx, n, b, B):
     assert s.version() == 1
 
 
+_KERNEL_AB = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_1506_04448_b200 as skb
+out = []
+for n, b, B, seed in [(40, 1024, 5, 1), (64, 4096, 20, 2), (36, 1 << 16, 3, 3), (17, 64, 4, 4), (120, 16384, 6, 5)]:
+    rng = np.random.default_rng(seed)
+    A = rng.normal(size=(n, n, n))
+    T = sum(A.transpose(p) for p in [(0, 1, 2), (0, 2, 1), (1, 0, 2), (1, 2, 0), (2, 0, 1), (2, 1, 0)]) / 6
+    s = skb.SymTensorSketchSet(n, b, B, seed)
+    s.accumulate_dense(T, assume_symmetric=True)
+    out.append(s.data())
+np.savez(sys.argv[2], *out)
+"""
+
+
+def test_sym_build_kernels_bit_identical(tmp_path):
+    """The class-list kernel (default) and the contiguous-window kernel both add the same
+    exact fixed-point values, so their sketches must agree bit for bit (b = 2^16 takes
+    the 2-bucket-bit class split)."""
+    import os
+    import subprocess
+    import sys
+
+    root = str(pathlib.Path(__file__).resolve().parents[1])
+    res = {}
+    for kern in ("cls", "flat"):
+        env = dict(os.environ)
+        env.pop("SKC_BUILD_KERNEL", None)
+        if kern == "flat":
+            env["SKC_BUILD_KERNEL"] = "flat"
+        f = tmp_path / f"{kern}.npz"
+        subprocess.run([sys.executable, "-c", _KERNEL_AB, root, str(f)], check=True, env=env)
+        z = np.load(f)
+        res[kern] = [z[k] for k in sorted(z.files, key=lambda x: int(x.split("_")[1]))]
+    for a, b in zip(res["cls"], res["flat"]):
+        assert np.array_equal(a, b)
+
+
 def test_sym_dense_build_is_deterministic(gpu_ctx):
     T = sym_tensor(48, 3)
     outs = []
