@@ -81,7 +81,11 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
         return (e && (std::string(e) == "flat" || std::string(e) == "rows")) ? 1 : 0;
     }();
     int cls_bits = -1;
-    if (sym && kernel_choice == 0 && b <= (1u << 22) && b >= 64) {
+    // (class lists pack k above the 3-term bucket sum: n <= 2^(28 - log2 b))
+    int logb = 0;
+    while ((1u << logb) < b) ++logb;
+    if (sym && kernel_choice == 0 && b <= (1u << 22) && b >= 64 && logb + 2 < 30 &&
+        static_cast<long long>(n - 1) < (1ll << (28 - logb))) {
         for (int t = 0; t <= 3; ++t)
             if (cls_smem_bytes(b, t, n) <= static_cast<size_t>(ctx->smem_optin - 1024)) {
                 cls_bits = t;

@@ -648,14 +648,14 @@ __global__ void __launch_bounds__(1024, 1) k_build_flat(BuildArgs a) {
 // of the class list, gathered from the row in qbuf: every (entry, replicate) pair is
 // evaluated once, in the one window it lands in (no out-of-window evaluations, no trash
 // atomics), against ~2.2 evaluations per pair for the contiguous-slot windows above.
-constexpr int kClsRows = 16;
+constexpr int kClsRows = 32;
 __host__ __device__ constexpr int cls_meta_words() { return 4 * kClsRows + 4; }  // int4 per row (+ align)
 __host__ __device__ constexpr int cls_sfx_words(int C, int n) { return (C * (n + 1) + 1) / 2; }
 
 size_t cls_smem_bytes(std::uint32_t b, int tbits, int n) {
     const int C = 2 << tbits;
     const size_t W = static_cast<size_t>(b) >> tbits;
-    return sizeof(std::uint32_t) * (2 * W + 3 * (size_t)n + cls_sfx_words(C, n) + 4 + 32 * (size_t)cls_meta_words());
+    return sizeof(std::uint32_t) * (2 * W + 2 * (size_t)n + cls_sfx_words(C, n) + 4 + 32 * (size_t)cls_meta_words());
 }
 
 template <int TB>
@@ -667,20 +667,25 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
     __shared__ int s_cend[C];
     const int n = a.n, nrows = a.nrows;
     const int W = static_cast<int>((a.bmask + 1u) >> TB);  // slots per plane
-    uint2* lst = reinterpret_cast<uint2*>(sm + 2 * W);   // n: (word, k) grouped by class
+    // n list words grouped by class: h_k | k << KS | e_k << 30 (KS = log2 b + 2 clears the
+    // 3-term bucket sum; the host checks that k fits below bit 30)
+    std::uint32_t* lst = sm + 2 * W;
     std::uint32_t* pw = reinterpret_cast<std::uint32_t*>(lst + n);  // n: h | e << 30
     unsigned short* sfx = reinterpret_cast<unsigned short*>(pw + n);  // C x (n + 1)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // per-warp row metadata, one int4 per row: (end entry, list position - entry index,
     // qbuf index - k relative to the chunk, c_ij | d << 24 | e_ij << 30)
     int4* meta = reinterpret_cast<int4*>(
-        sm + ((static_cast<size_t>(2 * W + 3 * n + cls_sfx_words(C, n)) + 3) & ~static_cast<size_t>(3))) + warp * kClsRows;
+        sm + ((static_cast<size_t>(2 * W + 2 * n + cls_sfx_words(C, n)) + 3) & ~static_cast<size_t>(3))) + warp * kClsRows;
     const int F = *a.scale_exp;
     std::uint32_t sbase = static_cast<std::uint32_t>(__cvta_generic_to_shared(sm));
     asm volatile("mov.b32 %0, %0;" : "+r"(sbase));
     const std::uint32_t hioff = pin(4u * static_cast<std::uint32_t>(W));
     const std::uint32_t bmask = pin(a.bmask);
     const std::uint32_t lst_s = pin(sbase + 8u * static_cast<std::uint32_t>(W));
+    const int KS = __popc(a.bmask) + 2;
+    const std::uint32_t kmask = pin((1u << (30 - KS)) - 1u);
+    const std::uint32_t wmask = pin(~(kmask << KS));
     unsigned long long t_start = 0, switches = 0;
     if (a.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 
@@ -721,7 +726,7 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
                     const int rc = __shfl_sync(0xffffffffu, run, cc);
                     const int pos = rc + __popc(mk & lt);
                     if (k < n) sfx[cc * (n + 1) + k] = static_cast<unsigned short>(pos);
-                    if (c == cc) lst[pos] = make_uint2(w, static_cast<std::uint32_t>(k));
+                    if (c == cc) lst[pos] = w | (static_cast<std::uint32_t>(k) << KS);
                     if (lane == cc) run += __popc(mk);
                 }
             }
@@ -765,24 +770,33 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
             if (lane < nr) meta[lane] = make_int4(incl, pos0 - (incl - cnt), static_cast<int>(off - off0) - j, static_cast<int>(pwd));
             __syncwarp();
             const long long* qch = a.qbuf + off0;
+            asm volatile("mov.b64 %0, %0;" : "+l"(qch));  // one IMAD.WIDE per gather address
             int t = 0;
             int4 cur = meta[0];
             // load stage: list entry, gathered q and the packed word p = c_ij + h_k | d | e.
             // Lanes past the chunk end get q = 0 and a private slot (their add is a no-op).
+            auto fetch = [&](long long& q, std::uint32_t& p, int e) {
+                if (e >= cur.x) {  // crossed into a later row of the chunk
+                    cur = meta[++t];
+                    while (e >= cur.x) cur = meta[++t];
+                }
+                const std::uint32_t lw = lds_u32(lst_s + 4u * static_cast<std::uint32_t>(e + cur.y));
+                q = __ldg(qch + static_cast<std::uint32_t>(cur.z + static_cast<int>((lw >> KS) & kmask)));
+                p = static_cast<std::uint32_t>(cur.w) + (lw & wmask);
+            };
+            // Full 128-entry blocks skip the per-entry bound checks; in the chunk's last
+            // block, lanes past the end get q = 0 and a private slot (a no-op add).
             auto load4 = [&](long long (&q)[4], std::uint32_t (&p)[4], int eb) {
+                if (eb + 128 <= E) {
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int e = eb + lane + 32 * u;
-                    q[u] = 0;
-                    p[u] = static_cast<std::uint32_t>(lane);
-                    if (e < E) {
-                        while (e >= cur.x) cur = meta[++t];
-                        uint2 lw;
-                        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
-                                     : "=r"(lw.x), "=r"(lw.y)
-                                     : "r"(lst_s + 8u * static_cast<std::uint32_t>(e + cur.y)));
-                        q[u] = __ldg(qch + static_cast<std::uint32_t>(cur.z + static_cast<int>(lw.y)));
-                        p[u] = static_cast<std::uint32_t>(cur.w) + lw.x;
+                    for (int u = 0; u < 4; ++u) fetch(q[u], p[u], eb + lane + 32 * u);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int e = eb + lane + 32 * u;
+                        q[u] = 0;
+                        p[u] = static_cast<std::uint32_t>(lane);
+                        if (e < E) fetch(q[u], p[u], e);
                     }
                 }
             };
