@@ -72,6 +72,28 @@ __global__ void __launch_bounds__(NTQ) k_build_quantize(const TT* __restrict__ T
     double* st = stage + (size_t)warp * n;
     double blk = 0.0;
     bool bad = false;
+    // 16-byte path: the first 128-pair block of the warp's next row is loaded before the
+    // current row's reduction and stores, so each warp keeps a row's reads in flight.
+    const bool v16 = sizeof(TT) == 8 && vec16;
+    auto row_geom = [&](int r, const double2*& tp, int& npair, int& off) {
+        const std::uint32_t ijr = rowtab[r];
+        const int ir = static_cast<int>(ijr >> 16), jr = static_cast<int>(ijr & 0xFFFFu);
+        const int k0r = SYM ? jr : 0;
+        const size_t e0 = ((size_t)ir * n + jr) * n + k0r;
+        const size_t ea = e0 & ~(size_t)1;
+        npair = static_cast<int>((e0 + (n - k0r) - ea + 1) >> 1);
+        tp = reinterpret_cast<const double2*>(T) + (ea >> 1);
+        off = static_cast<int>(e0 - ea);
+    };
+    auto load_first = [&](int r, double2 (&v)[4]) {
+        const double2* tp;
+        int npair, off;
+        row_geom(r, tp, npair, off);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = (lane + 32 * u < npair) ? tp[lane + 32 * u] : make_double2(0.0, 0.0);
+    };
+    double2 pv[4];
+    if (v16 && blockIdx.x * W + warp < nrows) load_first(blockIdx.x * W + warp, pv);
     for (int row = blockIdx.x * W + warp; row < nrows; row += gridDim.x * W) {
         const std::uint32_t ij = rowtab[row];
         const int i = static_cast<int>(ij >> 16), j = static_cast<int>(ij & 0xFFFFu);
@@ -80,19 +102,22 @@ __global__ void __launch_bounds__(NTQ) k_build_quantize(const TT* __restrict__ T
         const double kdiag = SYM ? ((i == j) ? 1.0 : 3.0) : 1.0;
         const double koff = SYM ? ((i == j) ? 3.0 : 6.0) : 1.0;
         double a0 = 0.0;
-        if (sizeof(TT) == 8 && vec16) {
+        if (v16) {
             // 16-byte loads from a 16-byte aligned base covering the row segment: T may be
             // pinned host memory read in place over PCIe, where wider requests carry less
             // header overhead per byte. 4 pair-loads in flight per lane.
-            const size_t e0 = ((size_t)i * n + j) * n + k0;  // element index of (i, j, k0)
-            const size_t ea = e0 & ~(size_t)1;
-            const int npair = static_cast<int>((e0 + (n - k0) - ea + 1) >> 1);
-            const double2* tp = reinterpret_cast<const double2*>(T) + (ea >> 1);
-            const int off = static_cast<int>(e0 - ea);  // 0 or 1: leading element to skip
-            for (int pb = lane; pb < npair; pb += 128) {
-                double2 v[4];
+            const double2* tp;
+            int npair, off;  // off 0 or 1: leading element to skip
+            row_geom(row, tp, npair, off);
+            double2 v[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) v[u] = (pb + 32 * u < npair) ? tp[pb + 32 * u] : make_double2(0.0, 0.0);
+            for (int u = 0; u < 4; ++u) v[u] = pv[u];
+            if (row + gridDim.x * W < nrows) load_first(row + gridDim.x * W, pv);
+            for (int pb = lane; pb < npair; pb += 128) {
+                if (pb != lane) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) v[u] = (pb + 32 * u < npair) ? tp[pb + 32 * u] : make_double2(0.0, 0.0);
+                }
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const int q = 2 * (pb + 32 * u) - off;  // row-relative index of v[u].x
