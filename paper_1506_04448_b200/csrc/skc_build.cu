@@ -677,15 +677,15 @@ constexpr int kClsRows = 32;
 __host__ __device__ constexpr int cls_meta_words() { return 4 * kClsRows + 4; }  // int4 per row (+ align)
 __host__ __device__ constexpr int cls_sfx_words(int C, int n) { return (C * (n + 1) + 1) / 2; }
 
-size_t cls_smem_bytes(std::uint32_t b, int tbits, int n) {
-    const int C = 2 << tbits;
+size_t cls_smem_bytes(std::uint32_t b, int tbits, int n, bool sym) {
+    const int C = (sym ? 2 : 1) << tbits;
     const size_t W = static_cast<size_t>(b) >> tbits;
-    return sizeof(std::uint32_t) * (2 * W + 2 * (size_t)n + cls_sfx_words(C, n) + 4 + 32 * (size_t)cls_meta_words());
+    return sizeof(std::uint32_t) * (2 * W + 3 * (size_t)n + cls_sfx_words(C, n) + 4 + 32 * (size_t)cls_meta_words());
 }
 
-template <int TB>
+template <bool SYM, int TB>
 __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
-    constexpr int NT = 1024, C = 2 << TB;
+    constexpr int NT = 1024, C = (SYM ? 2 : 1) << TB;
     constexpr std::uint32_t tmask = (1u << TB) - 1u;
     extern __shared__ __align__(16) std::uint32_t sm[];
     __shared__ int s_next_g;
@@ -695,13 +695,13 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
     // n list words grouped by class: h_k | k << KS | e_k << 30 (KS = log2 b + 2 clears the
     // 3-term bucket sum; the host checks that k fits below bit 30)
     std::uint32_t* lst = sm + 2 * W;
-    std::uint32_t* pw = reinterpret_cast<std::uint32_t*>(lst + n);  // n: h | e << 30
-    unsigned short* sfx = reinterpret_cast<unsigned short*>(pw + n);  // C x (n + 1)
+    std::uint32_t* pw = reinterpret_cast<std::uint32_t*>(lst + n);  // sym n: h | e << 30; asym 2n: modes 1, 2
+    unsigned short* sfx = reinterpret_cast<unsigned short*>(pw + 2 * n);  // C x (n + 1)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // per-warp row metadata, one int4 per row: (end entry, list position - entry index,
     // qbuf index - k relative to the chunk, c_ij | d << 24 | e_ij << 30)
     int4* meta = reinterpret_cast<int4*>(
-        sm + ((static_cast<size_t>(2 * W + 2 * n + cls_sfx_words(C, n)) + 3) & ~static_cast<size_t>(3))) + warp * kClsRows;
+        sm + ((static_cast<size_t>(2 * W + 3 * n + cls_sfx_words(C, n)) + 3) & ~static_cast<size_t>(3))) + warp * kClsRows;
     const int F = *a.scale_exp;
     std::uint32_t sbase = static_cast<std::uint32_t>(__cvta_generic_to_shared(sm));
     asm volatile("mov.b32 %0, %0;" : "+r"(sbase));
@@ -716,16 +716,21 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
 
     int g = static_cast<int>((static_cast<long long>(blockIdx.x) * a.G) / gridDim.x);
     while (g >= 0) {
-        const int m = g / C, P = (g >> TB) & 1, r = g & static_cast<int>(tmask);
+        const int m = g / C, P = SYM ? (g >> TB) & 1 : 0, r = g & static_cast<int>(tmask);
         for (int s = threadIdx.x; s < 2 * W; s += NT) sm[s] = 0u;
-        for (int k = threadIdx.x; k < n; k += NT) pw[k] = a.packed[(size_t)m * n + k];
+        // asym packed words are h | neg << 31 for modes 1..3 (B x 3 x n): the list holds
+        // mode 3, the row pair word is mode 1 (i) + mode 2 (j); bit 31 of a sum is the sign
+        for (int k = threadIdx.x; k < (SYM ? n : 2 * n); k += NT) pw[k] = a.packed[(size_t)m * (SYM ? n : 3 * n) + k];
         __syncthreads();
+        const std::uint32_t* lw_src = SYM ? pw : a.packed + (size_t)m * 3 * n + 2 * n;
         if (warp == 0) {  // stable class grouping of k and the suffix tables
-            auto cls_of = [&](std::uint32_t w) { return static_cast<int>((((w >> 30) & 1u) << TB) | (w & tmask)); };
+            auto cls_of = [&](std::uint32_t w) {
+                return static_cast<int>(SYM ? ((((w >> 30) & 1u) << TB) | (w & tmask)) : (w & tmask));
+            };
             int cnt = 0;  // lane c: size of class c
             for (int base = 0; base < n; base += 32) {
                 const int k = base + lane;
-                const int c = k < n ? cls_of(pw[k]) : -1;
+                const int c = k < n ? cls_of(lw_src[k]) : -1;
 #pragma unroll
                 for (int cc = 0; cc < C; ++cc) {
                     const int pc = __popc(__ballot_sync(0xffffffffu, c == cc));
@@ -743,7 +748,7 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
             const std::uint32_t lt = (1u << lane) - 1u;
             for (int base = 0; base < n; base += 32) {
                 const int k = base + lane;
-                const std::uint32_t w = k < n ? pw[k] : 0u;
+                const std::uint32_t w = k < n ? lw_src[k] : 0u;
                 const int c = k < n ? cls_of(w) : -1;
 #pragma unroll
                 for (int cc = 0; cc < C; ++cc) {
@@ -775,10 +780,11 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
                 off = __ldg(a.rowoff + row);
                 const int i = static_cast<int>(ij >> 16);
                 j = static_cast<int>(ij & 0xFFFFu);
-                const std::uint32_t pij = pw[i] + pw[j];
-                const int cl = static_cast<int>(((((pij >> 30) & 1u) ^ static_cast<std::uint32_t>(P)) << TB) |
-                                                ((static_cast<std::uint32_t>(r) - pij) & tmask));
-                pos0 = sfx[cl * (n + 1) + j];
+                const std::uint32_t pij = pw[i] + pw[(SYM ? 0 : n) + j];
+                const int cl = SYM ? static_cast<int>(((((pij >> 30) & 1u) ^ static_cast<std::uint32_t>(P)) << TB) |
+                                                      ((static_cast<std::uint32_t>(r) - pij) & tmask))
+                                   : static_cast<int>((static_cast<std::uint32_t>(r) - pij) & tmask);
+                pos0 = sfx[cl * (n + 1) + (SYM ? j : 0)];
                 cnt = s_cend[cl] - pos0;
                 int d = static_cast<int>(__ldg(a.rowF + row)) - F;
                 d = d < 0 ? 0 : (d > 63 ? 63 : d);  // zero rows may sit below F; q >> 63 of |q| < 2^62 is 0 / -1
@@ -792,7 +798,8 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
             }
             const long long off0 = __shfl_sync(0xffffffffu, off, 0);
             const int E = __shfl_sync(0xffffffffu, incl, 31);
-            if (lane < nr) meta[lane] = make_int4(incl, pos0 - (incl - cnt), static_cast<int>(off - off0) - j, static_cast<int>(pwd));
+            if (lane < nr)
+                meta[lane] = make_int4(incl, pos0 - (incl - cnt), static_cast<int>(off - off0) - (SYM ? j : 0), static_cast<int>(pwd));
             __syncwarp();
             const long long* qch = a.qbuf + off0;
             asm volatile("mov.b64 %0, %0;" : "+l"(qch));  // one IMAD.WIDE per gather address
@@ -851,10 +858,10 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
         }
         __syncthreads();
         // flush: window slot s is bucket (s << TB) | r of replicate m, parity P
-        unsigned long long* out = a.acc + (long long)m * 2ll * (a.bmask + 1) + P;
+        unsigned long long* out = a.acc + (long long)m * (SYM ? 2ll : 1ll) * (a.bmask + 1) + P;
         for (int s = threadIdx.x; s < W; s += NT) {
             const unsigned long long v = (static_cast<unsigned long long>(sm[W + s]) << 32) | sm[s];
-            if (v) atomicAdd(out + 2ll * ((static_cast<long long>(s) << TB) | r), v);
+            if (v) atomicAdd(out + (SYM ? 2ll : 1ll) * ((static_cast<long long>(s) << TB) | r), v);
         }
         if (threadIdx.x == 0) {
             int best = -1, left = 0;
@@ -882,9 +889,14 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
 
 template <int TB>
 static void cls_launch(cudaStream_t st, const BuildPlan& p, const BuildArgs& a) {
-    const size_t smem = cls_smem_bytes(p.bmask + 1u, TB, p.n);
-    cudaFuncSetAttribute(k_build_cls<TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_build_cls<TB><<<p.P, 1024, smem, st>>>(a);
+    const size_t smem = cls_smem_bytes(p.bmask + 1u, TB, p.n, p.sym);
+    if (p.sym) {
+        cudaFuncSetAttribute(k_build_cls<true, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_build_cls<true, TB><<<p.P, 1024, smem, st>>>(a);
+    } else {
+        cudaFuncSetAttribute(k_build_cls<false, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_build_cls<false, TB><<<p.P, 1024, smem, st>>>(a);
+    }
     count_launch();
 }
 
@@ -952,7 +964,7 @@ void launch_build_main(cudaStream_t st, const void* T, const BuildPlan& p) {
     a.acc = p.acc;
 
     a.trace = p.trace;
-    if (p.sym && p.cls_bits >= 0) {
+    if (p.cls_bits >= 0) {
         switch (p.cls_bits) {
             case 0: cls_launch<0>(st, p, a); break;
             case 1: cls_launch<1>(st, p, a); break;

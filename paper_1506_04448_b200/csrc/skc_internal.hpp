@@ -83,7 +83,7 @@ struct BuildPlan {
     int P, G;
     int* next_row;               // G counters
     bool flat;                   // flat-chunk kernel or the row-walk kernel
-    int cls_bits = -1;           // >= 0: class-list kernel, windows = (replicate, parity, bucket mod 2^cls_bits)
+    int cls_bits = -1;           // >= 0: class-list kernel, windows = (replicate, [parity,] bucket mod 2^cls_bits)
     unsigned long long* acc;     // total_slots exact fixed-point accumulators
     unsigned long long* trace;   // optional per-CTA (start, end, switches) (SKC_BUILD_TRACE)
     long long total_slots;   // B x 2b (sym) or B x b (asym)
@@ -104,7 +104,7 @@ struct BuildPlan {
 };
 constexpr int kPrepassBlocks = 1024;
 size_t build_smem_bytes(long long slots_per_cta, int R, int n);
-size_t cls_smem_bytes(std::uint32_t b, int tbits, int n);
+size_t cls_smem_bytes(std::uint32_t b, int tbits, int n, bool sym);
 void launch_build_prepass(cudaStream_t st, const void* T, const BuildPlan& p);
 void launch_build_main(cudaStream_t st, const void* T, const BuildPlan& p);
 void launch_build_finalize(cudaStream_t st, const BuildPlan& p);

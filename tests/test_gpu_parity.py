@@ -93,14 +93,17 @@ for n, b, B, seed in [(40, 1024, 5, 1), (64, 4096, 20, 2), (36, 1 << 16, 3, 3), 
     s = skb.SymTensorSketchSet(n, b, B, seed)
     s.accumulate_dense(T, assume_symmetric=True)
     out.append(s.data())
+    a = skb.AsymTensorSketchSet(n, b, B, seed)
+    a.accumulate_dense(A)
+    out.append(a.data())
 np.savez(sys.argv[2], *out)
 """
 
 
 def test_sym_build_kernels_bit_identical(tmp_path):
     """The class-list kernel (default) and the contiguous-window kernel both add the same
-    exact fixed-point values, so their sketches must agree bit for bit (b = 2^16 takes
-    the 2-bucket-bit class split)."""
+    exact fixed-point values, so their sketches must agree bit for bit, symmetric and
+    asymmetric (b = 2^16 takes the bucket-class split)."""
     import os
     import subprocess
     import sys
