@@ -347,10 +347,10 @@ def run_b200(args):
                 "ms_per_step": e2e_ms, "ms_per_step_median": e2e_med, "pcie": pcie,
                 "path": "accumulate_dense(pinned host tensor) + replicate data readback into pinned host memory (public API)"},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "hbm", "kernel": "k_build_flat",
+        "roofline": {"bound": "hbm", "kernel": "k_build_cls",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None,
-                     "traffic": traffic_from_profiles("k_build_flat"),
+                     "traffic": traffic_from_profiles("k_build_cls"),
                      "algorithmic_bytes_per_launch": simplex_bytes_rank,
                      "kernel_ms_per_launch": main_ms / main_cnt if main_cnt else None,
                      "prepass_ms_per_launch": pre_ms / main_cnt if main_cnt else None,
