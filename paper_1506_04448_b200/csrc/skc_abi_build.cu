@@ -107,6 +107,22 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
     require(R <= 16, "accumulate_dense: slot range spans too many replicates");
     const long long tot = rt.cum.back();
     const int P = std::max(1, ctx->sms);  // one persistent CTA per SM, rows handed out dynamically
+    // The exact accumulators and row counters are zero between builds: the finalize
+    // re-zeroes what the build used. A fresh allocation (or a build that failed before its
+    // finalize was enqueued) is cleared here.
+    auto ensure_clean = [&] {
+        if (ctx->build_scratch_clean && ctx->build_acc.p == ctx->build_acc_clean_p &&
+            ctx->build_ints.p == ctx->build_ints_clean_p && ctx->build_acc.count == ctx->build_acc_clean_n &&
+            ctx->build_ints.count == ctx->build_ints_clean_n)
+            return;
+        CK(cudaMemsetAsync(ctx->build_acc.p, 0, ctx->build_acc.count * sizeof(unsigned long long), ctx->stream));
+        CK(cudaMemsetAsync(ctx->build_ints.p, 0, ctx->build_ints.count * sizeof(int), ctx->stream));
+        ctx->build_acc_clean_p = ctx->build_acc.p;
+        ctx->build_ints_clean_p = ctx->build_ints.p;
+        ctx->build_acc_clean_n = ctx->build_acc.count;
+        ctx->build_ints_clean_n = ctx->build_ints.count;
+        ctx->build_scratch_clean = true;
+    };
     ctx->build_ints.alloc(static_cast<size_t>(G));
     ctx->build_acc.alloc(static_cast<size_t>(total_slots));
     ctx->qbuf.alloc(static_cast<size_t>(std::max<long long>(1, tot)));
@@ -174,6 +190,8 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
         ctx->build_ints.alloc(static_cast<size_t>(K) * G);
         ctx->ints.alloc(16);
         ctx->prepass.alloc(static_cast<size_t>(K) * qsms);
+        ensure_clean();
+        ctx->build_scratch_clean = false;
         if (!ctx->stream2) CK(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
         if (!ctx->ev_q[0])
             for (int c = 0; c < 5; ++c) CK(cudaEventCreateWithFlags(&ctx->ev_q[c], cudaEventDisableTiming));
@@ -216,15 +234,14 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
                     if (ptrace) CK(cudaEventRecord(te[2][c], ctx->stream2));
                     launch_build_main(ctx->stream2, Tdev, pc);
                     if (ptrace) CK(cudaEventRecord(te[3][c], ctx->stream2));
-                } else {
-                    CK(cudaMemsetAsync(pc.acc, 0, sizeof(unsigned long long) * (size_t)total_slots, ctx->stream2));
-                }
+                }  // (an empty chunk's accumulator stays zero)
             }
             CK(cudaEventRecord(ctx->ev_q[K], ctx->stream2));
             CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_q[K], 0));
             BuildPlan pf = p;
             pf.acc = ctx->build_acc.p;
-            launch_build_finalize_multi(ctx->stream, pf, K, ctx->ints.p + 4);
+            launch_build_finalize_multi(ctx->stream, pf, K, ctx->ints.p + 4, ctx->build_ints.p, K * G);
+            ctx->build_scratch_clean = true;
             if (ptrace) {
                 ctx->sync();
                 for (int c = 0; c < K && c < 4; ++c) {
@@ -241,6 +258,8 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
         }
         ctx->check_launch();
     } else {
+        ensure_clean();
+        ctx->build_scratch_clean = false;
         {
             SKC_PROF(ctx, "build_prepass");
             launch_build_prepass(ctx->stream, Tdev, p);
@@ -254,6 +273,7 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
         {
             SKC_PROF(ctx, "build_finalize");
             launch_build_finalize(ctx->stream, p);  // device-side no-op when nonfinite
+            ctx->build_scratch_clean = true;
         }
         ctx->check_launch();
     }

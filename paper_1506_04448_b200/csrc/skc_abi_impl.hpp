@@ -145,6 +145,10 @@ struct skc_context {
     DevBuf<double> dbl;  // [0] best value
     DevBuf<int> build_ints;                // per-type row counters of the dense build
     DevBuf<unsigned long long> build_acc;  // exact fixed-point slot accumulators
+    bool build_scratch_clean = false;      // build_acc / build_ints are all zero (finalize re-zeroes them)
+    const void* build_acc_clean_p = nullptr;  // the buffers (pointer, size) that were cleared
+    const void* build_ints_clean_p = nullptr;
+    size_t build_acc_clean_n = 0, build_ints_clean_n = 0;
     DevBuf<double> U, part, values, freq_acc, X;
     DevBuf<double2> tmp;
     DevBuf<int> flags;

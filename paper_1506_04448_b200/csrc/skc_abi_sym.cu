@@ -209,7 +209,10 @@ int skc_sym_accumulate_dense(skc_sym_set* s, const void* T, int dtype, int locat
             }
         }
         s->version++;  // sketch.cpp:324
-        run_dense_build(ctx, Td, s->n, dtype, true, i0, i1, s->B, s->b, s->packed.p, s->data.p, zc);
+        {
+            SKC_PROF(ctx, "build_total");
+            run_dense_build(ctx, Td, s->n, dtype, true, i0, i1, s->B, s->b, s->packed.p, s->data.p, zc);
+        }
         ctx->sync();
     });
 }

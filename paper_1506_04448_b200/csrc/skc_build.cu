@@ -24,6 +24,7 @@
 // F = 61 - ceil(log2(sum kappa|T|)) from a deterministic pre-pass bounds every bucket.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "skc_host.hpp"
@@ -178,24 +179,6 @@ __global__ void __launch_bounds__(NTQ) k_build_quantize(const TT* __restrict__ T
     if (threadIdx.x == 0) partials[blockIdx.x] = s;
 }
 
-// Global exponent F = 61 - ceil(log2(sum kappa|T|)): every bucket sum of q stays below 2^62.
-__global__ void k_build_scale(const double* __restrict__ partials, int np, int* __restrict__ scale_exp) {
-    __shared__ double red[8];
-    double acc = 0.0;
-    for (int i = threadIdx.x; i < np; i += 256) acc += partials[i];
-    const double s = block_sum_b<256>(acc, red);
-    if (threadIdx.x == 0) {
-        int F = 0;
-        if (s > 0.0 && isfinite(s)) {
-            int ex;
-            frexp(s, &ex);  // s <= 2^ex
-            F = 61 - ex;
-            F = F > 1000 ? 1000 : (F < -1000 ? -1000 : F);
-        }
-        *scale_exp = F;
-    }
-}
-
 // Default: kPrepassBlocks x 256 threads over all SMs (HBM-bound). Pipelined zero-copy
 // builds use p.prepass_blocks x 1024-thread blocks on a few SMs (PCIe-bound), leaving the
 // rest to the concurrent main pass of the previous chunk.
@@ -231,8 +214,6 @@ void launch_build_prepass(cudaStream_t st, const void* T, const BuildPlan& p) {
         else QUANT(float, false)
     }
 #undef QUANT
-    count_launch();
-    k_build_scale<<<1, 256, 0, st>>>(p.prepass_partials, blocks, p.scale_exp);
     count_launch();
 }
 
@@ -290,12 +271,40 @@ struct BuildArgs {
     const short* rowF;
     const long long* qbuf;
     const std::uint32_t* packed;
-    const int* scale_exp;
-    int* next_row;                 // G row (or tile) counters (zeroed per build)
+    const double* partials;        // pre-pass L1 partials (np of them)
+    int np;
+    int* scale_out;                // global exponent F, written by CTA 0 for the finalize
+    int* next_row;                 // G row (or tile) counters (zero on entry; the finalize re-zeroes them)
 
-    unsigned long long* acc;       // total_slots exact accumulators (zeroed per build)
+    unsigned long long* acc;       // total_slots exact accumulators (zero on entry; the finalize re-zeroes them)
     unsigned long long* trace;     // optional: per-CTA (start, end, switches)
 };
+
+// Global exponent F = 61 - ceil(log2(sum kappa|T|)), so every bucket sum of q stays below
+// 2^62. Every CTA sums the pre-pass partials in the same fixed order (lane-strided, then a
+// fixed shuffle tree read from lane 0), so all CTAs agree; CTA 0 publishes F.
+__device__ int cta_scale_exp(const BuildArgs& a) {
+    __shared__ int sF;
+    if (threadIdx.x < 32) {
+        double acc = 0.0;
+        for (int x = threadIdx.x; x < a.np; x += 32) acc += a.partials[x];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (threadIdx.x == 0) {
+            int F = 0;
+            if (acc > 0.0 && isfinite(acc)) {
+                int ex;
+                frexp(acc, &ex);  // acc <= 2^ex
+                F = 61 - ex;
+                F = F > 1000 ? 1000 : (F < -1000 ? -1000 : F);
+            }
+            sF = F;
+            if (blockIdx.x == 0) *a.scale_out = F;
+        }
+    }
+    __syncthreads();
+    return sF;
+}
 
 struct RowMeta {
     int i, j, k0, d;
@@ -341,7 +350,7 @@ __global__ void __launch_bounds__(NT, 1) k_build_dyn(BuildArgs a) {
     const int n = a.n, nrows = a.nrows;
     const long long spr = SYM ? 2ll * (a.bmask + 1) : static_cast<long long>(a.bmask + 1);
     const int prow = SYM ? n : 3 * n;
-    const int F = *a.scale_exp;
+    const int F = cta_scale_exp(a);
     std::uint32_t sbase = static_cast<std::uint32_t>(__cvta_generic_to_shared(sacc));
     asm volatile("mov.b32 %0, %0;" : "+r"(sbase));  // keep in a register (no per-use S2UR/ULEA)
     const std::uint32_t hioff = 4u * static_cast<std::uint32_t>(plane);
@@ -503,7 +512,7 @@ __global__ void __launch_bounds__(1024, 1) k_build_flat(BuildArgs a) {
     std::uint32_t* m_pij = reinterpret_cast<std::uint32_t*>(m_d + kFlatRows);  // RMAX x kFlatRows
     const long long spr = SYM ? 2ll * (a.bmask + 1) : static_cast<long long>(a.bmask + 1);
     const int prow = SYM ? n : 3 * n;
-    const int F = *a.scale_exp;
+    const int F = cta_scale_exp(a);
     std::uint32_t sbase = static_cast<std::uint32_t>(__cvta_generic_to_shared(sacc));
     asm volatile("mov.b32 %0, %0;" : "+r"(sbase));  // keep in a register (no per-use S2UR/ULEA)
     const std::uint32_t hioff = 4u * static_cast<std::uint32_t>(plane);
@@ -702,7 +711,7 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
     // qbuf index - k relative to the chunk, c_ij | d << 24 | e_ij << 30)
     int4* meta = reinterpret_cast<int4*>(
         sm + ((static_cast<size_t>(2 * W + 3 * n + cls_sfx_words(C, n)) + 3) & ~static_cast<size_t>(3))) + warp * kClsRows;
-    const int F = *a.scale_exp;
+    const int F = cta_scale_exp(a);
     std::uint32_t sbase = static_cast<std::uint32_t>(__cvta_generic_to_shared(sm));
     asm volatile("mov.b32 %0, %0;" : "+r"(sbase));
     const std::uint32_t hioff = pin(4u * static_cast<std::uint32_t>(W));
@@ -944,8 +953,6 @@ size_t build_smem_bytes(long long slots_per_cta, int R, int n) {
 
 void launch_build_main(cudaStream_t st, const void* T, const BuildPlan& p) {
     (void)T;
-    cudaMemsetAsync(p.next_row, 0, sizeof(int) * (size_t)p.G, st);
-    cudaMemsetAsync(p.acc, 0, sizeof(unsigned long long) * (size_t)p.total_slots, st);
     BuildArgs a;
     a.n = p.n;
     a.B = p.B;
@@ -959,7 +966,9 @@ void launch_build_main(cudaStream_t st, const void* T, const BuildPlan& p) {
     a.rowF = p.rowF;
     a.qbuf = p.qbuf;
     a.packed = p.packed;
-    a.scale_exp = p.scale_exp;
+    a.partials = p.prepass_partials;
+    a.np = p.prepass_blocks;
+    a.scale_out = p.scale_exp;
     a.next_row = p.next_row;
     a.acc = p.acc;
 
@@ -978,18 +987,25 @@ void launch_build_main(cudaStream_t st, const void* T, const BuildPlan& p) {
 }
 
 // ---- finalize --------------------------------------------------------------------------
-// data += acc * 2^-F, skipped entirely when the pre-pass flagged a non-finite entry (the
-// caller then reports the error with the set untouched). For the symmetric set the slot
-// index is the double index into interleaved (re, im) data; the asymmetric set is real-only.
+// data += acc * 2^-F, skipped when the pre-pass flagged a non-finite entry (the caller then
+// reports the error with the set untouched). For the symmetric set the slot index is the
+// double index into interleaved (re, im) data; the asymmetric set is real-only. The
+// accumulators and the row counters are re-zeroed here for the next build (no memsets).
+__device__ __forceinline__ double pow2_neg(int F) {  // 2^-F exactly, |F| <= 1000
+    return __longlong_as_double(static_cast<long long>(1023 - F) << 52);
+}
 template <bool SYM>
-__global__ void k_build_finalize(const unsigned long long* __restrict__ acc, long long total_slots,
+__global__ void k_build_finalize(unsigned long long* __restrict__ acc, long long total_slots,
                                  const int* __restrict__ scale_exp, const int* __restrict__ nonfinite,
-                                 double* __restrict__ data) {
+                                 double* __restrict__ data, int* __restrict__ counters, int ncounters) {
     const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (s >= total_slots || *nonfinite) return;
+    if (s < ncounters) counters[s] = 0;
+    if (s >= total_slots) return;
     const long long q = static_cast<long long>(acc[s]);
     if (q == 0) return;
-    const double v = ldexp(static_cast<double>(q), -*scale_exp);
+    acc[s] = 0ull;
+    if (*nonfinite) return;
+    const double v = static_cast<double>(q) * pow2_neg(*scale_exp);  // == ldexp(double(q), -F)
     if (SYM)
         data[s] += v;
     else
@@ -998,43 +1014,49 @@ __global__ void k_build_finalize(const unsigned long long* __restrict__ acc, lon
 
 // Pipelined builds: K chunk accumulators with their own exponents, summed in chunk order.
 template <bool SYM>
-__global__ void k_build_finalize_multi(const unsigned long long* __restrict__ acc, int K, long long total_slots,
+__global__ void k_build_finalize_multi(unsigned long long* __restrict__ acc, int K, long long total_slots,
                                        const int* __restrict__ scale_exps, const int* __restrict__ nonfinite,
-                                       double* __restrict__ data) {
+                                       double* __restrict__ data, int* __restrict__ counters, int ncounters) {
     const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (s >= total_slots || *nonfinite) return;
+    if (s < ncounters) counters[s] = 0;
+    if (s >= total_slots) return;
+    const bool bad = *nonfinite != 0;
     double v = 0.0;
     bool any = false;
     for (int c = 0; c < K; ++c) {
         const long long q = static_cast<long long>(acc[(long long)c * total_slots + s]);
         if (q) {
-            v += ldexp(static_cast<double>(q), -scale_exps[c]);
+            acc[(long long)c * total_slots + s] = 0ull;
+            v += static_cast<double>(q) * pow2_neg(scale_exps[c]);
             any = true;
         }
     }
-    if (!any) return;
+    if (!any || bad) return;
     if (SYM)
         data[s] += v;
     else
         data[2 * s] += v;
 }
-void launch_build_finalize_multi(cudaStream_t st, const BuildPlan& p, int K, const int* scale_exps) {
+void launch_build_finalize_multi(cudaStream_t st, const BuildPlan& p, int K, const int* scale_exps, int* counters,
+                                 int ncounters) {
+    const unsigned grid = cdiv(std::max<long long>(p.total_slots, ncounters), 256);
     if (p.sym)
-        k_build_finalize_multi<true><<<cdiv(p.total_slots, 256), 256, 0, st>>>(p.acc, K, p.total_slots, scale_exps,
-                                                                               p.nonfinite, p.data_as_double);
+        k_build_finalize_multi<true><<<grid, 256, 0, st>>>(p.acc, K, p.total_slots, scale_exps, p.nonfinite,
+                                                           p.data_as_double, counters, ncounters);
     else
-        k_build_finalize_multi<false><<<cdiv(p.total_slots, 256), 256, 0, st>>>(p.acc, K, p.total_slots, scale_exps,
-                                                                                p.nonfinite, p.data_as_double);
+        k_build_finalize_multi<false><<<grid, 256, 0, st>>>(p.acc, K, p.total_slots, scale_exps, p.nonfinite,
+                                                            p.data_as_double, counters, ncounters);
     count_launch();
 }
 
 void launch_build_finalize(cudaStream_t st, const BuildPlan& p) {
+    const unsigned grid = cdiv(std::max<long long>(p.total_slots, p.G), 256);
     if (p.sym)
-        k_build_finalize<true><<<cdiv(p.total_slots, 256), 256, 0, st>>>(p.acc, p.total_slots, p.scale_exp,
-                                                                         p.nonfinite, p.data_as_double);
+        k_build_finalize<true><<<grid, 256, 0, st>>>(p.acc, p.total_slots, p.scale_exp, p.nonfinite, p.data_as_double,
+                                                     p.next_row, p.G);
     else
-        k_build_finalize<false><<<cdiv(p.total_slots, 256), 256, 0, st>>>(p.acc, p.total_slots, p.scale_exp,
-                                                                          p.nonfinite, p.data_as_double);
+        k_build_finalize<false><<<grid, 256, 0, st>>>(p.acc, p.total_slots, p.scale_exp, p.nonfinite, p.data_as_double,
+                                                      p.next_row, p.G);
     count_launch();
 }
 

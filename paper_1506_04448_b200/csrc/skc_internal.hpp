@@ -108,7 +108,8 @@ size_t cls_smem_bytes(std::uint32_t b, int tbits, int n, bool sym);
 void launch_build_prepass(cudaStream_t st, const void* T, const BuildPlan& p);
 void launch_build_main(cudaStream_t st, const void* T, const BuildPlan& p);
 void launch_build_finalize(cudaStream_t st, const BuildPlan& p);
-void launch_build_finalize_multi(cudaStream_t st, const BuildPlan& p, int K, const int* scale_exps);
+void launch_build_finalize_multi(cudaStream_t st, const BuildPlan& p, int K, const int* scale_exps, int* counters,
+                                 int ncounters);
 
 // LDA moments / whitening (skc_whiten.cu)
 void launch_corpus_prep(cudaStream_t st, int V, long long D, const long long* doc_ptr, const int* count,
