@@ -699,6 +699,7 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
     extern __shared__ __align__(16) std::uint32_t sm[];
     __shared__ int s_next_g;
     __shared__ int s_cend[C];
+    __shared__ int s_wcnt[C * 32];  // per-(class, 32-k segment) counts, then their scan
     const int n = a.n, nrows = a.nrows;
     const int W = static_cast<int>((a.bmask + 1u) >> TB);  // slots per plane
     // n list words grouped by class: h_k | k << KS | e_k << 30 (KS = log2 b + 2 clears the
@@ -732,10 +733,50 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
         for (int k = threadIdx.x; k < (SYM ? n : 2 * n); k += NT) pw[k] = a.packed[(size_t)m * (SYM ? n : 3 * n) + k];
         __syncthreads();
         const std::uint32_t* lw_src = SYM ? pw : a.packed + (size_t)m * 3 * n + 2 * n;
-        if (warp == 0) {  // stable class grouping of k and the suffix tables
-            auto cls_of = [&](std::uint32_t w) {
-                return static_cast<int>(SYM ? ((((w >> 30) & 1u) << TB) | (w & tmask)) : (w & tmask));
-            };
+        auto cls_of = [&](std::uint32_t w) {
+            return static_cast<int>(SYM ? ((((w >> 30) & 1u) << TB) | (w & tmask)) : (w & tmask));
+        };
+        const std::uint32_t lt = (1u << lane) - 1u;
+        if (n <= 32 * 32) {
+            // stable class grouping of k and the suffix tables, one 32-k segment per warp:
+            // per-segment class counts, a class-major scan over the segments, then each
+            // warp places its k's (3 barriers instead of one warp walking all of n)
+            const int k = warp * 32 + lane;
+            const std::uint32_t w = k < n ? lw_src[k] : 0u;
+            const int c = k < n ? cls_of(w) : -1;
+            std::uint32_t mk[C];
+#pragma unroll
+            for (int cc = 0; cc < C; ++cc) mk[cc] = __ballot_sync(0xffffffffu, c == cc);
+#pragma unroll
+            for (int cc = 0; cc < C; ++cc)
+                if (lane == cc) s_wcnt[cc * 32 + warp] = __popc(mk[cc]);
+            __syncthreads();
+            if (warp == 0) {  // exclusive scan over (class, segment) in class-major order
+                int base = 0;
+                for (int cc = 0; cc < C; ++cc) {
+                    const int v = s_wcnt[cc * 32 + lane];
+                    int incl = v;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += t;
+                    }
+                    s_wcnt[cc * 32 + lane] = base + incl - v;
+                    base += __shfl_sync(0xffffffffu, incl, 31);
+                    if (lane == 0) s_cend[cc] = base;
+                }
+            }
+            __syncthreads();
+            if (warp * 32 < n) {
+#pragma unroll
+                for (int cc = 0; cc < C; ++cc) {
+                    const int pos = s_wcnt[cc * 32 + warp] + __popc(mk[cc] & lt);
+                    if (k < n) sfx[cc * (n + 1) + k] = static_cast<unsigned short>(pos);
+                    if (c == cc) lst[pos] = w | (static_cast<std::uint32_t>(k) << KS);
+                }
+            }
+            if (threadIdx.x < C) sfx[threadIdx.x * (n + 1) + n] = static_cast<unsigned short>(s_cend[threadIdx.x]);
+        } else if (warp == 0) {  // large n: one warp walks the k segments in order
             int cnt = 0;  // lane c: size of class c
             for (int base = 0; base < n; base += 32) {
                 const int k = base + lane;
@@ -754,7 +795,6 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
             }
             run -= cnt;  // lane c: start of class c
             if (lane < C) s_cend[lane] = run + cnt;
-            const std::uint32_t lt = (1u << lane) - 1u;
             for (int base = 0; base < n; base += 32) {
                 const int k = base + lane;
                 const std::uint32_t w = k < n ? lw_src[k] : 0u;
@@ -866,11 +906,25 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
             c0 = __shfl_sync(0xffffffffu, cn, 0);
         }
         __syncthreads();
-        // flush: window slot s is bucket (s << TB) | r of replicate m, parity P
-        unsigned long long* out = a.acc + (long long)m * (SYM ? 2ll : 1ll) * (a.bmask + 1) + P;
-        for (int s = threadIdx.x; s < W; s += NT) {
-            const unsigned long long v = (static_cast<unsigned long long>(sm[W + s]) << 32) | sm[s];
-            if (v) atomicAdd(out + (SYM ? 2ll : 1ll) * ((static_cast<long long>(s) << TB) | r), v);
+        unsigned long long t_f0 = 0;
+        if (a.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_f0));
+        // flush into the window-major exact accumulators acc[g * W + s]: consecutive
+        // threads add consecutive 8-byte words (coalesced RED.64; integer adds commute, so
+        // the sketch stays bit-deterministic)
+        {
+            unsigned long long* out = a.acc + static_cast<long long>(g) * W;
+            for (int s = threadIdx.x; s < W; s += NT) {
+                const unsigned long long v = (static_cast<unsigned long long>(sm[W + s]) << 32) | sm[s];
+                if (v) atomicAdd(out + s, v);
+            }
+        }
+        if (a.trace) {
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                unsigned long long t_f1;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_f1));
+                switches += (t_f1 - t_f0) << 16;  // trace: flush ns in the high bits
+            }
         }
         if (threadIdx.x == 0) {
             int best = -1, left = 0;
@@ -994,29 +1048,58 @@ void launch_build_main(cudaStream_t st, const void* T, const BuildPlan& p) {
 __device__ __forceinline__ double pow2_neg(int F) {  // 2^-F exactly, |F| <= 1000
     return __longlong_as_double(static_cast<long long>(1023 - F) << 52);
 }
+// Data slot of accumulator index ai: the contiguous-window kernels keep data order; the
+// class-list kernel keeps window-major order ai = g * W + t (tb >= 0: bucket-class bits),
+// window g = (replicate m, [parity P,] residue r), bucket (t << tb) | r. The finalize walks
+// ai (coalesced accumulator reads) and scatters into the interleaved data.
+__device__ __forceinline__ long long data_index(long long ai, int tb, bool sym, std::uint32_t bmask) {
+    if (tb < 0) return ai;
+    const int logb = __popc(bmask);
+    const int logW = logb - tb, logC = tb + (sym ? 1 : 0);
+    const long long g = ai >> logW, t = ai & ((1ll << logW) - 1);
+    const long long m = g >> logC, rem = g & ((1ll << logC) - 1);
+    const long long r = rem & ((1ll << tb) - 1), P = sym ? rem >> tb : 0;
+    const long long bucket = (t << tb) | r;
+    return sym ? (m << (logb + 1)) + 2 * bucket + P : (m << logb) + bucket;
+}
 template <bool SYM>
 __global__ void k_build_finalize(unsigned long long* __restrict__ acc, long long total_slots,
                                  const int* __restrict__ scale_exp, const int* __restrict__ nonfinite,
-                                 double* __restrict__ data, int* __restrict__ counters, int ncounters) {
-    const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (s < ncounters) counters[s] = 0;
-    if (s >= total_slots) return;
-    const long long q = static_cast<long long>(acc[s]);
-    if (q == 0) return;
-    acc[s] = 0ull;
-    if (*nonfinite) return;
-    const double v = static_cast<double>(q) * pow2_neg(*scale_exp);  // == ldexp(double(q), -F)
-    if (SYM)
-        data[s] += v;
-    else
-        data[2 * s] += v;
+                                 double* __restrict__ data, int* __restrict__ counters, int ncounters, int tb,
+                                 std::uint32_t bmask) {
+    // 4 slots per thread (strided by the grid) so each thread has independent loads in flight
+    const long long base = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    if (base < ncounters) counters[base] = 0;
+    const bool bad = *nonfinite != 0;
+    const double sc = pow2_neg(*scale_exp);
+    long long q[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const long long s = base + u * stride;
+        q[u] = s < total_slots ? static_cast<long long>(acc[s]) : 0ll;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const long long s = base + u * stride;
+        if (q[u] == 0) continue;
+        acc[s] = 0ull;
+        if (bad) continue;
+        const double v = static_cast<double>(q[u]) * sc;  // == ldexp(double(q), -F)
+        const long long d = data_index(s, tb, SYM, bmask);
+        if (SYM)
+            data[d] += v;
+        else
+            data[2 * d] += v;
+    }
 }
 
 // Pipelined builds: K chunk accumulators with their own exponents, summed in chunk order.
 template <bool SYM>
 __global__ void k_build_finalize_multi(unsigned long long* __restrict__ acc, int K, long long total_slots,
                                        const int* __restrict__ scale_exps, const int* __restrict__ nonfinite,
-                                       double* __restrict__ data, int* __restrict__ counters, int ncounters) {
+                                       double* __restrict__ data, int* __restrict__ counters, int ncounters, int tb,
+                                       std::uint32_t bmask) {
     const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (s < ncounters) counters[s] = 0;
     if (s >= total_slots) return;
@@ -1032,31 +1115,32 @@ __global__ void k_build_finalize_multi(unsigned long long* __restrict__ acc, int
         }
     }
     if (!any || bad) return;
+    const long long d = data_index(s, tb, SYM, bmask);
     if (SYM)
-        data[s] += v;
+        data[d] += v;
     else
-        data[2 * s] += v;
+        data[2 * d] += v;
 }
 void launch_build_finalize_multi(cudaStream_t st, const BuildPlan& p, int K, const int* scale_exps, int* counters,
                                  int ncounters) {
     const unsigned grid = cdiv(std::max<long long>(p.total_slots, ncounters), 256);
     if (p.sym)
         k_build_finalize_multi<true><<<grid, 256, 0, st>>>(p.acc, K, p.total_slots, scale_exps, p.nonfinite,
-                                                           p.data_as_double, counters, ncounters);
+                                                           p.data_as_double, counters, ncounters, p.cls_bits, p.bmask);
     else
         k_build_finalize_multi<false><<<grid, 256, 0, st>>>(p.acc, K, p.total_slots, scale_exps, p.nonfinite,
-                                                            p.data_as_double, counters, ncounters);
+                                                            p.data_as_double, counters, ncounters, p.cls_bits, p.bmask);
     count_launch();
 }
 
 void launch_build_finalize(cudaStream_t st, const BuildPlan& p) {
-    const unsigned grid = cdiv(std::max<long long>(p.total_slots, p.G), 256);
+    const unsigned grid = cdiv(std::max<long long>((p.total_slots + 3) / 4, p.G), 256);
     if (p.sym)
         k_build_finalize<true><<<grid, 256, 0, st>>>(p.acc, p.total_slots, p.scale_exp, p.nonfinite, p.data_as_double,
-                                                     p.next_row, p.G);
+                                                     p.next_row, p.G, p.cls_bits, p.bmask);
     else
         k_build_finalize<false><<<grid, 256, 0, st>>>(p.acc, p.total_slots, p.scale_exp, p.nonfinite, p.data_as_double,
-                                                      p.next_row, p.G);
+                                                      p.next_row, p.G, p.cls_bits, p.bmask);
     count_launch();
 }
 
