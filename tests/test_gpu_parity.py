@@ -96,6 +96,25 @@ for n, b, B, seed in [(40, 1024, 5, 1), (64, 4096, 20, 2), (36, 1 << 16, 3, 3), 
     a = skb.AsymTensorSketchSet(n, b, B, seed)
     a.accumulate_dense(A)
     out.append(a.data())
+for n, b, B, seed in [(20, 1 << 15, 2, 6), (24, 1 << 17, 2, 7)]:  # 1 and 3 bucket-class bits
+    rng = np.random.default_rng(seed)
+    A = rng.normal(size=(n, n, n))
+    T = sum(A.transpose(p) for p in [(0, 1, 2), (0, 2, 1), (1, 0, 2), (1, 2, 0), (2, 0, 1), (2, 1, 0)]) / 6
+    s = skb.SymTensorSketchSet(n, b, B, seed)
+    s.accumulate_dense(T, assume_symmetric=True)
+    out.append(s.data())
+    a = skb.AsymTensorSketchSet(n, b, B, seed)
+    a.accumulate_dense(A)
+    out.append(a.data())
+# n > 1024: the class tables take the one-warp path; device-generated fp32 tensor
+import torch
+ctx = skb.default_context(0)
+n = 1100
+Td = torch.empty(n ** 3, dtype=torch.float32, device="cuda")
+skb.gen_planted_tensor_device(ctx, n, 4, 0.01, 8, Td.data_ptr(), dtype=np.float32)
+s = skb.SymTensorSketchSet(n, 1 << 12, 2, 8, ctx)
+s.accumulate_dense(Td, assume_symmetric=True)
+out.append(s.data())
 np.savez(sys.argv[2], *out)
 """
 
@@ -103,7 +122,7 @@ np.savez(sys.argv[2], *out)
 def test_sym_build_kernels_bit_identical(tmp_path):
     """The class-list kernel (default) and the contiguous-window kernel both add the same
     exact fixed-point values, so their sketches must agree bit for bit, symmetric and
-    asymmetric (b = 2^16 takes the bucket-class split)."""
+    asymmetric, with 0-3 bucket-class bits (b = 2^14 .. 2^17) and n > 1024 (fp32)."""
     import os
     import subprocess
     import sys
