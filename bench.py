@@ -115,6 +115,25 @@ def pcie_link(device):
         return None
 
 
+def scatter_roofline(adds, kernel_ms):
+    """Exact adds as 2 random u32 shared atomics each, against the measured random ATOMS
+    ceiling (microbench/atomics.cu: ops/clk/SM at 4 CTAs/SM) x 148 SMs x the max SM clock."""
+    if not kernel_ms:
+        return None
+    ceil = None
+    p = ROOT / "profiles" / "r01_microbench_atomics.jsonl"
+    try:
+        rows = [json.loads(l) for l in p.read_text().splitlines() if l.strip()]
+        hdr = rows[0]
+        best = max(r["ops_per_clk_per_sm"] for r in rows if r.get("test") == "smem_u32_atomsadd")
+        ceil = best * hdr["sms"] * hdr["clock_khz"] * 1e3
+    except Exception:
+        return None
+    achieved = 2.0 * adds / (kernel_ms * 1e-3)
+    return {"bound": "smem_atomics", "achieved": achieved, "peak": ceil, "unit": "u32 atomics/s",
+            "frac": achieved / ceil, "peak_source": "profiles/r01_microbench_atomics.jsonl"}
+
+
 def contraction_roofline(per_s, n, b, B):
     """SURVEY 8(d) model of one median-of-B T(I,u,u): 4B length-b transforms at 5 b log2 b
     nominal flops each plus B(5n + 40b); shared memory moves 32b bytes per radix-2 pass
@@ -358,6 +377,9 @@ def run_b200(args):
                      "scatter_adds_per_s": (simplex_entries(n, i0, i1) * B) / (main_ms / main_cnt * 1e-3) if main_cnt else None,
                      "frac_vs_8tbs": (achieved / 8000.0) if achieved else None,
                      "peak_source": peak_src},
+        # the ceiling the scatter actually meets: random u32 shared-memory atomics (two
+        # exact limbs per add), against the microbenchmarked rate (profiles/r01_microbench_atomics.jsonl)
+        "scatter_roofline": scatter_roofline(simplex_entries(n, i0, i1) * B, main_ms / main_cnt if main_cnt else None),
         "clocks": clocks,
     }
     if world == 1 and not args.no_cpu_baseline:
