@@ -1,5 +1,5 @@
 cd /root/repo
-python -m pytest tests -m gpu -x -q -k "dense or config1 or bit_identical" > gpurun_out/t1.log 2>&1; tail -1 gpurun_out/t1.log
+python -m pytest tests -m gpu -x -q -k "dense or config1 or kernels_agree" > gpurun_out/t1.log 2>&1; tail -1 gpurun_out/t1.log
 python bench.py --steps 10 > gpurun_out/bench_cls.json 2>gpurun_out/bench_cls.err
 python -c "
 import json

@@ -127,7 +127,7 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
     ctx->build_acc.alloc(static_cast<size_t>(total_slots));
     ctx->qbuf.alloc(static_cast<size_t>(std::max<long long>(1, tot)));
     ctx->rowF.alloc(static_cast<size_t>(rt.nrows));
-    ctx->prepass.alloc(kPrepassBlocks);
+    ctx->prepass.alloc(2 * kPrepassBlocks);  // L1 sums, then maxima
     ctx->ints.alloc(16);
 
     BuildPlan p;
@@ -148,6 +148,9 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
     // sets take the row-walk kernel, which uses the plain packed form)
     p.flat = !row_variant && (!sym || b <= (1u << 27));
     p.cls_bits = cls_bits;
+    // class-list builds read T in place when it is device-resident (row offsets relative to
+    // a 32-row chunk fit in 32 bits for n <= 30000), else a packed raw copy of the rows
+    p.xsrc_mode = cls_bits < 0 ? 0 : ((!zero_copy && n <= 30000) ? 1 : 2);
     static const bool trace_on = std::getenv("SKC_BUILD_TRACE") != nullptr;
     DevBuf<unsigned long long> trace;
     p.trace = nullptr;
@@ -189,7 +192,7 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
         ctx->build_acc.alloc(static_cast<size_t>(K) * total_slots);
         ctx->build_ints.alloc(static_cast<size_t>(K) * G);
         ctx->ints.alloc(16);
-        ctx->prepass.alloc(static_cast<size_t>(K) * qsms);
+        ctx->prepass.alloc(2 * static_cast<size_t>(K) * qsms);
         ensure_clean();
         ctx->build_scratch_clean = false;
         if (!ctx->stream2) CK(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
@@ -220,7 +223,7 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
                 pc.rowoff = rt.offs.p + rb[c];
                 pc.rowF = ctx->rowF.p + rb[c];
                 pc.nrows = rb[c + 1] - rb[c];
-                pc.prepass_partials = ctx->prepass.p + static_cast<size_t>(c) * qsms;
+                pc.prepass_partials = ctx->prepass.p + 2 * static_cast<size_t>(c) * qsms;
                 pc.scale_exp = ctx->ints.p + 4 + c;
                 pc.reset_nonfinite = false;
                 pc.acc = ctx->build_acc.p + static_cast<size_t>(c) * total_slots;

@@ -53,13 +53,18 @@ __device__ double block_sum_b(double v, double* red) {
 }
 }  // namespace
 
-// ---- quantize pass ----------------------------------------------------------------
-// One warp per row: reads the row segment twice (the second read hits L1), computes
-// the row's L1 mass sum kappa|T| in a fixed order, and writes the packed fixed-point
-// stream qbuf[rowoff + e] = round(kappa T 2^Frow) with Frow = 61 - ceil(log2 rowL1).
-// The main pass rescales q >> (Frow - F) to the global exponent F, so T is read from
-// HBM once per build. Per-block L1 partials are summed in a fixed order (deterministic).
-template <typename TT, bool SYM, int NTQ>
+// ---- pre-pass ---------------------------------------------------------------------
+// One warp per row segment T[i][j][k0:n]. Every mode computes the row's L1 mass
+// sum kappa|T| in a fixed order, the block max of kappa|T| and the non-finite flag; the
+// per-block partials (L1 at [blk], max at [gridDim + blk]) give the global exponent.
+//   kQuant: writes the packed fixed-point stream qbuf[rowoff + e] = round(kappa T 2^Frow),
+//           Frow = 61 - ceil(log2 rowL1), for the contiguous-window kernels (they rescale
+//           q >> (Frow - F));
+//   kRaw:   writes the row segment as is (packed, element type TT) for the class-list
+//           kernel when T is not device-resident (pinned host memory read over the bus);
+//   kNone:  no writes (the class-list kernel gathers from a device-resident T).
+enum PrepassMode { kQuant = 0, kRaw = 1, kNone = 2 };
+template <typename TT, bool SYM, int NTQ, int MODE>
 __global__ void __launch_bounds__(NTQ) k_build_quantize(const TT* __restrict__ T, int n,
                                                        const std::uint32_t* __restrict__ rowtab,
                                                        const long long* __restrict__ rowoff, int nrows,
@@ -71,8 +76,9 @@ __global__ void __launch_bounds__(NTQ) k_build_quantize(const TT* __restrict__ T
     __shared__ double red[W];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double* st = stage + (size_t)warp * n;
-    double blk = 0.0;
+    double blk = 0.0, bmax = 0.0;
     bool bad = false;
+    TT* xraw = reinterpret_cast<TT*>(qbuf);  // kRaw output
     // 16-byte path: the first 128-pair block of the warp's next row is loaded before the
     // current row's reduction and stores, so each warp keeps a row's reads in flight.
     const bool v16 = sizeof(TT) == 8 && vec16;
@@ -103,6 +109,7 @@ __global__ void __launch_bounds__(NTQ) k_build_quantize(const TT* __restrict__ T
         const double kdiag = SYM ? ((i == j) ? 1.0 : 3.0) : 1.0;
         const double koff = SYM ? ((i == j) ? 3.0 : 6.0) : 1.0;
         double a0 = 0.0;
+        TT* xo = MODE == kRaw ? xraw + rowoff[row] : nullptr;
         if (v16) {
             // 16-byte loads from a 16-byte aligned base covering the row segment: T may be
             // pinned host memory read in place over PCIe, where wider requests carry less
@@ -129,8 +136,10 @@ __global__ void __launch_bounds__(NTQ) k_build_quantize(const TT* __restrict__ T
                             const double x = h ? v[u].y : v[u].x;
                             const int k = k0 + kk;
                             const double kv = ((SYM && k == j) ? kdiag : koff) * x;
-                            st[kk] = kv;
+                            if (MODE == kQuant) st[kk] = kv;
+                            if (MODE == kRaw) xo[kk] = static_cast<TT>(x);
                             a0 += fabs(kv);
+                            bmax = fmax(bmax, fabs(kv));
                             bad |= !isfinite(x);
                         }
                     }
@@ -147,8 +156,10 @@ __global__ void __launch_bounds__(NTQ) k_build_quantize(const TT* __restrict__ T
                     const int k = kb + 32 * u;
                     if (k < n) {
                         const double kv = ((SYM && k == j) ? kdiag : koff) * v[u];
-                        st[k - k0] = kv;
+                        if (MODE == kQuant) st[k - k0] = kv;
+                        if (MODE == kRaw) xo[k - k0] = rp[k];
                         a0 += fabs(kv);
+                        bmax = fmax(bmax, fabs(kv));
                         bad |= !isfinite(v[u]);
                     }
                 }
@@ -156,27 +167,41 @@ __global__ void __launch_bounds__(NTQ) k_build_quantize(const TT* __restrict__ T
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) a0 += __shfl_xor_sync(0xffffffffu, a0, o);
-        int F = 0;
-        if (a0 > 0.0 && isfinite(a0)) {
-            int ex;
-            frexp(a0, &ex);
-            F = 61 - ex;
-            F = F > 1000 ? 1000 : (F < -1000 ? -1000 : F);
+        a0 = __shfl_sync(0xffffffffu, a0, 0);  // lane 0's sum for every lane (xor trees may differ in the last bit)
+        if (MODE == kQuant) {
+            int F = 0;
+            if (a0 > 0.0 && isfinite(a0)) {
+                int ex;
+                frexp(a0, &ex);
+                F = 61 - ex;
+                F = F > 1000 ? 1000 : (F < -1000 ? -1000 : F);
+            }
+            const double scale = ldexp(1.0, F);
+            __syncwarp();
+            long long* qo = qbuf + rowoff[row] - k0;
+            for (int k = k0 + lane; k < n; k += 32) {
+                const double kv = st[k - k0];
+                qo[k] = isfinite(kv) ? __double2ll_rn(kv * scale) : 0ll;
+            }
+            __syncwarp();
+            if (lane == 0) rowF[row] = static_cast<short>(F);
         }
-        const double scale = ldexp(1.0, F);
-        __syncwarp();
-        long long* qo = qbuf + rowoff[row] - k0;
-        for (int k = k0 + lane; k < n; k += 32) {
-            const double kv = st[k - k0];
-            qo[k] = isfinite(kv) ? __double2ll_rn(kv * scale) : 0ll;
-        }
-        __syncwarp();
-        if (lane == 0) rowF[row] = static_cast<short>(F);
         blk += (lane == 0) ? a0 : 0.0;
     }
     if (bad) atomicOr(nonfinite, 1);
     const double s = block_sum_b<NTQ>(blk, red);
     if (threadIdx.x == 0) partials[blockIdx.x] = s;
+    // block max of kappa|T| (order-free)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) bmax = fmax(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
+    __syncthreads();
+    if (lane == 0) red[warp] = bmax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double mx = 0.0;
+        for (int w = 0; w < W; ++w) mx = fmax(mx, red[w]);
+        partials[gridDim.x + blockIdx.x] = mx;
+    }
 }
 
 // Default: kPrepassBlocks x 256 threads over all SMs (HBM-bound). Pipelined zero-copy
@@ -187,24 +212,32 @@ void launch_build_prepass(cudaStream_t st, const void* T, const BuildPlan& p) {
     const bool wide = p.prepass_threads == 1024;
     const int blocks = p.prepass_blocks;
     const bool vec16 = (reinterpret_cast<std::uintptr_t>(T) & 15) == 0;
-#define QUANT(TT, SY)                                                                                                 \
+    const int mode = p.xsrc_mode == 0 ? kQuant : p.xsrc_mode == 1 ? kNone : kRaw;
+#define QUANT_M(TT, SY, MD)                                                                                           \
     {                                                                                                                 \
         if (wide) {                                                                                                   \
-            const int w = p.prepass_warps;                                                                            \
-            const size_t smem = sizeof(double) * 32 * (size_t)p.n;                                                    \
-            (void)w;                                                                                                  \
-            cudaFuncSetAttribute(k_build_quantize<TT, SY, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-            k_build_quantize<TT, SY, 1024><<<blocks, 1024, smem, st>>>((const TT*)T, p.n, p.rowtab, p.rowoff, p.nrows,  \
-                                                                       p.qbuf, p.rowF, p.prepass_partials,             \
-                                                                       p.nonfinite, vec16);                            \
-        } else {                                                                                                      \
-            const size_t smem = sizeof(double) * 8 * (size_t)p.n;                                                     \
+            const size_t smem = MD == kQuant ? sizeof(double) * 32 * (size_t)p.n : 0;                                 \
             if (smem > 48 * 1024)                                                                                     \
-                cudaFuncSetAttribute(k_build_quantize<TT, SY, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-            k_build_quantize<TT, SY, 256><<<blocks, 256, smem, st>>>((const TT*)T, p.n, p.rowtab, p.rowoff, p.nrows,    \
-                                                                     p.qbuf, p.rowF, p.prepass_partials, p.nonfinite,  \
-                                                                     vec16);                                           \
+                cudaFuncSetAttribute(k_build_quantize<TT, SY, 1024, MD>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                     (int)smem);                                                                      \
+            k_build_quantize<TT, SY, 1024, MD><<<blocks, 1024, smem, st>>>((const TT*)T, p.n, p.rowtab, p.rowoff,    \
+                                                                           p.nrows, p.qbuf, p.rowF,                  \
+                                                                           p.prepass_partials, p.nonfinite, vec16);  \
+        } else {                                                                                                      \
+            const size_t smem = MD == kQuant ? sizeof(double) * 8 * (size_t)p.n : 0;                                  \
+            if (smem > 48 * 1024)                                                                                     \
+                cudaFuncSetAttribute(k_build_quantize<TT, SY, 256, MD>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                                     (int)smem);                                                                      \
+            k_build_quantize<TT, SY, 256, MD><<<blocks, 256, smem, st>>>((const TT*)T, p.n, p.rowtab, p.rowoff,      \
+                                                                         p.nrows, p.qbuf, p.rowF,                    \
+                                                                         p.prepass_partials, p.nonfinite, vec16);    \
         }                                                                                                             \
+    }
+#define QUANT(TT, SY)                                \
+    {                                                \
+        if (mode == kQuant) QUANT_M(TT, SY, kQuant)  \
+        else if (mode == kRaw) QUANT_M(TT, SY, kRaw) \
+        else QUANT_M(TT, SY, kNone)                  \
     }
     if (p.sym) {
         if (p.dtype == 0) QUANT(double, true)
@@ -214,6 +247,7 @@ void launch_build_prepass(cudaStream_t st, const void* T, const BuildPlan& p) {
         else QUANT(float, false)
     }
 #undef QUANT
+#undef QUANT_M
     count_launch();
 }
 
@@ -271,8 +305,10 @@ struct BuildArgs {
     const short* rowF;
     const long long* qbuf;
     const std::uint32_t* packed;
-    const double* partials;        // pre-pass L1 partials (np of them)
+    const double* partials;        // pre-pass partials: np L1 sums, then np maxima of kappa|T|
     int np;
+    const void* xsrc;              // class-list kernel: T itself (xmode 1) or its packed row copy (xmode 2)
+    int xmode;
     int* scale_out;                // global exponent F, written by CTA 0 for the finalize
     int* next_row;                 // G row (or tile) counters (zero on entry; the finalize re-zeroes them)
 
@@ -280,22 +316,31 @@ struct BuildArgs {
     unsigned long long* trace;     // optional: per-CTA (start, end, switches)
 };
 
-// Global exponent F = 61 - ceil(log2(sum kappa|T|)), so every bucket sum of q stays below
-// 2^62. Every CTA sums the pre-pass partials in the same fixed order (lane-strided, then a
-// fixed shuffle tree read from lane 0), so all CTAs agree; CTA 0 publishes F.
+// Global exponent F = min(61 - ceil(log2(sum kappa|T|)), 50 - ceil(log2(max kappa|T|))):
+// every bucket sum of q stays below 2^62 and every single |q| below 2^50, so the class-list
+// kernel can round kappa*T*2^F to an integer with one fma against 1.5*2^52. Every CTA
+// sums the pre-pass partials in the same fixed order (lane-strided, then a fixed shuffle
+// tree read from lane 0), so all CTAs agree; CTA 0 publishes F.
 __device__ int cta_scale_exp(const BuildArgs& a) {
     __shared__ int sF;
     if (threadIdx.x < 32) {
-        double acc = 0.0;
-        for (int x = threadIdx.x; x < a.np; x += 32) acc += a.partials[x];
+        double acc = 0.0, mx = 0.0;
+        for (int x = threadIdx.x; x < a.np; x += 32) {
+            acc += a.partials[x];
+            mx = fmax(mx, a.partials[a.np + x]);
+        }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        for (int o = 16; o > 0; o >>= 1) {
+            acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
         if (threadIdx.x == 0) {
             int F = 0;
             if (acc > 0.0 && isfinite(acc)) {
-                int ex;
+                int ex, exm;
                 frexp(acc, &ex);  // acc <= 2^ex
-                F = 61 - ex;
+                frexp(mx, &exm);  // mx <= 2^exm
+                F = min(61 - ex, 50 - exm);
                 F = F > 1000 ? 1000 : (F < -1000 ? -1000 : F);
             }
             sF = F;
@@ -692,7 +737,13 @@ size_t cls_smem_bytes(std::uint32_t b, int tbits, int n, bool sym) {
     return sizeof(std::uint32_t) * (2 * W + 3 * (size_t)n + cls_sfx_words(C, n) + 4 + 32 * (size_t)cls_meta_words());
 }
 
-template <bool SYM, int TB>
+// Entries are read straight from T (device-resident: xmode 1) or from the pre-pass's packed
+// row copy (xmode 2), element type XT, and rounded to q = round(kappa * T * 2^F) by one fma
+// against 1.5 * 2^52 (|q| < 2^50 by the choice of F). The scale's sign bit carries the
+// complex4 sign, so the add needs no separate negation. kappa is per row (6 or 3 sym; 1
+// asym); the k = j entry of a sym row, whose kappa is 3 (or 1), gets its correction
+// (-3 or -2) added once per row when the row's metadata is built.
+template <bool SYM, int TB, typename XT>
 __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
     constexpr int NT = 1024, C = (SYM ? 2 : 1) << TB;
     constexpr std::uint32_t tmask = (1u << TB) - 1u;
@@ -709,7 +760,7 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
     unsigned short* sfx = reinterpret_cast<unsigned short*>(pw + 2 * n);  // C x (n + 1)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // per-warp row metadata, one int4 per row: (end entry, list position - entry index,
-    // qbuf index - k relative to the chunk, c_ij | d << 24 | e_ij << 30)
+    // source element index of (i, j, 0) relative to the chunk, c_ij | [i == j] << 24 | e_ij << 30)
     int4* meta = reinterpret_cast<int4*>(
         sm + ((static_cast<size_t>(2 * W + 3 * n + cls_sfx_words(C, n)) + 3) & ~static_cast<size_t>(3))) + warp * kClsRows;
     const int F = cta_scale_exp(a);
@@ -721,6 +772,18 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
     const int KS = __popc(a.bmask) + 2;
     const std::uint32_t kmask = pin((1u << (30 - KS)) - 1u);
     const std::uint32_t wmask = pin(~(kmask << KS));
+    const XT* __restrict__ xsrc = static_cast<const XT*>(a.xsrc);
+    // high word of kappa * 2^F: sym kappa 6 = 1.5 * 2^2 (kappa 3 is one exponent step less);
+    // asym kappa 1
+    const std::uint32_t sc_hi0 = pin(SYM ? ((static_cast<std::uint32_t>(1023 + F + 2) << 20) | (1u << 19))
+                                         : (static_cast<std::uint32_t>(1023 + F) << 20));
+    constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+    constexpr long long kMagicBits = 0x4338000000000000ll;
+    // exact round(x * sc): |x * sc| < 2^50, one rounding in the fma
+    auto to_fixed = [](double x, std::uint32_t schi) -> long long {
+        const double sc = __hiloint2double(static_cast<int>(schi), 0);
+        return __double_as_longlong(fma(x, sc, kMagic)) - kMagicBits;
+    };
     unsigned long long t_start = 0, switches = 0;
     if (a.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 
@@ -820,24 +883,37 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
             int cn = 0;  // next grab, one chunk ahead
             if (lane == 0) cn = atomicAdd(a.next_row + g, kClsRows);
             const int nr = min(kClsRows, nrows - c0);
-            long long off = 0;
+            long long off = 0;  // source element index of (i, j, 0)
             int cnt = 0, pos0 = 0, j = 0;
             std::uint32_t pwd = 0;
             if (lane < nr) {
                 const int row = c0 + lane;
                 const std::uint32_t ij = __ldg(a.rowtab + row);
-                off = __ldg(a.rowoff + row);
                 const int i = static_cast<int>(ij >> 16);
                 j = static_cast<int>(ij & 0xFFFFu);
+                off = a.xmode == 1 ? (static_cast<long long>(i) * n + j) * n : __ldg(a.rowoff + row) - (SYM ? j : 0);
                 const std::uint32_t pij = pw[i] + pw[(SYM ? 0 : n) + j];
                 const int cl = SYM ? static_cast<int>(((((pij >> 30) & 1u) ^ static_cast<std::uint32_t>(P)) << TB) |
                                                       ((static_cast<std::uint32_t>(r) - pij) & tmask))
                                    : static_cast<int>((static_cast<std::uint32_t>(r) - pij) & tmask);
                 pos0 = sfx[cl * (n + 1) + (SYM ? j : 0)];
                 cnt = s_cend[cl] - pos0;
-                int d = static_cast<int>(__ldg(a.rowF + row)) - F;
-                d = d < 0 ? 0 : (d > 63 ? 63 : d);  // zero rows may sit below F; q >> 63 of |q| < 2^62 is 0 / -1
-                pwd = pij + (static_cast<std::uint32_t>(d) << 24);  // bucket sums < 3b <= 2^24 stay below bit 24
+                const bool ii = SYM && i == j;
+                pwd = pij + (ii ? (1u << 24) : 0u);  // bucket sums < 3b <= 2^24 stay below bit 24
+                if (SYM && cnt > 0) {
+                    // k = j: kappa 3 (i < j) or 1 (i = j) where the row walk applies 6 or 3
+                    const std::uint32_t lw0 = lst[pos0];
+                    if (static_cast<int>((lw0 >> KS) & kmask) == j) {
+                        const double x = static_cast<double>(xsrc[off + j]);
+                        const std::uint32_t p0 = pij + (lw0 & wmask);
+                        // -3 * 2^F = -1.5 * 2^(F+1);  -2 * 2^F = -1.0 * 2^(F+1)
+                        const std::uint32_t hi = ((static_cast<std::uint32_t>(1023 + F + 1) << 20) | (ii ? 0u : (1u << 19))) ^
+                                                 0x80000000u ^ (p0 & 0x80000000u);
+                        const unsigned long long qd = static_cast<unsigned long long>(to_fixed(x, hi));
+                        add64_idx((p0 & bmask) >> TB, sbase, hioff, static_cast<std::uint32_t>(qd),
+                                  static_cast<std::uint32_t>(qd >> 32));
+                    }
+                }
             }
             int incl = cnt;
 #pragma unroll
@@ -847,16 +923,15 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
             }
             const long long off0 = __shfl_sync(0xffffffffu, off, 0);
             const int E = __shfl_sync(0xffffffffu, incl, 31);
-            if (lane < nr)
-                meta[lane] = make_int4(incl, pos0 - (incl - cnt), static_cast<int>(off - off0) - (SYM ? j : 0), static_cast<int>(pwd));
+            if (lane < nr) meta[lane] = make_int4(incl, pos0 - (incl - cnt), static_cast<int>(off - off0), static_cast<int>(pwd));
             __syncwarp();
-            const long long* qch = a.qbuf + off0;
+            const XT* qch = xsrc + off0;
             asm volatile("mov.b64 %0, %0;" : "+l"(qch));  // one IMAD.WIDE per gather address
             int t = 0;
             int4 cur = meta[0];
             // load stage: list entry, gathered q and the packed word p = c_ij + h_k | d | e.
             // Lanes past the chunk end get q = 0 and a private slot (their add is a no-op).
-            auto fetch = [&](long long& q, std::uint32_t& p, int e) {
+            auto fetch = [&](XT& q, std::uint32_t& p, int e) {
                 if (e >= cur.x) {  // crossed into a later row of the chunk
                     cur = meta[++t];
                     while (e >= cur.x) cur = meta[++t];
@@ -867,7 +942,7 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
             };
             // Full 128-entry blocks skip the per-entry bound checks; in the chunk's last
             // block, lanes past the end get q = 0 and a private slot (a no-op add).
-            auto load4 = [&](long long (&q)[4], std::uint32_t (&p)[4], int eb) {
+            auto load4 = [&](XT (&q)[4], std::uint32_t (&p)[4], int eb) {
                 if (eb + 128 <= E) {
 #pragma unroll
                     for (int u = 0; u < 4; ++u) fetch(q[u], p[u], eb + lane + 32 * u);
@@ -881,18 +956,18 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
                     }
                 }
             };
-            auto process = [&](const long long (&q)[4], const std::uint32_t (&p)[4], int eb) {
+            auto process = [&](const XT (&q)[4], const std::uint32_t (&p)[4], int eb) {
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     if (eb + 32 * u >= E) break;  // warp-uniform
-                    const unsigned long long qq = static_cast<unsigned long long>(q[u] >> ((p[u] >> 24) & 63u));
-                    const bool neg = static_cast<int>(p[u]) < 0;
-                    const unsigned long long v = neg ? 0ull - qq : qq;
+                    // kappa * 2^F with the complex4 sign (bit 31 of p) in its sign bit
+                    const std::uint32_t hi = (SYM ? sc_hi0 - ((p[u] & (1u << 24)) >> 4) : sc_hi0) ^ (p[u] & 0x80000000u);
+                    const unsigned long long v = static_cast<unsigned long long>(to_fixed(static_cast<double>(q[u]), hi));
                     const std::uint32_t s = (p[u] & bmask) >> TB;
                     add64_idx(s, sbase, hioff, static_cast<std::uint32_t>(v), static_cast<std::uint32_t>(v >> 32));
                 }
             };
-            long long qa[4], qb[4];
+            XT qa[4], qb[4];
             std::uint32_t pa[4], pb[4];
             load4(qa, pa, 0);
             for (int eb = 0; eb < E; eb += 256) {
@@ -950,15 +1025,20 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
     }
 }
 
+template <bool SYM, int TB, typename XT>
+static void cls_launch2(cudaStream_t st, const BuildPlan& p, const BuildArgs& a, size_t smem) {
+    cudaFuncSetAttribute(k_build_cls<SYM, TB, XT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_build_cls<SYM, TB, XT><<<p.P, 1024, smem, st>>>(a);
+}
 template <int TB>
 static void cls_launch(cudaStream_t st, const BuildPlan& p, const BuildArgs& a) {
     const size_t smem = cls_smem_bytes(p.bmask + 1u, TB, p.n, p.sym);
     if (p.sym) {
-        cudaFuncSetAttribute(k_build_cls<true, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_build_cls<true, TB><<<p.P, 1024, smem, st>>>(a);
+        if (p.dtype == 0) cls_launch2<true, TB, double>(st, p, a, smem);
+        else cls_launch2<true, TB, float>(st, p, a, smem);
     } else {
-        cudaFuncSetAttribute(k_build_cls<false, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_build_cls<false, TB><<<p.P, 1024, smem, st>>>(a);
+        if (p.dtype == 0) cls_launch2<false, TB, double>(st, p, a, smem);
+        else cls_launch2<false, TB, float>(st, p, a, smem);
     }
     count_launch();
 }
@@ -1006,7 +1086,6 @@ size_t build_smem_bytes(long long slots_per_cta, int R, int n) {
 }
 
 void launch_build_main(cudaStream_t st, const void* T, const BuildPlan& p) {
-    (void)T;
     BuildArgs a;
     a.n = p.n;
     a.B = p.B;
@@ -1022,6 +1101,8 @@ void launch_build_main(cudaStream_t st, const void* T, const BuildPlan& p) {
     a.packed = p.packed;
     a.partials = p.prepass_partials;
     a.np = p.prepass_blocks;
+    a.xsrc = p.xsrc_mode == 1 ? T : static_cast<const void*>(p.qbuf);
+    a.xmode = p.xsrc_mode;
     a.scale_out = p.scale_exp;
     a.next_row = p.next_row;
     a.acc = p.acc;

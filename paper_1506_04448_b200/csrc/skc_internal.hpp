@@ -84,6 +84,9 @@ struct BuildPlan {
     int* next_row;               // G counters
     bool flat;                   // flat-chunk kernel or the row-walk kernel
     int cls_bits = -1;           // >= 0: class-list kernel, windows = (replicate, [parity,] bucket mod 2^cls_bits)
+    int xsrc_mode = 0;           // 0: pre-pass writes the fixed-point stream (contiguous-window kernels);
+                                 // 1: class-list kernel reads the device-resident T (pre-pass: sums only);
+                                 // 2: pre-pass writes a packed raw copy of the rows (bus-read T)
     unsigned long long* acc;     // total_slots exact fixed-point accumulators
     unsigned long long* trace;   // optional per-CTA (start, end, switches) (SKC_BUILD_TRACE)
     long long total_slots;   // B x 2b (sym) or B x b (asym)
