@@ -204,6 +204,88 @@ __global__ void __launch_bounds__(NTQ) k_build_quantize(const TT* __restrict__ T
     }
 }
 
+// Sums-only pre-pass for device-resident tensors (class-list builds): per row segment,
+// sum and max of |T| over k > k0 and the k = k0 entry separately, then kappa applied per
+// row (sym: 6/3 off the diagonal pair, 3/1 on it; asym 1). Coalesced 4-deep loads, two
+// floating-point ops per element; non-finite entries surface as a non-finite row sum.
+template <typename TT, bool SYM>
+__global__ void __launch_bounds__(256) k_build_sums(const TT* __restrict__ T, int n,
+                                                    const std::uint32_t* __restrict__ rowtab, int nrows,
+                                                    double* __restrict__ partials, int* __restrict__ nonfinite) {
+    constexpr int W = 8;
+    __shared__ double red[W];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double blk = 0.0, bmax = 0.0;
+    bool bad = false;
+    // two rows per warp step (their loads in flight together)
+    const int stride = gridDim.x * W;
+    for (int row = blockIdx.x * W + warp; row < nrows; row += 2 * stride) {
+        int ii[2], jj[2], kk0[2];
+        const TT* rp[2];
+        double v[2][4];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int rw = row + h * stride;
+            const bool ok = rw < nrows;
+            const std::uint32_t ij = ok ? rowtab[rw] : 0u;
+            ii[h] = static_cast<int>(ij >> 16);
+            jj[h] = static_cast<int>(ij & 0xFFFFu);
+            kk0[h] = ok ? (SYM ? jj[h] : 0) : n;
+            rp[h] = T + ((size_t)ii[h] * n + jj[h]) * n;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int k = kk0[h] + lane + 32 * u;
+                v[h][u] = (k < n) ? static_cast<double>(__ldg(rp[h] + k)) : 0.0;
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            double so = 0.0, mo = 0.0, dg = 0.0;
+            for (int kb = kk0[h] + lane; kb < n; kb += 128) {
+                if (kb != kk0[h] + lane) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) v[h][u] = (kb + 32 * u < n) ? static_cast<double>(__ldg(rp[h] + kb + 32 * u)) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const double a = fabs(v[h][u]);
+                    if (SYM && kb + 32 * u == kk0[h]) {
+                        dg = a;
+                    } else {
+                        so += a;
+                        mo = fmax(mo, a);
+                    }
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                so += __shfl_xor_sync(0xffffffffu, so, o);
+                mo = fmax(mo, __shfl_xor_sync(0xffffffffu, mo, o));
+            }
+            dg = __shfl_sync(0xffffffffu, dg, 0);  // lane 0 held k = k0
+            so = __shfl_sync(0xffffffffu, so, 0);
+            const int i = ii[h], j = jj[h];
+            const double ko = SYM ? (i == j ? 3.0 : 6.0) : 1.0, kd = SYM ? (i == j ? 1.0 : 3.0) : 1.0;
+            const double L1 = ko * so + kd * dg;
+            const double mx = fmax(ko * mo, kd * dg);
+            bad |= !isfinite(L1) || !isfinite(mx);
+            blk += (lane == 0) ? L1 : 0.0;
+            bmax = fmax(bmax, mx);
+        }
+    }
+    if (bad) atomicOr(nonfinite, 1);
+    const double s = block_sum_b<256>(blk, red);
+    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+    __syncthreads();
+    if (lane == 0) red[warp] = bmax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double mx = 0.0;
+        for (int w = 0; w < W; ++w) mx = fmax(mx, red[w]);
+        partials[gridDim.x + blockIdx.x] = mx;
+    }
+}
+
 // Default: kPrepassBlocks x 256 threads over all SMs (HBM-bound). Pipelined zero-copy
 // builds use p.prepass_blocks x 1024-thread blocks on a few SMs (PCIe-bound), leaving the
 // rest to the concurrent main pass of the previous chunk.
@@ -233,11 +315,12 @@ void launch_build_prepass(cudaStream_t st, const void* T, const BuildPlan& p) {
                                                                          p.prepass_partials, p.nonfinite, vec16);    \
         }                                                                                                             \
     }
-#define QUANT(TT, SY)                                \
-    {                                                \
-        if (mode == kQuant) QUANT_M(TT, SY, kQuant)  \
-        else if (mode == kRaw) QUANT_M(TT, SY, kRaw) \
-        else QUANT_M(TT, SY, kNone)                  \
+#define QUANT(TT, SY)                                                                                 \
+    {                                                                                                 \
+        if (mode == kQuant) QUANT_M(TT, SY, kQuant)                                                   \
+        else if (mode == kRaw) QUANT_M(TT, SY, kRaw)                                                  \
+        else k_build_sums<TT, SY><<<blocks, 256, 0, st>>>((const TT*)T, p.n, p.rowtab, p.nrows,      \
+                                                          p.prepass_partials, p.nonfinite);           \
     }
     if (p.sym) {
         if (p.dtype == 0) QUANT(double, true)
