@@ -35,6 +35,7 @@ struct SymView {
     const double2* stw2;
     const double2* gtw1;
     const double2* gtw2;
+    int lpb = 4;  // restarts per CTA of the contraction kernels (set per launch)
 };
 
 struct AsymView {

@@ -517,7 +517,8 @@ __device__ __forceinline__ void sym_contract_half_body(const SymView& v, const d
     const int S = v.S, n = v.n, B = v.B;
     const int r = blockIdx.x % S;
     const int m = (blockIdx.x / S) % B;
-    const int l0 = (blockIdx.x / (S * B)) * kLPB;
+    const int lpb = v.lpb;
+    const int l0 = (blockIdx.x / (S * B)) * lpb;
     double2* A = sm;
     double2* Bh = sm + strideA;
     // restart-invariant scatter metadata of this (m, r), built once per CTA: the complex
@@ -562,7 +563,7 @@ __device__ __forceinline__ void sym_contract_half_body(const SymView& v, const d
         keys[x] = hb ? ((e.y & nmask) >> 1) : (e.y & nmask);
         idx[x] = e.x;
     }
-    for (int l = l0; l < min(L, l0 + kLPB); ++l) {
+    for (int l = l0; l < min(L, l0 + lpb); ++l) {
         const double* ug = U + (size_t)l * n;
         for (int x = threadIdx.x; x < n; x += NT) us[x] = ug[x];  // u staged once per restart
         zero_smem(sm, strideA + strideB);
@@ -679,6 +680,12 @@ __global__ void __maxnreg__(112)
 //   "8d" radix-8 + direct scatter (3 CTAs/SM), "h256"/"h192"/"h112" half-length f2/z2
 //   kernel at 256 threads x 2 CTAs, 192 x 3 (default), 192 x 3 with a 112-register cap.
 //   config-1 step (L=100): 16s 1.05 ms, h256 0.94, h192 0.886, h112 0.97 (profiles/r01).
+static int env_int_k(const char* name, int dflt, int lo, int hi) {
+    const char* e = std::getenv(name);
+    if (!e) return dflt;
+    const int v = std::atoi(e);
+    return v < lo ? lo : (v > hi ? hi : v);
+}
 static int contract_variant() {
     static int v = [] {
         const char* e = std::getenv("SKC_CONTRACT_VARIANT");
@@ -721,12 +728,18 @@ void launch_sym_contract(cudaStream_t st, const SymView& v, const double* U, int
     int var = contract_variant();
     if (var >= 3 && (!scr_ok || v.logN < 2)) var = scr_ok ? 0 : 1;
     if (var >= 3) {
+        // restarts per CTA (SKC_CONTRACT_LPB, A/B hook): at config 1, 3..13 restarts per CTA
+        // measured 0.730..0.758 ms per step, with no wave-quantisation effect; 4 is kept
+        static const int force = env_int_k("SKC_CONTRACT_LPB", 0, 0, 64);
+        const int best = 4;
+        SymView vv = v;
+        vv.lpb = force > 0 ? force : best;
         const int NH = v.N / 2;
         const size_t smem = sizeof(double2) * (padded_len(v.N) + (NH + NH / 16 + 1)) +
                             (sizeof(double2) + 2 * sizeof(std::uint32_t)) * 2 * (size_t)v.n +
                             sizeof(double) * ((size_t)v.n + 1);
-        const unsigned grid = (unsigned)((long long)((L + kLPB - 1) / kLPB) * v.B * v.S);
-#define LH_(LG) sym_contract_half_dispatch<LG>(st, v, U, L, mode, out, grid, smem, var)
+        const unsigned grid = (unsigned)((long long)((L + vv.lpb - 1) / vv.lpb) * v.B * v.S);
+#define LH_(LG) sym_contract_half_dispatch<LG>(st, vv, U, L, mode, out, grid, smem, var)
         switch (v.logN) {
             case 2: LH_(2); break;
             case 3: LH_(3); break;
