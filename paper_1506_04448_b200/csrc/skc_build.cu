@@ -7,21 +7,23 @@
 //              sign xi1 xi2 xi3.
 //
 // Layout of the work. The B x b complex sketch set (5.2 MB at config 1) does not fit one
-// SM's shared memory and each tensor entry lands in B random buckets, so the slot space
-// (replicate, bucket, re/im) is cut into G contiguous ranges ("types") of ~27K slots
-// (~220 KB of limbs). One persistent 1024-thread CTA per SM holds one type's window and
-// streams the sorted-triple rows (coalesced, a lane per k), evaluating each entry
-// against the 1-2 replicates the window overlaps. Rows are handed out dynamically from
-// per-type atomic counters and CTAs migrate between types, so the SMs finish together
-// (a static split measured 1.3x max/avg imbalance from R=1 vs R=2 windows and short
-// rows). The measured alternative that enumerated only owned contributions through
-// per-class suffix tables executed 3x more instructions (profiles/).
+// SM's shared memory and each tensor entry lands in B random buckets. The default
+// kernel (k_build_cls) cuts the slot space into classes: a window is one (replicate,
+// parity, bucket residue) class, and for every row (i, j) the entries that land in it are
+// one contiguous run of a per-window class list of the k indices, so each (entry,
+// replicate) pair is evaluated exactly once. One persistent 1024-thread CTA per SM holds
+// one window; rows are handed out dynamically from per-window counters and CTAs migrate
+// between windows, so the SMs finish together and all windows sweep the rows in the same
+// order (their gathers of the same rows hit L2). The older contiguous-slot-range kernel
+// (k_build_flat: every CTA evaluates every entry against the 1-2 replicates its range
+// overlaps) remains for small asymmetric builds and as an A/B reference.
 //
 // Accumulation is exact 64-bit fixed point: q = round(kappa*T*2^F) is split into two
 // 32-bit limbs added with native ATOMS.ADD (shared fp64 atomics are CAS loops on
 // sm_100a); the carry out of the low limb is taken from the returned old value, so the
 // sum is exact mod 2^64 under any interleaving and the build is bit-deterministic.
-// F = 61 - ceil(log2(sum kappa|T|)) from a deterministic pre-pass bounds every bucket.
+// F = min(61 - ceil(log2(sum kappa|T|)), 50 - ceil(log2(max kappa|T|))) from a
+// deterministic pre-pass bounds every bucket sum by 2^62 and every single |q| by 2^50.
 #include <cuda_runtime.h>
 
 #include <algorithm>
