@@ -838,6 +838,49 @@ __global__ void __launch_bounds__(256) k_median_cols(const double* __restrict__ 
     med[t] = (Bn & 1) ? hi : 0.5 * (lo + hi);
 }
 
+// Tiled form: a block takes 32 consecutive columns i of one restart l. Its 256 threads
+// first sum the S residue partials of every (column, replicate) pair (coalesced over i,
+// same order as k_median_cols), then rank every pair within its column (ties by index),
+// so the L x n x B x S partials are read with 8x the parallelism of one thread per column.
+template <int BT>
+__global__ void __launch_bounds__(256) k_median_tile(const double* __restrict__ part, int L, int B, int S, int n,
+                                                      double* __restrict__ med) {
+    constexpr int CAP = BT > 0 ? BT : kMaxB;
+    __shared__ double est[CAP][33];
+    __shared__ double sel[2][32];
+    const int Bn = BT > 0 ? BT : B;
+    const int tiles = (n + 31) / 32;
+    const int l = blockIdx.x / tiles, i0 = (blockIdx.x - l * tiles) * 32;
+    const int il = threadIdx.x & 31;
+    const int i = i0 + il;
+    for (int m = threadIdx.x >> 5; m < Bn; m += 8) {
+        double sacc = 0.0;
+        if (i < n) {
+            const double* p = part + (((size_t)l * Bn + m) * S) * n + i;
+            sacc = p[0];
+            for (int r = 1; r < S; ++r) sacc += p[(size_t)r * n];
+        }
+        est[m][il] = sacc;
+    }
+    __syncthreads();
+    const int hiR = Bn / 2, loR = Bn / 2 - 1;
+    for (int a = threadIdx.x >> 5; a < Bn; a += 8) {
+        const double x = est[a][il];
+        int rank = 0;
+        for (int c = 0; c < Bn; ++c) {
+            const double y = est[c][il];
+            rank += (y < x) || (y == x && c < a);
+        }
+        if (rank == hiR) sel[1][il] = x;
+        if (rank == loR) sel[0][il] = x;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32 && i < n) {
+        const double hi = sel[1][il], lo = Bn > 1 ? sel[0][il] : 0.0;
+        med[(size_t)l * n + i] = (Bn & 1) ? hi : 0.5 * (lo + hi);
+    }
+}
+
 // Unext[l] = med[l] / ||med[l]|| (decompose.cpp:35-40), flags[l] set when ||.|| <= tol.
 __global__ void __launch_bounds__(256) k_normalize_rows(const double* __restrict__ med, int n,
                                                          double* __restrict__ Unext, double tol,
@@ -865,12 +908,26 @@ void launch_median_rows(cudaStream_t st, const double* part, int L, int B, int S
                         double tol, int* flags, double* scratch) {
     double* med = out ? out : scratch;
     const long long tot = (long long)L * n;
-    const unsigned grid = cdiv(tot, 256);
-    switch (B) {
-        case 10: k_median_cols<10><<<grid, 256, 0, st>>>(part, L, B, S, n, med); break;
-        case 20: k_median_cols<20><<<grid, 256, 0, st>>>(part, L, B, S, n, med); break;
-        case 40: k_median_cols<40><<<grid, 256, 0, st>>>(part, L, B, S, n, med); break;
-        default: k_median_cols<0><<<grid, 256, 0, st>>>(part, L, B, S, n, med); break;
+    static const bool cols = [] {
+        const char* e = std::getenv("SKC_MEDIAN_COLS");  // "1": one thread per column (A/B)
+        return e && std::atoi(e) == 1;
+    }();
+    if (cols) {
+        const unsigned grid = cdiv(tot, 256);
+        switch (B) {
+            case 10: k_median_cols<10><<<grid, 256, 0, st>>>(part, L, B, S, n, med); break;
+            case 20: k_median_cols<20><<<grid, 256, 0, st>>>(part, L, B, S, n, med); break;
+            case 40: k_median_cols<40><<<grid, 256, 0, st>>>(part, L, B, S, n, med); break;
+            default: k_median_cols<0><<<grid, 256, 0, st>>>(part, L, B, S, n, med); break;
+        }
+    } else {
+        const unsigned grid = static_cast<unsigned>((long long)L * ((n + 31) / 32));
+        switch (B) {
+            case 10: k_median_tile<10><<<grid, 256, 0, st>>>(part, L, B, S, n, med); break;
+            case 20: k_median_tile<20><<<grid, 256, 0, st>>>(part, L, B, S, n, med); break;
+            case 40: k_median_tile<40><<<grid, 256, 0, st>>>(part, L, B, S, n, med); break;
+            default: k_median_tile<0><<<grid, 256, 0, st>>>(part, L, B, S, n, med); break;
+        }
     }
     SKC_LAUNCHED();
     if (Unext) {
