@@ -514,6 +514,53 @@ def test_config1_full_size_build_and_contractions_match_oracle(gpu_ctx):
         assert abs(ws.vvv(U[l]) - o.vvv(U[l])) <= 1e-9 * abs(o.vvv(U[l]))
 
 
+# ---------------------------------------------------------------- BASELINE config 2 at full size
+def test_config2_full_size_properties(gpu_ctx):
+    """BASELINE config 2 (n=1000 fp32, b=2^16, B=10: the class-list kernel with two
+    bucket-class bits) through size-independent properties: the hash tables equal the
+    oracle's; the sketch of the planted tensor equals the sum of its four equal-work
+    i-slice sketches (the multi-GPU sharding identity) to 1e-11; and the sketch of a
+    sparse symmetric tensor equals the explicit sum over its sorted triples built from the
+    oracle's tables (kappa, bucket, complex4 sign) to 1e-12."""
+    import torch
+
+    from paper_1506_04448_b200.distributed import equal_work_slices
+
+    n, b, B, seed = 1000, 1 << 16, 10, 20150615
+    s = skb().SymTensorSketchSet(n, b, B, seed, gpu_ctx)
+    o = O.SymSet(n, b, B, seed)
+    for m in range(B):
+        t, ot = s.tables(m), o.tables(m)
+        for x, y in zip(t, ot[:4]):
+            assert np.array_equal(x, y)
+    T = torch.empty(n ** 3, dtype=torch.float32, device="cuda")
+    skb().gen_planted_tensor_device(gpu_ctx, n, 100, 0.01, seed, T.data_ptr(), dtype=np.float32)
+    s.accumulate_dense(T, assume_symmetric=True)
+    parts = skb().SymTensorSketchSet(n, b, B, seed, gpu_ctx)
+    for i0, i1 in equal_work_slices(n, 4):
+        parts.accumulate_dense(T, assume_symmetric=True, i0=i0, i1=i1)
+    assert rel_per_replicate(parts.data(), s.data()) <= 1e-11
+    del T
+    # sparse: three symmetric entries (distinct, two-equal, all-equal index patterns)
+    entries = {(3, 500, 999): 1.25, (7, 7, 640): -2.5, (999, 999, 999): 0.75}
+    Ts = torch.zeros((n, n, n), dtype=torch.float32, device="cuda")
+    import itertools
+
+    for (i, j, k), v in entries.items():
+        for pi in set(itertools.permutations((i, j, k))):
+            Ts[pi] = v
+    sp = skb().SymTensorSketchSet(n, b, B, seed, gpu_ctx)
+    sp.accumulate_dense(Ts.reshape(-1), assume_symmetric=True)
+    want = np.zeros((B, b), dtype=np.complex128)
+    root = [1, 1j, -1, -1j]
+    for m in range(B):
+        h, _, _, e = o.tables(m)[:4]
+        for (i, j, k), v in entries.items():
+            kappa = 6 if len({i, j, k}) == 3 else (3 if len({i, j, k}) == 2 else 1)
+            want[m, (int(h[i]) + int(h[j]) + int(h[k])) % b] += kappa * v * root[(int(e[i]) + int(e[j]) + int(e[k])) & 3]
+    assert rel_per_replicate(sp.data(), want) <= 1e-12
+
+
 # ---------------------------------------------------------------- RTPM at BASELINE config 0, full size
 def test_rtpm_config0_full_size_matches_oracle_fixture(gpu_ctx):
     """BASELINE config 0 in full (n=100, b=2^12, B=20, k=10, L=50, T=30) against the
