@@ -133,14 +133,16 @@ SKC_HD PassPlan make_plan(int N) {
 // One forward (DIF) pass on item w of array x (length N, padded smem layout).
 // tw: table of w_b^k = (cos 2 pi k / b, sin 2 pi k / b), k in [0, b).
 // logb_over: log2(b) used to index tw for stage twiddles w_{2hs}^{-pos}.
+// Core of a DIF pass item: loads the item's R inputs, runs the butterflies and leaves the
+// outputs in v (output q belongs at position base + q * g).
 template <int LOGR>
-SKC_HD void dif_pass_item(double2* x, int w, int h, const double2* tw, int logb) {
+SKC_HD void dif_item_core(double2* x, int w, int h, const double2* tw, int logb, double2 (&v)[1 << LOGR], int& base,
+                          int& g) {
     constexpr int R = 1 << LOGR;
-    const int g = (2 * h) >> LOGR;  // element spacing
+    g = (2 * h) >> LOGR;  // element spacing
     const int block = w / g;
     const int pos = w - block * g;
-    const int base = block * 2 * h + pos;
-    double2 v[R];
+    base = block * 2 * h + pos;
 #pragma unroll
     for (int q = 0; q < R; ++q) v[q] = x[pad16(base + q * g)];
     // stage twiddles: w_{2h}^{-pos} from the table, then w_{2hs}^{-pos} = (w_{2h}^{-pos})^(2^s)
@@ -161,6 +163,13 @@ SKC_HD void dif_pass_item(double2* x, int w, int h, const double2* tw, int logb)
             v[q + Hq] = cmul(d, tw2);
         }
     }
+}
+template <int LOGR>
+SKC_HD void dif_pass_item(double2* x, int w, int h, const double2* tw, int logb) {
+    constexpr int R = 1 << LOGR;
+    double2 v[R];
+    int base, g;
+    dif_item_core<LOGR>(x, w, h, tw, logb, v, base, g);
 #pragma unroll
     for (int q = 0; q < R; ++q) x[pad16(base + q * g)] = v[q];
 }
@@ -275,6 +284,25 @@ struct DitPasses<LOGN, LR, -1> {
 template <int LOGN, int LR = 4>
 __device__ __forceinline__ void dif_local(double2* sm, int na, const double2* twl) {
     DifPasses<LOGN, LR, 0>::run(sm, na, twl);
+}
+// DIF of one padded array whose last pass hands every output (local position j, value)
+// to epi instead of storing it, so a pointwise epilogue (e.g. the moment cube-accumulate)
+// needs no extra pass over shared memory; epi owns A[pad16(j)] (each j is visited once).
+// The caller synchronises afterwards.
+template <int LOGN, int LR, typename Epi>
+__device__ __forceinline__ void dif_local_epilogue(double2* A, const double2* twl, Epi epi) {
+    constexpr int NP = plan_npass(LOGN, LR);
+    DifPasses<LOGN, LR, 0, NP - 1>::run(A, 1, twl);
+    constexpr int R_ = plan_logr(LOGN, NP - 1, LR);
+    constexpr int H = plan_h(LOGN, NP - 1, LR);
+    constexpr int items = (1 << LOGN) >> R_;
+    for (int w = threadIdx.x; w < items; w += blockDim.x) {
+        double2 v[1 << R_];
+        int base, g;
+        dif_item_core<R_>(A, w, H, twl, LOGN, v, base, g);
+#pragma unroll
+        for (int q = 0; q < (1 << R_); ++q) epi(base + q * g, v[q]);
+    }
 }
 template <int LOGN, int LR = 4>
 __device__ __forceinline__ void dit_local(double2* sm, int na, const double2* twl) {

@@ -1017,7 +1017,9 @@ __global__ void __launch_bounds__(kFftThreads, SKC_FFT_MINB)
     // SCR: the sample-invariant scatter metadata of this (m, r) (weight root4(e)
     // conj(w_b^{r t}), local key, index i) is built once; per sample a run head sums
     // wv[q] x[idx[q]] over its run.
-    double2* wv = ACC + N + 8;                                         // n (SCR)
+    // ACC uses the padded layout of A: the fused last DIF pass touches 16 consecutive
+    // positions per thread, which the padding spreads over the banks
+    double2* wv = ACC + stride;                                        // n (SCR)
     std::uint32_t* keys = reinterpret_cast<std::uint32_t*>(wv + n);   // n (SCR)
     std::uint32_t* idx = keys + n;                                     // n (SCR)
     double* xs = reinterpret_cast<double*>(idx + n);  // 2 x n (SCR): sample double buffer (2n u32: 8-byte aligned)
@@ -1026,7 +1028,7 @@ __global__ void __launch_bounds__(kFftThreads, SKC_FFT_MINB)
     const uint2* plan = v.plan1 + (size_t)m * n;
     const std::uint32_t bmask = v.b - 1;
     const std::uint32_t nmask = static_cast<std::uint32_t>(N - 1);
-    zero_smem(ACC, N + 8);
+    zero_smem(ACC, stride);
     zero_smem(A, stride);
     if (SCR) {
         const double2* stw = v.stw1 ? v.stw1 + ((size_t)m * S + r) * n : nullptr;
@@ -1077,18 +1079,17 @@ __global__ void __launch_bounds__(kFftThreads, SKC_FFT_MINB)
             scatter_plan(A, plan, n, N, r, bmask, 0x0FFFFFFFu, v.tw, vx);
         }
         __syncthreads();
-        dif_local<LOGN, LR>(A, 1, v.twl);
         const double ws = (w ? w[s] : 1.0) * wscale;
-        for (int j = threadIdx.x; j < N; j += blockDim.x) {
-            const double2 z = A[pad16(j)];
+        // the last DIF pass feeds the cube-accumulate directly (no extra pass over A)
+        dif_local_epilogue<LOGN, LR>(A, v.twl, [&](int j, double2 z) {
             A[pad16(j)] = mk(0.0, 0.0);  // ready for the next sample's scatter
             const double2 z3 = cmul(cmul(z, z), z);
-            ACC[j] = cadd(ACC[j], cscale(z3, ws));
-        }
+            ACC[pad16(j)] = cadd(ACC[pad16(j)], cscale(z3, ws));
+        });
         __syncthreads();
     }
     double2* o = reinterpret_cast<double2*>(acc) + (((size_t)ch * B + m) * S + r) * N;
-    for (int j = threadIdx.x; j < N; j += blockDim.x) o[j] = ACC[j];
+    for (int j = threadIdx.x; j < N; j += blockDim.x) o[j] = ACC[pad16(j)];
 }
 // Max radix of the local DIF passes (A/B hook): 4 = radix-16 (make_plan), 3 = radix-8.
 static int env_lr(const char* name) {
@@ -1114,7 +1115,7 @@ static void moment_launch(cudaStream_t st, const SymView& v, const double* X, co
 void launch_sym_moment_accumulate(cudaStream_t st, const SymView& v, const double* X, const double* w, double wscale,
                                   long long Nsamp, int chunks, double* acc) {
     const bool scr = v.n <= kScatterMax;
-    const size_t smem = sizeof(double2) * (padded_len(v.N) + v.N + 8) +
+    const size_t smem = sizeof(double2) * (2 * padded_len(v.N)) +
                         (scr ? (sizeof(double2) + 2 * sizeof(std::uint32_t) + 2 * sizeof(double)) * (size_t)v.n + 8 : 0);
     const unsigned grid = (unsigned)((long long)chunks * v.B * v.S);
     static const int lr = env_lr("SKC_MOMENT_LR");

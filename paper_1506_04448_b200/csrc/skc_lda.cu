@@ -267,15 +267,15 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int ch = blockIdx.x / (S * B);
     double2* A = sm;
     double2* ACC = sm + stride;
-    double2* CR = ACC + N;
-    ScatterMeta mt{CR + N, nullptr, nullptr};
+    double2* CR = ACC + stride;  // ACC and CR padded like A (the fused last DIF pass writes 16 consecutive positions per thread)
+    ScatterMeta mt{CR + stride, nullptr, nullptr};
     mt.keys = reinterpret_cast<std::uint32_t*>(mt.wv + n);
     mt.idx = mt.keys + n;
     double* rows = reinterpret_cast<double*>(mt.idx + n);  // 2 x n (2n u32: 8-byte aligned)
     const long long per = (Du + chunks - 1) / chunks;
     const long long i0 = (long long)ch * per, i1 = min(Du, i0 + per);
     zero_sm(A, stride);
-    zero_sm(ACC, 2 * N);
+    zero_sm(ACC, 2 * stride);
     build_meta(mt, v.plan1 + (size_t)m * n, v.stw1 ? v.stw1 + ((size_t)m * S + r) * n : nullptr, v.tw, n, N, r,
                v.b - 1);
     if (i0 < i1) async_row(rows, P + (size_t)used_docs[i0] * n, n);
@@ -288,22 +288,21 @@ __global__ void __launch_bounds__(kThreads, 2)
         const long long d = used_docs[it];
         scatter_meta(A, mt, rows + (size_t)((it - i0) & 1) * n, n);
         __syncthreads();
-        dif_local<LOGN>(A, 1, v.twl);
         const double a1 = s1[d], a2 = s2[d];
-        for (int j = threadIdx.x; j < N; j += blockDim.x) {
-            const double2 f = A[pad16(j)];
+        // the last DIF pass feeds the accumulators directly (no extra pass over A)
+        dif_local_epilogue<LOGN, 4>(A, v.twl, [&](int j, double2 f) {
             A[pad16(j)] = mk(0.0, 0.0);
             const double2 sq = cmul(f, f);
-            ACC[j] = cadd(ACC[j], cscale(cmul(sq, f), a1));  // lda.cpp:205
-            CR[j] = cadd(CR[j], cscale(sq, a2));              // lda.cpp:206
-        }
+            ACC[pad16(j)] = cadd(ACC[pad16(j)], cscale(cmul(sq, f), a1));  // lda.cpp:205
+            CR[pad16(j)] = cadd(CR[pad16(j)], cscale(sq, a2));              // lda.cpp:206
+        });
     }
     __syncthreads();
     double2* ao = reinterpret_cast<double2*>(acc_out) + (((size_t)ch * B + m) * S + r) * N;
     double2* co = reinterpret_cast<double2*>(cross_out) + (((size_t)ch * B + m) * S + r) * N;
     for (int j = threadIdx.x; j < N; j += blockDim.x) {
-        ao[j] = ACC[j];
-        co[j] = CR[j];
+        ao[j] = ACC[pad16(j)];
+        co[j] = CR[pad16(j)];
     }
 }
 
@@ -435,7 +434,7 @@ void launch_lda_accumulate(cudaStream_t st, const SymView& v, long long Du, cons
                            const double* s1, const double* s2, int V, const double* W, const double* coeff1,
                            const double* sumwn, int chunks_d, int chunks_v, double* acc, double* cross) {
     const size_t meta = (sizeof(double2) + 2 * sizeof(std::uint32_t)) * (size_t)v.n;
-    const size_t smem_d = sizeof(double2) * (padded_len(v.N) + 2 * v.N) + meta + 2 * sizeof(double) * (size_t)v.n;
+    const size_t smem_d = sizeof(double2) * (3 * padded_len(v.N)) + meta + 2 * sizeof(double) * (size_t)v.n;
     const size_t smem_v = sizeof(double2) * (2 * padded_len(v.N) + v.N) + meta + 4 * sizeof(double) * (size_t)v.n;
     const unsigned grid_d = (unsigned)((long long)chunks_d * v.B * v.S);
     const unsigned grid_v = (unsigned)((long long)chunks_v * v.B * v.S);
