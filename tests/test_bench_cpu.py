@@ -1,0 +1,31 @@
+"""bench.py contract checks that need no GPU: the reference arm's JSON line (the oracle
+restatement timed on the host cores) and the roofline helpers."""
+import json
+import pathlib
+import subprocess
+import sys
+
+ROOT = pathlib.Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+
+def test_reference_arm_json_line():
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--steps", "1", "--warmup", "1"],
+                         check=True, capture_output=True, text=True, cwd=str(ROOT), timeout=600)
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference"
+    assert line["value"] > 0 and line["unit"] == "entries/s" and line["higher_is_better"] is True
+    assert line["cpu_baseline"]["kind"] in ("port", "reference") and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["value"] == line["value"]
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
+    assert line["config"]["n"] == 400 and line["config"]["b"] == 1 << 14 and line["config"]["B"] == 20
+
+
+def test_scatter_roofline_uses_measured_ceiling():
+    import bench
+
+    r = bench.scatter_roofline(10746800 * 20, 0.43)
+    assert r["bound"] == "smem_atomics" and r["unit"] == "u32 atomics/s"
+    assert 0.0 < r["frac"] < 1.0
+    assert abs(r["achieved"] - 2 * 10746800 * 20 / 0.43e-3) < 1.0
+    assert bench.scatter_roofline(1, None) is None
