@@ -67,6 +67,11 @@ int skc_context_destroy(skc_context* ctx) {
         cudaStreamSynchronize(ctx->stream);
         if (ctx->stream2) cudaStreamSynchronize(ctx->stream2);
         if (ctx->cublas) cublasDestroy(ctx->cublas);
+        for (auto& r : ctx->prof) {
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+        for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
         cudaStream_t st = ctx->stream, st2 = ctx->stream2;
         cudaEvent_t ev[5];
         for (int c = 0; c < 5; ++c) ev[c] = ctx->ev_q[c];
@@ -87,7 +92,14 @@ int skc_context_synchronize(skc_context* ctx) {
 int skc_profile_enable(skc_context* ctx, int on) {
     return guard([&] {
         check_vec(ctx, "context");
+        ctx->use();
         ctx->prof_on = on != 0;
+        // pre-create events so timed loops under profiling pay no event creation
+        while (ctx->prof_on && ctx->ev_pool.size() < 512) {
+            cudaEvent_t e = nullptr;
+            CK(cudaEventCreate(&e));
+            ctx->ev_pool.push_back(e);
+        }
     });
 }
 int skc_profile_reset(skc_context* ctx) {
@@ -95,9 +107,9 @@ int skc_profile_reset(skc_context* ctx) {
         check_vec(ctx, "context");
         ctx->use();
         ctx->sync();
-        for (auto& r : ctx->prof) {
-            cudaEventDestroy(r.a);
-            cudaEventDestroy(r.b);
+        for (auto& r : ctx->prof) {  // back to the pool
+            ctx->ev_pool.push_back(r.a);
+            ctx->ev_pool.push_back(r.b);
         }
         ctx->prof.clear();
     });

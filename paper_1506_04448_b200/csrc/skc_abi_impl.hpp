@@ -161,6 +161,17 @@ struct skc_context {
     };
     bool prof_on = false;
     std::vector<ProfRec> prof;
+    std::vector<cudaEvent_t> ev_pool;  // recycled profiling events (creation costs host time in timed loops)
+    cudaEvent_t pooled_event() {
+        if (!ev_pool.empty()) {
+            cudaEvent_t e = ev_pool.back();
+            ev_pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e = nullptr;
+        CK(cudaEventCreate(&e));
+        return e;
+    }
 
     void use() const { CK(cudaSetDevice(device)); }
     // w_N^k tables for the CTA-local transforms (contiguous; the full-b table would be
@@ -208,13 +219,18 @@ struct ProfScope {
     cudaEvent_t a = nullptr;
     ProfScope(skc_context* ctx, const char* nm) : c(ctx), name(nm) {
         if (!c->prof_on) return;
-        CK(cudaEventCreate(&a));
+        a = c->pooled_event();
         CK(cudaEventRecord(a, c->stream));
     }
     ~ProfScope() {
         if (!c->prof_on || !a) return;
         cudaEvent_t b = nullptr;
-        if (cudaEventCreate(&b) != cudaSuccess) return;
+        if (!c->ev_pool.empty()) {
+            b = c->ev_pool.back();
+            c->ev_pool.pop_back();
+        } else if (cudaEventCreate(&b) != cudaSuccess) {
+            return;
+        }
         cudaEventRecord(b, c->stream);
         c->prof.push_back({name, a, b});
     }
