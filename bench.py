@@ -42,28 +42,70 @@ def simplex_entries(n, i0=0, i1=None):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled during the timed region.
+
+    NVML (pynvml) is queried every ~1 ms from a side thread, so even a ~20 ms timed region
+    gets a median over many samples; nvidia-smi (~50 ms per query) is the fallback."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event reason bits: hw_slowdown, hw_thermal_slowdown, sw_thermal_slowdown, sw_power_cap
+    BITS = (0x8, 0x40, 0x20, 0x4)
 
-    def __init__(self, device):
+    def __init__(self, device, interval=0.001):
         self.device = device
+        self.interval = interval
         self.rows = []
+        self.source = None
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._h = None
+            try:  # the CUDA ordinal may differ from NVML's index: match by PCI bus id
+                import torch
+
+                pr = torch.cuda.get_device_properties(int(device))
+                bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+                self._h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                self._h = pynvml.nvmlDeviceGetHandleByIndex(int(device))
+            self._max = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._nvml = pynvml
+        except Exception:
+            self._nvml = None
+
+    def _sample_nvml(self):
+        nv = self._nvml
+        sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+        try:
+            rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        except Exception:
+            rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+        self.rows.append([str(sm), str(self._max), hex(rs)] + ["Active" if rs & bit else "Not Active" for bit in self.BITS])
+
+    def _sample_smi(self):
+        out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+        if out.returncode == 0 and out.stdout.strip():
+            self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                if out.returncode == 0 and out.stdout.strip():
-                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+                if self._nvml is not None:
+                    self._sample_nvml()
+                    self.source = "nvml"
+                else:
+                    self._sample_smi()
+                    self.source = "nvidia-smi"
             except Exception:
-                pass
-            self._stop.wait(0.2)
+                self._nvml = None  # fall back to nvidia-smi for the rest of the region
+            self._stop.wait(self.interval if self._nvml is not None else 0.2)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -73,6 +115,11 @@ class ClockSampler:
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=10)
+        if not self.rows:  # region shorter than one query: take one right after it
+            try:
+                self._sample_nvml() if self._nvml is not None else self._sample_smi()
+            except Exception:
+                pass
 
     def summary(self):
         if not self.rows:
@@ -82,7 +129,8 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[k] for r in self.rows for k in range(4) if len(r) > 3 + k and r[3 + k] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "sm_min_mhz": min(sm) if sm else None, "reasons": reasons, "samples": len(self.rows),
+                "source": self.source}
 
 
 def peaks():
