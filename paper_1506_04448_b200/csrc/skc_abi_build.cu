@@ -263,6 +263,11 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
     } else {
         ensure_clean();
         ctx->build_scratch_clean = false;
+        static const bool pdl_on = [] {
+            const char* e = std::getenv("SKC_BUILD_PDL");  // "0": A/B switch for the PDL launches
+            return !(e && std::string(e) == "0");
+        }();
+        p.pdl = pdl_on;
         {
             SKC_PROF(ctx, "build_prepass");
             launch_build_prepass(ctx->stream, Tdev, p);

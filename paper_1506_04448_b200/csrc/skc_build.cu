@@ -35,6 +35,23 @@
 namespace skc {
 
 namespace {
+// Launch with programmatic stream serialization when pdl is set: the kernel may begin
+// before its predecessor finishes and must griddepcontrol.wait before reading its output.
+template <typename... KA, typename... Args>
+void pdl_launch(void (*kern)(KA...), unsigned grid, unsigned block, size_t smem, cudaStream_t st, bool pdl,
+                Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, static_cast<KA>(args)...);
+}
 inline unsigned cdiv(long long a, long long b) { return static_cast<unsigned>((a + b - 1) / b); }
 
 template <int NT>
@@ -216,6 +233,9 @@ __global__ void __launch_bounds__(256) k_build_sums(const TT* __restrict__ T, in
                                                     double* __restrict__ partials, int* __restrict__ nonfinite) {
     constexpr int W = 8;
     __shared__ double red[W];
+    // the main pass (launched programmatically dependent) may start its prologue now; it
+    // waits on griddepcontrol.wait before reading these partials
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double blk = 0.0, bmax = 0.0;
     bool bad = false;
@@ -848,7 +868,10 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
     // source element index of (i, j, 0) relative to the chunk, c_ij | [i == j] << 24 | e_ij << 30)
     int4* meta = reinterpret_cast<int4*>(
         sm + ((static_cast<size_t>(2 * W + 3 * n + cls_sfx_words(C, n)) + 3) & ~static_cast<size_t>(3))) + warp * kClsRows;
-    const int F = cta_scale_exp(a);
+    // F comes from the pre-pass partials: read after griddepcontrol.wait, which the first
+    // window's prologue (zeroing, hash words, class lists) runs ahead of (PDL launch)
+    int F = 0;
+    bool have_F = false;
     std::uint32_t sbase = static_cast<std::uint32_t>(__cvta_generic_to_shared(sm));
     asm volatile("mov.b32 %0, %0;" : "+r"(sbase));
     const std::uint32_t hioff = pin(4u * static_cast<std::uint32_t>(W));
@@ -860,8 +883,7 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
     const XT* __restrict__ xsrc = static_cast<const XT*>(a.xsrc);
     // high word of kappa * 2^F: sym kappa 6 = 1.5 * 2^2 (kappa 3 is one exponent step less);
     // asym kappa 1
-    const std::uint32_t sc_hi0 = pin(SYM ? ((static_cast<std::uint32_t>(1023 + F + 2) << 20) | (1u << 19))
-                                         : (static_cast<std::uint32_t>(1023 + F) << 20));
+    std::uint32_t sc_hi0 = 0;
     constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
     constexpr long long kMagicBits = 0x4338000000000000ll;
     // exact round(x * sc): |x * sc| < 2^50, one rounding in the fma
@@ -960,6 +982,14 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
             if (lane < C) sfx[lane * (n + 1) + n] = static_cast<unsigned short>(run);
         }
         __syncthreads();
+        if (!have_F) {  // block-uniform
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            F = cta_scale_exp(a);
+            sc_hi0 = pin(SYM ? ((static_cast<std::uint32_t>(1023 + F + 2) << 20) | (1u << 19))
+                             : (static_cast<std::uint32_t>(1023 + F) << 20));
+            have_F = true;
+            asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        }
 
         int c0 = 0;
         if (lane == 0) c0 = atomicAdd(a.next_row + g, kClsRows);
@@ -1113,7 +1143,7 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
 template <bool SYM, int TB, typename XT>
 static void cls_launch2(cudaStream_t st, const BuildPlan& p, const BuildArgs& a, size_t smem) {
     cudaFuncSetAttribute(k_build_cls<SYM, TB, XT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_build_cls<SYM, TB, XT><<<p.P, 1024, smem, st>>>(a);
+    pdl_launch(k_build_cls<SYM, TB, XT>, p.P, 1024, smem, st, p.pdl, a);
 }
 template <int TB>
 static void cls_launch(cudaStream_t st, const BuildPlan& p, const BuildArgs& a) {
@@ -1236,6 +1266,7 @@ __global__ void k_build_finalize(unsigned long long* __restrict__ acc, long long
     // 4 slots per thread (strided by the grid) so each thread has independent loads in flight
     const long long base = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // main pass complete (PDL launch)
     if (base < ncounters) counters[base] = 0;
     const bool bad = *nonfinite != 0;
     const double sc = pow2_neg(*scale_exp);
@@ -1301,12 +1332,13 @@ void launch_build_finalize_multi(cudaStream_t st, const BuildPlan& p, int K, con
 
 void launch_build_finalize(cudaStream_t st, const BuildPlan& p) {
     const unsigned grid = cdiv(std::max<long long>((p.total_slots + 3) / 4, p.G), 256);
+    const bool pdl = p.pdl && p.cls_bits >= 0;  // only the class-list main pass triggers early
     if (p.sym)
-        k_build_finalize<true><<<grid, 256, 0, st>>>(p.acc, p.total_slots, p.scale_exp, p.nonfinite, p.data_as_double,
-                                                     p.next_row, p.G, p.cls_bits, p.bmask);
+        pdl_launch(k_build_finalize<true>, grid, 256, 0, st, pdl, p.acc, p.total_slots, p.scale_exp, p.nonfinite,
+                   p.data_as_double, p.next_row, p.G, p.cls_bits, p.bmask);
     else
-        k_build_finalize<false><<<grid, 256, 0, st>>>(p.acc, p.total_slots, p.scale_exp, p.nonfinite, p.data_as_double,
-                                                      p.next_row, p.G, p.cls_bits, p.bmask);
+        pdl_launch(k_build_finalize<false>, grid, 256, 0, st, pdl, p.acc, p.total_slots, p.scale_exp, p.nonfinite,
+                   p.data_as_double, p.next_row, p.G, p.cls_bits, p.bmask);
     count_launch();
 }
 
