@@ -268,6 +268,13 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
             return !(e && std::string(e) == "0");
         }();
         p.pdl = pdl_on;
+        if (p.xsrc_mode == 1) {  // device-resident class-list build: sums-only pre-pass
+            static const int sums_bps = env_int("SKC_SUMS_BPS", 5, 0, 8);  // 0: previous kernel (A/B)
+            if (sums_bps > 0) {
+                p.lean_sums = true;
+                p.prepass_blocks = std::min(kPrepassBlocks, std::max(1, ctx->sms) * sums_bps);
+            }
+        }
         {
             SKC_PROF(ctx, "build_prepass");
             launch_build_prepass(ctx->stream, Tdev, p);

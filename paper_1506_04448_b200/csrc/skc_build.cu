@@ -308,11 +308,88 @@ __global__ void __launch_bounds__(256) k_build_sums(const TT* __restrict__ T, in
     }
 }
 
+// Lean sums-only pre-pass (default for device-resident class-list builds). Each lane
+// keeps its own kappa-weighted L1 sum and maximum across all the rows its warp visits:
+// kappa is applied per element (the k = k0 entry takes the diagonal weight), so no row
+// needs a warp reduction; one block reduction at the end. Rows are dealt to warps in
+// grid-strided pairs with all of a pair's loads issued before any is consumed.
+// Non-finite entries surface as a non-finite lane sum.
+template <typename TT, bool SYM>
+__global__ void __launch_bounds__(256, 5) k_build_sums_lean(const TT* __restrict__ T, int n,
+                                                            const std::uint32_t* __restrict__ rowtab, int nrows,
+                                                            double* __restrict__ partials, int* __restrict__ nonfinite) {
+    constexpr int W = 8, U = 4;
+    __shared__ double red[W];
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double acc = 0.0, mx = 0.0;
+    const int stride = gridDim.x * W;
+    const int row0 = blockIdx.x * W + warp;
+    std::uint32_t nij[2];  // the next pair's (i, j) words, fetched one step ahead
+#pragma unroll
+    for (int h = 0; h < 2; ++h) nij[h] = row0 + h * stride < nrows ? __ldg(rowtab + row0 + h * stride) : 0u;
+    for (int row = row0; row < nrows; row += 2 * stride) {
+        const TT* rp[2];
+        int k0[2];
+        bool dg[2];
+        TT v[2][U];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int rw = row + h * stride;
+            const bool ok = rw < nrows;
+            const std::uint32_t ij = nij[h];
+            nij[h] = rw + 2 * stride < nrows ? __ldg(rowtab + rw + 2 * stride) : 0u;
+            const int i = static_cast<int>(ij >> 16), j = static_cast<int>(ij & 0xFFFFu);
+            k0[h] = ok ? (SYM ? j : 0) : n;
+            rp[h] = T + ((size_t)i * n + j) * n;
+            dg[h] = i == j;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int k = k0[h] + lane + 32 * u;
+                v[h][u] = k < n ? __ldg(rp[h] + k) : TT(0);
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            for (int kb = k0[h] + lane;; kb += 32 * U) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    // kappa: 6 (3 if i = j) off the k = k0 entry, 3 (1 if i = j) on it
+                    const double w = !SYM ? 1.0
+                                          : (kb + 32 * u == k0[h] ? (dg[h] ? 1.0 : 3.0) : (dg[h] ? 3.0 : 6.0));
+                    const double a = w * fabs(static_cast<double>(v[h][u]));
+                    acc += a;
+                    mx = fmax(mx, a);
+                }
+                if (kb + 32 * U >= n) break;
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int k = kb + 32 * U + 32 * u;
+                    v[h][u] = k < n ? __ldg(rp[h] + k) : TT(0);
+                }
+            }
+        }
+    }
+    // (no flag write: the main pass derives it from these partials)
+    const double s = block_sum_b<256>(acc, red);
+    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    __syncthreads();
+    if (lane == 0) red[warp] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = 0.0;
+        for (int w = 0; w < W; ++w) m = fmax(m, red[w]);
+        partials[gridDim.x + blockIdx.x] = m;
+    }
+}
+
 // Default: kPrepassBlocks x 256 threads over all SMs (HBM-bound). Pipelined zero-copy
 // builds use p.prepass_blocks x 1024-thread blocks on a few SMs (PCIe-bound), leaving the
 // rest to the concurrent main pass of the previous chunk.
 void launch_build_prepass(cudaStream_t st, const void* T, const BuildPlan& p) {
-    if (p.reset_nonfinite) cudaMemsetAsync(p.nonfinite, 0, sizeof(int), st);
+    if (p.reset_nonfinite && !p.lean_sums) cudaMemsetAsync(p.nonfinite, 0, sizeof(int), st);
     const bool wide = p.prepass_threads == 1024;
     const int blocks = p.prepass_blocks;
     const bool vec16 = (reinterpret_cast<std::uintptr_t>(T) & 15) == 0;
@@ -341,6 +418,8 @@ void launch_build_prepass(cudaStream_t st, const void* T, const BuildPlan& p) {
     {                                                                                                 \
         if (mode == kQuant) QUANT_M(TT, SY, kQuant)                                                   \
         else if (mode == kRaw) QUANT_M(TT, SY, kRaw)                                                  \
+        else if (p.lean_sums) k_build_sums_lean<TT, SY><<<blocks, 256, 0, st>>>(                      \
+            (const TT*)T, p.n, p.rowtab, p.nrows, p.prepass_partials, p.nonfinite);                   \
         else k_build_sums<TT, SY><<<blocks, 256, 0, st>>>((const TT*)T, p.n, p.rowtab, p.nrows,      \
                                                           p.prepass_partials, p.nonfinite);           \
     }
@@ -415,6 +494,7 @@ struct BuildArgs {
     const void* xsrc;              // class-list kernel: T itself (xmode 1) or its packed row copy (xmode 2)
     int xmode;
     int* scale_out;                // global exponent F, written by CTA 0 for the finalize
+    int* nonfinite_out;            // lean pre-pass: CTA 0 stores the flag from the partials (no memset)
     int* next_row;                 // G row (or tile) counters (zero on entry; the finalize re-zeroes them)
 
     unsigned long long* acc;       // total_slots exact accumulators (zero on entry; the finalize re-zeroes them)
@@ -449,7 +529,11 @@ __device__ int cta_scale_exp(const BuildArgs& a) {
                 F = F > 1000 ? 1000 : (F < -1000 ? -1000 : F);
             }
             sF = F;
-            if (blockIdx.x == 0) *a.scale_out = F;
+            if (blockIdx.x == 0) {
+                *a.scale_out = F;
+                // a non-finite entry makes its lane's (non-negative) sum, hence acc, non-finite
+                if (a.nonfinite_out) *a.nonfinite_out = isfinite(acc) ? 0 : 1;
+            }
         }
     }
     __syncthreads();
@@ -1219,6 +1303,7 @@ void launch_build_main(cudaStream_t st, const void* T, const BuildPlan& p) {
     a.xsrc = p.xsrc_mode == 1 ? T : static_cast<const void*>(p.qbuf);
     a.xmode = p.xsrc_mode;
     a.scale_out = p.scale_exp;
+    a.nonfinite_out = p.lean_sums ? p.nonfinite : nullptr;
     a.next_row = p.next_row;
     a.acc = p.acc;
 

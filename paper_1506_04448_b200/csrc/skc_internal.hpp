@@ -102,6 +102,7 @@ struct BuildPlan {
     double* prepass_partials;     // prepass_blocks
     int prepass_blocks = 1024, prepass_threads = 256, prepass_warps = 8;
     bool reset_nonfinite = true;
+    bool lean_sums = false;  // device-resident sums pre-pass: k_build_sums_lean
     bool pdl = false;  // main and finalize launched programmatically dependent (single-stream build)
     int* scale_exp;               // device int
     int* nonfinite;               // device int
