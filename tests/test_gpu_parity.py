@@ -286,6 +286,42 @@ def test_nonfinite_input_rejected(gpu_ctx):
         s.accumulate_dense(T, assume_symmetric=True)
 
 
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
+def test_nonfinite_device_tensor_rejected_then_next_build_clean(gpu_ctx, bad):
+    """Device-resident builds derive the non-finite flag from the sums pre-pass partials
+    (no per-call reset): a rejected build leaves the set untouched and the next valid
+    build on the same context succeeds and matches the oracle."""
+    import torch
+
+    n = 37
+    T = sym_tensor(n, 5)
+    ref = O.SymSet(n, 1024, 4, 3)
+    ref.accumulate_dense(T, True)
+    s = skb().SymTensorSketchSet(n, 1024, 4, 3, gpu_ctx)
+    Tb = T.copy()
+    for idx in [(3, 7, 20), (7, 20, 3), (20, 3, 7), (3, 20, 7), (7, 3, 20), (20, 7, 3)]:
+        Tb[idx] = bad
+    before = s.data().copy()
+    with pytest.raises(ValueError):
+        s.accumulate_dense(torch.from_numpy(Tb).cuda(), assume_symmetric=True)
+    assert np.array_equal(s.data(), before)
+    s.accumulate_dense(torch.from_numpy(T).cuda(), assume_symmetric=True)
+    assert rel_per_replicate(s.data(), ref.data()) <= SKETCH_TOL
+    # asymmetric set, large enough for the class-list build (and its lean pre-pass)
+    na = 170
+    Ta = np.random.default_rng(8).standard_normal((na, na, na))
+    aref = O.AsymSet(na, 2048, 2, 5)
+    aref.accumulate_dense(Ta)
+    a = skb().AsymTensorSketchSet(na, 2048, 2, 5, gpu_ctx)
+    Tab = Ta.copy()
+    Tab[na - 1, 0, na // 2] = bad
+    with pytest.raises(ValueError):
+        a.accumulate_dense(torch.from_numpy(Tab).cuda())
+    assert not np.any(a.data())
+    a.accumulate_dense(torch.from_numpy(Ta).cuda())
+    assert rel_per_replicate(a.data(), aref.data()) <= SKETCH_TOL
+
+
 @pytest.mark.parametrize("n,b,B", [(10, 64, 3), (24, 4096, 6), (16, 1 << 15, 2)])
 def test_asym_dense_build_matches_oracle(gpu_ctx, n, b, B):
     T = np.random.default_rng(n).normal(size=(n, n, n))
