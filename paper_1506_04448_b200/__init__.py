@@ -279,11 +279,20 @@ class SymTensorSketchSet:
         check(lib.skc_sym_info(self._h, C.byref(n), C.byref(b), C.byref(B), C.byref(s), C.byref(v)))
         return n.value, b.value, B.value, s.value, v.value
 
+    def _dims(self):
+        """(n, b, B): fixed for the life of a handle, so cached (one ctypes round trip saved per call)."""
+        d = self.__dict__.get("_dims_cache")
+        if d is None or d[0] != self._h:
+            i = self._info()
+            d = (self._h, i[:3])
+            self.__dict__["_dims_cache"] = d
+        return d[1]
+
     def n(self) -> int:
-        return self._info()[0]
+        return self._dims()[0]
 
     def b(self) -> int:
-        return self._info()[1]
+        return self._dims()[1]
 
     def replicates(self) -> int:
         return self._info()[2]
@@ -594,11 +603,20 @@ class AsymTensorSketchSet:
         check(lib.skc_asym_info(self._h, C.byref(n), C.byref(b), C.byref(B), C.byref(s), C.byref(v)))
         return n.value, b.value, B.value, s.value, v.value
 
+    def _dims(self):
+        """(n, b, B): fixed for the life of a handle, so cached (one ctypes round trip saved per call)."""
+        d = self.__dict__.get("_dims_cache")
+        if d is None or d[0] != self._h:
+            i = self._info()
+            d = (self._h, i[:3])
+            self.__dict__["_dims_cache"] = d
+        return d[1]
+
     def n(self):
-        return self._info()[0]
+        return self._dims()[0]
 
     def b(self):
-        return self._info()[1]
+        return self._dims()[1]
 
     def replicates(self):
         return self._info()[2]

@@ -292,9 +292,10 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
         }
         ctx->check_launch();
     }
-    int nonfinite = 0;
-    CK(cudaMemcpyAsync(&nonfinite, p.nonfinite, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    int* flag = ctx->pinned_ints();  // pinned: a direct DMA, not a staged pageable copy
+    CK(cudaMemcpyAsync(flag, p.nonfinite, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     ctx->sync();
+    const int nonfinite = *flag;
     // Fixed-point accumulation cannot carry NaN/Inf the way the reference's
     // floating-point sum would; reject instead of producing a wrong sketch.
     if (nonfinite) fail(kInvalidArgument, "accumulate_dense: tensor has a non-finite entry");

@@ -142,6 +142,11 @@ struct skc_context {
     DevBuf<short> rowF;
     DevBuf<double> prepass;
     DevBuf<int> ints;  // [0] scale exp, [1] nonfinite, [2] best tau, [3..] misc
+    int* host_ints = nullptr;  // pinned host scratch for small synchronous readbacks (DMA, no staging)
+    int* pinned_ints() {
+        if (!host_ints) CK(cudaMallocHost(reinterpret_cast<void**>(&host_ints), 16 * sizeof(int)));
+        return host_ints;
+    }
     DevBuf<double> dbl;  // [0] best value
     DevBuf<int> build_ints;                // per-type row counters of the dense build
     DevBuf<unsigned long long> build_acc;  // exact fixed-point slot accumulators
