@@ -1376,6 +1376,44 @@ __global__ void k_build_finalize(unsigned long long* __restrict__ acc, long long
     }
 }
 
+// Symmetric class-list builds with one window per (replicate, parity) (tb = 0): the real
+// and imaginary windows of replicate m are acc[2m*b + t] and acc[(2m+1)*b + t], so a
+// thread takes both and updates the complex data[m*b + t] with one 16-byte load and
+// store (the generic walk writes every other double). Same arithmetic as
+// k_build_finalize: a zero accumulator leaves its component untouched.
+__global__ void k_build_finalize_sym_pair(unsigned long long* __restrict__ acc, long long pairs, int logb,
+                                          const int* __restrict__ scale_exp, const int* __restrict__ nonfinite,
+                                          double2* __restrict__ data, int* __restrict__ counters, int ncounters) {
+    const long long base = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // main pass complete (PDL launch)
+    if (base < ncounters) counters[base] = 0;
+    const bool bad = *nonfinite != 0;
+    const double sc = pow2_neg(*scale_exp);
+    const long long bm = (1ll << logb) - 1;
+    long long q0[2], q1[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        const long long x = base + u * stride;
+        const long long a0 = ((x >> logb) << (logb + 1)) | (x & bm);  // (2m) * b + t
+        q0[u] = x < pairs ? static_cast<long long>(acc[a0]) : 0ll;
+        q1[u] = x < pairs ? static_cast<long long>(acc[a0 + (bm + 1)]) : 0ll;
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        if ((q0[u] | q1[u]) == 0) continue;
+        const long long x = base + u * stride;
+        const long long a0 = ((x >> logb) << (logb + 1)) | (x & bm);
+        if (q0[u]) acc[a0] = 0ull;
+        if (q1[u]) acc[a0 + (bm + 1)] = 0ull;
+        if (bad) continue;
+        double2 d = data[x];
+        if (q0[u]) d.x += static_cast<double>(q0[u]) * sc;
+        if (q1[u]) d.y += static_cast<double>(q1[u]) * sc;
+        data[x] = d;
+    }
+}
+
 // Pipelined builds: K chunk accumulators with their own exponents, summed in chunk order.
 template <bool SYM>
 __global__ void k_build_finalize_multi(unsigned long long* __restrict__ acc, int K, long long total_slots,
@@ -1418,7 +1456,17 @@ void launch_build_finalize_multi(cudaStream_t st, const BuildPlan& p, int K, con
 void launch_build_finalize(cudaStream_t st, const BuildPlan& p) {
     const unsigned grid = cdiv(std::max<long long>((p.total_slots + 3) / 4, p.G), 256);
     const bool pdl = p.pdl && p.cls_bits >= 0;  // only the class-list main pass triggers early
-    if (p.sym)
+    static const bool pair_on = [] {
+        const char* e = std::getenv("SKC_FINALIZE_PAIR");  // "0": generic walk (A/B)
+        return !(e && e[0] == '0');
+    }();
+    if (pair_on && p.sym && p.cls_bits == 0) {
+        const long long pairs = p.total_slots / 2;  // B x b complex entries
+        const int logb = __builtin_ctz(p.bmask + 1u);
+        const unsigned g2 = cdiv(std::max<long long>((pairs + 1) / 2, p.G), 256);
+        pdl_launch(k_build_finalize_sym_pair, g2, 256, 0, st, pdl, p.acc, pairs, logb, p.scale_exp, p.nonfinite,
+                   reinterpret_cast<double2*>(p.data_as_double), p.next_row, p.G);
+    } else if (p.sym)
         pdl_launch(k_build_finalize<true>, grid, 256, 0, st, pdl, p.acc, p.total_slots, p.scale_exp, p.nonfinite,
                    p.data_as_double, p.next_row, p.G, p.cls_bits, p.bmask);
     else
