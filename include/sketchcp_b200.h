@@ -69,6 +69,19 @@ int skc_context_destroy(skc_context* ctx);
 int skc_context_synchronize(skc_context* ctx);
 /* The stream all work of this context is enqueued on (cudaStream_t). */
 int skc_context_stream(skc_context* ctx, void** stream_out);
+/* Orders all later work of this context after everything already enqueued on
+ * `producer` (a cudaStream_t; NULL = the legacy default stream): an event is
+ * recorded on `producer` and the context stream waits on it, with no host sync.
+ * Ordering contract for device pointers: every entry point that takes a device
+ * pointer reads it on the context stream, so a caller whose input is produced
+ * on another stream (e.g. a framework's current stream) calls this first.
+ * Results are complete when the entry point returns (synchronous API) unless the
+ * entry point says otherwise. */
+int skc_context_wait_stream(skc_context* ctx, void* producer);
+/* Dense builds of fp32 tensors run with one 32-bit limb per sketch slot; a build whose
+ * limb overflowed (>= 512 same-signed full-scale adds to one slot in one pass) is
+ * discarded and repeated exactly with two limbs. Number of such repeats so far. */
+int skc_context_build_retries(skc_context* ctx, long long* out);
 int skc_device_count(int* out);
 /* Per-kernel device timing with CUDA events on the context stream (off by
  * default). skc_profile_get sums the recorded durations of one kernel family

@@ -88,6 +88,131 @@ __global__ void stream_read(const double2* __restrict__ a, size_t n, int passes,
   if (acc == 123.456) out[0] = acc;
 }
 
+
+// Conflict structure of u32 ATOMS: lane L hits bank (L * stride) mod 32 of a random
+// 32-word row, so stride 1 is conflict-free, 2 gives 2-way, 32 gives 32-way conflicts;
+// stride 0 keeps fully random banks (the reference point above).
+__global__ void smem_u32_banks(unsigned* out, int iters, int mask, int stride) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  unsigned* s = reinterpret_cast<unsigned*>(sm);
+  for (int i = threadIdx.x; i <= mask; i += blockDim.x) s[i] = 0;
+  __syncthreads();
+  const unsigned lane = threadIdx.x & 31;
+  uint32_t st = blockIdx.x * 7919u + (threadIdx.x >> 5) * 104729u;  // warp-uniform row stream
+#pragma unroll 8
+  for (int it = 0; it < iters; ++it) {
+    const uint32_t r = lcg(st);
+    const uint32_t a = stride ? (((r << 5) + lane * stride) & mask) : ((r * 2654435761u + lane * 40503u) & mask);
+    atomicAdd(&s[a], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) out[blockIdx.x] = s[blockIdx.x & mask];
+}
+
+// Exact 64-bit add as two limbs, the build kernel's pattern: ATOMS.ADD with return on the
+// low limb, the carry into a RED on the high limb (conflict-free or random banks).
+__global__ void smem_2limb_ret(unsigned* out, int iters, int mask, int cf) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  unsigned* s = reinterpret_cast<unsigned*>(sm);
+  for (int i = threadIdx.x; i <= 2 * mask + 1; i += blockDim.x) s[i] = 0;
+  __syncthreads();
+  const unsigned lane = threadIdx.x & 31;
+  uint32_t st = blockIdx.x * 7919u + (threadIdx.x >> 5) * 104729u + (cf ? 0u : lane * 7u);
+  uint32_t v = 0x9e3779b9u * (threadIdx.x + 1);
+#pragma unroll 4
+  for (int it = 0; it < iters; ++it) {
+    const uint32_t r = lcg(st);
+    const uint32_t a = cf ? (((r << 5) + lane) & mask) : (r & mask);
+    v = v * 1664525u + 1013904223u;
+    const unsigned old = atomicAdd(&s[a], v);
+    const unsigned c = (old + v) < old;
+    atomicAdd(&s[mask + 1 + a], (v >> 28) + c);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) out[blockIdx.x] = s[blockIdx.x & mask];
+}
+
+// One limb with the rare carry: |q| < 2^qb, the high limb (global, RED) is touched only
+// when the low limb wraps (probability ~|q| / 2^32 per add).
+__global__ void smem_1limb_rare(unsigned* out, unsigned long long* hi, int iters, int mask, int cf, int qb) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  unsigned* s = reinterpret_cast<unsigned*>(sm);
+  for (int i = threadIdx.x; i <= mask; i += blockDim.x) s[i] = 0;
+  __syncthreads();
+  const unsigned lane = threadIdx.x & 31;
+  uint32_t st = blockIdx.x * 7919u + (threadIdx.x >> 5) * 104729u + (cf ? 0u : lane * 7u);
+  uint32_t v = 0x9e3779b9u * (threadIdx.x + 1);
+  const int sh = 32 - qb;
+#pragma unroll 4
+  for (int it = 0; it < iters; ++it) {
+    const uint32_t r = lcg(st);
+    const uint32_t a = cf ? (((r << 5) + lane) & mask) : (r & mask);
+    v = v * 1664525u + 1013904223u;
+    const int q = static_cast<int>(v) >> sh;  // signed, |q| < 2^(qb-1)
+    const unsigned old = atomicAdd(&s[a], static_cast<unsigned>(q));
+    const unsigned nw = old + static_cast<unsigned>(q);
+    const int d = q >= 0 ? (nw < old ? 1 : 0) : (nw > old ? -1 : 0);
+    if (d) atomicAdd(hi + ((blockIdx.x * 4096u + a) & ((1u << 22) - 1)), static_cast<unsigned long long>(static_cast<long long>(d)));
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) out[blockIdx.x] = s[blockIdx.x & mask];
+}
+
+// Native u32 reduction into the partner CTA's shared memory (cluster of 2).
+__global__ void __cluster_dims__(2, 1, 1) dsmem_red_u32(unsigned* out, int iters, int mask, int cf) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  unsigned* s = reinterpret_cast<unsigned*>(sm);
+  cg::cluster_group cl = cg::this_cluster();
+  for (int i = threadIdx.x; i <= mask; i += blockDim.x) s[i] = 0;
+  cl.sync();
+  unsigned* remote = cl.map_shared_rank(s, cl.block_rank() ^ 1);
+  const unsigned lane = threadIdx.x & 31;
+  uint32_t st = blockIdx.x * 7919u + (threadIdx.x >> 5) * 104729u + (cf ? 0u : lane * 7u);
+#pragma unroll 8
+  for (int it = 0; it < iters; ++it) {
+    const uint32_t r = lcg(st);
+    const uint32_t a = cf ? (((r << 5) + lane) & mask) : (r & mask);
+    atomicAdd(&remote[a], 1u);
+  }
+  cl.sync();
+  if (threadIdx.x == 0) out[blockIdx.x] = s[blockIdx.x & mask];
+}
+
+// Shared-memory reads: 4- or 8-byte words at random or conflict-free addresses.
+template <typename T>
+__global__ void smem_read(unsigned* out, int iters, int mask, int cf) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  T* s = reinterpret_cast<T*>(sm);
+  for (int i = threadIdx.x; i <= mask; i += blockDim.x) s[i] = T(i);
+  __syncthreads();
+  const unsigned lane = threadIdx.x & 31;
+  uint32_t st = blockIdx.x * 7919u + (threadIdx.x >> 5) * 104729u + (cf ? 0u : lane * 7u);
+  T acc = T(0);
+#pragma unroll 8
+  for (int it = 0; it < iters; ++it) {
+    const uint32_t r = lcg(st);
+    const uint32_t a = cf ? (((r << 5) + lane) & mask) : (r & mask);
+    acc += s[a];
+  }
+  if (acc == T(12345)) out[blockIdx.x] = (unsigned)acc;
+}
+
+// L2 gathers of 4-byte words from an L2-resident array: each lane of a warp reads one
+// word from its own random 32-byte sector (stride 0), or the warp reads words spaced
+// `stride` apart inside one random row (the class-list gather pattern).
+__global__ void l2_gather(const float* __restrict__ a, int iters, unsigned mask, int stride, float* out) {
+  const unsigned lane = threadIdx.x & 31;
+  uint32_t st = blockIdx.x * 7919u + (threadIdx.x >> 5) * 104729u + (stride ? 0u : lane * 7u);
+  float acc = 0;
+#pragma unroll 8
+  for (int it = 0; it < iters; ++it) {
+    const uint32_t r = lcg(st);
+    const uint32_t idx = stride ? (((r << 10) + lane * stride) & mask) : ((r << 3) & mask);
+    acc += __ldg(a + idx);
+  }
+  if (acc == 123.456f) out[0] = acc;
+}
+
 template <typename K>
 float time_it(K launch, int reps = 5) {
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
@@ -161,6 +286,59 @@ int main() {
              mb, cps, ms, (double)(mb << 20) * passes / ms / 1e6);
     }
     cudaFree(a);
+  }
+  // ---- round 2: bank structure of the scatter (one CTA of 1024 threads per SM, 128 KB) ----
+  {
+    const int th = 1024, it2 = 2048, grid = sms;
+    const size_t sb = 128 << 10;
+    const int mask = (int)(sb / 4) - 1;
+    double ops = (double)grid * th * it2;
+    CK(cudaFuncSetAttribute(smem_u32_banks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+    for (int stride : {0, 1, 2, 4, 8, 32}) {
+      float ms = time_it([&] { smem_u32_banks<<<grid, th, sb>>>((unsigned*)buf, it2, mask, stride); });
+      CK(cudaGetLastError());
+      printf("{\"test\": \"smem_u32_atoms_banks\", \"lane_stride\": %d, \"ms\": %.4f, \"ops_per_clk_per_sm\": %.3f}\n",
+             stride, ms, ops / (ms * 1e-3) / sms / (clk * 1e3));
+    }
+    CK(cudaFuncSetAttribute(smem_2limb_ret, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+    for (int cf : {0, 1}) {
+      float ms = time_it([&] { smem_2limb_ret<<<grid, th, sb>>>((unsigned*)buf, it2, mask / 2, cf); });
+      CK(cudaGetLastError());
+      printf("{\"test\": \"smem_2limb_carry\", \"conflict_free\": %d, \"ms\": %.4f, \"adds_per_clk_per_sm\": %.3f}\n",
+             cf, ms, ops / (ms * 1e-3) / sms / (clk * 1e3));
+    }
+    unsigned long long* hi; CK(cudaMalloc(&hi, 8ull << 22)); CK(cudaMemset(hi, 0, 8ull << 22));
+    CK(cudaFuncSetAttribute(smem_1limb_rare, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+    for (int qb : {24, 28}) for (int cf : {0, 1}) {
+      float ms = time_it([&] { smem_1limb_rare<<<grid, th, sb>>>((unsigned*)buf, hi, it2, mask, cf, qb); });
+      CK(cudaGetLastError());
+      printf("{\"test\": \"smem_1limb_rare_carry\", \"q_bits\": %d, \"conflict_free\": %d, \"ms\": %.4f, \"adds_per_clk_per_sm\": %.3f}\n",
+             qb, cf, ms, ops / (ms * 1e-3) / sms / (clk * 1e3));
+    }
+    CK(cudaFuncSetAttribute(dsmem_red_u32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+    for (int cf : {0, 1}) {
+      float ms = time_it([&] { dsmem_red_u32<<<(grid / 2) * 2, th, sb>>>((unsigned*)buf, it2, mask, cf); });
+      CK(cudaGetLastError());
+      printf("{\"test\": \"dsmem_red_u32_cluster2\", \"conflict_free\": %d, \"ms\": %.4f, \"ops_per_clk_per_sm\": %.3f}\n",
+             cf, ms, (double)((grid / 2) * 2) * th * it2 / (ms * 1e-3) / sms / (clk * 1e3));
+    }
+    CK(cudaFuncSetAttribute(smem_read<unsigned>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+    CK(cudaFuncSetAttribute(smem_read<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+    for (int cf : {0, 1}) {
+      float ms = time_it([&] { smem_read<unsigned><<<grid, th, sb>>>((unsigned*)buf, it2, mask, cf); });
+      printf("{\"test\": \"smem_read_u32\", \"conflict_free\": %d, \"ms\": %.4f, \"ops_per_clk_per_sm\": %.3f}\n",
+             cf, ms, ops / (ms * 1e-3) / sms / (clk * 1e3));
+      ms = time_it([&] { smem_read<unsigned long long><<<grid, th, sb>>>((unsigned*)buf, it2, mask / 2, cf); });
+      printf("{\"test\": \"smem_read_u64\", \"conflict_free\": %d, \"ms\": %.4f, \"ops_per_clk_per_sm\": %.3f}\n",
+             cf, ms, ops / (ms * 1e-3) / sms / (clk * 1e3));
+    }
+    float* g; CK(cudaMalloc(&g, 64ull << 20)); CK(cudaMemset(g, 0, 64ull << 20));
+    for (int stride : {0, 1, 2, 4, 8}) {
+      float ms = time_it([&] { l2_gather<<<grid * 2, 512>>>(g, it2, (16u << 20) - 1, stride, (float*)buf); });
+      double loads = (double)grid * 2 * 512 * it2;
+      printf("{\"test\": \"l2_gather_f32\", \"lane_stride\": %d, \"ms\": %.4f, \"Gloads\": %.1f, \"useful_GBps\": %.1f}\n",
+             stride, ms, loads / ms / 1e6, loads * 4 / ms / 1e6);
+    }
   }
   return 0;
 }

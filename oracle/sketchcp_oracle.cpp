@@ -379,6 +379,97 @@ void sym_accumulate_dense(SymSet& s, const double* T, bool assume_symmetric) {
     }
 }
 
+// sketch.cpp:315-345 restricted to rows i in [i0, i1): the same loop order, the partial
+// sketch of one i-slice (the multi-GPU shard unit and the bounded CPU-baseline sample).
+// T points at row i0 ((i - i0) * n^2 + j * n + k), float64 or float32 (widened exactly,
+// as the reference would see the tensor converted to its fp64 DenseTensor3).
+template <typename TT>
+void sym_accumulate_dense_slice(SymSet& s, const TT* T, int i0, int i1) {
+    const int n = s.n;
+    ++s.version;
+    const std::uint32_t b = s.b;
+#pragma omp parallel for schedule(static)
+    for (int m = 0; m < s.B; ++m) {
+        auto& rep = s.reps[m];
+        for (int i = i0; i < i1; ++i) {
+            std::uint64_t hi = rep.bucket1[i];
+            unsigned ei = rep.sexp[i];
+            for (int j = i; j < n; ++j) {
+                std::uint64_t hij = hi + rep.bucket1[j];
+                unsigned eij = ei + rep.sexp[j];
+                const TT* row = &T[(static_cast<std::size_t>(i - i0) * n + j) * n];
+                for (int k = j; k < n; ++k) {
+                    double value = static_cast<double>(row[k]);
+                    if (value == 0.0) continue;
+                    double mult = (i == j && j == k) ? 1.0 : ((i == j || j == k) ? 3.0 : 6.0);
+                    std::uint32_t t = static_cast<std::uint32_t>((hij + rep.bucket1[k]) % b);
+                    rep.data[t] += mult * value * root4(eij + rep.sexp[k]);
+                }
+            }
+        }
+    }
+}
+
+// BASELINE configs 0-2 planted tensor, restated independently of the product library so
+// the CPU arms never load it: lambda ~ U[1,2] and the QR basis from the host Rng streams
+// (tags 0x61 / 0x62, modified Gram-Schmidt twice), noise sigma * N(0,1) per sorted triple
+// from a counter-based SplitMix64 hash of (a, b, c) and Box-Muller (tag 0x63), mirrored.
+// Entries of rows i in [i0, i1) are written to out[(i - i0) * n^2 + j * n + k].
+static std::uint64_t gen_mix64(std::uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+void gen_planted_slice(int n, int rank, double sigma, std::uint64_t seed, int i0, int i1, int f32, void* out,
+                       double* lambda_out, double* V_out) {
+    std::vector<double> lam(rank), V(static_cast<std::size_t>(rank) * n);
+    Rng lr(derive_seed(seed, 0x61));
+    for (int r = 0; r < rank; ++r) lam[r] = 1.0 + lr.uniform();
+    Rng br(derive_seed(seed, 0x62));
+    for (int r = 0; r < rank; ++r)
+        for (int i = 0; i < n; ++i) V[static_cast<std::size_t>(r) * n + i] = br.gaussian();
+    for (int pass = 0; pass < 2; ++pass)
+        for (int r = 0; r < rank; ++r) {
+            double* v = &V[static_cast<std::size_t>(r) * n];
+            for (int q = 0; q < r; ++q) {
+                const double* w = &V[static_cast<std::size_t>(q) * n];
+                double d = 0;
+                for (int i = 0; i < n; ++i) d += v[i] * w[i];
+                for (int i = 0; i < n; ++i) v[i] -= d * w[i];
+            }
+            double ss = 0;
+            for (int i = 0; i < n; ++i) ss += v[i] * v[i];
+            const double inv = 1.0 / std::sqrt(ss);
+            for (int i = 0; i < n; ++i) v[i] *= inv;
+        }
+    if (lambda_out) std::copy(lam.begin(), lam.end(), lambda_out);
+    if (V_out) std::copy(V.begin(), V.end(), V_out);
+    const std::uint64_t nseed = derive_seed(seed, 0x63);
+#pragma omp parallel for schedule(dynamic, 1) collapse(2)
+    for (int i = i0; i < i1; ++i)
+        for (int j = 0; j < n; ++j)
+            for (int k = 0; k < n; ++k) {
+                const int a = std::min(i, std::min(j, k)), c = std::max(i, std::max(j, k)), bb = i + j + k - a - c;
+                double s = 0.0;
+                for (int r = 0; r < rank; ++r)
+                    s += lam[r] * V[static_cast<std::size_t>(r) * n + a] * V[static_cast<std::size_t>(r) * n + bb] *
+                         V[static_cast<std::size_t>(r) * n + c];
+                if (sigma > 0.0) {
+                    const std::uint64_t key = ((static_cast<std::uint64_t>(a) * n + bb) * n + c);
+                    const std::uint64_t h1 = gen_mix64(nseed ^ (key * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull));
+                    const std::uint64_t h2 = gen_mix64(h1 + 0x9E3779B97F4A7C15ull);
+                    const double u1 = (static_cast<double>(h1 >> 11) + 1.0) * 0x1.0p-53;
+                    const double u2 = static_cast<double>(h2 >> 11) * 0x1.0p-53;
+                    s += sigma * std::sqrt(-2.0 * std::log(u1)) * std::cos(3.141592653589793238462643383279502884 * 2.0 * u2);
+                }
+                const std::size_t off = (static_cast<std::size_t>(i - i0) * n + j) * n + k;
+                if (f32)
+                    static_cast<float*>(out)[off] = static_cast<float>(s);
+                else
+                    static_cast<double*>(out)[off] = s;
+            }
+}
+
 // sketch.cpp:347-361
 void sym_add_scaled_rank1(SymSet& s, const double* u, double alpha) {
     if (alpha == 0.0) return;
@@ -1247,6 +1338,24 @@ int orc_sym_tables(void* h, int m, std::uint32_t* b1, std::uint32_t* b2, std::ui
 }
 int orc_sym_accumulate_dense(void* h, const double* T, int assume_symmetric) {
     return guard([&] { sym_accumulate_dense(*static_cast<SymSet*>(h), T, assume_symmetric != 0); });
+}
+int orc_sym_accumulate_dense_slice(void* h, const void* T, int f32, int i0, int i1) {
+    return guard([&] {
+        auto& st = *static_cast<SymSet*>(h);
+        if (i0 < 0 || i1 > st.n || i0 > i1) throw std::invalid_argument("accumulate_dense_slice: bad slice");
+        if (f32)
+            sym_accumulate_dense_slice(st, static_cast<const float*>(T), i0, i1);
+        else
+            sym_accumulate_dense_slice(st, static_cast<const double*>(T), i0, i1);
+    });
+}
+int orc_gen_planted_slice(int n, int rank, double sigma, std::uint64_t seed, int i0, int i1, int f32, void* out,
+                          double* lambda_out, double* V_out) {
+    return guard([&] {
+        if (n < 1 || rank < 1 || rank > n || i0 < 0 || i1 > n || i0 > i1)
+            throw std::invalid_argument("gen_planted_slice: bad arguments");
+        gen_planted_slice(n, rank, sigma, seed, i0, i1, f32, out, lambda_out, V_out);
+    });
 }
 int orc_sym_add_scaled_rank1(void* h, const double* u, double alpha) {
     return guard([&] { sym_add_scaled_rank1(*static_cast<SymSet*>(h), u, alpha); });

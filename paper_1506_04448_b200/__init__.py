@@ -152,6 +152,12 @@ class Context:
     def synchronize(self) -> None:
         check(lib.skc_context_synchronize(self._h))
 
+    def build_retries(self) -> int:
+        """fp32 dense builds repeated with two limbs after a one-limb overflow."""
+        v = C.c_longlong()
+        check(lib.skc_context_build_retries(self.handle, C.byref(v)))
+        return v.value
+
     def stream(self) -> int:
         s = C.c_void_p()
         check(lib.skc_context_stream(self._h, C.byref(s)))
@@ -191,7 +197,20 @@ def default_context(device: int = 0) -> Context:
     return _DEFAULT[device]
 
 
-def _tensor_arg(T, n: int):
+def _order_after_torch(ctx: "Context", *tensors) -> None:
+    """Orders the context stream after torch's current stream on the tensors' device, so a
+    device input still being produced by an in-flight torch kernel (e.g. `.contiguous()`,
+    `.to(float64)`, setitem) is complete before the library reads it
+    (skc_context_wait_stream; no host synchronisation)."""
+    import torch
+
+    dev = next((t.device for t in tensors if t is not None), None)
+    if dev is None:
+        return
+    check(lib.skc_context_wait_stream(ctx.handle, C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
+
+
+def _tensor_arg(T, n: int, ctx: "Context"):
     """Returns (pointer, dtype code, location, keepalive) for a dense n^3 tensor
     given as a numpy array (host) or a CUDA torch tensor (device)."""
     if hasattr(T, "is_cuda") and T.is_cuda:
@@ -202,6 +221,7 @@ def _tensor_arg(T, n: int):
         if T.numel() != n * n * n:
             raise ValueError("accumulate_dense: dimension mismatch")
         T = T.contiguous()
+        _order_after_torch(ctx, T)
         return C.c_void_p(T.data_ptr()), (SKC_F64 if T.dtype == torch.float64 else SKC_F32), SKC_DEVICE, T
     a = np.asarray(T)
     if a.dtype not in (np.float64, np.float32):
@@ -351,7 +371,7 @@ class SymTensorSketchSet:
     def accumulate_dense(self, T, assume_symmetric: bool = False, i0: int = 0, i1: int | None = None) -> None:
         """sketch.cpp:315-345; T numpy (host) or CUDA torch tensor (device), f64 or f32."""
         n = self.n()
-        ptr, dt, loc, _keep = _tensor_arg(T, n)
+        ptr, dt, loc, _keep = _tensor_arg(T, n, self.ctx)
         check(lib.skc_sym_accumulate_dense(self._h, ptr, dt, loc, int(bool(assume_symmetric)), int(i0),
                                            int(n if i1 is None else i1)))
 
@@ -377,6 +397,7 @@ class SymTensorSketchSet:
             if w is not None:
                 w = w.to(device=X.device, dtype=torch.float64).contiguous()
                 wp = C.cast(C.c_void_p(w.data_ptr()), C.POINTER(C.c_double))
+            _order_after_torch(self.ctx, X, w)
             check(lib.skc_sym_accumulate_moment(self._h, C.cast(C.c_void_p(X.data_ptr()), C.POINTER(C.c_double)),
                                                 wp, X.shape[0], SKC_DEVICE))
             return
@@ -657,7 +678,7 @@ class AsymTensorSketchSet:
     def accumulate_dense(self, T, i0: int = 0, i1: int | None = None) -> None:
         """sketch.cpp:173-193"""
         n = self.n()
-        ptr, dt, loc, _keep = _tensor_arg(T, n)
+        ptr, dt, loc, _keep = _tensor_arg(T, n, self.ctx)
         check(lib.skc_asym_accumulate_dense(self._h, ptr, dt, loc, int(i0), int(n if i1 is None else i1)))
 
     def rank1_sketch(self, m: int, u, v, w) -> np.ndarray:

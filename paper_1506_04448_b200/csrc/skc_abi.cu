@@ -73,6 +73,7 @@ int skc_context_destroy(skc_context* ctx) {
             cudaEventDestroy(r.b);
         }
         for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+        if (ctx->ev_order) cudaEventDestroy(ctx->ev_order);
         cudaStream_t st = ctx->stream, st2 = ctx->stream2;
         cudaEvent_t ev[5];
         for (int c = 0; c < 5; ++c) ev[c] = ctx->ev_q[c];
@@ -138,6 +139,24 @@ int skc_context_stream(skc_context* ctx, void** stream_out) {
     return guard([&] {
         check_vec(ctx, "context");
         *stream_out = reinterpret_cast<void*>(ctx->stream);
+    });
+}
+
+int skc_context_wait_stream(skc_context* ctx, void* producer) {
+    return guard([&] {
+        check_vec(ctx, "context");
+        ctx->use();
+        if (!ctx->ev_order) CK(cudaEventCreateWithFlags(&ctx->ev_order, cudaEventDisableTiming));
+        CK(cudaEventRecord(ctx->ev_order, static_cast<cudaStream_t>(producer)));
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_order, 0));
+    });
+}
+
+int skc_context_build_retries(skc_context* ctx, long long* out) {
+    return guard([&] {
+        check_vec(ctx, "context");
+        check_vec(out, "out");
+        *out = ctx->build_two_limb_retries;
     });
 }
 

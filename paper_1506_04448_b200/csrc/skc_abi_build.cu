@@ -47,7 +47,7 @@ const void* stage_tensor(skc_context* ctx, const void* T, int n, int dtype, int 
 }
 
 void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool sym, int i0, int i1, int B,
-                     std::uint32_t b, const std::uint32_t* packed, double2* data, bool zero_copy) {
+                     std::uint32_t b, const std::uint32_t* packed, double2* data, bool zero_copy, bool two_limb) {
     if (i0 >= i1) return;
     skc_context::RowTab& rt = ctx->rowtab(n, i0, i1, sym);
     if (rt.nrows == 0) return;
@@ -67,30 +67,22 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
     }
     long long spc = (total_slots + G - 1) / G;
     spc = (spc + 31) / 32 * 32;
-    if (const char* e = std::getenv("SKC_BUILD_SPC")) {  // experiment hook: forced window size
-        const long long f = std::atoll(e) / 32 * 32;
-        if (f >= 32 && f <= spc * 4 && build_smem_bytes(f, 16, n) <= static_cast<size_t>(ctx->smem_optin - 1024)) {
-            spc = f;
-            G = static_cast<int>((total_slots + spc - 1) / spc);
-        }
-    }
     // Dense builds take the class-list kernel when a (replicate, [parity,] bucket class)
     // window fits: the fewest bucket-class bits t <= 3 whose window + tables fit.
-    static const int kernel_choice = [] {
-        const char* e = std::getenv("SKC_BUILD_KERNEL");  // "flat" / "rows": A/B switches
-        return (e && (std::string(e) == "flat" || std::string(e) == "rows")) ? 1 : 0;
-    }();
-    int cls_bits = -1;
+    int cls_bits = -1, slab_cap = 0;
     // (class lists pack k above the 3-term bucket sum: n <= 2^(28 - log2 b))
     int logb = 0;
     while ((1u << logb) < b) ++logb;
     // (small asymmetric builds are flush/setup-bound with few windows: C0's asym build
     // measured 93 us on the contiguous-window kernel against 113 us here)
     const bool small_asym = !sym && rt.cum.back() < (4ll << 20);
-    if (kernel_choice == 0 && !small_asym && b <= (1u << 22) && b >= 64 &&
+    // fp32 input: one biased limb per slot, unless a previous attempt overflowed a limb
+    const bool one_limb = dtype == SKC_F32 && !two_limb;
+    if (!small_asym && b <= (1u << 21) && b >= 64 &&
         static_cast<long long>(n - 1) < (1ll << (28 - logb))) {
         for (int t = 0; t <= 3; ++t)
-            if (cls_smem_bytes(b, t, n, sym) <= static_cast<size_t>(ctx->smem_optin - 1024)) {
+            if ((slab_cap = cls_slab_cap(b, t, n, sym, one_limb, static_cast<size_t>(ctx->smem_optin - 4096))) >=
+                (t < 3 ? 32 : 1)) {
                 cls_bits = t;
                 break;
             }
@@ -140,24 +132,15 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
     p.G = G;
     p.next_row = ctx->build_ints.p;
     p.acc = ctx->build_acc.p;
-    static const bool row_variant = [] {
-        const char* e = std::getenv("SKC_BUILD_KERNEL");
-        return e && std::string(e) == "rows";
-    }();
-    // flat kernel's doubled SYM tables need bucket sums below bit 30: b <= 2^27 (larger
-    // sets take the row-walk kernel, which uses the plain packed form)
-    p.flat = !row_variant && (!sym || b <= (1u << 27));
+    // the flat kernel's doubled SYM tables need bucket sums below bit 30: b <= 2^27
+    if (cls_bits < 0 && sym && b > (1u << 27))
+        fail(kInvalidArgument, "accumulate_dense: symmetric dense builds support b <= 2^27");
     p.cls_bits = cls_bits;
+    p.slab_cap = slab_cap;
+    p.one_limb = cls_bits >= 0 && one_limb;
     // class-list builds read T in place when it is device-resident (row offsets relative to
     // a 32-row chunk fit in 32 bits for n <= 30000), else a packed raw copy of the rows
     p.xsrc_mode = cls_bits < 0 ? 0 : ((!zero_copy && n <= 30000) ? 1 : 2);
-    static const bool trace_on = std::getenv("SKC_BUILD_TRACE") != nullptr;
-    DevBuf<unsigned long long> trace;
-    p.trace = nullptr;
-    if (trace_on) {
-        trace.alloc(3 * static_cast<size_t>(P));
-        p.trace = trace.p;
-    }
     p.total_slots = total_slots;
     p.slots_per_cta = static_cast<int>(spc);
     p.R = R;
@@ -170,21 +153,21 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
     p.prepass_partials = ctx->prepass.p;
     p.scale_exp = ctx->ints.p;
     p.nonfinite = ctx->ints.p + 1;
+    p.ovf = ctx->ints.p + 3;  // nonfinite + kOvfOffset
+    if (!ctx->build_ovf_clean) {
+        CK(cudaMemsetAsync(p.ovf, 0, sizeof(int), ctx->stream));
+        ctx->build_ovf_clean = true;
+    }
     p.data_as_double = reinterpret_cast<double*>(data);
     // Zero-copy host input: the quantize pass is bus-bound, so the rows are cut into K
     // chunks and chunk c+1 is read over PCIe (a few SMs, wide blocks) while the main pass
     // of chunk c runs on the other SMs (second stream). Each chunk keeps its own exponent
     // and exact accumulator; the finalize sums the K chunk sketches in order.
-    static const bool pipe_on = [] {
-        const char* e = std::getenv("SKC_BUILD_PIPELINE");  // "0": A/B switch for the chunked path
-        return !(e && std::string(e) == "0");
-    }();
-    const int K = (pipe_on && zero_copy && rt.nrows >= 4096 &&
-                   sizeof(double) * 32 * (size_t)n <= (size_t)ctx->smem_optin - 1024)
-                      ? env_int("SKC_BUILD_K", 4, 2, 4)
+    const int K = (zero_copy && rt.nrows >= 4096 && sizeof(double) * 32 * (size_t)n <= (size_t)ctx->smem_optin - 1024)
+                      ? 4
                       : 1;
     if (K > 1) {
-        const int qsms = env_int("SKC_BUILD_QSMS", 16, 1, 64);  // SMs given to the bus-bound quantize pass
+        const int qsms = 16;  // SMs given to the bus-bound quantize pass
         p.P = std::max(1, ctx->sms - qsms);
         p.prepass_threads = 1024;
         p.prepass_blocks = qsms;
@@ -211,12 +194,6 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
         CK(cudaMemsetAsync(p.nonfinite, 0, sizeof(int), ctx->stream));
         {
             SKC_PROF(ctx, "build_pipelined");
-            static const bool ptrace = std::getenv("SKC_PIPE_TRACE") != nullptr;
-            cudaEvent_t te[4][5];
-            if (ptrace)
-                for (auto& row : te)
-                    for (auto& e : row) CK(cudaEventCreate(&e));
-            if (ptrace) CK(cudaEventRecord(te[0][0], ctx->stream));
             for (int c = 0; c < K; ++c) {
                 BuildPlan pc = p;
                 pc.rowtab = rt.rows.p + rb[c];
@@ -228,15 +205,11 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
                 pc.reset_nonfinite = false;
                 pc.acc = ctx->build_acc.p + static_cast<size_t>(c) * total_slots;
                 pc.next_row = ctx->build_ints.p + static_cast<size_t>(c) * G;
-                if (ptrace) CK(cudaEventRecord(te[0][c + 1 < 5 ? c + 1 : 4], ctx->stream));
                 if (pc.nrows > 0) launch_build_prepass(ctx->stream, Tdev, pc);
-                if (ptrace) CK(cudaEventRecord(te[1][c], ctx->stream));
                 CK(cudaEventRecord(ctx->ev_q[c], ctx->stream));
                 CK(cudaStreamWaitEvent(ctx->stream2, ctx->ev_q[c], 0));
                 if (pc.nrows > 0) {
-                    if (ptrace) CK(cudaEventRecord(te[2][c], ctx->stream2));
                     launch_build_main(ctx->stream2, Tdev, pc);
-                    if (ptrace) CK(cudaEventRecord(te[3][c], ctx->stream2));
                 }  // (an empty chunk's accumulator stays zero)
             }
             CK(cudaEventRecord(ctx->ev_q[K], ctx->stream2));
@@ -245,36 +218,14 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
             pf.acc = ctx->build_acc.p;
             launch_build_finalize_multi(ctx->stream, pf, K, ctx->ints.p + 4, ctx->build_ints.p, K * G);
             ctx->build_scratch_clean = true;
-            if (ptrace) {
-                ctx->sync();
-                for (int c = 0; c < K && c < 4; ++c) {
-                    float q0, q1, m0, m1;
-                    cudaEventElapsedTime(&q0, te[0][0], te[0][c + 1 < 5 ? c + 1 : 4]);
-                    cudaEventElapsedTime(&q1, te[0][0], te[1][c]);
-                    cudaEventElapsedTime(&m0, te[0][0], te[2][c]);
-                    cudaEventElapsedTime(&m1, te[0][0], te[3][c]);
-                    std::fprintf(stderr, "chunk %d quantize %.3f-%.3f ms main %.3f-%.3f ms\n", c, q0, q1, m0, m1);
-                }
-                for (auto& row : te)
-                    for (auto& e : row) cudaEventDestroy(e);
-            }
         }
         ctx->check_launch();
     } else {
         ensure_clean();
         ctx->build_scratch_clean = false;
-        static const bool pdl_on = [] {
-            const char* e = std::getenv("SKC_BUILD_PDL");  // "0": A/B switch for the PDL launches
-            return !(e && std::string(e) == "0");
-        }();
-        p.pdl = pdl_on;
-        if (p.xsrc_mode == 1) {  // device-resident class-list build: sums-only pre-pass
-            static const int sums_bps = env_int("SKC_SUMS_BPS", 5, 0, 8);  // 0: previous kernel (A/B)
-            if (sums_bps > 0) {
-                p.lean_sums = true;
-                p.prepass_blocks = std::min(kPrepassBlocks, std::max(1, ctx->sms) * sums_bps);
-            }
-        }
+        p.pdl = true;
+        if (p.xsrc_mode == 1)  // device-resident class-list build: sums-only pre-pass, one wave of 5 blocks/SM
+            p.prepass_blocks = std::min(kPrepassBlocks, std::max(1, ctx->sms) * 5);
         {
             SKC_PROF(ctx, "build_prepass");
             launch_build_prepass(ctx->stream, Tdev, p);
@@ -293,21 +244,22 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
         ctx->check_launch();
     }
     int* flag = ctx->pinned_ints();  // pinned: a direct DMA, not a staged pageable copy
-    CK(cudaMemcpyAsync(flag, p.nonfinite, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(flag, p.nonfinite, 3 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     ctx->sync();
-    const int nonfinite = *flag;
+    const int nonfinite = flag[0], overflow = flag[2];
     // Fixed-point accumulation cannot carry NaN/Inf the way the reference's
     // floating-point sum would; reject instead of producing a wrong sketch.
-    if (nonfinite) fail(kInvalidArgument, "accumulate_dense: tensor has a non-finite entry");
-    if (trace_on) {
-        std::vector<unsigned long long> t(3 * static_cast<size_t>(P));
-        CK(cudaMemcpy(t.data(), trace.p, t.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-        unsigned long long t0 = ~0ull;
-        for (int x = 0; x < P; ++x) t0 = std::min(t0, t[3 * x]);
-        std::fprintf(stderr, "build trace: G=%d spc=%lld P=%d\n", G, spc, P);
-        for (int x = 0; x < P; ++x)
-            std::fprintf(stderr, "cta %3d start %7.1f us dur %7.1f us switches %llu\n", x, (t[3 * x] - t0) * 1e-3,
-                         (t[3 * x + 1] - t[3 * x]) * 1e-3, t[3 * x + 2]);
+    if (nonfinite) {
+        if (overflow) {
+            CK(cudaMemsetAsync(p.ovf, 0, sizeof(int), ctx->stream));
+            ctx->sync();
+        }
+        fail(kInvalidArgument, "accumulate_dense: tensor has a non-finite entry");
+    }
+    if (overflow) {  // a one-limb window overflowed: the finalize added nothing; redo exactly
+        CK(cudaMemsetAsync(p.ovf, 0, sizeof(int), ctx->stream));
+        ++ctx->build_two_limb_retries;
+        run_dense_build(ctx, Tdev, n, dtype, sym, i0, i1, B, b, packed, data, zero_copy, true);
     }
 }
 

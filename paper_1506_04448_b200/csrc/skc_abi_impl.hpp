@@ -123,6 +123,7 @@ struct skc_context {
     cudaStream_t stream = nullptr;
     cudaStream_t stream2 = nullptr;  // pipelined zero-copy builds: main pass of chunk c
     cudaEvent_t ev_q[5] = {};        // chunk c quantized / all chunks done
+    cudaEvent_t ev_order = nullptr;  // skc_context_wait_stream
     cublasHandle_t cublas = nullptr;  // LDA whitening block products (lazy)
     int sms = 148;
     int smem_optin = 227 * 1024;
@@ -151,6 +152,8 @@ struct skc_context {
     DevBuf<int> build_ints;                // per-type row counters of the dense build
     DevBuf<unsigned long long> build_acc;  // exact fixed-point slot accumulators
     bool build_scratch_clean = false;      // build_acc / build_ints are all zero (finalize re-zeroes them)
+    bool build_ovf_clean = false;          // ints[3] (one-limb overflow flag) is zero
+    long long build_two_limb_retries = 0;  // one-limb builds redone with two limbs (overflow)
     const void* build_acc_clean_p = nullptr;  // the buffers (pointer, size) that were cleared
     const void* build_ints_clean_p = nullptr;
     size_t build_acc_clean_n = 0, build_ints_clean_n = 0;
@@ -415,7 +418,7 @@ inline int wave_chunks(int sms, int per_rep, long long cap) {
 const void* stage_tensor(skc_context* ctx, const void* T, int n, int dtype, int location, bool sym, int i0, int i1,
                          bool need_full, size_t* h2d_bytes, bool* zero_copy = nullptr);
 void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool sym, int i0, int i1, int B,
-                     std::uint32_t b, const std::uint32_t* packed, double2* data, bool zero_copy);
+                     std::uint32_t b, const std::uint32_t* packed, double2* data, bool zero_copy, bool two_limb = false);
 // skc_abi.cu
 void spectrum_to_host(skc_context* ctx, const double2* spec, int m, std::uint32_t b, int N, int logN, int S,
                       double* out);

@@ -16,7 +16,8 @@
 // between windows, so the SMs finish together and all windows sweep the rows in the same
 // order (their gathers of the same rows hit L2). The older contiguous-slot-range kernel
 // (k_build_flat: every CTA evaluates every entry against the 1-2 replicates its range
-// overlaps) remains for small asymmetric builds and as an A/B reference.
+// overlaps) remains for small asymmetric builds and for shapes outside the class-list
+// limits (b > 2^22, or n beyond the packed list words).
 //
 // Accumulation is exact 64-bit fixed point: q = round(kappa*T*2^F) is split into two
 // 32-bit limbs added with native ATOMS.ADD (shared fp64 atomics are CAS loops on
@@ -223,91 +224,6 @@ __global__ void __launch_bounds__(NTQ) k_build_quantize(const TT* __restrict__ T
     }
 }
 
-// Sums-only pre-pass for device-resident tensors (class-list builds): per row segment,
-// sum and max of |T| over k > k0 and the k = k0 entry separately, then kappa applied per
-// row (sym: 6/3 off the diagonal pair, 3/1 on it; asym 1). Coalesced 4-deep loads, two
-// floating-point ops per element; non-finite entries surface as a non-finite row sum.
-template <typename TT, bool SYM>
-__global__ void __launch_bounds__(256) k_build_sums(const TT* __restrict__ T, int n,
-                                                    const std::uint32_t* __restrict__ rowtab, int nrows,
-                                                    double* __restrict__ partials, int* __restrict__ nonfinite) {
-    constexpr int W = 8;
-    __shared__ double red[W];
-    // the main pass (launched programmatically dependent) may start its prologue now; it
-    // waits on griddepcontrol.wait before reading these partials
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double blk = 0.0, bmax = 0.0;
-    bool bad = false;
-    // two rows per warp step (their loads in flight together)
-    const int stride = gridDim.x * W;
-    for (int row = blockIdx.x * W + warp; row < nrows; row += 2 * stride) {
-        int ii[2], jj[2], kk0[2];
-        const TT* rp[2];
-        double v[2][4];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int rw = row + h * stride;
-            const bool ok = rw < nrows;
-            const std::uint32_t ij = ok ? rowtab[rw] : 0u;
-            ii[h] = static_cast<int>(ij >> 16);
-            jj[h] = static_cast<int>(ij & 0xFFFFu);
-            kk0[h] = ok ? (SYM ? jj[h] : 0) : n;
-            rp[h] = T + ((size_t)ii[h] * n + jj[h]) * n;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int k = kk0[h] + lane + 32 * u;
-                v[h][u] = (k < n) ? static_cast<double>(__ldg(rp[h] + k)) : 0.0;
-            }
-        }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            double so = 0.0, mo = 0.0, dg = 0.0;
-            for (int kb = kk0[h] + lane; kb < n; kb += 128) {
-                if (kb != kk0[h] + lane) {
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) v[h][u] = (kb + 32 * u < n) ? static_cast<double>(__ldg(rp[h] + kb + 32 * u)) : 0.0;
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const double a = fabs(v[h][u]);
-                    if (SYM && kb + 32 * u == kk0[h]) {
-                        dg = a;
-                    } else {
-                        so += a;
-                        mo = fmax(mo, a);
-                    }
-                }
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                so += __shfl_xor_sync(0xffffffffu, so, o);
-                mo = fmax(mo, __shfl_xor_sync(0xffffffffu, mo, o));
-            }
-            dg = __shfl_sync(0xffffffffu, dg, 0);  // lane 0 held k = k0
-            so = __shfl_sync(0xffffffffu, so, 0);
-            const int i = ii[h], j = jj[h];
-            const double ko = SYM ? (i == j ? 3.0 : 6.0) : 1.0, kd = SYM ? (i == j ? 1.0 : 3.0) : 1.0;
-            const double L1 = ko * so + kd * dg;
-            const double mx = fmax(ko * mo, kd * dg);
-            bad |= !isfinite(L1) || !isfinite(mx);
-            blk += (lane == 0) ? L1 : 0.0;
-            bmax = fmax(bmax, mx);
-        }
-    }
-    if (bad) atomicOr(nonfinite, 1);
-    const double s = block_sum_b<256>(blk, red);
-    if (threadIdx.x == 0) partials[blockIdx.x] = s;
-    __syncthreads();
-    if (lane == 0) red[warp] = bmax;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double mx = 0.0;
-        for (int w = 0; w < W; ++w) mx = fmax(mx, red[w]);
-        partials[gridDim.x + blockIdx.x] = mx;
-    }
-}
-
 // Lean sums-only pre-pass (default for device-resident class-list builds). Each lane
 // keeps its own kappa-weighted L1 sum and maximum across all the rows its warp visits:
 // kappa is applied per element (the k = k0 entry takes the diagonal weight), so no row
@@ -389,7 +305,7 @@ __global__ void __launch_bounds__(256, 5) k_build_sums_lean(const TT* __restrict
 // builds use p.prepass_blocks x 1024-thread blocks on a few SMs (PCIe-bound), leaving the
 // rest to the concurrent main pass of the previous chunk.
 void launch_build_prepass(cudaStream_t st, const void* T, const BuildPlan& p) {
-    if (p.reset_nonfinite && !p.lean_sums) cudaMemsetAsync(p.nonfinite, 0, sizeof(int), st);
+    if (p.reset_nonfinite && p.xsrc_mode != 1) cudaMemsetAsync(p.nonfinite, 0, sizeof(int), st);
     const bool wide = p.prepass_threads == 1024;
     const int blocks = p.prepass_blocks;
     const bool vec16 = (reinterpret_cast<std::uintptr_t>(T) & 15) == 0;
@@ -418,10 +334,8 @@ void launch_build_prepass(cudaStream_t st, const void* T, const BuildPlan& p) {
     {                                                                                                 \
         if (mode == kQuant) QUANT_M(TT, SY, kQuant)                                                   \
         else if (mode == kRaw) QUANT_M(TT, SY, kRaw)                                                  \
-        else if (p.lean_sums) k_build_sums_lean<TT, SY><<<blocks, 256, 0, st>>>(                      \
+        else k_build_sums_lean<TT, SY><<<blocks, 256, 0, st>>>(                                       \
             (const TT*)T, p.n, p.rowtab, p.nrows, p.prepass_partials, p.nonfinite);                   \
-        else k_build_sums<TT, SY><<<blocks, 256, 0, st>>>((const TT*)T, p.n, p.rowtab, p.nrows,      \
-                                                          p.prepass_partials, p.nonfinite);           \
     }
     if (p.sym) {
         if (p.dtype == 0) QUANT(double, true)
@@ -436,7 +350,6 @@ void launch_build_prepass(cudaStream_t st, const void* T, const BuildPlan& p) {
 }
 
 // ---- main pass -----------------------------------------------------------------------
-constexpr int kChunkRows = 16;  // rows per warp-level grab
 
 // Exact 64-bit add of (ql, qh) into the limb pair (lo at addr_lo, hi at addr_hi). The
 // limbs live in separate planes (4-byte stride: random slots spread over all 32 banks).
@@ -495,10 +408,13 @@ struct BuildArgs {
     int xmode;
     int* scale_out;                // global exponent F, written by CTA 0 for the finalize
     int* nonfinite_out;            // lean pre-pass: CTA 0 stores the flag from the partials (no memset)
+    int* ovf_out;                  // one-limb windows: set when a limb overflowed (zero on entry)
+    int sym_even_F;                // symmetric one-limb / two-limb class-list builds: F even (see cta_scale_exp)
     int* next_row;                 // G row (or tile) counters (zero on entry; the finalize re-zeroes them)
+    int qbits;                     // max |q| exponent: 50 (two limbs) or 22 (one limb, fp32 input)
+    int slab_cap;                  // class-list kernel: slabs per warp table
 
     unsigned long long* acc;       // total_slots exact accumulators (zero on entry; the finalize re-zeroes them)
-    unsigned long long* trace;     // optional: per-CTA (start, end, switches)
 };
 
 // Global exponent F = min(61 - ceil(log2(sum kappa|T|)), 50 - ceil(log2(max kappa|T|))):
@@ -525,8 +441,12 @@ __device__ int cta_scale_exp(const BuildArgs& a) {
                 int ex, exm;
                 frexp(acc, &ex);  // acc <= 2^ex
                 frexp(mx, &exm);  // mx <= 2^exm
-                F = min(61 - ex, 50 - exm);
+                F = min(61 - ex, a.qbits - exm);
                 F = F > 1000 ? 1000 : (F < -1000 ? -1000 : F);
+                // symmetric class-list builds take F even: the exponent field of the scale
+                // kappa * 2^F = 1.5 * 2^(F+2) is then odd, so kappa 6 -> 3 (i = j rows) is one
+                // XOR of its low bit (the row word carries that bit)
+                if (a.sym_even_F) F &= ~1;
             }
             sF = F;
             if (blockIdx.x == 0) {
@@ -538,182 +458,6 @@ __device__ int cta_scale_exp(const BuildArgs& a) {
     }
     __syncthreads();
     return sF;
-}
-
-struct RowMeta {
-    int i, j, k0, d;
-    const long long* qrow;  // qbuf + rowoff - k0: entry k of the row at qrow[k]
-};
-template <bool SYM>
-__device__ __forceinline__ RowMeta load_meta(const BuildArgs& a, int row, int F) {
-    const std::uint32_t ij = __ldg(a.rowtab + row);
-    const long long off = __ldg(a.rowoff + row);
-    const int rf = __ldg(a.rowF + row);
-    RowMeta m;
-    m.i = static_cast<int>(ij >> 16);
-    m.j = static_cast<int>(ij & 0xFFFFu);
-    m.k0 = SYM ? m.j : 0;
-    m.d = rf - F;  // >= 0
-    m.qrow = a.qbuf + off - m.k0;
-    return m;
-}
-__device__ __forceinline__ void load_block(long long (&q)[4], const long long* qrow, int kb, int n) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) q[u] = (kb + 32 * u < n) ? __ldg(qrow + kb + 32 * u) : 0ll;
-}
-
-// Persistent CTAs with dynamic load balancing. A CTA holds the limb window of one slot
-// range ("type" g: ~27K contiguous slots of the B x (2b | b) slot space); its warps grab
-// 16-row chunks of the sorted-triple row stream from the type's atomic counter and
-// evaluate every streamed entry against the (1..RMAX) replicates the range overlaps:
-// in-range contributions go to the window, the rest to a per-lane trash pair. When a
-// type's rows run out, the CTA adds its window into the global exact accumulators
-// (integer RED.64: order-independent, so the sketch stays bit-deterministic) and moves
-// to the type with the most rows left. Each warp walks its rows software-pipelined: the
-// next 128-entry block's loads are issued before the current block is processed, the
-// next row's metadata one row ahead and the next chunk grab one chunk ahead.
-template <bool SYM, int RMAX, int NT>
-__global__ void __launch_bounds__(NT, 1) k_build_dyn(BuildArgs a) {
-    constexpr int kBuildThreads = NT;
-    extern __shared__ std::uint32_t sacc[];
-    __shared__ int s_next_g;
-    const int spc = a.slots_per_cta;
-    const int plane = spc + 32;                  // limbs + 32 trash slots
-    std::uint32_t* ptab = sacc + 2 * plane;      // RMAX x n (streamed-mode hashes)
-    std::uint32_t* pij_tab = ptab + RMAX * a.n;  // RMAX x 2n (row-pair hashes)
-    const int n = a.n, nrows = a.nrows;
-    const long long spr = SYM ? 2ll * (a.bmask + 1) : static_cast<long long>(a.bmask + 1);
-    const int prow = SYM ? n : 3 * n;
-    const int F = cta_scale_exp(a);
-    std::uint32_t sbase = static_cast<std::uint32_t>(__cvta_generic_to_shared(sacc));
-    asm volatile("mov.b32 %0, %0;" : "+r"(sbase));  // keep in a register (no per-use S2UR/ULEA)
-    const std::uint32_t hioff = 4u * static_cast<std::uint32_t>(plane);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const std::uint32_t trash_idx = static_cast<std::uint32_t>(spc + lane);
-    unsigned long long t_start = 0, switches = 0;
-    if (a.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-
-    int g = static_cast<int>((static_cast<long long>(blockIdx.x) * a.G) / gridDim.x);
-    while (g >= 0) {
-        const long long slot_lo = (long long)g * spc;
-        const long long slot_hi = min(slot_lo + spc, a.total_slots);
-        const int nslots = static_cast<int>(slot_hi - slot_lo);
-        const int m_lo = static_cast<int>(slot_lo / spr);
-        const int R = static_cast<int>((slot_hi - 1) / spr) - m_lo + 1;
-        for (int s = threadIdx.x; s < 2 * plane; s += kBuildThreads) sacc[s] = 0u;
-        for (int x = threadIdx.x; x < RMAX * n; x += kBuildThreads) {
-            const int r = x / n, k = x - r * n;
-            const std::uint32_t* pm = a.packed + (size_t)(m_lo + min(r, R - 1)) * prow;
-            ptab[x] = pm[(SYM ? 0 : 2 * n) + k];
-            pij_tab[r * 2 * n + k] = pm[k];
-            pij_tab[r * 2 * n + n + k] = pm[(SYM ? 0 : n) + k];
-        }
-        __syncthreads();
-        int base[RMAX];
-#pragma unroll
-        for (int r = 0; r < RMAX; ++r) base[r] = static_cast<int>((long long)(m_lo + r) * spr - slot_lo);
-
-        // ---- warp row iterator: current chunk [c0, c1), next chunk start (prefetched grab)
-        int c0 = 0, c1 = 0, ncs = 0;
-        if (lane == 0) c0 = atomicAdd(a.next_row + g, kChunkRows);
-        c0 = __shfl_sync(0xffffffffu, c0, 0);
-        if (c0 < nrows) {
-            c1 = min(c0 + kChunkRows, nrows);
-            if (lane == 0) ncs = atomicAdd(a.next_row + g, kChunkRows);  // one chunk ahead
-            ncs = __shfl_sync(0xffffffffu, ncs, 0);
-            int row = c0;
-            RowMeta mc = load_meta<SYM>(a, row, F), mn{};
-            // next row: same chunk, else the prefetched chunk
-            int nrow = (row + 1 < c1) ? row + 1 : ncs;
-            bool has_next = nrow < nrows;
-            if (has_next) mn = load_meta<SYM>(a, nrow, F);
-            int kb = mc.k0 + lane;
-            long long qc[4];
-            load_block(qc, mc.qrow, kb, n);
-            std::uint32_t pij[RMAX];
-#pragma unroll
-            for (int r = 0; r < RMAX; ++r) pij[r] = pij_tab[r * 2 * n + mc.i] + pij_tab[r * 2 * n + n + mc.j];
-            for (;;) {
-                const bool same_row = kb - lane + 128 < n;
-                const bool nvalid = same_row || has_next;
-                const int nkb = same_row ? kb + 128 : mn.k0 + lane;
-                long long qn[4];
-                if (nvalid) load_block(qn, same_row ? mc.qrow : mn.qrow, nkb, n);
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int k = kb + 32 * u;
-                    if (k - lane >= n) break;  // warp-uniform: no lane of this group is in the row
-                    if (k < n) {
-                        // zero entries add nothing (sketch.cpp:337 skips them)
-                        const unsigned long long q = static_cast<unsigned long long>(qc[u] >> mc.d);
-                        const unsigned long long nq = 0ull - q;
-                        const std::uint32_t ql = static_cast<std::uint32_t>(q), qh = static_cast<std::uint32_t>(q >> 32);
-                        const std::uint32_t nql = static_cast<std::uint32_t>(nq), nqh = static_cast<std::uint32_t>(nq >> 32);
-#pragma unroll
-                        for (int r = 0; r < RMAX; ++r) {
-                            if (r < R) {  // CTA-uniform
-                                const std::uint32_t p = pij[r] + ptab[r * n + k];
-                                const std::uint32_t s = static_cast<std::uint32_t>(base[r]) +
-                                                        (SYM ? (((p & a.bmask) << 1) | ((p >> 30) & 1u)) : (p & a.bmask));
-                                const bool neg = static_cast<int>(p) < 0;
-                                const std::uint32_t addr =
-                                    sbase + 4u * (s < static_cast<std::uint32_t>(nslots) ? s : trash_idx);
-                                add64(addr, addr + hioff, neg ? nql : ql, neg ? nqh : qh);
-                            }
-                        }
-                    }
-                }
-                if (!nvalid) break;
-                if (!same_row) {
-                    if (row + 1 >= c1) {  // entering the prefetched chunk: grab the one after
-                        c0 = nrow;
-                        c1 = min(c0 + kChunkRows, nrows);
-                        if (lane == 0) ncs = atomicAdd(a.next_row + g, kChunkRows);
-                        ncs = __shfl_sync(0xffffffffu, ncs, 0);
-                    }
-                    row = nrow;
-                    mc = mn;
-                    nrow = (row + 1 < c1) ? row + 1 : ncs;
-                    has_next = nrow < nrows;
-                    if (has_next) mn = load_meta<SYM>(a, nrow, F);
-#pragma unroll
-                    for (int r = 0; r < RMAX; ++r) pij[r] = pij_tab[r * 2 * n + mc.i] + pij_tab[r * 2 * n + n + mc.j];
-                }
-                kb = nkb;
-#pragma unroll
-                for (int u = 0; u < 4; ++u) qc[u] = qn[u];
-            }
-        }
-        __syncthreads();
-        // flush the window into the exact global accumulators
-        unsigned long long* out = a.acc + slot_lo;
-        for (int s = threadIdx.x; s < nslots; s += kBuildThreads) {
-            const unsigned long long v = (static_cast<unsigned long long>(sacc[plane + s]) << 32) | sacc[s];
-            if (v) atomicAdd(out + s, v);
-        }
-        // next type: the one with the most rows left (ties: lowest index)
-        if (threadIdx.x == 0) {
-            int best = -1, left = 0;
-            for (int t = 0; t < a.G; ++t) {
-                const int l = nrows - *((volatile int*)(a.next_row + t));
-                if (l > left) {
-                    left = l;
-                    best = t;
-                }
-            }
-            s_next_g = best;
-            ++switches;
-        }
-        __syncthreads();
-        g = s_next_g;
-    }
-    if (a.trace && threadIdx.x == 0) {
-        unsigned long long t_end;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
-        a.trace[3 * blockIdx.x] = t_start;
-        a.trace[3 * blockIdx.x + 1] = t_end;
-        a.trace[3 * blockIdx.x + 2] = switches;
-    }
 }
 
 // Flat-chunk variant of the persistent build (default). A warp grabs a chunk of up to 16
@@ -751,8 +495,6 @@ __global__ void __launch_bounds__(1024, 1) k_build_flat(BuildArgs a) {
     asm volatile("mov.b32 %0, %0;" : "+r"(sbase));  // keep in a register (no per-use S2UR/ULEA)
     const std::uint32_t hioff = 4u * static_cast<std::uint32_t>(plane);
     const std::uint32_t trash_idx = static_cast<std::uint32_t>(spc + lane);
-    unsigned long long t_start = 0, switches = 0;
-    if (a.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 
     int g = static_cast<int>((static_cast<long long>(blockIdx.x) * a.G) / gridDim.x);
     while (g >= 0) {
@@ -890,17 +632,9 @@ __global__ void __launch_bounds__(1024, 1) k_build_flat(BuildArgs a) {
                 }
             }
             s_next_g = best;
-            ++switches;
         }
         __syncthreads();
         g = s_next_g;
-    }
-    if (a.trace && threadIdx.x == 0) {
-        unsigned long long t_end;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
-        a.trace[3 * blockIdx.x] = t_start;
-        a.trace[3 * blockIdx.x + 1] = t_end;
-        a.trace[3 * blockIdx.x + 2] = switches;
     }
 }
 
@@ -916,58 +650,110 @@ __global__ void __launch_bounds__(1024, 1) k_build_flat(BuildArgs a) {
 // of the class list, gathered from the row in qbuf: every (entry, replicate) pair is
 // evaluated once, in the one window it lands in (no out-of-window evaluations, no trash
 // atomics), against ~2.2 evaluations per pair for the contiguous-slot windows above.
-constexpr int kClsRows = 32;
-__host__ __device__ constexpr int cls_meta_words() { return 4 * kClsRows + 4; }  // int4 per row (+ align)
+constexpr int kClsRows = 32;  // rows per grab
+constexpr int kSlabCapMax = 256;  // most 32-entry slabs in a warp's table
 __host__ __device__ constexpr int cls_sfx_words(int C, int n) { return (C * (n + 1) + 1) / 2; }
 
-size_t cls_smem_bytes(std::uint32_t b, int tbits, int n, bool sym) {
+// Window limbs (plus 32 dummy slots per plane), class list, hash words, suffix tables.
+static size_t cls_fixed_bytes(std::uint32_t b, int tbits, int n, bool sym, bool one_limb) {
     const int C = (sym ? 2 : 1) << tbits;
     const size_t W = static_cast<size_t>(b) >> tbits;
-    return sizeof(std::uint32_t) * (2 * W + 3 * (size_t)n + cls_sfx_words(C, n) + 4 + 32 * (size_t)cls_meta_words());
+    return (sizeof(std::uint32_t) * ((one_limb ? 1 : 2) * (W + 32) + 3 * (size_t)n + cls_sfx_words(C, n)) + 15) &
+           ~size_t(15);
+}
+// Slabs per warp table that fit beside the fixed part in `limit` bytes, or 0 when even
+// one row of the largest possible class (n entries) does not fit.
+int cls_slab_cap(std::uint32_t b, int tbits, int n, bool sym, bool one_limb, size_t limit) {
+    const size_t fixed = cls_fixed_bytes(b, tbits, n, sym, one_limb);
+    if (fixed >= limit) return 0;
+    long long cap = static_cast<long long>((limit - fixed) / (32 * sizeof(int4)));
+    cap = cap < kSlabCapMax ? cap : kSlabCapMax;
+    return cap < (n + 31) / 32 ? 0 : static_cast<int>(cap);
+}
+size_t cls_smem_bytes(std::uint32_t b, int tbits, int n, bool sym, bool one_limb, int slab_cap) {
+    return cls_fixed_bytes(b, tbits, n, sym, one_limb) + 32 * sizeof(int4) * static_cast<size_t>(slab_cap);
 }
 
+// One-limb add for fp32 inputs (|q| < 2^22): the window keeps each slot's exact sum
+// mod 2^32 biased by 2^31, so the centred value v = limb ^ 2^31 starts at 0 and a pass's
+// partial sums (~sqrt(count) * |q|) stay far from the +-2^31 edge. The flush adds v
+// itself to the slot's 64-bit accumulator, so without an overflow the accumulator holds
+// the exact sum, as with two limbs; the returned old limb shows any overflow (one LOP3).
+constexpr std::uint32_t kLimbBias = 0x80000000u;
+// The centred value can only overflow after 2^(31-22) = 512 same-signed full-scale adds
+// to one slot within one window pass, so the add does not branch on it: each lane ORs the
+// overflow test into `ovf` (sign bit = some add overflowed), the window pass reports it,
+// and the host then discards the build (the finalize adds nothing) and repeats it exactly
+// with two limbs. Ordinary data never takes that path.
+__device__ __forceinline__ void add32_idx(std::uint32_t idx, std::uint32_t sbase, std::int32_t q, std::uint32_t& ovf) {
+    std::uint32_t old;
+    asm volatile(
+        "{\n\t.reg .u32 al;\n\t"
+        "mad.lo.u32 al, %1, 4, %2;\n\t"
+        "atom.shared.add.u32 %0, [al], %3;\n\t}"
+        : "=r"(old)
+        : "r"(idx), "r"(sbase), "r"(static_cast<std::uint32_t>(q)));
+    const std::uint32_t nw = old + static_cast<std::uint32_t>(q);
+    // signed overflow of the centred v + q: v and q share a sign and v's sign flips
+    ovf |= (old ^ nw) & ~(old ^ kLimbBias ^ static_cast<std::uint32_t>(q));
+}
 // Entries are read straight from T (device-resident: xmode 1) or from the pre-pass's packed
 // row copy (xmode 2), element type XT, and rounded to q = round(kappa * T * 2^F) by one fma
-// against 1.5 * 2^52 (|q| < 2^50 by the choice of F). The scale's sign bit carries the
+// against 1.5 * 2^52 (fp64 input, two limbs, |q| < 2^50) or 1.5 * 2^23 (fp32 input, one
+// limb, |q| < 2^22): exact single rounding either way. The scale's sign bit carries the
 // complex4 sign, so the add needs no separate negation. kappa is per row (6 or 3 sym; 1
 // asym); the k = j entry of a sym row, whose kappa is 3 (or 1), gets its correction
 // (-3 or -2) added once per row when the row's metadata is built.
-template <bool SYM, int TB, typename XT>
+//
+// A warp grabs R rows of its window (R <= 32, sized so every 32-entry slab of the rows'
+// in-window runs fits the warp's slab table), builds one int4 per slab (list position of
+// its lane 0, source offset of the row, row pair word, active lanes) and then walks the
+// slab table four slabs per step: each slab is one row's 32 consecutive class-list
+// entries (lane l takes entry l), so the row data come from one broadcast LDS.128 and no
+// lane keeps a row cursor; all four slabs' list words and gathers are issued before
+// their adds. (A row-at-a-time walk with the row data broadcast by shuffles measured
+// 3.54 ms at config 2 against 2.72 for the table.)
+template <bool SYM, int TB, typename XT, bool L1>
 __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
-    constexpr int NT = 1024, C = (SYM ? 2 : 1) << TB;
+    constexpr int NT = 1024, C = (SYM ? 2 : 1) << TB, NPL = L1 ? 1 : 2;  // limb planes in the window
     constexpr std::uint32_t tmask = (1u << TB) - 1u;
     extern __shared__ __align__(16) std::uint32_t sm[];
     __shared__ int s_next_g;
     __shared__ int s_cend[C];
     __shared__ int s_wcnt[C * 32];  // per-(class, 32-k segment) counts, then their scan
     const int n = a.n, nrows = a.nrows;
-    const int W = static_cast<int>((a.bmask + 1u) >> TB);  // slots per plane
+    const int W = static_cast<int>((a.bmask + 1u) >> TB);  // slots per window
+    const int WP = W + 32;  // plane stride: slots W + lane are inactive lanes' private dummy slots
     // n list words grouped by class: h_k | k << KS | e_k << 30 (KS = log2 b + 2 clears the
     // 3-term bucket sum; the host checks that k fits below bit 30)
-    std::uint32_t* lst = sm + 2 * W;
+    std::uint32_t* lst = sm + NPL * WP;
     std::uint32_t* pw = reinterpret_cast<std::uint32_t*>(lst + n);  // sym n: h | e << 30; asym 2n: modes 1, 2
     unsigned short* sfx = reinterpret_cast<unsigned short*>(pw + 2 * n);  // C x (n + 1)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // per-warp row metadata, one int4 per row: (end entry, list position - entry index,
-    // source element index of (i, j, 0) relative to the chunk, c_ij | [i == j] << 24 | e_ij << 30)
-    int4* meta = reinterpret_cast<int4*>(
-        sm + ((static_cast<size_t>(2 * W + 3 * n + cls_sfx_words(C, n)) + 3) & ~static_cast<size_t>(3))) + warp * kClsRows;
+    // per-warp slab table, one int4 per slab: (list position of lane 0, source element index
+    // of (i, j, 0) relative to the grab, c_ij | [i == j] << 23 | e_ij << 30, active lanes)
+    int4* slab = reinterpret_cast<int4*>(
+                     sm + ((static_cast<size_t>(NPL * WP + 3 * n + cls_sfx_words(C, n)) + 3) & ~static_cast<size_t>(3))) +
+                 warp * a.slab_cap;
     // F comes from the pre-pass partials: read after griddepcontrol.wait, which the first
     // window's prologue (zeroing, hash words, class lists) runs ahead of (PDL launch)
     int F = 0;
     bool have_F = false;
     std::uint32_t sbase = static_cast<std::uint32_t>(__cvta_generic_to_shared(sm));
     asm volatile("mov.b32 %0, %0;" : "+r"(sbase));
-    const std::uint32_t hioff = pin(4u * static_cast<std::uint32_t>(W));
+    const std::uint32_t hioff = pin(4u * static_cast<std::uint32_t>(WP));
     const std::uint32_t bmask = pin(a.bmask);
-    const std::uint32_t lst_s = pin(sbase + 8u * static_cast<std::uint32_t>(W));
+    const std::uint32_t lst_s = pin(sbase + 4u * NPL * static_cast<std::uint32_t>(WP));
     const int KS = __popc(a.bmask) + 2;
     const std::uint32_t kmask = pin((1u << (30 - KS)) - 1u);
     const std::uint32_t wmask = pin(~(kmask << KS));
     const XT* __restrict__ xsrc = static_cast<const XT*>(a.xsrc);
-    // high word of kappa * 2^F: sym kappa 6 = 1.5 * 2^2 (kappa 3 is one exponent step less);
-    // asym kappa 1
+    // high word of kappa * 2^F (fp64; the float bits for one limb): sym kappa 6 = 1.5 * 2^2
+    // (kappa 3 is one exponent step less); asym kappa 1
+    constexpr int EXS = L1 ? 23 : 20;          // exponent field position
+    constexpr int EXB = L1 ? 127 : 1023;       // exponent bias
     std::uint32_t sc_hi0 = 0;
+    std::uint32_t ovf = 0;  // one-limb overflow indicator (sign bit)
     constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
     constexpr long long kMagicBits = 0x4338000000000000ll;
     // exact round(x * sc): |x * sc| < 2^50, one rounding in the fma
@@ -975,13 +761,16 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
         const double sc = __hiloint2double(static_cast<int>(schi), 0);
         return __double_as_longlong(fma(x, sc, kMagic)) - kMagicBits;
     };
-    unsigned long long t_start = 0, switches = 0;
-    if (a.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    // exact round(x * sc) in fp32: |x * sc| < 2^22, one rounding in the fma against 1.5 * 2^23
+    auto to_fixed32 = [](float x, std::uint32_t scbits) -> std::int32_t {
+        return __float_as_int(__fmaf_rn(x, __int_as_float(static_cast<int>(scbits)), 12582912.0f)) - 0x4B400000;
+    };
 
     int g = static_cast<int>((static_cast<long long>(blockIdx.x) * a.G) / gridDim.x);
     while (g >= 0) {
         const int m = g / C, P = SYM ? (g >> TB) & 1 : 0, r = g & static_cast<int>(tmask);
-        for (int s = threadIdx.x; s < 2 * W; s += NT) sm[s] = 0u;
+        for (int s = threadIdx.x; s < NPL * WP; s += NT) sm[s] = L1 ? kLimbBias : 0u;
+        unsigned long long* gacc = a.acc + static_cast<long long>(g) * W;  // this window's accumulators
         // asym packed words are h | neg << 31 for modes 1..3 (B x 3 x n): the list holds
         // mode 3, the row pair word is mode 1 (i) + mode 2 (j); bit 31 of a sum is the sign
         for (int k = threadIdx.x; k < (SYM ? n : 2 * n); k += NT) pw[k] = a.packed[(size_t)m * (SYM ? n : 3 * n) + k];
@@ -1069,27 +858,31 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
         if (!have_F) {  // block-uniform
             asm volatile("griddepcontrol.wait;" ::: "memory");
             F = cta_scale_exp(a);
-            sc_hi0 = pin(SYM ? ((static_cast<std::uint32_t>(1023 + F + 2) << 20) | (1u << 19))
-                             : (static_cast<std::uint32_t>(1023 + F) << 20));
+            sc_hi0 = pin(SYM ? ((static_cast<std::uint32_t>(EXB + F + 2) << EXS) | (1u << (EXS - 1)))
+                             : (static_cast<std::uint32_t>(EXB + F) << EXS));
             have_F = true;
             asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         }
 
+        // rows per grab: every slab of the grabbed rows' runs must fit the warp's table
+        int maxsl = 1;
+        for (int cc = 0; cc < C; ++cc) maxsl = max(maxsl, (s_cend[cc] - (cc ? s_cend[cc - 1] : 0) + 31) >> 5);
+        const int R = max(1, min(kClsRows, a.slab_cap / maxsl));
         int c0 = 0;
-        if (lane == 0) c0 = atomicAdd(a.next_row + g, kClsRows);
+        if (lane == 0) c0 = atomicAdd(a.next_row + g, R);
         c0 = __shfl_sync(0xffffffffu, c0, 0);
         while (c0 < nrows) {
-            int cn = 0;  // next grab, one chunk ahead
-            if (lane == 0) cn = atomicAdd(a.next_row + g, kClsRows);
-            const int nr = min(kClsRows, nrows - c0);
+            int cn = 0;  // next grab, one grab ahead
+            if (lane == 0) cn = atomicAdd(a.next_row + g, R);
+            const int nr = min(R, nrows - c0);
             long long off = 0;  // source element index of (i, j, 0)
-            int cnt = 0, pos0 = 0, j = 0;
+            int cnt = 0, pos0 = 0;
             std::uint32_t pwd = 0;
             if (lane < nr) {
                 const int row = c0 + lane;
                 const std::uint32_t ij = __ldg(a.rowtab + row);
                 const int i = static_cast<int>(ij >> 16);
-                j = static_cast<int>(ij & 0xFFFFu);
+                const int j = static_cast<int>(ij & 0xFFFFu);
                 off = a.xmode == 1 ? (static_cast<long long>(i) * n + j) * n : __ldg(a.rowoff + row) - (SYM ? j : 0);
                 const std::uint32_t pij = pw[i] + pw[(SYM ? 0 : n) + j];
                 const int cl = SYM ? static_cast<int>(((((pij >> 30) & 1u) ^ static_cast<std::uint32_t>(P)) << TB) |
@@ -1098,107 +891,95 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
                 pos0 = sfx[cl * (n + 1) + (SYM ? j : 0)];
                 cnt = s_cend[cl] - pos0;
                 const bool ii = SYM && i == j;
-                pwd = pij + (ii ? (1u << 24) : 0u);  // bucket sums < 3b <= 2^24 stay below bit 24
+                // bucket sums < 3b <= 3 * 2^21 stay below bit 23; bit 23 marks i = j (kappa 3)
+                pwd = pij + (ii ? (1u << 23) : 0u);
                 if (SYM && cnt > 0) {
                     // k = j: kappa 3 (i < j) or 1 (i = j) where the row walk applies 6 or 3
                     const std::uint32_t lw0 = lst[pos0];
                     if (static_cast<int>((lw0 >> KS) & kmask) == j) {
-                        const double x = static_cast<double>(xsrc[off + j]);
                         const std::uint32_t p0 = pij + (lw0 & wmask);
                         // -3 * 2^F = -1.5 * 2^(F+1);  -2 * 2^F = -1.0 * 2^(F+1)
-                        const std::uint32_t hi = ((static_cast<std::uint32_t>(1023 + F + 1) << 20) | (ii ? 0u : (1u << 19))) ^
-                                                 0x80000000u ^ (p0 & 0x80000000u);
-                        const unsigned long long qd = static_cast<unsigned long long>(to_fixed(x, hi));
-                        add64_idx((p0 & bmask) >> TB, sbase, hioff, static_cast<std::uint32_t>(qd),
-                                  static_cast<std::uint32_t>(qd >> 32));
+                        const std::uint32_t hi =
+                            ((static_cast<std::uint32_t>(EXB + F + 1) << EXS) | (ii ? 0u : (1u << (EXS - 1)))) ^
+                            0x80000000u ^ (p0 & 0x80000000u);
+                        if (L1) {
+                            add32_idx((p0 & bmask) >> TB, sbase, to_fixed32(static_cast<float>(xsrc[off + j]), hi),
+                                      ovf);
+                        } else {
+                            const unsigned long long qd =
+                                static_cast<unsigned long long>(to_fixed(static_cast<double>(xsrc[off + j]), hi));
+                            add64_idx((p0 & bmask) >> TB, sbase, hioff, static_cast<std::uint32_t>(qd),
+                                      static_cast<std::uint32_t>(qd >> 32));
+                        }
                     }
                 }
             }
-            int incl = cnt;
+            const int nsl = (cnt + 31) >> 5;
+            int incl = nsl;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const int v = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += v;
             }
             const long long off0 = __shfl_sync(0xffffffffu, off, 0);
-            const int E = __shfl_sync(0xffffffffu, incl, 31);
-            if (lane < nr) meta[lane] = make_int4(incl, pos0 - (incl - cnt), static_cast<int>(off - off0), static_cast<int>(pwd));
+            const int S = __shfl_sync(0xffffffffu, incl, 31);
+            for (int q = 0, sb = incl - nsl; q < nsl; ++q)
+                slab[sb + q] = make_int4(pos0 + 32 * q, static_cast<int>(off - off0), static_cast<int>(pwd), cnt - 32 * q);
             __syncwarp();
             const XT* qch = xsrc + off0;
             asm volatile("mov.b64 %0, %0;" : "+l"(qch));  // one IMAD.WIDE per gather address
-            int t = 0;
-            int4 cur = meta[0];
-            // load stage: list entry, gathered q and the packed word p = c_ij + h_k | d | e.
-            // Lanes past the chunk end get q = 0 and a private slot (their add is a no-op).
-            auto fetch = [&](XT& q, std::uint32_t& p, int e) {
-                if (e >= cur.x) {  // crossed into a later row of the chunk
-                    cur = meta[++t];
-                    while (e >= cur.x) cur = meta[++t];
+            // four slabs per step, branch-free: inactive lanes load a valid entry of their
+            // slab's row (list index clamped) and add 0 into their private dummy slot
+            // W + lane; the last partial step re-reads the last slab with no active lanes
+            auto step4 = [&](int s0, bool full) {
+                XT xv[4];
+                std::uint32_t pv[4], sv[4];
+                bool act[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int4 d = slab[full ? s0 + u : min(s0 + u, S - 1)];  // broadcast
+                    act[u] = lane < (full || s0 + u < S ? d.w : 0);
+                    const std::uint32_t lw =
+                        lds_u32(lst_s + 4u * static_cast<std::uint32_t>(d.x + min(lane, d.w - 1)));
+                    xv[u] = __ldg(qch + static_cast<std::uint32_t>(d.y + static_cast<int>((lw >> KS) & kmask)));
+                    pv[u] = static_cast<std::uint32_t>(d.z) + (lw & wmask);
+                    sv[u] = act[u] ? (pv[u] & bmask) >> TB : static_cast<std::uint32_t>(W + lane);
                 }
-                const std::uint32_t lw = lds_u32(lst_s + 4u * static_cast<std::uint32_t>(e + cur.y));
-                q = __ldg(qch + static_cast<std::uint32_t>(cur.z + static_cast<int>((lw >> KS) & kmask)));
-                p = static_cast<std::uint32_t>(cur.w) + (lw & wmask);
-            };
-            // Full 128-entry blocks skip the per-entry bound checks; in the chunk's last
-            // block, lanes past the end get q = 0 and a private slot (a no-op add).
-            auto load4 = [&](XT (&q)[4], std::uint32_t (&p)[4], int eb) {
-                if (eb + 128 <= E) {
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) fetch(q[u], p[u], eb + lane + 32 * u);
-                } else {
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int e = eb + lane + 32 * u;
-                        q[u] = 0;
-                        p[u] = static_cast<std::uint32_t>(lane);
-                        if (e < E) fetch(q[u], p[u], e);
+                for (int u = 0; u < 4; ++u) {
+                    // kappa * 2^F with the complex4 sign (bit 31 of p) in its sign bit
+                    if (L1) {
+                        // fp32 scale: the sign (bit 31) and the i = j halving (bit 23, the low
+                        // exponent bit) in one LOP3
+                        const std::uint32_t hi = sc_hi0 ^ (pv[u] & (SYM ? 0x80800000u : 0x80000000u));
+                        const std::int32_t q = to_fixed32(static_cast<float>(xv[u]), hi);
+                        add32_idx(sv[u], sbase, act[u] ? q : 0, ovf);
+                    } else {
+                        // fp64 scale high word: exponent low bit at 20 (F even: halving = XOR)
+                        const std::uint32_t hi = (SYM ? sc_hi0 ^ ((pv[u] >> 3) & (1u << 20)) : sc_hi0) ^
+                                                 (pv[u] & 0x80000000u);
+                        const long long v = act[u] ? to_fixed(static_cast<double>(xv[u]), hi) : 0ll;
+                        add64_idx(sv[u], sbase, hioff, static_cast<std::uint32_t>(v),
+                                  static_cast<std::uint32_t>(static_cast<unsigned long long>(v) >> 32));
                     }
                 }
             };
-            auto process = [&](const XT (&q)[4], const std::uint32_t (&p)[4], int eb) {
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    if (eb + 32 * u >= E) break;  // warp-uniform
-                    // kappa * 2^F with the complex4 sign (bit 31 of p) in its sign bit
-                    const std::uint32_t hi = (SYM ? sc_hi0 - ((p[u] & (1u << 24)) >> 4) : sc_hi0) ^ (p[u] & 0x80000000u);
-                    const unsigned long long v = static_cast<unsigned long long>(to_fixed(static_cast<double>(q[u]), hi));
-                    const std::uint32_t s = (p[u] & bmask) >> TB;
-                    add64_idx(s, sbase, hioff, static_cast<std::uint32_t>(v), static_cast<std::uint32_t>(v >> 32));
-                }
-            };
-            XT qa[4], qb[4];
-            std::uint32_t pa[4], pb[4];
-            load4(qa, pa, 0);
-            for (int eb = 0; eb < E; eb += 256) {
-                load4(qb, pb, eb + 128);
-                process(qa, pa, eb);
-                if (eb + 128 >= E) break;
-                load4(qa, pa, eb + 256);
-                process(qb, pb, eb + 128);
-            }
+            int s0 = 0;
+            for (; s0 + 4 <= S; s0 += 4) step4(s0, true);
+            if (s0 < S) step4(s0, false);
             __syncwarp();
             c0 = __shfl_sync(0xffffffffu, cn, 0);
         }
+        if (L1 && __any_sync(0xffffffffu, static_cast<std::int32_t>(ovf) < 0) && lane == 0) atomicOr(a.ovf_out, 1);
         __syncthreads();
-        unsigned long long t_f0 = 0;
-        if (a.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_f0));
         // flush into the window-major exact accumulators acc[g * W + s]: consecutive
         // threads add consecutive 8-byte words (coalesced RED.64; integer adds commute, so
         // the sketch stays bit-deterministic)
-        {
-            unsigned long long* out = a.acc + static_cast<long long>(g) * W;
-            for (int s = threadIdx.x; s < W; s += NT) {
-                const unsigned long long v = (static_cast<unsigned long long>(sm[W + s]) << 32) | sm[s];
-                if (v) atomicAdd(out + s, v);
-            }
-        }
-        if (a.trace) {
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                unsigned long long t_f1;
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_f1));
-                switches += (t_f1 - t_f0) << 16;  // trace: flush ns in the high bits
-            }
+        for (int s = threadIdx.x; s < W; s += NT) {
+            const unsigned long long v =
+                L1 ? static_cast<unsigned long long>(static_cast<long long>(static_cast<std::int32_t>(sm[s] ^ kLimbBias)))
+                   : (static_cast<unsigned long long>(sm[WP + s]) << 32) | sm[s];
+            if (v) atomicAdd(gacc + s, v);
         }
         if (threadIdx.x == 0) {
             int best = -1, left = 0;
@@ -1210,57 +991,46 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
                 }
             }
             s_next_g = best;
-            ++switches;
         }
         __syncthreads();
         g = s_next_g;
     }
-    if (a.trace && threadIdx.x == 0) {
-        unsigned long long t_end;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
-        a.trace[3 * blockIdx.x] = t_start;
-        a.trace[3 * blockIdx.x + 1] = t_end;
-        a.trace[3 * blockIdx.x + 2] = switches;
+    if (!have_F) {  // (a CTA that took no window) still orders itself after the pre-pass and
+                    // derives F, so CTA 0 always publishes scale_exp / nonfinite for the finalize
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        F = cta_scale_exp(a);
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     }
 }
 
-template <bool SYM, int TB, typename XT>
+template <bool SYM, int TB, typename XT, bool L1>
 static void cls_launch2(cudaStream_t st, const BuildPlan& p, const BuildArgs& a, size_t smem) {
-    cudaFuncSetAttribute(k_build_cls<SYM, TB, XT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    pdl_launch(k_build_cls<SYM, TB, XT>, p.P, 1024, smem, st, p.pdl, a);
+    cudaFuncSetAttribute(k_build_cls<SYM, TB, XT, L1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    pdl_launch(k_build_cls<SYM, TB, XT, L1>, p.P, 1024, smem, st, p.pdl, a);
 }
+// fp64 input: two limbs (|q| < 2^50, the fp64 tolerance); fp32 input: one biased limb with
+// the rare carry (|q| < 2^22: resolution 2^-22 of max kappa|T|, against the 1e-4 fp32
+// contract), half the window bytes, so half the bucket classes and half the gathers per entry
 template <int TB>
 static void cls_launch(cudaStream_t st, const BuildPlan& p, const BuildArgs& a) {
-    const size_t smem = cls_smem_bytes(p.bmask + 1u, TB, p.n, p.sym);
+    const size_t smem = cls_smem_bytes(p.bmask + 1u, TB, p.n, p.sym, p.one_limb, p.slab_cap);
     if (p.sym) {
-        if (p.dtype == 0) cls_launch2<true, TB, double>(st, p, a, smem);
-        else cls_launch2<true, TB, float>(st, p, a, smem);
+        if (p.dtype == 0) cls_launch2<true, TB, double, false>(st, p, a, smem);
+        else if (p.one_limb) cls_launch2<true, TB, float, true>(st, p, a, smem);
+        else cls_launch2<true, TB, float, false>(st, p, a, smem);
     } else {
-        if (p.dtype == 0) cls_launch2<false, TB, double>(st, p, a, smem);
-        else cls_launch2<false, TB, float>(st, p, a, smem);
+        if (p.dtype == 0) cls_launch2<false, TB, double, false>(st, p, a, smem);
+        else if (p.one_limb) cls_launch2<false, TB, float, true>(st, p, a, smem);
+        else cls_launch2<false, TB, float, false>(st, p, a, smem);
     }
     count_launch();
 }
 
-// Threads per CTA: 1024 (32 warps, 64 registers) by default; SKC_BUILD_NT=512 trades
-// warps for registers (experiment hook).
 template <bool SYM, int RMAX>
 static void build_launch(cudaStream_t st, const BuildPlan& p, const BuildArgs& a) {
-    static const int nt = [] {
-        const char* e = std::getenv("SKC_BUILD_NT");
-        return (e && std::atoi(e) == 512) ? 512 : 1024;
-    }();
     const size_t smem = build_smem_bytes(p.slots_per_cta, RMAX, p.n);
-    if (p.flat) {
-        cudaFuncSetAttribute(k_build_flat<SYM, RMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_build_flat<SYM, RMAX><<<p.P, 1024, smem, st>>>(a);
-    } else if (nt == 512) {
-        cudaFuncSetAttribute(k_build_dyn<SYM, RMAX, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_build_dyn<SYM, RMAX, 512><<<p.P, 512, smem, st>>>(a);
-    } else {
-        cudaFuncSetAttribute(k_build_dyn<SYM, RMAX, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_build_dyn<SYM, RMAX, 1024><<<p.P, 1024, smem, st>>>(a);
-    }
+    cudaFuncSetAttribute(k_build_flat<SYM, RMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_build_flat<SYM, RMAX><<<p.P, 1024, smem, st>>>(a);
     count_launch();
 }
 
@@ -1303,11 +1073,14 @@ void launch_build_main(cudaStream_t st, const void* T, const BuildPlan& p) {
     a.xsrc = p.xsrc_mode == 1 ? T : static_cast<const void*>(p.qbuf);
     a.xmode = p.xsrc_mode;
     a.scale_out = p.scale_exp;
-    a.nonfinite_out = p.lean_sums ? p.nonfinite : nullptr;
+    a.nonfinite_out = p.xsrc_mode == 1 ? p.nonfinite : nullptr;
+    a.ovf_out = p.ovf;
+    a.sym_even_F = (p.cls_bits >= 0 && p.sym) ? 1 : 0;
     a.next_row = p.next_row;
     a.acc = p.acc;
+    a.qbits = (p.cls_bits >= 0 && p.one_limb) ? 22 : 50;
+    a.slab_cap = p.slab_cap;
 
-    a.trace = p.trace;
     if (p.cls_bits >= 0) {
         switch (p.cls_bits) {
             case 0: cls_launch<0>(st, p, a); break;
@@ -1326,6 +1099,8 @@ void launch_build_main(cudaStream_t st, const void* T, const BuildPlan& p) {
 // reports the error with the set untouched). For the symmetric set the slot index is the
 // double index into interleaved (re, im) data; the asymmetric set is real-only. The
 // accumulators and the row counters are re-zeroed here for the next build (no memsets).
+// The one-limb overflow flag lives kOvfOffset ints after the non-finite flag.
+constexpr int kOvfOffset = 2;
 __device__ __forceinline__ double pow2_neg(int F) {  // 2^-F exactly, |F| <= 1000
     return __longlong_as_double(static_cast<long long>(1023 - F) << 52);
 }
@@ -1353,7 +1128,7 @@ __global__ void k_build_finalize(unsigned long long* __restrict__ acc, long long
     const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
     asm volatile("griddepcontrol.wait;" ::: "memory");  // main pass complete (PDL launch)
     if (base < ncounters) counters[base] = 0;
-    const bool bad = *nonfinite != 0;
+    const bool bad = (nonfinite[0] | nonfinite[kOvfOffset]) != 0;
     const double sc = pow2_neg(*scale_exp);
     long long q[4];
 #pragma unroll
@@ -1388,7 +1163,7 @@ __global__ void k_build_finalize_sym_pair(unsigned long long* __restrict__ acc, 
     const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
     asm volatile("griddepcontrol.wait;" ::: "memory");  // main pass complete (PDL launch)
     if (base < ncounters) counters[base] = 0;
-    const bool bad = *nonfinite != 0;
+    const bool bad = (nonfinite[0] | nonfinite[kOvfOffset]) != 0;
     const double sc = pow2_neg(*scale_exp);
     const long long bm = (1ll << logb) - 1;
     long long q0[2], q1[2];
@@ -1423,7 +1198,7 @@ __global__ void k_build_finalize_multi(unsigned long long* __restrict__ acc, int
     const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (s < ncounters) counters[s] = 0;
     if (s >= total_slots) return;
-    const bool bad = *nonfinite != 0;
+    const bool bad = (nonfinite[0] | nonfinite[kOvfOffset]) != 0;
     double v = 0.0;
     bool any = false;
     for (int c = 0; c < K; ++c) {
@@ -1456,11 +1231,7 @@ void launch_build_finalize_multi(cudaStream_t st, const BuildPlan& p, int K, con
 void launch_build_finalize(cudaStream_t st, const BuildPlan& p) {
     const unsigned grid = cdiv(std::max<long long>((p.total_slots + 3) / 4, p.G), 256);
     const bool pdl = p.pdl && p.cls_bits >= 0;  // only the class-list main pass triggers early
-    static const bool pair_on = [] {
-        const char* e = std::getenv("SKC_FINALIZE_PAIR");  // "0": generic walk (A/B)
-        return !(e && e[0] == '0');
-    }();
-    if (pair_on && p.sym && p.cls_bits == 0) {
+    if (p.sym && p.cls_bits == 0) {
         const long long pairs = p.total_slots / 2;  // B x b complex entries
         const int logb = __builtin_ctz(p.bmask + 1u);
         const unsigned g2 = cdiv(std::max<long long>((pairs + 1) / 2, p.G), 256);

@@ -83,13 +83,14 @@ struct BuildPlan {
     // row hand-out per type (next_row counters) and migration between types
     int P, G;
     int* next_row;               // G counters
-    bool flat;                   // flat-chunk kernel or the row-walk kernel
     int cls_bits = -1;           // >= 0: class-list kernel, windows = (replicate, [parity,] bucket mod 2^cls_bits)
+    int slab_cap = 0;            // class-list kernel: 32-entry slabs per warp table
+    bool one_limb = false;       // class-list kernel: one biased 32-bit limb per slot (fp32 input)
+    int* ovf = nullptr;          // one-limb overflow flag (= nonfinite + 2)
     int xsrc_mode = 0;           // 0: pre-pass writes the fixed-point stream (contiguous-window kernels);
                                  // 1: class-list kernel reads the device-resident T (pre-pass: sums only);
                                  // 2: pre-pass writes a packed raw copy of the rows (bus-read T)
     unsigned long long* acc;     // total_slots exact fixed-point accumulators
-    unsigned long long* trace;   // optional per-CTA (start, end, switches) (SKC_BUILD_TRACE)
     long long total_slots;   // B x 2b (sym) or B x b (asym)
     int slots_per_cta;
     int R;                   // max replicates a slot range overlaps
@@ -102,7 +103,6 @@ struct BuildPlan {
     double* prepass_partials;     // prepass_blocks
     int prepass_blocks = 1024, prepass_threads = 256, prepass_warps = 8;
     bool reset_nonfinite = true;
-    bool lean_sums = false;  // device-resident sums pre-pass: k_build_sums_lean
     bool pdl = false;  // main and finalize launched programmatically dependent (single-stream build)
     int* scale_exp;               // device int
     int* nonfinite;               // device int
@@ -110,7 +110,8 @@ struct BuildPlan {
 };
 constexpr int kPrepassBlocks = 1024;
 size_t build_smem_bytes(long long slots_per_cta, int R, int n);
-size_t cls_smem_bytes(std::uint32_t b, int tbits, int n, bool sym);
+int cls_slab_cap(std::uint32_t b, int tbits, int n, bool sym, bool one_limb, size_t limit);
+size_t cls_smem_bytes(std::uint32_t b, int tbits, int n, bool sym, bool one_limb, int slab_cap);
 void launch_build_prepass(cudaStream_t st, const void* T, const BuildPlan& p);
 void launch_build_main(cudaStream_t st, const void* T, const BuildPlan& p);
 void launch_build_finalize(cudaStream_t st, const BuildPlan& p);

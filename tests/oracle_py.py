@@ -49,6 +49,9 @@ def _setup(L):
         "orc_num_threads": (C.c_int, []),
         "orc_set_num_threads": (None, [C.c_int]),
         "orc_derive_seed": (C.c_uint64, [C.c_uint64] * 4),
+        "orc_sym_accumulate_dense_slice": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int]),
+        "orc_gen_planted_slice": (C.c_int, [C.c_int, C.c_int, C.c_double, C.c_uint64, C.c_int, C.c_int, C.c_int, vp,
+                                            d_p, d_p]),
         "orc_rng_u64": (None, [C.c_uint64, C.c_int, u64_p]),
         "orc_rng_gaussian": (None, [C.c_uint64, C.c_int, d_p]),
         "orc_rng_unit_sphere": (None, [C.c_uint64, C.c_int, d_p]),
@@ -211,6 +214,16 @@ class SymSet:
     def accumulate_dense(self, T, assume_symmetric=False):
         T = f64(T)
         _chk(lib().orc_sym_accumulate_dense(self.h, dp(T), int(bool(assume_symmetric))))
+
+    def accumulate_dense_slice(self, T, i0, i1):
+        """Rows i in [i0, i1) of sketch.cpp:315-345; T holds those rows (float64 or float32)."""
+        a = np.ascontiguousarray(T)
+        if a.dtype not in (np.float64, np.float32):
+            a = a.astype(np.float64)
+        if a.size != (i1 - i0) * self.n * self.n:
+            raise ValueError("accumulate_dense_slice: T must hold (i1 - i0) * n^2 entries")
+        _chk(lib().orc_sym_accumulate_dense_slice(self.h, a.ctypes.data_as(vp), int(a.dtype == np.float32),
+                                                  int(i0), int(i1)))
 
     def add_scaled_rank1(self, u, alpha):
         _chk(lib().orc_sym_add_scaled_rank1(self.h, dp(f64(u)), float(alpha)))
@@ -396,6 +409,18 @@ def lda_whiten(m2, k):
     W, Uw, sv = np.zeros((V, k)), np.zeros((V, k)), np.zeros(k)
     _chk(lib().orc_lda_whiten(V, dp(m2), k, dp(W), dp(Uw), dp(sv)))
     return W, Uw, sv
+
+
+def gen_planted_slice(n, rank, sigma, seed, i0=0, i1=None, dtype=np.float64):
+    """BASELINE configs 0-2 planted tensor rows [i0, i1) (the device generator's noise model),
+    restated here so CPU arms never load the product library. Returns (T_slice, lambda, V)."""
+    i1 = n if i1 is None else i1
+    T = np.empty((i1 - i0, n, n), dtype=dtype)
+    lam = np.empty(rank)
+    V = np.empty((rank, n))
+    _chk(lib().orc_gen_planted_slice(n, rank, float(sigma), int(seed), int(i0), int(i1),
+                                     int(np.dtype(dtype) == np.float32), T.ctypes.data_as(vp), dp(lam), dp(V)))
+    return T, lam, np.ascontiguousarray(V.T)
 
 
 def greedy_match(rec, truth):
