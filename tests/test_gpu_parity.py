@@ -197,8 +197,9 @@ def test_device_input_ordered_after_torch_stream(gpu_ctx):
         big = torch.randn(4096, 4096, device="cuda")
         for _ in range(20):  # keep the stream busy, then produce the input on it
             big = big @ big * 1e-3
-        Td = torch.from_numpy(T).to("cuda", non_blocking=True).t().contiguous().t()  # non-contiguous -> copy kernel
-        Td = Td.contiguous().reshape(-1) + 0.0
+        # T is symmetric: the permuted copy has the same values (copy kernels on the side stream)
+        Td = torch.from_numpy(T).to("cuda", non_blocking=True).permute(2, 1, 0).contiguous()
+        Td = Td.reshape(-1) + 0.0
         s = skb().SymTensorSketchSet(n, b, B, 5, gpu_ctx)
         s.accumulate_dense(Td, assume_symmetric=True)
     assert np.array_equal(s.data(), ref.data())
@@ -295,7 +296,9 @@ def test_dense_pinned_pipelined_build(gpu_ctx, sym):
         s.accumulate_dense(pinned)
         d.accumulate_dense(torch.from_numpy(T).cuda())
     assert rel_per_replicate(s.data(), ref.data()) <= SKETCH_TOL
-    assert rel_per_replicate(s.data(), d.data()) <= 1e-13
+    # per-chunk exponents (pinned) vs the global one (device): both exact fixed point at
+    # resolutions ~2^-61 of their L1 mass, so they differ only by that rounding
+    assert rel_per_replicate(s.data(), d.data()) <= 1e-12
     bad = pinned.copy()
     bad[n - 1, n - 1, n - 1] = np.nan
     bad = torch.from_numpy(bad).pin_memory().numpy()
