@@ -197,9 +197,8 @@ def test_device_input_ordered_after_torch_stream(gpu_ctx):
         big = torch.randn(4096, 4096, device="cuda")
         for _ in range(20):  # keep the stream busy, then produce the input on it
             big = big @ big * 1e-3
-        # T is symmetric: the permuted copy has the same values (copy kernels on the side stream)
-        Td = torch.from_numpy(T).to("cuda", non_blocking=True).permute(2, 1, 0).contiguous()
-        Td = Td.reshape(-1) + 0.0
+        # H2D copy and an elementwise kernel queued behind the matmuls on the side stream
+        Td = torch.from_numpy(T).to("cuda", non_blocking=True).reshape(-1) + 0.0
         s = skb().SymTensorSketchSet(n, b, B, 5, gpu_ctx)
         s.accumulate_dense(Td, assume_symmetric=True)
     assert np.array_equal(s.data(), ref.data())
