@@ -69,7 +69,7 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
     spc = (spc + 31) / 32 * 32;
     // Dense builds take the class-list kernel when a (replicate, [parity,] bucket class)
     // window fits: the fewest bucket-class bits t <= 3 whose window + tables fit.
-    int cls_bits = -1, slab_cap = 0;
+    int cls_bits = -1;
     // (class lists pack k above the 3-term bucket sum: n <= 2^(28 - log2 b))
     int logb = 0;
     while ((1u << logb) < b) ++logb;
@@ -81,8 +81,7 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
     if (!small_asym && b <= (1u << 21) && b >= 64 &&
         static_cast<long long>(n - 1) < (1ll << (28 - logb))) {
         for (int t = 0; t <= 3; ++t)
-            if ((slab_cap = cls_slab_cap(b, t, n, sym, one_limb, static_cast<size_t>(ctx->smem_optin - 4096))) >=
-                (t < 3 ? 32 : 1)) {
+            if (cls_smem_bytes(b, t, n, sym, one_limb) <= static_cast<size_t>(ctx->smem_optin - 4096)) {
                 cls_bits = t;
                 break;
             }
@@ -136,7 +135,6 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
     if (cls_bits < 0 && sym && b > (1u << 27))
         fail(kInvalidArgument, "accumulate_dense: symmetric dense builds support b <= 2^27");
     p.cls_bits = cls_bits;
-    p.slab_cap = slab_cap;
     p.one_limb = cls_bits >= 0 && one_limb;
     // class-list builds read T in place when it is device-resident (row offsets relative to
     // a 32-row chunk fit in 32 bits for n <= 30000), else a packed raw copy of the rows

@@ -412,7 +412,6 @@ struct BuildArgs {
     int sym_even_F;                // symmetric one-limb / two-limb class-list builds: F even (see cta_scale_exp)
     int* next_row;                 // G row (or tile) counters (zero on entry; the finalize re-zeroes them)
     int qbits;                     // max |q| exponent: 50 (two limbs) or 22 (one limb, fp32 input)
-    int slab_cap;                  // class-list kernel: slabs per warp table
 
     unsigned long long* acc;       // total_slots exact accumulators (zero on entry; the finalize re-zeroes them)
 };
@@ -651,51 +650,49 @@ __global__ void __launch_bounds__(1024, 1) k_build_flat(BuildArgs a) {
 // evaluated once, in the one window it lands in (no out-of-window evaluations, no trash
 // atomics), against ~2.2 evaluations per pair for the contiguous-slot windows above.
 constexpr int kClsRows = 32;  // rows per grab
-constexpr int kSlabCapMax = 256;  // most 32-entry slabs in a warp's table
 __host__ __device__ constexpr int cls_sfx_words(int C, int n) { return (C * (n + 1) + 1) / 2; }
 
-// Window limbs (plus 32 dummy slots per plane), class list, hash words, suffix tables.
-static size_t cls_fixed_bytes(std::uint32_t b, int tbits, int n, bool sym, bool one_limb) {
+// Window limbs (plus 32 dummy slots per plane), class list, hash words, suffix tables and
+// the 32 warps' row tables (one int4 per row of a grab).
+size_t cls_smem_bytes(std::uint32_t b, int tbits, int n, bool sym, bool one_limb) {
     const int C = (sym ? 2 : 1) << tbits;
     const size_t W = static_cast<size_t>(b) >> tbits;
-    return (sizeof(std::uint32_t) * ((one_limb ? 1 : 2) * (W + 32) + 3 * (size_t)n + cls_sfx_words(C, n)) + 15) &
-           ~size_t(15);
-}
-// Slabs per warp table that fit beside the fixed part in `limit` bytes, or 0 when even
-// one row of the largest possible class (n entries) does not fit.
-int cls_slab_cap(std::uint32_t b, int tbits, int n, bool sym, bool one_limb, size_t limit) {
-    const size_t fixed = cls_fixed_bytes(b, tbits, n, sym, one_limb);
-    if (fixed >= limit) return 0;
-    long long cap = static_cast<long long>((limit - fixed) / (32 * sizeof(int4)));
-    cap = cap < kSlabCapMax ? cap : kSlabCapMax;
-    return cap < (n + 31) / 32 ? 0 : static_cast<int>(cap);
-}
-size_t cls_smem_bytes(std::uint32_t b, int tbits, int n, bool sym, bool one_limb, int slab_cap) {
-    return cls_fixed_bytes(b, tbits, n, sym, one_limb) + 32 * sizeof(int4) * static_cast<size_t>(slab_cap);
+    const size_t fixed = (sizeof(std::uint32_t) * ((one_limb ? 1 : 2) * (W + 32) + 3 * (size_t)n + cls_sfx_words(C, n)) + 15) &
+                         ~size_t(15);
+    return fixed + 32 * kClsRows * sizeof(int4);
 }
 
 // One-limb add for fp32 inputs (|q| < 2^22): the window keeps each slot's exact sum
 // mod 2^32 biased by 2^31, so the centred value v = limb ^ 2^31 starts at 0 and a pass's
 // partial sums (~sqrt(count) * |q|) stay far from the +-2^31 edge. The flush adds v
 // itself to the slot's 64-bit accumulator, so without an overflow the accumulator holds
-// the exact sum, as with two limbs; the returned old limb shows any overflow (one LOP3).
+// the exact sum, as with two limbs.
 constexpr std::uint32_t kLimbBias = 0x80000000u;
-// The centred value can only overflow after 2^(31-22) = 512 same-signed full-scale adds
-// to one slot within one window pass, so the add does not branch on it: each lane ORs the
-// overflow test into `ovf` (sign bit = some add overflowed), the window pass reports it,
-// and the host then discards the build (the finalize adds nothing) and repeats it exactly
-// with two limbs. Ordinary data never takes that path.
-__device__ __forceinline__ void add32_idx(std::uint32_t idx, std::uint32_t sbase, std::int32_t q, std::uint32_t& ovf) {
+// Overflow guard, conservative and branch-free: an add whose returned old limb has
+// |v| >= 2^30 (bits 31 and 30 of the limb equal) sets the sign bit of `ovf`. An add that
+// starts below 2^30 in magnitude ends below 2^30 + 2^22 < 2^31, so no add can overflow
+// without an earlier or the same add being flagged. The window pass reports the flag and
+// the host then discards the build (the finalize adds nothing) and repeats it exactly with
+// two limbs. Ordinary data (|v| needs ~2^8 same-signed full-scale adds to one slot) never
+// takes that path.
+__device__ __forceinline__ void add32_at(std::uint32_t addr, std::int32_t q, std::uint32_t& ovf) {
     std::uint32_t old;
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(static_cast<std::uint32_t>(q)));
+    ovf |= ~(old ^ (old << 1));
+}
+__device__ __forceinline__ void add32_idx(std::uint32_t idx, std::uint32_t sbase, std::int32_t q, std::uint32_t& ovf) {
+    add32_at(sbase + 4u * idx, q, ovf);
+}
+// Exact 64-bit add at a precomputed low-limb byte address (the high limb is hioff above).
+__device__ __forceinline__ void add64_at(std::uint32_t al, std::uint32_t hioff, std::uint32_t ql, std::uint32_t qh) {
     asm volatile(
-        "{\n\t.reg .u32 al;\n\t"
-        "mad.lo.u32 al, %1, 4, %2;\n\t"
-        "atom.shared.add.u32 %0, [al], %3;\n\t}"
-        : "=r"(old)
-        : "r"(idx), "r"(sbase), "r"(static_cast<std::uint32_t>(q)));
-    const std::uint32_t nw = old + static_cast<std::uint32_t>(q);
-    // signed overflow of the centred v + q: v and q share a sign and v's sign flips
-    ovf |= (old ^ nw) & ~(old ^ kLimbBias ^ static_cast<std::uint32_t>(q));
+        "{\n\t.reg .u32 ah, old, c;\n\t"
+        "add.u32 ah, %0, %1;\n\t"
+        "atom.shared.add.u32 old, [%0], %2;\n\t"
+        "add.cc.u32 c, old, %2;\n\t"
+        "addc.u32 c, %3, 0;\n\t"
+        "red.shared.add.u32 [ah], c;\n\t}" ::"r"(al),
+        "r"(hioff), "r"(ql), "r"(qh));
 }
 // Entries are read straight from T (device-resident: xmode 1) or from the pre-pass's packed
 // row copy (xmode 2), element type XT, and rounded to q = round(kappa * T * 2^F) by one fma
@@ -705,14 +702,13 @@ __device__ __forceinline__ void add32_idx(std::uint32_t idx, std::uint32_t sbase
 // asym); the k = j entry of a sym row, whose kappa is 3 (or 1), gets its correction
 // (-3 or -2) added once per row when the row's metadata is built.
 //
-// A warp grabs R rows of its window (R <= 32, sized so every 32-entry slab of the rows'
-// in-window runs fits the warp's slab table), builds one int4 per slab (list position of
-// its lane 0, source offset of the row, row pair word, active lanes) and then walks the
-// slab table four slabs per step: each slab is one row's 32 consecutive class-list
-// entries (lane l takes entry l), so the row data come from one broadcast LDS.128 and no
-// lane keeps a row cursor; all four slabs' list words and gathers are issued before
-// their adds. (A row-at-a-time walk with the row data broadcast by shuffles measured
-// 3.54 ms at config 2 against 2.72 for the table.)
+// A warp grabs 32 rows of its window and walks their in-window runs as one flat entry
+// range: a warp-level scan of the run lengths gives each row's end, lane e takes entries
+// e, e+32, ... across row boundaries with a row cursor over one int4 of row metadata per row
+// (end entry, list position - entry index, source offset, row word), reads the list word,
+// gathers the entry from the row and adds it. Four 32-entry blocks are fetched before
+// their adds, ping-pong (measured against a per-row 32-entry slab table: config 1
+// 0.449 vs 0.501 ms, config 2 2.60 vs 2.69 ms, bit-identical; microbench/walk_ab.sh).
 template <bool SYM, int TB, typename XT, bool L1>
 __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
     constexpr int NT = 1024, C = (SYM ? 2 : 1) << TB, NPL = L1 ? 1 : 2;  // limb planes in the window
@@ -730,11 +726,10 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
     std::uint32_t* pw = reinterpret_cast<std::uint32_t*>(lst + n);  // sym n: h | e << 30; asym 2n: modes 1, 2
     unsigned short* sfx = reinterpret_cast<unsigned short*>(pw + 2 * n);  // C x (n + 1)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // per-warp slab table, one int4 per slab: (list position of lane 0, source element index
-    // of (i, j, 0) relative to the grab, c_ij | [i == j] << 23 | e_ij << 30, active lanes)
-    int4* slab = reinterpret_cast<int4*>(
+    // per-warp row table of the current grab: one int4 per row
+    int4* meta = reinterpret_cast<int4*>(
                      sm + ((static_cast<size_t>(NPL * WP + 3 * n + cls_sfx_words(C, n)) + 3) & ~static_cast<size_t>(3))) +
-                 warp * a.slab_cap;
+                 warp * kClsRows;
     // F comes from the pre-pass partials: read after griddepcontrol.wait, which the first
     // window's prologue (zeroing, hash words, class lists) runs ahead of (PDL launch)
     int F = 0;
@@ -864,10 +859,7 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
             asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         }
 
-        // rows per grab: every slab of the grabbed rows' runs must fit the warp's table
-        int maxsl = 1;
-        for (int cc = 0; cc < C; ++cc) maxsl = max(maxsl, (s_cend[cc] - (cc ? s_cend[cc - 1] : 0) + 31) >> 5);
-        const int R = max(1, min(kClsRows, a.slab_cap / maxsl));
+        constexpr int R = kClsRows;
         int c0 = 0;
         if (lane == 0) c0 = atomicAdd(a.next_row + g, R);
         c0 = __shfl_sync(0xffffffffu, c0, 0);
@@ -914,60 +906,105 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
                     }
                 }
             }
-            const int nsl = (cnt + 31) >> 5;
-            int incl = nsl;
+            // flat walk: the grab's in-window runs are one contiguous entry range; lane e
+            // takes entries e, e+32, ... across row boundaries with a row cursor over one
+            // int4 per row (end entry, list position - entry index, source offset, row word)
+            int incl = cnt;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const int v = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += v;
             }
             const long long off0 = __shfl_sync(0xffffffffu, off, 0);
-            const int S = __shfl_sync(0xffffffffu, incl, 31);
-            for (int q = 0, sb = incl - nsl; q < nsl; ++q)
-                slab[sb + q] = make_int4(pos0 + 32 * q, static_cast<int>(off - off0), static_cast<int>(pwd), cnt - 32 * q);
+            const int E = __shfl_sync(0xffffffffu, incl, 31);
+            // .y: byte address of the row's list run, minus 4 x its first entry index
+            if (lane < nr)
+                meta[lane] = make_int4(incl, static_cast<int>(lst_s + 4u * static_cast<std::uint32_t>(pos0 - (incl - cnt))),
+                                       static_cast<int>(off - off0), static_cast<int>(pwd));
             __syncwarp();
             const XT* qch = xsrc + off0;
-            asm volatile("mov.b64 %0, %0;" : "+l"(qch));  // one IMAD.WIDE per gather address
-            // four slabs per step, branch-free: inactive lanes load a valid entry of their
-            // slab's row (list index clamped) and add 0 into their private dummy slot
-            // W + lane; the last partial step re-reads the last slab with no active lanes
-            auto step4 = [&](int s0, bool full) {
-                XT xv[4];
-                std::uint32_t pv[4], sv[4];
-                bool act[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int4 d = slab[full ? s0 + u : min(s0 + u, S - 1)];  // broadcast
-                    act[u] = lane < (full || s0 + u < S ? d.w : 0);
-                    const std::uint32_t lw =
-                        lds_u32(lst_s + 4u * static_cast<std::uint32_t>(d.x + min(lane, d.w - 1)));
-                    xv[u] = __ldg(qch + static_cast<std::uint32_t>(d.y + static_cast<int>((lw >> KS) & kmask)));
-                    pv[u] = static_cast<std::uint32_t>(d.z) + (lw & wmask);
-                    sv[u] = act[u] ? (pv[u] & bmask) >> TB : static_cast<std::uint32_t>(W + lane);
+            asm volatile("mov.b64 %0, %0;" : "+l"(qch));
+            int t = 0;
+            int4 cur = meta[0];
+            auto fetch = [&](XT& x, std::uint32_t& pv, int e) {
+                if (e >= cur.x) {  // crossed into a later row of the grab
+                    cur = meta[++t];
+                    while (e >= cur.x) cur = meta[++t];
                 }
+                const std::uint32_t lw = lds_u32(static_cast<std::uint32_t>(cur.y) + 4u * static_cast<std::uint32_t>(e));
+                x = __ldg(qch + static_cast<std::uint32_t>(cur.z + static_cast<int>((lw >> KS) & kmask)));
+                pv = static_cast<std::uint32_t>(cur.w) + (lw & wmask);
+            };
+            // lanes past the grab's end add 0 into their private dummy slot W + lane
+            auto load4 = [&](XT (&x)[4], std::uint32_t (&pv)[4], bool (&ac)[4], int eb) {
+                if (eb + 128 <= E) {
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    // kappa * 2^F with the complex4 sign (bit 31 of p) in its sign bit
-                    if (L1) {
-                        // fp32 scale: the sign (bit 31) and the i = j halving (bit 23, the low
-                        // exponent bit) in one LOP3
-                        const std::uint32_t hi = sc_hi0 ^ (pv[u] & (SYM ? 0x80800000u : 0x80000000u));
-                        const std::int32_t q = to_fixed32(static_cast<float>(xv[u]), hi);
-                        add32_idx(sv[u], sbase, act[u] ? q : 0, ovf);
-                    } else {
-                        // fp64 scale high word: exponent low bit at 20 (F even: halving = XOR)
-                        const std::uint32_t hi = (SYM ? sc_hi0 ^ ((pv[u] >> 3) & (1u << 20)) : sc_hi0) ^
-                                                 (pv[u] & 0x80000000u);
-                        const long long v = act[u] ? to_fixed(static_cast<double>(xv[u]), hi) : 0ll;
-                        add64_idx(sv[u], sbase, hioff, static_cast<std::uint32_t>(v),
-                                  static_cast<std::uint32_t>(static_cast<unsigned long long>(v) >> 32));
+                    for (int u = 0; u < 4; ++u) {
+                        fetch(x[u], pv[u], eb + lane + 32 * u);
+                        ac[u] = true;
+                    }
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int e = eb + lane + 32 * u;
+                        x[u] = XT(0);
+                        pv[u] = 0u;
+                        ac[u] = e < E;
+                        if (ac[u]) fetch(x[u], pv[u], e);
                     }
                 }
             };
-            int s0 = 0;
-            for (; s0 + 4 <= S; s0 += 4) step4(s0, true);
-            if (s0 < S) step4(s0, false);
-            __syncwarp();
+            // byte address of the entry's low limb: window slot (p & bmask) >> TB
+            auto slot_addr = [&](std::uint32_t pv) -> std::uint32_t {
+                const std::uint32_t x = pv & (bmask & ~tmask);
+                if constexpr (TB <= 2) return sbase + (x << (2 - TB));
+                else return sbase + (x >> (TB - 2));
+            };
+            auto add_one = [&](XT x, std::uint32_t pv, std::uint32_t addr, bool act) {
+                // kappa * 2^F with the complex4 sign (bit 31 of p) in its sign bit
+                if (L1) {
+                    // fp32 scale: the sign (bit 31) and the i = j halving (bit 23, the low
+                    // exponent bit) in one LOP3
+                    const std::uint32_t hi = sc_hi0 ^ (pv & (SYM ? 0x80800000u : 0x80000000u));
+                    const std::int32_t q = to_fixed32(static_cast<float>(x), hi);
+                    add32_at(addr, act ? q : 0, ovf);
+                } else {
+                    // fp64 scale high word: exponent low bit at 20 (F even: halving = XOR)
+                    const std::uint32_t hi = (SYM ? sc_hi0 ^ ((pv >> 3) & (1u << 20)) : sc_hi0) ^ (pv & 0x80000000u);
+                    const long long v = act ? to_fixed(static_cast<double>(x), hi) : 0ll;
+                    add64_at(addr, hioff, static_cast<std::uint32_t>(v),
+                             static_cast<std::uint32_t>(static_cast<unsigned long long>(v) >> 32));
+                }
+            };
+            // full 128-entry blocks: no bound checks
+            auto process_full = [&](const XT (&x)[4], const std::uint32_t (&pv)[4]) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) add_one(x[u], pv[u], slot_addr(pv[u]), true);
+            };
+            // the grab's last block: lanes past the end add 0 into their private dummy slot
+            auto process_tail = [&](const XT (&x)[4], const std::uint32_t (&pv)[4], const bool (&ac)[4], int eb) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (eb + 32 * u >= E) break;  // warp-uniform
+                    add_one(x[u], pv[u], ac[u] ? slot_addr(pv[u]) : sbase + 4u * static_cast<std::uint32_t>(W + lane), ac[u]);
+                }
+            };
+            auto process = [&](const XT (&x)[4], const std::uint32_t (&pv)[4], const bool (&ac)[4], int eb) {
+                if (eb + 128 <= E) process_full(x, pv);
+                else process_tail(x, pv, ac, eb);
+            };
+            XT xa[4], xb[4];
+            std::uint32_t pa[4], pb[4];
+            bool aa[4], ab[4];
+            load4(xa, pa, aa, 0);
+            for (int eb = 0; eb < E; eb += 256) {
+                load4(xb, pb, ab, eb + 128);
+                process(xa, pa, aa, eb);
+                if (eb + 128 >= E) break;
+                load4(xa, pa, aa, eb + 256);
+                process(xb, pb, ab, eb + 128);
+            }
+            __syncwarp();  // the row table is rewritten by the next grab
             c0 = __shfl_sync(0xffffffffu, cn, 0);
         }
         if (L1 && __any_sync(0xffffffffu, static_cast<std::int32_t>(ovf) < 0) && lane == 0) atomicOr(a.ovf_out, 1);
@@ -1013,7 +1050,7 @@ static void cls_launch2(cudaStream_t st, const BuildPlan& p, const BuildArgs& a,
 // contract), half the window bytes, so half the bucket classes and half the gathers per entry
 template <int TB>
 static void cls_launch(cudaStream_t st, const BuildPlan& p, const BuildArgs& a) {
-    const size_t smem = cls_smem_bytes(p.bmask + 1u, TB, p.n, p.sym, p.one_limb, p.slab_cap);
+    const size_t smem = cls_smem_bytes(p.bmask + 1u, TB, p.n, p.sym, p.one_limb);
     if (p.sym) {
         if (p.dtype == 0) cls_launch2<true, TB, double, false>(st, p, a, smem);
         else if (p.one_limb) cls_launch2<true, TB, float, true>(st, p, a, smem);
@@ -1079,7 +1116,6 @@ void launch_build_main(cudaStream_t st, const void* T, const BuildPlan& p) {
     a.next_row = p.next_row;
     a.acc = p.acc;
     a.qbits = (p.cls_bits >= 0 && p.one_limb) ? 22 : 50;
-    a.slab_cap = p.slab_cap;
 
     if (p.cls_bits >= 0) {
         switch (p.cls_bits) {

@@ -84,7 +84,6 @@ struct BuildPlan {
     int P, G;
     int* next_row;               // G counters
     int cls_bits = -1;           // >= 0: class-list kernel, windows = (replicate, [parity,] bucket mod 2^cls_bits)
-    int slab_cap = 0;            // class-list kernel: 32-entry slabs per warp table
     bool one_limb = false;       // class-list kernel: one biased 32-bit limb per slot (fp32 input)
     int* ovf = nullptr;          // one-limb overflow flag (= nonfinite + 2)
     int xsrc_mode = 0;           // 0: pre-pass writes the fixed-point stream (contiguous-window kernels);
@@ -110,8 +109,7 @@ struct BuildPlan {
 };
 constexpr int kPrepassBlocks = 1024;
 size_t build_smem_bytes(long long slots_per_cta, int R, int n);
-int cls_slab_cap(std::uint32_t b, int tbits, int n, bool sym, bool one_limb, size_t limit);
-size_t cls_smem_bytes(std::uint32_t b, int tbits, int n, bool sym, bool one_limb, int slab_cap);
+size_t cls_smem_bytes(std::uint32_t b, int tbits, int n, bool sym, bool one_limb);
 void launch_build_prepass(cudaStream_t st, const void* T, const BuildPlan& p);
 void launch_build_main(cudaStream_t st, const void* T, const BuildPlan& p);
 void launch_build_finalize(cudaStream_t st, const BuildPlan& p);
