@@ -244,6 +244,43 @@ int skc_sym_rtpm(skc_sym_set* s, int k, int L, int T_iters, uint64_t seed, doubl
 int skc_sym_rtpm_restarts(skc_sym_set* s, const double* U0_host, int L, int T_iters, double tol,
                           double* finals_out, double* values_out);
 
+/* ---- multi-GPU: NCCL over NVLink / NVSwitch (B200 extension) ----------------
+ * Replaces the reference's in-process OpenMP loops over replicates (sketch.cpp:325,
+ * contraction.cpp:145) and its serial restart loop (decompose.cpp:92-112) with one
+ * replica of a set per GPU and partitions that need one exchange each:
+ *   dense build: equal-work i-slices of the sorted triples; pre-pass partials
+ *     all-gathered (one global exponent), exact int64 accumulators all-reduced, so the
+ *     sketch is bit-identical at any rank count;
+ *   moment: sample blocks, per-residue partial transforms all-reduced;
+ *   LDA sketch_whitened_m3: document blocks, corpus globals then data all-reduced;
+ *   RTPM: restart blocks of ceil(L/R), selection values all-gathered, the first maximum
+ *     over tau on every rank, the winner's vector broadcast, identical deflation.
+ * A communicator spans R ranks, one context (GPU) each. Ranks live in one process
+ * (skc_group_create: ncclCommInitAll over a device list, contexts returned in rank
+ * order) or in one process each (rank 0 makes an id with skc_nccl_unique_id, every rank
+ * passes it to skc_context_comm_init). The *_group calls are collective: every process
+ * calls them with its local replicas (sets on its contexts, rank order); every replica
+ * holds the same sketch before and after. Per-set input pointers may all be the same
+ * host array; SKC_DEVICE inputs are per-set device pointers (each holding the whole
+ * tensor / sample matrix; a rank reads only its block). */
+int skc_nccl_unique_id(char* out /* 128 bytes */);
+int skc_context_comm_init(skc_context* ctx, int nranks, int rank, const char* id /* 128 bytes */);
+int skc_group_create(const int* devices, int ndev, skc_context** ctxs_out /* ndev */);
+int skc_context_comm_info(const skc_context* ctx, int* nranks, int* rank);
+/* host plumbing (no device): the i-slice bounds[nranks + 1] of a dense build and the
+ * restart block [t0, t1) of a rank */
+int skc_group_slices(int n, int sym, int nranks, int* bounds);
+int skc_group_restart_chunk(int L, int nranks, int rank, int* t0, int* t1);
+int skc_sym_accumulate_dense_group(skc_sym_set* const* sets, int nsets, const void* const* T, int dtype, int location,
+                                   int assume_symmetric);
+int skc_sym_accumulate_moment_group(skc_sym_set* const* sets, int nsets, const double* const* X, const double* const* w,
+                                    long long N, int location);
+int skc_sym_rtpm_group(skc_sym_set* const* sets, int nsets, int k, int L, int T_iters, uint64_t seed, double tol,
+                       const double* inits, double* lambda, double* V, int* best_tau);
+int skc_sym_sketch_whitened_m3_group(skc_sym_set* const* sets, int nsets, int V, long long D, const long long* doc_ptr,
+                                     const int* word, const int* count, const double* W, double alpha0,
+                                     long long* used, long long* skipped);
+
 /* ---- asymmetric sketch set: AsymTensorSketchSet (sketch.hpp:27-82) --------- */
 int skc_asym_create(skc_context* ctx, int n, uint32_t b, int B, uint64_t master_seed, skc_asym_set** out);
 /* hcoef B*3*2, xcoef B*3*6 (AsymTensorSketchSet::load, sketch.cpp:276-296) */

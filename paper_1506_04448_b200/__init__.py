@@ -139,11 +139,26 @@ def device_count() -> int:
 class Context:
     """One CUDA device + stream (the C-ABI skc_context)."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, *, _handle=None):
+        if _handle is not None:
+            self._h = _handle
+            self.device = device
+            return
         h = C.c_void_p()
         check(lib.skc_context_create(device, C.byref(h)))
         self._h = h
         self.device = device
+
+    def comm_init(self, nranks: int, rank: int, uid: bytes) -> None:
+        """Join an NCCL communicator of nranks processes (one GPU each) with the id from
+        nccl_unique_id() on rank 0 (skc_context_comm_init)."""
+        check(lib.skc_context_comm_init(self._h, int(nranks), int(rank), bytes(uid)))
+
+    def comm_info(self):
+        """(nranks, rank) of this context's communicator ((1, 0) without one)."""
+        a, b = C.c_int(), C.c_int()
+        check(lib.skc_context_comm_info(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     @property
     def handle(self):
@@ -950,3 +965,100 @@ def gen_planted_tensor_device(ctx: Context, n: int, rank: int, sigma: float, see
                                             SKC_F64 if np.dtype(dtype) == np.float64 else SKC_F32,
                                             C.c_void_p(out_ptr), _dp(lam), _dp(V)))
     return lam, np.ascontiguousarray(V.T)
+
+
+# ---------------------------------------------------------------- multi-GPU (NCCL)
+def nccl_unique_id() -> bytes:
+    """A fresh NCCL communicator id (128 bytes) for Context.comm_init on every rank."""
+    buf = C.create_string_buffer(128)
+    check(lib.skc_nccl_unique_id(buf))
+    return buf.raw
+
+
+def group_slices(n: int, world: int, sym: bool = True) -> list[tuple[int, int]]:
+    """Equal-work i-slices of a dense build across `world` ranks (skc_group_slices)."""
+    b = (C.c_int * (world + 1))()
+    check(lib.skc_group_slices(int(n), int(bool(sym)), int(world), b))
+    return [(b[r], b[r + 1]) for r in range(world)]
+
+
+def group_restart_chunk(L: int, world: int, rank: int) -> tuple[int, int]:
+    """Restarts [t0, t1) of a rank in a multi-GPU RTPM (skc_group_restart_chunk)."""
+    a, b = C.c_int(), C.c_int()
+    check(lib.skc_group_restart_chunk(int(L), int(world), int(rank), C.byref(a), C.byref(b)))
+    return a.value, b.value
+
+
+def group_contexts(devices) -> list[Context]:
+    """One context per GPU in `devices`, joined by one NCCL communicator (ncclCommInitAll,
+    skc_group_create), in rank order."""
+    devices = [int(d) for d in devices]
+    arr = (C.c_int * len(devices))(*devices)
+    hs = (C.c_void_p * len(devices))()
+    check(lib.skc_group_create(arr, len(devices), hs))
+    return [Context(d, _handle=C.c_void_p(hs[i])) for i, d in enumerate(devices)]
+
+
+class SymReplicas:
+    """Replicas of one SymTensorSketchSet on the GPUs of an NCCL communicator: this
+    process's local contexts (all of them after group_contexts(); one per process after
+    Context.comm_init). Every operation is collective over all ranks and leaves every
+    replica holding the same sketch (include/sketchcp_b200.h, multi-GPU section)."""
+
+    def __init__(self, n: int, b: int, B: int, master_seed: int, contexts):
+        self.contexts = list(contexts)
+        self.sets = [SymTensorSketchSet(n, b, B, master_seed, c) for c in self.contexts]
+
+    def _handles(self):
+        return (C.c_void_p * len(self.sets))(*[s.handle.value for s in self.sets])
+
+    def __len__(self):
+        return len(self.sets)
+
+    def accumulate_dense(self, T, assume_symmetric: bool = True) -> None:
+        """sketch.cpp:315-345 over equal-work i-slices, exact accumulators all-reduced. T:
+        one numpy array for all replicas, or one CUDA tensor per replica (on its device)."""
+        Ts = T if isinstance(T, (list, tuple)) else [T] * len(self.sets)
+        args = [_tensor_arg(t, s.n(), s.ctx) for t, s in zip(Ts, self.sets)]
+        ptrs = (C.c_void_p * len(args))(*[a[0].value if isinstance(a[0], C.c_void_p) else a[0] for a in args])
+        dt, loc = args[0][1], args[0][2]
+        check(lib.skc_sym_accumulate_dense_group(self._handles(), len(self.sets), ptrs, dt, loc,
+                                                 int(bool(assume_symmetric))))
+
+    def accumulate_moment(self, X, w=None) -> None:
+        """data += sum_i w_i sketch(x_i^(x)3) over sample blocks; X (N, n) host numpy."""
+        n = self.sets[0].n()
+        X = _f64(X)
+        if X.ndim != 2 or X.shape[1] != n:
+            raise ValueError("accumulate_moment: dimension mismatch")
+        wa = None if w is None else _f64(w, (X.shape[0],))
+        xs = (C.c_void_p * len(self.sets))(*([X.ctypes.data] * len(self.sets)))
+        ws = None if wa is None else (C.c_void_p * len(self.sets))(*([wa.ctypes.data] * len(self.sets)))
+        check(lib.skc_sym_accumulate_moment_group(self._handles(), len(self.sets), xs, ws, X.shape[0], SKC_HOST))
+
+    def rtpm(self, cfg: "PowerConfig", inits=None) -> "CpDecomposition":
+        """decompose.cpp:83-115 with the L restarts split across ranks; the replicas are left
+        deflated."""
+        n = self.sets[0].n()
+        lam = np.empty(cfg.k)
+        V = np.empty((cfg.k, n))
+        bt = (C.c_int * cfg.k)()
+        ip = None
+        if inits is not None:
+            inits = _f64(inits, (cfg.k, cfg.L, n))
+            ip = _dp(inits)
+        check(lib.skc_sym_rtpm_group(self._handles(), len(self.sets), int(cfg.k), int(cfg.L), int(cfg.T_iters),
+                                     int(cfg.seed), float(cfg.tol), ip, _dp(lam), _dp(V), bt))
+        return CpDecomposition.symmetric_of(lam, np.ascontiguousarray(V.T), np.array(bt[: cfg.k]))
+
+    def sketch_whitened_m3(self, V: int, doc_ptr, word, count, W, alpha0: float):
+        """lda.cpp:145-226 over document blocks; returns (used, skipped) of the whole corpus."""
+        _keep, (D, dpp, wdp, ctp) = _corpus_args(doc_ptr, word, count)
+        Wm = _f64(W)
+        used, skipped = C.c_longlong(), C.c_longlong()
+        check(lib.skc_sym_sketch_whitened_m3_group(self._handles(), len(self.sets), int(V), D, dpp, wdp, ctp, _dp(Wm),
+                                                   float(alpha0), C.byref(used), C.byref(skipped)))
+        return used.value, skipped.value
+
+    def data(self, r: int = 0) -> np.ndarray:
+        return self.sets[r].data()

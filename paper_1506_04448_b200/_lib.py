@@ -21,6 +21,23 @@ if not LIB_PATH.exists():
         "(this package has no CPU fallback)"
     )
 
+def _preload_nccl() -> None:
+    """The library links libnccl.so.2 (multi-GPU paths). When torch's bundled NCCL is
+    installed, load that copy first, so the process holds one NCCL (the soname resolves to
+    the loaded copy) whichever of torch and this library is imported first."""
+    import sys
+
+    for base in sys.path:
+        cand = pathlib.Path(base or ".") / "nvidia" / "nccl" / "lib" / "libnccl.so.2"
+        if cand.exists():
+            try:
+                C.CDLL(str(cand), mode=C.RTLD_GLOBAL)
+            except OSError:
+                pass
+            return
+
+
+_preload_nccl()
 lib = C.CDLL(str(LIB_PATH))
 
 c_int, c_u32, c_u64, c_ll, c_double, c_size = C.c_int, C.c_uint32, C.c_uint64, C.c_longlong, C.c_double, C.c_size_t
@@ -98,6 +115,18 @@ SIGNATURES = {
     "skc_sym_cached_transform": (c_int, [p_void, c_int, p_double]),
     "skc_sym_rtpm": (c_int, [p_void, c_int, c_int, c_int, c_u64, c_double, p_double, p_double, p_double, p_int]),
     "skc_sym_rtpm_restarts": (c_int, [p_void, p_double, c_int, c_int, c_double, p_double, p_double]),
+    "skc_nccl_unique_id": (c_int, [C.c_char_p]),
+    "skc_context_comm_init": (c_int, [p_void, c_int, c_int, C.c_char_p]),
+    "skc_group_create": (c_int, [p_int, c_int, pp_void]),
+    "skc_context_comm_info": (c_int, [p_void, p_int, p_int]),
+    "skc_group_slices": (c_int, [c_int, c_int, c_int, p_int]),
+    "skc_group_restart_chunk": (c_int, [c_int, c_int, c_int, p_int, p_int]),
+    "skc_sym_accumulate_dense_group": (c_int, [pp_void, c_int, pp_void, c_int, c_int, c_int]),
+    "skc_sym_accumulate_moment_group": (c_int, [pp_void, c_int, pp_void, pp_void, c_ll, c_int]),
+    "skc_sym_rtpm_group": (c_int, [pp_void, c_int, c_int, c_int, c_int, c_u64, c_double, p_double, p_double,
+                                   p_double, p_int]),
+    "skc_sym_sketch_whitened_m3_group": (c_int, [pp_void, c_int, c_int, c_ll, p_ll, p_int, p_int, p_double, c_double,
+                                                 p_ll, p_ll]),
     "skc_asym_create": (c_int, [p_void, c_int, c_u32, c_int, c_u64, pp_void]),
     "skc_asym_create_from_coefficients": (
         c_int,

@@ -67,6 +67,7 @@ int skc_context_destroy(skc_context* ctx) {
         cudaStreamSynchronize(ctx->stream);
         if (ctx->stream2) cudaStreamSynchronize(ctx->stream2);
         if (ctx->cublas) cublasDestroy(ctx->cublas);
+        if (ctx->comm) ncclCommDestroy(ctx->comm);
         if (ctx->host_ints) cudaFreeHost(ctx->host_ints);
         for (auto& r : ctx->prof) {
             cudaEventDestroy(r.a);

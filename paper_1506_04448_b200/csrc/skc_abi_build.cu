@@ -46,11 +46,31 @@ const void* stage_tensor(skc_context* ctx, const void* T, int n, int dtype, int 
     return dst;
 }
 
-void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool sym, int i0, int i1, int B,
-                     std::uint32_t b, const std::uint32_t* packed, double2* data, bool zero_copy, bool two_limb) {
-    if (i0 >= i1) return;
-    skc_context::RowTab& rt = ctx->rowtab(n, i0, i1, sym);
-    if (rt.nrows == 0) return;
+// The exact accumulators and row counters are zero between builds: the finalize re-zeroes
+// what the build used. A fresh allocation (or a build that failed before its finalize was
+// enqueued) is cleared here.
+void ensure_build_scratch_clean(skc_context* ctx) {
+    if (ctx->build_scratch_clean && ctx->build_acc.p == ctx->build_acc_clean_p &&
+        ctx->build_ints.p == ctx->build_ints_clean_p && ctx->build_acc.count == ctx->build_acc_clean_n &&
+        ctx->build_ints.count == ctx->build_ints_clean_n)
+        return;
+    CK(cudaMemsetAsync(ctx->build_acc.p, 0, ctx->build_acc.count * sizeof(unsigned long long), ctx->stream));
+    CK(cudaMemsetAsync(ctx->build_ints.p, 0, ctx->build_ints.count * sizeof(int), ctx->stream));
+    ctx->build_acc_clean_p = ctx->build_acc.p;
+    ctx->build_ints_clean_p = ctx->build_ints.p;
+    ctx->build_acc_clean_n = ctx->build_acc.count;
+    ctx->build_ints_clean_n = ctx->build_ints.count;
+    ctx->build_scratch_clean = true;
+}
+
+// Scratch and launch plan of one dense build of rows [i0, i1) on ctx (no launches). The
+// plan depends only on the shape (n, b, B, dtype, sym, limbs), so replicas of a set on
+// several devices get the same accumulator layout, and an empty row range still yields a
+// valid plan (nrows 0).
+skc_context::RowTab& prepare_dense_build(skc_context* ctx, int n, int dtype, bool sym, int i0, int i1, int B,
+                                         std::uint32_t b, const std::uint32_t* packed, double2* data, bool zero_copy,
+                                         bool two_limb, BuildPlan& p) {
+    skc_context::RowTab& rt = ctx->rowtab(n, i0, std::max(i0, i1), sym);
     const long long total_slots = static_cast<long long>(B) * (sym ? 2ll * b : static_cast<long long>(b));
     // slots per CTA limited by shared memory (limbs + per-replicate hash tables)
     int G = 1;
@@ -98,30 +118,14 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
     require(R <= 16, "accumulate_dense: slot range spans too many replicates");
     const long long tot = rt.cum.back();
     const int P = std::max(1, ctx->sms);  // one persistent CTA per SM, rows handed out dynamically
-    // The exact accumulators and row counters are zero between builds: the finalize
-    // re-zeroes what the build used. A fresh allocation (or a build that failed before its
-    // finalize was enqueued) is cleared here.
-    auto ensure_clean = [&] {
-        if (ctx->build_scratch_clean && ctx->build_acc.p == ctx->build_acc_clean_p &&
-            ctx->build_ints.p == ctx->build_ints_clean_p && ctx->build_acc.count == ctx->build_acc_clean_n &&
-            ctx->build_ints.count == ctx->build_ints_clean_n)
-            return;
-        CK(cudaMemsetAsync(ctx->build_acc.p, 0, ctx->build_acc.count * sizeof(unsigned long long), ctx->stream));
-        CK(cudaMemsetAsync(ctx->build_ints.p, 0, ctx->build_ints.count * sizeof(int), ctx->stream));
-        ctx->build_acc_clean_p = ctx->build_acc.p;
-        ctx->build_ints_clean_p = ctx->build_ints.p;
-        ctx->build_acc_clean_n = ctx->build_acc.count;
-        ctx->build_ints_clean_n = ctx->build_ints.count;
-        ctx->build_scratch_clean = true;
-    };
     ctx->build_ints.alloc(static_cast<size_t>(G));
     ctx->build_acc.alloc(static_cast<size_t>(total_slots));
     ctx->qbuf.alloc(static_cast<size_t>(std::max<long long>(1, tot)));
-    ctx->rowF.alloc(static_cast<size_t>(rt.nrows));
+    ctx->rowF.alloc(static_cast<size_t>(std::max(1, rt.nrows)));
     ctx->prepass.alloc(2 * kPrepassBlocks);  // L1 sums, then maxima
     ctx->ints.alloc(16);
 
-    BuildPlan p;
+    p = BuildPlan();
     p.n = n;
     p.sym = sym;
     p.dtype = dtype;
@@ -157,6 +161,20 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
         ctx->build_ovf_clean = true;
     }
     p.data_as_double = reinterpret_cast<double*>(data);
+    if (p.xsrc_mode == 1)  // device-resident class-list build: sums-only pre-pass, one wave of 5 blocks/SM
+        p.prepass_blocks = std::min(kPrepassBlocks, std::max(1, ctx->sms) * 5);
+    return rt;
+}
+
+void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool sym, int i0, int i1, int B,
+                     std::uint32_t b, const std::uint32_t* packed, double2* data, bool zero_copy, bool two_limb) {
+    if (i0 >= i1) return;
+    BuildPlan p;
+    skc_context::RowTab& rt = prepare_dense_build(ctx, n, dtype, sym, i0, i1, B, b, packed, data, zero_copy, two_limb, p);
+    if (rt.nrows == 0) return;
+    const long long total_slots = p.total_slots;
+    const long long tot = rt.cum.back();
+    const int G = p.G;
     // Zero-copy host input: the quantize pass is bus-bound, so the rows are cut into K
     // chunks and chunk c+1 is read over PCIe (a few SMs, wide blocks) while the main pass
     // of chunk c runs on the other SMs (second stream). Each chunk keeps its own exponent
@@ -174,7 +192,7 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
         ctx->build_ints.alloc(static_cast<size_t>(K) * G);
         ctx->ints.alloc(16);
         ctx->prepass.alloc(2 * static_cast<size_t>(K) * qsms);
-        ensure_clean();
+        ensure_build_scratch_clean(ctx);
         ctx->build_scratch_clean = false;
         if (!ctx->stream2) CK(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
         if (!ctx->ev_q[0])
@@ -219,11 +237,9 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
         }
         ctx->check_launch();
     } else {
-        ensure_clean();
+        ensure_build_scratch_clean(ctx);
         ctx->build_scratch_clean = false;
         p.pdl = true;
-        if (p.xsrc_mode == 1)  // device-resident class-list build: sums-only pre-pass, one wave of 5 blocks/SM
-            p.prepass_blocks = std::min(kPrepassBlocks, std::max(1, ctx->sms) * 5);
         {
             SKC_PROF(ctx, "build_prepass");
             launch_build_prepass(ctx->stream, Tdev, p);

@@ -3,6 +3,7 @@
 // include/sketchcp_b200.h. Not a public header.
 #pragma once
 #include <cublas_v2.h>
+#include <nccl.h>
 #include <cuda_runtime.h>
 #include <omp.h>
 
@@ -120,6 +121,11 @@ using namespace skcabi;
 // ============================ context ============================================
 struct skc_context {
     int device = 0;
+    // NCCL communicator over the replicas of a set on several GPUs (skc_group_create or
+    // skc_context_comm_init); nranks 1 without one
+    ncclComm_t comm = nullptr;
+    int rank = 0, nranks = 1;
+    DevBuf<double> gathered;  // all-gathered pre-pass partials / restart values
     cudaStream_t stream = nullptr;
     cudaStream_t stream2 = nullptr;  // pipelined zero-copy builds: main pass of chunk c
     cudaEvent_t ev_q[5] = {};        // chunk c quantized / all chunks done
@@ -419,6 +425,22 @@ const void* stage_tensor(skc_context* ctx, const void* T, int n, int dtype, int 
                          bool need_full, size_t* h2d_bytes, bool* zero_copy = nullptr);
 void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool sym, int i0, int i1, int B,
                      std::uint32_t b, const std::uint32_t* packed, double2* data, bool zero_copy, bool two_limb = false);
+void ensure_build_scratch_clean(skc_context* ctx);
+skc_context::RowTab& prepare_dense_build(skc_context* ctx, int n, int dtype, bool sym, int i0, int i1, int B,
+                                         std::uint32_t b, const std::uint32_t* packed, double2* data, bool zero_copy,
+                                         bool two_limb, BuildPlan& p);
+// skc_abi_sym.cu
+void check_symmetric(skc_context* ctx, const void* Td, int dtype, int n);
+void sym_moment_partial(skc_sym_set* s, const double* Xd, const double* wd, long long Nsamp);
+void sym_moment_combine(skc_sym_set* s, double alpha);
+void rtpm_restarts_device(skc_sym_set* s, int L, int T_iters, double tol);
+void check_degenerate(skc_context* ctx, int L);
+// skc_abi_lda.cu
+void upload_corpus(skc_context* ctx, int V, long long D, const long long* doc_ptr, const int* word, const int* count,
+                   CorpusDev& c, const std::string& who = "lda", bool check_counts = true);
+void sketch_whitened_m3_dev(skc_sym_set* s, CorpusDev& c, const double* W, double alpha0, long long* used_out,
+                            long long* skipped_out, long long global_used = -1, const double* global_m1 = nullptr,
+                            bool add_q_cubed = true);
 // skc_abi.cu
 void spectrum_to_host(skc_context* ctx, const double2* spec, int m, std::uint32_t b, int N, int logN, int S,
                       double* out);

@@ -6,7 +6,7 @@
 namespace skcabi {
 
 void upload_corpus(skc_context* ctx, int V, long long D, const long long* doc_ptr, const int* word, const int* count,
-                   CorpusDev& c, const std::string& who = "lda", bool check_counts = true) {
+                   CorpusDev& c, const std::string& who, bool check_counts) {
     require(V >= 1 && D >= 0, who + ": invalid corpus dimensions");
     check_vec(doc_ptr, (who + ": doc_ptr").c_str());
     const long long nnz = doc_ptr[D];
@@ -268,8 +268,8 @@ void whiten_randomized(skc_context* ctx, int V, int k, int oversample, int iters
 // sketch is linear in the per-document terms, so summing the shards' data reproduces the
 // full sketch_whitened_m3.
 void sketch_whitened_m3_dev(skc_sym_set* s, CorpusDev& c, const double* W, double alpha0, long long* used_out,
-                            long long* skipped_out, long long global_used = -1, const double* global_m1 = nullptr,
-                            bool add_q_cubed = true) {
+                            long long* skipped_out, long long global_used, const double* global_m1,
+                            bool add_q_cubed) {
     check_vec(W, "sketch_whitened_m3: W");
     const int k = s->n;  // lda.cpp:149-151: set dimension must equal the whitening rank
     require(k <= 2048, "sketch_whitened_m3: whitening rank above 2048 is not supported on the device path");

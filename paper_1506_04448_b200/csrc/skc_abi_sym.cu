@@ -171,6 +171,34 @@ int skc_sym_coefficients(const skc_sym_set* s, uint64_t* hcoef, uint64_t* scoef)
     });
 }
 
+}  // extern "C"
+namespace skcabi {
+// first_asymmetric_triple (tensor.cpp:32-45) over a device-visible n^3 tensor; throws
+// the reference's invalid_argument message at the first failure.
+void check_symmetric(skc_context* ctx, const void* Td, int dtype, int n) {
+    ctx->asym_key.alloc(1);
+    unsigned long long init = ~0ull;
+    CK(cudaMemcpyAsync(ctx->asym_key.p, &init, 8, cudaMemcpyHostToDevice, ctx->stream));
+    long long tot = static_cast<long long>(n) * n * n;
+    k_first_asym<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, ctx->stream>>>(Td, dtype, n, 1e-9, ctx->asym_key.p);
+    count_launch();
+    ctx->check_launch();
+    unsigned long long key = 0;
+    CK(cudaMemcpyAsync(&key, ctx->asym_key.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    if (key != ~0ull) {
+        const long long idx = static_cast<long long>(key >> 3);
+        const int p = static_cast<int>(key & 7);
+        const int i = static_cast<int>(idx / ((long long)n * n)), j = static_cast<int>((idx / n) % n),
+                  k = static_cast<int>(idx % n);
+        const int perms[5][3] = {{i, k, j}, {j, i, k}, {j, k, i}, {k, i, j}, {k, j, i}};
+        fail(kInvalidArgument, "accumulate_dense: input tensor is not symmetric at (" + std::to_string(perms[p][0] + 1) +
+                                   "," + std::to_string(perms[p][1] + 1) + "," + std::to_string(perms[p][2] + 1) + ")");
+    }
+}
+}  // namespace skcabi
+extern "C" {
+
 int skc_sym_accumulate_dense(skc_sym_set* s, const void* T, int dtype, int location, int assume_symmetric, int i0,
                              int i1) {
     return guard([&] {
@@ -184,30 +212,7 @@ int skc_sym_accumulate_dense(skc_sym_set* s, const void* T, int dtype, int locat
         ctx->use();
         bool zc = false;
         const void* Td = stage_tensor(ctx, T, s->n, dtype, location, true, i0, i1, !assume_symmetric, nullptr, &zc);
-        if (!assume_symmetric) {
-            ctx->asym_key.alloc(1);
-            unsigned long long init = ~0ull;
-            CK(cudaMemcpyAsync(ctx->asym_key.p, &init, 8, cudaMemcpyHostToDevice, ctx->stream));
-            long long tot = static_cast<long long>(s->n) * s->n * s->n;
-            k_first_asym<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, ctx->stream>>>(Td, dtype, s->n, 1e-9,
-                                                                                           ctx->asym_key.p);
-            count_launch();
-            ctx->check_launch();
-            unsigned long long key = 0;
-            CK(cudaMemcpyAsync(&key, ctx->asym_key.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
-            ctx->sync();
-            if (key != ~0ull) {
-                const long long idx = static_cast<long long>(key >> 3);
-                const int p = static_cast<int>(key & 7);
-                const int n = s->n;
-                const int i = static_cast<int>(idx / ((long long)n * n)), j = static_cast<int>((idx / n) % n),
-                          k = static_cast<int>(idx % n);
-                const int perms[5][3] = {{i, k, j}, {j, i, k}, {j, k, i}, {k, i, j}, {k, j, i}};
-                fail(kInvalidArgument, "accumulate_dense: input tensor is not symmetric at (" +
-                                           std::to_string(perms[p][0] + 1) + "," + std::to_string(perms[p][1] + 1) +
-                                           "," + std::to_string(perms[p][2] + 1) + ")");
-            }
-        }
+        if (!assume_symmetric) check_symmetric(ctx, Td, dtype, s->n);
         s->version++;  // sketch.cpp:324
         {
             SKC_PROF(ctx, "build_total");
@@ -217,13 +222,16 @@ int skc_sym_accumulate_dense(skc_sym_set* s, const void* T, int dtype, int locat
     });
 }
 
+}  // extern "C"
+namespace skcabi {
 // Frequency-domain rank-1 / moment accumulation shared by add_scaled_rank1,
 // accumulate_moment and RTPM deflation. X: device N x n.
-static void sym_moment_device(skc_sym_set* s, const double* Xd, const double* wd, double alpha, long long Nsamp) {
+// Frequency-domain accumulation of sum_s w_s F(CS(x_s))^3 over Nsamp samples, reduced over
+// chunks and inverted per residue into ctx->tmp (B x b, linear in the samples).
+void sym_moment_partial(skc_sym_set* s, const double* Xd, const double* wd, long long Nsamp) {
     skc_context* ctx = s->ctx;
     const int per_rep = s->B * s->S;
-    int chunks = wave_chunks(ctx->sms, per_rep, Nsamp);
-    chunks = static_cast<int>(std::min<long long>(Nsamp, env_int("SKC_MOMENT_CHUNKS", chunks, 1, 1 << 16)));  // A/B hook
+    const int chunks = wave_chunks(ctx->sms, per_rep, Nsamp);
     ctx->freq_acc.alloc(static_cast<size_t>(chunks) * per_rep * s->N * 2);
     ctx->tmp.alloc(static_cast<size_t>(s->B) * s->b);
     SymView v = s->view();
@@ -238,12 +246,23 @@ static void sym_moment_device(skc_sym_set* s, const double* Xd, const double* wd
                                    v.twl, ctx->tmp.p);
     }
     ctx->check_launch();
+}
+// data += alpha x (residue combination of ctx->tmp)
+void sym_moment_combine(skc_sym_set* s, double alpha) {
+    skc_context* ctx = s->ctx;
+    SymView v = s->view();
     {
         SKC_PROF(ctx, "combine");
         launch_combine_residues(ctx->stream, ctx->tmp.p, s->B, s->S, s->N, s->b, v.tw, alpha, -1, false, s->data.p);
     }
     ctx->check_launch();
 }
+static void sym_moment_device(skc_sym_set* s, const double* Xd, const double* wd, double alpha, long long Nsamp) {
+    sym_moment_partial(s, Xd, wd, Nsamp);
+    sym_moment_combine(s, alpha);
+}
+}  // namespace skcabi
+extern "C" {
 
 int skc_sym_add_scaled_rank1(skc_sym_set* s, const double* u_host, double alpha) {
     return guard([&] {
@@ -479,10 +498,12 @@ int skc_sym_cached_transform(skc_sym_set* s, int m, double* out_host) {
     });
 }
 
+}  // extern "C"
+namespace skcabi {
 // ---- RTPM ----
 // Runs T power steps on L restarts resident at ctx->U (device) and the median vvv of
 // the finals into ctx->values. Degenerate flags accumulate in ctx->flags.
-static void rtpm_restarts_device(skc_sym_set* s, int L, int T_iters, double tol) {
+void rtpm_restarts_device(skc_sym_set* s, int L, int T_iters, double tol) {
     skc_context* ctx = s->ctx;
     s->ensure_fresh();
     ctx->flags.alloc(static_cast<size_t>(L));
@@ -505,14 +526,15 @@ static void rtpm_restarts_device(skc_sym_set* s, int L, int T_iters, double tol)
     launch_sym_vvv_finish(ctx->stream, ctx->part.p, L, s->B, s->S, s->b, ctx->values.p);
     ctx->check_launch();
 }
-
-static void check_degenerate(skc_context* ctx, int L) {
+void check_degenerate(skc_context* ctx, int L) {
     std::vector<int> f(L);
     CK(cudaMemcpyAsync(f.data(), ctx->flags.p, sizeof(int) * L, cudaMemcpyDeviceToHost, ctx->stream));
     ctx->sync();
     for (int x : f)
         if (x) fail(kDegenerate, "power update produced a vanishing iterate");  // decompose.cpp:37-38
 }
+}  // namespace skcabi
+extern "C" {
 
 int skc_sym_rtpm(skc_sym_set* s, int k, int L, int T_iters, uint64_t seed, double tol, const double* inits,
                  double* lambda, double* V, int* best_tau) {

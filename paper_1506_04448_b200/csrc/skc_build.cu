@@ -402,8 +402,8 @@ struct BuildArgs {
     const short* rowF;
     const long long* qbuf;
     const std::uint32_t* packed;
-    const double* partials;        // pre-pass partials: np L1 sums, then np maxima of kappa|T|
-    int np;
+    const double* partials;        // pre-pass partials: nseg x [np L1 sums, np maxima of kappa|T|]
+    int np, nseg;                  // nseg > 1: all-gathered partials of nseg ranks
     const void* xsrc;              // class-list kernel: T itself (xmode 1) or its packed row copy (xmode 2)
     int xmode;
     int* scale_out;                // global exponent F, written by CTA 0 for the finalize
@@ -425,9 +425,11 @@ __device__ int cta_scale_exp(const BuildArgs& a) {
     __shared__ int sF;
     if (threadIdx.x < 32) {
         double acc = 0.0, mx = 0.0;
-        for (int x = threadIdx.x; x < a.np; x += 32) {
-            acc += a.partials[x];
-            mx = fmax(mx, a.partials[a.np + x]);
+        for (int x = threadIdx.x; x < a.np * a.nseg; x += 32) {
+            const int sg = x / a.np, id = x - sg * a.np;
+            const double* seg = a.partials + 2ll * sg * a.np;
+            acc += seg[id];
+            mx = fmax(mx, seg[a.np + id]);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -1107,6 +1109,7 @@ void launch_build_main(cudaStream_t st, const void* T, const BuildPlan& p) {
     a.packed = p.packed;
     a.partials = p.prepass_partials;
     a.np = p.prepass_blocks;
+    a.nseg = p.nseg;
     a.xsrc = p.xsrc_mode == 1 ? T : static_cast<const void*>(p.qbuf);
     a.xmode = p.xsrc_mode;
     a.scale_out = p.scale_exp;

@@ -99,7 +99,8 @@ struct BuildPlan {
     const long long* rowoff;      // packed-stream offset of each row
     long long* qbuf;              // packed fixed-point stream (quantize pass)
     short* rowF;                  // per-row exponent of qbuf
-    double* prepass_partials;     // prepass_blocks
+    double* prepass_partials;     // nseg segments of [prepass_blocks L1 sums, prepass_blocks maxima]
+    int nseg = 1;                 // > 1: all-gathered partials of nseg ranks (multi-GPU build)
     int prepass_blocks = 1024, prepass_threads = 256, prepass_warps = 8;
     bool reset_nonfinite = true;
     bool pdl = false;  // main and finalize launched programmatically dependent (single-stream build)

@@ -156,3 +156,28 @@ def test_lda_heldout_likelihood_matches_restatement():
         tot_ll += float(cs @ np.log(p)) / m
     assert abs(ll - tot_ll / used) <= 1e-10 * abs(tot_ll / used)
     assert fl == floored
+
+
+def test_group_slices_and_restart_chunks():
+    """Host plumbing of the multi-GPU C-ABI (no device): equal-work i-slices cover [0, n)
+    in order and agree with distributed.equal_work_slices; restart blocks of
+    ceil(L / R) partition [0, L) in tau order."""
+    import paper_1506_04448_b200 as skb
+    from paper_1506_04448_b200.distributed import equal_work_slices
+
+    for n in (1, 5, 100, 400, 1000):
+        for world in (1, 2, 3, 4, 8):
+            sl = skb.group_slices(n, world)
+            assert sl[0][0] == 0 and sl[-1][1] == n
+            assert all(a[1] == b[0] and a[0] <= a[1] for a, b in zip(sl, sl[1:]))
+            assert sl == [tuple(x) for x in equal_work_slices(n, world)]
+            if n >= 100:
+                work = [sum((n - i) * (n - i + 1) // 2 for i in range(a, b)) for a, b in sl]
+                assert max(work) - min(work) <= (n * (n + 1) // 2) * 2  # within ~one row pair of slices
+    for L in (1, 7, 50, 100):
+        for world in (1, 2, 3, 8, 13):
+            ch = [skb.group_restart_chunk(L, world, r) for r in range(world)]
+            blk = -(-L // world)
+            assert ch[0][0] == 0 and ch[-1][1] == L
+            for r, (a, b) in enumerate(ch):
+                assert a == min(L, r * blk) and b == min(L, (r + 1) * blk)
