@@ -312,7 +312,8 @@ def config_dict(world):
             "seed": CFG["seed"], "input_dtype": "f32",
             "l2": "input (4 GB tensor, 669 MB of sorted triples) larger than L2; L2 also flushed "
                   "(256 MiB write) before every timed step",
-            "parallelism": f"i-slices x{world} + NCCL all-reduce" if world > 1 else "single GPU"}
+            "parallelism": f"i-slices x{world}, exact int64 accumulators all-reduced in-library over NCCL"
+            if world > 1 else "single GPU"}
 
 
 # ---------------------------------------------------------------- product arm
@@ -341,23 +342,23 @@ def run_b200(args):
     i0, i1 = equal_work_slices(n, world)[rank]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     sset = skb.SymTensorSketchSet(n, b, B, CFG["seed"], ctx)
-    dptr, dbytes = sset.data_device()
-
-    class _CAI:  # zero-copy torch view of the set's device data for the collective
-        __cuda_array_interface__ = {"shape": (dbytes // 8,), "typestr": "<f8", "data": (dptr, False), "version": 3}
-
-    data_view = torch.as_tensor(_CAI(), device=dev)
+    reps = None
+    if world > 1 or args.group:
+        # in-library NCCL (include/sketchcp_b200.h multi-GPU section): each rank builds its
+        # equal-work i-slice and the exact int64 accumulators are all-reduced inside the call
+        uid = [skb.nccl_unique_id() if rank == 0 else None]
+        if dist is not None:
+            dist.broadcast_object_list(uid, src=0)
+        ctx.comm_init(world, rank, uid[0])
+        reps = skb.SymReplicas(n, b, B, CFG["seed"], [ctx])
+        sset = reps.sets[0]
     out_host = torch.empty((B, b), dtype=torch.complex128).pin_memory().numpy()
 
     def step(T, host=False):
-        if world > 1 and rank != 0:
-            with torch.cuda.stream(ext):
-                data_view.zero_()  # prior sketch counted once by the all-reduce
-        sset.accumulate_dense(T, assume_symmetric=True, i0=i0, i1=i1)
-        if world > 1:
-            with torch.cuda.stream(ext):
-                dist.all_reduce(data_view)
-            sset.bump_version()
+        if reps is not None:
+            reps.accumulate_dense(T if host else [T], assume_symmetric=True)
+        else:
+            sset.accumulate_dense(T, assume_symmetric=True)
         if host:
             return sset.data(out=out_host)
         return None
@@ -570,6 +571,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--group", action="store_true", help="take the multi-GPU (NCCL group) build path even at N=1")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

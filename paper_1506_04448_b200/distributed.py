@@ -254,8 +254,9 @@ def lda_shard_globals(V: int, doc_ptr, word, count, group=None):
     used3 = float(np.sum(tot >= 3))
     buf = torch.from_numpy(np.concatenate([m1, [used1, used3]]))
     if dist.is_initialized() and dist.get_world_size(group) > 1:
+        buf = buf.to(_backend_device(group))  # an NCCL group reduces device tensors only
         dist.all_reduce(buf, group=group)
-    g = buf.numpy()
+    g = buf.cpu().numpy()
     if g[V] <= 0:
         raise ValueError("compute_m1: no nonempty documents")
     return int(round(g[V + 1])), g[:V] / g[V], int(used1), int(used3)
@@ -278,5 +279,34 @@ def sharded_sketch_whitened_m3(sset, V: int, doc_ptr, word, count, W, alpha0: fl
 
     stats = torch.tensor([used, skipped], dtype=torch.int64)
     if world > 1:
+        stats = stats.to(_backend_device(group))
         dist.all_reduce(stats, group=group)
     return int(stats[0]), int(stats[1])
+
+
+def _backend_device(group=None):
+    """Where collective buffers must live for the group's backend (cuda for NCCL)."""
+    import torch
+    import torch.distributed as dist
+
+    if dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def process_group_replicas(n: int, b: int, B: int, master_seed: int, ctx, group=None):
+    """SymReplicas over the ranks of a torch.distributed group, one GPU each: rank 0 makes
+    the NCCL id in the library, torch.distributed only carries it. The returned replicas'
+    collective calls (dense build, moment, LDA, RTPM) run the in-library NCCL paths of
+    include/sketchcp_b200.h (exact accumulator all-reduce, device-side M1, split restarts)."""
+    import torch.distributed as dist
+
+    from . import SymReplicas, nccl_unique_id
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    uid = [nccl_unique_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(uid, src=0, group=group)
+    ctx.comm_init(world, rank, uid[0])
+    return SymReplicas(n, b, B, master_seed, [ctx])
