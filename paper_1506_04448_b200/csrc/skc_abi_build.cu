@@ -179,7 +179,10 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
     // chunks and chunk c+1 is read over PCIe (a few SMs, wide blocks) while the main pass
     // of chunk c runs on the other SMs (second stream). Each chunk keeps its own exponent
     // and exact accumulator; the finalize sums the K chunk sketches in order.
-    const int K = (zero_copy && rt.nrows >= 4096 && sizeof(double) * 32 * (size_t)n <= (size_t)ctx->smem_optin - 1024)
+    // (the raw-copy pre-pass of class-list builds stages nothing in shared memory; the
+    // fixed-point pre-pass of the contiguous-window kernels stages 32 rows)
+    const int K = (zero_copy && rt.nrows >= 4096 &&
+                   (p.xsrc_mode == 2 || sizeof(double) * 32 * (size_t)n <= (size_t)ctx->smem_optin - 1024))
                       ? 4
                       : 1;
     if (K > 1) {

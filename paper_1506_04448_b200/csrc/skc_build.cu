@@ -99,18 +99,29 @@ __global__ void __launch_bounds__(NTQ) k_build_quantize(const TT* __restrict__ T
     double blk = 0.0, bmax = 0.0;
     bool bad = false;
     TT* xraw = reinterpret_cast<TT*>(qbuf);  // kRaw output
-    // 16-byte path: the first 128-pair block of the warp's next row is loaded before the
+    // 16-byte path: the first 128-vector block of the warp's next row is loaded before the
     // current row's reduction and stores, so each warp keeps a row's reads in flight.
-    const bool v16 = sizeof(TT) == 8 && vec16;
+    // EPV elements per 16-byte vector (2 fp64, 4 fp32).
+    constexpr int EPV = 16 / static_cast<int>(sizeof(TT));
+    const bool v16 = vec16;
     auto row_geom = [&](int r, const double2*& tp, int& npair, int& off) {
         const std::uint32_t ijr = rowtab[r];
         const int ir = static_cast<int>(ijr >> 16), jr = static_cast<int>(ijr & 0xFFFFu);
         const int k0r = SYM ? jr : 0;
         const size_t e0 = ((size_t)ir * n + jr) * n + k0r;
-        const size_t ea = e0 & ~(size_t)1;
-        npair = static_cast<int>((e0 + (n - k0r) - ea + 1) >> 1);
-        tp = reinterpret_cast<const double2*>(T) + (ea >> 1);
+        const size_t ea = e0 & ~static_cast<size_t>(EPV - 1);
+        npair = static_cast<int>((e0 + (n - k0r) - ea + EPV - 1) / EPV);
+        tp = reinterpret_cast<const double2*>(T + ea);
         off = static_cast<int>(e0 - ea);
+    };
+    // element h of a 16-byte vector
+    auto elem = [](const double2& v, int h) -> double {
+        if constexpr (sizeof(TT) == 8) {
+            return h ? v.y : v.x;
+        } else {
+            const unsigned long long w = static_cast<unsigned long long>(__double_as_longlong((h >> 1) ? v.y : v.x));
+            return static_cast<double>(__int_as_float(static_cast<int>((h & 1) ? (w >> 32) : (w & 0xFFFFFFFFull))));
+        }
     };
     auto load_first = [&](int r, double2 (&v)[4]) {
         const double2* tp;
@@ -133,9 +144,9 @@ __global__ void __launch_bounds__(NTQ) k_build_quantize(const TT* __restrict__ T
         if (v16) {
             // 16-byte loads from a 16-byte aligned base covering the row segment: T may be
             // pinned host memory read in place over PCIe, where wider requests carry less
-            // header overhead per byte. 4 pair-loads in flight per lane.
+            // header overhead per byte. 4 vector loads in flight per lane.
             const double2* tp;
-            int npair, off;  // off 0 or 1: leading element to skip
+            int npair, off;  // off < EPV: leading elements to skip
             row_geom(row, tp, npair, off);
             double2 v[4];
 #pragma unroll
@@ -148,12 +159,12 @@ __global__ void __launch_bounds__(NTQ) k_build_quantize(const TT* __restrict__ T
                 }
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const int q = 2 * (pb + 32 * u) - off;  // row-relative index of v[u].x
+                    const int q = EPV * (pb + 32 * u) - off;  // row-relative index of element 0 of v[u]
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
+                    for (int h = 0; h < EPV; ++h) {
                         const int kk = q + h;
                         if (kk >= 0 && kk < n - k0) {
-                            const double x = h ? v[u].y : v[u].x;
+                            const double x = elem(v[u], h);
                             const int k = k0 + kk;
                             const double kv = ((SYM && k == j) ? kdiag : koff) * x;
                             if (MODE == kQuant) st[kk] = kv;

@@ -928,3 +928,22 @@ def test_sketch_save_load_round_trip(gpu_ctx, tmp_path):  # SPEC.md:307 bit-exac
     trunc.write_bytes(p.read_bytes()[:200])
     with pytest.raises(skb().FormatError, match="truncated"):
         skb().SymTensorSketchSet.load(trunc, gpu_ctx)
+
+
+@pytest.mark.parametrize("n", [140, 257])
+def test_dense_pinned_pipelined_build_fp32(gpu_ctx, n):
+    """fp32 pinned input: the chunked zero-copy pipeline with 16-byte bus reads of four
+    fp32 entries (row segments at any alignment), one-limb windows and per-chunk
+    exponents; against the fp64 oracle of the same entries and the device-resident build."""
+    import torch
+
+    T = sym_tensor(n, 32).astype(np.float32)
+    pinned = torch.from_numpy(T.copy()).pin_memory().numpy()
+    ref = O.SymSet(n, 4096, 5, 6)
+    ref.accumulate_dense(T.astype(np.float64), True)
+    s = skb().SymTensorSketchSet(n, 4096, 5, 6, gpu_ctx)
+    d = skb().SymTensorSketchSet(n, 4096, 5, 6, gpu_ctx)
+    s.accumulate_dense(pinned, assume_symmetric=True)
+    d.accumulate_dense(torch.from_numpy(T).cuda(), assume_symmetric=True)
+    assert rel_per_replicate(s.data(), ref.data()) <= 1e-6
+    assert rel_per_replicate(s.data(), d.data()) <= 1e-6
