@@ -189,15 +189,7 @@ void whiten_randomized(skc_context* ctx, int V, int k, int oversample, int iters
     if (oversample < 0) oversample = std::max(16, k / 4);
     if (iters < 0) iters = 12;
     const int p = std::min(V, (k + oversample + 31) / 32 * 32);
-    static const bool trace = std::getenv("SKC_WHITEN_TRACE") != nullptr;
-    auto t_last = std::chrono::steady_clock::now();
-    auto tick = [&](const char* what) {
-        if (!trace) return;
-        ctx->sync();
-        const auto now = std::chrono::steady_clock::now();
-        std::fprintf(stderr, "whiten %-12s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(now - t_last).count());
-        t_last = now;
-    };
+    auto tick = [](const char*) {};  // (phase marks of the whitening pipeline)
     Rng rng(derive_seed(seed, seed_tag::kWhitenProbe));  // host stream: MGS completion only
     DevBuf<double> Q, Y;
     Q.alloc(static_cast<size_t>(V) * p);

@@ -459,7 +459,10 @@ int skc_sym_ivv(skc_sym_set* s, const double* U_host, int L, double* out_host) {
         ctx->U.upload(U_host, static_cast<size_t>(L) * s->n, ctx->stream);
         sym_contract_batch(s, ctx->U.p, L, 0);
         ctx->values.alloc(static_cast<size_t>(L) * s->n);
-        launch_median_rows(ctx->stream, ctx->part.p, L, s->B, s->S, s->n, ctx->values.p, nullptr, 0.0, nullptr);
+        {
+            SKC_PROF(ctx, "median");
+            launch_median_rows(ctx->stream, ctx->part.p, L, s->B, s->S, s->n, ctx->values.p, nullptr, 0.0, nullptr);
+        }
         ctx->check_launch();
         CK(cudaMemcpyAsync(out_host, ctx->values.p, static_cast<size_t>(L) * s->n * 8, cudaMemcpyDeviceToHost,
                            ctx->stream));

@@ -668,34 +668,11 @@ __global__ void __launch_bounds__(NT, MINB)
     k_sym_contract_half(SymView v, const double* __restrict__ U, int L, int mode, double* __restrict__ out) {
     sym_contract_half_body<LOGN, NT>(v, U, L, mode, out);
 }
-// 192 threads x 3 CTAs per SM with a 112-register cap (launch bounds alone pick 96 and spill)
-template <int LOGN>
-__global__ void __maxnreg__(112)
-    k_sym_contract_half_r112(SymView v, const double* __restrict__ U, int L, int mode, double* __restrict__ out) {
-    sym_contract_half_body<LOGN, 192>(v, U, L, mode, out);
-}
-
-// Variant selection (A/B measured on B200, see profiles/): SKC_CONTRACT_VARIANT =
-//   "16s" radix-16 + scratch scatter (2 CTAs/SM), "16d" radix-16 + direct scatter,
-//   "8d" radix-8 + direct scatter (3 CTAs/SM), "h256"/"h192"/"h112" half-length f2/z2
-//   kernel at 256 threads x 2 CTAs, 192 x 3 (default), 192 x 3 with a 112-register cap.
-//   config-1 step (L=100): 16s 1.05 ms, h256 0.94, h192 0.886, h112 0.97 (profiles/r01).
-static int env_int_k(const char* name, int dflt, int lo, int hi) {
-    const char* e = std::getenv(name);
-    if (!e) return dflt;
-    const int v = std::atoi(e);
-    return v < lo ? lo : (v > hi ? hi : v);
-}
-static int contract_variant() {
-    static int v = [] {
-        const char* e = std::getenv("SKC_CONTRACT_VARIANT");
-        if (!e) return 4;
-        std::string s(e);
-        return s == "16s" ? 0 : s == "16d" ? 1 : s == "8d" ? 2 : s == "h256" ? 3 : s == "h192" ? 4 : s == "h112" ? 5 : 4;
-    }();
-    return v;
-}
-
+// Contraction kernels (measured on B200, profiles/r01): the half-length f2/z2 kernel at
+// 192 threads x 3 CTAs per SM is the default (config-1 step 0.886 ms against 1.05 for the
+// full-length radix-16 kernel with scratch scatter, 0.94 for 256 x 2 CTAs, 0.97 for a
+// 112-register cap). The full-length kernel (scratch or direct scatter) covers the shapes
+// the half-length one does not: n above the shared-memory scatter limit, local N < 4.
 template <int LG, int VAR, int LR, int MINB>
 static void sym_contract_launch(cudaStream_t st, const SymView& v, const double* U, int L, int mode, double* out,
                                 unsigned grid, size_t smem) {
@@ -710,36 +687,19 @@ static void sym_contract_half_launch(cudaStream_t st, const SymView& v, const do
     k_sym_contract_half<LG, NT, MINB><<<grid, NT, smem, st>>>(v, U, L, mode, out);
 }
 
-template <int LG>
-static void sym_contract_half_dispatch(cudaStream_t st, const SymView& v, const double* U, int L, int mode, double* out,
-                                       unsigned grid, size_t smem, int var) {
-    if (var == 3) {
-        sym_contract_half_launch<LG, 256, 2>(st, v, U, L, mode, out, grid, smem);
-    } else if (var == 4) {
-        sym_contract_half_launch<LG, 192, 3>(st, v, U, L, mode, out, grid, smem);
-    } else {
-        cudaFuncSetAttribute(k_sym_contract_half_r112<LG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_sym_contract_half_r112<LG><<<grid, 192, smem, st>>>(v, U, L, mode, out);
-    }
-}
 
 void launch_sym_contract(cudaStream_t st, const SymView& v, const double* U, int L, int mode, double* out) {
     const bool scr_ok = v.n <= kScatterMax;
-    int var = contract_variant();
-    if (var >= 3 && (!scr_ok || v.logN < 2)) var = scr_ok ? 0 : 1;
-    if (var >= 3) {
-        // restarts per CTA (SKC_CONTRACT_LPB, A/B hook): at config 1, 3..13 restarts per CTA
-        // measured 0.730..0.758 ms per step, with no wave-quantisation effect; 4 is kept
-        static const int force = env_int_k("SKC_CONTRACT_LPB", 0, 0, 64);
-        const int best = 4;
+    if (scr_ok && v.logN >= 2) {
+        // 4 restarts per CTA (config 1: 3..13 per CTA measured 0.730..0.758 ms per step)
         SymView vv = v;
-        vv.lpb = force > 0 ? force : best;
+        vv.lpb = 4;
         const int NH = v.N / 2;
         const size_t smem = sizeof(double2) * (padded_len(v.N) + (NH + NH / 16 + 1)) +
                             (sizeof(double2) + 2 * sizeof(std::uint32_t)) * 2 * (size_t)v.n +
                             sizeof(double) * ((size_t)v.n + 1);
         const unsigned grid = (unsigned)((long long)((L + vv.lpb - 1) / vv.lpb) * v.B * v.S);
-#define LH_(LG) sym_contract_half_dispatch<LG>(st, vv, U, L, mode, out, grid, smem, var)
+#define LH_(LG) sym_contract_half_launch<LG, 192, 3>(st, vv, U, L, mode, out, grid, smem)
         switch (v.logN) {
             case 2: LH_(2); break;
             case 3: LH_(3); break;
@@ -760,16 +720,14 @@ void launch_sym_contract(cudaStream_t st, const SymView& v, const double* U, int
         return;
     }
     const size_t smem = sizeof(double2) * 2 * padded_len(v.N) +
-                        (var == 0 ? (sizeof(double2) + sizeof(std::uint32_t)) * 2 * (size_t)v.n : 0);
+                        (scr_ok ? (sizeof(double2) + sizeof(std::uint32_t)) * 2 * (size_t)v.n : 0);
     const unsigned grid = (unsigned)((long long)((L + kLPB - 1) / kLPB) * v.B * v.S);
 #define L_(LG)                                                                                         \
     {                                                                                                  \
-        if (var == 0)                                                                                  \
+        if (scr_ok)                                                                                    \
             sym_contract_launch<LG, 1, 4, 2>(st, v, U, L, mode, out, grid, smem);                      \
-        else if (var == 1)                                                                             \
-            sym_contract_launch<LG, 2, 4, 2>(st, v, U, L, mode, out, grid, smem);                      \
         else                                                                                           \
-            sym_contract_launch<LG, 2, 3, 3>(st, v, U, L, mode, out, grid, smem);                      \
+            sym_contract_launch<LG, 2, 4, 2>(st, v, U, L, mode, out, grid, smem);                      \
     }
     SKC_LOGN_SWITCH(v.logN, L_)
 #undef L_
@@ -799,45 +757,6 @@ __device__ __forceinline__ double median_of(const double* est, int B) {
 }
 
 // part: L x B x S x n -> med: L x n medians over B of the residue sums (fixed order).
-// One thread per (l, i), grid over all L*n; BT > 0 keeps the B estimates in registers.
-template <int BT>
-__global__ void __launch_bounds__(256) k_median_cols(const double* __restrict__ part, int L, int B, int S, int n,
-                                                      double* __restrict__ med) {
-    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (t >= (long long)L * n) return;
-    const int l = static_cast<int>(t / n), i = static_cast<int>(t - (long long)l * n);
-    constexpr int CAP = BT > 0 ? BT : kMaxB;
-    double est[CAP];
-    const int Bn = BT > 0 ? BT : B;
-#pragma unroll
-    for (int m = 0; m < CAP; ++m) {
-        if (m < Bn) {
-            const double* p = part + (((size_t)l * Bn + m) * S) * n + i;
-            double s = p[0];
-            for (int r = 1; r < S; ++r) s += p[(size_t)r * n];
-            est[m] = s;
-        }
-    }
-    // rank selection, ties by index: the (B/2-1)-th and (B/2)-th order statistics
-    const int hiR = Bn / 2, loR = Bn / 2 - 1;
-    double hi = 0.0, lo = 0.0;
-#pragma unroll
-    for (int a = 0; a < CAP; ++a) {
-        if (a >= Bn) break;
-        const double x = est[a];
-        int rank = 0;
-#pragma unroll
-        for (int c = 0; c < CAP; ++c) {
-            if (c >= Bn) break;
-            const double y = est[c];
-            rank += (y < x) || (y == x && c < a);
-        }
-        if (rank == hiR) hi = x;
-        if (rank == loR) lo = x;
-    }
-    med[t] = (Bn & 1) ? hi : 0.5 * (lo + hi);
-}
-
 // Tiled form: a block takes 32 consecutive columns i of one restart l. Its 256 threads
 // first sum the S residue partials of every (column, replicate) pair (coalesced over i,
 // same order as k_median_cols), then rank every pair within its column (ties by index),
@@ -907,27 +826,12 @@ __global__ void __launch_bounds__(256) k_normalize_rows(const double* __restrict
 void launch_median_rows(cudaStream_t st, const double* part, int L, int B, int S, int n, double* out, double* Unext,
                         double tol, int* flags, double* scratch) {
     double* med = out ? out : scratch;
-    const long long tot = (long long)L * n;
-    static const bool cols = [] {
-        const char* e = std::getenv("SKC_MEDIAN_COLS");  // "1": one thread per column (A/B)
-        return e && std::atoi(e) == 1;
-    }();
-    if (cols) {
-        const unsigned grid = cdiv(tot, 256);
-        switch (B) {
-            case 10: k_median_cols<10><<<grid, 256, 0, st>>>(part, L, B, S, n, med); break;
-            case 20: k_median_cols<20><<<grid, 256, 0, st>>>(part, L, B, S, n, med); break;
-            case 40: k_median_cols<40><<<grid, 256, 0, st>>>(part, L, B, S, n, med); break;
-            default: k_median_cols<0><<<grid, 256, 0, st>>>(part, L, B, S, n, med); break;
-        }
-    } else {
-        const unsigned grid = static_cast<unsigned>((long long)L * ((n + 31) / 32));
-        switch (B) {
-            case 10: k_median_tile<10><<<grid, 256, 0, st>>>(part, L, B, S, n, med); break;
-            case 20: k_median_tile<20><<<grid, 256, 0, st>>>(part, L, B, S, n, med); break;
-            case 40: k_median_tile<40><<<grid, 256, 0, st>>>(part, L, B, S, n, med); break;
-            default: k_median_tile<0><<<grid, 256, 0, st>>>(part, L, B, S, n, med); break;
-        }
+    const unsigned grid = static_cast<unsigned>((long long)L * ((n + 31) / 32));
+    switch (B) {
+        case 10: k_median_tile<10><<<grid, 256, 0, st>>>(part, L, B, S, n, med); break;
+        case 20: k_median_tile<20><<<grid, 256, 0, st>>>(part, L, B, S, n, med); break;
+        case 40: k_median_tile<40><<<grid, 256, 0, st>>>(part, L, B, S, n, med); break;
+        default: k_median_tile<0><<<grid, 256, 0, st>>>(part, L, B, S, n, med); break;
     }
     SKC_LAUNCHED();
     if (Unext) {
@@ -1091,11 +995,6 @@ __global__ void __launch_bounds__(kFftThreads, SKC_FFT_MINB)
     double2* o = reinterpret_cast<double2*>(acc) + (((size_t)ch * B + m) * S + r) * N;
     for (int j = threadIdx.x; j < N; j += blockDim.x) o[j] = ACC[pad16(j)];
 }
-// Max radix of the local DIF passes (A/B hook): 4 = radix-16 (make_plan), 3 = radix-8.
-static int env_lr(const char* name) {
-    const char* e = std::getenv(name);
-    return (e && std::atoi(e) == 3) ? 3 : 4;
-}
 template <int LR>
 static void moment_launch(cudaStream_t st, const SymView& v, const double* X, const double* w, double wscale,
                           long long Nsamp, int chunks, double* acc, bool scr, size_t smem, unsigned grid) {
@@ -1118,11 +1017,7 @@ void launch_sym_moment_accumulate(cudaStream_t st, const SymView& v, const doubl
     const size_t smem = sizeof(double2) * (2 * padded_len(v.N)) +
                         (scr ? (sizeof(double2) + 2 * sizeof(std::uint32_t) + 2 * sizeof(double)) * (size_t)v.n + 8 : 0);
     const unsigned grid = (unsigned)((long long)chunks * v.B * v.S);
-    static const int lr = env_lr("SKC_MOMENT_LR");
-    if (lr == 3)
-        moment_launch<3>(st, v, X, w, wscale, Nsamp, chunks, acc, scr, smem, grid);
-    else
-        moment_launch<4>(st, v, X, w, wscale, Nsamp, chunks, acc, scr, smem, grid);
+    moment_launch<4>(st, v, X, w, wscale, Nsamp, chunks, acc, scr, smem, grid);  // radix-16 local passes
     SKC_LAUNCHED();
     count_transforms((std::uint64_t)Nsamp * v.B * v.S, v.S);
 }

@@ -81,44 +81,6 @@ def test_sym_dense_build_matches_oracle(gpu_ctx, n, b, B):
     assert s.version() == 1
 
 
-_FINALIZE_AB = r"""
-import sys, numpy as np
-sys.path.insert(0, sys.argv[1])
-import paper_1506_04448_b200 as skb
-out = []
-for n, b, B, seed in [(40, 1024, 5, 1), (64, 4096, 20, 2), (120, 16384, 6, 5), (20, 1 << 15, 2, 6)]:
-    rng = np.random.default_rng(seed)
-    s = skb.SymTensorSketchSet(n, b, B, seed)
-    for rep in range(2):  # the second build adds onto existing data
-        A = rng.normal(size=(n, n, n))
-        T = sum(A.transpose(p) for p in [(0, 1, 2), (0, 2, 1), (1, 0, 2), (1, 2, 0), (2, 0, 1), (2, 1, 0)]) / 6
-        s.accumulate_dense(T, assume_symmetric=True)
-        out.append(s.data())
-np.savez(sys.argv[2], *out)
-"""
-
-
-def test_paired_finalize_bit_identical(tmp_path):
-    """The paired (real, imaginary window) finalize of symmetric one-window-per-parity
-    builds and the generic per-slot walk (SKC_FINALIZE_PAIR=0) give bit-identical sets,
-    including a second build onto existing data."""
-    import os
-    import subprocess
-    import sys
-
-    root = str(pathlib.Path(__file__).resolve().parents[1])
-    res = {}
-    for v in ("1", "0"):
-        env = dict(os.environ, SKC_FINALIZE_PAIR=v)
-        f = tmp_path / f"fin{v}.npz"
-        subprocess.run([sys.executable, "-c", _FINALIZE_AB, root, str(f)], check=True, env=env)
-        z = np.load(f)
-        res[v] = [z[k] for k in sorted(z.files, key=lambda x: int(x.split("_")[1]))]
-    assert len(res["1"]) == 8
-    for a, b in zip(res["1"], res["0"]):
-        assert np.array_equal(a, b)
-
-
 @pytest.mark.parametrize("n,b,B,seed", [(40, 1024, 5, 1), (64, 4096, 20, 2), (36, 1 << 16, 3, 3), (17, 64, 4, 4),
                                         (120, 16384, 6, 5), (20, 1 << 15, 2, 6), (24, 1 << 17, 2, 7)])
 def test_dense_builds_across_bucket_class_bits_match_oracle(gpu_ctx, n, b, B, seed):
