@@ -688,12 +688,37 @@ static void sym_contract_half_launch(cudaStream_t st, const SymView& v, const do
 }
 
 
+// Restarts per CTA of the half-length contraction kernel (3 resident CTAs per SM): each
+// CTA builds its (replicate, residue) scatter metadata once and then runs its restarts one
+// after another, so the step's makespan is ~ ceil(CTAs / resident slots) x (restarts per
+// CTA + setup), setup ~ 0.3 restart. Config 1 (16000 restart-residue tasks) is flat in this
+// choice (3..13 per CTA measured 0.730..0.758 ms); config 0 (2000 tasks, ~1.2 waves at 4 per
+// CTA) takes 5 per CTA, one wave (RTPM contraction time -10%).
+static int contract_restarts_per_cta(int L, int per_restart_ctas) {
+    static int sms[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int& nsm = sms[dev & 63];
+    if (nsm == 0) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const long long slots = 3ll * (nsm > 0 ? nsm : 148);
+    int best = 4;
+    double best_cost = 1e300;
+    for (int lpb = 1; lpb <= 8; ++lpb) {
+        const long long ctas = static_cast<long long>((L + lpb - 1) / lpb) * per_restart_ctas;
+        const double cost = static_cast<double>((ctas + slots - 1) / slots) * (lpb + 0.3);
+        if (cost < best_cost - 1e-9) {
+            best_cost = cost;
+            best = lpb;
+        }
+    }
+    return best;
+}
+
 void launch_sym_contract(cudaStream_t st, const SymView& v, const double* U, int L, int mode, double* out) {
     const bool scr_ok = v.n <= kScatterMax;
     if (scr_ok && v.logN >= 2) {
-        // 4 restarts per CTA (config 1: 3..13 per CTA measured 0.730..0.758 ms per step)
         SymView vv = v;
-        vv.lpb = 4;
+        vv.lpb = contract_restarts_per_cta(L, v.B * v.S);
         const int NH = v.N / 2;
         const size_t smem = sizeof(double2) * (padded_len(v.N) + (NH + NH / 16 + 1)) +
                             (sizeof(double2) + 2 * sizeof(std::uint32_t)) * 2 * (size_t)v.n +
