@@ -47,7 +47,20 @@ static std::vector<std::pair<const char*, std::function<void()>>>& registry() {
 struct Reg {
     Reg(const char* n, std::function<void()> f) { registry().emplace_back(n, std::move(f)); }
 };
-#define TEST_CASE(name, fn) static void fn(); static Reg reg_##fn(name, fn); static void fn()
+#define TEST_CASE("compat Eigen: column-to-column assignment copies coefficients", test_column_assign) {
+    Eigen::MatrixXd A(3, 2), B(3, 2);
+    for (int i = 0; i < 3; ++i) {
+        A(i, 0) = i + 1;
+        A(i, 1) = 10 * (i + 1);
+    }
+    B.col(1) = A.col(0);  // both non-const views: must copy, not rebind
+    for (int i = 0; i < 3; ++i) CHECK(B(i, 1) == i + 1 && B(i, 0) == 0.0);
+    const Eigen::MatrixXd& Ac = A;
+    B.col(0) = Ac.col(1);
+    for (int i = 0; i < 3; ++i) CHECK(B(i, 0) == 10 * (i + 1));
+}
+
+TEST_CASE(name, fn) static void fn(); static Reg reg_##fn(name, fn); static void fn()
 
 static double max_abs_diff(const cvec& a, const cvec& b) {
     double m = 0;
