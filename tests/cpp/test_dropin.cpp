@@ -47,20 +47,7 @@ static std::vector<std::pair<const char*, std::function<void()>>>& registry() {
 struct Reg {
     Reg(const char* n, std::function<void()> f) { registry().emplace_back(n, std::move(f)); }
 };
-#define TEST_CASE("compat Eigen: column-to-column assignment copies coefficients", test_column_assign) {
-    Eigen::MatrixXd A(3, 2), B(3, 2);
-    for (int i = 0; i < 3; ++i) {
-        A(i, 0) = i + 1;
-        A(i, 1) = 10 * (i + 1);
-    }
-    B.col(1) = A.col(0);  // both non-const views: must copy, not rebind
-    for (int i = 0; i < 3; ++i) CHECK(B(i, 1) == i + 1 && B(i, 0) == 0.0);
-    const Eigen::MatrixXd& Ac = A;
-    B.col(0) = Ac.col(1);
-    for (int i = 0; i < 3; ++i) CHECK(B(i, 0) == 10 * (i + 1));
-}
-
-TEST_CASE(name, fn) static void fn(); static Reg reg_##fn(name, fn); static void fn()
+#define TEST_CASE(name, fn) static void fn(); static Reg reg_##fn(name, fn); static void fn()
 
 static double max_abs_diff(const cvec& a, const cvec& b) {
     double m = 0;
@@ -86,6 +73,19 @@ static DenseTensor3 rank1(const Eigen::VectorXd& u, double a) {
         for (int j = 0; j < n; ++j)
             for (int k = 0; k < n; ++k) T.at(i, j, k) = a * u[i] * u[j] * u[k];
     return T;
+}
+
+TEST_CASE("compat Eigen: column-to-column assignment copies coefficients", test_column_assign) {
+    Eigen::MatrixXd A(3, 2), B(3, 2);
+    for (int i = 0; i < 3; ++i) {
+        A(i, 0) = i + 1;
+        A(i, 1) = 10 * (i + 1);
+    }
+    B.col(1) = A.col(0);  // both non-const views: must copy, not rebind
+    for (int i = 0; i < 3; ++i) CHECK(B(i, 1) == i + 1 && B(i, 0) == 0.0);
+    const Eigen::MatrixXd& Ac = A;
+    B.col(0) = Ac.col(1);
+    for (int i = 0; i < 3; ++i) CHECK(B(i, 0) == 10 * (i + 1));
 }
 
 TEST_CASE("hash KATs (test_hashing.cpp:47-56,142-146)", hash_kats) {
