@@ -82,6 +82,9 @@ int skc_context_wait_stream(skc_context* ctx, void* producer);
  * limb overflowed (>= 512 same-signed full-scale adds to one slot in one pass) is
  * discarded and repeated exactly with two limbs. Number of such repeats so far. */
 int skc_context_build_retries(skc_context* ctx, long long* out);
+/* Dense builds redone in magnitude bands: tensors whose entries span more magnitudes than
+ * one exact fixed-point scale resolves to ~2^-34 of each bucket (high dynamic range). */
+int skc_context_build_banded(skc_context* ctx, long long* out);
 int skc_device_count(int* out);
 /* Per-kernel device timing with CUDA events on the context stream (off by
  * default). skc_profile_get sums the recorded durations of one kernel family

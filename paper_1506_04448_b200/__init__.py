@@ -173,6 +173,12 @@ class Context:
         check(lib.skc_context_build_retries(self.handle, C.byref(v)))
         return v.value
 
+    def build_banded(self) -> int:
+        """Dense builds redone in magnitude bands (high-dynamic-range tensors)."""
+        v = C.c_longlong()
+        check(lib.skc_context_build_banded(self.handle, C.byref(v)))
+        return v.value
+
     def stream(self) -> int:
         s = C.c_void_p()
         check(lib.skc_context_stream(self._h, C.byref(s)))

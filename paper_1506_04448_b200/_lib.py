@@ -64,6 +64,7 @@ SIGNATURES = {
     "skc_context_stream": (c_int, [p_void, pp_void]),
     "skc_context_wait_stream": (c_int, [p_void, p_void]),
     "skc_context_build_retries": (c_int, [p_void, p_ll]),
+    "skc_context_build_banded": (c_int, [p_void, p_ll]),
     "skc_device_count": (c_int, [p_int]),
     "skc_profile_enable": (c_int, [p_void, c_int]),
     "skc_profile_reset": (c_int, [p_void]),

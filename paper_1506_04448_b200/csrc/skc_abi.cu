@@ -160,6 +160,13 @@ int skc_context_build_retries(skc_context* ctx, long long* out) {
         *out = ctx->build_two_limb_retries;
     });
 }
+int skc_context_build_banded(skc_context* ctx, long long* out) {
+    return guard([&] {
+        check_vec(ctx, "context");
+        check_vec(out, "out");
+        *out = ctx->build_banded;
+    });
+}
 
 uint64_t skc_derive_seed(uint64_t master, uint64_t tag, uint64_t i0, uint64_t i1) {
     return derive_seed(master, tag, i0, i1);

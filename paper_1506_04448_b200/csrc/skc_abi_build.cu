@@ -122,7 +122,7 @@ skc_context::RowTab& prepare_dense_build(skc_context* ctx, int n, int dtype, boo
     ctx->build_acc.alloc(static_cast<size_t>(total_slots));
     ctx->qbuf.alloc(static_cast<size_t>(std::max<long long>(1, tot)));
     ctx->rowF.alloc(static_cast<size_t>(std::max(1, rt.nrows)));
-    ctx->prepass.alloc(2 * kPrepassBlocks);  // L1 sums, then maxima
+    ctx->prepass.alloc(4 * kPrepassBlocks);  // sums, maxima, sums of squares, minima
     ctx->ints.alloc(16);
 
     p = BuildPlan();
@@ -163,7 +163,62 @@ skc_context::RowTab& prepare_dense_build(skc_context* ctx, int n, int dtype, boo
     p.data_as_double = reinterpret_cast<double*>(data);
     if (p.xsrc_mode == 1)  // device-resident class-list build: sums-only pre-pass, one wave of 5 blocks/SM
         p.prepass_blocks = std::min(kPrepassBlocks, std::max(1, ctx->sms) * 5);
+    p.total_entries = tot;
     return rt;
+}
+
+// High-dynamic-range builds (the resolution check of the main pass flagged the tensor):
+// entries are split by the magnitude of kappa|T| into bands of at most 16 binades (from the
+// exponent histogram, empty ranges skipped), and each band is built with its own exponent
+// from its own sums: the raw-copy (class-list) or fixed-point (contiguous-window) pre-pass
+// writes the band's entries and zeros elsewhere, then the main pass and the finalize add
+// that band's sketch to the data. Within a band max/min kappa|T| < 2^16, so every bucket
+// keeps <= ~2^-34 of its own magnitude; the fp64 reference sum (sketch.cpp:340) keeps
+// ~2^-52 of its terms' magnitude. Exact per band, bands added in fp64 (one rounding each).
+void run_dense_build_banded(skc_context* ctx, const void* Tdev, int n, int dtype, bool sym, int i0, int i1, int B,
+                            std::uint32_t b, const std::uint32_t* packed, double2* data, bool zero_copy) {
+    BuildPlan p;
+    skc_context::RowTab& rt = prepare_dense_build(ctx, n, dtype, sym, i0, i1, B, b, packed, data, zero_copy, true, p);
+    if (rt.nrows == 0) return;
+    DevBuf<unsigned long long> hist;
+    hist.alloc(kExpBins);
+    CK(cudaMemsetAsync(hist.p, 0, sizeof(unsigned long long) * kExpBins, ctx->stream));
+    launch_build_exp_hist(ctx->stream, Tdev, p, hist.p);
+    ctx->check_launch();
+    std::vector<unsigned long long> h(kExpBins);
+    CK(cudaMemcpyAsync(h.data(), hist.p, sizeof(unsigned long long) * kExpBins, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    for (int e = kExpBins - 1; e >= 0;) {
+        while (e >= 0 && h[e] == 0) --e;
+        if (e < 0) break;
+        const int top = e, bot = std::max(0, top - 15);
+        e = bot - 1;
+        BuildPlan q = p;
+        q.band_lo = std::ldexp(1.0, bot - kExpBias);
+        q.band_hi = std::ldexp(1.0, top - kExpBias + 1);
+        q.rho_max = INFINITY;
+        q.xsrc_mode = q.cls_bits >= 0 ? 2 : 0;  // the pre-pass writes the band's (masked) copy
+        q.prepass_blocks = kPrepassBlocks;
+        q.pdl = false;
+        ensure_build_scratch_clean(ctx);
+        ctx->build_scratch_clean = false;
+        CK(cudaMemsetAsync(q.nonfinite, 0, sizeof(int), ctx->stream));
+        {
+            SKC_PROF(ctx, "build_prepass");
+            launch_build_prepass(ctx->stream, Tdev, q);
+        }
+        {
+            SKC_PROF(ctx, "build_main");
+            launch_build_main(ctx->stream, Tdev, q);
+        }
+        {
+            SKC_PROF(ctx, "build_finalize");
+            launch_build_finalize(ctx->stream, q);
+        }
+        ctx->build_scratch_clean = true;
+        ctx->check_launch();
+    }
+    ++ctx->build_banded;
 }
 
 void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool sym, int i0, int i1, int B,
@@ -194,7 +249,7 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
         ctx->build_acc.alloc(static_cast<size_t>(K) * total_slots);
         ctx->build_ints.alloc(static_cast<size_t>(K) * G);
         ctx->ints.alloc(16);
-        ctx->prepass.alloc(2 * static_cast<size_t>(K) * qsms);
+        ctx->prepass.alloc(4 * static_cast<size_t>(K) * qsms);
         ensure_build_scratch_clean(ctx);
         ctx->build_scratch_clean = false;
         if (!ctx->stream2) CK(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
@@ -219,7 +274,8 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
                 pc.rowoff = rt.offs.p + rb[c];
                 pc.rowF = ctx->rowF.p + rb[c];
                 pc.nrows = rb[c + 1] - rb[c];
-                pc.prepass_partials = ctx->prepass.p + 2 * static_cast<size_t>(c) * qsms;
+                pc.total_entries = rt.cum[rb[c + 1]] - rt.cum[rb[c]];
+                pc.prepass_partials = ctx->prepass.p + 4 * static_cast<size_t>(c) * qsms;
                 pc.scale_exp = ctx->ints.p + 4 + c;
                 pc.reset_nonfinite = false;
                 pc.acc = ctx->build_acc.p + static_cast<size_t>(c) * total_slots;
@@ -263,7 +319,7 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
     int* flag = ctx->pinned_ints();  // pinned: a direct DMA, not a staged pageable copy
     CK(cudaMemcpyAsync(flag, p.nonfinite, 3 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     ctx->sync();
-    const int nonfinite = flag[0], overflow = flag[2];
+    const int nonfinite = flag[0], overflow = flag[2] & 1, hdr = flag[2] & 2;
     // Fixed-point accumulation cannot carry NaN/Inf the way the reference's
     // floating-point sum would; reject instead of producing a wrong sketch.
     if (nonfinite) {
@@ -272,6 +328,11 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
             ctx->sync();
         }
         fail(kInvalidArgument, "accumulate_dense: tensor has a non-finite entry");
+    }
+    if (hdr) {  // beyond one fixed-point scale: the finalize added nothing; redo in magnitude bands
+        CK(cudaMemsetAsync(p.ovf, 0, sizeof(int), ctx->stream));
+        run_dense_build_banded(ctx, Tdev, n, dtype, sym, i0, i1, B, b, packed, data, zero_copy);
+        return;
     }
     if (overflow) {  // a one-limb window overflowed: the finalize added nothing; redo exactly
         CK(cudaMemsetAsync(p.ovf, 0, sizeof(int), ctx->stream));

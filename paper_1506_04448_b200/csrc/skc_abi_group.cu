@@ -91,7 +91,7 @@ void each_collective(std::vector<Local>& loc, F&& f) {
 }
 
 void dense_group_attempt(std::vector<Local>& loc, const void* const* T, int dtype, int location, bool two_limb,
-                         bool* overflow) {
+                         bool* overflow, bool* hdr) {
     const int n = loc[0].s->n, R = loc[0].ctx->nranks;
     const std::vector<int> bounds = group_slices(n, true, R);
     std::vector<BuildPlan> plans(loc.size());
@@ -105,6 +105,7 @@ void dense_group_attempt(std::vector<Local>& loc, const void* const* T, int dtyp
         Tdev[d] = stage_tensor(ctx, T[d], n, dtype, location, true, i0, i1, false, nullptr, &zc);
         BuildPlan& p = plans[d];
         prepare_dense_build(ctx, n, dtype, true, i0, i1, s->B, s->b, s->packed.p, s->data.p, zc, two_limb, p);
+        p.total_entries = static_cast<long long>(n) * (n + 1) * (n + 2) / 6;  // the whole build (global mean)
         // the same partial count on every rank (the all-gather concatenates them)
         p.prepass_blocks = std::min(kPrepassBlocks, std::max(1, ctx->sms) * 5);
         p.pdl = false;
@@ -116,11 +117,11 @@ void dense_group_attempt(std::vector<Local>& loc, const void* const* T, int dtyp
             launch_build_prepass(ctx->stream, Tdev[d], p);  // (an empty slice writes zero partials)
         }
         ctx->check_launch();
-        ctx->gathered.alloc(2ull * p.prepass_blocks * R);
+        ctx->gathered.alloc(4ull * p.prepass_blocks * R);
     }
     each_collective(loc, [&](Local& l) {
         const size_t d = &l - loc.data();
-        NC(ncclAllGather(plans[d].prepass_partials, l.ctx->gathered.p, 2ull * plans[d].prepass_blocks, ncclDouble,
+        NC(ncclAllGather(plans[d].prepass_partials, l.ctx->gathered.p, 4ull * plans[d].prepass_blocks, ncclDouble,
                          l.ctx->comm, l.ctx->stream));
     });
     for (size_t d = 0; d < loc.size(); ++d) {
@@ -159,13 +160,15 @@ void dense_group_attempt(std::vector<Local>& loc, const void* const* T, int dtyp
     }
     bool nonfinite = false;
     *overflow = false;
+    *hdr = false;
     for (size_t d = 0; d < loc.size(); ++d) {
         loc[d].ctx->use();
         loc[d].ctx->sync();
         nonfinite |= flags[d][0] != 0;
-        *overflow |= flags[d][2] != 0;
+        *overflow |= (flags[d][2] & 1) != 0;
+        *hdr |= (flags[d][2] & 2) != 0;
     }
-    if (*overflow || nonfinite)
+    if (*overflow || *hdr || nonfinite)
         for (size_t d = 0; d < loc.size(); ++d) {
             loc[d].ctx->use();
             CK(cudaMemsetAsync(plans[d].ovf, 0, sizeof(int), loc[d].ctx->stream));
@@ -283,11 +286,37 @@ int skc_sym_accumulate_dense_group(skc_sym_set* const* sets, int nsets, const vo
                 check_symmetric(l.ctx, Tf, dtype, n);
             }
         for (auto& l : loc) l.s->version++;  // sketch.cpp:324
-        bool overflow = false;
-        dense_group_attempt(loc, T, dtype, location, false, &overflow);
-        if (overflow) {  // some rank's one-limb window overflowed: every rank redoes the build with two limbs
+        bool overflow = false, hdr = false;
+        dense_group_attempt(loc, T, dtype, location, false, &overflow, &hdr);
+        if (overflow && !hdr) {  // a one-limb window overflowed: every rank redoes the build with two limbs
             for (auto& l : loc) ++l.ctx->build_two_limb_retries;
-            dense_group_attempt(loc, T, dtype, location, true, &overflow);
+            dense_group_attempt(loc, T, dtype, location, true, &overflow, &hdr);
+        }
+        if (hdr) {
+            // high dynamic range (the same verdict on every rank): each rank builds its slice in
+            // magnitude bands, rank 0 onto the shared prior and the others onto zero, and the
+            // replicas' data are summed (fp64; bit identity across rank counts does not carry
+            // over to this path)
+            const std::vector<int> bounds = group_slices(n, true, loc[0].ctx->nranks);
+            for (size_t d = 0; d < loc.size(); ++d) {
+                skc_context* ctx = loc[d].ctx;
+                skc_sym_set* s = loc[d].s;
+                ctx->use();
+                const int i0 = bounds[ctx->rank], i1 = bounds[ctx->rank + 1];
+                bool zc = false;
+                const void* Td = stage_tensor(ctx, T[d], n, dtype, location, true, i0, i1, false, nullptr, &zc);
+                if (ctx->nranks > 1 && ctx->rank != 0)
+                    CK(cudaMemsetAsync(s->data.p, 0, sizeof(double2) * s->B * s->b, ctx->stream));
+                run_dense_build_banded(ctx, Td, n, dtype, true, i0, i1, s->B, s->b, s->packed.p, s->data.p, zc);
+            }
+            each_collective(loc, [&](Local& l) {
+                NC(ncclAllReduce(l.s->data.p, l.s->data.p, 2ull * l.s->B * l.s->b, ncclDouble, ncclSum, l.ctx->comm,
+                                 l.ctx->stream));
+            });
+            for (auto& l : loc) {
+                l.ctx->use();
+                l.ctx->sync();
+            }
         }
     });
 }

@@ -147,6 +147,7 @@ struct skc_context {
     bool build_scratch_clean = false;      // build_acc / build_ints are all zero (finalize re-zeroes them)
     bool build_ovf_clean = false;          // ints[3] (one-limb overflow flag) is zero
     long long build_two_limb_retries = 0;  // one-limb builds redone with two limbs (overflow)
+    long long build_banded = 0;            // builds redone in magnitude bands (high dynamic range)
     const void* build_acc_clean_p = nullptr;  // the buffers (pointer, size) that were cleared
     const void* build_ints_clean_p = nullptr;
     size_t build_acc_clean_n = 0, build_ints_clean_n = 0;
@@ -413,6 +414,8 @@ const void* stage_tensor(skc_context* ctx, const void* T, int n, int dtype, int 
 void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool sym, int i0, int i1, int B,
                      std::uint32_t b, const std::uint32_t* packed, double2* data, bool zero_copy, bool two_limb = false);
 void ensure_build_scratch_clean(skc_context* ctx);
+void run_dense_build_banded(skc_context* ctx, const void* Tdev, int n, int dtype, bool sym, int i0, int i1, int B,
+                            std::uint32_t b, const std::uint32_t* packed, double2* data, bool zero_copy);
 skc_context::RowTab& prepare_dense_build(skc_context* ctx, int n, int dtype, bool sym, int i0, int i1, int B,
                                          std::uint32_t b, const std::uint32_t* packed, double2* data, bool zero_copy,
                                          bool two_limb, BuildPlan& p);

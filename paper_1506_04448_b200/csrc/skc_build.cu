@@ -73,6 +73,40 @@ __device__ double block_sum_b(double v, double* red) {
 }
 }  // namespace
 
+// Block reduction of the pre-pass statistics into partials segment k at [k * grid + blk]:
+// 0 the kappa|T| sum (fixed shuffle/block order), 1 its maximum, 2 the sum of squares
+// (fixed order), 3 the smallest nonzero kappa|T|. 2 and 3 feed the main pass's resolution
+// check (cta_scale_exp).
+template <int NT>
+__device__ void prepass_block_stats(double sum, double mx, double sq, double mn, double* red, double* partials) {
+    constexpr int W = NT / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const double s = block_sum_b<NT>(sum, red);
+    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+    const double q = block_sum_b<NT>(sq, red);
+    if (threadIdx.x == 0) partials[2 * gridDim.x + blockIdx.x] = q;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    }
+    __syncthreads();
+    if (lane == 0) {
+        red[warp] = mx;
+        red[W + warp] = mn;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = 0.0, l = INFINITY;
+        for (int w = 0; w < W; ++w) {
+            m = fmax(m, red[w]);
+            l = fmin(l, red[W + w]);
+        }
+        partials[gridDim.x + blockIdx.x] = m;
+        partials[3 * gridDim.x + blockIdx.x] = l;
+    }
+}
+
 // ---- pre-pass ---------------------------------------------------------------------
 // One warp per row segment T[i][j][k0:n]. Every mode computes the row's L1 mass
 // sum kappa|T| in a fixed order, the block max of kappa|T| and the non-finite flag; the
@@ -90,13 +124,13 @@ __global__ void __launch_bounds__(NTQ) k_build_quantize(const TT* __restrict__ T
                                                        const long long* __restrict__ rowoff, int nrows,
                                                        long long* __restrict__ qbuf, short* __restrict__ rowF,
                                                        double* __restrict__ partials, int* __restrict__ nonfinite,
-                                                       bool vec16) {
+                                                       bool vec16, double band_lo, double band_hi) {
     constexpr int W = NTQ / 32;
     extern __shared__ double stage[];  // W warps x n: each element of T is read exactly once
-    __shared__ double red[W];
+    __shared__ double red[2 * W];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double* st = stage + (size_t)warp * n;
-    double blk = 0.0, bmax = 0.0;
+    double blk = 0.0, bmax = 0.0, bsq = 0.0, bmn = INFINITY;
     bool bad = false;
     TT* xraw = reinterpret_cast<TT*>(qbuf);  // kRaw output
     // 16-byte path: the first 128-vector block of the warp's next row is loaded before the
@@ -166,11 +200,16 @@ __global__ void __launch_bounds__(NTQ) k_build_quantize(const TT* __restrict__ T
                         if (kk >= 0 && kk < n - k0) {
                             const double x = elem(v[u], h);
                             const int k = k0 + kk;
-                            const double kv = ((SYM && k == j) ? kdiag : koff) * x;
+                            const double kv0 = ((SYM && k == j) ? kdiag : koff) * x;
+                            // magnitude band [band_lo, band_hi) of kappa |T| (HDR builds; else all)
+                            const bool keep = fabs(kv0) >= band_lo && fabs(kv0) < band_hi;
+                            const double kv = keep ? kv0 : 0.0;
                             if (MODE == kQuant) st[kk] = kv;
-                            if (MODE == kRaw) xo[kk] = static_cast<TT>(x);
+                            if (MODE == kRaw) xo[kk] = keep ? static_cast<TT>(x) : TT(0);
                             a0 += fabs(kv);
                             bmax = fmax(bmax, fabs(kv));
+                            bsq += kv * kv;
+                            if (kv != 0.0) bmn = fmin(bmn, fabs(kv));
                             bad |= !isfinite(x);
                         }
                     }
@@ -186,11 +225,15 @@ __global__ void __launch_bounds__(NTQ) k_build_quantize(const TT* __restrict__ T
                 for (int u = 0; u < 4; ++u) {
                     const int k = kb + 32 * u;
                     if (k < n) {
-                        const double kv = ((SYM && k == j) ? kdiag : koff) * v[u];
+                        const double kv0 = ((SYM && k == j) ? kdiag : koff) * v[u];
+                        const bool keep = fabs(kv0) >= band_lo && fabs(kv0) < band_hi;
+                        const double kv = keep ? kv0 : 0.0;
                         if (MODE == kQuant) st[k - k0] = kv;
-                        if (MODE == kRaw) xo[k - k0] = rp[k];
+                        if (MODE == kRaw) xo[k - k0] = keep ? rp[k] : TT(0);
                         a0 += fabs(kv);
                         bmax = fmax(bmax, fabs(kv));
+                        bsq += kv * kv;
+                        if (kv != 0.0) bmn = fmin(bmn, fabs(kv));
                         bad |= !isfinite(v[u]);
                     }
                 }
@@ -220,19 +263,7 @@ __global__ void __launch_bounds__(NTQ) k_build_quantize(const TT* __restrict__ T
         blk += (lane == 0) ? a0 : 0.0;
     }
     if (bad) atomicOr(nonfinite, 1);
-    const double s = block_sum_b<NTQ>(blk, red);
-    if (threadIdx.x == 0) partials[blockIdx.x] = s;
-    // block max of kappa|T| (order-free)
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) bmax = fmax(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
-    __syncthreads();
-    if (lane == 0) red[warp] = bmax;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double mx = 0.0;
-        for (int w = 0; w < W; ++w) mx = fmax(mx, red[w]);
-        partials[gridDim.x + blockIdx.x] = mx;
-    }
+    prepass_block_stats<NTQ>(blk, bmax, bsq, bmn, red, partials);
 }
 
 // Lean sums-only pre-pass (default for device-resident class-list builds). Each lane
@@ -246,10 +277,11 @@ __global__ void __launch_bounds__(256, 5) k_build_sums_lean(const TT* __restrict
                                                             const std::uint32_t* __restrict__ rowtab, int nrows,
                                                             double* __restrict__ partials, int* __restrict__ nonfinite) {
     constexpr int W = 8, U = 4;
-    __shared__ double red[W];
+    __shared__ double red[2 * W];
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double acc = 0.0, mx = 0.0;
+    double acc = 0.0, mx = 0.0, sq = 0.0;
+    float mn = INFINITY;  // smallest nonzero kappa|T|, rounded down (a register less than fp64)
     const int stride = gridDim.x * W;
     const int row0 = blockIdx.x * W + warp;
     std::uint32_t nij[2];  // the next pair's (i, j) words, fetched one step ahead
@@ -287,6 +319,8 @@ __global__ void __launch_bounds__(256, 5) k_build_sums_lean(const TT* __restrict
                     const double a = w * fabs(static_cast<double>(v[h][u]));
                     acc += a;
                     mx = fmax(mx, a);
+                    sq = fma(a, a, sq);
+                    mn = fminf(mn, a > 0.0 ? __double2float_rd(a) : INFINITY);
                 }
                 if (kb + 32 * U >= n) break;
 #pragma unroll
@@ -298,18 +332,44 @@ __global__ void __launch_bounds__(256, 5) k_build_sums_lean(const TT* __restrict
         }
     }
     // (no flag write: the main pass derives it from these partials)
-    const double s = block_sum_b<256>(acc, red);
-    if (threadIdx.x == 0) partials[blockIdx.x] = s;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    prepass_block_stats<256>(acc, mx, sq, static_cast<double>(mn), red, partials);
+}
+
+// Exponent histogram of kappa|T| over the build's rows (HDR builds only): one warp per row,
+// shared-memory bins, one global add per non-empty bin and block.
+template <typename TT, bool SYM>
+__global__ void __launch_bounds__(256) k_build_exp_hist(const TT* __restrict__ T, int n,
+                                                         const std::uint32_t* __restrict__ rowtab, int nrows,
+                                                         unsigned long long* __restrict__ hist) {
+    __shared__ unsigned int sh[kExpBins];
+    for (int x = threadIdx.x; x < kExpBins; x += 256) sh[x] = 0u;
     __syncthreads();
-    if (lane == 0) red[warp] = mx;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double m = 0.0;
-        for (int w = 0; w < W; ++w) m = fmax(m, red[w]);
-        partials[gridDim.x + blockIdx.x] = m;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int row = blockIdx.x * 8 + warp; row < nrows; row += gridDim.x * 8) {
+        const std::uint32_t ij = rowtab[row];
+        const int i = static_cast<int>(ij >> 16), j = static_cast<int>(ij & 0xFFFFu);
+        const int k0 = SYM ? j : 0;
+        const TT* rp = T + ((size_t)i * n + j) * n;
+        for (int k = k0 + lane; k < n; k += 32) {
+            const double w = !SYM ? 1.0 : (k == k0 ? (i == j ? 1.0 : 3.0) : (i == j ? 3.0 : 6.0));
+            const double a = w * fabs(static_cast<double>(rp[k]));
+            if (a > 0.0 && isfinite(a)) atomicAdd(&sh[ilogb(a) + kExpBias], 1u);
+        }
     }
+    __syncthreads();
+    for (int x = threadIdx.x; x < kExpBins; x += 256)
+        if (sh[x]) atomicAdd(hist + x, static_cast<unsigned long long>(sh[x]));
+}
+void launch_build_exp_hist(cudaStream_t st, const void* T, const BuildPlan& p, unsigned long long* hist) {
+    const unsigned grid = 4u * 148u;
+    if (p.sym) {
+        if (p.dtype == 0) k_build_exp_hist<double, true><<<grid, 256, 0, st>>>((const double*)T, p.n, p.rowtab, p.nrows, hist);
+        else k_build_exp_hist<float, true><<<grid, 256, 0, st>>>((const float*)T, p.n, p.rowtab, p.nrows, hist);
+    } else {
+        if (p.dtype == 0) k_build_exp_hist<double, false><<<grid, 256, 0, st>>>((const double*)T, p.n, p.rowtab, p.nrows, hist);
+        else k_build_exp_hist<float, false><<<grid, 256, 0, st>>>((const float*)T, p.n, p.rowtab, p.nrows, hist);
+    }
+    count_launch();
 }
 
 // Default: kPrepassBlocks x 256 threads over all SMs (HBM-bound). Pipelined zero-copy
@@ -330,7 +390,8 @@ void launch_build_prepass(cudaStream_t st, const void* T, const BuildPlan& p) {
                                      (int)smem);                                                                      \
             k_build_quantize<TT, SY, 1024, MD><<<blocks, 1024, smem, st>>>((const TT*)T, p.n, p.rowtab, p.rowoff,    \
                                                                            p.nrows, p.qbuf, p.rowF,                  \
-                                                                           p.prepass_partials, p.nonfinite, vec16);  \
+                                                                           p.prepass_partials, p.nonfinite, vec16,   \
+                                                                           p.band_lo, p.band_hi);                    \
         } else {                                                                                                      \
             const size_t smem = MD == kQuant ? sizeof(double) * 8 * (size_t)p.n : 0;                                  \
             if (smem > 48 * 1024)                                                                                     \
@@ -338,7 +399,8 @@ void launch_build_prepass(cudaStream_t st, const void* T, const BuildPlan& p) {
                                      (int)smem);                                                                      \
             k_build_quantize<TT, SY, 256, MD><<<blocks, 256, smem, st>>>((const TT*)T, p.n, p.rowtab, p.rowoff,      \
                                                                          p.nrows, p.qbuf, p.rowF,                    \
-                                                                         p.prepass_partials, p.nonfinite, vec16);    \
+                                                                         p.prepass_partials, p.nonfinite, vec16,     \
+                                                                         p.band_lo, p.band_hi);                      \
         }                                                                                                             \
     }
 #define QUANT(TT, SY)                                                                                 \
@@ -423,6 +485,9 @@ struct BuildArgs {
     int sym_even_F;                // symmetric one-limb / two-limb class-list builds: F even (see cta_scale_exp)
     int* next_row;                 // G row (or tile) counters (zero on entry; the finalize re-zeroes them)
     int qbits;                     // max |q| exponent: 50 (two limbs) or 22 (one limb, fp32 input)
+    long long total_entries;       // entries of the whole build (all ranks): the mean of kappa|T|
+    double entries_per_slot;       // total_entries / slots per replicate (bucket thickness)
+    double rho_max;                // resolution bound (see cta_scale_exp)
 
     unsigned long long* acc;       // total_slots exact accumulators (zero on entry; the finalize re-zeroes them)
 };
@@ -432,20 +497,25 @@ struct BuildArgs {
 // kernel can round kappa*T*2^F to an integer with one fma against 1.5*2^52. Every CTA
 // sums the pre-pass partials in the same fixed order (lane-strided, then a fixed shuffle
 // tree read from lane 0), so all CTAs agree; CTA 0 publishes F.
+__shared__ int s_hdr;  // set by cta_scale_exp: this build adds nothing (resolution check)
 __device__ int cta_scale_exp(const BuildArgs& a) {
     __shared__ int sF;
     if (threadIdx.x < 32) {
-        double acc = 0.0, mx = 0.0;
+        double acc = 0.0, mx = 0.0, sq = 0.0, mn = INFINITY;
         for (int x = threadIdx.x; x < a.np * a.nseg; x += 32) {
             const int sg = x / a.np, id = x - sg * a.np;
-            const double* seg = a.partials + 2ll * sg * a.np;
+            const double* seg = a.partials + 4ll * sg * a.np;
             acc += seg[id];
             mx = fmax(mx, seg[a.np + id]);
+            sq += seg[2 * a.np + id];
+            mn = fmin(mn, seg[3 * a.np + id]);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             acc += __shfl_xor_sync(0xffffffffu, acc, o);
             mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            sq += __shfl_xor_sync(0xffffffffu, sq, o);
+            mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
         }
         if (threadIdx.x == 0) {
             int F = 0;
@@ -460,11 +530,32 @@ __device__ int cta_scale_exp(const BuildArgs& a) {
                 // XOR of its low bit (the row word carries that bit)
                 if (a.sym_even_F) F &= ~1;
             }
+            // Resolution check: the fixed-point step 2^-F relative to the mean kappa|T| bounds
+            // the relative error of every bucket (it is ~0.6 x that ratio, the sqrt(count)
+            // of the rounding walk cancelling against the bucket's own growth). Above rho_max
+            // (one limb: 2^-17, two limbs: 2^-33, i.e. entries spanning more magnitudes than
+            // one fixed-point scale keeps to the contract) nothing is added: the host redoes
+            // the build with two limbs (flag 1) or in magnitude bands (flag 2).
+            // Buckets are sums of ~c = entries_per_slot terms. When they are thin (c < 8: a
+            // bucket may be one or two entries) or the mass sits in few entries (N_eff =
+            // (sum)^2 / sum of squares, c N_eff / N < 1: most buckets hold none of the heavy
+            // entries), a bucket may hold only small entries, so the step is measured against
+            // the smallest nonzero one; otherwise against the mean.
+            int hdr = 0;
+            if (acc > 0.0 && isfinite(acc) && isfinite(sq)) {
+                const double N = static_cast<double>(a.total_entries);
+                const double neff = (acc / sqrt(sq)) * (acc / sqrt(sq));
+                const bool thin = a.entries_per_slot < 8.0 || a.entries_per_slot * neff < N;
+                const double rho = thin ? ldexp(1.0, -F) / mn : ldexp(N, -F) / acc;
+                if (rho > a.rho_max) hdr = a.qbits < 50 ? 1 : 2;
+            }
             sF = F;
+            s_hdr = hdr;
             if (blockIdx.x == 0) {
                 *a.scale_out = F;
                 // a non-finite entry makes its lane's (non-negative) sum, hence acc, non-finite
                 if (a.nonfinite_out) *a.nonfinite_out = isfinite(acc) ? 0 : 1;
+                if (hdr) atomicOr(a.ovf_out, hdr);
             }
         }
     }
@@ -503,6 +594,7 @@ __global__ void __launch_bounds__(1024, 1) k_build_flat(BuildArgs a) {
     const long long spr = SYM ? 2ll * (a.bmask + 1) : static_cast<long long>(a.bmask + 1);
     const int prow = SYM ? n : 3 * n;
     const int F = cta_scale_exp(a);
+    if (s_hdr) return;
     std::uint32_t sbase = static_cast<std::uint32_t>(__cvta_generic_to_shared(sacc));
     asm volatile("mov.b32 %0, %0;" : "+r"(sbase));  // keep in a register (no per-use S2UR/ULEA)
     const std::uint32_t hioff = 4u * static_cast<std::uint32_t>(plane);
@@ -871,6 +963,7 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
             have_F = true;
             asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         }
+        if (s_hdr) break;  // block-uniform: the build is redone (two limbs / bands)
 
         constexpr int R = kClsRows;
         int c0 = 0;
@@ -1130,6 +1223,9 @@ void launch_build_main(cudaStream_t st, const void* T, const BuildPlan& p) {
     a.next_row = p.next_row;
     a.acc = p.acc;
     a.qbits = (p.cls_bits >= 0 && p.one_limb) ? 22 : 50;
+    a.total_entries = p.total_entries;
+    a.entries_per_slot = static_cast<double>(p.total_entries) / (p.sym ? 2.0 * (p.bmask + 1.0) : (p.bmask + 1.0));
+    a.rho_max = p.rho_max > 0 ? p.rho_max : (a.qbits < 50 ? 0x1p-17 : 0x1p-33);
 
     if (p.cls_bits >= 0) {
         switch (p.cls_bits) {

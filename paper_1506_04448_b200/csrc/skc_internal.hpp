@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
 
 #include "skc_fft.cuh"
@@ -107,7 +108,14 @@ struct BuildPlan {
     int* scale_exp;               // device int
     int* nonfinite;               // device int
     double* data_as_double;       // B x b x 2
+    long long total_entries = 0;  // entries of the whole build (all ranks' slices)
+    double rho_max = 0.0;         // resolution bound of the build (0: by limbs; +inf: band passes)
+    double band_lo = 0.0, band_hi = INFINITY;  // magnitude band of kappa|T| (HDR band passes)
 };
+// Exponent histogram of kappa|T| over a build's rows (HDR builds): hist[e + kExpBias] counts
+// the entries with 2^e <= kappa|T| < 2^(e+1), zeros not counted.
+constexpr int kExpBias = 1100, kExpBins = 2200;
+void launch_build_exp_hist(cudaStream_t st, const void* T, const BuildPlan& p, unsigned long long* hist);
 constexpr int kPrepassBlocks = 1024;
 size_t build_smem_bytes(long long slots_per_cta, int R, int n);
 size_t cls_smem_bytes(std::uint32_t b, int tbits, int n, bool sym, bool one_limb);
