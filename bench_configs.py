@@ -1,6 +1,6 @@
 #!/usr/bin/env python
 """Secondary measurements for every BASELINE.json config (the driver's bench.py line is
-config 1). One JSON line per measurement; device times come from the library's CUDA-event
+config 2). One JSON line per measurement; device times come from the library's CUDA-event
 profiler or CUDA events on the library stream, CPU baselines from the oracle restatement
 on the host cores (bounded samples, stated in each line).
 
@@ -169,9 +169,24 @@ def c3(skb, ctx, quick):
     ctx.synchronize()
     ms = sum(ctx.profile_get(k)[0] for k in ["moment", "freq_inverse", "combine"])
     ctx.profile(False)
+    # CPU baseline: the oracle's per-sample add_scaled_rank1 (sketch.cpp:347-361, OpenMP over
+    # the B replicates) on a bounded sample of the same samples, extrapolated linearly in N
+    import oracle_py as O
+
+    Ns = 64 if quick else 512
+    Xs = X[:Ns].cpu().numpy()
+    O.lib().orc_set_num_threads(os.cpu_count() or 1)
+    o = O.SymSet(n, b, B, 4)
+    t0 = time.perf_counter()
+    for i in range(Ns):
+        o.add_scaled_rank1(Xs[i], 1.0 / N)
+    cpu_s = time.perf_counter() - t0
     emit({"config": 3, "what": "factored moment sketch (frequency-domain accumulation), device-resident samples",
           "N": N, "n": n, "b": b, "B": B, "device_ms": ms, "samples_per_s": N / (ms * 1e-3),
-          "sample_generation_s_not_timed": gen_s})
+          "sample_generation_s_not_timed": gen_s,
+          "cpu_baseline": {"samples_per_s": Ns / cpu_s, "cores": min(O.lib().orc_num_threads(), B), "kind": "port",
+                           "sample": f"{Ns} samples through the oracle's add_scaled_rank1 loop; N=2^22 extrapolates "
+                                     f"to {N / (Ns / cpu_s):.0f} s"}})
     k = 5 if quick else 50
     t0 = time.perf_counter()
     dec = skb.robust_tpm_fast(s, skb.PowerConfig(k=k, L=30, T_iters=30, seed=1))
@@ -257,9 +272,29 @@ def c4(skb, ctx, quick):
     wall = time.perf_counter() - t0
     dev = {x: ctx.profile_get(x)[0] for x in ["lda_docs", "lda_vocab", "lda_accumulate"]}
     ctx.profile(False)
+    # CPU baseline: the oracle's sketch_whitened_m3 (lda.cpp:145-226) at the full vocabulary on
+    # two document prefixes; time = (V-loop, fixed) + D x (per document), extrapolated to D
+    import oracle_py as O
+
+    O.lib().orc_set_num_threads(os.cpu_count() or 1)
+    cpu = []
+    for Dp in ((200, 400) if quick else (1000, 2000)):
+        sub_ptr = doc_ptr[: Dp + 1]
+        nz = int(sub_ptr[-1])
+        o = O.SymSet(K, b, B, 9)
+        t0 = time.perf_counter()
+        o.sketch_whitened_m3(V, sub_ptr, words[:nz], counts[:nz], W, alpha0)
+        cpu.append((Dp, time.perf_counter() - t0))
+    per_doc = (cpu[1][1] - cpu[0][1]) / (cpu[1][0] - cpu[0][0])
+    fixed = max(0.0, cpu[0][1] - per_doc * cpu[0][0])
+    cpu_full_s = fixed + per_doc * D
     emit({"config": 4, "what": "sketch_whitened_m3 given W on the device-resident corpus", "V": V,
           "K": K, "D": D, "nnz": int(words.size), "used": used, "skipped": skipped, "seconds": wall,
-          "device_ms_by_kernel": dev, "docs_per_s_device": used / (sum(dev.values()) * 1e-3)})
+          "device_ms_by_kernel": dev, "docs_per_s_device": used / (sum(dev.values()) * 1e-3),
+          "cpu_baseline": {"docs_per_s": D / cpu_full_s, "cores": min(O.lib().orc_num_threads(), B), "kind": "port",
+                           "sample": f"oracle sketch_whitened_m3 on the first {cpu[0][0]} and {cpu[1][0]} documents "
+                                     f"({cpu[0][1]:.1f} s, {cpu[1][1]:.1f} s): V-loop {fixed:.1f} s + "
+                                     f"{per_doc * 1e3:.2f} ms/document, extrapolated to D={D}: {cpu_full_s:.0f} s"}})
     k = 5 if quick else 100
     t0 = time.perf_counter()
     dec = skb.robust_tpm_fast(s, skb.PowerConfig(k=k, L=100, T_iters=30, seed=2))
