@@ -197,15 +197,17 @@ int skc_lda_whiten_corpus_handle(skc_lda_corpus* c, double alpha0, int k, int ov
 int skc_sym_sketch_whitened_m3_corpus(skc_sym_set* s, skc_lda_corpus* c, const double* W, double alpha0,
                                       long long* used, long long* skipped);
 
-/* recover_params(D, wm, alpha0) (lda.cpp:228-248), host math: lambda[k], A = D.A (k x k
- * row-major, column i = component i), unwhiten V x k -> Phi V x k (columns projected onto
- * the simplex, lda.cpp:250-271) and alpha[k]. */
-int skc_lda_recover_params(int V, int k, const double* lambda, const double* A, const double* unwhiten, double alpha0,
-                           double* Phi, double* alpha);
-/* heldout_likelihood(model, held) (lda.cpp:273-320): Phi V x k, held-out corpus CSR over
- * vocabulary Vh <= V; documents fitted in parallel, summed in document order. */
-int skc_lda_heldout_likelihood(int V, int k, const double* Phi, int Vh, long long D, const long long* doc_ptr,
-                               const int* word, const int* count, double* ll_out, long long* floored_words);
+/* recover_params(D, wm, alpha0) (lda.cpp:228-248) on ctx's device: lambda[k], A = D.A (k x k
+ * row-major, column i = component i), unwhiten V x k -> Phi V x k (mu_i = 0.5 (alpha0 + 2)
+ * lambda_i unwhiten A[:, i] projected onto the simplex, lda.cpp:250-271) and alpha[k]. */
+int skc_lda_recover_params(skc_context* ctx, int V, int k, const double* lambda, const double* A,
+                           const double* unwhiten, double alpha0, double* Phi, double* alpha);
+/* heldout_likelihood(model, held) (lda.cpp:273-320) on ctx's device: Phi V x k (k <= 128),
+ * held-out corpus CSR over vocabulary Vh <= V; one warp per document (500 projected-
+ * gradient steps), the per-document values summed in document order. */
+int skc_lda_heldout_likelihood(skc_context* ctx, int V, int k, const double* Phi, int Vh, long long D,
+                               const long long* doc_ptr, const int* word, const int* count, double* ll_out,
+                               long long* floored_words);
 
 /* replicate(m).data -> host (B-major when m < 0: all replicates, B*b complex). */
 int skc_sym_read_data(const skc_sym_set* s, int m, double* out_host);

@@ -38,6 +38,9 @@ namespace orc {
 using cd = std::complex<double>;
 using cvec = std::vector<cd>;
 
+struct NumericalError : std::runtime_error {  // common.hpp:20-23
+    using std::runtime_error::runtime_error;
+};
 struct DegenerateIterationError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
@@ -1066,6 +1069,111 @@ void lda_whiten(int V, const double* m2, int k, double* W, double* unwhiten, dou
     }
 }
 
+// lda.cpp:250-271 project_to_simplex: sort descending, last prefix index whose value
+// exceeds its running threshold, uniform if none.
+std::vector<double> project_to_simplex(const double* y, int n) {
+    std::vector<double> u(y, y + n);
+    std::sort(u.begin(), u.end(), std::greater<double>());
+    double css = 0, theta = 0;
+    int rho = 0;
+    for (int i = 0; i < n; ++i) {
+        css += u[i];
+        const double t = (css - 1.0) / (i + 1);
+        if (u[i] - t > 0) {
+            rho = i + 1;
+            theta = t;
+        }
+    }
+    std::vector<double> x(n);
+    if (rho == 0) {
+        std::fill(x.begin(), x.end(), 1.0 / n);
+        return x;
+    }
+    for (int i = 0; i < n; ++i) x[i] = std::max(y[i] - theta, 0.0);
+    return x;
+}
+
+// lda.cpp:228-248 recover_params: A k x k row-major (column i = component i), unwhiten and
+// Phi V x k row-major.
+void lda_recover_params(int V, int k, const double* lambda, const double* A, const double* unwhiten, double alpha0,
+                        double* Phi, double* alpha) {
+    if (k < 1) throw std::invalid_argument("recover_params: empty decomposition");
+    std::vector<double> mu(V);
+    for (int i = 0; i < k; ++i) {
+        const double lam = lambda[i];
+        if (lam == 0.0) throw NumericalError("recover_params: zero eigenvalue at component " + std::to_string(i + 1));
+        alpha[i] = 4.0 * alpha0 * (alpha0 + 1.0) / ((alpha0 + 2.0) * (alpha0 + 2.0) * lam * lam);
+        for (int w = 0; w < V; ++w) {
+            double s = 0;
+            for (int c = 0; c < k; ++c) s += unwhiten[static_cast<std::size_t>(w) * k + c] * A[static_cast<std::size_t>(c) * k + i];
+            mu[w] = 0.5 * (alpha0 + 2.0) * lam * s;
+        }
+        const std::vector<double> ph = project_to_simplex(mu.data(), V);
+        for (int w = 0; w < V; ++w) Phi[static_cast<std::size_t>(w) * k + i] = ph[w];
+    }
+}
+
+// lda.cpp:273-320 heldout_likelihood (sequential, document order).
+double lda_heldout_likelihood(int V, int k, const double* Phi, int Vh, long long D, const long long* doc_ptr,
+                              const int* word, const int* count, long long* floored_out) {
+    if (Vh > V) throw std::invalid_argument("heldout_likelihood: corpus vocabulary exceeds the model's");
+    std::vector<double> gram(static_cast<std::size_t>(k) * k, 0.0);
+    for (int a = 0; a < k; ++a)
+        for (int b = 0; b < k; ++b) {
+            double s = 0;
+            for (int w = 0; w < V; ++w) s += Phi[static_cast<std::size_t>(w) * k + a] * Phi[static_cast<std::size_t>(w) * k + b];
+            gram[static_cast<std::size_t>(b) * k + a] = s;
+        }
+    std::vector<double> ev(k), evec(static_cast<std::size_t>(k) * k);
+    sym_eigen_jacobi(k, gram.data(), ev.data(), evec.data());
+    double lips = -std::numeric_limits<double>::infinity();
+    for (double e : ev) lips = std::max(lips, e);
+    const double step = lips > 0 ? 1.0 / lips : 1.0;
+    long long floored = 0, used = 0;
+    double total = 0;
+    for (long long d = 0; d < D; ++d) {
+        long long tot = 0;
+        for (long long q = doc_ptr[d]; q < doc_ptr[d + 1]; ++q) tot += count[q];
+        if (tot < 1) continue;
+        ++used;
+        std::vector<double> pi(k, 1.0 / k);
+        if (k == 1) {
+            pi.assign(1, 1.0);
+        } else {
+            std::vector<double> phi_tw(k, 0.0), g(k), nx(k);
+            const double inv_m = 1.0 / static_cast<double>(tot);
+            for (long long q = doc_ptr[d]; q < doc_ptr[d + 1]; ++q)
+                for (int a = 0; a < k; ++a) phi_tw[a] += (inv_m * count[q]) * Phi[static_cast<std::size_t>(word[q]) * k + a];
+            for (int it = 0; it < 500; ++it) {
+                for (int a = 0; a < k; ++a) {
+                    double s = 0;
+                    for (int b = 0; b < k; ++b) s += gram[static_cast<std::size_t>(b) * k + a] * pi[b];
+                    g[a] = pi[a] - step * (s - phi_tw[a]);
+                }
+                nx = project_to_simplex(g.data(), k);
+                double moved = 0;
+                for (int a = 0; a < k; ++a) moved += (nx[a] - pi[a]) * (nx[a] - pi[a]);
+                pi.swap(nx);
+                if (std::sqrt(moved) <= 1e-8) break;
+            }
+        }
+        double ll = 0;
+        for (long long q = doc_ptr[d]; q < doc_ptr[d + 1]; ++q) {
+            double p = 0;
+            for (int a = 0; a < k; ++a) p += Phi[static_cast<std::size_t>(word[q]) * k + a] * pi[a];
+            if (p < 1e-12) {
+                p = 1e-12;
+                ++floored;
+            }
+            ll += count[q] * std::log(p);
+        }
+        total += ll / static_cast<double>(tot);
+    }
+    if (floored_out) *floored_out = floored;
+    if (used == 0) throw NumericalError("heldout_likelihood: empty held-out corpus");
+    return total / static_cast<double>(used);
+}
+
 void fourier_sketch(const SymRep& rep, std::uint32_t b, const double* v, int k, cvec& out) {
     out.assign(b, {0.0, 0.0});
     for (int i = 0; i < k; ++i) out[rep.bucket1[i]] += root4(rep.sexp[i]) * v[i];
@@ -1422,6 +1530,14 @@ int orc_sym_cached_transform(void* h, int m, double* out) {
 int orc_sym_rtpm(void* h, int k, int L, int T, std::uint64_t seed, double tol, const double* inits,
                  double* lambda, double* V, int* best_taus) {
     return guard([&] { robust_tpm_fast(*static_cast<SymSet*>(h), k, L, T, seed, tol, inits, lambda, V, best_taus); });
+}
+int orc_lda_recover_params(int V, int k, const double* lambda, const double* A, const double* unwhiten,
+                           double alpha0, double* Phi, double* alpha) {
+    return guard([&] { lda_recover_params(V, k, lambda, A, unwhiten, alpha0, Phi, alpha); });
+}
+int orc_lda_heldout_likelihood(int V, int k, const double* Phi, int Vh, long long D, const long long* doc_ptr,
+                               const int* word, const int* count, double* ll, long long* floored) {
+    return guard([&] { *ll = lda_heldout_likelihood(V, k, Phi, Vh, D, doc_ptr, word, count, floored); });
 }
 int orc_lda_sketch_whitened_m3(void* h, int V, int D, const long long* doc_ptr, const int* word,
                                const int* count, const double* W, double alpha0, long long* used,

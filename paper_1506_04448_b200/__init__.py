@@ -929,8 +929,9 @@ class LdaModel:
         return float(self.alpha.sum())
 
 
-def recover_params(dec: "CpDecomposition", wm: WhiteningMap, alpha0: float) -> LdaModel:
-    """lda.cpp:228-248 (host math)."""
+def recover_params(dec: "CpDecomposition", wm: WhiteningMap, alpha0: float, ctx: Context | None = None) -> LdaModel:
+    """lda.cpp:228-248 on the device (topic vectors and their simplex projections)."""
+    ctx = ctx or default_context()
     A = _f64(dec.A)
     k = A.shape[1]
     if A.shape[0] != wm.W.shape[1]:
@@ -938,17 +939,18 @@ def recover_params(dec: "CpDecomposition", wm: WhiteningMap, alpha0: float) -> L
     lam = _f64(dec.lambda_)
     V = wm.unwhiten.shape[0]
     Phi, alpha = np.empty((V, k)), np.empty(k)
-    check(lib.skc_lda_recover_params(V, k, _dp(lam), _dp(A), _dp(_f64(wm.unwhiten)), float(alpha0), _dp(Phi),
-                                     _dp(alpha)))
+    check(lib.skc_lda_recover_params(ctx.handle, V, k, _dp(lam), _dp(A), _dp(_f64(wm.unwhiten)), float(alpha0),
+                                     _dp(Phi), _dp(alpha)))
     return LdaModel(Phi, alpha)
 
 
-def heldout_likelihood(model: LdaModel, V_held: int, doc_ptr, word, count):
-    """lda.cpp:273-320 -> (mean per-word log-likelihood, floored word count)."""
+def heldout_likelihood(model: LdaModel, V_held: int, doc_ptr, word, count, ctx: Context | None = None):
+    """lda.cpp:273-320 on the device -> (mean per-word log-likelihood, floored word count)."""
+    ctx = ctx or default_context()
     Phi = _f64(model.Phi)
     keep, (D, dpp, wdp, ctp) = _corpus_args(doc_ptr, word, count)
     ll, fl = C.c_double(), C.c_longlong()
-    check(lib.skc_lda_heldout_likelihood(Phi.shape[0], Phi.shape[1], _dp(Phi), int(V_held), D, dpp, wdp, ctp,
+    check(lib.skc_lda_heldout_likelihood(ctx.handle, Phi.shape[0], Phi.shape[1], _dp(Phi), int(V_held), D, dpp, wdp, ctp,
                                          C.byref(ll), C.byref(fl)))
     return ll.value, fl.value
 

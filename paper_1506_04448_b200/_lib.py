@@ -100,8 +100,8 @@ SIGNATURES = {
     "skc_lda_m2_apply": (c_int, [p_void, c_int, c_ll, p_ll, p_int, p_int, c_double, c_int, p_double, p_double]),
     "skc_lda_whiten_corpus": (c_int, [p_void, c_int, c_ll, p_ll, p_int, p_int, c_double, c_int, c_int, c_int, c_u64,
                                       p_double, p_double, p_double]),
-    "skc_lda_recover_params": (c_int, [c_int, c_int, p_double, p_double, p_double, c_double, p_double, p_double]),
-    "skc_lda_heldout_likelihood": (c_int, [c_int, c_int, p_double, c_int, c_ll, p_ll, p_int, p_int, p_double, p_ll]),
+    "skc_lda_recover_params": (c_int, [p_void, c_int, c_int, p_double, p_double, p_double, c_double, p_double, p_double]),
+    "skc_lda_heldout_likelihood": (c_int, [p_void, c_int, c_int, p_double, c_int, c_ll, p_ll, p_int, p_int, p_double, p_ll]),
     "skc_lda_whiten_dense": (c_int, [p_void, c_int, p_double, c_int, c_int, c_int, c_u64, p_double, p_double,
                                      p_double]),
     "skc_sym_aux_sketches": (c_int, [p_void, c_int, p_double, p_double, p_double, p_double]),

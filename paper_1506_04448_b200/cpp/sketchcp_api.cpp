@@ -717,7 +717,7 @@ LdaModel recover_params(const CpDecomposition& D, const WhiteningMap& wm, double
         for (int j = 0; j < r; ++j) U[static_cast<std::size_t>(w) * r + j] = wm.unwhiten(w, j);
     LdaModel m;
     m.alpha.resize(k);
-    check(skc_lda_recover_params(V, k, D.lambda.data(), A.data(), U.data(), alpha0, Phi.data(), m.alpha.data()));
+    check(skc_lda_recover_params(context(), V, k, D.lambda.data(), A.data(), U.data(), alpha0, Phi.data(), m.alpha.data()));
     m.Phi.resize(V, k);
     for (int w = 0; w < V; ++w)
         for (int j = 0; j < k; ++j) m.Phi(w, j) = Phi[static_cast<std::size_t>(w) * k + j];
@@ -729,7 +729,7 @@ Eigen::VectorXd project_to_simplex(const Eigen::VectorXd& y) {
     const int n = static_cast<int>(y.size());
     double one = 1.0, a = 1.0, alpha = 0.0;
     Eigen::VectorXd out(n);
-    check(skc_lda_recover_params(n, 1, &one, &a, y.data(), 0.0, out.data(), &alpha));
+    check(skc_lda_recover_params(context(), n, 1, &one, &a, y.data(), 0.0, out.data(), &alpha));
     return out;
 }
 
@@ -741,7 +741,7 @@ double heldout_likelihood(const LdaModel& m, const Corpus& held, long long* floo
         for (int j = 0; j < k; ++j) Phi[static_cast<std::size_t>(w) * k + j] = m.Phi(w, j);
     double ll = 0.0;
     long long fl = 0;
-    check(skc_lda_heldout_likelihood(V, k, Phi.data(), held.V, csr.D(), csr.doc_ptr.data(), csr.word.data(),
+    check(skc_lda_heldout_likelihood(context(), V, k, Phi.data(), held.V, csr.D(), csr.doc_ptr.data(), csr.word.data(),
                                      csr.count.data(), &ll, &fl));
     if (floored_words) *floored_words = fl;
     return ll;

@@ -444,9 +444,10 @@ int skc_lda_whiten_dense(skc_context* ctx, int V, const double* m2, int k, int o
 }
 
 // lda.cpp:228-248: topics and prior from the whitened CP decomposition (host math, O(V k)).
-int skc_lda_recover_params(int V, int k, const double* lambda, const double* A, const double* unwhiten, double alpha0,
-                           double* Phi, double* alpha) {
+int skc_lda_recover_params(skc_context* ctx, int V, int k, const double* lambda, const double* A,
+                           const double* unwhiten, double alpha0, double* Phi, double* alpha) {
     return guard([&] {
+        check_vec(ctx, "context");
         require(k >= 1, "recover_params: empty decomposition");
         check_vec(lambda, "recover_params: lambda");
         check_vec(A, "recover_params: A");
@@ -454,93 +455,79 @@ int skc_lda_recover_params(int V, int k, const double* lambda, const double* A, 
         check_vec(Phi, "recover_params: Phi");
         check_vec(alpha, "recover_params: alpha");
         require(V >= 1, "recover_params: decomposition/whitening rank mismatch");
-        std::vector<double> mu(V);
-        for (int i = 0; i < k; ++i) {
+        for (int i = 0; i < k; ++i) {  // lda.cpp:236-241
             const double lam = lambda[i];
             if (lam == 0.0) fail(kNumericalError, "recover_params: zero eigenvalue at component " + std::to_string(i + 1));
             alpha[i] = 4.0 * alpha0 * (alpha0 + 1.0) / ((alpha0 + 2.0) * (alpha0 + 2.0) * lam * lam);
-            for (int w = 0; w < V; ++w) {  // mu = 0.5 (a0 + 2) lam * unwhiten A[:, i]
-                double s = 0.0;
-                for (int c = 0; c < k; ++c) s += unwhiten[static_cast<size_t>(w) * k + c] * A[static_cast<size_t>(c) * k + i];
-                mu[w] = 0.5 * (alpha0 + 2.0) * lam * s;
-            }
-            const std::vector<double> ph = project_to_simplex(mu.data(), V);
-            for (int w = 0; w < V; ++w) Phi[static_cast<size_t>(w) * k + i] = ph[w];
         }
+        ctx->use();
+        DevBuf<double> dl, dA, dU, mu, dP;
+        dl.upload(lambda, static_cast<size_t>(k), ctx->stream);
+        dA.upload(A, static_cast<size_t>(k) * k, ctx->stream);
+        dU.upload(unwhiten, static_cast<size_t>(V) * k, ctx->stream);
+        mu.alloc(static_cast<size_t>(V) * k);
+        dP.alloc(static_cast<size_t>(V) * k);
+        launch_lda_recover_params(ctx->stream, V, k, dl.p, dA.p, dU.p, alpha0, mu.p, dP.p);
+        ctx->check_launch();
+        CK(cudaMemcpyAsync(Phi, dP.p, sizeof(double) * V * k, cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->sync();
     });
 }
 
-// lda.cpp:273-320: mean per-document held-out log-likelihood, mixtures by simplex-
-// projected gradient (500 steps, stop at |step| <= 1e-8). Documents in parallel
-// (each is independent; the final sum runs in document order).
-int skc_lda_heldout_likelihood(int V, int k, const double* Phi, int Vh, long long D, const long long* doc_ptr,
-                               const int* word, const int* count, double* ll_out, long long* floored_out) {
+// lda.cpp:273-320: mean per-document held-out log-likelihood; the mixtures by projected
+// gradient on the device (one warp per document, skc_lda_post.cu); the step from the
+// largest eigenvalue of the k x k Gram (host Jacobi); the sum in document order.
+int skc_lda_heldout_likelihood(skc_context* ctx, int V, int k, const double* Phi, int Vh, long long D,
+                               const long long* doc_ptr, const int* word, const int* count, double* ll_out,
+                               long long* floored_out) {
     return guard([&] {
+        check_vec(ctx, "context");
         check_vec(Phi, "heldout_likelihood: Phi");
         check_vec(doc_ptr, "heldout_likelihood: doc_ptr");
         check_vec(ll_out, "heldout_likelihood: out");
         require(Vh <= V, "heldout_likelihood: corpus vocabulary exceeds the model's");
-        std::vector<double> gram(static_cast<size_t>(k) * k, 0.0);
-        for (int a = 0; a < k; ++a)
-            for (int b = 0; b < k; ++b) {
-                double s = 0.0;
-                for (int w = 0; w < V; ++w) s += Phi[static_cast<size_t>(w) * k + a] * Phi[static_cast<size_t>(w) * k + b];
-                gram[static_cast<size_t>(b) * k + a] = s;
-            }
+        require(k >= 1 && k <= 128, "heldout_likelihood: the device path supports k <= 128");
+        require(D >= 0 && doc_ptr[0] == 0, "heldout_likelihood: doc_ptr must start at 0");
+        const long long nnz = doc_ptr[D];
+        for (long long q = 0; q < nnz; ++q)
+            require(word[q] >= 0 && word[q] < Vh, "heldout_likelihood: word index out of range");
+        ctx->use();
+        DevBuf<double> dP, G, per;
+        DevBuf<long long> dptr, fl;
+        DevBuf<int> dw, dc;
+        dP.upload(Phi, static_cast<size_t>(V) * k, ctx->stream);
+        G.alloc(static_cast<size_t>(k) * k);
+        launch_phi_gram(ctx->stream, V, k, dP.p, G.p);
+        std::vector<double> gram(static_cast<size_t>(k) * k);
+        CK(cudaMemcpyAsync(gram.data(), G.p, sizeof(double) * k * k, cudaMemcpyDeviceToHost, ctx->stream));
+        dptr.upload(doc_ptr, static_cast<size_t>(D) + 1, ctx->stream);
+        dw.upload(word, static_cast<size_t>(std::max<long long>(nnz, 1)), ctx->stream);
+        dc.upload(count, static_cast<size_t>(std::max<long long>(nnz, 1)), ctx->stream);
+        per.alloc(static_cast<size_t>(std::max<long long>(D, 1)));
+        fl.alloc(static_cast<size_t>(std::max<long long>(D, 1)));
+        ctx->sync();
         std::vector<double> ev, U;
         sym_eigen_host(k, gram, ev, U);
         const double lips = ev.empty() ? 0.0 : ev.back();
         const double step = lips > 0 ? 1.0 / lips : 1.0;
-        std::vector<double> per(static_cast<size_t>(std::max<long long>(D, 1)), 0.0);
-        std::vector<long long> fl(static_cast<size_t>(std::max<long long>(D, 1)), 0);
-        std::vector<char> used(static_cast<size_t>(std::max<long long>(D, 1)), 0);
-#pragma omp parallel for schedule(dynamic, 16)
-        for (long long d = 0; d < D; ++d) {
-            long long tot = 0;
-            for (long long q = doc_ptr[d]; q < doc_ptr[d + 1]; ++q) tot += count[q];
-            if (tot < 1) continue;
-            used[d] = 1;
-            std::vector<double> pi(k, 1.0 / k);
-            if (k > 1) {
-                std::vector<double> phi_tw(k, 0.0), grad(k), next(k);
-                const double inv_m = 1.0 / static_cast<double>(tot);
-                for (long long q = doc_ptr[d]; q < doc_ptr[d + 1]; ++q)
-                    for (int a = 0; a < k; ++a)
-                        phi_tw[a] += (inv_m * count[q]) * Phi[static_cast<size_t>(word[q]) * k + a];
-                for (int it = 0; it < 500; ++it) {
-                    for (int a = 0; a < k; ++a) {
-                        double s = 0.0;
-                        for (int b = 0; b < k; ++b) s += gram[static_cast<size_t>(b) * k + a] * pi[b];
-                        grad[a] = pi[a] - step * (s - phi_tw[a]);
-                    }
-                    next = project_to_simplex(grad.data(), k);
-                    double moved = 0.0;
-                    for (int a = 0; a < k; ++a) moved += (next[a] - pi[a]) * (next[a] - pi[a]);
-                    pi.swap(next);
-                    if (std::sqrt(moved) <= 1e-8) break;
-                }
-            } else {
-                pi.assign(1, 1.0);
-            }
-            double ll = 0.0;
-            for (long long q = doc_ptr[d]; q < doc_ptr[d + 1]; ++q) {
-                double pw = 0.0;
-                for (int a = 0; a < k; ++a) pw += Phi[static_cast<size_t>(word[q]) * k + a] * pi[a];
-                if (pw < 1e-12) {
-                    pw = 1e-12;
-                    ++fl[d];
-                }
-                ll += count[q] * std::log(pw);
-            }
-            per[d] = ll / static_cast<double>(tot);
+        if (D > 0) {
+            launch_lda_heldout(ctx->stream, k, D, dptr.p, dw.p, dc.p, dP.p, G.p, step, per.p, fl.p);
+            ctx->check_launch();
         }
+        std::vector<double> hp(static_cast<size_t>(std::max<long long>(D, 1)));
+        std::vector<long long> hf(static_cast<size_t>(std::max<long long>(D, 1)));
+        if (D > 0) {
+            CK(cudaMemcpyAsync(hp.data(), per.p, sizeof(double) * D, cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaMemcpyAsync(hf.data(), fl.p, sizeof(long long) * D, cudaMemcpyDeviceToHost, ctx->stream));
+        }
+        ctx->sync();
         double total = 0.0;
         long long nused = 0, floored = 0;
         for (long long d = 0; d < D; ++d)
-            if (used[d]) {
-                total += per[d];
+            if (!std::isnan(hp[d])) {
+                total += hp[d];
                 ++nused;
-                floored += fl[d];
+                floored += hf[d];
             }
         if (floored_out) *floored_out = floored;
         if (nused == 0) fail(kNumericalError, "heldout_likelihood: empty held-out corpus");

@@ -190,6 +190,12 @@ void launch_sym_aux(cudaStream_t st, const SymView& v, int m, const double* u, d
 void launch_rank1_trunc_product(cudaStream_t st, const double2* spec2, long long len, double2* acc);
 void launch_add_third(cudaStream_t st, const double2* s3, std::uint32_t b, double2* out);
 
+// LDA recover_params / heldout_likelihood (skc_lda_post.cu)
+void launch_lda_recover_params(cudaStream_t st, int V, int k, const double* lambda, const double* A,
+                               const double* unwhiten, double alpha0, double* mu, double* Phi);
+void launch_phi_gram(cudaStream_t st, int V, int k, const double* Phi, double* G);
+bool launch_lda_heldout(cudaStream_t st, int k, long long D, const long long* doc_ptr, const int* word, const int* count,
+                        const double* Phi, const double* G, double step, double* per, long long* floored);
 // LDA whitened third moment (skc_lda.cu)
 void launch_lda_docs(cudaStream_t st, int k, long long D, const long long* doc_ptr, const int* word, const int* count,
                      const double* W, double alpha0, double* P, double* s1, double* s2, long long* total);

@@ -53,6 +53,9 @@ def _setup(L):
         "orc_gen_planted_slice": (C.c_int, [C.c_int, C.c_int, C.c_double, C.c_uint64, C.c_int, C.c_int, C.c_int, vp,
                                             d_p, d_p]),
         "orc_rng_u64": (None, [C.c_uint64, C.c_int, u64_p]),
+        "orc_lda_recover_params": (C.c_int, [C.c_int, C.c_int, d_p, d_p, d_p, C.c_double, d_p, d_p]),
+        "orc_lda_heldout_likelihood": (C.c_int, [C.c_int, C.c_int, d_p, C.c_int, C.c_longlong, ll_p, i_p, i_p, d_p,
+                                                 ll_p]),
         "orc_rng_gaussian": (None, [C.c_uint64, C.c_int, d_p]),
         "orc_rng_unit_sphere": (None, [C.c_uint64, C.c_int, d_p]),
         "orc_polyhash_from_seed": (C.c_int, [C.c_int, C.c_uint32, C.c_uint64, u64_p]),
@@ -434,3 +437,23 @@ def greedy_match(rec, truth):
     out = np.empty((r, 4))
     _chk(lib().orc_greedy_match(dp(Rc), r, dp(Gc), g, n, dp(out)))
     return out
+
+
+def lda_recover_params(V, k, lam, A, unwhiten, alpha0):
+    """lda.cpp:228-248 restated (sort-based simplex projection). A k x k, column i = component."""
+    Phi, alpha = np.empty((V, k)), np.empty(k)
+    _chk(lib().orc_lda_recover_params(V, k, dp(f64(lam)), dp(f64(A)), dp(f64(unwhiten)), float(alpha0), dp(Phi),
+                                      dp(alpha)))
+    return Phi, alpha
+
+
+def lda_heldout_likelihood(Phi, Vh, doc_ptr, word, count):
+    """lda.cpp:273-320 restated (documents in order)."""
+    V, k = Phi.shape
+    dpn = np.ascontiguousarray(doc_ptr, dtype=np.int64)
+    wd = np.ascontiguousarray(word, dtype=np.int32)
+    ct = np.ascontiguousarray(count, dtype=np.int32)
+    ll, fl = C.c_double(), C.c_longlong()
+    _chk(lib().orc_lda_heldout_likelihood(V, k, dp(f64(Phi)), int(Vh), dpn.size - 1, dpn.ctypes.data_as(ll_p),
+                                          wd.ctypes.data_as(i_p), ct.ctypes.data_as(i_p), C.byref(ll), C.byref(fl)))
+    return ll.value, fl.value

@@ -909,3 +909,40 @@ def test_dense_pinned_pipelined_build_fp32(gpu_ctx, n):
     d.accumulate_dense(torch.from_numpy(T).cuda(), assume_symmetric=True)
     assert rel_per_replicate(s.data(), ref.data()) <= 1e-6
     assert rel_per_replicate(s.data(), d.data()) <= 1e-6
+
+
+# ---------------------------------------------------------------- LDA recover_params / heldout (§8f rank 4)
+def test_lda_recover_params_matches_oracle(gpu_ctx):
+    """recover_params (lda.cpp:228-248) on the device -- the V x k x k product and the
+    simplex projection by bisection -- against the oracle's sort-based projection, at the
+    config-4 vocabulary (V=50000) with k=100."""
+    rng = np.random.default_rng(7)
+    V, k, alpha0 = 50000, 100, 1.0
+    lam = rng.uniform(0.5, 2.0, size=k)
+    A = np.linalg.qr(rng.normal(size=(k, k)))[0]
+    Uw = rng.normal(size=(V, k)) * 1e-3
+    Uw[rng.integers(0, V, size=300)] += 0.05  # a few heavy words per component
+    wm = skb().WhiteningMap(np.zeros((V, k)), Uw, np.ones(k))
+    m = skb().recover_params(skb().CpDecomposition.symmetric_of(lam, A), wm, alpha0, ctx=gpu_ctx)
+    Po, ao = O.lda_recover_params(V, k, lam, A, Uw, alpha0)
+    assert np.max(np.abs(m.Phi - Po)) <= 1e-12
+    assert np.allclose(m.Phi.sum(axis=0), 1.0, atol=1e-12)
+    assert np.array_equal(m.alpha, ao)
+    with pytest.raises(skb().NumericalError, match="zero eigenvalue at component 2"):
+        skb().recover_params(skb().CpDecomposition.symmetric_of(np.r_[1.0, 0.0, np.ones(k - 2)], A), wm, alpha0,
+                             ctx=gpu_ctx)
+
+
+@pytest.mark.parametrize("k", [1, 3, 40, 100])
+def test_lda_heldout_likelihood_matches_oracle(gpu_ctx, k):
+    """heldout_likelihood (lda.cpp:273-320): one warp per document on the device against
+    the oracle's sequential documents (500 projected-gradient steps each)."""
+    from lda_fixtures import synthetic_corpus
+
+    V = 400
+    doc_ptr, word, count, _ = synthetic_corpus(V=V, k=max(k, 2), D=300, mean_len=40, seed=11)
+    Phi = np.random.default_rng(5).dirichlet(np.full(V, 0.3), size=k).T
+    ll, fl = skb().heldout_likelihood(skb().LdaModel(Phi, np.ones(k)), V, doc_ptr, word, count, ctx=gpu_ctx)
+    llo, flo = O.lda_heldout_likelihood(Phi, V, doc_ptr, word, count)
+    assert abs(ll - llo) <= 1e-9 * abs(llo)
+    assert fl == flo

@@ -94,7 +94,9 @@ def test_no_gpu_means_loud_failure():
         skb.Context(0)
 
 
-# ---- LDA recover_params / heldout_likelihood (lda.cpp:228-320): host math, no GPU -------
+# ---- LDA recover_params / heldout_likelihood (lda.cpp:228-320): the oracle pinned to an --
+# independent numpy restatement (the device path is checked against the oracle in
+# tests/test_gpu_parity.py)
 def _np_project_to_simplex(y):
     u = np.sort(y)[::-1]
     css = np.cumsum(u)
@@ -105,33 +107,28 @@ def _np_project_to_simplex(y):
     return np.maximum(y - t[ok[-1]], 0.0)
 
 
-def test_lda_recover_params_matches_restatement():
-    import paper_1506_04448_b200 as skb
-
+def test_oracle_lda_recover_params_matches_restatement():
     rng = np.random.default_rng(1)
     V, k, alpha0 = 30, 4, 0.8
     lam = rng.uniform(0.5, 2.0, size=k)
     A = np.linalg.qr(rng.normal(size=(k, k)))[0]
     Uw = rng.normal(size=(V, k))
-    wm = skb.WhiteningMap(np.zeros((V, k)), Uw, np.ones(k))
-    dec = skb.CpDecomposition.symmetric_of(lam, A)
-    m = skb.recover_params(dec, wm, alpha0)
+    Phi, alpha = O.lda_recover_params(V, k, lam, A, Uw, alpha0)
     for i in range(k):
         mu = 0.5 * (alpha0 + 2.0) * lam[i] * (Uw @ A[:, i])
-        assert np.allclose(m.Phi[:, i], _np_project_to_simplex(mu), rtol=0, atol=1e-14)
-        assert np.isclose(m.alpha[i], 4 * alpha0 * (alpha0 + 1) / ((alpha0 + 2) ** 2 * lam[i] ** 2), rtol=1e-15)
-    with pytest.raises(skb.NumericalError, match="zero eigenvalue at component 2"):
-        skb.recover_params(skb.CpDecomposition.symmetric_of(np.array([1.0, 0.0, 1.0, 1.0]), A), wm, alpha0)
+        assert np.allclose(Phi[:, i], _np_project_to_simplex(mu), rtol=0, atol=1e-14)
+        assert np.isclose(alpha[i], 4 * alpha0 * (alpha0 + 1) / ((alpha0 + 2) ** 2 * lam[i] ** 2), rtol=1e-15)
+    with pytest.raises(O.OracleError, match="zero eigenvalue at component 2"):
+        O.lda_recover_params(V, k, np.array([1.0, 0.0, 1.0, 1.0]), A, Uw, alpha0)
 
 
-def test_lda_heldout_likelihood_matches_restatement():
-    import paper_1506_04448_b200 as skb
+def test_oracle_lda_heldout_likelihood_matches_restatement():
     from lda_fixtures import synthetic_corpus
 
     V, k = 25, 3
     doc_ptr, word, count, _ = synthetic_corpus(V=V, k=k, D=30, mean_len=10, seed=8)
     Phi = np.random.default_rng(3).dirichlet(np.full(V, 0.5), size=k).T
-    ll, fl = skb.heldout_likelihood(skb.LdaModel(Phi, np.ones(k)), V, doc_ptr, word, count)
+    ll, fl = O.lda_heldout_likelihood(Phi, V, doc_ptr, word, count)
     gram = Phi.T @ Phi
     step = 1.0 / np.linalg.eigvalsh(gram).max()
     tot_ll, used, floored = 0.0, 0, 0
