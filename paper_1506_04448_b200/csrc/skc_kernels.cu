@@ -969,15 +969,58 @@ __global__ void __launch_bounds__(kFftThreads, SKC_FFT_MINB)
             idx[q] = e.x;
         }
     }
-    // the next sample's row is copied into the other half of xs (cp.async) while the
-    // current one is transformed
+    // The next sample's row is copied into the other half of xs while the current one is
+    // transformed: one bulk (TMA) copy of the whole row, completing on an mbarrier per half,
+    // when rows are 16-byte aligned (n even, X aligned); else per-element 8-byte cp.async.
+    __shared__ __align__(8) unsigned long long mbar[2];
+    const bool bulk = SCR && ((n & 1) == 0) && ((reinterpret_cast<std::uintptr_t>(X) & 15) == 0);
+    const std::uint32_t mb0 = static_cast<std::uint32_t>(__cvta_generic_to_shared(&mbar[0]));
+    if (bulk && threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(mb0) : "memory");
+        asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(mb0 + 8u) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
     auto prefetch = [&](long long smp) {
         if (!SCR || smp >= s1) return;
         const double* src = X + (size_t)smp * n;
-        double* dst = xs + (size_t)(smp & 1) * n;
+        const int half = static_cast<int>((smp - s0) & 1);
+        double* dst = xs + (size_t)half * n;
+        if (bulk) {
+            if (threadIdx.x == 0) {
+                const std::uint32_t bytes = static_cast<std::uint32_t>(n) * 8u;
+                const std::uint32_t mb = mb0 + 8u * static_cast<std::uint32_t>(half);
+                const std::uint32_t da = static_cast<std::uint32_t>(__cvta_generic_to_shared(dst));
+                // the half was last read by generic loads (ordered by the loop's barriers)
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(da),
+                    "l"(src), "r"(bytes), "r"(mb)
+                    : "memory");
+            }
+            return;
+        }
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
             const std::uint32_t da = static_cast<std::uint32_t>(__cvta_generic_to_shared(dst + i));
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(da), "l"(src + i) : "memory");
+        }
+    };
+    // sample smp's row has landed in its half (parity of that half's use count)
+    auto wait_row = [&](long long smp) {
+        if (bulk) {
+            const long long t = smp - s0;
+            const std::uint32_t mb = mb0 + 8u * static_cast<std::uint32_t>(t & 1);
+            const std::uint32_t par = static_cast<std::uint32_t>((t >> 1) & 1);
+            std::uint32_t done = 0;
+            while (!done)
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                    : "=r"(done)
+                    : "r"(mb), "r"(par)
+                    : "memory");
+        } else {
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
         }
     };
     prefetch(s0);
@@ -987,11 +1030,11 @@ __global__ void __launch_bounds__(kFftThreads, SKC_FFT_MINB)
         const double* x = X + (size_t)s * n;
         prefetch(s + 1);
         asm volatile("cp.async.commit_group;" ::: "memory");
-        asm volatile("cp.async.wait_group 1;" ::: "memory");  // this sample's row has landed
+        wait_row(s);  // this sample's row has landed
         __syncthreads();
         // A is all-zero here (initially, then re-zeroed by the accumulate pass below)
         if (SCR) {
-            const double* xr = xs + (size_t)(s & 1) * n;
+            const double* xr = xs + (size_t)((s - s0) & 1) * n;
             for (int q = threadIdx.x; q < n; q += blockDim.x) {
                 const std::uint32_t key = keys[q];
                 if (q > 0 && keys[q - 1] == key) continue;
