@@ -118,3 +118,31 @@ def test_ordinary_tensors_keep_the_single_scale_fast_path(gpu_ctx):
         s = skb().SymTensorSketchSet(n, 4096, 4, 3, gpu_ctx)
         s.accumulate_dense(torch.from_numpy(np.asarray(T)).cuda(), assume_symmetric=True)
     assert gpu_ctx.build_retries() == r0 and gpu_ctx.build_banded() == b0
+
+
+@pytest.mark.parametrize("n,b", [(20, 1024), (48, 4096)])
+def test_hdr_asym_per_bucket_error_vs_oracle(gpu_ctx, n, b):
+    """Asymmetric builds (sketch.cpp:173-193) with entries spanning 1e12: the small build
+    takes the contiguous-window kernel (fixed-point pre-pass, banded), the larger the
+    class-list kernel; every bucket within 1e-10 of its mass either way."""
+    B, seed = 4, 29
+    rng = np.random.default_rng(n)
+    T = rng.choice([-1.0, 1.0], size=(n, n, n)) * 10.0 ** rng.uniform(-12, 0, size=(n, n, n))
+    o = O.AsymSet(n, b, B, seed)
+    o.accumulate_dense(T)
+    A = np.zeros((B, b))
+    ii, jj, kk = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
+    for m in range(B):
+        bk = np.asarray(o.tables(m)[0], dtype=np.int64)
+        slot = (bk[0][ii] + bk[1][jj] + bk[2][kk]) % b
+        np.add.at(A[m], slot.ravel(), np.abs(T).ravel())
+    before = gpu_ctx.build_banded()
+    s = skb().AsymTensorSketchSet(n, b, B, seed, gpu_ctx)
+    s.accumulate_dense(T)
+    # thin buckets (~8 entries per slot at n=20) and heavy tails (at n=48, ~27 entries per
+    # slot but only ~2 of them carry the mass) go to bands
+    assert gpu_ctx.build_banded() == before + 1
+    got, ref = s.data(), o.data()
+    mask = A > 0
+    err = np.max(np.abs(got.real - ref.real)[mask] / A[mask])
+    assert err <= 1e-10, err
