@@ -79,8 +79,9 @@ int skc_context_stream(skc_context* ctx, void** stream_out);
  * entry point says otherwise. */
 int skc_context_wait_stream(skc_context* ctx, void* producer);
 /* Dense builds of fp32 tensors run with one 32-bit limb per sketch slot; a build whose
- * limb overflowed (>= 512 same-signed full-scale adds to one slot in one pass) is
- * discarded and repeated exactly with two limbs. Number of such repeats so far. */
+ * limb could overflow (a partial sum reached 2^30, i.e. ~2^8 same-signed full-scale adds
+ * to one slot in one pass) or whose entries need a finer scale is discarded and repeated
+ * exactly with two limbs. Number of such repeats so far. */
 int skc_context_build_retries(skc_context* ctx, long long* out);
 /* Dense builds redone in magnitude bands: tensors whose entries span more magnitudes than
  * one exact fixed-point scale resolves to ~2^-34 of each bucket (high dynamic range). */
