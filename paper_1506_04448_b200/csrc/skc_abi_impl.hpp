@@ -244,6 +244,20 @@ struct ProfScope {
 // ============================ sets ===============================================
 struct skc_sym_set {
     skc_context* ctx = nullptr;
+    // CUDA graphs of the RTPM power-step loop on this set, keyed by what the captured
+    // launches bake in besides the set's own buffers (shape, tolerance, context scratch)
+    struct RtpmGraph {
+        cudaGraphExec_t exec = nullptr;
+        std::uint64_t launches = 0, transforms = 0;
+    };
+    std::map<std::vector<std::uint64_t>, RtpmGraph> rtpm_graphs;
+    skc_sym_set() = default;
+    skc_sym_set(const skc_sym_set&) = delete;
+    skc_sym_set& operator=(const skc_sym_set&) = delete;
+    ~skc_sym_set() {
+        for (auto& g : rtpm_graphs)
+            if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
+    }
     int n = 0;
     std::uint32_t b = 2;
     int logb = 1;

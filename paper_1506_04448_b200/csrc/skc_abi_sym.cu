@@ -506,12 +506,9 @@ namespace skcabi {
 // ---- RTPM ----
 // Runs T power steps on L restarts resident at ctx->U (device) and the median vvv of
 // the finals into ctx->values. Degenerate flags accumulate in ctx->flags.
-void rtpm_restarts_device(skc_sym_set* s, int L, int T_iters, double tol) {
+static void rtpm_restarts_launches(skc_sym_set* s, int L, int T_iters, double tol) {
     skc_context* ctx = s->ctx;
-    s->ensure_fresh();
-    ctx->flags.alloc(static_cast<size_t>(L));
     CK(cudaMemsetAsync(ctx->flags.p, 0, sizeof(int) * L, ctx->stream));
-    ctx->part.alloc(static_cast<size_t>(L) * s->B * s->S * std::max(s->n, 3));
     const SymView v = s->view();
     for (int t = 0; t < T_iters; ++t) {
         {
@@ -519,15 +516,59 @@ void rtpm_restarts_device(skc_sym_set* s, int L, int T_iters, double tol) {
             launch_sym_contract(ctx->stream, v, ctx->U.p, L, 0, ctx->part.p);
         }
         SKC_PROF(ctx, "median");
-        ctx->values.alloc(static_cast<size_t>(L) * s->n);
         launch_median_rows(ctx->stream, ctx->part.p, L, s->B, s->S, s->n, nullptr, ctx->U.p, tol, ctx->flags.p,
                            ctx->values.p);
     }
-    ctx->check_launch();
     launch_sym_contract(ctx->stream, v, ctx->U.p, L, 1, ctx->part.p);
-    ctx->values.alloc(static_cast<size_t>(L));
     launch_sym_vvv_finish(ctx->stream, ctx->part.p, L, s->B, s->S, s->b, ctx->values.p);
-    ctx->check_launch();
+}
+void rtpm_restarts_device(skc_sym_set* s, int L, int T_iters, double tol) {
+    skc_context* ctx = s->ctx;
+    s->ensure_fresh();
+    ctx->flags.alloc(static_cast<size_t>(L));
+    ctx->part.alloc(static_cast<size_t>(L) * s->B * s->S * std::max(s->n, 3));
+    ctx->values.alloc(static_cast<size_t>(L) * s->n);
+    if (ctx->prof_on) {  // per-kernel event scopes: launch directly
+        rtpm_restarts_launches(s, L, T_iters, tol);
+        ctx->check_launch();
+        return;
+    }
+    // The T power steps and the selection values are one CUDA graph, captured once per
+    // (set, L, T, tol, buffers) and replayed per component: 2T + 3 launches per replay.
+    std::uint64_t tolbits;
+    std::memcpy(&tolbits, &tol, sizeof(tolbits));
+    const std::vector<std::uint64_t> key = {static_cast<std::uint64_t>(L),
+                                            static_cast<std::uint64_t>(T_iters), tolbits,
+                                            reinterpret_cast<std::uint64_t>(ctx->U.p),
+                                            reinterpret_cast<std::uint64_t>(ctx->part.p),
+                                            reinterpret_cast<std::uint64_t>(ctx->values.p),
+                                            reinterpret_cast<std::uint64_t>(ctx->flags.p),
+                                            reinterpret_cast<std::uint64_t>(s->spec.p),
+                                            reinterpret_cast<std::uint64_t>(s->data.p)};
+    auto it = s->rtpm_graphs.find(key);
+    if (it == s->rtpm_graphs.end()) {
+        // attributes and lazily built tables are set up by one direct run
+        rtpm_restarts_launches(s, L, T_iters, tol);
+        ctx->check_launch();
+        const std::uint64_t l0 = launch_count(), f0 = transform_units();
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        rtpm_restarts_launches(s, L, T_iters, tol);
+        CK(cudaStreamEndCapture(ctx->stream, &g));
+        skc_sym_set::RtpmGraph rg;
+        CK(cudaGraphInstantiate(&rg.exec, g, 0));
+        cudaGraphDestroy(g);
+        rg.launches = launch_count() - l0;
+        rg.transforms = transform_units() - f0;
+        if (s->rtpm_graphs.size() > 16) {  // bounded cache
+            for (auto& e : s->rtpm_graphs) cudaGraphExecDestroy(e.second.exec);
+            s->rtpm_graphs.clear();
+        }
+        s->rtpm_graphs[key] = rg;
+        return;  // the direct run above computed this call's results
+    }
+    CK(cudaGraphLaunch(it->second.exec, ctx->stream));
+    count_replay(it->second.launches, it->second.transforms);
 }
 void check_degenerate(skc_context* ctx, int L) {
     std::vector<int> f(L);

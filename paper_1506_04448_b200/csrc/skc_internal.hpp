@@ -57,6 +57,9 @@ struct AsymView {
 
 std::uint64_t launch_count();
 void count_launch();
+void count_replay(std::uint64_t launches, std::uint64_t transforms);
+std::uint64_t launch_count();
+std::uint64_t transform_units();
 std::uint64_t transform_units();          // local FFTs executed, in units of length-N transforms
 void count_transforms(std::uint64_t local_ffts, int S);  // accumulate S-split counts
 

@@ -61,6 +61,11 @@ std::uint64_t launch_count() { return g_launches.load(); }
 void count_launch() { g_launches.fetch_add(1); }
 std::uint64_t transform_units() { return g_transforms.load(); }
 void count_transforms(std::uint64_t local_ffts, int S) { g_transforms.fetch_add(local_ffts / (S > 0 ? S : 1)); }
+// replays of captured CUDA graphs count their kernels and transforms again
+void count_replay(std::uint64_t launches, std::uint64_t transforms) {
+    g_launches.fetch_add(launches);
+    g_transforms.fetch_add(transforms);
+}
 
 #define SKC_LAUNCHED() count_launch()
 
