@@ -69,6 +69,7 @@ int skc_context_destroy(skc_context* ctx) {
         if (ctx->cublas) cublasDestroy(ctx->cublas);
         if (ctx->comm) ncclCommDestroy(ctx->comm);
         if (ctx->host_ints) cudaFreeHost(ctx->host_ints);
+        if (ctx->host_dbl) cudaFreeHost(ctx->host_dbl);
         for (auto& r : ctx->prof) {
             cudaEventDestroy(r.a);
             cudaEventDestroy(r.b);

@@ -137,6 +137,18 @@ struct skc_context {
     DevBuf<double> prepass;
     DevBuf<int> ints;  // [0] scale exp, [1] nonfinite, [2] best tau, [3..] misc
     int* host_ints = nullptr;  // pinned host scratch for small synchronous readbacks (DMA, no staging)
+    double* host_dbl = nullptr;  // pinned host scratch for RTPM inits (grown on demand)
+    size_t host_dbl_n = 0;
+    double* pinned_doubles(size_t count) {
+        if (count > host_dbl_n) {
+            if (host_dbl) cudaFreeHost(host_dbl);
+            host_dbl = nullptr;
+            host_dbl_n = 0;
+            CK(cudaMallocHost(reinterpret_cast<void**>(&host_dbl), count * sizeof(double)));
+            host_dbl_n = count;
+        }
+        return host_dbl;
+    }
     int* pinned_ints() {
         if (!host_ints) CK(cudaMallocHost(reinterpret_cast<void**>(&host_ints), 16 * sizeof(int)));
         return host_ints;

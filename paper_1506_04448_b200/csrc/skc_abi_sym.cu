@@ -593,29 +593,33 @@ int skc_sym_rtpm(skc_sym_set* s, int k, int L, int T_iters, uint64_t seed, doubl
         skc_context* ctx = s->ctx;
         ctx->use();
         const int n = s->n;
-        std::vector<double> gen;
+        const size_t Ln = static_cast<size_t>(L) * n;
+        // inits Rng(derive_seed(seed, 0x31, c, tau)).unit_sphere(n) (decompose.cpp:96-97) in
+        // pinned double buffers: component c+1's are drawn on the host (restarts in
+        // parallel, each stream independent) while the device runs component c
+        double* pin[2] = {nullptr, nullptr};
         if (!inits) {
-            gen.resize(static_cast<size_t>(L) * n);
+            pin[0] = ctx->pinned_doubles(2 * Ln);
+            pin[1] = pin[0] + Ln;
         }
+        auto draw = [&](int c, double* dst) {
+#pragma omp parallel for schedule(static)
+            for (int t = 0; t < L; ++t) {
+                Rng rng(derive_seed(seed, seed_tag::kPowerInit, static_cast<std::uint64_t>(c), static_cast<std::uint64_t>(t)));
+                rng.unit_sphere(n, dst + static_cast<size_t>(t) * n);
+            }
+        };
+        if (!inits) draw(0, pin[0]);
         ctx->ints.alloc(16);
         ctx->dbl.alloc(4);
         ctx->X.alloc(static_cast<size_t>(n));
         for (int c = 0; c < k; ++c) {
-            const double* U0;
-            if (inits) {
-                U0 = inits + static_cast<size_t>(c) * L * n;
-            } else {
-                for (int t = 0; t < L; ++t) {
-                    Rng rng(derive_seed(seed, seed_tag::kPowerInit, static_cast<std::uint64_t>(c),
-                                        static_cast<std::uint64_t>(t)));
-                    rng.unit_sphere(n, gen.data() + static_cast<size_t>(t) * n);
-                }
-                U0 = gen.data();
-            }
-            ctx->U.upload(U0, static_cast<size_t>(L) * n, ctx->stream);
+            const double* U0 = inits ? inits + static_cast<size_t>(c) * Ln : pin[c & 1];
+            ctx->U.upload(U0, Ln, ctx->stream);
             rtpm_restarts_device(s, L, T_iters, tol);
             launch_argmax_first(ctx->stream, ctx->values.p, L, ctx->ints.p + 2, ctx->dbl.p);
             ctx->check_launch();
+            if (!inits && c + 1 < k) draw(c + 1, pin[(c + 1) & 1]);  // overlaps the device work
             int bt = 0;
             double lam = 0.0;
             CK(cudaMemcpyAsync(&bt, ctx->ints.p + 2, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));

@@ -538,14 +538,15 @@ __device__ int cta_scale_exp(const BuildArgs& a) {
             // the build with two limbs (flag 1) or in magnitude bands (flag 2).
             // Buckets are sums of ~c = entries_per_slot terms (Poisson). When they are thin
             // (c < 8: a bucket may be one or two entries) or the mass sits in few entries
-            // (N_eff = (sum)^2 / sum of squares; c N_eff / N < 16: some buckets likely hold
-            // none of the heavy entries), a bucket may hold only small entries, so the step is
-            // measured against the smallest nonzero one; otherwise against the mean.
+            // (N_eff = (sum)^2 / sum of squares; c N_eff / N < 4: some buckets likely hold
+            // none of the heavy entries; light tails have N_eff / N ~ 2/pi), a bucket may
+            // hold only small entries, so the step is measured against the smallest nonzero
+            // one; otherwise against the mean.
             int hdr = 0;
             if (acc > 0.0 && isfinite(acc) && isfinite(sq)) {
                 const double N = static_cast<double>(a.total_entries);
                 const double neff = (acc / sqrt(sq)) * (acc / sqrt(sq));
-                const bool thin = a.entries_per_slot < 8.0 || a.entries_per_slot * neff < 16.0 * N;
+                const bool thin = a.entries_per_slot < 8.0 || a.entries_per_slot * neff < 4.0 * N;
                 const double rho = thin ? ldexp(1.0, -F) / mn : ldexp(N, -F) / acc;
                 if (rho > a.rho_max) hdr = a.qbits < 50 ? 1 : 2;
             }

@@ -109,10 +109,13 @@ def test_hdr_fp32_goes_to_two_limbs_or_bands(gpu_ctx):
 
 
 def test_ordinary_tensors_keep_the_single_scale_fast_path(gpu_ctx):
-    """Gaussian data (the BASELINE generators) stay on one exact scale: no retry, no bands."""
+    """The BASELINE generators (planted rank + Gaussian noise) stay on one exact scale: no
+    retry, no bands -- config 0's shape (n=100, b=2^12: ~21 entries per slot) included."""
     import torch
 
     r0, b0 = gpu_ctx.build_retries(), gpu_ctx.build_banded()
+    T0, _, _ = skb().gen_planted_tensor(100, 10, 0.01, 11)
+    skb().SymTensorSketchSet(100, 1 << 12, 20, 5, gpu_ctx).accumulate_dense(T0, assume_symmetric=True)
     for n, dt in ((120, np.float64), (160, np.float32)):
         T, _, _ = skb().gen_planted_tensor(n, 5, 0.01, 7, dtype=dt)
         s = skb().SymTensorSketchSet(n, 4096, 4, 3, gpu_ctx)
