@@ -394,6 +394,7 @@ int skc_sym_rtpm_group(skc_sym_set* const* sets, int nsets, int k, int L, int T_
             if (inits) {
                 U0 = inits + static_cast<size_t>(c) * L * n;
             } else {  // Rng(derive_seed(seed, 0x31, c, tau)).unit_sphere(n) (decompose.cpp:96-97)
+#pragma omp parallel for schedule(static)
                 for (int t = 0; t < L; ++t) {
                     Rng rng(derive_seed(seed, seed_tag::kPowerInit, static_cast<std::uint64_t>(c),
                                         static_cast<std::uint64_t>(t)));
