@@ -563,7 +563,7 @@ double sym_vvv(SymWs& ws, const double* u) {
     const int n = s.n, B = s.B;
     const std::uint32_t b = s.b;
     std::vector<double> est(B);
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) if (!omp_in_parallel())
     for (int m = 0; m < B; ++m) {
         const auto& rep = s.reps[m];
         cvec f1(b, {0.0, 0.0}), f2(b, {0.0, 0.0});
@@ -600,7 +600,7 @@ void sym_ivv(SymWs& ws, const double* u, double* result) {
     const std::uint32_t b = s.b;
     std::vector<double> vals(static_cast<std::size_t>(B) * n);
     const double inv_b = 1.0 / static_cast<double>(b);
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) if (!omp_in_parallel())
     for (int m = 0; m < B; ++m) {
         const auto& rep = s.reps[m];
         cvec f1(b, {0.0, 0.0}), f2(b, {0.0, 0.0}), z1(b), z2(b);
@@ -658,8 +658,14 @@ void robust_tpm_fast(SymSet& s, int k, int L, int T_iters, std::uint64_t seed, d
     std::vector<double> out(n);
     for (int c = 0; c < k; ++c) {
         std::vector<std::vector<double>> finals(L);
+        // restarts are independent (decompose.cpp:93-104): run them on the threads (each
+        // contraction then runs serially, same arithmetic); a degenerate iterate throws at
+        // the lowest restart index, as the serial loop would
+        sym_ensure_fresh(ws);
+        std::vector<std::string> err(L);
+#pragma omp parallel for schedule(dynamic, 1)
         for (int tau = 0; tau < L; ++tau) {
-            std::vector<double> u;
+            std::vector<double> u, out(n);
             if (inits) {
                 u.assign(inits + (static_cast<std::size_t>(c) * L + tau) * n,
                          inits + (static_cast<std::size_t>(c) * L + tau + 1) * n);
@@ -667,17 +673,26 @@ void robust_tpm_fast(SymSet& s, int k, int L, int T_iters, std::uint64_t seed, d
                 Rng rng(derive_seed(seed, kPowerInit, c, tau));
                 u = rng.unit_sphere(n);
             }
-            for (int t = 0; t < T_iters; ++t) {
-                sym_ivv(ws, u.data(), out.data());
-                u = out;
-                normalized_or_throw(u, tol);
+            try {
+                for (int t = 0; t < T_iters; ++t) {
+                    sym_ivv(ws, u.data(), out.data());
+                    u = out;
+                    normalized_or_throw(u, tol);
+                }
+            } catch (const std::exception& e) {
+                err[tau] = e.what();
             }
             finals[tau] = u;
         }
+        for (int tau = 0; tau < L; ++tau)
+            if (!err[tau].empty()) throw DegenerateIterationError(err[tau]);
         double best = -std::numeric_limits<double>::infinity();
         int best_tau = 0;
+        std::vector<double> values(L);
+#pragma omp parallel for schedule(dynamic, 1)
+        for (int tau = 0; tau < L; ++tau) values[tau] = sym_vvv(ws, finals[tau].data());
         for (int tau = 0; tau < L; ++tau) {
-            double value = sym_vvv(ws, finals[tau].data());
+            double value = values[tau];
             if (value > best) {
                 best = value;
                 best_tau = tau;
@@ -1514,6 +1529,25 @@ int orc_sym_vvv(void* h, const double* u, double* out) {
         auto& s = *static_cast<SymSet*>(h);
         SymWs ws{&s, s.version - 1, {}};
         *out = sym_vvv(ws, u);
+    });
+}
+// L contractions against one cached spectrum, restarts on the threads (test helpers)
+int orc_sym_ivv_batch(void* h, int L, const double* U, double* out) {
+    return guard([&] {
+        auto& s = *static_cast<SymSet*>(h);
+        SymWs ws{&s, s.version - 1, {}};
+        sym_ensure_fresh(ws);
+#pragma omp parallel for schedule(dynamic, 1)
+        for (int l = 0; l < L; ++l) sym_ivv(ws, U + static_cast<std::size_t>(l) * s.n, out + static_cast<std::size_t>(l) * s.n);
+    });
+}
+int orc_sym_vvv_batch(void* h, int L, const double* U, double* out) {
+    return guard([&] {
+        auto& s = *static_cast<SymSet*>(h);
+        SymWs ws{&s, s.version - 1, {}};
+        sym_ensure_fresh(ws);
+#pragma omp parallel for schedule(dynamic, 1)
+        for (int l = 0; l < L; ++l) out[l] = sym_vvv(ws, U + static_cast<std::size_t>(l) * s.n);
     });
 }
 int orc_sym_cached_transform(void* h, int m, double* out) {

@@ -66,7 +66,6 @@ int skc_context_destroy(skc_context* ctx) {
         cudaSetDevice(ctx->device);
         cudaStreamSynchronize(ctx->stream);
         if (ctx->stream2) cudaStreamSynchronize(ctx->stream2);
-        if (ctx->cublas) cublasDestroy(ctx->cublas);
         if (ctx->comm) ncclCommDestroy(ctx->comm);
         if (ctx->host_ints) cudaFreeHost(ctx->host_ints);
         if (ctx->host_dbl) cudaFreeHost(ctx->host_dbl);

@@ -392,8 +392,6 @@ int skc_asym_als(skc_asym_set* s, int k, int max_iters, double tol, uint64_t see
         double* fac[3] = {F.p, F.p + nk, F.p + 2 * nk};
         s->ensure_fresh();
         ctx->part.alloc(static_cast<size_t>(k) * s->B * s->S * n);
-        cublasHandle_t hb = cublas_of(ctx);
-        const double one = 1.0, zero = 0.0;
         std::vector<double> g1(static_cast<size_t>(k) * k), g2(g1.size()), G(g1.size());
         std::vector<double> lambda(k, 1.0), lambda_prev(k, 1.0);  // s.lambda = Ones (decompose.cpp:129)
         int it = 0;
@@ -405,8 +403,8 @@ int skc_asym_als(skc_asym_set* s, int k, int max_iters, double tol, uint64_t see
                 launch_median_rows(ctx->stream, ctx->part.p, k, s->B, s->S, n, M.p, nullptr, 0.0, nullptr);
                 ctx->check_launch();
                 // G = (F1' F1) .* (F2' F2)
-                CB(cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, k, k, n, &one, fac[f1], n, fac[f1], n, &zero, G1.p, k));
-                CB(cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, k, k, n, &one, fac[f2], n, fac[f2], n, &zero, G2.p, k));
+                dgemm_cm(ctx, true, false, k, k, n, fac[f1], n, fac[f1], n, G1.p, k);
+                dgemm_cm(ctx, true, false, k, k, n, fac[f2], n, fac[f2], n, G2.p, k);
                 CK(cudaMemcpyAsync(g1.data(), G1.p, g1.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
                 CK(cudaMemcpyAsync(g2.data(), G2.p, g2.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
                 ctx->sync();
@@ -415,7 +413,7 @@ int skc_asym_als(skc_asym_set* s, int k, int max_iters, double tol, uint64_t see
                 CK(cudaMemcpyAsync(P.p, Pinv.data(), Pinv.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
                 // target = M * pinv(G); normalize_columns(target, prev, lambda)
                 CK(cudaMemcpyAsync(prev.p, fac[mode], nk * 8, cudaMemcpyDeviceToDevice, ctx->stream));
-                CB(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, n, k, k, &one, M.p, n, P.p, k, &zero, fac[mode], n));
+                dgemm_cm(ctx, false, false, n, k, k, M.p, n, P.p, k, fac[mode], n);
                 launch_normalize_columns(ctx->stream, n, k, fac[mode], prev.p, lam.p);
                 ctx->check_launch();
             }

@@ -2,7 +2,6 @@
 // device buffers, the context and the sketch-set objects behind the opaque handles of
 // include/sketchcp_b200.h. Not a public header.
 #pragma once
-#include <cublas_v2.h>
 #include <nccl.h>
 #include <cuda_runtime.h>
 #include <omp.h>
@@ -117,7 +116,7 @@ struct skc_context {
     cudaStream_t stream2 = nullptr;  // pipelined zero-copy builds: main pass of chunk c
     cudaEvent_t ev_q[5] = {};        // chunk c quantized / all chunks done
     cudaEvent_t ev_order = nullptr;  // skc_context_wait_stream
-    cublasHandle_t cublas = nullptr;  // LDA whitening block products (lazy)
+    DevBuf<double> gemm_ws;  // split-K partials of the block products (dgemm_cm)
     int sms = 148;
     int smem_optin = 227 * 1024;
     std::map<std::uint32_t, std::unique_ptr<DevBuf<double2>>> twiddles;
@@ -385,17 +384,15 @@ inline void validate_set_args(int n, std::uint32_t b, int B) {
 inline void check_vec(const void* p, const char* what) { require(p != nullptr, std::string(what) + ": null pointer"); }
 
 // ---- LDA moments and whitening (lda.cpp:88-143; kernels in skc_whiten.cu) ---------------
-#define CB(call)                                                                                      \
-    do {                                                                                              \
-        cublasStatus_t st_ = (call);                                                                  \
-        if (st_ != CUBLAS_STATUS_SUCCESS)                                                             \
-            fail(kCudaError, std::string("cuBLAS error ") + std::to_string(static_cast<int>(st_)) + " at " #call); \
-    } while (0)
-
-inline cublasHandle_t cublas_of(skc_context* ctx) {
-    if (!ctx->cublas) CB(cublasCreate(&ctx->cublas));
-    CB(cublasSetStream(ctx->cublas, ctx->stream));
-    return ctx->cublas;
+// Column-major DGEMM in cuBLAS's argument convention (alpha 1, beta 0), on the repo's own
+// kernel (skc_gemm.cu): C (m x n, ldc) = op(A) op(B), op(A) m x k, op(B) k x n.
+inline void dgemm_cm(skc_context* ctx, bool ta, bool tb, int m, int n, int k, const double* A, int lda,
+                     const double* B, int ldb, double* C, int ldc) {
+    const int z = k > 0 ? dgemm_slices(m, n, k, ctx->sms) : 1;
+    if (z > 1) ctx->gemm_ws.alloc(static_cast<size_t>(z) * m * n);
+    launch_dgemm(ctx->stream, ctx->sms, m, n, k, A, ta ? lda : 1, ta ? 1 : lda, B, tb ? ldb : 1, tb ? 1 : ldb, C, 1, ldc,
+                 ctx->gemm_ws.p);
+    ctx->check_launch();
 }
 
 // Corpus on the device: CSR (document-major) and its word-major transpose, per-document

@@ -101,15 +101,13 @@ struct OrthWork {
     DevBuf<double> G, Rinv, tmp;
 };
 void orthonormalize(skc_context* ctx, int V, int p, const double* Yd, double* Qd, OrthWork& w, Rng& rng) {
-    cublasHandle_t h = cublas_of(ctx);
-    const double one = 1.0, zero = 0.0;
     w.G.alloc(static_cast<size_t>(p) * p);
     w.Rinv.alloc(static_cast<size_t>(p) * p);
     w.tmp.alloc(static_cast<size_t>(V) * p);
     std::vector<double> G(static_cast<size_t>(p) * p), Ri(static_cast<size_t>(p) * p);
     const double* src = Yd;
     for (int pass = 0; pass < 2; ++pass) {
-        CB(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, p, p, V, &one, src, p, src, p, &zero, w.G.p, p));
+        dgemm_cm(ctx, false, true, p, p, V, src, p, src, p, w.G.p, p);
         CK(cudaMemcpyAsync(G.data(), w.G.p, G.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         ctx->sync();
         // Cholesky G = R^T R (R upper, col-major)
@@ -176,7 +174,7 @@ void orthonormalize(skc_context* ctx, int V, int p, const double* Yd, double* Qd
         CK(cudaMemcpyAsync(w.Rinv.p, Ri.data(), Ri.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
         // Q^T = Rinv^T Y^T  (col-major: (p x V) = (p x p)^T (p x V))
         double* dst = (pass == 0) ? w.tmp.p : Qd;
-        CB(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, p, V, p, &one, w.Rinv.p, p, src, p, &zero, dst, p));
+        dgemm_cm(ctx, true, false, p, V, p, w.Rinv.p, p, src, p, dst, p);
         src = dst;
     }
 }
@@ -208,11 +206,9 @@ void whiten_randomized(skc_context* ctx, int V, int k, int oversample, int iters
     }
     apply(Q.p, Y.p, p);
     // Rayleigh-Ritz: H = Q^T M2 Q (p x p)
-    cublasHandle_t h = cublas_of(ctx);
-    const double one = 1.0, zero = 0.0;
     DevBuf<double> Hd;
     Hd.alloc(static_cast<size_t>(p) * p);
-    CB(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, p, p, V, &one, Q.p, p, Y.p, p, &zero, Hd.p, p));
+    dgemm_cm(ctx, false, true, p, p, V, Q.p, p, Y.p, p, Hd.p, p);
     std::vector<double> H(static_cast<size_t>(p) * p);
     CK(cudaMemcpyAsync(H.data(), Hd.p, H.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     ctx->sync();
@@ -241,7 +237,7 @@ void whiten_randomized(skc_context* ctx, int V, int k, int oversample, int iters
     Ukd.upload(Uk.data(), Uk.size(), ctx->stream);
     Vk.alloc(static_cast<size_t>(V) * k);
     // Vk (V x k row-major = k x V col-major) = Uk^T (k x p) Q^T (p x V)
-    CB(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, k, V, p, &one, Ukd.p, p, Q.p, p, &zero, Vk.p, k));
+    dgemm_cm(ctx, true, false, k, V, p, Ukd.p, p, Q.p, p, Vk.p, k);
     fwd.upload(fw.data(), fw.size(), ctx->stream);
     fud.upload(fu.data(), fu.size(), ctx->stream);
     out.alloc(static_cast<size_t>(V) * k);
@@ -431,13 +427,11 @@ int skc_lda_whiten_dense(skc_context* ctx, int V, const double* m2, int k, int o
                 M[static_cast<size_t>(i) * V + j] = M[static_cast<size_t>(j) * V + i] = m2[static_cast<size_t>(i) * V + j];
         DevBuf<double> Md;
         Md.upload(M.data(), M.size(), ctx->stream);
-        cublasHandle_t h = cublas_of(ctx);
-        const double one = 1.0, zero = 0.0;
         whiten_randomized(
             ctx, V, k, oversample, iters, seed,
             [&](const double* Xd, double* Yd, int p) {
                 // Y^T (p x V) = X^T (p x V) M2 (V x V)
-                CB(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, p, V, V, &one, Xd, p, Md.p, V, &zero, Yd, p));
+                dgemm_cm(ctx, false, false, p, V, V, Xd, p, Md.p, V, Yd, p);
             },
             W, unwhiten, singular_values);
     });

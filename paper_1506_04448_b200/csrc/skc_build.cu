@@ -769,14 +769,15 @@ size_t cls_smem_bytes(std::uint32_t b, int tbits, int n, bool sym, bool one_limb
 }
 
 // One-limb add for fp32 inputs (|q| < 2^22): the window keeps each slot's exact sum
-// mod 2^32 biased by 2^31, so the centred value v = limb ^ 2^31 starts at 0 and a pass's
-// partial sums (~sqrt(count) * |q|) stay far from the +-2^31 edge. The flush adds v
-// itself to the slot's 64-bit accumulator, so without an overflow the accumulator holds
-// the exact sum, as with two limbs.
-constexpr std::uint32_t kLimbBias = 0x80000000u;
-// Overflow guard, conservative and branch-free: an add whose returned old limb has
-// |v| >= 2^30 (bits 31 and 30 of the limb equal) sets the sign bit of `ovf`. An add that
-// starts below 2^30 in magnitude ends below 2^30 + 2^22 < 2^31, so no add can overflow
+// mod 2^32 biased by 2^30, u = v + 2^30, so the centred value v starts at 0 and a pass's
+// partial sums (~sqrt(count) * |q|) stay far from the edges. The flush adds
+// v = int32(u - 2^30) to the slot's 64-bit accumulator, so without an overflow the
+// accumulator holds the exact sum, as with two limbs.
+constexpr std::uint32_t kLimbBias = 0x40000000u;
+// Overflow guard, conservative and branch-free, one OR per add: bit 31 of the returned old
+// limb u is set exactly when the state before the add was outside [-2^30, 2^30) (as long
+// as |v| < 2^30 + 2^31, which holds below). An add that starts inside ends inside
+// (-2^30 - 2^22, 2^30 + 2^22), which the flush decodes exactly, so no add can overflow
 // without an earlier or the same add being flagged. The window pass reports the flag and
 // the host then discards the build (the finalize adds nothing) and repeats it exactly with
 // two limbs. Ordinary data (|v| needs ~2^8 same-signed full-scale adds to one slot) never
@@ -784,7 +785,7 @@ constexpr std::uint32_t kLimbBias = 0x80000000u;
 __device__ __forceinline__ void add32_at(std::uint32_t addr, std::int32_t q, std::uint32_t& ovf) {
     std::uint32_t old;
     asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(static_cast<std::uint32_t>(q)));
-    ovf |= ~(old ^ (old << 1));
+    ovf |= old;
 }
 __device__ __forceinline__ void add32_idx(std::uint32_t idx, std::uint32_t sbase, std::int32_t q, std::uint32_t& ovf) {
     add32_at(sbase + 4u * idx, q, ovf);
@@ -1121,7 +1122,7 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
         // the sketch stays bit-deterministic)
         for (int s = threadIdx.x; s < W; s += NT) {
             const unsigned long long v =
-                L1 ? static_cast<unsigned long long>(static_cast<long long>(static_cast<std::int32_t>(sm[s] ^ kLimbBias)))
+                L1 ? static_cast<unsigned long long>(static_cast<long long>(static_cast<std::int32_t>(sm[s] - kLimbBias)))
                    : (static_cast<unsigned long long>(sm[WP + s]) << 32) | sm[s];
             if (v) atomicAdd(gacc + s, v);
         }

@@ -137,6 +137,11 @@ void launch_m2_apply(cudaStream_t st, int V, long long D, int p, const long long
                      const long long* chunk_lo, const long long* chunk_hi, const long long* word_chunk,
                      const double* s2, const double* diag, const double* m1p, double inv_used1, double inv_used2,
                      double a, const double* X, double* Z, double* part, double* mx, double* Y);
+// FP64 C = op(A) op(B) with element strides (skc_gemm.cu); split-K partials in ws
+// (dgemm_slices(M, N, K, sms) x M x N doubles when more than one slice)
+int dgemm_slices(int M, int N, int K, int sms);
+void launch_dgemm(cudaStream_t st, int sms, int M, int N, int K, const double* A, long long ai, long long ak,
+                  const double* B, long long bk, long long bj, double* C, long long ci, long long cj, double* ws);
 void launch_scale_cols(cudaStream_t st, long long rows, int k, const double* in, const double* f, double* out);
 void launch_normalize_columns(cudaStream_t st, int n, int k, double* F, const double* prev, double* lambda);
 void launch_gaussian_fill(cudaStream_t st, unsigned long long seed, long long count, double* out);

@@ -77,6 +77,8 @@ def _setup(L):
         "orc_sym_rank1_truncated": (C.c_int, [vp, C.c_int, d_p, d_p]),
         "orc_sym_ivv": (C.c_int, [vp, d_p, d_p]),
         "orc_sym_vvv": (C.c_int, [vp, d_p, d_p]),
+        "orc_sym_ivv_batch": (C.c_int, [vp, C.c_int, d_p, d_p]),
+        "orc_sym_vvv_batch": (C.c_int, [vp, C.c_int, d_p, d_p]),
         "orc_sym_cached_transform": (C.c_int, [vp, C.c_int, d_p]),
         "orc_sym_rtpm": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_double, d_p, d_p, d_p, i_p]),
         "orc_lda_sketch_whitened_m3": (C.c_int, [vp, C.c_int, C.c_int, ll_p, i_p, i_p, d_p, C.c_double, ll_p, ll_p]),
@@ -259,6 +261,19 @@ class SymSet:
         out = C.c_double()
         _chk(lib().orc_sym_vvv(self.h, dp(f64(u)), C.byref(out)))
         return out.value
+
+    def ivv_batch(self, U):
+        """ivv of each row of U (L x n), restarts on the oracle's threads."""
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        out = np.empty_like(U)
+        _chk(lib().orc_sym_ivv_batch(self.h, U.shape[0], dp(U), dp(out)))
+        return out
+
+    def vvv_batch(self, U):
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        out = np.empty(U.shape[0])
+        _chk(lib().orc_sym_vvv_batch(self.h, U.shape[0], dp(U), dp(out)))
+        return out
 
     def cached_transform(self, m):
         out = np.empty(self.b, dtype=np.complex128)

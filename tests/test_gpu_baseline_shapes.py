@@ -65,12 +65,12 @@ def stepwise_component(gpu_ctx, state, n, b, B, set_seed, L, T, inits):
     prev = U
     for t in range(T):
         G = ws.Ivv(U)
-        R = np.stack([o.ivv(U[l]) for l in range(L)])
+        R = o.ivv_batch(U)
         worst = max(worst, max(_rel_inf(G[l], R[l]) for l in range(L)))
         prev = U
         U = R / np.linalg.norm(R, axis=1, keepdims=True)  # normalized_or_throw (decompose.cpp:35-40)
     vg = ws.vvv(U)
-    vo = np.array([o.vvv(U[l]) for l in range(L)])
+    vo = o.vvv_batch(U)
     vworst = float(np.max(np.abs(vg - vo)) / np.max(np.abs(vo)))
     top = np.sort(vo)[::-1]
     # the driver's own last step from U_{T-1}: normalisation, selection and (lambda, v)

@@ -744,6 +744,26 @@ def test_lda_whiten_matches_dense_eigensolver_oracle(gpu_ctx, dense):
     assert np.max(np.abs(wm.W.T @ M2 @ wm.W - np.eye(k))) <= 1e-8
 
 
+def test_lda_whiten_dense_large_block_products(gpu_ctx):
+    """At V = 2304 the whitening's block products run split along K (the p x p Grams over
+    V rows and the dense p x V x V moment apply, skc_gemm.cu): the top-k eigenpairs of a
+    planted PSD moment match numpy's eigendecomposition and W' M2 W = I (lda.hpp:43)."""
+    V, k = 2304, 20
+    rng = np.random.default_rng(41)
+    Uq, _ = np.linalg.qr(rng.normal(size=(V, k)))
+    ev = np.geomspace(40.0, 2.0, k)
+    N = rng.normal(size=(V, V)) * 1e-3
+    M2 = (Uq * ev) @ Uq.T + (N + N.T) / 2
+    w_ref, U_ref = np.linalg.eigh(M2)
+    sv_ref = w_ref[::-1][:k]
+    wm = skb().whiten(M2, k, iters=30, ctx=gpu_ctx)
+    assert np.max(np.abs(wm.singular_values - sv_ref) / sv_ref) <= 1e-9
+    assert np.max(np.abs(wm.W.T @ M2 @ wm.W - np.eye(k))) <= 1e-8
+    Wn = wm.W * np.sqrt(sv_ref)  # unit eigenvectors
+    top = U_ref[:, ::-1][:, :k]
+    assert np.max(np.abs(np.abs(np.sum(Wn * top, axis=0)) - 1.0)) <= 1e-8
+
+
 def test_lda_device_corpus_handle_matches_per_call_path(gpu_ctx):
     """The device-resident corpus gives the same whitening and sketch as the per-call
     entry points (same operator, same order), bit for bit."""

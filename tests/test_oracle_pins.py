@@ -378,3 +378,34 @@ def test_oracle_pinv_spectral_matches_numpy():
     H = rng.normal(size=(5, 5))
     H = H @ H.T + 5 * np.eye(5)
     assert np.max(np.abs(O.pinv_spectral(H) - np.linalg.inv(H))) <= 1e-13
+
+
+def test_threaded_restarts_match_serial_oracle():
+    """The oracle's restart-parallel RTPM and batch contractions (test helpers) give the
+    same bits as one thread: each contraction's arithmetic is unchanged."""
+    n, b, B = 20, 256, 5
+    rng = np.random.default_rng(8)
+    T = rng.normal(size=(n, n, n))
+    T = (T + T.transpose(0, 2, 1) + T.transpose(1, 0, 2) + T.transpose(1, 2, 0) + T.transpose(2, 0, 1)
+         + T.transpose(2, 1, 0)) / 6
+    def fresh():
+        x = O.SymSet(n, b, B, 9)
+        x.accumulate_dense(T, True)
+        return x
+
+    s = fresh()
+    U = rng.normal(size=(7, n))
+    t0 = O.lib().orc_num_threads()
+    try:
+        O.lib().orc_set_num_threads(1)
+        serial = fresh().rtpm(3, 6, 5, seed=4)
+        ivv1 = np.stack([s.ivv(u) for u in U])
+        vvv1 = np.array([s.vvv(u) for u in U])
+        O.lib().orc_set_num_threads(4)
+        par = fresh().rtpm(3, 6, 5, seed=4)
+        assert np.array_equal(s.ivv_batch(U), ivv1)
+        assert np.array_equal(s.vvv_batch(U), vvv1)
+    finally:
+        O.lib().orc_set_num_threads(t0)
+    for a, c in zip(serial, par):
+        assert np.array_equal(a, c)
