@@ -231,17 +231,37 @@ def scatter_roofline(adds, kernel_ms, limbs=2, gather_stride=None):
     return out
 
 
+def _fp64_peaks():
+    """Measured DFMA rate and 16-byte shared-memory bandwidth (microbench/fp64_peak.cu on one
+    B200; the committed copy under profiles/)."""
+    peak, smem = None, None
+    try:
+        for line in (ROOT / "profiles" / "r02_fp64_peak.jsonl").read_text().splitlines():
+            d = json.loads(line)
+            if d.get("test") == "dfma_peak":
+                peak = max(peak or 0.0, d["tflops"])
+            if d.get("test") == "smem_lds128":
+                smem = max(smem or 0.0, d["TBps"])
+    except (OSError, ValueError, KeyError):
+        pass
+    return peak, smem
+
+
 def contraction_roofline(per_s, n, b, B):
     """SURVEY 8(d) model of one median-of-B T(I,u,u): 4B length-b transforms at 5 b log2 b
-    nominal flops each plus B(5n + 40b). Peak: the vendor FP64 figure (not measured here)."""
+    nominal flops each plus B(5n + 40b). Peak: the DFMA rate measured on a B200
+    (profiles/r02_fp64_peak.jsonl), else the vendor figure."""
     if not per_s:
         return None
     logb = b.bit_length() - 1
     flops = 4 * B * 5 * b * logb + B * (5 * n + 40 * b)
     tflops = per_s * flops / 1e12
+    peak, smem = _fp64_peaks()
+    src = "measured DFMA rate (profiles/r02_fp64_peak.jsonl)" if peak else "vendor B200 FP64 figure"
+    peak = peak or 37.0
     return {"bound": "fp64", "nominal_flops_per_contraction": flops, "achieved_tflops": tflops,
-            "peak_tflops": 37.0, "peak_source": "vendor B200 FP64 figure", "frac": tflops / 37.0,
-            "smem_peak_tbs": 148 * 128 * 1.965e9 / 1e12}
+            "peak_tflops": peak, "peak_source": src, "frac": tflops / peak,
+            "smem_peak_tbs": smem or 148 * 128 * 1.965e9 / 1e12}
 
 
 # ---------------------------------------------------------------- CPU (oracle) legs

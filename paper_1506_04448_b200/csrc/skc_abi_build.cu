@@ -63,6 +63,11 @@ void ensure_build_scratch_clean(skc_context* ctx) {
     ctx->build_scratch_clean = true;
 }
 
+#ifndef SKC_LOCK_MB  // experiment builds (microbench/lock_ab.sh) compile other spreads; 0: off
+#define SKC_LOCK_MB 12
+#endif
+constexpr double kLockMB = SKC_LOCK_MB;
+
 // Scratch and launch plan of one dense build of rows [i0, i1) on ctx (no launches). The
 // plan depends only on the shape (n, b, B, dtype, sym, limbs), so replicas of a set on
 // several devices get the same accumulator layout, and an empty row range still yields a
@@ -118,7 +123,7 @@ skc_context::RowTab& prepare_dense_build(skc_context* ctx, int n, int dtype, boo
     require(R <= 16, "accumulate_dense: slot range spans too many replicates");
     const long long tot = rt.cum.back();
     const int P = std::max(1, ctx->sms);  // one persistent CTA per SM, rows handed out dynamically
-    ctx->build_ints.alloc(static_cast<size_t>(G));
+    ctx->build_ints.alloc(2 * static_cast<size_t>(G));
     ctx->build_acc.alloc(static_cast<size_t>(total_slots));
     ctx->qbuf.alloc(static_cast<size_t>(std::max<long long>(1, tot)));
     ctx->rowF.alloc(static_cast<size_t>(std::max(1, rt.nrows)));
@@ -164,6 +169,16 @@ skc_context::RowTab& prepare_dense_build(skc_context* ctx, int n, int dtype, boo
     if (p.xsrc_mode == 1)  // device-resident class-list build: sums-only pre-pass, one wave of 5 blocks/SM
         p.prepass_blocks = std::min(kPrepassBlocks, std::max(1, ctx->sms) * 5);
     p.total_entries = tot;
+    // Lockstep of the class-list windows: every window sweeps all rows, so the rows are read
+    // from HBM once only while the windows' cursors stay within what L2 holds. ~12 MB of
+    // rows (the two L2 partitions mirror each other's lines: ~60 MB usable); off when the
+    // whole stream fits.
+    {
+        const double es = dtype == SKC_F32 ? 4.0 : 8.0;
+        const double bytes = static_cast<double>(tot) * es;
+        if (kLockMB > 0 && cls_bits >= 0 && rt.nrows > 0 && bytes > 48e6)
+            p.lock_rows = std::max(256, static_cast<int>(kLockMB * 1e6 / (bytes / rt.nrows)));
+    }
     return rt;
 }
 
@@ -247,7 +262,7 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
         p.prepass_blocks = qsms;
         p.prepass_warps = 32;
         ctx->build_acc.alloc(static_cast<size_t>(K) * total_slots);
-        ctx->build_ints.alloc(static_cast<size_t>(K) * G);
+        ctx->build_ints.alloc(2 * static_cast<size_t>(K) * G);
         ctx->ints.alloc(16);
         ctx->prepass.alloc(4 * static_cast<size_t>(K) * qsms);
         ensure_build_scratch_clean(ctx);
@@ -279,7 +294,7 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
                 pc.scale_exp = ctx->ints.p + 4 + c;
                 pc.reset_nonfinite = false;
                 pc.acc = ctx->build_acc.p + static_cast<size_t>(c) * total_slots;
-                pc.next_row = ctx->build_ints.p + static_cast<size_t>(c) * G;
+                pc.next_row = ctx->build_ints.p + 2 * static_cast<size_t>(c) * G;
                 if (pc.nrows > 0) launch_build_prepass(ctx->stream, Tdev, pc);
                 CK(cudaEventRecord(ctx->ev_q[c], ctx->stream));
                 CK(cudaStreamWaitEvent(ctx->stream2, ctx->ev_q[c], 0));
@@ -291,7 +306,7 @@ void run_dense_build(skc_context* ctx, const void* Tdev, int n, int dtype, bool 
             CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_q[K], 0));
             BuildPlan pf = p;
             pf.acc = ctx->build_acc.p;
-            launch_build_finalize_multi(ctx->stream, pf, K, ctx->ints.p + 4, ctx->build_ints.p, K * G);
+            launch_build_finalize_multi(ctx->stream, pf, K, ctx->ints.p + 4, ctx->build_ints.p, 2 * K * G);
             ctx->build_scratch_clean = true;
         }
         ctx->check_launch();

@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 
 #include "skc_host.hpp"
@@ -483,7 +484,10 @@ struct BuildArgs {
     int* nonfinite_out;            // lean pre-pass: CTA 0 stores the flag from the partials (no memset)
     int* ovf_out;                  // one-limb windows: set when a limb overflowed (zero on entry)
     int sym_even_F;                // symmetric one-limb / two-limb class-list builds: F even (see cta_scale_exp)
-    int* next_row;                 // G row (or tile) counters (zero on entry; the finalize re-zeroes them)
+    int* next_row;                 // G row (or tile) counters, then G per-window CTA counts (class-list
+                                   // kernel); zero on entry, the finalize re-zeroes all 2G
+    int lock_rows;                 // class-list kernel: a CTA leaves a window this many rows ahead of a
+                                   // window with fewer CTAs (windows sweep the rows together: L2 reuse)
     int qbits;                     // max |q| exponent: 50 (two limbs) or 22 (one limb, fp32 input)
     long long total_entries;       // entries of the whole build (all ranks): the mean of kappa|T|
     double entries_per_slot;       // total_entries / slots per replicate (bucket thickness)
@@ -822,9 +826,11 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
     constexpr std::uint32_t tmask = (1u << TB) - 1u;
     extern __shared__ __align__(16) std::uint32_t sm[];
     __shared__ int s_next_g;
+    __shared__ int s_leave;  // set by warp 0: the CTA moves to window s_next_g after the grabs in flight
     __shared__ int s_cend[C];
     __shared__ int s_wcnt[C * 32];  // per-(class, 32-k segment) counts, then their scan
     const int n = a.n, nrows = a.nrows;
+    int* const ncta = a.next_row + a.G;  // CTAs working on each window
     const int W = static_cast<int>((a.bmask + 1u) >> TB);  // slots per window
     const int WP = W + 32;  // plane stride: slots W + lane are inactive lanes' private dummy slots
     // n list words grouped by class: h_k | k << KS | e_k << 30 (KS = log2 b + 2 clears the
@@ -869,8 +875,10 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
     };
 
     int g = static_cast<int>((static_cast<long long>(blockIdx.x) * a.G) / gridDim.x);
+    if (threadIdx.x == 0) atomicAdd(ncta + g, 1);
     while (g >= 0) {
         const int m = g / C, P = SYM ? (g >> TB) & 1 : 0, r = g & static_cast<int>(tmask);
+        if (threadIdx.x == 0) s_leave = 0;
         for (int s = threadIdx.x; s < NPL * WP; s += NT) sm[s] = L1 ? kLimbBias : 0u;
         unsigned long long* gacc = a.acc + static_cast<long long>(g) * W;  // this window's accumulators
         // asym packed words are h | neg << 31 for modes 1..3 (B x 3 x n): the list holds
@@ -971,9 +979,49 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
         int c0 = 0;
         if (lane == 0) c0 = atomicAdd(a.next_row + g, R);
         c0 = __shfl_sync(0xffffffffu, c0, 0);
+        int grabs = 0;
         while (c0 < nrows) {
-            int cn = 0;  // next grab, one grab ahead
-            if (lane == 0) cn = atomicAdd(a.next_row + g, R);
+            // Lockstep: every 4th grab warp 0 compares this window's cursor with the others.
+            // A window worked by more CTAs runs ahead; once it leads a window with fewer CTAs
+            // by lock_rows, one CTA moves there (the counts swap, so the lead shrinks again).
+            // All windows then stay within ~lock_rows of each other and every row is fetched
+            // from HBM about once for all of them.
+            if (warp == 0 && (++grabs & 3) == 0 && *((volatile int*)&s_leave) == 0) {
+                const int mine = *((volatile int*)(a.next_row + g));
+                const int cmine = *((volatile int*)(ncta + g));
+                int best = INT_MAX, bt = -1;
+                for (int tt = lane; tt < a.G; tt += 32) {
+                    const int cur = *((volatile int*)(a.next_row + tt));
+                    const int ct = *((volatile int*)(ncta + tt));
+                    if (ct < cmine && mine - cur > a.lock_rows && cur < best) {
+                        best = cur;
+                        bt = tt;
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const int ob = __shfl_xor_sync(0xffffffffu, best, o), ot = __shfl_xor_sync(0xffffffffu, bt, o);
+                    if (ob < best || (ob == best && ot > bt)) {
+                        best = ob;
+                        bt = ot;
+                    }
+                }
+                if (bt >= 0 && mine < nrows) {
+                    if (lane == 0) {
+                        const int old = atomicSub(ncta + g, 1);
+                        if (old > *((volatile int*)(ncta + bt))) {
+                            atomicAdd(ncta + bt, 1);
+                            s_next_g = bt;
+                            __threadfence_block();
+                            s_leave = 1;
+                        } else {
+                            atomicAdd(ncta + g, 1);  // another CTA of this window moved first
+                        }
+                    }
+                }
+            }
+            int cn = INT_MAX;  // next grab, one grab ahead (none once the CTA is leaving)
+            if (lane == 0 && *((volatile int*)&s_leave) == 0) cn = atomicAdd(a.next_row + g, R);
             const int nr = min(R, nrows - c0);
             long long off = 0;  // source element index of (i, j, 0)
             int cnt = 0, pos0 = 0;
@@ -1126,7 +1174,7 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
                    : (static_cast<unsigned long long>(sm[WP + s]) << 32) | sm[s];
             if (v) atomicAdd(gacc + s, v);
         }
-        if (threadIdx.x == 0) {
+        if (threadIdx.x == 0 && s_leave == 0) {  // rows exhausted: the window with the most rows left
             int best = -1, left = 0;
             for (int tt = 0; tt < a.G; ++tt) {
                 const int l = nrows - *((volatile int*)(a.next_row + tt));
@@ -1135,10 +1183,13 @@ __global__ void __launch_bounds__(1024, 1) k_build_cls(BuildArgs a) {
                     best = tt;
                 }
             }
+            atomicSub(ncta + g, 1);
+            if (best >= 0) atomicAdd(ncta + best, 1);
             s_next_g = best;
         }
         __syncthreads();
         g = s_next_g;
+        __syncthreads();  // s_leave is reset at the top of the next window
     }
     if (!have_F) {  // (a CTA that took no window) still orders itself after the pre-pass and
                     // derives F, so CTA 0 always publishes scale_exp / nonfinite for the finalize
@@ -1223,6 +1274,7 @@ void launch_build_main(cudaStream_t st, const void* T, const BuildPlan& p) {
     a.ovf_out = p.ovf;
     a.sym_even_F = (p.cls_bits >= 0 && p.sym) ? 1 : 0;
     a.next_row = p.next_row;
+    a.lock_rows = p.lock_rows;
     a.acc = p.acc;
     a.qbits = (p.cls_bits >= 0 && p.one_limb) ? 22 : 50;
     a.total_entries = p.total_entries;
@@ -1377,20 +1429,20 @@ void launch_build_finalize_multi(cudaStream_t st, const BuildPlan& p, int K, con
 }
 
 void launch_build_finalize(cudaStream_t st, const BuildPlan& p) {
-    const unsigned grid = cdiv(std::max<long long>((p.total_slots + 3) / 4, p.G), 256);
+    const unsigned grid = cdiv(std::max<long long>((p.total_slots + 3) / 4, 2 * p.G), 256);
     const bool pdl = p.pdl && p.cls_bits >= 0;  // only the class-list main pass triggers early
     if (p.sym && p.cls_bits == 0) {
         const long long pairs = p.total_slots / 2;  // B x b complex entries
         const int logb = __builtin_ctz(p.bmask + 1u);
-        const unsigned g2 = cdiv(std::max<long long>((pairs + 1) / 2, p.G), 256);
+        const unsigned g2 = cdiv(std::max<long long>((pairs + 1) / 2, 2 * p.G), 256);
         pdl_launch(k_build_finalize_sym_pair, g2, 256, 0, st, pdl, p.acc, pairs, logb, p.scale_exp, p.nonfinite,
-                   reinterpret_cast<double2*>(p.data_as_double), p.next_row, p.G);
+                   reinterpret_cast<double2*>(p.data_as_double), p.next_row, 2 * p.G);
     } else if (p.sym)
         pdl_launch(k_build_finalize<true>, grid, 256, 0, st, pdl, p.acc, p.total_slots, p.scale_exp, p.nonfinite,
-                   p.data_as_double, p.next_row, p.G, p.cls_bits, p.bmask);
+                   p.data_as_double, p.next_row, 2 * p.G, p.cls_bits, p.bmask);
     else
         pdl_launch(k_build_finalize<false>, grid, 256, 0, st, pdl, p.acc, p.total_slots, p.scale_exp, p.nonfinite,
-                   p.data_as_double, p.next_row, p.G, p.cls_bits, p.bmask);
+                   p.data_as_double, p.next_row, 2 * p.G, p.cls_bits, p.bmask);
     count_launch();
 }
 

@@ -86,7 +86,8 @@ struct BuildPlan {
     // work split: G contiguous slot ranges ("types"), P persistent CTAs with dynamic
     // row hand-out per type (next_row counters) and migration between types
     int P, G;
-    int* next_row;               // G counters
+    int* next_row;               // 2G ints: G row counters, then G per-window CTA counts
+    int lock_rows = 0x3fffffff;  // class-list windows stay within this many rows of each other
     int cls_bits = -1;           // >= 0: class-list kernel, windows = (replicate, [parity,] bucket mod 2^cls_bits)
     bool one_limb = false;       // class-list kernel: one biased 32-bit limb per slot (fp32 input)
     int* ovf = nullptr;          // one-limb overflow flag (= nonfinite + 2)
