@@ -67,6 +67,10 @@ void ensure_build_scratch_clean(skc_context* ctx) {
 #define SKC_LOCK_MB 12
 #endif
 constexpr double kLockMB = SKC_LOCK_MB;
+#ifndef SKC_SUMS_MINB  // resident blocks per SM of the lean sums pre-pass (skc_build.cu)
+#define SKC_SUMS_MINB 5
+#endif
+constexpr int kSumsBlocksPerSM = SKC_SUMS_MINB;
 
 // Scratch and launch plan of one dense build of rows [i0, i1) on ctx (no launches). The
 // plan depends only on the shape (n, b, B, dtype, sym, limbs), so replicas of a set on
@@ -167,7 +171,7 @@ skc_context::RowTab& prepare_dense_build(skc_context* ctx, int n, int dtype, boo
     }
     p.data_as_double = reinterpret_cast<double*>(data);
     if (p.xsrc_mode == 1)  // device-resident class-list build: sums-only pre-pass, one wave of 5 blocks/SM
-        p.prepass_blocks = std::min(kPrepassBlocks, std::max(1, ctx->sms) * 5);
+        p.prepass_blocks = std::min(kPrepassBlocks, std::max(1, ctx->sms) * kSumsBlocksPerSM);
     p.total_entries = tot;
     // Lockstep of the class-list windows: every window sweeps all rows, so the rows are read
     // from HBM once only while the windows' cursors stay within what L2 holds. ~12 MB of

@@ -268,16 +268,46 @@ __global__ void __launch_bounds__(NTQ) k_build_quantize(const TT* __restrict__ T
 }
 
 // Lean sums-only pre-pass (default for device-resident class-list builds). Each lane
-// keeps its own kappa-weighted L1 sum and maximum across all the rows its warp visits:
-// kappa is applied per element (the k = k0 entry takes the diagonal weight), so no row
-// needs a warp reduction; one block reduction at the end. Rows are dealt to warps in
-// grid-strided pairs with all of a pair's loads issued before any is consumed.
-// Non-finite entries surface as a non-finite lane sum.
+// keeps its own kappa-weighted L1 sum, maximum, sum of squares and smallest nonzero magnitude
+// across all the rows its warp visits; one block reduction at the end. kappa is constant
+// along a row except on its k = j entry (6 / 3 off the diagonal rows, 3 / 1 on them), so a
+// lane accumulates the row unweighted -- per entry one widening, one add, one fma, a float
+// (or double) max and an integer min of the magnitude bits -- and applies the row's kappa
+// once; lane 0 peels the k = j entry. (The previous form weighted every entry: 34 warp
+// instructions per 32 entries, issue- and conversion-bound at 2.6 TB/s on fp32 input.)
+// Rows are dealt to warps in grid-strided pairs with all of a pair's loads issued before any
+// is consumed. Non-finite entries surface as a non-finite lane sum.
+__device__ __forceinline__ float mag(float x) { return fabsf(x); }
+__device__ __forceinline__ double mag(double x) { return fabs(x); }
+__device__ __forceinline__ float max_of(float a, float b) { return fmaxf(a, b); }  // NaN: the sum carries it
+__device__ __forceinline__ double max_of(double a, double b) { return fmax(a, b); }
+template <typename TT>
+struct MagBits;  // magnitude bits as an unsigned integer: orders like the magnitude itself
+template <>
+struct MagBits<float> {
+    using U = std::uint32_t;
+    static __device__ __forceinline__ U of(float a) { return __float_as_uint(a); }
+    static __device__ __forceinline__ double back(U u) { return static_cast<double>(__uint_as_float(u)); }
+};
+template <>
+struct MagBits<double> {  // the high word (exponent and 20 mantissa bits): rounds the minimum down
+    using U = std::uint32_t;
+    static __device__ __forceinline__ U of(double a) { return static_cast<U>(__double2hiint(a)); }
+    static __device__ __forceinline__ double back(U u) { return __hiloint2double(static_cast<int>(u), 0); }
+};
+#ifndef SKC_SUMS_MINB  // experiment builds only
+#define SKC_SUMS_MINB 5
+#endif
+#ifndef SKC_SUMS_U32
+#define SKC_SUMS_U32 4
+#endif
 template <typename TT, bool SYM>
-__global__ void __launch_bounds__(256, 5) k_build_sums_lean(const TT* __restrict__ T, int n,
+__global__ void __launch_bounds__(256, SKC_SUMS_MINB) k_build_sums_lean(const TT* __restrict__ T, int n,
                                                             const std::uint32_t* __restrict__ rowtab, int nrows,
                                                             double* __restrict__ partials, int* __restrict__ nonfinite) {
-    constexpr int W = 8, U = 4;
+    constexpr int W = 8, U = sizeof(TT) == 4 ? SKC_SUMS_U32 : 4;  // (8 fp32 loads per lane and row measured no faster: sums_ab.sh)
+    using MB = MagBits<TT>;
+    using UB = typename MB::U;
     __shared__ double red[2 * W];
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -288,6 +318,12 @@ __global__ void __launch_bounds__(256, 5) k_build_sums_lean(const TT* __restrict
     std::uint32_t nij[2];  // the next pair's (i, j) words, fetched one step ahead
 #pragma unroll
     for (int h = 0; h < 2; ++h) nij[h] = row0 + h * stride < nrows ? __ldg(rowtab + row0 + h * stride) : 0u;
+    // one entry of weight w into the lane totals
+    auto fold = [&](double w, double d, TT m, UB nz) {
+        acc = fma(w, d, acc);
+        mx = fmax(mx, w * static_cast<double>(m));
+        if (nz != ~UB(0)) mn = fminf(mn, __double2float_rd(w * MB::back(nz + 1)));
+    };
     for (int row = row0; row < nrows; row += 2 * stride) {
         const TT* rp[2];
         int k0[2];
@@ -311,17 +347,28 @@ __global__ void __launch_bounds__(256, 5) k_build_sums_lean(const TT* __restrict
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
+            // kappa: 6 (3 if i = j) off the k = j entry, 3 (1 if i = j) on it
+            const double wr = !SYM ? 1.0 : (dg[h] ? 3.0 : 6.0);
+            if (SYM && lane == 0 && k0[h] < n) {  // the k = j entry, peeled
+                const TT a0 = mag(v[h][0]);
+                const double d0 = static_cast<double>(a0), w0 = dg[h] ? 1.0 : 3.0;
+                fold(w0, d0, a0, MB::of(a0) - 1);
+                sq = fma(w0 * d0, w0 * d0, sq);
+                v[h][0] = TT(0);
+            }
+            double rs = 0.0, rq = 0.0;  // the row's unweighted sum and sum of squares (this lane)
+            TT rm = TT(0);               // ... maximum
+            UB rn = ~UB(0);              // ... smallest nonzero magnitude bits - 1 (zero wraps to the top)
             for (int kb = k0[h] + lane;; kb += 32 * U) {
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    // kappa: 6 (3 if i = j) off the k = k0 entry, 3 (1 if i = j) on it
-                    const double w = !SYM ? 1.0
-                                          : (kb + 32 * u == k0[h] ? (dg[h] ? 1.0 : 3.0) : (dg[h] ? 3.0 : 6.0));
-                    const double a = w * fabs(static_cast<double>(v[h][u]));
-                    acc += a;
-                    mx = fmax(mx, a);
-                    sq = fma(a, a, sq);
-                    mn = fminf(mn, a > 0.0 ? __double2float_rd(a) : INFINITY);
+                    const TT a = mag(v[h][u]);
+                    const double d = static_cast<double>(a);
+                    rs += d;
+                    rq = fma(d, d, rq);
+                    rm = max_of(rm, a);
+                    const UB nb = MB::of(a) - 1;
+                    rn = nb < rn ? nb : rn;
                 }
                 if (kb + 32 * U >= n) break;
 #pragma unroll
@@ -330,6 +377,9 @@ __global__ void __launch_bounds__(256, 5) k_build_sums_lean(const TT* __restrict
                     v[h][u] = k < n ? __ldg(rp[h] + k) : TT(0);
                 }
             }
+            fold(wr, rs, rm, rn);
+            sq = fma(wr * wr, rq, sq);
+            // (a NaN entry drops out of the maximum: rs carries it into acc)
         }
     }
     // (no flag write: the main pass derives it from these partials)
