@@ -9,7 +9,7 @@
 // m_d >= 2, and m1 = (1/used1) sum_{m_d >= 1} n_d / m_d. This equals the reference's
 // position-pair sum, pair(a, a) = c_a (c_a - 1), exactly, duplicates included. Top-k
 // eigenpairs come from randomized subspace iteration with Rayleigh-Ritz (host code in
-// skc_abi_lda.cu; the block products use cuBLAS DGEMM).
+// skc_abi_lda.cu; the block products use the FP64 kernel of skc_gemm.cu).
 //
 //   k_corpus_docs   per document: m_d, s2_d, 1/m_d                       (thread/doc)
 //   k_m2_word_prep  per word: diag_w = sum s2_d c_dw, m1_w (CSC, fixed order)  (thread/word)
