@@ -1068,6 +1068,151 @@ __global__ void __launch_bounds__(kFftThreads, SKC_FFT_MINB)
     double2* o = reinterpret_cast<double2*>(acc) + (((size_t)ch * B + m) * S + r) * N;
     for (int j = threadIdx.x; j < N; j += blockDim.x) o[j] = ACC[pad16(j)];
 }
+// Paired-sample form of k_sym_moment for local length 2048 (the b >= 2^11 shapes: configs 3
+// and 4). Two samples go through the transform together and the accumulators live in
+// registers:
+//   - the passes run 16 x 16 x 8 (the same radix-2 stage sequence as the 8 x 16 x 16 plan, so
+//     the same bit-reversed layout): the two radix-16 passes have 2 x 128 items for the 256
+//     threads (one sample left half of them idle), and the closing radix-8 pass gives thread
+//     t the 8 consecutive outputs [8t, 8t + 8) of every sample, so the cube-accumulate adds
+//     into 8 complex registers instead of a read-modify-write of a shared-memory array;
+//   - the freed array holds the second sample: same shared-memory footprint, 2 CTAs per SM,
+//     half the barriers per sample;
+//   - both rows of a pair arrive by ONE bulk (TMA) copy (rows s, s + 1 are contiguous in X)
+//     into a single buffer, issued once the scatter has consumed the previous pair.
+template <int LOGN>
+__global__ void __launch_bounds__((1 << LOGN) / 8, 2)
+    k_sym_moment_pair(SymView v, const double* __restrict__ X, const double* __restrict__ w, double wscale,
+                      long long Nsamp, int chunks, double* __restrict__ acc) {
+    extern __shared__ double2 sm[];
+    constexpr int N = 1 << LOGN, NT = N / 8;
+    constexpr int stride = N + (N >> 4) + 1;
+    static_assert(LOGN >= 8 && (LOGN - 3) % 4 == 0, "16 x ... x 16 x 8 pass plan");
+    const int S = v.S, n = v.n, B = v.B;
+    const int r = blockIdx.x % S;
+    const int m = (blockIdx.x / S) % B;
+    const int ch = blockIdx.x / (S * B);
+    double2* A0 = sm;
+    double2* A1 = sm + stride;
+    double2* wv = A1 + stride;                                         // n
+    std::uint32_t* keys = reinterpret_cast<std::uint32_t*>(wv + n);   // n
+    std::uint32_t* idx = keys + n;                                     // n
+    double* xs = reinterpret_cast<double*>(idx + n + (n & 1));         // 2 x n: the pair's rows
+    const long long per = (Nsamp + chunks - 1) / chunks;
+    const long long s0 = (long long)ch * per, s1 = min(Nsamp, s0 + per);
+    const uint2* plan = v.plan1 + (size_t)m * n;
+    const std::uint32_t bmask = v.b - 1;
+    const std::uint32_t nmask = static_cast<std::uint32_t>(N - 1);
+    zero_smem(A0, 2 * stride);
+    {
+        const double2* stw = v.stw1 ? v.stw1 + ((size_t)m * S + r) * n : nullptr;
+        for (int q = threadIdx.x; q < n; q += NT) {
+            const uint2 e = plan[q];
+            const double2 tw = stw ? stw[q] : conj(v.tw[(static_cast<std::uint32_t>(r) * (e.y & 0x0FFFFFFFu)) & bmask]);
+            wv[q] = cmul(root4_times(e.y >> 28, 1.0), tw);
+            keys[q] = e.y & nmask;
+            idx[q] = e.x;
+        }
+    }
+    __shared__ __align__(8) unsigned long long mbar;
+    const bool bulk = ((n & 1) == 0) && ((reinterpret_cast<std::uintptr_t>(X) & 15) == 0);
+    const std::uint32_t mb = static_cast<std::uint32_t>(__cvta_generic_to_shared(&mbar));
+    if (bulk && threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(mb) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // rows [smp, smp + cnt) -> xs (thread 0; the buffer's previous readers are behind a barrier)
+    auto prefetch = [&](long long smp) {
+        if (!bulk || smp >= s1 || threadIdx.x != 0) return;
+        const std::uint32_t bytes = static_cast<std::uint32_t>(min(2ll, s1 - smp)) * static_cast<std::uint32_t>(n) * 8u;
+        const std::uint32_t da = static_cast<std::uint32_t>(__cvta_generic_to_shared(xs));
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(da),
+                     "l"(X + (size_t)smp * n), "r"(bytes), "r"(mb)
+                     : "memory");
+    };
+    double2 accr[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) accr[q] = mk(0.0, 0.0);
+    const int wi = static_cast<int>((threadIdx.x & ~15u) | ((threadIdx.x & 7u) << 1) | ((threadIdx.x >> 3) & 1u));
+    prefetch(s0);
+    std::uint32_t par = 0;
+    for (long long s = s0; s < s1; s += 2) {
+        const int cnt = static_cast<int>(min(2ll, s1 - s));
+        if (bulk) {
+            std::uint32_t done = 0;
+            while (!done)
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                    : "=r"(done)
+                    : "r"(mb), "r"(par)
+                    : "memory");
+            par ^= 1u;
+        } else {
+            for (int i = threadIdx.x; i < cnt * n; i += NT) xs[i] = X[(size_t)s * n + i];
+            __syncthreads();
+        }
+        // A0, A1 are all-zero here (initially, then re-zeroed by the closing pass). A run head
+        // sums its run of equal keys in plan order for both samples (sketch.cpp:353-356).
+        for (int q = threadIdx.x; q < n; q += NT) {
+            const std::uint32_t key = keys[q];
+            if (q > 0 && keys[q - 1] == key) continue;
+            double2 a0 = mk(0.0, 0.0), a1 = mk(0.0, 0.0);
+            for (int q2 = q; q2 < n && keys[q2] == key; ++q2) {
+                const int i = static_cast<int>(idx[q2]);
+                const double2 wq = wv[q2];
+                const double x0 = xs[i], x1 = cnt > 1 ? xs[n + i] : 0.0;
+                a0 = cadd(a0, mk(wq.x * x0, wq.y * x0));
+                a1 = cadd(a1, mk(wq.x * x1, wq.y * x1));
+            }
+            A0[pad16(static_cast<int>(key))] = a0;
+            if (cnt > 1) A1[pad16(static_cast<int>(key))] = a1;
+        }
+        __syncthreads();
+        prefetch(s + 2);  // xs is consumed: the next pair lands during the passes
+        // radix-16 passes: half-sizes N/2, N/32, ... down to 64 (2 x N/16 items)
+        constexpr int NP16 = (LOGN - 3) / 4;
+#pragma unroll
+        for (int pz = 0; pz < NP16; ++pz) {
+            const int h = (N >> 1) >> (4 * pz);
+            for (int it = threadIdx.x; it < cnt * (N / 16); it += NT) {
+                const int a = it / (N / 16);
+                dif_pass_item<4>(a ? A1 : A0, it - a * (N / 16), h, v.twl, LOGN);
+            }
+            __syncthreads();
+        }
+        // closing radix-8 pass (half-size 4): a thread holds the 8 consecutive outputs of item wi
+        // of each sample. Item w starts at padded position 8w + w/2, i.e. bank group (w/2) mod 8,
+        // so the 8 lanes of a quarter-warp take items 2l + p (l = lane & 7): distinct groups
+        // (items 8q .. 8q + 7 in lane order would collide two by two)
+#pragma unroll 1
+        for (int c = 0; c < cnt; ++c) {
+            double2* A = c ? A1 : A0;
+            const double ws = (w ? w[s + c] : 1.0) * wscale;
+            double2 z[8];
+            int base, g;
+            dif_item_core<3>(A, wi, 4, v.twl, LOGN, z, base, g);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                A[pad16(base + q * g)] = mk(0.0, 0.0);  // ready for the next pair's scatter
+                const double2 z3 = cmul(cmul(z[q], z[q]), z[q]);
+                accr[q] = cadd(accr[q], cscale(z3, ws));
+            }
+        }
+        __syncthreads();
+    }
+    double2* o = reinterpret_cast<double2*>(acc) + (((size_t)ch * B + m) * S + r) * N;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) o[8 * wi + q] = accr[q];
+}
+size_t moment_pair_smem(int N, int n) {
+    return sizeof(double2) * 2 * static_cast<size_t>(padded_len(N)) +
+           (sizeof(double2) + 2 * sizeof(std::uint32_t)) * static_cast<size_t>(n) + sizeof(std::uint32_t) * (n & 1) +
+           2 * sizeof(double) * static_cast<size_t>(n);
+}
+
 template <int LR>
 static void moment_launch(cudaStream_t st, const SymView& v, const double* X, const double* w, double wscale,
                           long long Nsamp, int chunks, double* acc, bool scr, size_t smem, unsigned grid) {
@@ -1087,9 +1232,17 @@ static void moment_launch(cudaStream_t st, const SymView& v, const double* X, co
 void launch_sym_moment_accumulate(cudaStream_t st, const SymView& v, const double* X, const double* w, double wscale,
                                   long long Nsamp, int chunks, double* acc) {
     const bool scr = v.n <= kScatterMax;
+    const unsigned grid = (unsigned)((long long)chunks * v.B * v.S);
+    if (scr && v.logN == 11) {  // local length 2048: paired samples, register accumulators
+        const size_t smem2 = moment_pair_smem(v.N, v.n);
+        cudaFuncSetAttribute(k_sym_moment_pair<11>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+        k_sym_moment_pair<11><<<grid, 256, smem2, st>>>(v, X, w, wscale, Nsamp, chunks, acc);
+        SKC_LAUNCHED();
+        count_transforms((std::uint64_t)Nsamp * v.B * v.S, v.S);
+        return;
+    }
     const size_t smem = sizeof(double2) * (2 * padded_len(v.N)) +
                         (scr ? (sizeof(double2) + 2 * sizeof(std::uint32_t) + 2 * sizeof(double)) * (size_t)v.n + 8 : 0);
-    const unsigned grid = (unsigned)((long long)chunks * v.B * v.S);
     moment_launch<4>(st, v, X, w, wscale, Nsamp, chunks, acc, scr, smem, grid);  // radix-16 local passes
     SKC_LAUNCHED();
     count_transforms((std::uint64_t)Nsamp * v.B * v.S, v.S);
