@@ -306,6 +306,104 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
 }
 
+// Paired-document form of k_lda_acc_docs for local length 2048 (config 4: b = 2^14). Two
+// documents go through a 16 x 16 x 8 pass plan together (2 x 128 radix-16 items for the 256
+// threads; one document left half of them idle), the closing radix-8 pass gives a thread the
+// same 8 consecutive outputs of both, so ACC lives in 8 complex registers; CR stays in shared
+// memory (padded like A), and the array ACC used to take holds the second document. Items
+// are taken in the bank-conflict-free order of k_sym_moment_pair (skc_kernels.cu).
+template <int LOGN>
+__global__ void __launch_bounds__((1 << LOGN) / 8, 2)
+    k_lda_acc_docs_pair(SymView v, long long Du, const long long* __restrict__ used_docs, const double* __restrict__ P,
+                        const double* __restrict__ s1, const double* __restrict__ s2, int chunks,
+                        double* __restrict__ acc_out, double* __restrict__ cross_out) {
+    extern __shared__ double2 sm[];
+    constexpr int N = 1 << LOGN, NT = N / 8;
+    constexpr int stride = N + (N >> 4) + 1;
+    static_assert(LOGN >= 8 && (LOGN - 3) % 4 == 0, "16 x ... x 16 x 8 pass plan");
+    const int S = v.S, n = v.n, B = v.B;
+    const int r = blockIdx.x % S;
+    const int m = (blockIdx.x / S) % B;
+    const int ch = blockIdx.x / (S * B);
+    double2* A0 = sm;
+    double2* A1 = sm + stride;
+    double2* CR = A1 + stride;
+    ScatterMeta mt{CR + stride, nullptr, nullptr};
+    mt.keys = reinterpret_cast<std::uint32_t*>(mt.wv + n);
+    mt.idx = mt.keys + n;
+    double* rows = reinterpret_cast<double*>(mt.idx + n);  // the pair's rows (2n u32 before: 8-byte aligned)
+    const long long per = (Du + chunks - 1) / chunks;
+    const long long i0 = (long long)ch * per, i1 = min(Du, i0 + per);
+    zero_sm(A0, 3 * stride);
+    build_meta(mt, v.plan1 + (size_t)m * n, v.stw1 ? v.stw1 + ((size_t)m * S + r) * n : nullptr, v.tw, n, N, r,
+               v.b - 1);
+    auto fetch = [&](long long it) {
+        if (it < i1) async_row(rows, P + (size_t)used_docs[it] * n, n);
+        if (it + 1 < i1) async_row(rows + n, P + (size_t)used_docs[it + 1] * n, n);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    double2 accr[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) accr[q] = mk(0.0, 0.0);
+    const int wi = static_cast<int>((threadIdx.x & ~15u) | ((threadIdx.x & 7u) << 1) | ((threadIdx.x >> 3) & 1u));
+    fetch(i0);
+    for (long long it = i0; it < i1; it += 2) {
+        const int cnt = static_cast<int>(min(2ll, i1 - it));
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+        for (int q = threadIdx.x; q < n; q += NT) {  // run heads, both documents (plan order)
+            const std::uint32_t key = mt.keys[q];
+            if (q > 0 && mt.keys[q - 1] == key) continue;
+            double2 a0 = mk(0.0, 0.0), a1 = mk(0.0, 0.0);
+            for (int q2 = q; q2 < n && mt.keys[q2] == key; ++q2) {
+                const int i = static_cast<int>(mt.idx[q2]);
+                const double2 wq = mt.wv[q2];
+                const double x0 = rows[i], x1 = cnt > 1 ? rows[n + i] : 0.0;
+                a0 = cadd(a0, mk(wq.x * x0, wq.y * x0));
+                a1 = cadd(a1, mk(wq.x * x1, wq.y * x1));
+            }
+            A0[pad16(static_cast<int>(key))] = a0;
+            if (cnt > 1) A1[pad16(static_cast<int>(key))] = a1;
+        }
+        __syncthreads();
+        fetch(it + 2);  // the rows are consumed: the next pair lands during the passes
+        constexpr int NP16 = (LOGN - 3) / 4;
+#pragma unroll
+        for (int pz = 0; pz < NP16; ++pz) {
+            const int h = (N >> 1) >> (4 * pz);
+            for (int w = threadIdx.x; w < cnt * (N / 16); w += NT) {
+                const int a = w / (N / 16);
+                dif_pass_item<4>(a ? A1 : A0, w - a * (N / 16), h, v.twl, LOGN);
+            }
+            __syncthreads();
+        }
+#pragma unroll 1
+        for (int c = 0; c < cnt; ++c) {
+            double2* A = c ? A1 : A0;
+            const long long d = used_docs[it + c];
+            const double a1 = s1[d], a2 = s2[d];
+            double2 z[8];
+            int base, g;
+            dif_item_core<3>(A, wi, 4, v.twl, LOGN, z, base, g);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int pj = pad16(base + q * g);
+                A[pj] = mk(0.0, 0.0);
+                const double2 sq = cmul(z[q], z[q]);
+                accr[q] = cadd(accr[q], cscale(cmul(sq, z[q]), a1));  // lda.cpp:205
+                CR[pj] = cadd(CR[pj], cscale(sq, a2));               // lda.cpp:206
+            }
+        }
+        // (the next scatter is behind the barrier at the top of the loop)
+    }
+    __syncthreads();
+    double2* ao = reinterpret_cast<double2*>(acc_out) + (((size_t)ch * B + m) * S + r) * N;
+    double2* co = reinterpret_cast<double2*>(cross_out) + (((size_t)ch * B + m) * S + r) * N;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) ao[8 * wi + q] = accr[q];
+    for (int j = threadIdx.x; j < N; j += NT) co[j] = CR[pad16(j)];
+}
+
 template <int LOGN>
 __global__ void __launch_bounds__(kThreads, 2)
     k_lda_acc_vocab(SymView v, int V, const double* __restrict__ W, const double* __restrict__ coeff1,
@@ -429,6 +527,11 @@ void launch_lda_q(cudaStream_t st, int k, int V, const double* W, const double* 
         default: break;            \
     }
 
+#ifdef SKC_LDA_NOPAIR  // experiment builds: the one-document kernel at every length
+constexpr bool kPairDocs = false;
+#else
+constexpr bool kPairDocs = true;
+#endif
 // acc: (chunks_d + chunks_v) partial spectra (documents first), cross: chunks_d.
 void launch_lda_accumulate(cudaStream_t st, const SymView& v, long long Du, const long long* used_docs, const double* P,
                            const double* s1, const double* s2, int V, const double* W, const double* coeff1,
@@ -447,8 +550,12 @@ void launch_lda_accumulate(cudaStream_t st, const SymView& v, long long Du, cons
     {                                                                                                               \
         cudaFuncSetAttribute(k_lda_acc_docs<LG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_d);         \
         cudaFuncSetAttribute(k_lda_acc_vocab<LG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_v);        \
-        if (Du > 0) k_lda_acc_docs<LG><<<grid_d, kThreads, smem_d, st>>>(v, Du, used_docs, P, s1, s2, chunks_d, acc, cross); \
+        if (Du > 0 && (LG != 11 || !kPairDocs)) k_lda_acc_docs<LG><<<grid_d, kThreads, smem_d, st>>>(v, Du, used_docs, P, s1, s2, chunks_d, acc, cross); \
         if (V > 0) k_lda_acc_vocab<LG><<<grid_v, kThreads, smem_v, st>>>(v, V, W, coeff1, sumwn, chunks_v, acc_v);          \
+    }
+    if (Du > 0 && v.logN == 11 && kPairDocs) {  // local length 2048: paired documents, ACC in registers (launched first)
+        cudaFuncSetAttribute(k_lda_acc_docs_pair<11>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_d);
+        k_lda_acc_docs_pair<11><<<grid_d, 256, smem_d, st>>>(v, Du, used_docs, P, s1, s2, chunks_d, acc, cross);
     }
     SKC_LOGN_SWITCH_L(v.logN, L_)
 #undef L_
