@@ -102,6 +102,25 @@ SKC_HD double2 const_root(int M, int q) {
     return mk(c16[idx], -s16[idx]);
 }
 
+// d * w_M^{-q} (forward sign; CONJ: d * w_M^{+q}) for a compile-time root: the multiples of
+// pi/4 need no multiplication (or one scaling by sqrt(1/2)). Used by the passes whose stage
+// twiddle is 1 (element spacing 1: the last DIF pass, the first DIT pass), where every
+// butterfly factor is such a constant.
+SKC_HD double2 cmul_root(double2 d, int M, int q, bool cj) {
+    const int idx = q * (16 / M);  // angle 2 pi idx / 16, idx in [0, 8)
+    const double c = 0.70710678118654752440;
+    switch (idx) {
+        case 0: return d;
+        case 4: return cj ? mk(-d.y, d.x) : mk(d.y, -d.x);
+        case 2: return cj ? mk(c * (d.x - d.y), c * (d.x + d.y)) : mk(c * (d.x + d.y), c * (d.y - d.x));
+        case 6: return cj ? mk(-c * (d.x + d.y), c * (d.x - d.y)) : mk(c * (d.y - d.x), -c * (d.x + d.y));
+        default: {
+            const double2 r = const_root(M, q);
+            return cmul(d, cj ? conj(r) : r);
+        }
+    }
+}
+
 // Pass plan for a local length N = 2^p: the first pass takes radix 2^(p mod 4)
 // (if nonzero), every later pass radix 16. Pass j starts at half-size h_j.
 struct PassPlan {
@@ -135,7 +154,8 @@ SKC_HD PassPlan make_plan(int N) {
 // logb_over: log2(b) used to index tw for stage twiddles w_{2hs}^{-pos}.
 // Core of a DIF pass item: loads the item's R inputs, runs the butterflies and leaves the
 // outputs in v (output q belongs at position base + q * g).
-template <int LOGR>
+// UNIT: the pass has element spacing 1 (2h = R), so pos = 0 and every stage twiddle is 1.
+template <int LOGR, bool UNIT = false>
 SKC_HD void dif_item_core(double2* x, int w, int h, const double2* tw, int logb, double2 (&v)[1 << LOGR], int& base,
                           int& g) {
     constexpr int R = 1 << LOGR;
@@ -145,6 +165,20 @@ SKC_HD void dif_item_core(double2* x, int w, int h, const double2* tw, int logb,
     base = block * 2 * h + pos;
 #pragma unroll
     for (int q = 0; q < R; ++q) v[q] = x[pad16(base + q * g)];
+    if (UNIT) {
+#pragma unroll
+        for (int s = 0; s < LOGR; ++s) {
+            const int Hq = R >> (s + 1);
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                if (q & Hq) continue;
+                const double2 a = v[q], c = v[q + Hq];
+                v[q] = cadd(a, c);
+                v[q + Hq] = cmul_root(csub(a, c), R >> s, q & (Hq - 1), false);
+            }
+        }
+        return;
+    }
     // stage twiddles: w_{2h}^{-pos} from the table, then w_{2hs}^{-pos} = (w_{2h}^{-pos})^(2^s)
     // by repeated squaring (one table read per item instead of LOGR)
     double2 W = conj(tw[static_cast<unsigned>(pos) << (logb - ilog2(static_cast<unsigned>(2 * h)))]);
@@ -164,18 +198,18 @@ SKC_HD void dif_item_core(double2* x, int w, int h, const double2* tw, int logb,
         }
     }
 }
-template <int LOGR>
+template <int LOGR, bool UNIT = false>
 SKC_HD void dif_pass_item(double2* x, int w, int h, const double2* tw, int logb) {
     constexpr int R = 1 << LOGR;
     double2 v[R];
     int base, g;
-    dif_item_core<LOGR>(x, w, h, tw, logb, v, base, g);
+    dif_item_core<LOGR, UNIT>(x, w, h, tw, logb, v, base, g);
 #pragma unroll
     for (int q = 0; q < R; ++q) x[pad16(base + q * g)] = v[q];
 }
 
 // Mirror inverse (DIT) pass: unscaled, conjugate twiddles.
-template <int LOGR>
+template <int LOGR, bool UNIT = false>
 SKC_HD void dit_pass_item(double2* x, int w, int h, const double2* tw, int logb) {
     constexpr int R = 1 << LOGR;
     const int g = (2 * h) >> LOGR;
@@ -185,24 +219,39 @@ SKC_HD void dit_pass_item(double2* x, int w, int h, const double2* tw, int logb)
     double2 v[R];
 #pragma unroll
     for (int q = 0; q < R; ++q) v[q] = x[pad16(base + q * g)];
-    // stage twiddles w_{2hs}^{pos}, s = 0..LOGR-1, by repeated squaring of w_{2h}^{pos}
-    double2 Ws[LOGR];
-    Ws[0] = tw[static_cast<unsigned>(pos) << (logb - ilog2(static_cast<unsigned>(2 * h)))];
+    if (UNIT) {  // element spacing 1: every stage twiddle is 1
 #pragma unroll
-    for (int s = 1; s < LOGR; ++s) Ws[s] = cmul(Ws[s - 1], Ws[s - 1]);
+        for (int s = LOGR - 1; s >= 0; --s) {
+            const int Hq = R >> (s + 1);
 #pragma unroll
-    for (int s = LOGR - 1; s >= 0; --s) {
-        const int Hq = R >> (s + 1);
-        const double2 W = Ws[s];
+            for (int q = 0; q < R; ++q) {
+                if (q & Hq) continue;
+                const double2 a = v[q];
+                const double2 c = cmul_root(v[q + Hq], R >> s, q & (Hq - 1), true);
+                v[q] = cadd(a, c);
+                v[q + Hq] = csub(a, c);
+            }
+        }
+    } else {
+        // stage twiddles w_{2hs}^{pos}, s = 0..LOGR-1, by repeated squaring of w_{2h}^{pos}
+        double2 Ws[LOGR];
+        Ws[0] = tw[static_cast<unsigned>(pos) << (logb - ilog2(static_cast<unsigned>(2 * h)))];
 #pragma unroll
-        for (int q = 0; q < R; ++q) {
-            if (q & Hq) continue;
-            const int qp = q & (Hq - 1);
-            double2 tw2 = (qp == 0) ? W : cmul(W, conj(const_root(R >> s, qp)));
-            double2 a = v[q];
-            double2 c = cmul(v[q + Hq], tw2);
-            v[q] = cadd(a, c);
-            v[q + Hq] = csub(a, c);
+        for (int s = 1; s < LOGR; ++s) Ws[s] = cmul(Ws[s - 1], Ws[s - 1]);
+#pragma unroll
+        for (int s = LOGR - 1; s >= 0; --s) {
+            const int Hq = R >> (s + 1);
+            const double2 W = Ws[s];
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                if (q & Hq) continue;
+                const int qp = q & (Hq - 1);
+                double2 tw2 = (qp == 0) ? W : cmul(W, conj(const_root(R >> s, qp)));
+                double2 a = v[q];
+                double2 c = cmul(v[q + Hq], tw2);
+                v[q] = cadd(a, c);
+                v[q + Hq] = csub(a, c);
+            }
         }
     }
 #pragma unroll
@@ -210,19 +259,21 @@ SKC_HD void dit_pass_item(double2* x, int w, int h, const double2* tw, int logb)
 }
 
 SKC_HD void dif_pass_dispatch(int logr, double2* x, int w, int h, const double2* tw, int logb) {
+    const bool unit = (2 * h) == (1 << logr);  // element spacing 1
     switch (logr) {
-        case 1: dif_pass_item<1>(x, w, h, tw, logb); break;
-        case 2: dif_pass_item<2>(x, w, h, tw, logb); break;
-        case 3: dif_pass_item<3>(x, w, h, tw, logb); break;
-        default: dif_pass_item<4>(x, w, h, tw, logb); break;
+        case 1: unit ? dif_pass_item<1, true>(x, w, h, tw, logb) : dif_pass_item<1>(x, w, h, tw, logb); break;
+        case 2: unit ? dif_pass_item<2, true>(x, w, h, tw, logb) : dif_pass_item<2>(x, w, h, tw, logb); break;
+        case 3: unit ? dif_pass_item<3, true>(x, w, h, tw, logb) : dif_pass_item<3>(x, w, h, tw, logb); break;
+        default: unit ? dif_pass_item<4, true>(x, w, h, tw, logb) : dif_pass_item<4>(x, w, h, tw, logb); break;
     }
 }
 SKC_HD void dit_pass_dispatch(int logr, double2* x, int w, int h, const double2* tw, int logb) {
+    const bool unit = (2 * h) == (1 << logr);
     switch (logr) {
-        case 1: dit_pass_item<1>(x, w, h, tw, logb); break;
-        case 2: dit_pass_item<2>(x, w, h, tw, logb); break;
-        case 3: dit_pass_item<3>(x, w, h, tw, logb); break;
-        default: dit_pass_item<4>(x, w, h, tw, logb); break;
+        case 1: unit ? dit_pass_item<1, true>(x, w, h, tw, logb) : dit_pass_item<1>(x, w, h, tw, logb); break;
+        case 2: unit ? dit_pass_item<2, true>(x, w, h, tw, logb) : dit_pass_item<2>(x, w, h, tw, logb); break;
+        case 3: unit ? dit_pass_item<3, true>(x, w, h, tw, logb) : dit_pass_item<3>(x, w, h, tw, logb); break;
+        default: unit ? dit_pass_item<4, true>(x, w, h, tw, logb) : dit_pass_item<4>(x, w, h, tw, logb); break;
     }
 }
 
@@ -251,7 +302,7 @@ struct DifPasses {
         constexpr int stride = (1 << LOGN) + ((1 << LOGN) >> 4) + 1;
         for (int w = threadIdx.x; w < na * items; w += blockDim.x) {
             const int a = w / items;
-            dif_pass_item<R_>(sm + a * stride, w - a * items, H, twl, LOGN);
+            dif_pass_item<R_, 2 * H == (1 << R_)>(sm + a * stride, w - a * items, H, twl, LOGN);
         }
         __syncthreads();
         DifPasses<LOGN, LR, P + 1, NP>::run(sm, na, twl);
@@ -271,7 +322,7 @@ struct DitPasses {
         constexpr int stride = (1 << LOGN) + ((1 << LOGN) >> 4) + 1;
         for (int w = threadIdx.x; w < na * items; w += blockDim.x) {
             const int a = w / items;
-            dit_pass_item<R_>(sm + a * stride, w - a * items, H, twl, LOGN);
+            dit_pass_item<R_, 2 * H == (1 << R_)>(sm + a * stride, w - a * items, H, twl, LOGN);
         }
         __syncthreads();
         DitPasses<LOGN, LR, P - 1>::run(sm, na, twl);
@@ -299,7 +350,7 @@ __device__ __forceinline__ void dif_local_epilogue(double2* A, const double2* tw
     for (int w = threadIdx.x; w < items; w += blockDim.x) {
         double2 v[1 << R_];
         int base, g;
-        dif_item_core<R_>(A, w, H, twl, LOGN, v, base, g);
+        dif_item_core<R_, 2 * H == (1 << R_)>(A, w, H, twl, LOGN, v, base, g);
 #pragma unroll
         for (int q = 0; q < (1 << R_); ++q) epi(base + q * g, v[q]);
     }

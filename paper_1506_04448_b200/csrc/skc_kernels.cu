@@ -473,9 +473,9 @@ struct DifPair {
         constexpr int IB = PB >= 0 ? (1 << (LOGN - 1)) >> RB : 0;
         for (int w = threadIdx.x; w < IA + IB; w += blockDim.x) {
             if (w < IA)
-                dif_pass_item<RA>(A, w, HA, twl, LOGN);
+                dif_pass_item<RA, 2 * HA == (1 << RA)>(A, w, HA, twl, LOGN);
             else
-                dif_pass_item<RB>(Bh, w - IA, HB, twl, LOGN);
+                dif_pass_item<RB, 2 * HB == (1 << RB)>(Bh, w - IA, HB, twl, LOGN);
         }
         __syncthreads();
         DifPair<LOGN, LR, P + 1, NPA, NPB>::run(A, Bh, twl);
@@ -495,9 +495,9 @@ struct DitPair {
         constexpr int IB = PB >= 0 ? (1 << (LOGN - 1)) >> RB : 0;
         for (int w = threadIdx.x; w < IA + IB; w += blockDim.x) {
             if (w < IA)
-                dit_pass_item<RA>(A, w, HA, twl, LOGN);
+                dit_pass_item<RA, 2 * HA == (1 << RA)>(A, w, HA, twl, LOGN);
             else
-                dit_pass_item<RB>(Bh, w - IA, HB, twl, LOGN);
+                dit_pass_item<RB, 2 * HB == (1 << RB)>(Bh, w - IA, HB, twl, LOGN);
         }
         __syncthreads();
         DitPair<LOGN, LR, P - 1, NPA, NPB>::run(A, Bh, twl);
@@ -1193,7 +1193,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 8, 2)
             const double ws = (w ? w[s + c] : 1.0) * wscale;
             double2 z[8];
             int base, g;
-            dif_item_core<3>(A, wi, 4, v.twl, LOGN, z, base, g);
+            dif_item_core<3, true>(A, wi, 4, v.twl, LOGN, z, base, g);
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
                 A[pad16(base + q * g)] = mk(0.0, 0.0);  // ready for the next pair's scatter

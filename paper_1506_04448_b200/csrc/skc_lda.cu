@@ -384,7 +384,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 8, 2)
             const double a1 = s1[d], a2 = s2[d];
             double2 z[8];
             int base, g;
-            dif_item_core<3>(A, wi, 4, v.twl, LOGN, z, base, g);
+            dif_item_core<3, true>(A, wi, 4, v.twl, LOGN, z, base, g);
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
                 const int pj = pad16(base + q * g);
