@@ -519,6 +519,16 @@ __device__ __forceinline__ void sym_contract_half_body(const SymView& v, const d
     constexpr int N = 1 << LOGN, NH = N / 2;
     constexpr int strideA = N + (N >> 4) + 1;
     constexpr int strideB = NH + (NH >> 4) + 1;
+#ifndef SKC_CB_SC  // loads in flight per thread in the scatter / pointwise / gather phases
+#define SKC_CB_SC 4
+#endif
+#ifndef SKC_CB_PW
+#define SKC_CB_PW 3
+#endif
+#ifndef SKC_CB_GA
+#define SKC_CB_GA 3
+#endif
+    constexpr int SB = SKC_CB_SC, PB = SKC_CB_PW, GB = SKC_CB_GA;
     const int S = v.S, n = v.n, B = v.B;
     const int r = blockIdx.x % S;
     const int m = (blockIdx.x / S) % B;
@@ -531,9 +541,11 @@ __device__ __forceinline__ void sym_contract_half_body(const SymView& v, const d
     // plan entry. Per restart only u (staged in us) changes, so a run head sums
     // wv[q] * u[idx[q]] (f2: u^2) over its run straight from shared memory.
     double2* wv = Bh + strideB;                                               // 2n
-    std::uint32_t* keys = reinterpret_cast<std::uint32_t*>(wv + 2 * n);      // 2n
-    std::uint32_t* idx = keys + 2 * n;                                        // 2n
-    double* us = reinterpret_cast<double*>(idx + 2 * n);  // n (4n u32 keep 8-byte alignment)
+    // (local key | head << 31 | run continues << 30, index i) per plan entry: a run of equal
+    // keys is summed by its head, in plan order; the flags spare the per-restart scatter the
+    // neighbour reads, so an entry's loads are independent and issue together
+    uint2* kx = reinterpret_cast<uint2*>(wv + 2 * n);                         // 2n
+    double* us = reinterpret_cast<double*>(kx + 2 * n);                       // n
     const std::uint32_t bmask = v.b - 1;
     const std::uint32_t nmask = static_cast<std::uint32_t>(N - 1);
     const double2* fT = v.spec + ((size_t)m * S + r) * N;
@@ -561,12 +573,16 @@ __device__ __forceinline__ void sym_contract_half_body(const SymView& v, const d
     for (int x = threadIdx.x; x < 2 * n; x += NT) {
         const bool hb = x >= n;
         const int q = hb ? x - n : x;
-        const uint2 e = hb ? p2[q] : p1[q];
+        const uint2* pl = hb ? p2 : p1;
+        const uint2 e = pl[q];
         const double2 w = ttab ? (hb ? v.stw2 : v.stw1)[mr + q]
                                : conj(v.tw[(static_cast<std::uint32_t>(r) * (e.y & 0x0FFFFFFFu)) & bmask]);
         wv[x] = cmul(root4_times(e.y >> 28, 1.0), w);
-        keys[x] = hb ? ((e.y & nmask) >> 1) : (e.y & nmask);
-        idx[x] = e.x;
+        auto key_of = [&](std::uint32_t y) { return hb ? ((y & nmask) >> 1) : (y & nmask); };
+        const std::uint32_t key = key_of(e.y);
+        const bool head = q == 0 || key_of(pl[q - 1].y) != key;
+        const bool cont = q + 1 < n && key_of(pl[q + 1].y) == key;
+        kx[x] = make_uint2(key | (head ? 0x80000000u : 0u) | (cont ? 0x40000000u : 0u), e.x);
     }
     for (int l = l0; l < min(L, l0 + lpb); ++l) {
         const double* ug = U + (size_t)l * n;
@@ -576,19 +592,38 @@ __device__ __forceinline__ void sym_contract_half_body(const SymView& v, const d
         PH(0)
         // deterministic scatter (contraction.cpp:150-154): the head of each run of equal
         // keys sums its run in plan order; f1 values u_i, f2 values u_i^2
-        for (int x = threadIdx.x; x < 2 * n; x += NT) {
-            const int lo = (x >= n) ? n : 0;
-            const std::uint32_t key = keys[x];
-            if (x > lo && keys[x - 1] == key) continue;
-            const bool hb = x >= n;
-            double2 acc = mk(0.0, 0.0);
-            for (int x2 = x; x2 < lo + n && keys[x2] == key; ++x2) {
-                const double ui = us[idx[x2]];
-                const double2 w = wv[x2];
-                const double val = hb ? ui * ui : ui;
-                acc = cadd(acc, mk(w.x * val, w.y * val));
+        // (batches of 4 entries per thread: all their metadata loads, then the u loads, then
+        // the products, so the shared-memory latencies overlap instead of chaining)
+        for (int x0 = threadIdx.x; x0 < 2 * n; x0 += SB * NT) {
+            uint2 k[SB];
+            double2 w[SB];
+            double ui[SB];
+#pragma unroll
+            for (int c = 0; c < SB; ++c) {
+                const int x = x0 + c * NT;
+                k[c] = x < 2 * n ? kx[x] : make_uint2(0u, 0u);
+                w[c] = x < 2 * n ? wv[x] : mk(0.0, 0.0);
             }
-            (hb ? Bh : A)[pad16(static_cast<int>(key))] = acc;
+#pragma unroll
+            for (int c = 0; c < SB; ++c) ui[c] = (k[c].x >> 31) ? us[k[c].y] : 0.0;
+#pragma unroll
+            for (int c = 0; c < SB; ++c) {
+                if (!(k[c].x >> 31)) continue;  // not a run head (or past the end)
+                const int x = x0 + c * NT;
+                const bool hb = x >= n;
+                const double val = hb ? ui[c] * ui[c] : ui[c];
+                double2 acc = mk(w[c].x * val, w[c].y * val);
+                std::uint32_t kk = k[c].x;
+                for (int x2 = x + 1; kk & 0x40000000u; ++x2) {  // the rest of the run, plan order
+                    const uint2 k2 = kx[x2];
+                    const double u2 = us[k2.y];
+                    const double2 w2 = wv[x2];
+                    const double v2 = hb ? u2 * u2 : u2;
+                    acc = cadd(acc, mk(w2.x * v2, w2.y * v2));
+                    kk = k2.x;
+                }
+                (hb ? Bh : A)[pad16(static_cast<int>(k[c].x & 0x3FFFFFFFu))] = acc;
+            }
         }
         __syncthreads();
         PH(1)
@@ -598,14 +633,26 @@ __device__ __forceinline__ void sym_contract_half_body(const SymView& v, const d
 
         if (mode == 0) {
             // z1 = fT conj(f1^2 + f2) (full), Z2 = fT conj(f1) folded to N/2 (contraction.cpp:158-162)
-            for (int q = threadIdx.x; q < NH; q += NT) {
-                const int p0 = 2 * q, p1i = 2 * q + 1;
-                const double2 t0 = fT[p0], t1 = fT[p1i];
-                const double2 u0 = A[pad16(p0)], u1 = A[pad16(p1i)];
-                const double2 f2 = Bh[pad16(q)];
-                A[pad16(p0)] = cmulc(t0, cadd(cmul(u0, u0), f2));
-                A[pad16(p1i)] = cmulc(t1, cadd(cmul(u1, u1), f2));
-                Bh[pad16(q)] = cadd(cmulc(t0, u0), cmulc(t1, u1));
+            // (the spectrum slice comes from L2: three positions' loads are issued together)
+            for (int q0 = threadIdx.x; q0 < NH; q0 += PB * NT) {
+                double2 t0[PB], t1[PB];
+#pragma unroll
+                for (int c = 0; c < PB; ++c) {
+                    const int q = q0 + c * NT;
+                    t0[c] = q < NH ? fT[2 * q] : mk(0.0, 0.0);
+                    t1[c] = q < NH ? fT[2 * q + 1] : mk(0.0, 0.0);
+                }
+#pragma unroll
+                for (int c = 0; c < PB; ++c) {
+                    const int q = q0 + c * NT;
+                    if (q >= NH) break;
+                    const int p0 = 2 * q, p1i = 2 * q + 1;
+                    const double2 u0 = A[pad16(p0)], u1 = A[pad16(p1i)];
+                    const double2 f2 = Bh[pad16(q)];
+                    A[pad16(p0)] = cmulc(t0[c], cadd(cmul(u0, u0), f2));
+                    A[pad16(p1i)] = cmulc(t1[c], cadd(cmul(u1, u1), f2));
+                    Bh[pad16(q)] = cadd(cmulc(t0[c], u0), cmulc(t1[c], u1));
+                }
             }
             __syncthreads();
             PH(4)
@@ -613,16 +660,39 @@ __device__ __forceinline__ void sym_contract_half_body(const SymView& v, const d
             PH(5)
             const double inv_b = 1.0 / static_cast<double>(v.b);
             double* o = out + (((size_t)l * B + m) * S + r) * n;
+            if (ttab) {  // folded gather weights (k_sym_twiddle_tables); three entries' loads together
+                for (int i0 = threadIdx.x; i0 < n; i0 += GB * NT) {
+                    std::uint32_t t1[GB], t2[GB];
+                    double2 g1[GB], g2[GB];
+#pragma unroll
+                    for (int c = 0; c < GB; ++c) {
+                        const int i = i0 + c * NT;
+                        const bool ok = i < n;
+                        t1[c] = ok ? b1[i] : 0u;
+                        t2[c] = ok ? b2[i] : 0u;
+                        g1[c] = ok ? v.gtw1[mr + i] : mk(0.0, 0.0);
+                        g2[c] = ok ? v.gtw2[mr + i] : mk(0.0, 0.0);
+                    }
+#pragma unroll
+                    for (int c = 0; c < GB; ++c) {
+                        const int i = i0 + c * NT;
+                        if (i >= n) break;
+                        const double ui = us[i];
+                        const double2 a1 = A[pad16(static_cast<int>(t1[c] & nmask))];
+                        const double2 a2 = Bh[pad16(static_cast<int>((t2[c] & nmask) >> 1))];
+                        double val = (a1.x * g1[c].x - a1.y * g1[c].y) + ui * (a2.x * g2[c].x - a2.y * g2[c].y);
+                        if (r == 0) val += ui * ui * re_rot_conj(3u * se[i], dm[b3[i]]) * (1.0 / 3.0);
+                        o[i] = val;
+                    }
+                }
+            } else
             for (int i = threadIdx.x; i < n; i += NT) {
                 const double ui = us[i];
                 const std::uint32_t t1 = b1[i], t2 = b2[i];
                 const double2 a1 = A[pad16(static_cast<int>(t1 & nmask))];
                 const double2 a2 = Bh[pad16(static_cast<int>((t2 & nmask) >> 1))];
                 double val;
-                if (ttab) {  // folded gather weights (k_sym_twiddle_tables)
-                    const double2 g1 = v.gtw1[mr + i], g2 = v.gtw2[mr + i];
-                    val = (a1.x * g1.x - a1.y * g1.y) + ui * (a2.x * g2.x - a2.y * g2.y);
-                } else {
+                {
                     const unsigned e = se[i];
                     const double2 z1 = cmul(a1, v.tw[(static_cast<std::uint32_t>(r) * t1) & bmask]);
                     const double2 z2 = cmul(a2, v.tw[(static_cast<std::uint32_t>(r) * t2) & bmask]);
