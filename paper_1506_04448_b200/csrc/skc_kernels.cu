@@ -1165,9 +1165,9 @@ __global__ void __launch_bounds__((1 << LOGN) / 8, 2)
     double2* A0 = sm;
     double2* A1 = sm + stride;
     double2* wv = A1 + stride;                                         // n
-    std::uint32_t* keys = reinterpret_cast<std::uint32_t*>(wv + n);   // n
-    std::uint32_t* idx = keys + n;                                     // n
-    double* xs = reinterpret_cast<double*>(idx + n + (n & 1));         // 2 x n: the pair's rows
+    // (local key | head << 31 | run continues << 30, index i): see sym_contract_half_body
+    uint2* kx = reinterpret_cast<uint2*>(wv + n);                      // n
+    double* xs = reinterpret_cast<double*>(kx + n);                    // 2 x n: the pair's rows
     const long long per = (Nsamp + chunks - 1) / chunks;
     const long long s0 = (long long)ch * per, s1 = min(Nsamp, s0 + per);
     const uint2* plan = v.plan1 + (size_t)m * n;
@@ -1180,8 +1180,10 @@ __global__ void __launch_bounds__((1 << LOGN) / 8, 2)
             const uint2 e = plan[q];
             const double2 tw = stw ? stw[q] : conj(v.tw[(static_cast<std::uint32_t>(r) * (e.y & 0x0FFFFFFFu)) & bmask]);
             wv[q] = cmul(root4_times(e.y >> 28, 1.0), tw);
-            keys[q] = e.y & nmask;
-            idx[q] = e.x;
+            const std::uint32_t key = e.y & nmask;
+            const bool head = q == 0 || (plan[q - 1].y & nmask) != key;
+            const bool cont = q + 1 < n && (plan[q + 1].y & nmask) == key;
+            kx[q] = make_uint2(key | (head ? 0x80000000u : 0u) | (cont ? 0x40000000u : 0u), e.x);
         }
     }
     __shared__ __align__(8) unsigned long long mbar;
@@ -1226,19 +1228,40 @@ __global__ void __launch_bounds__((1 << LOGN) / 8, 2)
         }
         // A0, A1 are all-zero here (initially, then re-zeroed by the closing pass). A run head
         // sums its run of equal keys in plan order for both samples (sketch.cpp:353-356).
-        for (int q = threadIdx.x; q < n; q += NT) {
-            const std::uint32_t key = keys[q];
-            if (q > 0 && keys[q - 1] == key) continue;
-            double2 a0 = mk(0.0, 0.0), a1 = mk(0.0, 0.0);
-            for (int q2 = q; q2 < n && keys[q2] == key; ++q2) {
-                const int i = static_cast<int>(idx[q2]);
-                const double2 wq = wv[q2];
-                const double x0 = xs[i], x1 = cnt > 1 ? xs[n + i] : 0.0;
-                a0 = cadd(a0, mk(wq.x * x0, wq.y * x0));
-                a1 = cadd(a1, mk(wq.x * x1, wq.y * x1));
+        // (4 entries per thread at a time: metadata loads, then the sample loads, then the products)
+        const double* xs1 = cnt > 1 ? xs + n : xs;
+        for (int q0 = threadIdx.x; q0 < n; q0 += 4 * NT) {
+            uint2 k[4];
+            double2 wq[4];
+            double x0[4], x1[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int q = q0 + c * NT;
+                k[c] = q < n ? kx[q] : make_uint2(0u, 0u);
+                wq[c] = q < n ? wv[q] : mk(0.0, 0.0);
             }
-            A0[pad16(static_cast<int>(key))] = a0;
-            if (cnt > 1) A1[pad16(static_cast<int>(key))] = a1;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                x0[c] = (k[c].x >> 31) ? xs[k[c].y] : 0.0;
+                x1[c] = (k[c].x >> 31) ? xs1[k[c].y] : 0.0;
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                if (!(k[c].x >> 31)) continue;  // not a run head (or past the end)
+                double2 a0 = mk(wq[c].x * x0[c], wq[c].y * x0[c]), a1 = mk(wq[c].x * x1[c], wq[c].y * x1[c]);
+                std::uint32_t kk = k[c].x;
+                for (int q2 = q0 + c * NT + 1; kk & 0x40000000u; ++q2) {  // the rest of the run, plan order
+                    const uint2 k2 = kx[q2];
+                    const double2 w2 = wv[q2];
+                    const double y0 = xs[k2.y], y1 = xs1[k2.y];
+                    a0 = cadd(a0, mk(w2.x * y0, w2.y * y0));
+                    a1 = cadd(a1, mk(w2.x * y1, w2.y * y1));
+                    kk = k2.x;
+                }
+                const int pj = pad16(static_cast<int>(k[c].x & 0x3FFFFFFFu));
+                A0[pj] = a0;
+                if (cnt > 1) A1[pj] = a1;
+            }
         }
         __syncthreads();
         prefetch(s + 2);  // xs is consumed: the next pair lands during the passes
@@ -1279,8 +1302,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 8, 2)
 }
 size_t moment_pair_smem(int N, int n) {
     return sizeof(double2) * 2 * static_cast<size_t>(padded_len(N)) +
-           (sizeof(double2) + 2 * sizeof(std::uint32_t)) * static_cast<size_t>(n) + sizeof(std::uint32_t) * (n & 1) +
-           2 * sizeof(double) * static_cast<size_t>(n);
+           (sizeof(double2) + sizeof(uint2)) * static_cast<size_t>(n) + 2 * sizeof(double) * static_cast<size_t>(n);
 }
 
 template <int LR>
