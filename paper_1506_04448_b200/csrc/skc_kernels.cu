@@ -1230,27 +1230,41 @@ __global__ void __launch_bounds__((1 << LOGN) / 8, 2)
         // sums its run of equal keys in plan order for both samples (sketch.cpp:353-356).
         // (4 entries per thread at a time: metadata loads, then the sample loads, then the products)
         const double* xs1 = cnt > 1 ? xs + n : xs;
+        // With n keys over N positions ~40% of the entries sit in runs of two or more (n = 1000,
+        // N = 2048), so a head always reads its successor too and adds it under the continue
+        // flag; only runs of three or more take the loop.
         for (int q0 = threadIdx.x; q0 < n; q0 += 4 * NT) {
-            uint2 k[4];
-            double2 wq[4];
-            double x0[4], x1[4];
+            uint2 k[4], kn[4];
+            double2 wq[4], wn[4];
+            double x0[4], x1[4], y0[4], y1[4];
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 const int q = q0 + c * NT;
+                const int qn = min(q + 1, n - 1);
                 k[c] = q < n ? kx[q] : make_uint2(0u, 0u);
                 wq[c] = q < n ? wv[q] : mk(0.0, 0.0);
+                kn[c] = q < n ? kx[qn] : make_uint2(0u, 0u);
+                wn[c] = q < n ? wv[qn] : mk(0.0, 0.0);
             }
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
-                x0[c] = (k[c].x >> 31) ? xs[k[c].y] : 0.0;
-                x1[c] = (k[c].x >> 31) ? xs1[k[c].y] : 0.0;
+                const bool hd = k[c].x >> 31, two = hd && (k[c].x & 0x40000000u);
+                x0[c] = hd ? xs[k[c].y] : 0.0;
+                x1[c] = hd ? xs1[k[c].y] : 0.0;
+                y0[c] = two ? xs[kn[c].y] : 0.0;
+                y1[c] = two ? xs1[kn[c].y] : 0.0;
             }
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 if (!(k[c].x >> 31)) continue;  // not a run head (or past the end)
                 double2 a0 = mk(wq[c].x * x0[c], wq[c].y * x0[c]), a1 = mk(wq[c].x * x1[c], wq[c].y * x1[c]);
-                std::uint32_t kk = k[c].x;
-                for (int q2 = q0 + c * NT + 1; kk & 0x40000000u; ++q2) {  // the rest of the run, plan order
+                std::uint32_t kk = 0u;
+                if (k[c].x & 0x40000000u) {  // second entry of the run (plan order)
+                    a0 = cadd(a0, mk(wn[c].x * y0[c], wn[c].y * y0[c]));
+                    a1 = cadd(a1, mk(wn[c].x * y1[c], wn[c].y * y1[c]));
+                    kk = kn[c].x;
+                }
+                for (int q2 = q0 + c * NT + 2; kk & 0x40000000u; ++q2) {  // third and later entries
                     const uint2 k2 = kx[q2];
                     const double2 w2 = wv[q2];
                     const double y0 = xs[k2.y], y1 = xs1[k2.y];
