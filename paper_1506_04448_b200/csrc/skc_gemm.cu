@@ -108,7 +108,9 @@ int dgemm_slices(int M, int N, int K, int sms) {
     const long long tiles = static_cast<long long>((M + BM - 1) / BM) * ((N + BN - 1) / BN);
     if (tiles >= sms) return 1;
     const long long want = (2LL * sms + tiles - 1) / tiles;
-    return static_cast<int>(std::max(1LL, std::min<long long>(want, K / 512)));
+    // (slices of at least 64: the ALS Grams, k x k from n ~ 1000 rows, would otherwise be one
+    // CTA walking 60 dependent slabs)
+    return static_cast<int>(std::max(1LL, std::min<long long>(want, K / 64)));
 }
 
 void launch_dgemm(cudaStream_t st, int sms, int M, int N, int K, const double* A, long long ai, long long ak,
