@@ -180,7 +180,10 @@ skc_context::RowTab& prepare_dense_build(skc_context* ctx, int n, int dtype, boo
     {
         const double es = dtype == SKC_F32 ? 4.0 : 8.0;
         const double bytes = static_cast<double>(tot) * es;
-        if (kLockMB > 0 && cls_bits >= 0 && rt.nrows > 0 && bytes > 48e6)
+        // (only with >= 3 CTAs per window: at 148 CTAs over 80 windows the moves cost 0.4-2.4%
+        // more than the L2 hits return, and over 160 windows CTAs would chase empty windows:
+        // 1.49 against 0.88 ms, microbench/lock_many_windows.py)
+        if (kLockMB > 0 && cls_bits >= 0 && rt.nrows > 0 && bytes > 48e6 && P >= 3 * G)
             p.lock_rows = std::max(256, static_cast<int>(kLockMB * 1e6 / (bytes / rt.nrows)));
     }
     return rt;
