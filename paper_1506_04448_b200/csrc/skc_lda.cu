@@ -458,6 +458,82 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int j = threadIdx.x; j < N; j += blockDim.x) ao[j] = ACC[j];
 }
 
+// Vocabulary pass at local length 2048 on the 16 x 16 x 8 plan: a word's two arrays (F(w),
+// F(sumwn)) already fill the radix-16 passes (2 x 128 items); the closing radix-8 pass hands
+// a thread the same 8 outputs of both, so the product (lda.cpp:216-217) is formed and
+// accumulated in registers: no pointwise pass over the arrays and no shared-memory ACC.
+template <int LOGN>
+__global__ void __launch_bounds__((1 << LOGN) / 8, 2)
+    k_lda_acc_vocab_reg(SymView v, int V, const double* __restrict__ W, const double* __restrict__ coeff1,
+                        const double* __restrict__ sumwn, int chunks, double* __restrict__ acc_out) {
+    extern __shared__ double2 sm[];
+    constexpr int N = 1 << LOGN, NT = N / 8;
+    constexpr int stride = N + (N >> 4) + 1;
+    static_assert(LOGN >= 8 && (LOGN - 3) % 4 == 0, "16 x ... x 16 x 8 pass plan");
+    const int S = v.S, n = v.n, B = v.B;
+    const int r = blockIdx.x % S;
+    const int m = (blockIdx.x / S) % B;
+    const int ch = blockIdx.x / (S * B);
+    double2* A = sm;
+    double2* Bw = sm + stride;
+    ScatterMeta mt{Bw + stride, nullptr, nullptr};
+    mt.keys = reinterpret_cast<std::uint32_t*>(mt.wv + n);
+    mt.idx = mt.keys + n;
+    double* rows = reinterpret_cast<double*>(mt.idx + n);  // 2 x (W row, sumwn row)
+    const long long per = ((long long)V + chunks - 1) / chunks;
+    const long long i0 = (long long)ch * per, i1 = min((long long)V, i0 + per);
+    zero_sm(A, 2 * stride);
+    build_meta(mt, v.plan1 + (size_t)m * n, v.stw1 ? v.stw1 + ((size_t)m * S + r) * n : nullptr, v.tw, n, N, r,
+               v.b - 1);
+    auto fetch = [&](long long w, int buf) {
+        async_row(rows + (size_t)buf * 2 * n, W + (size_t)w * n, n);
+        async_row(rows + (size_t)buf * 2 * n + n, sumwn + (size_t)w * n, n);
+    };
+    double2 accr[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) accr[q] = mk(0.0, 0.0);
+    const int wi = static_cast<int>((threadIdx.x & ~15u) | ((threadIdx.x & 7u) << 1) | ((threadIdx.x >> 3) & 1u));
+    if (i0 < i1) fetch(i0, 0);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    for (long long w = i0; w < i1; ++w) {
+        if (w + 1 < i1) fetch(w + 1, static_cast<int>((w + 1 - i0) & 1));
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncthreads();
+        const double* row = rows + (size_t)((w - i0) & 1) * 2 * n;
+        scatter_meta(A, mt, row, n);
+        scatter_meta(Bw, mt, row + n, n);
+        __syncthreads();
+        constexpr int NP16 = (LOGN - 3) / 4;
+#pragma unroll
+        for (int pz = 0; pz < NP16; ++pz) {
+            const int h = (N >> 1) >> (4 * pz);
+            for (int it = threadIdx.x; it < 2 * (N / 16); it += NT) {
+                const int a = it / (N / 16);
+                dif_pass_item<4>(a ? Bw : A, it - a * (N / 16), h, v.twl, LOGN);
+            }
+            __syncthreads();
+        }
+        const double c1 = coeff1[w];
+        double2 zw[8], zs[8];
+        int base, g;
+        dif_item_core<3, true>(A, wi, 4, v.twl, LOGN, zw, base, g);
+        dif_item_core<3, true>(Bw, wi, 4, v.twl, LOGN, zs, base, g);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int pj = pad16(base + q * g);
+            A[pj] = mk(0.0, 0.0);
+            Bw[pj] = mk(0.0, 0.0);
+            const double2 w2 = cmul(zw[q], zw[q]);
+            accr[q] = cadd(accr[q], cmul(w2, csub(cscale(zw[q], c1), cscale(zs[q], 3.0))));  // lda.cpp:216-217
+        }
+        // (the next scatter is behind the barrier at the top of the loop)
+    }
+    double2* ao = reinterpret_cast<double2*>(acc_out) + (((size_t)ch * B + m) * S + r) * N;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) ao[8 * wi + q] = accr[q];
+}
+
 // acc = (sum acc - 3 sum cross F(q)) / D + c_m1 F(q)^3 (lda.cpp:211, 220-221), inverse DIT.
 template <int LOGN>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -551,11 +627,15 @@ void launch_lda_accumulate(cudaStream_t st, const SymView& v, long long Du, cons
         cudaFuncSetAttribute(k_lda_acc_docs<LG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_d);         \
         cudaFuncSetAttribute(k_lda_acc_vocab<LG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_v);        \
         if (Du > 0 && (LG != 11 || !kPairDocs)) k_lda_acc_docs<LG><<<grid_d, kThreads, smem_d, st>>>(v, Du, used_docs, P, s1, s2, chunks_d, acc, cross); \
-        if (V > 0) k_lda_acc_vocab<LG><<<grid_v, kThreads, smem_v, st>>>(v, V, W, coeff1, sumwn, chunks_v, acc_v);          \
+        if (V > 0 && (LG != 11 || !kPairDocs)) k_lda_acc_vocab<LG><<<grid_v, kThreads, smem_v, st>>>(v, V, W, coeff1, sumwn, chunks_v, acc_v); \
     }
     if (Du > 0 && v.logN == 11 && kPairDocs) {  // local length 2048: paired documents, ACC in registers (launched first)
         cudaFuncSetAttribute(k_lda_acc_docs_pair<11>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_d);
         k_lda_acc_docs_pair<11><<<grid_d, 256, smem_d, st>>>(v, Du, used_docs, P, s1, s2, chunks_d, acc, cross);
+    }
+    if (V > 0 && v.logN == 11 && kPairDocs) {  // local length 2048: product accumulated in registers
+        cudaFuncSetAttribute(k_lda_acc_vocab_reg<11>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_v);
+        k_lda_acc_vocab_reg<11><<<grid_v, 256, smem_v, st>>>(v, V, W, coeff1, sumwn, chunks_v, acc_v);
     }
     SKC_LOGN_SWITCH_L(v.logN, L_)
 #undef L_
