@@ -1173,18 +1173,77 @@ __global__ void __launch_bounds__((1 << LOGN) / 8, 2)
     const uint2* plan = v.plan1 + (size_t)m * n;
     const std::uint32_t bmask = v.b - 1;
     const std::uint32_t nmask = static_cast<std::uint32_t>(N - 1);
-    zero_smem(A0, 2 * stride);
+    // Scatter order. The plan lists the entries by local key, equal keys adjacent (a run is
+    // summed in plan order, sketch.cpp:353-356). Entries are regrouped by their rank in the
+    // run: rank 0 (one per occupied position, ~79% of the entries at n = 1000) sorted by the
+    // sample index i, then rank 1 sorted by i, then the deeper ranks in plan order. Phase 1 of a
+    // scatter writes the rank-0 products (distinct positions, the sample read almost
+    // contiguously instead of at random), phase 2 adds the rank-1 products and walks what is
+    // left of the run: the same additions in the same order as a head walking its run.
+    //   kx.x = local key | position of the run's rank-2 entry << 12 | run continues << 30
+    __shared__ int s_cls[3];  // class sizes: rank 0, rank 1, rank >= 2
     {
+        double2* twv = A0;                                                 // n (plan order)
+        uint2* tkx = reinterpret_cast<uint2*>(A0 + n);                     // n: (key | min(rank, 2) << 12 | cont << 30, i)
+        unsigned short* inv = reinterpret_cast<unsigned short*>(A1);       // n: plan position of index i
+        unsigned short* dst = inv + n + (n & 1);                           // n: final position of plan entry q
         const double2* stw = v.stw1 ? v.stw1 + ((size_t)m * S + r) * n : nullptr;
         for (int q = threadIdx.x; q < n; q += NT) {
             const uint2 e = plan[q];
             const double2 tw = stw ? stw[q] : conj(v.tw[(static_cast<std::uint32_t>(r) * (e.y & 0x0FFFFFFFu)) & bmask]);
-            wv[q] = cmul(root4_times(e.y >> 28, 1.0), tw);
+            twv[q] = cmul(root4_times(e.y >> 28, 1.0), tw);
             const std::uint32_t key = e.y & nmask;
-            const bool head = q == 0 || (plan[q - 1].y & nmask) != key;
+            int rk = 0;
+            while (rk < 2 && q - rk - 1 >= 0 && (plan[q - rk - 1].y & nmask) == key) ++rk;
             const bool cont = q + 1 < n && (plan[q + 1].y & nmask) == key;
-            kx[q] = make_uint2(key | (head ? 0x80000000u : 0u) | (cont ? 0x40000000u : 0u), e.x);
+            tkx[q] = make_uint2(key | (static_cast<std::uint32_t>(rk) << 12) | (cont ? 0x40000000u : 0u), e.x);
+            inv[e.x] = static_cast<unsigned short>(q);
         }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            const int lane = threadIdx.x;
+            const std::uint32_t lt = (1u << lane) - 1u;
+            int c0 = 0, c1 = 0, c2 = 0;
+            for (int base = 0; base < n; base += 32) {  // class sizes
+                const int q = base + lane;
+                const int rk = q < n ? static_cast<int>((tkx[q].x >> 12) & 3u) : -1;
+                c0 += __popc(__ballot_sync(0xffffffffu, rk == 0));
+                c1 += __popc(__ballot_sync(0xffffffffu, rk == 1));
+            }
+            const int b1 = c0, b2 = c0 + c1;
+            c0 = 0;
+            c1 = 0;
+            for (int base = 0; base < n; base += 32) {
+                const int i = base + lane;  // ranks 0 and 1 in index order
+                const int qi = i < n ? static_cast<int>(inv[i]) : 0;
+                const int rki = i < n ? static_cast<int>((tkx[qi].x >> 12) & 3u) : -1;
+                const std::uint32_t m0 = __ballot_sync(0xffffffffu, rki == 0), m1 = __ballot_sync(0xffffffffu, rki == 1);
+                if (rki == 0) dst[qi] = static_cast<unsigned short>(c0 + __popc(m0 & lt));
+                if (rki == 1) dst[qi] = static_cast<unsigned short>(b1 + c1 + __popc(m1 & lt));
+                c0 += __popc(m0);
+                c1 += __popc(m1);
+                const int q = base + lane;  // deeper ranks in plan order
+                const int rkq = q < n ? static_cast<int>((tkx[q].x >> 12) & 3u) : -1;
+                const std::uint32_t m2 = __ballot_sync(0xffffffffu, rkq == 2);
+                if (rkq == 2) dst[q] = static_cast<unsigned short>(b2 + c2 + __popc(m2 & lt));
+                c2 += __popc(m2);
+            }
+            if (lane == 0) {
+                s_cls[0] = b1;
+                s_cls[1] = b2 - b1;
+                s_cls[2] = c2;
+            }
+        }
+        __syncthreads();
+        for (int q = threadIdx.x; q < n; q += NT) {
+            const uint2 t = tkx[q];
+            const int d = dst[q];
+            const std::uint32_t nxt = (t.x & 0x40000000u) ? static_cast<std::uint32_t>(dst[q + 1]) : 0u;
+            wv[d] = twv[q];
+            kx[d] = make_uint2((t.x & 0x40000FFFu) | (nxt << 12), t.y);
+        }
+        __syncthreads();
+        zero_smem(A0, 2 * stride);
     }
     __shared__ __align__(8) unsigned long long mbar;
     const bool bulk = ((n & 1) == 0) && ((reinterpret_cast<std::uintptr_t>(X) & 15) == 0);
@@ -1226,56 +1285,51 @@ __global__ void __launch_bounds__((1 << LOGN) / 8, 2)
             for (int i = threadIdx.x; i < cnt * n; i += NT) xs[i] = X[(size_t)s * n + i];
             __syncthreads();
         }
-        // A0, A1 are all-zero here (initially, then re-zeroed by the closing pass). A run head
-        // sums its run of equal keys in plan order for both samples (sketch.cpp:353-356).
-        // (4 entries per thread at a time: metadata loads, then the sample loads, then the products)
+        // A0, A1 are all-zero here (initially, then re-zeroed by the closing pass).
         const double* xs1 = cnt > 1 ? xs + n : xs;
-        // With n keys over N positions ~40% of the entries sit in runs of two or more (n = 1000,
-        // N = 2048), so a head always reads its successor too and adds it under the continue
-        // flag; only runs of three or more take the loop.
-        for (int q0 = threadIdx.x; q0 < n; q0 += 4 * NT) {
-            uint2 k[4], kn[4];
-            double2 wq[4], wn[4];
-            double x0[4], x1[4], y0[4], y1[4];
+        const int R0 = s_cls[0], R1 = s_cls[1];
+        // phase 1: rank-0 entries (4 per thread at a time: metadata, then the sample, then the products)
+        for (int e0 = threadIdx.x; e0 < R0; e0 += 4 * NT) {
+            uint2 k[4];
+            double2 wq[4];
+            double x0[4], x1[4];
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
-                const int q = q0 + c * NT;
-                const int qn = min(q + 1, n - 1);
-                k[c] = q < n ? kx[q] : make_uint2(0u, 0u);
-                wq[c] = q < n ? wv[q] : mk(0.0, 0.0);
-                kn[c] = q < n ? kx[qn] : make_uint2(0u, 0u);
-                wn[c] = q < n ? wv[qn] : mk(0.0, 0.0);
+                const int e = min(e0 + c * NT, R0 - 1);
+                k[c] = kx[e];
+                wq[c] = wv[e];
             }
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
-                const bool hd = k[c].x >> 31, two = hd && (k[c].x & 0x40000000u);
-                x0[c] = hd ? xs[k[c].y] : 0.0;
-                x1[c] = hd ? xs1[k[c].y] : 0.0;
-                y0[c] = two ? xs[kn[c].y] : 0.0;
-                y1[c] = two ? xs1[kn[c].y] : 0.0;
+                x0[c] = xs[k[c].y];
+                x1[c] = xs1[k[c].y];
             }
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
-                if (!(k[c].x >> 31)) continue;  // not a run head (or past the end)
-                double2 a0 = mk(wq[c].x * x0[c], wq[c].y * x0[c]), a1 = mk(wq[c].x * x1[c], wq[c].y * x1[c]);
-                std::uint32_t kk = 0u;
-                if (k[c].x & 0x40000000u) {  // second entry of the run (plan order)
-                    a0 = cadd(a0, mk(wn[c].x * y0[c], wn[c].y * y0[c]));
-                    a1 = cadd(a1, mk(wn[c].x * y1[c], wn[c].y * y1[c]));
-                    kk = kn[c].x;
-                }
-                for (int q2 = q0 + c * NT + 2; kk & 0x40000000u; ++q2) {  // third and later entries
-                    const uint2 k2 = kx[q2];
-                    const double2 w2 = wv[q2];
-                    const double y0 = xs[k2.y], y1 = xs1[k2.y];
-                    a0 = cadd(a0, mk(w2.x * y0, w2.y * y0));
-                    a1 = cadd(a1, mk(w2.x * y1, w2.y * y1));
-                    kk = k2.x;
-                }
-                const int pj = pad16(static_cast<int>(k[c].x & 0x3FFFFFFFu));
-                A0[pj] = a0;
-                if (cnt > 1) A1[pj] = a1;
+                if (e0 + c * NT >= R0) break;
+                const int pj = pad16(static_cast<int>(k[c].x & 0xFFFu));
+                A0[pj] = mk(wq[c].x * x0[c], wq[c].y * x0[c]);
+                if (cnt > 1) A1[pj] = mk(wq[c].x * x1[c], wq[c].y * x1[c]);
             }
+        }
+        __syncthreads();
+        // phase 2: rank-1 entries add to their position, then the rest of the run in plan order
+        for (int e = R0 + threadIdx.x; e < R0 + R1; e += NT) {
+            uint2 k = kx[e];
+            double2 wq = wv[e];
+            const int pj = pad16(static_cast<int>(k.x & 0xFFFu));
+            double2 a0 = A0[pj], a1 = cnt > 1 ? A1[pj] : mk(0.0, 0.0);
+            for (;;) {
+                const double y0 = xs[k.y], y1 = xs1[k.y];
+                a0 = cadd(a0, mk(wq.x * y0, wq.y * y0));
+                a1 = cadd(a1, mk(wq.x * y1, wq.y * y1));
+                if (!(k.x & 0x40000000u)) break;
+                const int e2 = static_cast<int>((k.x >> 12) & 0xFFFu);  // the run's next entry
+                k = kx[e2];
+                wq = wv[e2];
+            }
+            A0[pj] = a0;
+            if (cnt > 1) A1[pj] = a1;
         }
         __syncthreads();
         prefetch(s + 2);  // xs is consumed: the next pair lands during the passes
